@@ -1,0 +1,202 @@
+// Launchers for the tcgen05 implicit-GEMM conv engine (tc_conv.cuh).
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+
+#include "kernels.h"
+#include "tc_conv.cuh"
+
+namespace vdnnk {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+constexpr int kStages = 4;
+constexpr int kNumSms = 148;
+
+bool build_common(const ConvArgs& a, ConvParams& p) {
+  std::memset(&p, 0, sizeof(p));
+  if (a.nseg < 1 || a.nseg > kMaxSegs) return false;
+  p.N = a.n;
+  p.H = a.h;
+  p.W = a.w;
+  p.Ho = a.ho();
+  p.Wo = a.wo();
+  p.Cout = a.cout;
+  p.kh = a.kh;
+  p.kw = a.kw;
+  p.stride = a.stride;
+  p.pad = a.pad;
+  p.nseg = a.nseg;
+  int cb = 0;
+  bool vec = true;
+  for (int i = 0; i < a.nseg; ++i) {
+    p.seg[i].x = a.x[i];
+    p.seg[i].dx = a.dx[i];
+    p.seg[i].C = a.c[i];
+    p.seg[i].cbase = cb;
+    cb += a.c[i];
+    if (a.c[i] % 4 != 0) vec = false;
+  }
+  p.C = cb;
+  p.KK = a.kh * a.kw * cb;
+  // virtual 32-channel chunks per segment
+  int nch = 0;
+  if (vec) {
+    for (int i = 0; i < a.nseg && vec; ++i) {
+      for (int c0 = 0; c0 < a.c[i]; c0 += 32) {
+        if (nch >= kMaxChunks) {
+          vec = false;
+          break;
+        }
+        Chunk& c = p.chunk[nch++];
+        c.seg = static_cast<int16_t>(i);
+        c.coff = static_cast<int16_t>(c0);
+        c.valid = static_cast<int16_t>(std::min(32, a.c[i] - c0));
+        c.cbase = static_cast<int16_t>(p.seg[i].cbase + c0);
+      }
+    }
+  }
+  p.vec_in = vec ? 1 : 0;
+  p.nchunk = vec ? nch : 0;
+  p.vec_out = (a.cout % 4 == 0) ? 1 : 0;
+  return true;
+}
+
+template <int BN>
+cudaError_t launch_bn(const ConvParams& p, int splits, cudaStream_t st) {
+  using L = TcSmem<BN, kStages>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         L::kTotal);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((p.M + kBM - 1) / kBM, (p.Ncols + BN - 1) / BN, splits);
+  tc_conv_kernel<BN, kStages><<<grid, 160, L::kTotal, st>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
+  if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
+  if (p.Ncols <= 64) return launch_bn<64>(p, splits, st);
+  return launch_bn<128>(p, splits, st);
+}
+
+int pick_bn(int ncols) { return ncols <= 64 ? 64 : 128; }
+
+int wgrad_rows(const ConvParams& p) { return p.vec_in ? p.kh * p.kw * p.nchunk * 32 : p.KK; }
+
+}  // namespace
+
+uint64_t launch_count() { return g_launches.load(); }
+void count_launch(uint64_t k) { g_launches.fetch_add(k); }
+
+cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
+                       cudaStream_t st) {
+  ConvParams p;
+  if (!build_common(a, p)) return cudaErrorInvalidValue;
+  p.kind = kFprop;
+  p.epi = accumulate ? kEpiAccum : kEpiStore;
+  p.w = w;
+  p.bias = bias;
+  p.y = y;
+  p.M = a.n * p.Ho * p.Wo;
+  p.Ncols = a.cout;
+  p.kblocks = p.vec_in ? a.kh * a.kw * p.nchunk : (p.KK + kBK - 1) / kBK;
+  p.kb_per_split = p.kblocks;
+  return launch(p, 1, st);
+}
+
+cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st) {
+  ConvParams p;
+  if (!build_common(a, p)) return cudaErrorInvalidValue;
+  if (a.stride != 1) return cudaErrorNotSupported;
+  p.kind = kDgrad;
+  p.epi = accumulate ? kEpiAccum : kEpiStore;
+  p.w = w;
+  p.dy = dy;
+  p.M = a.n * a.h * a.w;
+  p.Ncols = p.vec_in ? p.nchunk * 32 : p.C;
+  p.kblocks = p.vec_out ? a.kh * a.kw * ((a.cout + 31) / 32) : (a.kh * a.kw * a.cout + kBK - 1) / kBK;
+  p.kb_per_split = p.kblocks;
+  return launch(p, 1, st);
+}
+
+size_t conv_wgrad_ws_bytes(const ConvArgs& a) {
+  ConvParams p;
+  if (!build_common(a, p)) return 0;
+  const int M = wgrad_rows(p);
+  const int bn = pick_bn(a.cout);
+  const int tiles = ((M + kBM - 1) / kBM) * ((a.cout + bn - 1) / bn);
+  const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
+  const int kblocks = static_cast<int>((P + kBK - 1) / kBK);
+  int splits = std::max(1, (2 * kNumSms + tiles - 1) / tiles);
+  splits = std::min(splits, std::max(1, kblocks / 8));
+  if (splits <= 1) return 0;
+  return static_cast<size_t>(splits) * M * a.cout * sizeof(float);
+}
+
+__global__ void wgrad_reduce_kernel(const __grid_constant__ ConvParams p, int splits) {
+  const int64_t total = static_cast<int64_t>(p.Cout) * p.M;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(idx % p.M);
+    const int co = static_cast<int>(idx / p.M);
+    bool valid;
+    const int widx = wgrad_widx(p, m, valid);
+    if (!valid) continue;
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += p.out[static_cast<int64_t>(k) * total + idx];
+    if (p.w_mut && p.epi == kEpiSgd)
+      p.w_mut[static_cast<int64_t>(co) * p.KK + widx] -= p.lr * s;
+    else
+      p.y[static_cast<int64_t>(co) * p.KK + widx] = s;  // y aliases dw_out here
+  }
+}
+
+cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float lr, float* dw_out, float* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  ConvParams p;
+  if (!build_common(a, p)) return cudaErrorInvalidValue;
+  p.kind = kWgrad;
+  p.dy = dy;
+  p.w = w_mut;
+  p.w_mut = w_mut;
+  p.lr = lr;
+  p.M = wgrad_rows(p);
+  p.Ncols = a.cout;
+  const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
+  p.kblocks = static_cast<int>((P + kBK - 1) / kBK);
+  const int bn = pick_bn(a.cout);
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((a.cout + bn - 1) / bn);
+  int splits = std::max(1, (2 * kNumSms + tiles - 1) / tiles);
+  splits = std::min(splits, std::max(1, p.kblocks / 8));
+  const size_t per = static_cast<size_t>(p.M) * a.cout * sizeof(float);
+  if (ws == nullptr || per == 0) splits = 1;
+  else splits = static_cast<int>(std::min<size_t>(splits, ws_bytes / per));
+  if (splits < 1) splits = 1;
+  p.kb_per_split = (p.kblocks + splits - 1) / splits;
+  splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;
+  if (splits <= 1) {
+    p.epi = dw_out ? kEpiGrad : kEpiSgd;
+    p.out = dw_out;
+    p.kb_per_split = p.kblocks;
+    return launch(p, 1, st);
+  }
+  p.epi = kEpiPartial;
+  p.out = ws;
+  cudaError_t e = launch(p, splits, st);
+  if (e != cudaSuccess) return e;
+  p.epi = dw_out ? kEpiGrad : kEpiSgd;
+  p.y = dw_out;
+  if (dw_out) p.w_mut = nullptr;
+  const int64_t total = static_cast<int64_t>(p.Cout) * p.M;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 4 * kNumSms));
+  wgrad_reduce_kernel<<<blocks, 256, 0, st>>>(p, splits);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace vdnnk

@@ -1,0 +1,420 @@
+// Memory-bound kernels: in-place ReLU fwd/bwd, gradient folding, max-pool
+// fwd/bwd (floor mode, no padding), softmax cross-entropy, bias gradient,
+// SGD, and deterministic synthetic-data fills.
+//
+// Dataflow contracts (reference file:line):
+//  * ACTV is in place on the producer's Y and its BWD is in place on the
+//    gradient buffer, masked by Y > 0 (net_graph.hpp:384-389,
+//    simulator.hpp:102-104, footprint.hpp:62).
+//  * POOL BWD reads X and its own Y (simulator.hpp:97-100); pooling is floor
+//    mode with no padding (net_graph.hpp:325-334).
+//  * LOSS reads nothing in BWD (simulator.hpp:105-107); the softmax gradient
+//    is produced during LOSS FWD into a non-pool scratch.
+#include <cfloat>
+
+#include "kernels.h"
+
+namespace vdnnk {
+
+namespace {
+constexpr int kThreads = 256;
+constexpr int kNumSms = 148;
+
+inline int grid_for(size_t n, int per_thread = 1) {
+  size_t blocks = (n + static_cast<size_t>(kThreads) * per_thread - 1) / (static_cast<size_t>(kThreads) * per_thread);
+  if (blocks < 1) blocks = 1;
+  if (blocks > static_cast<size_t>(kNumSms) * 16) blocks = static_cast<size_t>(kNumSms) * 16;
+  return static_cast<int>(blocks);
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ float u01(uint64_t bits) {  // [0, 1)
+  return static_cast<float>(bits >> 40) * (1.0f / 16777216.0f);
+}
+}  // namespace
+
+// ------------------------------------------------------------- ReLU -------
+__global__ void relu_fwd_kernel(float* __restrict__ y, size_t n) {
+  const size_t n4 = n / 4;
+  float4* y4 = reinterpret_cast<float4*>(y);
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float4 v = y4[i];
+    v.x = fmaxf(v.x, 0.f);
+    v.y = fmaxf(v.y, 0.f);
+    v.z = fmaxf(v.z, 0.f);
+    v.w = fmaxf(v.w, 0.f);
+    y4[i] = v;
+  }
+  for (size_t i = n4 * 4 + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    y[i] = fmaxf(y[i], 0.f);
+}
+
+cudaError_t relu_fwd(float* y, size_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  relu_fwd_kernel<<<grid_for(n, 16), kThreads, 0, st>>>(y, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+struct PtrList {
+  const float* p[8];
+};
+
+__global__ void relu_bwd_kernel(float* __restrict__ g, PtrList extra, int nextra, const float* __restrict__ y,
+                                size_t n) {
+  const size_t n4 = n / 4;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float4 v = reinterpret_cast<float4*>(g)[i];
+    for (int k = 0; k < nextra; ++k) {
+      const float4 e = reinterpret_cast<const float4*>(extra.p[k])[i];
+      v.x += e.x;
+      v.y += e.y;
+      v.z += e.z;
+      v.w += e.w;
+    }
+    const float4 a = reinterpret_cast<const float4*>(y)[i];
+    v.x = a.x > 0.f ? v.x : 0.f;
+    v.y = a.y > 0.f ? v.y : 0.f;
+    v.z = a.z > 0.f ? v.z : 0.f;
+    v.w = a.w > 0.f ? v.w : 0.f;
+    reinterpret_cast<float4*>(g)[i] = v;
+  }
+  for (size_t i = n4 * 4 + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float v = g[i];
+    for (int k = 0; k < nextra; ++k) v += extra.p[k][i];
+    g[i] = y[i] > 0.f ? v : 0.f;
+  }
+}
+
+cudaError_t relu_bwd(float* g0, const float* const* extra, int nextra, const float* y, size_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  if (nextra > 8) return cudaErrorInvalidValue;
+  PtrList pl{};
+  for (int i = 0; i < nextra; ++i) pl.p[i] = extra[i];
+  relu_bwd_kernel<<<grid_for(n, 16), kThreads, 0, st>>>(g0, pl, nextra, y, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void add_into_kernel(float* __restrict__ dst, PtrList src, int nsrc, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float v = dst[i];
+    for (int k = 0; k < nsrc; ++k) v += src.p[k][i];
+    dst[i] = v;
+  }
+}
+
+cudaError_t add_into(float* dst, const float* const* src, int nsrc, size_t n, cudaStream_t st) {
+  if (n == 0 || nsrc == 0) return cudaSuccess;
+  if (nsrc > 8) return cudaErrorInvalidValue;
+  PtrList pl{};
+  for (int i = 0; i < nsrc; ++i) pl.p[i] = src[i];
+  add_into_kernel<<<grid_for(n, 4), kThreads, 0, st>>>(dst, pl, nsrc, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- max-pool -----
+struct PoolDev {
+  int n, h, w, window, stride, ho, wo, nseg, ctot;
+  const float* x[kMaxConvSegs];
+  float* dx[kMaxConvSegs];
+  int c[kMaxConvSegs];
+  int cbase[kMaxConvSegs];
+};
+
+static PoolDev to_dev(const PoolArgs& a) {
+  PoolDev d{};
+  d.n = a.n;
+  d.h = a.h;
+  d.w = a.w;
+  d.window = a.window;
+  d.stride = a.stride;
+  d.ho = a.ho();
+  d.wo = a.wo();
+  d.nseg = a.nseg;
+  int cb = 0;
+  for (int i = 0; i < a.nseg; ++i) {
+    d.x[i] = a.x[i];
+    d.dx[i] = a.dx[i];
+    d.c[i] = a.c[i];
+    d.cbase[i] = cb;
+    cb += a.c[i];
+  }
+  d.ctot = cb;
+  return d;
+}
+
+__device__ __forceinline__ int pool_seg(const PoolDev& d, int c) {
+  int s = 0;
+  for (int i = 1; i < d.nseg; ++i)
+    if (c >= d.cbase[i]) s = i;
+  return s;
+}
+
+// Y[n][oh][ow][c] = max over the window (row-major scan, first max wins).
+__global__ void maxpool_fwd_kernel(const __grid_constant__ PoolDev d, float* __restrict__ y) {
+  const size_t total = static_cast<size_t>(d.n) * d.ho * d.wo * d.ctot;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % d.ctot);
+    size_t t = i / d.ctot;
+    const int ow = static_cast<int>(t % d.wo);
+    t /= d.wo;
+    const int oh = static_cast<int>(t % d.ho);
+    const int n = static_cast<int>(t / d.ho);
+    const int s = pool_seg(d, c);
+    const int cl = c - d.cbase[s];
+    const float* x = d.x[s];
+    const int C = d.c[s];
+    float m = -FLT_MAX;
+    bool first = true;
+    for (int r = 0; r < d.window; ++r) {
+      const int ih = oh * d.stride + r;
+      for (int q = 0; q < d.window; ++q) {
+        const int iw = ow * d.stride + q;
+        const float v = x[((static_cast<size_t>(n) * d.h + ih) * d.w + iw) * C + cl];
+        if (first || v > m) {
+          m = v;
+          first = false;
+        }
+      }
+    }
+    y[i] = m;
+  }
+}
+
+cudaError_t maxpool_fwd(const PoolArgs& a, float* y, cudaStream_t st) {
+  const PoolDev d = to_dev(a);
+  const size_t total = static_cast<size_t>(d.n) * d.ho * d.wo * d.ctot;
+  if (total == 0) return cudaSuccess;
+  maxpool_fwd_kernel<<<grid_for(total, 4), kThreads, 0, st>>>(d, y);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Gather form (deterministic): every input element sums dY over the windows
+// whose first-maximum position it is.
+__global__ void maxpool_bwd_kernel(const __grid_constant__ PoolDev d, const float* __restrict__ y,
+                                   const float* __restrict__ dy) {
+  const size_t total = static_cast<size_t>(d.n) * d.h * d.w * d.ctot;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % d.ctot);
+    size_t t = i / d.ctot;
+    const int iw = static_cast<int>(t % d.w);
+    t /= d.w;
+    const int ih = static_cast<int>(t % d.h);
+    const int n = static_cast<int>(t / d.h);
+    const int s = pool_seg(d, c);
+    if (d.dx[s] == nullptr) continue;
+    const int cl = c - d.cbase[s];
+    const float* x = d.x[s];
+    const int C = d.c[s];
+    // windows oh with oh*stride <= ih < oh*stride + window
+    int oh_lo = ih - d.window + 1;
+    oh_lo = oh_lo <= 0 ? 0 : (oh_lo + d.stride - 1) / d.stride;
+    int oh_hi = ih / d.stride;
+    if (oh_hi > d.ho - 1) oh_hi = d.ho - 1;
+    int ow_lo = iw - d.window + 1;
+    ow_lo = ow_lo <= 0 ? 0 : (ow_lo + d.stride - 1) / d.stride;
+    int ow_hi = iw / d.stride;
+    if (ow_hi > d.wo - 1) ow_hi = d.wo - 1;
+    float g = 0.f;
+    for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+      for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+        const size_t oidx = ((static_cast<size_t>(n) * d.ho + oh) * d.wo + ow) * d.ctot + c;
+        const float ym = y[oidx];
+        // first position in row-major window order holding the max
+        int ar = -1, aq = -1;
+        for (int r = 0; r < d.window && ar < 0; ++r) {
+          for (int q = 0; q < d.window; ++q) {
+            const float v =
+                x[((static_cast<size_t>(n) * d.h + oh * d.stride + r) * d.w + ow * d.stride + q) * C + cl];
+            if (v == ym) {
+              ar = r;
+              aq = q;
+              break;
+            }
+          }
+        }
+        if (oh * d.stride + ar == ih && ow * d.stride + aq == iw) g += dy[oidx];
+      }
+    }
+    d.dx[s][((static_cast<size_t>(n) * d.h + ih) * d.w + iw) * C + cl] = g;
+  }
+}
+
+cudaError_t maxpool_bwd(const PoolArgs& a, const float* y, const float* dy, cudaStream_t st) {
+  const PoolDev d = to_dev(a);
+  const size_t total = static_cast<size_t>(d.n) * d.h * d.w * d.ctot;
+  if (total == 0) return cudaSuccess;
+  maxpool_bwd_kernel<<<grid_for(total, 4), kThreads, 0, st>>>(d, y, dy);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------- softmax x-entropy ----
+// One warp per row; loss averaged over rows by a single-block deterministic
+// reduction.
+__global__ void softmax_xent_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels, int n,
+                                    int k, float* __restrict__ grad, float* __restrict__ row_loss) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const float* z = logits + static_cast<size_t>(warp) * k;
+  float m = -FLT_MAX;
+  for (int i = lane; i < k; i += 32) m = fmaxf(m, z[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float s = 0.f;
+  for (int i = lane; i < k; i += 32) s += expf(z[i] - m);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float lse = m + logf(s);
+  const int lab = labels[warp];
+  const float inv_n = 1.0f / static_cast<float>(n);
+  for (int i = lane; i < k; i += 32) {
+    const float pr = expf(z[i] - lse);
+    grad[static_cast<size_t>(warp) * k + i] = (pr - (i == lab ? 1.f : 0.f)) * inv_n;
+  }
+  if (lane == 0) row_loss[warp] = lse - z[lab];
+}
+
+__global__ void mean_kernel(const float* __restrict__ v, int n, float* __restrict__ out) {
+  __shared__ float part[256];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = part[0] / static_cast<float>(n);
+}
+
+cudaError_t softmax_xent_fwd(const float* logits, const int32_t* labels, int n, int k, float* grad_scratch,
+                             float* row_loss, float* loss, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int threads = 256;
+  const int blocks = (n * 32 + threads - 1) / threads;
+  softmax_xent_kernel<<<blocks, threads, 0, st>>>(logits, labels, n, k, grad_scratch, row_loss);
+  mean_kernel<<<1, 256, 0, st>>>(row_loss, n, loss);
+  count_launch(2);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- bias / SGD -------
+__global__ void bias_grad_kernel(const float* __restrict__ dy, int n, int o, float* __restrict__ bias, float lr,
+                                 float* __restrict__ db) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= o) return;
+  float s = 0.f;
+  for (int i = 0; i < n; ++i) s += dy[static_cast<size_t>(i) * o + j];
+  if (db)
+    db[j] = s;
+  else
+    bias[j] -= lr * s;
+}
+
+cudaError_t bias_grad(const float* dy, int n, int o, float* bias, float lr, float* db_out, cudaStream_t st) {
+  if (o <= 0) return cudaSuccess;
+  bias_grad_kernel<<<(o + 255) / 256, 256, 0, st>>>(dy, n, o, bias, lr, db_out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float lr, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    w[i] -= lr * g[i];
+}
+
+cudaError_t sgd_update(float* w, const float* g, float lr, size_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  sgd_kernel<<<grid_for(n, 8), kThreads, 0, st>>>(w, g, lr, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void scale_kernel(float* __restrict__ x, float s, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] *= s;
+}
+
+cudaError_t scale_inplace(float* x, float s, size_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  scale_kernel<<<grid_for(n, 8), kThreads, 0, st>>>(x, s, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- fills ---------
+__global__ void fill_normal_kernel(float* __restrict__ w, size_t n, float stddev, uint64_t seed) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint64_t a = splitmix64(seed * 0x100000001B3ull + 2 * i);
+    const uint64_t b = splitmix64(seed * 0x100000001B3ull + 2 * i + 1);
+    const float u1 = 1.0f - u01(a);  // (0, 1]
+    const float u2 = u01(b);
+    w[i] = stddev * sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+  }
+}
+
+cudaError_t fill_normal(float* w, size_t n, float stddev, uint64_t seed, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  fill_normal_kernel<<<grid_for(n, 8), kThreads, 0, st>>>(w, n, stddev, seed);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void fill_uniform_kernel(float* __restrict__ x, size_t n, float lo, float hi, uint64_t seed) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] = lo + (hi - lo) * u01(splitmix64(seed * 0x9E3779B97F4A7C15ull + i));
+}
+
+cudaError_t fill_uniform(float* x, size_t n, float lo, float hi, uint64_t seed, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  fill_uniform_kernel<<<grid_for(n, 8), kThreads, 0, st>>>(x, n, lo, hi, seed);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void fill_const_kernel(float* __restrict__ x, size_t n, float v) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] = v;
+}
+
+cudaError_t fill_const(float* x, size_t n, float v, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  fill_const_kernel<<<grid_for(n, 8), kThreads, 0, st>>>(x, n, v);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void fill_labels_kernel(int32_t* __restrict__ y, size_t n, int classes, uint64_t seed) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    y[i] = static_cast<int32_t>(splitmix64(seed * 0x9E3779B97F4A7C15ull + i) % static_cast<uint64_t>(classes));
+}
+
+cudaError_t fill_labels(int32_t* y, size_t n, int classes, uint64_t seed, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  fill_labels_kernel<<<grid_for(n), kThreads, 0, st>>>(y, n, classes, seed);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace vdnnk

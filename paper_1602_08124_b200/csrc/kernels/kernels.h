@@ -1,0 +1,83 @@
+// Host-side launch interface of the sm_100a kernels (internal to libvdnn).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vdnnk {
+
+constexpr int kMaxConvSegs = 8;
+
+// A (possibly channel-concatenated) NHWC conv input and its gradient planes.
+// FC layers are passed as 1x1 convs over a 1x1 image whose channels are the
+// flattened (h, w, c) features of each input segment.
+struct ConvArgs {
+  int n = 0, h = 0, w = 0;                 // input spatial dims
+  int nseg = 0;
+  const float* x[kMaxConvSegs] = {};       // segment inputs (fprop / wgrad)
+  float* dx[kMaxConvSegs] = {};            // segment gradient planes (dgrad), may be null
+  int c[kMaxConvSegs] = {};                // segment channels
+  int cout = 0, kh = 1, kw = 1, stride = 1, pad = 0;
+  int ho() const { return (h + 2 * pad - kh) / stride + 1; }
+  int wo() const { return (w + 2 * pad - kw) / stride + 1; }
+  int cin() const {
+    int t = 0;
+    for (int i = 0; i < nseg; ++i) t += c[i];
+    return t;
+  }
+};
+
+// Tensor-core conv contractions (kind::tf32, fp32 accumulate).
+cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
+                       cudaStream_t st);
+cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st);
+// Weight gradient. If dw_out is null: fused SGD  w_mut -= lr * dW.
+// Otherwise dW is written to dw_out (KRSC layout) and w_mut is untouched.
+// `ws` holds split-K partials; pass conv_wgrad_ws_bytes(a) bytes (or less:
+// fewer splits are used).
+cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float lr, float* dw_out, float* ws,
+                       size_t ws_bytes, cudaStream_t st);
+size_t conv_wgrad_ws_bytes(const ConvArgs& a);
+
+// Memory-bound kernels.
+cudaError_t relu_fwd(float* y, size_t n, cudaStream_t st);
+// g0 = (g0 + sum extra) * (y > 0); in place on g0.
+cudaError_t relu_bwd(float* g0, const float* const* extra, int nextra, const float* y, size_t n, cudaStream_t st);
+cudaError_t add_into(float* dst, const float* const* src, int nsrc, size_t n, cudaStream_t st);
+struct PoolArgs {
+  int n = 0, h = 0, w = 0, window = 2, stride = 2;
+  int nseg = 0;
+  const float* x[kMaxConvSegs] = {};
+  float* dx[kMaxConvSegs] = {};
+  int c[kMaxConvSegs] = {};
+  int ho() const { return (h - window) / stride + 1; }
+  int wo() const { return (w - window) / stride + 1; }
+  int ctot() const {
+    int t = 0;
+    for (int i = 0; i < nseg; ++i) t += c[i];
+    return t;
+  }
+};
+cudaError_t maxpool_fwd(const PoolArgs& a, float* y, cudaStream_t st);
+cudaError_t maxpool_bwd(const PoolArgs& a, const float* y, const float* dy, cudaStream_t st);
+// Mean softmax cross-entropy over n rows of k logits. Writes the gradient
+// (softmax - onehot)/n into grad_scratch, the per-row loss into row_loss and
+// the mean loss into *loss (all device pointers).
+cudaError_t softmax_xent_fwd(const float* logits, const int32_t* labels, int n, int k, float* grad_scratch,
+                             float* row_loss, float* loss, cudaStream_t st);
+// bias -= lr * sum_n dy[n][o]   (or db_out[o] = sum when db_out != null)
+cudaError_t bias_grad(const float* dy, int n, int o, float* bias, float lr, float* db_out, cudaStream_t st);
+cudaError_t sgd_update(float* w, const float* g, float lr, size_t n, cudaStream_t st);
+cudaError_t scale_inplace(float* x, float s, size_t n, cudaStream_t st);
+// Deterministic synthetic data: He-normal weights, U[-1,1) images, labels.
+cudaError_t fill_normal(float* w, size_t n, float stddev, uint64_t seed, cudaStream_t st);
+cudaError_t fill_uniform(float* x, size_t n, float lo, float hi, uint64_t seed, cudaStream_t st);
+cudaError_t fill_const(float* x, size_t n, float v, cudaStream_t st);
+cudaError_t fill_labels(int32_t* y, size_t n, int classes, uint64_t seed, cudaStream_t st);
+
+// Number of kernel launches issued by the calls above since process start
+// (used by bench.py's gpu_launches claim).
+uint64_t launch_count();
+void count_launch(uint64_t k = 1);
+
+}  // namespace vdnnk

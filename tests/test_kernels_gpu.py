@@ -1,0 +1,195 @@
+"""Kernel-level parity: tcgen05 conv/FC contractions and memory-bound kernels
+versus a float64 CPU reference of the same op (torch functional ops).
+
+Tolerance: the tensor-core path is kind::tf32 (10-bit mantissa inputs, fp32
+accumulate). We bound the max abs error by TF32_TOL times the max |reference|
+of the output tensor (plus the K-dependent accumulation noise is far below
+that). Memory-bound kernels are exact (bit-equal) except softmax (1e-6).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_1602_08124_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+TF32_TOL = 4e-3
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def _desc(n, h, w, xs, cs, cout, k, stride, pad, dxs=None):
+    d = L.ConvDesc()
+    d.n, d.h, d.w, d.nseg = n, h, w, len(cs)
+    for i, c in enumerate(cs):
+        d.x[i] = xs[i].data_ptr() if xs is not None and xs[i] is not None else None
+        d.dx[i] = dxs[i].data_ptr() if dxs is not None and dxs[i] is not None else None
+        d.c[i] = c
+    d.cout, d.kh, d.kw, d.stride, d.pad = cout, k, k, stride, pad
+    return d
+
+
+def _ref_conv(x_nhwc_list, w_krsc, stride, pad):
+    x = torch.cat([t.double().cpu() for t in x_nhwc_list], dim=3).permute(0, 3, 1, 2)
+    w = w_krsc.double().cpu().permute(0, 3, 1, 2)
+    x.requires_grad_(True)
+    w.requires_grad_(True)
+    y = torch.nn.functional.conv2d(x, w, stride=stride, padding=pad)
+    return x, w, y
+
+
+def _close(a, b, tol=TF32_TOL):
+    a = a.double().cpu()
+    b = b.double().cpu()
+    scale = max(b.abs().max().item(), 1e-30)
+    err = (a - b).abs().max().item() / scale
+    assert err < tol, f"max rel err {err:.3e} (scale {scale:.3e})"
+
+
+CASES = [
+    # n, h, w, segs, cout, k, stride, pad
+    (2, 14, 14, [64], 128, 3, 1, 1),
+    (2, 9, 9, [32, 32, 16], 64, 3, 1, 1),     # concat join, partial chunk
+    (3, 35, 35, [3], 64, 11, 4, 0),           # AlexNet-style first layer (scalar K)
+    (2, 8, 8, [5, 3], 7, 3, 1, 1),            # odd channels everywhere (scalar paths)
+    (4, 7, 7, [256], 96, 1, 1, 0),            # 1x1
+    (5, 1, 1, [300], 40, 1, 1, 0),            # FC as 1x1 over a 1x1 image
+    (2, 12, 12, [8], 300, 5, 1, 2),           # Cout > tile N
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_conv_fprop_dgrad_wgrad(case):
+    dev = _dev()
+    n, h, w, segs, cout, k, stride, pad = case
+    g = torch.Generator().manual_seed(CASES.index(case) + 1)
+    xs = [torch.randn(n, h, w, c, generator=g).to(dev) for c in segs]
+    cin = sum(segs)
+    wt = (torch.randn(cout, k, k, cin, generator=g) * (2.0 / (k * k * cin)) ** 0.5).to(dev)
+    ho = (h + 2 * pad - k) // stride + 1
+    wo = (w + 2 * pad - k) // stride + 1
+    y = torch.empty(n, ho, wo, cout, device=dev)
+    d = _desc(n, h, w, xs, segs, cout, k, stride, pad)
+    L.call("vdnn_kernel_conv_fprop", C.byref(d), C.c_void_p(wt.data_ptr()), None, C.c_void_p(y.data_ptr()), None)
+    torch.cuda.synchronize()
+    xr, wr, yr = _ref_conv(xs, wt, stride, pad)
+    _close(y, yr.permute(0, 2, 3, 1))
+
+    dy = torch.randn(n, ho, wo, cout, generator=g).to(dev)
+    yr.backward(dy.double().cpu().permute(0, 3, 1, 2))
+    if stride == 1:
+        dxs = [torch.full_like(t, float("nan")) for t in xs]
+        d2 = _desc(n, h, w, xs, segs, cout, k, stride, pad, dxs)
+        L.call("vdnn_kernel_conv_dgrad", C.byref(d2), C.c_void_p(wt.data_ptr()), C.c_void_p(dy.data_ptr()),
+               0, None)
+        torch.cuda.synchronize()
+        gx = xr.grad.permute(0, 2, 3, 1)
+        off = 0
+        for t, c in zip(dxs, segs):
+            _close(t, gx[..., off:off + c])
+            off += c
+    # wgrad with dW output (no SGD), with and without split-K workspace
+    for use_ws in (False, True):
+        dw = torch.full_like(wt, float("nan"))
+        ws_bytes = L.lib().vdnn_kernel_conv_wgrad_ws_bytes(C.byref(d)) if use_ws else 0
+        ws = torch.empty(max(ws_bytes // 4, 1), device=dev)
+        L.call("vdnn_kernel_conv_wgrad", C.byref(d), C.c_void_p(dy.data_ptr()), C.c_void_p(wt.data_ptr()),
+               C.c_float(0.0), C.c_void_p(dw.data_ptr()), C.c_void_p(ws.data_ptr() if use_ws else 0),
+               C.c_size_t(ws_bytes), None)
+        torch.cuda.synchronize()
+        _close(dw, wr.grad.permute(0, 2, 3, 1))
+    # fused SGD epilogue
+    w2 = wt.clone()
+    lr = 0.01
+    L.call("vdnn_kernel_conv_wgrad", C.byref(d), C.c_void_p(dy.data_ptr()), C.c_void_p(w2.data_ptr()),
+           C.c_float(lr), None, None, C.c_size_t(0), None)
+    torch.cuda.synchronize()
+    ref = wt.double().cpu() - lr * wr.grad.permute(0, 2, 3, 1)
+    diff = (w2.double().cpu() - ref).abs().max().item()
+    assert diff < TF32_TOL * lr * max(wr.grad.abs().max().item(), 1e-30) + 1e-7
+
+
+def test_wgrad_split_k_large_reduction():
+    """K = N*Ho*Wo large enough that split-K partials + reduce kernel run."""
+    dev = _dev()
+    n, h, w, c, cout = 8, 56, 56, 64, 64
+    g = torch.Generator().manual_seed(7)
+    x = torch.randn(n, h, w, c, generator=g).to(dev)
+    dy = torch.randn(n, h, w, cout, generator=g).to(dev)
+    wt = torch.zeros(cout, 3, 3, c, device=dev)
+    d = _desc(n, h, w, [x], [c], cout, 3, 1, 1)
+    ws_bytes = L.lib().vdnn_kernel_conv_wgrad_ws_bytes(C.byref(d))
+    assert ws_bytes > 0
+    ws = torch.empty(ws_bytes // 4, device=dev)
+    dw = torch.empty_like(wt)
+    L.call("vdnn_kernel_conv_wgrad", C.byref(d), C.c_void_p(dy.data_ptr()), C.c_void_p(wt.data_ptr()),
+           C.c_float(0.0), C.c_void_p(dw.data_ptr()), C.c_void_p(ws.data_ptr()), C.c_size_t(ws_bytes), None)
+    torch.cuda.synchronize()
+    xr, wr, yr = _ref_conv([x], wt, 1, 1)
+    yr.backward(dy.double().cpu().permute(0, 3, 1, 2))
+    _close(dw, wr.grad.permute(0, 2, 3, 1))
+
+
+@pytest.mark.parametrize("window,stride,segs", [(3, 2, [64]), (2, 2, [16, 8]), (2, 2, [3])])
+def test_maxpool(window, stride, segs):
+    dev = _dev()
+    n, h, w = 2, 13, 13
+    g = torch.Generator().manual_seed(3)
+    # ties on purpose: relu'd inputs have many zeros
+    xs = [torch.relu(torch.randn(n, h, w, c, generator=g)).to(dev) for c in segs]
+    ho, wo = (h - window) // stride + 1, (w - window) // stride + 1
+    ct = sum(segs)
+    y = torch.empty(n, ho, wo, ct, device=dev)
+    d = _desc(n, h, w, xs, segs, 0, 1, 1, 0)
+    L.call("vdnn_kernel_maxpool_fwd", C.byref(d), window, stride, C.c_void_p(y.data_ptr()), None)
+    torch.cuda.synchronize()
+    xc = torch.cat([t.cpu() for t in xs], dim=3).permute(0, 3, 1, 2).double().requires_grad_(True)
+    yr = torch.nn.functional.max_pool2d(xc, window, stride)
+    assert torch.equal(y.cpu().double(), yr.detach().permute(0, 2, 3, 1))
+    dy = torch.randn(n, ho, wo, ct, generator=g).to(dev)
+    dxs = [torch.full_like(t, float("nan")) for t in xs]
+    d2 = _desc(n, h, w, xs, segs, 0, 1, 1, 0, dxs)
+    L.call("vdnn_kernel_maxpool_bwd", C.byref(d2), window, stride, C.c_void_p(y.data_ptr()),
+           C.c_void_p(dy.data_ptr()), None)
+    torch.cuda.synchronize()
+    yr.backward(dy.cpu().double().permute(0, 3, 1, 2))
+    gx = xc.grad.permute(0, 2, 3, 1)
+    off = 0
+    for t, c in zip(dxs, segs):
+        torch.testing.assert_close(t.cpu().double(), gx[..., off:off + c], rtol=1e-6, atol=1e-6)
+        off += c
+
+
+def test_relu_and_softmax():
+    dev = _dev()
+    g = torch.Generator().manual_seed(11)
+    x = torch.randn(1000003, generator=g).to(dev)
+    y = x.clone()
+    L.call("vdnn_kernel_relu_fwd", C.c_void_p(y.data_ptr()), C.c_size_t(y.numel()), None)
+    gr = torch.randn(1000003, generator=g).to(dev)
+    g2 = gr.clone()
+    L.call("vdnn_kernel_relu_bwd", C.c_void_p(g2.data_ptr()), C.c_void_p(y.data_ptr()), C.c_size_t(y.numel()), None)
+    torch.cuda.synchronize()
+    assert torch.equal(y, torch.relu(x))
+    assert torch.equal(g2, torch.where(y > 0, gr, torch.zeros_like(gr)))
+    n, k = 37, 1000
+    z = torch.randn(n, k, generator=g).to(dev) * 3
+    lab = torch.randint(0, k, (n,), generator=g, dtype=torch.int32).to(dev)
+    grad = torch.empty(n, k, device=dev)
+    rl = torch.empty(n, device=dev)
+    loss = torch.empty(1, device=dev)
+    L.call("vdnn_kernel_softmax_xent", C.c_void_p(z.data_ptr()), C.c_void_p(lab.data_ptr()), n, k,
+           C.c_void_p(grad.data_ptr()), C.c_void_p(rl.data_ptr()), C.c_void_p(loss.data_ptr()), None)
+    torch.cuda.synchronize()
+    zr = z.double().cpu().requires_grad_(True)
+    lr_ = torch.nn.functional.cross_entropy(zr, lab.long().cpu())
+    lr_.backward()
+    assert abs(loss.item() - lr_.item()) < 1e-5 * max(1.0, abs(lr_.item()))
+    torch.testing.assert_close(grad.double().cpu(), zr.grad, rtol=1e-4, atol=1e-7)
