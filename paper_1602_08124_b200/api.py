@@ -1,0 +1,708 @@
+"""Python mirror of the reference's network-definition and offload-policy API.
+
+Names, argument meaning and error behaviour follow vdnnsim
+(/root/reference/proj/include/vdnnsim): ``NetworkGraph`` (net_graph.hpp:101),
+``build_preset``/``extend_vgg`` (presets.hpp:123-140), ``CostModel``
+(cost_model.hpp:65), ``static_decision`` (decision.hpp:68), ``simulate``
+(simulator.hpp:568), ``dynamic_select`` (policy.hpp:115), ``greedy_downgrade``
+(policy.hpp:65), ``simulate_oracle`` (policy.hpp:152), ``replay_check``
+(replay.hpp:95), ``baseline_footprint`` (footprint.hpp:81). Everything runs in
+libvdnn.so (C++ planner); this module only marshals.
+
+Errors: the reference throws ``vdnnsim::Error`` subclasses; here the same
+conditions raise the matching Python exception below (all subclasses of
+``VdnnError``). OOM is never an exception: it is ``RunReport.pass_ = False``
+with ``RunReport.oom`` set.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from . import _lib as L
+from ._lib import VdnnError
+
+KUNLIMITED_BYTES = 1 << 62  # core.hpp:17
+
+
+class ShapeMismatch(VdnnError):
+    pass
+
+
+class UnknownPreset(VdnnError):
+    pass
+
+
+class InvalidDepth(VdnnError):
+    pass
+
+
+class OverflowError_(VdnnError):
+    pass
+
+
+class WrongLayerKind(VdnnError):
+    pass
+
+
+class PoolUseError(VdnnError):
+    pass
+
+
+class InvalidDecision(VdnnError):
+    pass
+
+
+class ConfigError(VdnnError):
+    pass
+
+
+_ERRS = {
+    L.SHAPE_MISMATCH: ShapeMismatch, L.UNKNOWN_PRESET: UnknownPreset, L.INVALID_DEPTH: InvalidDepth,
+    L.OVERFLOW: OverflowError_, L.WRONG_LAYER_KIND: WrongLayerKind, L.POOL_MISUSE: PoolUseError,
+    L.INVALID_DECISION: InvalidDecision, L.CONFIG_ERROR: ConfigError,
+}
+
+
+def _call(name: str, *args) -> None:
+    st = getattr(L.lib(), name)(*args)
+    if st != L.OK:
+        msg = L.lib().vdnn_last_error().decode(errors="replace")
+        raise _ERRS.get(st, VdnnError)(st, msg)
+
+
+class LayerKind(enum.IntEnum):
+    Input = 0
+    Conv = 1
+    Actv = 2
+    Pool = 3
+    Fc = 4
+    Loss = 5
+
+
+class JoinRule(enum.IntEnum):
+    Concat = 0
+    Elementwise = 1
+
+
+class AlgoId(enum.IntEnum):
+    ImplicitGemm = 0
+    GemmWs = 1
+    Fft = 2
+
+
+class PolicyKind(enum.IntEnum):
+    Baseline = 0
+    VdnnAll = 1
+    VdnnConv = 2
+
+
+class AlgoMode(enum.IntEnum):
+    MemoryOptimal = 0
+    PerfOptimal = 1
+
+
+class GradientScheme(enum.IntEnum):
+    TwoBufferReuse = 0
+    PerLayer = 1
+
+
+class Stream(enum.IntEnum):
+    Compute = 0
+    Memory = 1
+
+
+class EventKind(enum.IntEnum):
+    Fwd = 0
+    Bwd = 1
+    Offload = 2
+    Prefetch = 3
+    Alloc = 4
+    Release = 5
+    Sync = 6
+
+
+class Phase(enum.IntEnum):
+    Setup = 0
+    Forward = 1
+    Backward = 2
+
+
+_EV_NAMES = ["FWD", "BWD", "OFFLOAD", "PREFETCH", "ALLOC", "RELEASE", "SYNC"]
+_PHASE_NAMES = ["setup", "forward", "backward"]
+
+
+@dataclass(frozen=True)
+class TensorShape:
+    n: int
+    c: int
+    h: int
+    w: int
+
+    def elements(self) -> int:
+        return self.n * self.c * self.h * self.w
+
+
+@dataclass(frozen=True)
+class LayerDescriptor:
+    id: int
+    kind: LayerKind
+    inputs: Tuple[int, ...]
+    join: JoinRule
+    params: Tuple[int, int, int, int]
+
+
+# ------------------------------------------------------------------ graph --
+class NetworkGraph:
+    """DAG of layers in topological id order (net_graph.hpp:101-229)."""
+
+    def __init__(self, batch: int = 1, _handle=None):
+        self._h = C.c_void_p()
+        if _handle is not None:
+            self._h = _handle
+        else:
+            _call("vdnn_graph_create", C.c_uint64(batch), C.byref(self._h))
+        self._finalized = _handle is not None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and L._lib is not None:
+            L._lib.vdnn_graph_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @staticmethod
+    def _ins(inputs: Sequence[int]):
+        arr = (C.c_int32 * max(len(inputs), 1))(*inputs)
+        return arr, len(inputs)
+
+    def add_input(self, c: int, h: int, w: int) -> int:
+        out = C.c_int32()
+        _call("vdnn_graph_add_input", self._h, C.c_uint64(c), C.c_uint64(h), C.c_uint64(w), C.byref(out))
+        return out.value
+
+    def add_conv(self, inputs: Sequence[int], out_channels: int, kernel: int, stride: int, pad: int,
+                 join: JoinRule = JoinRule.Concat) -> int:
+        arr, n = self._ins(inputs)
+        out = C.c_int32()
+        _call("vdnn_graph_add_conv", self._h, arr, n, C.c_uint64(out_channels), C.c_uint64(kernel),
+              C.c_uint64(stride), C.c_uint64(pad), int(join), C.byref(out))
+        return out.value
+
+    def add_actv(self, inp: int) -> int:
+        out = C.c_int32()
+        _call("vdnn_graph_add_actv", self._h, int(inp), C.byref(out))
+        return out.value
+
+    def add_pool(self, inputs: Sequence[int], window: int, stride: int, join: JoinRule = JoinRule.Concat) -> int:
+        arr, n = self._ins(inputs)
+        out = C.c_int32()
+        _call("vdnn_graph_add_pool", self._h, arr, n, C.c_uint64(window), C.c_uint64(stride), int(join), C.byref(out))
+        return out.value
+
+    def add_fc(self, inputs: Sequence[int], out_features: int, join: JoinRule = JoinRule.Concat) -> int:
+        arr, n = self._ins(inputs)
+        out = C.c_int32()
+        _call("vdnn_graph_add_fc", self._h, arr, n, C.c_uint64(out_features), int(join), C.byref(out))
+        return out.value
+
+    def add_loss(self, inp: int) -> int:
+        out = C.c_int32()
+        _call("vdnn_graph_add_loss", self._h, int(inp), C.byref(out))
+        return out.value
+
+    def finalize(self) -> "NetworkGraph":
+        _call("vdnn_graph_finalize", self._h)
+        self._finalized = True
+        return self
+
+    def size(self) -> int:
+        n = C.c_int32()
+        _call("vdnn_graph_size", self._h, C.byref(n))
+        return n.value
+
+    def __len__(self) -> int:
+        return self.size()
+
+    @property
+    def batch(self) -> int:
+        b = C.c_uint64()
+        _call("vdnn_graph_batch", self._h, C.byref(b))
+        return b.value
+
+    def _info(self, id: int) -> L.LayerInfo:
+        info = L.LayerInfo()
+        _call("vdnn_graph_layer", self._h, int(id), C.byref(info))
+        return info
+
+    def layer(self, id: int) -> LayerDescriptor:
+        i = self._info(id)
+        return LayerDescriptor(i.id, LayerKind(i.kind), tuple(i.inputs[: i.n_inputs]), JoinRule(i.join),
+                               (i.p0, i.p1, i.p2, i.p3))
+
+    def layers(self) -> List[LayerDescriptor]:
+        return [self.layer(i) for i in range(self.size())]
+
+    def shape(self, id: int) -> TensorShape:
+        i = self._info(id)
+        return TensorShape(i.n, i.c, i.h, i.w)
+
+    def refcnt(self, id: int) -> int:
+        return self._info(id).refcnt
+
+    def count_kind(self, k: LayerKind) -> int:
+        return sum(1 for l in self.layers() if l.kind == k)
+
+    def spec(self) -> str:
+        """Text form consumed by the oracle shim (oracle/ref_shim.cpp)."""
+        parts = [f"B={self.batch}"]
+        names = ["input", "conv", "actv", "pool", "fc", "loss"]
+        for l in self.layers():
+            ins = ",".join(str(q) for q in l.inputs) if l.inputs else "-"
+            parts.append(f"{names[l.kind]} {ins} {l.params[0]} {l.params[1]} {l.params[2]} {l.params[3]} {int(l.join)}")
+        return "|".join(parts)
+
+
+def build_preset(name: str, batch: int) -> NetworkGraph:
+    h = C.c_void_p()
+    _call("vdnn_preset", name.encode(), C.c_uint64(batch), C.byref(h))
+    return NetworkGraph(_handle=h)
+
+
+def extend_vgg(extra_conv_layers: int, batch: int) -> NetworkGraph:
+    h = C.c_void_p()
+    _call("vdnn_extend_vgg", int(extra_conv_layers), C.c_uint64(batch), C.byref(h))
+    return NetworkGraph(_handle=h)
+
+
+# ------------------------------------------------------------- cost model --
+@dataclass
+class CostModel:
+    """cost_model.hpp:15-26,65-75 (defaults: Titan X, PCIe 3)."""
+    peak_flops: float = 7e12
+    dram_bw: float = 336e9
+    mem_capacity: int = 12884901888
+    compute_efficiency: float = 0.5
+    link_effective_bw: float = 12.8e9
+    link_nominal_bw: float = 16e9
+    link_fixed_launch_overhead: float = 0.0
+    elem_size: int = 4
+    bwd_fwd_ratio: float = 2.0
+    speed_factor_implicit_gemm: float = 1.0
+    speed_factor_gemm_ws: float = 0.8
+    speed_factor_fft: float = 0.6
+    latency_overrides: Dict[int, Tuple[float, float]] = field(default_factory=dict)
+
+    def _c(self):
+        cm = L.CostModelC()
+        cm.peak_flops = self.peak_flops
+        cm.dram_bw = self.dram_bw
+        cm.mem_capacity = self.mem_capacity
+        cm.compute_efficiency = self.compute_efficiency
+        cm.link_effective_bw = self.link_effective_bw
+        cm.link_nominal_bw = self.link_nominal_bw
+        cm.link_launch_overhead = self.link_fixed_launch_overhead
+        cm.elem_size = self.elem_size
+        cm.bwd_fwd_ratio = self.bwd_fwd_ratio
+        cm.speed_factor_implicit_gemm = self.speed_factor_implicit_gemm
+        cm.speed_factor_gemm_ws = self.speed_factor_gemm_ws
+        cm.speed_factor_fft = self.speed_factor_fft
+        ids = sorted(self.latency_overrides)
+        n = len(ids)
+        keep = ((C.c_int32 * max(n, 1))(*ids), (C.c_double * max(n, 1))(*[self.latency_overrides[i][0] for i in ids]),
+                (C.c_double * max(n, 1))(*[self.latency_overrides[i][1] for i in ids]))
+        cm.n_overrides = n
+        cm.override_layer = C.cast(keep[0], C.POINTER(C.c_int32))
+        cm.override_fwd_s = C.cast(keep[1], C.POINTER(C.c_double))
+        cm.override_bwd_s = C.cast(keep[2], C.POINTER(C.c_double))
+        cm._keep = keep
+        return cm
+
+    def spec(self) -> str:
+        """Text form consumed by the oracle shim."""
+        kv = (f"pf={self.peak_flops!r},bw={self.dram_bw!r},cap={self.mem_capacity},eff={self.compute_efficiency!r},"
+              f"lbw={self.link_effective_bw!r},lnom={self.link_nominal_bw!r},lov={self.link_fixed_launch_overhead!r},"
+              f"es={self.elem_size},ratio={self.bwd_fwd_ratio!r},sfi={self.speed_factor_implicit_gemm!r},"
+              f"sfg={self.speed_factor_gemm_ws!r},sff={self.speed_factor_fft!r}")
+        if self.latency_overrides:
+            kv += ";ov=" + ",".join(f"{i}:{f!r}:{b!r}" for i, (f, b) in sorted(self.latency_overrides.items()))
+        return kv
+
+    def _u64(self, fn, g, id, *extra):
+        out = C.c_uint64()
+        cm = self._c()
+        _call(fn, C.byref(cm), g.handle, int(id), *extra, C.byref(out))
+        return out.value
+
+    def tensor_bytes_of_layer(self, g: NetworkGraph, id: int) -> int:
+        return self._u64("vdnn_cost_tensor_bytes", g, id)
+
+    def tensor_bytes_of(self, shape: TensorShape) -> int:
+        return shape.elements() * self.elem_size
+
+    def weight_bytes(self, g: NetworkGraph, id: int) -> int:
+        return self._u64("vdnn_cost_weight_bytes", g, id)
+
+    def conv_workspace(self, g: NetworkGraph, id: int, algo: AlgoId) -> int:
+        return self._u64("vdnn_cost_conv_workspace", g, id, int(algo))
+
+    def layer_latency(self, g: NetworkGraph, id: int, bwd: bool = False, algo: AlgoId = AlgoId.ImplicitGemm) -> float:
+        out = C.c_double()
+        cm = self._c()
+        _call("vdnn_cost_layer_latency", C.byref(cm), g.handle, int(id), int(bool(bwd)), int(algo), C.byref(out))
+        return out.value
+
+    def flops(self, g: NetworkGraph, id: int, bwd: bool = False) -> float:
+        out = C.c_double()
+        cm = self._c()
+        _call("vdnn_cost_flops", C.byref(cm), g.handle, int(id), int(bool(bwd)), C.byref(out))
+        return out.value
+
+    def transfer_latency(self, nbytes: int) -> float:
+        out = C.c_double()
+        cm = self._c()
+        _call("vdnn_cost_transfer_latency", C.byref(cm), C.c_uint64(nbytes), C.byref(out))
+        return out.value
+
+    def fastest_algo(self, g: NetworkGraph, id: int) -> AlgoId:
+        out = C.c_int32()
+        cm = self._c()
+        _call("vdnn_cost_fastest_algo", C.byref(cm), g.handle, int(id), C.byref(out))
+        return AlgoId(out.value)
+
+    def fft_applicable(self, g: NetworkGraph, id: int) -> bool:
+        l = g.layer(id)
+        return l.kind == LayerKind.Conv and l.params[1] == 1
+
+    def offload_interference_bound(self) -> float:
+        return self.link_nominal_bw / self.dram_bw
+
+
+def gradient_map_bytes(g: NetworkGraph, m: int, cm: CostModel) -> int:
+    return cm._u64("vdnn_gradient_map_bytes", g, m)
+
+
+# -------------------------------------------------------------- decisions --
+@dataclass
+class PolicyDecision:
+    """decision.hpp:30-57."""
+    offload: List[int]
+    algos: Dict[int, AlgoId]
+    gradient_scheme: GradientScheme = GradientScheme.PerLayer
+    label: str = ""
+
+    def offloads(self, id: int) -> bool:
+        return bool(self.offload[id])
+
+    @classmethod
+    def _from_handle(cls, h) -> "PolicyDecision":
+        n = C.c_int32()
+        _call("vdnn_decision_get", h, C.byref(n), None, None, None, None, C.c_size_t(0))
+        flags = (C.c_char * max(n.value, 1))()
+        algos = (C.c_int32 * max(n.value, 1))()
+        scheme = C.c_int32()
+        label = C.create_string_buffer(256)
+        _call("vdnn_decision_get", h, C.byref(n), flags, algos, C.byref(scheme), label, C.c_size_t(256))
+        return cls([1 if flags[i] != b"\x00" else 0 for i in range(n.value)],
+                   {i: AlgoId(algos[i]) for i in range(n.value) if algos[i] >= 0},
+                   GradientScheme(scheme.value), label.value.decode())
+
+    def _handle(self, g: NetworkGraph):
+        h = C.c_void_p()
+        _call("vdnn_decision_create", g.handle, C.byref(h))
+        try:
+            # the C side sizes offload to the graph; re-create if sizes differ (validate reports it)
+            if len(self.offload) != g.size():
+                raise InvalidDecision(L.INVALID_DECISION, "offload flags do not cover the graph")
+            for i, f in enumerate(self.offload):
+                if f:
+                    _call("vdnn_decision_set_offload", h, i, 1)
+            for i, a in self.algos.items():
+                _call("vdnn_decision_set_algo", h, int(i), int(a))
+            _call("vdnn_decision_set_scheme", h, int(self.gradient_scheme))
+            _call("vdnn_decision_set_label", h, self.label.encode())
+        except Exception:
+            L.lib().vdnn_decision_destroy(h)
+            raise
+        return _Owned(h, "vdnn_decision_destroy")
+
+    def validate(self, g: NetworkGraph) -> None:
+        d = self._handle(g)
+        _call("vdnn_decision_validate", d.h, g.handle)
+
+    def spec(self) -> str:
+        """Oracle-shim form: custom:<scheme>:<label>:<offload ids>:<id=algo>."""
+        off = ",".join(str(i) for i, f in enumerate(self.offload) if f)
+        alg = ",".join(f"{i}={int(a)}" for i, a in sorted(self.algos.items()))
+        return f"custom:{int(self.gradient_scheme)}:{self.label}:{off}:{alg}"
+
+
+class _Owned:
+    def __init__(self, h, destroy):
+        self.h = h
+        self._destroy = destroy
+
+    def __del__(self):
+        if self.h is not None and self.h.value and L._lib is not None:
+            getattr(L._lib, self._destroy)(self.h)
+            self.h = None
+
+
+def static_decision(kind: PolicyKind, mode: AlgoMode, g: NetworkGraph, cm: CostModel) -> PolicyDecision:
+    h = C.c_void_p()
+    c = cm._c()
+    _call("vdnn_decision_static", g.handle, int(kind), int(mode), C.byref(c), C.byref(h))
+    o = _Owned(h, "vdnn_decision_destroy")
+    return PolicyDecision._from_handle(o.h)
+
+
+# ---------------------------------------------------------------- reports --
+@dataclass
+class StreamEvent:
+    stream: Stream
+    kind: EventKind
+    layer: int
+    start: int
+    end: int
+    bytes: int
+    tag: str = ""
+    buffer: int = -1
+    offset: int = 0
+
+
+@dataclass
+class OomInfo:
+    layer: int
+    phase: Phase
+    fragmented: bool
+    requested: int
+    tag: str
+
+
+@dataclass
+class SimOptions:
+    keep_pool_trace: bool = False
+    include_weight_grads: bool = False
+
+
+class RunReport:
+    """sim_types.hpp:63-90; events are materialised lazily."""
+
+    def __init__(self, handle):
+        self._own = _Owned(handle, "vdnn_report_destroy")
+        s = L.ReportSummary()
+        _call("vdnn_report_summary_get", handle, C.byref(s))
+        self.pass_ = bool(s.pass_)
+        self.oom = (OomInfo(s.oom_layer, Phase(s.oom_phase), bool(s.oom_fragmented), s.oom_requested,
+                            s.oom_tag.decode()) if s.has_oom else None)
+        self.max_mem_bytes = s.max_mem_bytes
+        self.avg_mem_bytes = s.avg_mem_bytes
+        self.offload_traffic_bytes = s.offload_traffic_bytes
+        self.prefetch_traffic_bytes = s.prefetch_traffic_bytes
+        self.host_peak_bytes = s.host_peak_bytes
+        self.stall_fwd_offload_ns = s.stall_fwd_offload_ns
+        self.stall_bwd_prefetch_ns = s.stall_bwd_prefetch_ns
+        self.total_ns = s.total_ns
+        self.interference_bound = s.interference_bound
+        self._verdict = s.verdict.decode()
+        self._n = s.n_events
+        self._events = None
+
+    @property
+    def handle(self):
+        return self._own.h
+
+    def verdict(self) -> str:
+        return self._verdict
+
+    def stall_ns(self) -> int:
+        return self.stall_fwd_offload_ns + self.stall_bwd_prefetch_ns
+
+    def raw_events(self):
+        arr = (L.Event * max(self._n, 1))()
+        n = C.c_size_t()
+        _call("vdnn_report_events", self.handle, arr, C.c_size_t(self._n), C.byref(n))
+        return arr, n.value
+
+    @property
+    def events(self) -> List[StreamEvent]:
+        if self._events is None:
+            arr, n = self.raw_events()
+            self._events = [StreamEvent(Stream(e.stream), EventKind(e.kind), e.layer, e.start_ns, e.end_ns, e.bytes,
+                                        e.tag.decode(), e.buffer, e.offset) for e in arr[:n]]
+        return self._events
+
+    @property
+    def reuse_distance_ns(self) -> List[int]:
+        n = C.c_size_t()
+        _call("vdnn_report_reuse_distance", self.handle, None, C.c_size_t(0), C.byref(n))
+        out = (C.c_int64 * max(n.value, 1))()
+        _call("vdnn_report_reuse_distance", self.handle, out, n, C.byref(n))
+        return list(out[: n.value])
+
+    def pool_trace(self):
+        n = C.c_size_t()
+        _call("vdnn_report_pool_trace", self.handle, None, C.c_size_t(0), C.byref(n))
+        out = (L.PoolTraceRow * max(n.value, 1))()
+        _call("vdnn_report_pool_trace", self.handle, out, n, C.byref(n))
+        return [(r.time_ns, r.op.decode(), r.tag.decode(), r.offset, r.bytes, r.current, r.high_water)
+                for r in out[: n.value]]
+
+    def signature(self) -> str:
+        s = C.c_uint64()
+        _call("vdnn_report_signature", self.handle, C.byref(s))
+        return f"{s.value:016x}"
+
+    def layer_peaks(self, layers: int) -> Tuple[List[int], List[int]]:
+        f = (C.c_uint64 * max(layers, 1))()
+        b = (C.c_uint64 * max(layers, 1))()
+        _call("vdnn_report_layer_peaks", self.handle, int(layers), f, b)
+        return list(f[:layers]), list(b[:layers])
+
+
+def simulate(g: NetworkGraph, decision: PolicyDecision, cost: CostModel, capacity: int,
+             options: Optional[SimOptions] = None) -> RunReport:
+    options = options or SimOptions()
+    d = decision._handle(g)
+    c = cost._c()
+    flags = (1 if options.keep_pool_trace else 0) | (2 if options.include_weight_grads else 0)
+    h = C.c_void_p()
+    _call("vdnn_simulate", g.handle, d.h, C.byref(c), C.c_uint64(capacity), C.c_uint32(flags), C.byref(h))
+    return RunReport(h)
+
+
+def simulate_with_trace(g, decision, cost, capacity, options: Optional[SimOptions] = None):
+    opts = SimOptions(True, (options or SimOptions()).include_weight_grads)
+    r = simulate(g, decision, cost, capacity, opts)
+    return r, r.pool_trace()
+
+
+def simulate_oracle(g: NetworkGraph, cost: CostModel) -> RunReport:
+    c = cost._c()
+    h = C.c_void_p()
+    _call("vdnn_simulate_oracle", g.handle, C.byref(c), C.byref(h))
+    return RunReport(h)
+
+
+def per_layer_event_peaks(report: RunReport, layers: int) -> Tuple[List[int], List[int]]:
+    return report.layer_peaks(layers)
+
+
+@dataclass
+class ProfilePassResult:
+    phase: str
+    decision: PolicyDecision
+    pass_: bool
+    oom: Optional[OomInfo]
+    total_ns: int
+    max_mem_bytes: int
+
+
+@dataclass
+class DynamicSelection:
+    decision: Optional[PolicyDecision]
+    passes: List[ProfilePassResult]
+
+    def untrainable(self) -> bool:
+        return self.decision is None
+
+
+def dynamic_select(g: NetworkGraph, capacity: int, cost: CostModel) -> DynamicSelection:
+    c = cost._c()
+    h = C.c_void_p()
+    _call("vdnn_dynamic_select", g.handle, C.c_uint64(capacity), C.byref(c), C.byref(h))
+    own = _Owned(h, "vdnn_dyn_destroy")
+    n = C.c_size_t()
+    _call("vdnn_dyn_passes", own.h, None, C.c_size_t(0), C.byref(n))
+    infos = (L.PassInfo * max(n.value, 1))()
+    _call("vdnn_dyn_passes", own.h, infos, n, C.byref(n))
+    passes = []
+    for i, p in enumerate(infos[: n.value]):
+        dh = C.c_void_p()
+        _call("vdnn_dyn_pass_decision", own.h, C.c_size_t(i), C.byref(dh))
+        down = _Owned(dh, "vdnn_decision_destroy")
+        d = PolicyDecision._from_handle(down.h)
+        oom = OomInfo(p.oom_layer, Phase(p.oom_phase), False, 0, "") if p.has_oom else None
+        passes.append(ProfilePassResult(p.phase.decode(), d, bool(p.pass_), oom, p.total_ns, p.max_mem_bytes))
+    u = C.c_int32()
+    _call("vdnn_dyn_untrainable", own.h, C.byref(u))
+    dec = None
+    if not u.value:
+        dh = C.c_void_p()
+        _call("vdnn_dyn_decision", own.h, C.byref(dh))
+        down = _Owned(dh, "vdnn_decision_destroy")
+        dec = PolicyDecision._from_handle(down.h)
+    return DynamicSelection(dec, passes)
+
+
+def greedy_downgrade(g: NetworkGraph, capacity: int, offload_kind: PolicyKind, cost: CostModel
+                     ) -> Optional[PolicyDecision]:
+    c = cost._c()
+    found = C.c_int32()
+    h = C.c_void_p()
+    _call("vdnn_greedy_downgrade", g.handle, C.c_uint64(capacity), int(offload_kind), C.byref(c), C.byref(found),
+          C.byref(h))
+    if not found.value:
+        return None
+    own = _Owned(h, "vdnn_decision_destroy")
+    return PolicyDecision._from_handle(own.h)
+
+
+@dataclass
+class Violation:
+    kind: str
+    detail: str
+
+
+def replay_check(report: RunReport, g: NetworkGraph, decision: PolicyDecision, capacity: int) -> List[Violation]:
+    d = decision._handle(g)
+    n = C.c_size_t()
+    _call("vdnn_replay_check", report.handle, g.handle, d.h, C.c_uint64(capacity), None, C.c_size_t(0), C.byref(n))
+    out = (L.Violation * max(n.value, 1))()
+    _call("vdnn_replay_check", report.handle, g.handle, d.h, C.c_uint64(capacity), out, n, C.byref(n))
+    return [Violation(v.kind.decode(), v.detail.decode()) for v in out[: n.value]]
+
+
+@dataclass
+class FootprintReport:
+    weights_bytes: int
+    feature_maps_bytes: int
+    gradient_buffers_bytes: int
+    workspace_bytes: int
+    total_bytes: int
+    classifier_bytes: int
+
+    def feature_map_fraction(self) -> float:
+        return 0.0 if self.total_bytes == 0 else self.feature_maps_bytes / self.total_bytes
+
+
+def baseline_footprint(g: NetworkGraph, algos: Dict[int, AlgoId], cost: CostModel,
+                       include_weight_grads: bool = False) -> FootprintReport:
+    dec = PolicyDecision([0] * g.size(), dict(algos), GradientScheme.PerLayer, "")
+    d = dec._handle(g)
+    c = cost._c()
+    f = L.Footprint()
+    _call("vdnn_baseline_footprint", g.handle, d.h, C.byref(c), int(bool(include_weight_grads)), C.byref(f))
+    return FootprintReport(f.weights_bytes, f.feature_maps_bytes, f.gradient_buffers_bytes, f.workspace_bytes,
+                           f.total_bytes, f.classifier_bytes)
+
+
+def report_from_events(events, summary: Dict) -> RunReport:
+    """Wrap an externally produced event log (e.g. measured) as a RunReport."""
+    n = len(events)
+    arr = (L.Event * max(n, 1))()
+    for i, e in enumerate(events):
+        arr[i].stream, arr[i].kind, arr[i].layer, arr[i].buffer = int(e.stream), int(e.kind), e.layer, e.buffer
+        arr[i].start_ns, arr[i].end_ns, arr[i].bytes, arr[i].offset = e.start, e.end, e.bytes, e.offset
+        arr[i].tag = e.tag.encode()
+    s = L.ReportSummary()
+    for k, v in summary.items():
+        setattr(s, k, v)
+    h = C.c_void_p()
+    _call("vdnn_report_from_events", arr, C.c_size_t(n), C.byref(s), C.byref(h))
+    return RunReport(h)
