@@ -1,0 +1,240 @@
+"""ORACLE ONLY: CPU restatement of one training iteration as the executor runs it.
+
+The reference (vdnnsim) computes no values -- "numerical gradient computation
+is OUT of scope" -- so numeric parity is
+*unpinned by the reference*; this module restates the dataflow the reference
+fixes (simulator.hpp:90-131, footprint.hpp:58-71, net_graph.hpp:384-389) with
+standard definitions, in float64 on the CPU:
+
+* buffers are per feature-buffer owner; ACTV (ReLU) is applied *in place* on
+  the owner's buffer, and its backward masks the incoming gradient by
+  (owner buffer > 0) -- the same aliasing the reference's buffer model has;
+* CONV has no bias; FC has a bias stored after its [out][in] weights;
+  activations are NHWC, conv weights KRSC, FC input features are flattened
+  per input segment in (h, w, c) order and concatenated in input order;
+* no gradient w.r.t. the raw INPUT; concat-join gradients are split into
+  per-input planes; gradients arriving at a fork are summed;
+* max-pool is floor mode, no padding, first maximum wins ties;
+* LOSS = mean softmax cross-entropy; plain SGD w -= lr * dW.
+
+Only tests/, __graft_entry__.smoke() and bench.py's reference arm use this.
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Tuple
+
+import numpy as np
+import torch
+import torch.nn.functional as Fn
+
+INPUT, CONV, ACTV, POOL, FC, LOSS = range(6)
+
+
+class Layer:
+    def __init__(self, id, kind, inputs, params, shape):
+        self.id, self.kind, self.inputs, self.params, self.shape = id, kind, list(inputs), params, shape
+
+
+def layers_of(g) -> List[Layer]:
+    """From a paper_1602_08124_b200.NetworkGraph (finalized)."""
+    out = []
+    for l in g.layers():
+        s = g.shape(l.id)
+        out.append(Layer(l.id, int(l.kind), l.inputs, l.params, (s.n, s.c, s.h, s.w)))
+    return out
+
+
+def owner(L: List[Layer], i: int) -> int:
+    while L[i].kind == ACTV:
+        i = L[i].inputs[0]
+    return i
+
+
+def _nhwc(shape):
+    n, c, h, w = shape
+    return (n, h, w, c)
+
+
+def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np.ndarray, lr: float,
+               dtype=torch.float64) -> Tuple[float, Dict[int, np.ndarray], Dict[int, np.ndarray]]:
+    """Returns (loss, updated weights, weight gradients)."""
+    L = layers_of(g)
+    N = len(L)
+    buf: Dict[int, torch.Tensor] = {}
+    W = {k: torch.tensor(v, dtype=dtype) for k, v in weights.items()}
+    grads: Dict[int, torch.Tensor] = {}
+
+    def cat_in(l: Layer, flatten: bool = False):
+        parts = []
+        for q in l.inputs:
+            t = buf[owner(L, q)]
+            parts.append(t.reshape(t.shape[0], -1) if flatten else t)
+        return torch.cat(parts, dim=1 if flatten else 3)
+
+    def in_channels(l: Layer, flatten: bool = False):
+        cs = []
+        for q in l.inputs:
+            n, c, h, w = L[q].shape
+            cs.append(c * h * w if flatten else c)
+        return cs
+
+    # ---------------- forward
+    gscratch = None
+    loss = 0.0
+    for l in L:
+        if l.kind == INPUT:
+            buf[l.id] = torch.tensor(images, dtype=dtype).reshape(_nhwc(l.shape))
+        elif l.kind == CONV:
+            k, s, p, cout = l.params
+            x = cat_in(l).permute(0, 3, 1, 2)
+            cin = x.shape[1]
+            w = W[l.id].reshape(cout, k, k, cin).permute(0, 3, 1, 2)
+            buf[l.id] = Fn.conv2d(x, w, stride=s, padding=p).permute(0, 2, 3, 1).contiguous()
+        elif l.kind == ACTV:
+            o = owner(L, l.id)
+            buf[o] = torch.relu(buf[o])
+        elif l.kind == POOL:
+            k, s = l.params[0], l.params[1]
+            x = cat_in(l).permute(0, 3, 1, 2)
+            buf[l.id] = Fn.max_pool2d(x, k, s).permute(0, 2, 3, 1).contiguous()
+        elif l.kind == FC:
+            out = l.params[0]
+            x = cat_in(l, flatten=True)
+            fin = x.shape[1]
+            w = W[l.id][: out * fin].reshape(out, fin)
+            b = W[l.id][out * fin:]
+            buf[l.id] = (x @ w.t() + b).reshape(_nhwc(l.shape))
+        elif l.kind == LOSS:
+            z = buf[owner(L, l.inputs[0])].reshape(l.shape[0], -1)
+            lab = torch.tensor(labels, dtype=torch.long)
+            lse = torch.logsumexp(z, dim=1)
+            loss = float((lse - z[torch.arange(z.shape[0]), lab]).mean())
+            pr = torch.softmax(z, dim=1)
+            oh = torch.zeros_like(pr)
+            oh[torch.arange(z.shape[0]), lab] = 1.0
+            gscratch = (pr - oh) / z.shape[0]
+
+    # ---------------- backward
+    def produces(l: Layer) -> bool:
+        if l.kind in (ACTV, INPUT):
+            return False
+        return any(L[owner(L, q)].kind != INPUT for q in l.inputs)
+
+    planes: Dict[Tuple[int, int], torch.Tensor] = {}
+    merged: Dict[Tuple[int, int], Tuple[int, int]] = {}
+
+    def canon(key):
+        while key in merged:
+            key = merged[key]
+        return key
+
+    def readers_of(gid: int):
+        # grads_read: gradient buffers whose input chains pass through m
+        return gid
+
+    def incoming(m: int):
+        keys = []
+        for gid in range(N):
+            gl = L[gid]
+            if not produces(gl):
+                continue
+            for j, q in enumerate(gl.inputs):
+                if L[owner(L, q)].kind == INPUT:
+                    continue
+                cur = q
+                hit = False
+                while True:
+                    if cur == m:
+                        hit = True
+                        break
+                    if L[cur].kind != ACTV:
+                        break
+                    cur = L[cur].inputs[0]
+                if hit:
+                    c = canon((gid, j))
+                    if c not in keys:
+                        keys.append(c)
+        return keys
+
+    def set_planes(l: Layer, full: torch.Tensor, flatten: bool):
+        """Split a gradient w.r.t. the concatenated input into per-input planes."""
+        off = 0
+        cs = in_channels(l, flatten)
+        for j, q in enumerate(l.inputs):
+            c = cs[j]
+            if L[owner(L, q)].kind != INPUT:
+                part = full[:, off:off + c] if flatten else full[..., off:off + c]
+                planes[(l.id, j)] = part.reshape(_nhwc(L[q].shape)).contiguous()
+            off += c
+
+    for m in range(N - 1, -1, -1):
+        l = L[m]
+        if l.kind == INPUT:
+            continue
+        keys = incoming(m)
+        dy = None
+        if keys:
+            dy = planes[keys[0]]
+            if len(keys) > 1:
+                for k2 in keys[1:]:
+                    dy = dy + planes[k2]
+                    merged[k2] = keys[0]
+                planes[keys[0]] = dy
+        if l.kind == LOSS:
+            if produces(l):
+                planes[(m, 0)] = gscratch.reshape(_nhwc(L[l.inputs[0]].shape)).clone()
+        elif l.kind == ACTV:
+            y = buf[owner(L, m)]
+            planes[keys[0]] = torch.where(y > 0, dy, torch.zeros_like(dy))
+        elif l.kind == CONV:
+            k, s, p, cout = l.params
+            x = cat_in(l).permute(0, 3, 1, 2)
+            cin = x.shape[1]
+            w4 = W[m].reshape(cout, k, k, cin).permute(0, 3, 1, 2)
+            dyn = dy.permute(0, 3, 1, 2)
+            if produces(l):
+                dx = torch.nn.grad.conv2d_input(x.shape, w4, dyn, stride=s, padding=p)
+                set_planes(l, dx.permute(0, 2, 3, 1), False)
+            dw = torch.nn.grad.conv2d_weight(x, w4.shape, dyn, stride=s, padding=p)
+            gk = dw.permute(0, 2, 3, 1).reshape(-1)
+            grads[m] = gk
+            W[m] = W[m] - lr * gk
+        elif l.kind == FC:
+            out = l.params[0]
+            x = cat_in(l, flatten=True)
+            fin = x.shape[1]
+            w = W[m][: out * fin].reshape(out, fin)
+            d2 = dy.reshape(dy.shape[0], -1)
+            if produces(l):
+                set_planes(l, d2 @ w, True)
+            dw = d2.t() @ x
+            db = d2.sum(0)
+            gk = torch.cat([dw.reshape(-1), db])
+            grads[m] = gk
+            W[m] = W[m] - lr * gk
+        elif l.kind == POOL:
+            k, s = l.params[0], l.params[1]
+            x = cat_in(l).permute(0, 3, 1, 2).detach().requires_grad_(True)
+            y = Fn.max_pool2d(x, k, s)
+            y.backward(dy.permute(0, 3, 1, 2))
+            if produces(l):
+                set_planes(l, x.grad.permute(0, 2, 3, 1), False)
+    return loss, {k: v.numpy().astype(np.float32) for k, v in W.items()}, {k: v.numpy() for k, v in grads.items()}
+
+
+def he_weights(g, cost, seed: int = 5000) -> Dict[int, np.ndarray]:
+    """Host-side He-normal init (numpy), for tests that upload weights."""
+    rng = np.random.default_rng(seed)
+    out = {}
+    for l in layers_of(g):
+        if l.kind == CONV:
+            k, s, p, cout = l.params
+            cin = sum(layers_of(g)[q].shape[1] for q in l.inputs)
+            fan = k * k * cin
+            out[l.id] = (rng.standard_normal(cout * k * k * cin) * np.sqrt(2.0 / fan)).astype(np.float32)
+        elif l.kind == FC:
+            outf = l.params[0]
+            fin = sum(int(np.prod(layers_of(g)[q].shape[1:])) for q in l.inputs)
+            w = (rng.standard_normal(outf * fin) * np.sqrt(2.0 / fin)).astype(np.float32)
+            out[l.id] = np.concatenate([w, np.zeros(outf, np.float32)])
+    return out

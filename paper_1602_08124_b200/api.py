@@ -453,6 +453,11 @@ class _Owned:
             self.h = None
 
 
+class _Borrowed:
+    def __init__(self, h):
+        self.h = h
+
+
 def static_decision(kind: PolicyKind, mode: AlgoMode, g: NetworkGraph, cm: CostModel) -> PolicyDecision:
     h = C.c_void_p()
     c = cm._c()
@@ -493,8 +498,8 @@ class SimOptions:
 class RunReport:
     """sim_types.hpp:63-90; events are materialised lazily."""
 
-    def __init__(self, handle):
-        self._own = _Owned(handle, "vdnn_report_destroy")
+    def __init__(self, handle, owned: bool = True):
+        self._own = _Owned(handle, "vdnn_report_destroy") if owned else _Borrowed(handle)
         s = L.ReportSummary()
         _call("vdnn_report_summary_get", handle, C.byref(s))
         self.pass_ = bool(s.pass_)
@@ -706,3 +711,126 @@ def report_from_events(events, summary: Dict) -> RunReport:
     h = C.c_void_p()
     _call("vdnn_report_from_events", arr, C.c_size_t(n), C.byref(s), C.byref(h))
     return RunReport(h)
+
+
+# ---------------------------------------------------------------- session --
+class Session:
+    """B200 training session: replays the plan of (graph, decision, capacity)
+    on one device arena + pinned host arena with compute/memory streams.
+
+    There is no CPU fallback: creating a session needs a CUDA device and the
+    in-tree libvdnn.so; every failure raises.
+    """
+
+    def __init__(self, g: NetworkGraph, decision: PolicyDecision, cost: Optional[CostModel] = None,
+                 capacity: int = 12884901888, device: int = 0, weight_seed: int = 5000,
+                 external_grads: bool = False, record_timeline: bool = False):
+        self.graph = g
+        self.decision = decision
+        self.cost = cost or CostModel()
+        self.capacity = capacity
+        opt = L.SessionOptions()
+        L.lib().vdnn_session_options_default(C.byref(opt))
+        opt.device = device
+        opt.weight_seed = weight_seed
+        opt.external_grads = int(external_grads)
+        opt.record_timeline = int(record_timeline)
+        d = decision._handle(g)
+        c = self.cost._c()
+        h = C.c_void_p()
+        _call("vdnn_session_create", g.handle, d.h, C.byref(c), C.c_uint64(capacity), C.byref(opt), C.byref(h))
+        self._own = _Owned(h, "vdnn_session_destroy")
+        self.plan = RunReport(C.c_void_p(L.lib().vdnn_session_plan(h)), owned=False)
+        self._plan_keepalive = self._own
+        self.batch = g.batch
+        self._loss = C.c_float()
+
+    @property
+    def handle(self):
+        return self._own.h
+
+    def arena_info(self) -> Dict[str, int]:
+        a, lo, hb, sb = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _call("vdnn_session_arena_info", self.handle, C.byref(a), C.byref(lo), C.byref(hb), C.byref(sb))
+        return {"arena_bytes": a.value, "arena_base_offset": lo.value, "host_arena_bytes": hb.value,
+                "scratch_bytes": sb.value}
+
+    def set_batch(self, images, labels) -> None:
+        """Host arrays: images float32 NHWC [N,H,W,C] (C-contiguous), labels int32 [N]."""
+        import numpy as np
+        im = np.ascontiguousarray(images, dtype=np.float32)
+        lb = np.ascontiguousarray(labels, dtype=np.int32)
+        _call("vdnn_session_set_batch_host", self.handle, im.ctypes.data_as(C.c_void_p),
+              lb.ctypes.data_as(C.c_void_p))
+        self._keep = (im, lb)  # the copy is asynchronous: keep sources alive until the next call
+
+    def set_batch_ptr(self, images_ptr: int, labels_ptr: int, device: bool = False) -> None:
+        fn = "vdnn_session_set_batch_device" if device else "vdnn_session_set_batch_host"
+        _call(fn, self.handle, C.c_void_p(images_ptr), C.c_void_p(labels_ptr))
+
+    def synthetic_batch(self, seed: int = 1234) -> None:
+        _call("vdnn_session_synthetic_batch", self.handle, C.c_uint64(seed))
+
+    def step(self, lr: float = 0.01, want_loss: bool = True) -> Optional[float]:
+        if want_loss:
+            _call("vdnn_session_step", self.handle, C.c_float(lr), C.byref(self._loss))
+            return float(self._loss.value)
+        _call("vdnn_session_step", self.handle, C.c_float(lr), None)
+        return None
+
+    def synchronize(self) -> None:
+        _call("vdnn_session_synchronize", self.handle)
+
+    def weight_count(self, layer: int) -> int:
+        return self.cost.weight_bytes(self.graph, layer) // 4
+
+    def get_weights(self, layer: int):
+        import numpy as np
+        n = self.weight_count(layer)
+        out = np.empty(n, dtype=np.float32)
+        _call("vdnn_session_get_weights", self.handle, int(layer), out.ctypes.data_as(C.c_void_p), C.c_size_t(n))
+        return out
+
+    def set_weights(self, layer: int, values) -> None:
+        import numpy as np
+        v = np.ascontiguousarray(values, dtype=np.float32).ravel()
+        _call("vdnn_session_set_weights", self.handle, int(layer), v.ctypes.data_as(C.c_void_p),
+              C.c_size_t(v.size))
+
+    def read_feature(self, owner: int, count: int):
+        import numpy as np
+        out = np.empty(count, dtype=np.float32)
+        _call("vdnn_session_read_feature", self.handle, int(owner), out.ctypes.data_as(C.c_void_p),
+              C.c_size_t(count))
+        return out
+
+    def measured_report(self) -> RunReport:
+        h = C.c_void_p()
+        _call("vdnn_session_measured_report", self.handle, C.byref(h))
+        return RunReport(h)
+
+    def layer_times(self):
+        n = self.graph.size()
+        f = (C.c_double * n)()
+        b = (C.c_double * n)()
+        _call("vdnn_session_layer_times", self.handle, n, f, b)
+        return list(f), list(b)
+
+    def grad_arena(self) -> Tuple[int, int]:
+        p = C.c_void_p()
+        n = C.c_size_t()
+        _call("vdnn_session_grad_arena", self.handle, C.byref(p), C.byref(n))
+        return (p.value or 0), n.value
+
+    def apply_grads(self, lr: float, scale: float = 1.0) -> None:
+        _call("vdnn_session_apply_grads", self.handle, C.c_float(lr), C.c_float(scale))
+
+    @property
+    def stream(self) -> int:
+        p = C.c_void_p()
+        _call("vdnn_session_stream", self.handle, C.byref(p))
+        return p.value or 0
+
+
+def kernel_launch_count() -> int:
+    return int(L.lib().vdnn_kernel_launch_count())

@@ -1,0 +1,177 @@
+// extern "C" training-session entry points (the B200 executor).
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "../runtime/session.h"
+#include "capi_common.h"
+#include "handles.h"
+
+using vdnncapi::fail;
+
+struct vdnn_session {
+  vdnnrt::Session* s;
+  vdnn_report plan_view;
+};
+
+namespace {
+template <class F>
+vdnn_status guard(F&& f) {
+  try {
+    vdnncapi::clear_error();
+    return f();
+  } catch (const vdnnp::PlanError& e) {
+    const std::string msg = e.what();
+    if (msg.rfind("UNSUPPORTED", 0) == 0) return fail(VDNN_UNSUPPORTED, msg);
+    return fail(static_cast<vdnn_status>(static_cast<int>(e.code)), msg);
+  } catch (const std::bad_alloc&) {
+    return fail(VDNN_ERROR, "out of host memory");
+  } catch (const std::exception& e) {
+    return fail(VDNN_CUDA_ERROR, e.what());
+  }
+}
+vdnnrt::Session& S(vdnn_session* s) {
+  if (!s || !s->s) throw std::runtime_error("null session");
+  return *s->s;
+}
+}  // namespace
+
+extern "C" {
+
+void vdnn_session_options_default(vdnn_session_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->device = 0;
+  o->weight_seed = 5000;
+  o->external_grads = 0;
+  o->record_timeline = 0;
+  o->host_arena = 1;
+}
+
+vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, const vdnn_cost_model* cm,
+                                uint64_t capacity, const vdnn_session_options* opt, vdnn_session** out) {
+  return guard([&] {
+    if (!g || !d || !out) throw vdnnp::PlanError(vdnnp::Err::Generic, "null argument");
+    vdnnrt::Options o;
+    if (opt) {
+      o.device = opt->device;
+      o.weight_seed = opt->weight_seed;
+      o.external_grads = opt->external_grads != 0;
+      o.record_timeline = opt->record_timeline != 0;
+      o.host_arena = opt->host_arena != 0;
+    }
+    if (!g->net.finalized()) throw vdnnp::PlanError(vdnnp::Err::Generic, "graph is not finalized");
+    auto* s = new vdnnrt::Session(g->net, d->d, vdnncapi::cost_from(cm), capacity, o);
+    *out = new vdnn_session{s, vdnn_report{s->plan()}};
+    return VDNN_OK;
+  });
+}
+
+void vdnn_session_destroy(vdnn_session* s) {
+  if (!s) return;
+  delete s->s;
+  delete s;
+}
+
+const vdnn_report* vdnn_session_plan(const vdnn_session* s) { return s ? &s->plan_view : nullptr; }
+
+vdnn_status vdnn_session_arena_info(const vdnn_session* s, uint64_t* arena_bytes, uint64_t* lo, uint64_t* host_bytes,
+                                    uint64_t* scratch) {
+  return guard([&] {
+    const vdnnrt::Session& x = *s->s;
+    if (arena_bytes) *arena_bytes = x.arena_bytes();
+    if (lo) *lo = x.arena_lo();
+    if (host_bytes) *host_bytes = x.host_bytes();
+    if (scratch) *scratch = x.scratch_bytes();
+    return VDNN_OK;
+  });
+}
+
+vdnn_status vdnn_session_set_batch_host(vdnn_session* s, const float* images, const int32_t* labels) {
+  return guard([&] {
+    S(s).set_batch_host(images, labels);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_set_batch_device(vdnn_session* s, const float* images, const int32_t* labels) {
+  return guard([&] {
+    S(s).set_batch_device(images, labels);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_synthetic_batch(vdnn_session* s, uint64_t seed) {
+  return guard([&] {
+    S(s).synthetic_batch(seed);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_get_weights(vdnn_session* s, int32_t layer, float* host, size_t count) {
+  return guard([&] {
+    S(s).get_weights(layer, host, count);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_set_weights(vdnn_session* s, int32_t layer, const float* host, size_t count) {
+  return guard([&] {
+    S(s).set_weights(layer, host, count);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_step(vdnn_session* s, float lr, float* loss_host) {
+  return guard([&] {
+    S(s).step(lr, loss_host);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_synchronize(vdnn_session* s) {
+  return guard([&] {
+    S(s).synchronize();
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_read_feature(vdnn_session* s, int32_t owner, float* host, size_t count) {
+  return guard([&] {
+    S(s).read_feature(owner, host, count);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_measured_report(vdnn_session* s, vdnn_report** out) {
+  return guard([&] {
+    S(s).synchronize();
+    *out = new vdnn_report{S(s).measured_report()};
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_layer_times(vdnn_session* s, int32_t n, double* fwd_ms, double* bwd_ms) {
+  return guard([&] {
+    S(s).synchronize();
+    S(s).layer_times(n, fwd_ms, bwd_ms);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_grad_buffer(vdnn_session* s, int32_t layer, void** ptr, size_t* count) {
+  return guard([&] {
+    S(s).grad_buffer(layer, ptr, count);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_grad_arena(vdnn_session* s, void** ptr, size_t* count) {
+  return guard([&] {
+    S(s).grad_arena(ptr, count);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_apply_grads(vdnn_session* s, float lr, float scale) {
+  return guard([&] {
+    S(s).apply_grads(lr, scale);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_stream(vdnn_session* s, void** stream) {
+  return guard([&] {
+    *stream = S(s).stream();
+    return VDNN_OK;
+  });
+}
+
+}  // extern "C"

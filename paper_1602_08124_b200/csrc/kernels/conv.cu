@@ -41,7 +41,10 @@ bool build_common(const ConvArgs& a, ConvParams& p) {
   p.KK = a.kh * a.kw * cb;
   // virtual 32-channel chunks per segment
   int nch = 0;
-  if (vec) {
+  if (vec && a.nseg == 1) {
+    p.chunk_arith = 1;
+    nch = (cb + 31) / 32;
+  } else if (vec) {
     for (int i = 0; i < a.nseg && vec; ++i) {
       for (int c0 = 0; c0 < a.c[i]; c0 += 32) {
         if (nch >= kMaxChunks) {
@@ -49,10 +52,10 @@ bool build_common(const ConvArgs& a, ConvParams& p) {
           break;
         }
         Chunk& c = p.chunk[nch++];
-        c.seg = static_cast<int16_t>(i);
-        c.coff = static_cast<int16_t>(c0);
-        c.valid = static_cast<int16_t>(std::min(32, a.c[i] - c0));
-        c.cbase = static_cast<int16_t>(p.seg[i].cbase + c0);
+        c.seg = static_cast<int32_t>(i);
+        c.coff = static_cast<int32_t>(c0);
+        c.valid = static_cast<int32_t>(std::min(32, a.c[i] - c0));
+        c.cbase = static_cast<int32_t>(p.seg[i].cbase + c0);
       }
     }
   }

@@ -49,7 +49,7 @@ struct Seg {
 
 // A 32-wide "virtual channel chunk" of the concatenated input (vector mode).
 struct Chunk {
-  int16_t seg, coff, valid, cbase;
+  int32_t seg, coff, valid, cbase;
 };
 
 struct ConvParams {
@@ -60,6 +60,7 @@ struct ConvParams {
   int nseg;
   Seg seg[kMaxSegs];
   int nchunk;
+  int chunk_arith;            // single segment: chunk i = channels [32i, 32i+32) computed, not tabled
   Chunk chunk[kMaxChunks];
   int vec_in;                 // every segment C % 4 == 0: 16-B gathers over input channels
   int vec_out;                // Cout % 4 == 0
@@ -179,6 +180,19 @@ __device__ __forceinline__ uint32_t mnmaj_addr(uint32_t base, int k, int mc, int
   return base + mc * 4096 + k * 128 + (((((j >> 1) ^ (k & 3)) << 1) | (j & 1)) << 4);
 }
 
+__device__ __forceinline__ Chunk chunk_at(const ConvParams& p, int i) {
+  if (p.chunk_arith) {
+    Chunk c;
+    c.seg = 0;
+    c.coff = static_cast<int32_t>(i * 32);
+    const int v = p.C - i * 32;
+    c.valid = static_cast<int32_t>(v < 32 ? v : 32);
+    c.cbase = c.coff;
+    return c;
+  }
+  return p.chunk[i];
+}
+
 // ---------------------------------------------------------- gathers ------
 // Segment lookup for a flat channel index (scalar mode).
 __device__ __forceinline__ int seg_of(const ConvParams& p, int c) {
@@ -211,7 +225,7 @@ struct Gather {
     if (p.vec_in) {
       const int tap = kb / p.nchunk, ck = kb - tap * p.nchunk;
       const int r = tap / p.kw, s = tap - r * p.kw;
-      const Chunk c = p.chunk[ck];
+      const Chunk c = chunk_at(p, ck);
       const Seg sg = p.seg[c.seg];
       const int j = tid & 7;
       const bool jv = (j * 4) < c.valid;
@@ -380,7 +394,7 @@ struct Gather {
         const float* src = p.w;
         uint32_t bytes = 0;
         if (kv && vc < p.nchunk) {
-          const Chunk c = p.chunk[vc];
+          const Chunk c = chunk_at(p, vc);
           if (j * 4 < c.valid) {
             const int ftap = (p.kh - 1 - rr) * p.kw + (p.kw - 1 - ss);
             src = p.w + static_cast<int64_t>(co) * p.KK + ftap * p.C + c.cbase + j * 4;
@@ -442,7 +456,7 @@ struct Gather {
         uint32_t bytes = 0;
         if (pix < P && vcol < p.kh * p.kw * p.nchunk) {
           const int tap = vcol / p.nchunk, ck = vcol - tap * p.nchunk;
-          const Chunk c = p.chunk[ck];
+          const Chunk c = chunk_at(p, ck);
           if (j * 4 < c.valid) {
             const int r = tap / p.kw, s = tap - r * p.kw;
             const Pix x = decode_pix(pix, p.Ho, p.Wo);
@@ -525,7 +539,7 @@ __device__ __forceinline__ int wgrad_widx(const ConvParams& p, int m, bool& vali
       valid = false;
       return 0;
     }
-    const Chunk c = p.chunk[ck];
+    const Chunk c = chunk_at(p, ck);
     valid = lane < c.valid;
     return tap * p.C + c.cbase + lane;
   }
@@ -644,7 +658,7 @@ __global__ void __launch_bounds__(160, 1) tc_conv_kernel(const __grid_constant__
         if (p.vec_in) {
           const int vc = nb >> 5;
           if (vc >= p.nchunk) continue;
-          const Chunk c = p.chunk[vc];
+          const Chunk c = chunk_at(p, vc);
           const Seg sg = p.seg[c.seg];
           if (!sg.dx) continue;
           float* dst = sg.dx + static_cast<int64_t>(m) * sg.C + c.coff;

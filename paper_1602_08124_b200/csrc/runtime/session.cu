@@ -1,0 +1,847 @@
+// B200 executor for a vDNN plan.
+//
+// Layout:
+//   * one cudaMalloc'd device arena spanning the planned pool offsets
+//     [lo, hi); a buffer's pointer is base + its planned pool offset, so the
+//     arena enforces the HBM budget the planner was given and the offsets are
+//     byte-identical to the reference's (simulator.hpp:203-220);
+//   * one cudaHostAlloc'd pinned arena with a slot per offloaded feature
+//     buffer (HostLedger peak, memory_pool.hpp:225-256);
+//   * two streams: compute (FWD/BWD kernels) and memory (OFFLOAD D2H /
+//     PREFETCH H2D), gated by CUDA events exactly as the reference's sync
+//     rules (simulator.hpp:315-322 forward, :400-441 backward; PAPER.md
+//     Fig. 9): FWD(n+1) waits for layer n's offloads, BWD(m) waits for the
+//     prefetches it reads, and the next BWD waits for every prefetch launched
+//     during the current step. The memory stream waits for the compute
+//     stream's "step start" event so a transfer never touches an extent
+//     before every earlier user of it has finished.
+//   * non-pool scratch (documented in DESIGN.md): softmax gradient / loss,
+//     labels, split-K partials, and (data-parallel mode) the gradient arena.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <set>
+#include <stdexcept>
+
+#include "session.h"
+
+namespace vdnnrt {
+
+using namespace vdnnp;
+
+namespace {
+constexpr u64 kNoOff = ~u64{0};
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+}  // namespace
+
+void Session::check(cudaError_t e, const char* what) const {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, const Options& o)
+    : g_(g), d_(d), c_(c), cap_(capacity), o_(o) {
+  if (c_.elem != 4) throw PlanError(Err::Config, "the CUDA executor stores fp32 (elem_size 4)");
+  plan_ = vdnnp::plan(g_, d_, c_, cap_);
+  if (!plan_.pass) throw PlanError(Err::Generic, "plan does not fit the budget: " + plan_.verdict());
+  lv_ = analyze(g_, d_, c_);
+  L_ = g_.size();
+  for (const Node& l : g_.nodes()) {
+    if (l.join == Join::Elementwise && l.in.size() > 1)
+      throw PlanError(Err::Config, "UNSUPPORTED: elementwise joins are not implemented by the CUDA executor");
+    if (l.in.size() > static_cast<size_t>(vdnnk::kMaxConvSegs))
+      throw PlanError(Err::Config, "UNSUPPORTED: more than 8 inputs to one layer");
+    if (l.kind == Kind::Input) {
+      if (input_id_ >= 0) throw PlanError(Err::Config, "UNSUPPORTED: more than one INPUT layer");
+      input_id_ = l.id;
+    }
+    if (l.kind == Kind::Loss) {
+      if (loss_id_ >= 0) throw PlanError(Err::Config, "UNSUPPORTED: more than one LOSS layer");
+      loss_id_ = l.id;
+    }
+    if (l.kind == Kind::Conv && lv_.grad[static_cast<size_t>(l.id)] > 0 && l.s != 1)
+      throw PlanError(Err::Config, "UNSUPPORTED: data gradient of a strided conv that is not the first layer");
+  }
+  if (input_id_ < 0 || loss_id_ < 0) throw PlanError(Err::Config, "UNSUPPORTED: graph needs one INPUT and one LOSS");
+  logits_owner_ = g_.owner(g_.at(loss_id_).in[0]);
+  {
+    const Dims& ld = g_.dims(g_.at(loss_id_).in[0]);
+    classes_ = static_cast<int>(ld.c * ld.h * ld.w);
+  }
+
+  check(cudaSetDevice(o_.device), "cudaSetDevice");
+  check(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking), "stream");
+  check(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking), "stream");
+
+  // device arena over the planned offsets
+  u64 lo = ~u64{0}, hi = 0;
+  for (const Event& e : plan_.events) {
+    if (e.kind != Ev::Alloc) continue;
+    lo = std::min(lo, e.off);
+    hi = std::max(hi, e.off + round_up(e.bytes, kAlign));
+  }
+  if (hi <= lo) throw PlanError(Err::Generic, "empty plan");
+  arena_lo_ = lo;
+  arena_bytes_ = hi - lo;
+  check(cudaMalloc(&arena_, arena_bytes_), "cudaMalloc(device arena)");
+  base_ = arena_ - lo;
+
+  // pinned host arena: one slot per offloaded owner
+  host_slot_.assign(static_cast<size_t>(L_), kNoOff);
+  for (const Event& e : plan_.events)
+    if (e.kind == Ev::Offload && host_slot_[static_cast<size_t>(e.buffer)] == kNoOff) {
+      host_slot_[static_cast<size_t>(e.buffer)] = host_bytes_;
+      host_bytes_ += round_up(e.bytes, 4096);
+    }
+  if (host_bytes_ > 0) {
+    if (!o_.host_arena) throw PlanError(Err::Config, "plan offloads but the host arena is disabled");
+    check(cudaHostAlloc(&host_, host_bytes_, cudaHostAllocDefault), "cudaHostAlloc(host arena)");
+  }
+
+  // non-pool scratch
+  const u64 n = g_.batch();
+  check(cudaMalloc(&loss_grad_, n * static_cast<u64>(classes_) * 4), "cudaMalloc(loss grad)");
+  check(cudaMalloc(&row_loss_, n * 4), "cudaMalloc(row loss)");
+  check(cudaMalloc(&loss_, 4), "cudaMalloc(loss)");
+  check(cudaMalloc(&labels_, n * 4), "cudaMalloc(labels)");
+  check(cudaHostAlloc(&pinned_loss_, 4, cudaHostAllocDefault), "cudaHostAlloc(loss)");
+  scratch_bytes_ = n * static_cast<u64>(classes_) * 4 + n * 8 + 4;
+  check(cudaMemsetAsync(labels_, 0, n * 4, cs_), "memset labels");
+
+  build_program();
+
+  // split-K scratch: the largest wgrad partial buffer, capped at 256 MiB
+  size_t need = 0;
+  for (const BwdStep& s : bwd_) {
+    const Node& l = g_.at(s.layer);
+    if (l.kind != Kind::Conv && l.kind != Kind::Fc) continue;
+    need = std::max(need, vdnnk::conv_wgrad_ws_bytes(conv_args(s.layer, s.in_off, nullptr)));
+  }
+  splitk_bytes_ = std::min<size_t>(need, size_t{256} << 20);
+  if (splitk_bytes_ > 0) check(cudaMalloc(&splitk_, splitk_bytes_), "cudaMalloc(split-K)");
+  scratch_bytes_ += splitk_bytes_;
+
+  if (o_.external_grads) {
+    grad_off_.assign(static_cast<size_t>(L_), kNoOff);
+    for (int i = 0; i < L_; ++i) {
+      const u64 wb = lv_.wbytes[static_cast<size_t>(i)];
+      if (wb == 0) continue;
+      grad_off_[static_cast<size_t>(i)] = grads_count_;
+      grads_count_ += wb / 4;
+    }
+    check(cudaMalloc(&grads_, std::max<size_t>(grads_count_, 1) * 4), "cudaMalloc(grad arena)");
+    scratch_bytes_ += grads_count_ * 4;
+  }
+
+  // timing / gating events
+  const size_t nsteps = fwd_.size() + bwd_.size();
+  size_t nxfer = 0;
+  for (const auto& s : fwd_) nxfer += s.offloads.size();
+  for (const auto& s : bwd_) nxfer += s.prefetches.size();
+  step_ev_.resize(nsteps);
+  for (auto& e : step_ev_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  xfer_ev_.resize(std::max<size_t>(nxfer, 1));
+  for (auto& e : xfer_ev_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  if (o_.record_timeline) {
+    ev_.resize(2 * (nsteps + nxfer));
+    for (auto& e : ev_) check(cudaEventCreate(&e), "event");
+    t0_ev_.resize(nsteps);
+    for (auto& e : t0_ev_) check(cudaEventCreate(&e), "event");
+    check(cudaEventCreate(&ev_iter_), "event");
+  }
+  check(cudaEventCreateWithFlags(&ev_sync_, cudaEventDisableTiming), "event");
+
+  init_weights();
+  check(cudaStreamSynchronize(cs_), "init");
+}
+
+Session::~Session() {
+  if (cs_) cudaStreamSynchronize(cs_);
+  if (ms_) cudaStreamSynchronize(ms_);
+  for (auto e : ev_) cudaEventDestroy(e);
+  for (auto e : step_ev_) cudaEventDestroy(e);
+  for (auto e : t0_ev_) cudaEventDestroy(e);
+  for (auto e : xfer_ev_) cudaEventDestroy(e);
+  if (ev_iter_) cudaEventDestroy(ev_iter_);
+  if (ev_sync_) cudaEventDestroy(ev_sync_);
+  cudaFree(arena_);
+  if (host_) cudaFreeHost(host_);
+  cudaFree(loss_grad_);
+  cudaFree(row_loss_);
+  cudaFree(loss_);
+  cudaFree(labels_);
+  if (pinned_loss_) cudaFreeHost(pinned_loss_);
+  if (splitk_) cudaFree(splitk_);
+  if (grads_) cudaFree(grads_);
+  if (cs_) cudaStreamDestroy(cs_);
+  if (ms_) cudaStreamDestroy(ms_);
+}
+
+// ------------------------------------------------------------- program ----
+// Two-buffer (baseline) scheme: the plan provisions two network-max gradient
+// buffers (G2, simulator.hpp:259-264) and no per-layer dX. Assign every
+// producer's dX to one of them in backward order; a producer whose gradient
+// feeds the same fork as a live one accumulates into it (the fork sum).
+void Session::assign_two_buffer() {
+  std::vector<u64> g2;
+  for (const Event& e : plan_.events)
+    if (e.kind == Ev::Alloc && e.tag == "G2") g2.push_back(e.off);
+  g2_loc_.assign(static_cast<size_t>(L_), kNoOff);
+  g2_accum_.assign(static_cast<size_t>(L_), 0);
+  if (lv_.g2_bytes == 0) return;
+  if (g2.size() != 2) throw PlanError(Err::Generic, "two-buffer plan without two G2 buffers");
+  std::vector<int> left(static_cast<size_t>(L_), 0);
+  std::vector<int> slot_of(static_cast<size_t>(L_), -1);
+  std::vector<std::set<int>> occupants(2);
+  for (int m = L_ - 1; m >= 0; --m) {
+    const size_t i = static_cast<size_t>(m);
+    if (g_.at(m).kind == Kind::Input) continue;
+    if (lv_.grad[i] > 0) {
+      // fork accumulation: a live single-plane gradient w.r.t. the same tensor
+      const Node& l = g_.at(m);
+      int merge = -1;
+      std::vector<int> planes;
+      for (int q : l.in)
+        if (g_.at(g_.owner(q)).kind != Kind::Input) planes.push_back(q);
+      if (planes.size() == 1) {
+        for (int s = 0; s < 2 && merge < 0; ++s)
+          for (int p : occupants[static_cast<size_t>(s)]) {
+            const Node& pl = g_.at(p);
+            std::vector<int> pp;
+            for (int q : pl.in)
+              if (g_.at(g_.owner(q)).kind != Kind::Input) pp.push_back(q);
+            if (pp.size() == 1 && pp[0] == planes[0]) {
+              merge = p;
+              break;
+            }
+          }
+      }
+      if (merge >= 0) {
+        g2_loc_[i] = g2_loc_[static_cast<size_t>(merge)];
+        g2_accum_[i] = 1;
+        slot_of[i] = slot_of[static_cast<size_t>(merge)];
+      } else {
+        int s = occupants[0].empty() ? 0 : (occupants[1].empty() ? 1 : -1);
+        if (s < 0)
+          throw PlanError(Err::Config,
+                          "UNSUPPORTED: two-buffer gradient reuse needs more than two live gradient maps at layer " +
+                              std::to_string(m));
+        g2_loc_[i] = g2[static_cast<size_t>(s)];
+        slot_of[i] = s;
+      }
+      occupants[static_cast<size_t>(slot_of[i])].insert(m);
+      left[i] = static_cast<int>(lv_.grad_users[i].size());
+    }
+    // m's BWD consumed its dY: retire gradients whose readers are all done
+    for (int gb : lv_.grads_read[i]) {
+      const size_t gi = static_cast<size_t>(gb);
+      if (--left[gi] == 0) occupants[static_cast<size_t>(slot_of[gi])].erase(gb);
+    }
+    if (lv_.grad[i] > 0 && lv_.grad_users[i].empty()) occupants[static_cast<size_t>(slot_of[i])].erase(m);
+  }
+}
+
+void Session::build_program() {
+  const bool two = d_.scheme == Scheme::TwoBuffer;
+  if (two) assign_two_buffer();
+  std::vector<u64> feat(static_cast<size_t>(L_), kNoOff), grad(static_cast<size_t>(L_), kNoOff),
+      ws(static_cast<size_t>(L_), kNoOff);
+  u64 ws2 = kNoOff;
+  w_off_.assign(static_cast<size_t>(L_), kNoOff);
+  std::map<u64, u64> merged;  // fold map: plane location -> canonical location
+  auto canon = [&](u64 loc) {
+    while (merged.count(loc)) loc = merged[loc];
+    return loc;
+  };
+  // plane offset (bytes) of input j inside producer g's dX buffer
+  auto plane_rel = [&](int gprod, int j) -> u64 {
+    const Node& l = g_.at(gprod);
+    u64 off = 0;
+    for (int k = 0; k < j; ++k) {
+      const int q = l.in[static_cast<size_t>(k)];
+      if (g_.at(g_.owner(q)).kind == Kind::Input) continue;
+      off += c_.bytes_of(g_.dims(q));
+    }
+    return off;
+  };
+  auto grad_base = [&](int gprod) -> u64 { return two ? g2_loc_[static_cast<size_t>(gprod)] : grad[static_cast<size_t>(gprod)]; };
+
+  std::vector<Transfer> pending;  // prefetches since the last BWD
+  int xfer = 0, step = 0;
+  bool in_fwd = true;
+  for (const Event& e : plan_.events) {
+    const size_t b = e.buffer >= 0 ? static_cast<size_t>(e.buffer) : 0;
+    switch (e.kind) {
+      case Ev::Alloc:
+        if (e.tag == "X" || e.tag == "Y") {
+          feat[b] = e.off;
+          if (e.buffer == input_id_ && e.layer == input_id_ && x_off_ == 0 && in_fwd) x_off_ = e.off;
+        } else if (e.tag == "dX") {
+          grad[b] = e.off;
+        } else if (e.tag == "W") {
+          w_off_[b] = e.off;
+        } else if (e.tag == "WS") {
+          if (e.buffer < 0) ws2 = e.off;
+          else ws[b] = e.off;
+        }
+        break;
+      case Ev::Fwd: {
+        FwdStep s;
+        s.layer = e.layer;
+        const Node& l = g_.at(e.layer);
+        for (int q : l.in) s.in_off.push_back(feat[static_cast<size_t>(g_.owner(q))]);
+        if (l.kind == Kind::Actv)
+          s.out_off = feat[static_cast<size_t>(g_.owner(e.layer))];
+        else if (l.kind != Kind::Loss)
+          s.out_off = feat[static_cast<size_t>(e.layer)];
+        s.w_off = w_off_[static_cast<size_t>(e.layer)];
+        const u64 wsb = lv_.wsbytes[static_cast<size_t>(e.layer)];
+        if (wsb > 0) {
+          s.ws_off = two ? ws2 : ws[static_cast<size_t>(e.layer)];
+          s.ws_bytes = wsb;
+        }
+        s.ev = step++;
+        fwd_.push_back(s);
+        break;
+      }
+      case Ev::Offload: {
+        Transfer t;
+        t.owner = e.buffer;
+        t.bytes = e.bytes;
+        t.dev_off = feat[b];
+        t.host_off = host_slot_[b];
+        t.ev = xfer++;
+        fwd_.back().offloads.push_back(t);
+        break;
+      }
+      case Ev::Prefetch: {
+        in_fwd = false;
+        Transfer t;
+        t.owner = e.buffer;
+        t.bytes = e.bytes;
+        t.dev_off = feat[b];  // the ALLOC logged just before on the memory stream
+        t.host_off = host_slot_[b];
+        t.ev = xfer++;
+        pending.push_back(t);
+        break;
+      }
+      case Ev::Bwd: {
+        in_fwd = false;
+        BwdStep s;
+        s.layer = e.layer;
+        const int m = e.layer;
+        const size_t mi = static_cast<size_t>(m);
+        const Node& l = g_.at(m);
+        s.prefetches = pending;
+        pending.clear();
+        for (const Transfer& t : s.prefetches)
+          if (std::find(lv_.bwd_reads[mi].begin(), lv_.bwd_reads[mi].end(), t.owner) != lv_.bwd_reads[mi].end())
+            s.wait_prefetch.push_back(t.ev);
+        for (int q : l.in) s.in_off.push_back(feat[static_cast<size_t>(g_.owner(q))]);
+        if (l.kind == Kind::Actv)
+          s.out_off = feat[static_cast<size_t>(g_.owner(m))];
+        else if (l.kind == Kind::Pool)
+          s.out_off = feat[mi];
+        s.w_off = w_off_[mi];
+        const u64 wsb = lv_.wsbytes[mi];
+        if (wsb > 0) {
+          s.ws_off = two ? ws2 : ws[mi];
+          s.ws_bytes = wsb;
+        }
+        if (lv_.grad[mi] > 0) {
+          const u64 base = grad_base(m);
+          for (size_t j = 0; j < l.in.size(); ++j) {
+            const int q = l.in[j];
+            if (g_.at(g_.owner(q)).kind == Kind::Input)
+              s.plane_off.push_back(kNoOff);
+            else
+              s.plane_off.push_back(base + plane_rel(m, static_cast<int>(j)));
+          }
+          if (two) s.accumulate = g2_accum_[mi] != 0;
+        }
+        // incoming gradient planes: for each gradient buffer m reads, the
+        // planes whose input chain passes through m
+        std::vector<u64> dy;
+        for (int gb : lv_.grads_read[mi]) {
+          const Node& gl = g_.at(gb);
+          for (size_t j = 0; j < gl.in.size(); ++j) {
+            int cur = gl.in[j];
+            bool hit = false;
+            while (true) {
+              if (cur == m) {
+                hit = true;
+                break;
+              }
+              if (g_.at(cur).kind != Kind::Actv) break;
+              cur = g_.at(cur).in[0];
+            }
+            if (!hit) continue;
+            const u64 loc = canon(grad_base(gb) + plane_rel(gb, static_cast<int>(j)));
+            if (std::find(dy.begin(), dy.end(), loc) == dy.end()) dy.push_back(loc);
+          }
+        }
+        for (size_t k = 1; k < dy.size(); ++k) merged[dy[k]] = dy[0];  // this step folds them
+        s.dy_off = dy;
+        s.ev = step++;
+        bwd_.push_back(s);
+        break;
+      }
+      default:
+        break;
+    }
+  }
+  if (x_off_ == 0) x_off_ = feat[static_cast<size_t>(input_id_)];
+  // the setup allocation of the INPUT layer (first ALLOC X of buffer input_id_)
+  for (const Event& e : plan_.events)
+    if (e.kind == Ev::Alloc && e.buffer == input_id_ && (e.tag == "X" || e.tag == "Y")) {
+      x_off_ = e.off;
+      break;
+    }
+}
+
+// ------------------------------------------------------------- helpers ----
+vdnnk::ConvArgs Session::conv_args(int layer, const std::vector<u64>& in_off,
+                                   const std::vector<u64>* planes) const {
+  const Node& l = g_.at(layer);
+  vdnnk::ConvArgs a;
+  a.nseg = static_cast<int>(l.in.size());
+  const Dims& first = g_.dims(l.in[0]);
+  a.n = static_cast<int>(first.n);
+  const bool fc = l.kind == Kind::Fc;
+  a.h = fc ? 1 : static_cast<int>(first.h);
+  a.w = fc ? 1 : static_cast<int>(first.w);
+  for (int i = 0; i < a.nseg; ++i) {
+    const Dims& d = g_.dims(l.in[static_cast<size_t>(i)]);
+    a.c[i] = static_cast<int>(fc ? d.c * d.h * d.w : d.c);
+    a.x[i] = F(in_off[static_cast<size_t>(i)]);
+    a.dx[i] = nullptr;
+    if (planes && (*planes)[static_cast<size_t>(i)] != kNoOff) a.dx[i] = F((*planes)[static_cast<size_t>(i)]);
+  }
+  a.cout = static_cast<int>(l.out);
+  if (fc) {
+    a.kh = a.kw = 1;
+    a.stride = 1;
+    a.pad = 0;
+  } else {
+    a.kh = a.kw = static_cast<int>(l.k);
+    a.stride = static_cast<int>(l.s);
+    a.pad = static_cast<int>(l.p);
+  }
+  return a;
+}
+
+void Session::init_weights() {
+  for (const Node& l : g_.nodes()) {
+    const size_t i = static_cast<size_t>(l.id);
+    if (lv_.wbytes[i] == 0) continue;
+    float* w = F(w_off_[i]);
+    const u64 seed = o_.weight_seed + static_cast<u64>(l.id);
+    if (l.kind == Kind::Conv) {
+      const u64 fan = l.k * l.k * g_.in_dims(l.id).c;
+      check(vdnnk::fill_normal(w, lv_.wbytes[i] / 4, std::sqrt(2.0f / static_cast<float>(fan)), seed, cs_), "init");
+    } else {
+      const u64 in = g_.fc_inputs(l.id);
+      check(vdnnk::fill_normal(w, in * l.out, std::sqrt(2.0f / static_cast<float>(in)), seed, cs_), "init");
+      check(vdnnk::fill_const(w + in * l.out, l.out, 0.0f, cs_), "init");
+    }
+  }
+}
+
+// ------------------------------------------------------------- execution --
+void Session::run_fwd(const FwdStep& s, float lr) {
+  (void)lr;
+  const Node& l = g_.at(s.layer);
+  cudaEvent_t start = step_ev_[static_cast<size_t>(s.ev)];
+  check(cudaEventRecord(start, cs_), "record");
+  if (timed_) check(cudaEventRecord(t0_ev_[static_cast<size_t>(s.ev)], cs_), "record");
+  if (!s.offloads.empty()) {
+    // the offloaded inputs are complete once every earlier compute op is: gate on the step start
+    check(cudaStreamWaitEvent(ms_, start, 0), "wait");
+    for (const Transfer& t : s.offloads) {
+      if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev)], ms_), "record");
+      check(cudaMemcpyAsync(host_ + t.host_off, base_ + t.dev_off, t.bytes, cudaMemcpyDeviceToHost, ms_), "D2H");
+      if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev) + 1], ms_), "record");
+      check(cudaEventRecord(xfer_ev_[static_cast<size_t>(t.ev)], ms_), "record");
+    }
+  }
+  if (timed_) check(cudaEventRecord(ev_[2 * s.ev], cs_), "record");
+  switch (l.kind) {
+    case Kind::Conv:
+    case Kind::Fc: {
+      const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
+      const float* bias = l.kind == Kind::Fc ? F(s.w_off) + g_.fc_inputs(s.layer) * l.out : nullptr;
+      check(vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_), "conv_fprop");
+      break;
+    }
+    case Kind::Actv:
+      check(vdnnk::relu_fwd(F(s.out_off), g_.dims(s.layer).count(), cs_), "relu_fwd");
+      break;
+    case Kind::Pool: {
+      vdnnk::PoolArgs p;
+      const Dims& first = g_.dims(l.in[0]);
+      p.n = static_cast<int>(first.n);
+      p.h = static_cast<int>(first.h);
+      p.w = static_cast<int>(first.w);
+      p.window = static_cast<int>(l.k);
+      p.stride = static_cast<int>(l.s);
+      p.nseg = static_cast<int>(l.in.size());
+      for (int i = 0; i < p.nseg; ++i) {
+        p.x[i] = F(s.in_off[static_cast<size_t>(i)]);
+        p.c[i] = static_cast<int>(g_.dims(l.in[static_cast<size_t>(i)]).c);
+      }
+      check(vdnnk::maxpool_fwd(p, F(s.out_off), cs_), "maxpool_fwd");
+      break;
+    }
+    case Kind::Loss:
+      check(vdnnk::softmax_xent_fwd(F(s.in_off[0]), labels_, static_cast<int>(g_.batch()), classes_, loss_grad_,
+                                    row_loss_, loss_, cs_),
+            "softmax_xent");
+      break;
+    default:
+      break;
+  }
+  if (timed_) check(cudaEventRecord(ev_[2 * s.ev + 1], cs_), "record");
+  if (!s.offloads.empty())  // sync rule: FWD(n+1) may not start before n's offloads drain
+    check(cudaStreamWaitEvent(cs_, xfer_ev_[static_cast<size_t>(s.offloads.back().ev)], 0), "wait");
+}
+
+void Session::run_bwd(const BwdStep& s, float lr) {
+  const Node& l = g_.at(s.layer);
+  const size_t mi = static_cast<size_t>(s.layer);
+  cudaEvent_t start = step_ev_[static_cast<size_t>(s.ev)];
+  check(cudaEventRecord(start, cs_), "record");
+  if (timed_) check(cudaEventRecord(t0_ev_[static_cast<size_t>(s.ev)], cs_), "record");
+  if (!s.prefetches.empty()) {
+    check(cudaStreamWaitEvent(ms_, start, 0), "wait");
+    for (const Transfer& t : s.prefetches) {
+      if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev)], ms_), "record");
+      check(cudaMemcpyAsync(base_ + t.dev_off, host_ + t.host_off, t.bytes, cudaMemcpyHostToDevice, ms_), "H2D");
+      if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev) + 1], ms_), "record");
+      check(cudaEventRecord(xfer_ev_[static_cast<size_t>(t.ev)], ms_), "record");
+    }
+  }
+  for (int ev : s.wait_prefetch) check(cudaStreamWaitEvent(cs_, xfer_ev_[static_cast<size_t>(ev)], 0), "wait");
+  if (timed_) check(cudaEventRecord(ev_[2 * s.ev], cs_), "record");
+
+  float* dy = s.dy_off.empty() ? nullptr : F(s.dy_off[0]);
+  std::vector<const float*> extra;
+  for (size_t k = 1; k < s.dy_off.size(); ++k) extra.push_back(F(s.dy_off[k]));
+  if (l.kind != Kind::Actv && !extra.empty())
+    check(vdnnk::add_into(dy, extra.data(), static_cast<int>(extra.size()), g_.dims(s.layer).count(), cs_), "fold");
+
+  switch (l.kind) {
+    case Kind::Conv:
+    case Kind::Fc: {
+      const bool fc = l.kind == Kind::Fc;
+      if (!s.plane_off.empty()) {
+        const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off);
+        check(vdnnk::conv_dgrad(a, F(s.w_off), dy, s.accumulate, cs_), "conv_dgrad");
+      }
+      const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
+      // split-K partials live in a fixed non-pool scratch so the reduction
+      // order (and hence every bit of the update) is independent of the
+      // offload policy and of the algorithm's workspace extent
+      float* dw = grads_ ? grads_ + grad_off_[mi] : nullptr;
+      check(vdnnk::conv_wgrad(a, dy, F(s.w_off), lr, dw, splitk_, splitk_bytes_, cs_), "conv_wgrad");
+      if (fc) {
+        const u64 in = g_.fc_inputs(s.layer);
+        float* bias = F(s.w_off) + in * l.out;
+        float* db = grads_ ? grads_ + grad_off_[mi] + in * l.out : nullptr;
+        check(vdnnk::bias_grad(dy, static_cast<int>(g_.batch()), static_cast<int>(l.out), bias, lr, db, cs_),
+              "bias_grad");
+      }
+      break;
+    }
+    case Kind::Pool: {
+      vdnnk::PoolArgs p;
+      const Dims& first = g_.dims(l.in[0]);
+      p.n = static_cast<int>(first.n);
+      p.h = static_cast<int>(first.h);
+      p.w = static_cast<int>(first.w);
+      p.window = static_cast<int>(l.k);
+      p.stride = static_cast<int>(l.s);
+      p.nseg = static_cast<int>(l.in.size());
+      for (int i = 0; i < p.nseg; ++i) {
+        p.x[i] = F(s.in_off[static_cast<size_t>(i)]);
+        p.c[i] = static_cast<int>(g_.dims(l.in[static_cast<size_t>(i)]).c);
+        p.dx[i] = s.plane_off.empty() || s.plane_off[static_cast<size_t>(i)] == kNoOff
+                      ? nullptr
+                      : F(s.plane_off[static_cast<size_t>(i)]);
+      }
+      if (!s.plane_off.empty()) check(vdnnk::maxpool_bwd(p, F(s.out_off), dy, cs_), "maxpool_bwd");
+      break;
+    }
+    case Kind::Actv:
+      if (dy)
+        check(vdnnk::relu_bwd(dy, extra.data(), static_cast<int>(extra.size()), F(s.out_off),
+                              g_.dims(s.layer).count(), cs_),
+              "relu_bwd");
+      break;
+    case Kind::Loss:
+      if (!s.plane_off.empty() && s.plane_off[0] != kNoOff)
+        check(cudaMemcpyAsync(F(s.plane_off[0]), loss_grad_, g_.batch() * static_cast<u64>(classes_) * 4,
+                              cudaMemcpyDeviceToDevice, cs_),
+              "loss grad copy");
+      break;
+    default:
+      break;
+  }
+  if (timed_) check(cudaEventRecord(ev_[2 * s.ev + 1], cs_), "record");
+  if (!s.prefetches.empty())  // prefetches launched here land before the next BWD
+    check(cudaStreamWaitEvent(cs_, xfer_ev_[static_cast<size_t>(s.prefetches.back().ev)], 0), "wait");
+}
+
+void Session::step(float lr, float* loss_host) {
+  timed_ = o_.record_timeline;
+  if (timed_) check(cudaEventRecord(ev_iter_, cs_), "record");
+  // the memory stream never runs ahead into a new iteration
+  check(cudaEventRecord(ev_sync_, cs_), "record");
+  check(cudaStreamWaitEvent(ms_, ev_sync_, 0), "wait");
+  for (const FwdStep& s : fwd_) run_fwd(s, lr);
+  for (const BwdStep& s : bwd_) run_bwd(s, lr);
+  if (loss_host) {
+    check(cudaMemcpyAsync(pinned_loss_, loss_, 4, cudaMemcpyDeviceToHost, cs_), "loss D2H");
+    check(cudaStreamSynchronize(cs_), "sync");
+    *loss_host = *pinned_loss_;
+  }
+}
+
+void Session::synchronize() {
+  check(cudaStreamSynchronize(ms_), "sync");
+  check(cudaStreamSynchronize(cs_), "sync");
+}
+
+void Session::set_batch_host(const float* images, const int32_t* labels) {
+  const u64 bytes = lv_.feat[static_cast<size_t>(input_id_)];
+  if (images) check(cudaMemcpyAsync(F(x_off_), images, bytes, cudaMemcpyHostToDevice, cs_), "images H2D");
+  if (labels) check(cudaMemcpyAsync(labels_, labels, g_.batch() * 4, cudaMemcpyHostToDevice, cs_), "labels H2D");
+}
+
+void Session::set_batch_device(const float* images, const int32_t* labels) {
+  const u64 bytes = lv_.feat[static_cast<size_t>(input_id_)];
+  if (images) check(cudaMemcpyAsync(F(x_off_), images, bytes, cudaMemcpyDeviceToDevice, cs_), "images D2D");
+  if (labels) check(cudaMemcpyAsync(labels_, labels, g_.batch() * 4, cudaMemcpyDeviceToDevice, cs_), "labels D2D");
+}
+
+void Session::synthetic_batch(u64 seed) {
+  const u64 count = lv_.feat[static_cast<size_t>(input_id_)] / 4;
+  check(vdnnk::fill_uniform(F(x_off_), count, -1.0f, 1.0f, seed, cs_), "images");
+  check(vdnnk::fill_labels(labels_, g_.batch(), classes_, seed + 1, cs_), "labels");
+}
+
+void Session::get_weights(int layer, float* host, size_t count) {
+  if (layer < 0 || layer >= L_ || w_off_[static_cast<size_t>(layer)] == kNoOff)
+    throw PlanError(Err::Generic, "layer has no weights");
+  if (count * 4 != lv_.wbytes[static_cast<size_t>(layer)]) throw PlanError(Err::Generic, "weight count mismatch");
+  synchronize();
+  check(cudaMemcpy(host, F(w_off_[static_cast<size_t>(layer)]), count * 4, cudaMemcpyDeviceToHost), "D2H");
+}
+
+void Session::set_weights(int layer, const float* host, size_t count) {
+  if (layer < 0 || layer >= L_ || w_off_[static_cast<size_t>(layer)] == kNoOff)
+    throw PlanError(Err::Generic, "layer has no weights");
+  if (count * 4 != lv_.wbytes[static_cast<size_t>(layer)]) throw PlanError(Err::Generic, "weight count mismatch");
+  synchronize();
+  check(cudaMemcpy(F(w_off_[static_cast<size_t>(layer)]), host, count * 4, cudaMemcpyHostToDevice), "H2D");
+}
+
+void Session::read_feature(int owner, float* host, size_t count) {
+  // valid only for buffers still device-resident at the end of the step
+  // (e.g. the INPUT extent or any buffer in the baseline scheme)
+  synchronize();
+  u64 off = kNoOff;
+  for (const Event& e : plan_.events)
+    if (e.kind == Ev::Alloc && e.buffer == owner && (e.tag == "X" || e.tag == "Y")) off = e.off;
+  if (off == kNoOff) throw PlanError(Err::Generic, "owner has no feature buffer");
+  if (count * 4 > lv_.feat[static_cast<size_t>(owner)]) throw PlanError(Err::Generic, "count too large");
+  check(cudaMemcpy(host, F(off), count * 4, cudaMemcpyDeviceToHost), "D2H");
+}
+
+void Session::grad_buffer(int layer, void** ptr, size_t* count) {
+  if (!grads_ || layer < 0 || layer >= L_ || grad_off_[static_cast<size_t>(layer)] == kNoOff) {
+    *ptr = nullptr;
+    *count = 0;
+    return;
+  }
+  *ptr = grads_ + grad_off_[static_cast<size_t>(layer)];
+  *count = lv_.wbytes[static_cast<size_t>(layer)] / 4;
+}
+
+void Session::grad_arena(void** ptr, size_t* count) {
+  *ptr = grads_;
+  *count = grads_count_;
+}
+
+void Session::apply_grads(float lr, float scale) {
+  if (!grads_) throw PlanError(Err::Generic, "session was created without external_grads");
+  for (int i = 0; i < L_; ++i) {
+    const size_t k = static_cast<size_t>(i);
+    if (grad_off_[k] == kNoOff) continue;
+    check(vdnnk::sgd_update(F(w_off_[k]), grads_ + grad_off_[k], lr * scale, lv_.wbytes[k] / 4, cs_), "sgd");
+  }
+}
+
+// ------------------------------------------------------ measured report ----
+// Re-times the plan's event log with the CUDA-event measurements of the last
+// step. Per step: T0 = compute stream reaches the step (after the previous
+// step's sync waits), KS/KE = kernel group start/end, XS/XE = transfer
+// start/end. The non-timed rows take the simulator's anchors
+// (simulator.hpp:279-350 forward, :364-468 backward, :513-545 cleanup) on
+// these measured times, so the result can be replay-checked like a plan.
+vdnnp::Report Session::measured_report() const {
+  if (ev_.empty()) throw PlanError(Err::Generic, "session was created without record_timeline");
+  auto ns = [&](cudaEvent_t e) -> i64 {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ev_iter_, e) != cudaSuccess) return 0;
+    return std::max<i64>(0, static_cast<i64>(std::llround(static_cast<double>(ms) * 1e6)));
+  };
+  const size_t nst = fwd_.size() + bwd_.size();
+  const size_t nx = ev_.size() / 2 - nst;
+  std::vector<i64> t0(nst), ks(nst), ke(nst), xs(nx), xe(nx);
+  for (size_t i = 0; i < nst; ++i) {
+    t0[i] = ns(t0_ev_[i]);
+    ks[i] = std::max(t0[i], ns(ev_[2 * i]));
+    ke[i] = std::max(ks[i], ns(ev_[2 * i + 1]));
+  }
+  for (size_t i = 0; i < nx; ++i) {
+    xs[i] = ns(ev_[2 * (nst + i)]);
+    xe[i] = std::max(xs[i], ns(ev_[2 * (nst + i) + 1]));
+  }
+  vdnnp::Report r;
+  r.pass = true;
+  size_t fi = 0, bi = 0;
+  size_t xi = 0;
+  int cur = -1;          // step index of the current FWD/BWD group
+  bool bwd = false;
+  i64 last_x_end = 0, horizon = 0;
+  std::map<int, i64> off_end;
+  // the step an event belongs to is the next FWD/BWD row at or after it for
+  // ALLOC/PREFETCH (they precede their kernel), the last one for the rest
+  auto next_step = [&]() -> int {
+    if (!bwd && fi < fwd_.size()) return fwd_[fi].ev;
+    if (bi < bwd_.size()) return bwd_[bi].ev;
+    return cur;
+  };
+  for (size_t k = 0; k < plan_.events.size(); ++k) {
+    const Event& pe = plan_.events[k];
+    Event e = pe;
+    if (!bwd && pe.kind == Ev::Prefetch) bwd = true;
+    if (!bwd && pe.kind == Ev::Bwd) bwd = true;
+    if (!bwd && pe.kind == Ev::Alloc && pe.lane == Lane::Memory) bwd = true;
+    switch (pe.kind) {
+      case Ev::Fwd:
+        cur = fwd_[fi++].ev;
+        e.t0 = ks[static_cast<size_t>(cur)];
+        e.t1 = ke[static_cast<size_t>(cur)];
+        last_x_end = 0;
+        break;
+      case Ev::Bwd:
+        cur = bwd_[bi++].ev;
+        e.t0 = ks[static_cast<size_t>(cur)];
+        e.t1 = ke[static_cast<size_t>(cur)];
+        break;
+      case Ev::Offload:
+      case Ev::Prefetch:
+        e.t0 = xs[xi];
+        e.t1 = xe[xi];
+        ++xi;
+        last_x_end = e.t1;
+        if (pe.kind == Ev::Offload) off_end[pe.buffer] = e.t1;
+        break;
+      case Ev::Alloc: {
+        if (pe.t0 == 0 && fi == 0 && !bwd) {
+          e.t0 = e.t1 = 0;  // setup
+        } else {
+          const int st = next_step();
+          // forward / prefetch allocations at the step's T0; backward dX/WS/dW at kernel start
+          const bool at_ready = bwd && pe.lane == Lane::Compute;
+          e.t0 = e.t1 = at_ready ? ks[static_cast<size_t>(st)] : t0[static_cast<size_t>(st)];
+        }
+        break;
+      }
+      case Ev::Release: {
+        if (pe.layer < 0) {
+          e.t0 = e.t1 = horizon;  // cleanup
+        } else if (pe.lane == Lane::Memory) {
+          const i64 oe = off_end.count(pe.buffer) ? off_end[pe.buffer] : 0;
+          e.t0 = e.t1 = std::max(ke[static_cast<size_t>(cur)], oe);
+        } else {
+          e.t0 = e.t1 = ke[static_cast<size_t>(cur)];
+        }
+        break;
+      }
+      case Ev::Sync: {
+        const bool pre_kernel = k + 1 < plan_.events.size() &&
+                                (plan_.events[k + 1].kind == Ev::Alloc || plan_.events[k + 1].kind == Ev::Bwd) &&
+                                bwd && (bi < bwd_.size() && pe.layer == bwd_[bi].layer);
+        if (pre_kernel) {
+          const int st = bwd_[bi].ev;
+          e.t0 = t0[static_cast<size_t>(st)];
+          e.t1 = ks[static_cast<size_t>(st)];
+          r.stall_bwd += e.t1 - e.t0;
+        } else {
+          e.t0 = ke[static_cast<size_t>(cur)];
+          e.t1 = std::max(e.t0, last_x_end);
+          (bwd ? r.stall_bwd : r.stall_fwd) += e.t1 - e.t0;
+        }
+        break;
+      }
+    }
+    if (pe.kind != Ev::Release || pe.layer >= 0) horizon = std::max(horizon, e.t1);
+    r.events.push_back(e);
+  }
+  r.total = horizon;
+  // pool high water / time-weighted average reconstructed from the re-timed log
+  u64 live = 0, peak = 0;
+  vdnnp::u128 area = 0;
+  i64 last = 0;
+  for (const Event& e : r.events) {
+    if (e.kind != Ev::Alloc && e.kind != Ev::Release) continue;
+    area += static_cast<vdnnp::u128>(live) * static_cast<vdnnp::u128>(std::max<i64>(0, e.t0 - last));
+    last = std::max(last, e.t0);
+    if (e.kind == Ev::Alloc) {
+      live += round_up(e.bytes, kAlign);
+      peak = std::max(peak, live);
+    } else {
+      live -= round_up(e.bytes, kAlign);
+    }
+  }
+  if (r.total > last) area += static_cast<vdnnp::u128>(live) * static_cast<vdnnp::u128>(r.total - last);
+  r.max_mem = peak;
+  r.avg_mem = r.total > 0 ? static_cast<u64>(area / static_cast<vdnnp::u128>(r.total)) : 0;
+  r.offload_bytes = plan_.offload_bytes;
+  r.prefetch_bytes = plan_.prefetch_bytes;
+  r.host_peak = plan_.host_peak;
+  r.interference = plan_.interference;
+  r.reuse.assign(static_cast<size_t>(L_), -1);
+  std::vector<i64> fe(static_cast<size_t>(L_), -1), bs(static_cast<size_t>(L_), -1);
+  for (const Event& e : r.events) {
+    if (e.kind == Ev::Fwd) fe[static_cast<size_t>(e.layer)] = e.t1;
+    if (e.kind == Ev::Bwd) bs[static_cast<size_t>(e.layer)] = e.t0;
+  }
+  for (size_t i = 0; i < static_cast<size_t>(L_); ++i)
+    if (fe[i] >= 0 && bs[i] >= 0) r.reuse[i] = bs[i] - fe[i];
+  return r;
+}
+
+void Session::layer_times(int n, double* fwd_ms, double* bwd_ms) const {
+  if (ev_.empty()) throw PlanError(Err::Generic, "session was created without record_timeline");
+  for (int i = 0; i < n; ++i) {
+    if (fwd_ms) fwd_ms[i] = 0;
+    if (bwd_ms) bwd_ms[i] = 0;
+  }
+  auto el = [&](size_t k) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev_[2 * k], ev_[2 * k + 1]);
+    return static_cast<double>(ms);
+  };
+  for (const FwdStep& s : fwd_)
+    if (s.layer < n && fwd_ms) fwd_ms[s.layer] = el(static_cast<size_t>(s.ev));
+  for (const BwdStep& s : bwd_)
+    if (s.layer < n && bwd_ms) bwd_ms[s.layer] = el(static_cast<size_t>(s.ev));
+}
+
+}  // namespace vdnnrt

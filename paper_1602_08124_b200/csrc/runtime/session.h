@@ -1,0 +1,151 @@
+// B200 executor: replays a planner schedule on one device arena, a pinned
+// host arena, a compute stream and a dedicated memcpy stream.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../kernels/kernels.h"
+#include "../planner/planner.hpp"
+
+namespace vdnnrt {
+
+using vdnnp::i64;
+using vdnnp::u64;
+
+struct Options {
+  int device = 0;
+  u64 weight_seed = 5000;
+  bool external_grads = false;
+  bool record_timeline = false;
+  bool host_arena = true;
+};
+
+// One gradient plane: the slice of a dX buffer that holds the gradient w.r.t.
+// one input of its producer (split-plane layout for concat joins).
+struct Plane {
+  int producer = -1;  // layer whose BWD writes the buffer
+  int index = 0;      // which input of the producer
+};
+
+struct Transfer {
+  int owner = -1;
+  u64 bytes = 0;
+  u64 dev_off = 0;  // pool offset of the device extent
+  u64 host_off = 0;
+  int ev = -1;      // timing event pair index
+};
+
+struct FwdStep {
+  int layer = -1;
+  std::vector<u64> in_off;   // feature offsets of the layer's inputs (in input order, via owners)
+  u64 out_off = 0;           // own feature buffer (or owner's for ACTV)
+  u64 w_off = 0;
+  u64 ws_off = 0, ws_bytes = 0;
+  std::vector<Transfer> offloads;
+  int ev = -1;
+};
+
+struct BwdStep {
+  int layer = -1;
+  std::vector<Transfer> prefetches;     // issued at this step (opportunistic + on demand)
+  std::vector<int> wait_prefetch;       // owners whose prefetch must land before the kernels
+  std::vector<u64> in_off;              // features of inputs (X), in input order
+  u64 out_off = 0;                      // own feature buffer (POOL Y / ACTV owner)
+  u64 w_off = 0;
+  u64 ws_off = 0, ws_bytes = 0;
+  std::vector<u64> plane_off;           // dX planes written by this step (per input; ~0 = none)
+  bool accumulate = false;              // two-buffer fork accumulation
+  std::vector<u64> dy_off;              // distinct incoming gradient locations (first = canonical)
+  int ev = -1;
+};
+
+class Session {
+ public:
+  Session(const vdnnp::Net& g, const vdnnp::Decision& d, const vdnnp::Cost& c, u64 capacity, const Options& o);
+  ~Session();
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+
+  void set_batch_host(const float* images, const int32_t* labels);
+  void set_batch_device(const float* images, const int32_t* labels);
+  void synthetic_batch(u64 seed);
+  void get_weights(int layer, float* host, size_t count);
+  void set_weights(int layer, const float* host, size_t count);
+  void step(float lr, float* loss_host);
+  void synchronize();
+  void read_feature(int owner, float* host, size_t count);
+  vdnnp::Report measured_report() const;
+  void layer_times(int n, double* fwd_ms, double* bwd_ms) const;
+  void grad_buffer(int layer, void** ptr, size_t* count);
+  void grad_arena(void** ptr, size_t* count);
+  void apply_grads(float lr, float scale);
+
+  const vdnnp::Report& plan() const { return plan_; }
+  u64 arena_bytes() const { return arena_bytes_; }
+  u64 arena_lo() const { return arena_lo_; }
+  u64 host_bytes() const { return host_bytes_; }
+  u64 scratch_bytes() const { return scratch_bytes_; }
+  cudaStream_t stream() const { return cs_; }
+
+ private:
+  float* F(u64 off) const { return reinterpret_cast<float*>(base_ + off); }
+  void build_program();
+  void assign_two_buffer();
+  void init_weights();
+  void run_fwd(const FwdStep& s, float lr);
+  void run_bwd(const BwdStep& s, float lr);
+  vdnnk::ConvArgs conv_args(int layer, const std::vector<u64>& in_off, const std::vector<u64>* planes) const;
+  void check(cudaError_t e, const char* what) const;
+
+  vdnnp::Net g_;
+  vdnnp::Decision d_;
+  vdnnp::Cost c_;
+  u64 cap_;
+  Options o_;
+  vdnnp::Report plan_;
+  vdnnp::Liveness lv_;
+  int L_ = 0;
+  int input_id_ = -1, loss_id_ = -1, logits_owner_ = -1;
+  int classes_ = 0;
+
+  cudaStream_t cs_ = nullptr, ms_ = nullptr;
+  char* arena_ = nullptr;
+  char* base_ = nullptr;
+  u64 arena_lo_ = 0, arena_bytes_ = 0;
+  char* host_ = nullptr;
+  u64 host_bytes_ = 0;
+  std::vector<u64> host_slot_;  // per owner
+  u64 scratch_bytes_ = 0;
+  float* loss_grad_ = nullptr;
+  float* row_loss_ = nullptr;
+  float* loss_ = nullptr;
+  int32_t* labels_ = nullptr;
+  float* splitk_ = nullptr;
+  size_t splitk_bytes_ = 0;
+  float* grads_ = nullptr;       // external gradient arena
+  std::vector<u64> grad_off_;    // per layer float offset into grads_
+  size_t grads_count_ = 0;
+  float* pinned_loss_ = nullptr;
+
+  u64 x_off_ = 0;                // INPUT feature extent (setup allocation)
+  std::vector<u64> w_off_;       // per layer weight offset
+  std::vector<FwdStep> fwd_;
+  std::vector<BwdStep> bwd_;
+  // two-buffer scheme: dX location per producer
+  std::vector<u64> g2_loc_;
+  std::vector<char> g2_accum_;
+
+  // timing
+  std::vector<cudaEvent_t> ev_;  // pairs: [2i] start, [2i+1] end
+  cudaEvent_t ev_iter_ = nullptr;
+  cudaEvent_t ev_sync_ = nullptr;
+  std::vector<cudaEvent_t> step_ev_;  // compute-side step-start events (cross-stream gating)
+  std::vector<cudaEvent_t> t0_ev_;    // timed step-start events (record_timeline)
+  std::vector<cudaEvent_t> xfer_ev_;  // per transfer completion
+  bool timed_ = false;
+};
+
+}  // namespace vdnnrt
