@@ -243,6 +243,7 @@ typedef struct vdnn_session_options {
   int32_t external_grads;    /* 1: wgrad writes dW to a non-pool gradient arena (for allreduce) */
   int32_t record_timeline;   /* 1: record CUDA events per op for a measured report */
   int32_t host_arena;        /* 1: pinned host arena for offloads (required when the plan offloads) */
+  int32_t precise_fp32;      /* 1: conv/FC contractions as 3xTF32 (fp32-accurate); 0: TF32 */
 } vdnn_session_options;
 void vdnn_session_options_default(vdnn_session_options* o);
 
@@ -272,6 +273,8 @@ vdnn_status vdnn_session_measured_report(vdnn_session* s, vdnn_report** out);
 vdnn_status vdnn_session_layer_times(vdnn_session* s, int32_t n_layers, double* fwd_ms, double* bwd_ms);
 /* Gradient arena (external_grads=1): device pointer and float count of layer's dW (or 0). */
 vdnn_status vdnn_session_grad_buffer(vdnn_session* s, int32_t layer, void** dev_ptr, size_t* count);
+/* Copy layer's dW (+bias grad for FC) from the gradient arena to host (external_grads=1). */
+vdnn_status vdnn_session_get_grads(vdnn_session* s, int32_t layer, float* host, size_t count);
 /* Apply SGD from the gradient arena (after an external allreduce). */
 vdnn_status vdnn_session_apply_grads(vdnn_session* s, float lr, float grad_scale);
 /* Whole-gradient-arena pointer for a single bucketed allreduce. */
@@ -297,6 +300,8 @@ vdnn_status vdnn_kernel_conv_dgrad(const vdnn_conv_desc* d, const float* w, cons
 vdnn_status vdnn_kernel_conv_wgrad(const vdnn_conv_desc* d, const float* dy, float* w, float lr, float* dw_out,
                                    float* ws, size_t ws_bytes, void* stream);
 size_t vdnn_kernel_conv_wgrad_ws_bytes(const vdnn_conv_desc* d);
+/* Calling-thread switch for the kernel-level conv entry points: 1 = 3xTF32 (fp32-accurate), 0 = TF32. */
+void vdnn_kernel_set_precise(int32_t on);
 vdnn_status vdnn_kernel_maxpool_fwd(const vdnn_conv_desc* d, int32_t window, int32_t stride, float* y, void* stream);
 vdnn_status vdnn_kernel_maxpool_bwd(const vdnn_conv_desc* d, int32_t window, int32_t stride, const float* y,
                                     const float* dy, void* stream);

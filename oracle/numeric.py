@@ -55,9 +55,22 @@ def _nhwc(shape):
     return (n, h, w, c)
 
 
+def tf32(t: torch.Tensor) -> torch.Tensor:
+    """Emulate the tensor core's kind::tf32 operand read: keep the top 19 bits
+    (sign, 8-bit exponent, 10-bit mantissa) of each fp32 value (truncation)."""
+    i = t.to(torch.float32).contiguous().view(torch.int32)
+    return (i & ~0x1FFF).view(torch.float32).to(t.dtype)
+
+
 def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np.ndarray, lr: float,
-               dtype=torch.float64) -> Tuple[float, Dict[int, np.ndarray], Dict[int, np.ndarray]]:
-    """Returns (loss, updated weights, weight gradients)."""
+               dtype=torch.float64, tf32_operands: bool = False
+               ) -> Tuple[float, Dict[int, np.ndarray], Dict[int, np.ndarray]]:
+    """Returns (loss, updated weights, weight gradients).
+
+    tf32_operands=True rounds both operands of every conv/FC contraction the
+    way kind::tf32 reads them (fp32 values stay fp32 between layers); this is
+    the tight-tolerance oracle for the tensor-core path."""
+    q = tf32 if tf32_operands else (lambda t: t)
     L = layers_of(g)
     N = len(L)
     buf: Dict[int, torch.Tensor] = {}
@@ -89,7 +102,7 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
             x = cat_in(l).permute(0, 3, 1, 2)
             cin = x.shape[1]
             w = W[l.id].reshape(cout, k, k, cin).permute(0, 3, 1, 2)
-            buf[l.id] = Fn.conv2d(x, w, stride=s, padding=p).permute(0, 2, 3, 1).contiguous()
+            buf[l.id] = Fn.conv2d(q(x), q(w), stride=s, padding=p).permute(0, 2, 3, 1).contiguous()
         elif l.kind == ACTV:
             o = owner(L, l.id)
             buf[o] = torch.relu(buf[o])
@@ -103,7 +116,7 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
             fin = x.shape[1]
             w = W[l.id][: out * fin].reshape(out, fin)
             b = W[l.id][out * fin:]
-            buf[l.id] = (x @ w.t() + b).reshape(_nhwc(l.shape))
+            buf[l.id] = (q(x) @ q(w).t() + b).reshape(_nhwc(l.shape))
         elif l.kind == LOSS:
             z = buf[owner(L, l.inputs[0])].reshape(l.shape[0], -1)
             lab = torch.tensor(labels, dtype=torch.long)
@@ -193,9 +206,9 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
             w4 = W[m].reshape(cout, k, k, cin).permute(0, 3, 1, 2)
             dyn = dy.permute(0, 3, 1, 2)
             if produces(l):
-                dx = torch.nn.grad.conv2d_input(x.shape, w4, dyn, stride=s, padding=p)
+                dx = torch.nn.grad.conv2d_input(x.shape, q(w4), q(dyn), stride=s, padding=p)
                 set_planes(l, dx.permute(0, 2, 3, 1), False)
-            dw = torch.nn.grad.conv2d_weight(x, w4.shape, dyn, stride=s, padding=p)
+            dw = torch.nn.grad.conv2d_weight(q(x), w4.shape, q(dyn), stride=s, padding=p)
             gk = dw.permute(0, 2, 3, 1).reshape(-1)
             grads[m] = gk
             W[m] = W[m] - lr * gk
@@ -206,8 +219,8 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
             w = W[m][: out * fin].reshape(out, fin)
             d2 = dy.reshape(dy.shape[0], -1)
             if produces(l):
-                set_planes(l, d2 @ w, True)
-            dw = d2.t() @ x
+                set_planes(l, q(d2) @ q(w), True)
+            dw = q(d2).t() @ q(x)
             db = d2.sum(0)
             gk = torch.cat([dw.reshape(-1), db])
             grads[m] = gk

@@ -110,7 +110,7 @@ class Violation(C.Structure):
 class SessionOptions(C.Structure):
     _fields_ = [
         ("device", C.c_int32), ("weight_seed", C.c_uint64), ("external_grads", C.c_int32),
-        ("record_timeline", C.c_int32), ("host_arena", C.c_int32),
+        ("record_timeline", C.c_int32), ("host_arena", C.c_int32), ("precise_fp32", C.c_int32),
     ]
 
 
@@ -134,6 +134,8 @@ def lib() -> C.CDLL:
         _lib.vdnn_kernel_launch_count.restype = C.c_uint64
         _lib.vdnn_kernel_conv_wgrad_ws_bytes.restype = C.c_size_t
         _lib.vdnn_kernel_conv_wgrad_ws_bytes.argtypes = [C.c_void_p]
+        _lib.vdnn_kernel_set_precise.restype = None
+        _lib.vdnn_kernel_set_precise.argtypes = [C.c_int32]
         if hasattr(_lib, "vdnn_session_plan"):
             _lib.vdnn_session_plan.restype = C.c_void_p
             _lib.vdnn_session_plan.argtypes = [C.c_void_p]

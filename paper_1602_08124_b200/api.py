@@ -724,7 +724,7 @@ class Session:
 
     def __init__(self, g: NetworkGraph, decision: PolicyDecision, cost: Optional[CostModel] = None,
                  capacity: int = 12884901888, device: int = 0, weight_seed: int = 5000,
-                 external_grads: bool = False, record_timeline: bool = False):
+                 external_grads: bool = False, record_timeline: bool = False, precise_fp32: bool = False):
         self.graph = g
         self.decision = decision
         self.cost = cost or CostModel()
@@ -735,6 +735,7 @@ class Session:
         opt.weight_seed = weight_seed
         opt.external_grads = int(external_grads)
         opt.record_timeline = int(record_timeline)
+        opt.precise_fp32 = int(precise_fp32)
         d = decision._handle(g)
         c = self.cost._c()
         h = C.c_void_p()
@@ -821,6 +822,14 @@ class Session:
         n = C.c_size_t()
         _call("vdnn_session_grad_arena", self.handle, C.byref(p), C.byref(n))
         return (p.value or 0), n.value
+
+    def get_grads(self, layer: int):
+        """dW (and FC bias gradient) of the last step; needs external_grads=True."""
+        import numpy as np
+        n = self.weight_count(layer)
+        out = np.empty(n, dtype=np.float32)
+        _call("vdnn_session_get_grads", self.handle, int(layer), out.ctypes.data_as(C.c_void_p), C.c_size_t(n))
+        return out
 
     def apply_grads(self, lr: float, scale: float = 1.0) -> None:
         _call("vdnn_session_apply_grads", self.handle, C.c_float(lr), C.c_float(scale))

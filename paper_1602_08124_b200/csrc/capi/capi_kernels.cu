@@ -36,6 +36,7 @@ vdnn_status cuda_status(cudaError_t e, const char* what) {
 extern "C" {
 
 uint64_t vdnn_kernel_launch_count(void) { return vdnnk::launch_count(); }
+void vdnn_kernel_set_precise(int32_t on) { vdnnk::set_precise(on != 0); }
 
 vdnn_status vdnn_kernel_conv_fprop(const vdnn_conv_desc* d, const float* w, const float* bias, float* y,
                                    void* stream) {

@@ -46,6 +46,7 @@ void vdnn_session_options_default(vdnn_session_options* o) {
   o->external_grads = 0;
   o->record_timeline = 0;
   o->host_arena = 1;
+  o->precise_fp32 = 0;
 }
 
 vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, const vdnn_cost_model* cm,
@@ -59,6 +60,7 @@ vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, con
       o.external_grads = opt->external_grads != 0;
       o.record_timeline = opt->record_timeline != 0;
       o.host_arena = opt->host_arena != 0;
+      o.precise = opt->precise_fp32 != 0;
     }
     if (!g->net.finalized()) throw vdnnp::PlanError(vdnnp::Err::Generic, "graph is not finalized");
     auto* s = new vdnnrt::Session(g->net, d->d, vdnncapi::cost_from(cm), capacity, o);
@@ -158,6 +160,18 @@ vdnn_status vdnn_session_grad_buffer(vdnn_session* s, int32_t layer, void** ptr,
 vdnn_status vdnn_session_grad_arena(vdnn_session* s, void** ptr, size_t* count) {
   return guard([&] {
     S(s).grad_arena(ptr, count);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_get_grads(vdnn_session* s, int32_t layer, float* host, size_t count) {
+  return guard([&] {
+    void* p = nullptr;
+    size_t n = 0;
+    S(s).grad_buffer(layer, &p, &n);
+    if (!p || n != count) throw vdnnp::PlanError(vdnnp::Err::Generic, "no gradient buffer / count mismatch");
+    S(s).synchronize();
+    if (cudaMemcpy(host, p, count * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+      throw std::runtime_error("cudaMemcpy(grads)");
     return VDNN_OK;
   });
 }

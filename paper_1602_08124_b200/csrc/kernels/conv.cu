@@ -11,6 +11,7 @@ namespace vdnnk {
 namespace {
 std::atomic<uint64_t> g_launches{0};
 constexpr int kStages = 4;
+constexpr int kStagesPrecise = 3;
 constexpr int kNumSms = 148;
 
 bool build_common(const ConvArgs& a, ConvParams& p) {
@@ -65,26 +66,32 @@ bool build_common(const ConvArgs& a, ConvParams& p) {
   return true;
 }
 
-template <int BN>
+template <int BN, int STAGES, bool PRECISE>
 cudaError_t launch_bn(const ConvParams& p, int splits, cudaStream_t st) {
-  using L = TcSmem<BN, kStages>;
+  using L = TcSmem<BN, STAGES, PRECISE>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         L::kTotal);
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, STAGES, PRECISE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid((p.M + kBM - 1) / kBM, (p.Ncols + BN - 1) / BN, splits);
-  tc_conv_kernel<BN, kStages><<<grid, 160, L::kTotal, st>>>(p);
+  tc_conv_kernel<BN, STAGES, PRECISE><<<grid, 160, L::kTotal, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }
 
+thread_local bool g_precise = false;
+
 cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
-  if (p.Ncols <= 64) return launch_bn<64>(p, splits, st);
-  return launch_bn<128>(p, splits, st);
+  if (g_precise) {
+    if (p.Ncols <= 64) return launch_bn<64, kStagesPrecise, true>(p, splits, st);
+    return launch_bn<128, kStagesPrecise, true>(p, splits, st);
+  }
+  if (p.Ncols <= 64) return launch_bn<64, kStages, false>(p, splits, st);
+  return launch_bn<128, kStages, false>(p, splits, st);
 }
 
 int pick_bn(int ncols) { return ncols <= 64 ? 64 : 128; }
@@ -94,6 +101,8 @@ int wgrad_rows(const ConvParams& p) { return p.vec_in ? p.kh * p.kw * p.nchunk *
 }  // namespace
 
 uint64_t launch_count() { return g_launches.load(); }
+void set_precise(bool on) { g_precise = on; }
+bool precise() { return g_precise; }
 void count_launch(uint64_t k) { g_launches.fetch_add(k); }
 
 cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,

@@ -27,7 +27,11 @@ struct ConvArgs {
   }
 };
 
-// Tensor-core conv contractions (kind::tf32, fp32 accumulate).
+// Tensor-core conv contractions (kind::tf32, fp32 accumulate). With
+// set_precise(true) (per calling thread) every contraction runs as 3xTF32
+// (hi*hi + hi*lo + lo*hi), i.e. fp32-accurate products.
+void set_precise(bool on);
+bool precise();
 cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
                        cudaStream_t st);
 cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st);

@@ -548,18 +548,52 @@ __device__ __forceinline__ int wgrad_widx(const ConvParams& p, int m, bool& vali
 }
 
 // ------------------------------------------------------------ kernel ------
-template <int BN, int STAGES>
+// PRECISE = 3xTF32: each operand x = hi + lo with hi = tf32(x) (what the
+// tensor core reads from x itself: it truncates to 10 mantissa bits) and the
+// exactly representable residual lo = x - hi kept in a second tile; the
+// accumulator gets A*B + A*B_lo + A_lo*B, i.e. fp32-level products.
+template <int BN, int STAGES, bool PRECISE>
 struct TcSmem {
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = BN * 128;
-  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kHalf = kABytes + kBBytes;
+  static constexpr int kStage = PRECISE ? 2 * kHalf : kHalf;
   static constexpr int kTotal = STAGES * kStage + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
-template <int BN, int STAGES>
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void producers_sync() {  // named barrier over the 128 producer threads
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// lo = x - tf32_trunc(x) for every fp32 of a stage's A|B tiles (layout-agnostic
+// elementwise pass: the lo tiles mirror the hi tiles byte for byte).
+template <int BYTES>
+__device__ __forceinline__ void split_lo(uint32_t hi, uint32_t lo, int tid) {
+#pragma unroll 4
+  for (int off = tid * 16; off < BYTES; off += 128 * 16) {
+    uint32_t a, b, c, d;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(hi + off));
+    const float fa = __uint_as_float(a) - __uint_as_float(a & 0xFFFFE000u);
+    const float fb = __uint_as_float(b) - __uint_as_float(b & 0xFFFFE000u);
+    const float fc = __uint_as_float(c) - __uint_as_float(c & 0xFFFFE000u);
+    const float fd = __uint_as_float(d) - __uint_as_float(d & 0xFFFFE000u);
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lo + off), "f"(fa), "f"(fb), "f"(fc), "f"(fd)
+                 : "memory");
+  }
+}
+
+template <int BN, int STAGES, bool PRECISE>
 __global__ void __launch_bounds__(160, 1) tc_conv_kernel(const __grid_constant__ ConvParams p) {
   extern __shared__ uint8_t smem_raw[];
-  using L = TcSmem<BN, STAGES>;
+  using L = TcSmem<BN, STAGES, PRECISE>;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   const uint32_t bar_base = base + STAGES * L::kStage;
@@ -581,7 +615,7 @@ __global__ void __launch_bounds__(160, 1) tc_conv_kernel(const __grid_constant__
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), 128);
+      mbar_init(full_bar(s), 128);  // 128 producer arrivals (async cp.async arrive or plain arrive)
       mbar_init(empty_bar(s), 1);
     }
     mbar_init(accum_bar, 1);
@@ -614,7 +648,32 @@ __global__ void __launch_bounds__(160, 1) tc_conv_kernel(const __grid_constant__
         Gather<BN>::dgrad(p, m0, n0, kb, sa, sb, tid);
       else
         Gather<BN>::wgrad(p, m0, n0, kb, sa, sb, tid);
-      cp_async_arrive_noinc(full_bar(s));
+      if constexpr (!PRECISE) {
+        cp_async_arrive_noinc(full_bar(s));
+      } else {
+        // one stage of lag: split the previous stage once every producer's copies landed
+        cp_async_commit();
+        cp_async_wait<1>();
+        producers_sync();
+        if (it > 0) {
+          const int ps = (it - 1) % STAGES;
+          const uint32_t pa = base + ps * L::kStage;
+          split_lo<L::kHalf>(pa, pa + L::kHalf, tid);
+          fence_proxy_async();
+          mbar_arrive(full_bar(ps));
+        }
+      }
+    }
+    if constexpr (PRECISE) {
+      cp_async_wait<0>();
+      producers_sync();
+      if (nkb > 0) {
+        const int ps = (nkb - 1) % STAGES;
+        const uint32_t pa = base + ps * L::kStage;
+        split_lo<L::kHalf>(pa, pa + L::kHalf, tid);
+        fence_proxy_async();
+        mbar_arrive(full_bar(ps));
+      }
     }
     // ---------------- epilogue ----------------
     mbar_wait(accum_bar, 0);
@@ -737,7 +796,16 @@ __global__ void __launch_bounds__(160, 1) tc_conv_kernel(const __grid_constant__
                                    : make_sdesc(sa + kk * 32, 16, 1024, kSw128);
           const uint64_t bd = b_mn ? make_sdesc(sb + kk * 1024, 4096, 512, kSw128Base32)
                                    : make_sdesc(sb + kk * 32, 16, 1024, kSw128);
-          tc_mma_tf32(tmem, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+          if constexpr (PRECISE) {
+            // lo tiles sit kHalf bytes above the hi tiles with identical layout:
+            // descriptor start address += kHalf >> 4
+            constexpr uint64_t kLo = static_cast<uint64_t>(L::kHalf >> 4);
+            tc_mma_tf32(tmem, ad + kLo, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+            tc_mma_tf32(tmem, ad, bd + kLo, idesc, 1u);
+            tc_mma_tf32(tmem, ad, bd, idesc, 1u);
+          } else {
+            tc_mma_tf32(tmem, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+          }
         }
         tc_commit(empty_bar(s));
       }

@@ -596,6 +596,7 @@ void Session::run_bwd(const BwdStep& s, float lr) {
 
 void Session::step(float lr, float* loss_host) {
   timed_ = o_.record_timeline;
+  vdnnk::set_precise(o_.precise);
   if (timed_) check(cudaEventRecord(ev_iter_, cs_), "record");
   // the memory stream never runs ahead into a new iteration
   check(cudaEventRecord(ev_sync_, cs_), "record");

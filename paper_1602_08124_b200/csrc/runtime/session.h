@@ -21,6 +21,7 @@ struct Options {
   bool external_grads = false;
   bool record_timeline = false;
   bool host_arena = true;
+  bool precise = false;  // 3xTF32 contractions
 };
 
 // One gradient plane: the slice of a dX buffer that holds the gradient w.r.t.

@@ -6,10 +6,13 @@ device arena with real offload/prefetch copies. Compared with
 oracle/numeric.py (float64 CPU restatement of the same dataflow):
 
 * loss: |gpu - cpu| <= LOSS_TOL * max(1, |cpu|)
-* weight gradients (recovered as (W_before - W_after)/lr for every layer):
-  max |gpu - cpu| <= GRAD_TOL * max |cpu| per layer.
+* weight gradients (read back from the gradient arena, external_grads=True):
+  ||gpu - cpu||_2 <= TOL * ||cpu||_2 per layer (relative L2 norm: a ReLU mask
+  or max-pool argmax that flips on a near-tie routes one entry differently,
+  which a max-abs metric would amplify into a spurious failure).
 The tensor-core path computes in TF32 (10-bit mantissa inputs, fp32
-accumulate); GRAD_TOL covers TF32 rounding compounded through up to 8 layers.
+accumulate). Against the oracle that reads conv/FC operands the way kind::tf32
+does, the tolerance is TF32_GRAD_TOL; against plain float64, GRAD_TOL.
 Policies must not change the numbers: for a fork-free network every policy
 yields bit-identical weights after the step.
 """
@@ -22,9 +25,19 @@ import paper_1602_08124_b200 as V
 from oracle import numeric, refsim
 
 pytestmark = pytest.mark.gpu
-LOSS_TOL = 5e-3
-GRAD_TOL = 3e-2
 LR = 0.01
+# fp32 mode (precise_fp32=True: 3xTF32 contractions) vs the float64 oracle.
+# The tensor core's fp32 accumulation is not round-to-nearest: measured
+# single-layer bias ~7e-9 * K relative (K = reduction length), so deep nets
+# sit at ~1e-4 on the loss and <= ~6e-3 rel-L2 on early-layer dW (AlexNet).
+FP32_LOSS_TOL = 2e-4
+FP32_GRAD_TOL = 2e-2
+# TF32 mode (default) vs the float64 oracle: TF32 operand truncation (2^-11
+# relative per operand) compounds through the layers and flips near-tied
+# ReLU masks / pool argmaxes, so per-layer weight gradients of deep nets
+# differ by a few percent in relative L2 (measured: <= 8e-2 on AlexNet b8).
+TF32_LOSS_TOL = 1e-2
+TF32_GRAD_TOL = 1.5e-1
 
 
 def _need_gpu():
@@ -42,25 +55,38 @@ def _batch(g, seed=1234):
     return images, labels
 
 
-def _run_gpu(g, d, weights, images, labels, capacity=2 << 30, record=False):
-    s = V.Session(g, d, V.CostModel(), capacity, record_timeline=record)
+def _run_gpu(g, d, weights, images, labels, capacity=2 << 30, record=False, grads=False, precise=False):
+    """grads=True: dW goes to the gradient arena (read back exactly) instead of
+    the fused SGD epilogue; returns the gradients instead of updated weights."""
+    s = V.Session(g, d, V.CostModel(), capacity, record_timeline=record, external_grads=grads,
+                  precise_fp32=precise)
     for k, w in weights.items():
         s.set_weights(k, w)
     s.set_batch(images, labels)
     loss = s.step(LR)
+    if grads:
+        return s, loss, {k: s.get_grads(k) for k in weights}
     after = {k: s.get_weights(k) for k in weights}
     return s, loss, after
 
 
-def _check(g, weights, after, loss, images, labels, tag):
-    cl, cw, cg = numeric.train_step(g, weights, images, labels, LR)
-    assert abs(loss - cl) <= LOSS_TOL * max(1.0, abs(cl)), f"{tag}: loss {loss} vs {cl}"
+def _errs(g, weights, grads, loss, images, labels, tf32):
+    cl, cw, cg = numeric.train_step(g, weights, images, labels, LR, tf32_operands=tf32)
+    out = {}
     for k in weights:
-        gg = (weights[k].astype(np.float64) - after[k].astype(np.float64)) / LR
+        gg = grads[k].astype(np.float64)
         ref = cg[k]
-        scale = max(np.abs(ref).max(), 1e-12)
-        err = np.abs(gg - ref).max() / scale
-        assert err <= GRAD_TOL, f"{tag}: layer {k} grad err {err:.3e}"
+        out[k] = np.linalg.norm(gg - ref) / max(np.linalg.norm(ref), 1e-30)
+    return cl, out
+
+
+def _check(g, weights, grads, loss, images, labels, tag, precise):
+    cl, errs = _errs(g, weights, grads, loss, images, labels, False)
+    lt, gt = (FP32_LOSS_TOL, FP32_GRAD_TOL) if precise else (TF32_LOSS_TOL, TF32_GRAD_TOL)
+    print(tag, "precise" if precise else "tf32", "loss", loss, cl, {k: f"{v:.2e}" for k, v in errs.items()})
+    assert abs(loss - cl) <= lt * max(1.0, abs(cl)), f"{tag}: loss {loss} vs {cl}"
+    for k, e in errs.items():
+        assert e <= gt, f"{tag}: layer {k} grad rel-L2 err {e:.3e} (tol {gt})"
 
 
 POLICIES = [
@@ -71,16 +97,17 @@ POLICIES = [
 ]
 
 
+@pytest.mark.parametrize("precise", [True, False], ids=["fp32", "tf32"])
 @pytest.mark.parametrize("name,kind,mode", POLICIES)
-def test_alexnet_step_matches_oracle(name, kind, mode):
+def test_alexnet_step_matches_oracle(name, kind, mode, precise):
     _need_gpu()
     g = V.build_preset("alexnet", 8)
     cm = V.CostModel()
     w = numeric.he_weights(g, cm)
     images, labels = _batch(g)
     d = V.static_decision(kind, mode, g, cm)
-    s, loss, after = _run_gpu(g, d, w, images, labels, capacity=4 << 30)
-    _check(g, w, after, loss, images, labels, name)
+    s, loss, grads = _run_gpu(g, d, w, images, labels, capacity=4 << 30, grads=True, precise=precise)
+    _check(g, w, grads, loss, images, labels, name, precise)
 
 
 def test_policies_do_not_change_numbers():
@@ -101,16 +128,17 @@ def test_policies_do_not_change_numbers():
             assert np.array_equal(after[k], outs[0][2][k]), f"{name} layer {k}"
 
 
+@pytest.mark.parametrize("precise", [True, False], ids=["fp32", "tf32"])
 @pytest.mark.parametrize("name,kind,mode", POLICIES)
-def test_inception_fork_join_matches_oracle(name, kind, mode):
+def test_inception_fork_join_matches_oracle(name, kind, mode, precise):
     _need_gpu()
     g = V.build_preset("inception_toy", 4)
     cm = V.CostModel()
     w = numeric.he_weights(g, cm, seed=3)
     images, labels = _batch(g, seed=4)
     d = V.static_decision(kind, mode, g, cm)
-    s, loss, after = _run_gpu(g, d, w, images, labels)
-    _check(g, w, after, loss, images, labels, name)
+    s, loss, grads = _run_gpu(g, d, w, images, labels, grads=True, precise=precise)
+    _check(g, w, grads, loss, images, labels, name, precise)
 
 
 def _odd_graph():
@@ -130,16 +158,39 @@ def _odd_graph():
     return g.finalize()
 
 
+@pytest.mark.parametrize("precise", [True, False], ids=["fp32", "tf32"])
 @pytest.mark.parametrize("kind", [V.PolicyKind.VdnnAll, V.PolicyKind.VdnnConv, V.PolicyKind.Baseline])
-def test_odd_shapes_concat_alias_matches_oracle(kind):
+def test_odd_shapes_concat_alias_matches_oracle(kind, precise):
     _need_gpu()
     g = _odd_graph()
     cm = V.CostModel()
     w = numeric.he_weights(g, cm, seed=5)
     images, labels = _batch(g, seed=6)
     d = V.static_decision(kind, V.AlgoMode.MemoryOptimal, g, cm)
-    s, loss, after = _run_gpu(g, d, w, images, labels, capacity=64 << 20)
-    _check(g, w, after, loss, images, labels, str(kind))
+    s, loss, grads = _run_gpu(g, d, w, images, labels, capacity=64 << 20, grads=True, precise=precise)
+    _check(g, w, grads, loss, images, labels, str(kind), precise)
+    if not precise:
+        # single-precision rounding aside, the TF32 path is exactly "truncate
+        # operands to tf32, accumulate in fp32": the truncation-emulating
+        # oracle agrees to ~1e-6 on this shallow net
+        cl, errs = _errs(g, w, grads, loss, images, labels, True)
+        assert max(errs.values()) < 1e-4, errs
+
+
+def test_fused_sgd_matches_external_grads():
+    """The fused wgrad+SGD epilogue applies exactly lr * dW of the grad path."""
+    _need_gpu()
+    g = V.build_preset("inception_toy", 2)
+    cm = V.CostModel()
+    w = numeric.he_weights(g, cm, seed=9)
+    images, labels = _batch(g, seed=10)
+    d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+    _, l1, grads = _run_gpu(g, d, w, images, labels, grads=True)
+    _, l2, after = _run_gpu(g, d, w, images, labels)
+    assert l1 == l2
+    for k in w:
+        ref = w[k].astype(np.float32) - np.float32(LR) * grads[k]
+        np.testing.assert_allclose(after[k], ref, rtol=0, atol=2e-7 * max(1.0, float(np.abs(w[k]).max())))
 
 
 def test_dyn_under_tight_budget_and_measured_log_replays_clean():
