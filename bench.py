@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Headline benchmark: VGG-16 batch 256 training images/sec and peak GPU
+memory under a 12 GiB HBM budget with vDNN_dyn, next to vDNN_all, vDNN_conv
+and the no-offload baseline (BASELINE.json metric/config 4).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+One step = one full training iteration (forward, backward, SGD) of VGG-16 at
+batch 256 per GPU on synthetic data (U[-1,1) NHWC images, uniform labels,
+He-normal weights), replaying the bit-exact vDNN plan on the B200: offload and
+prefetch copies over PCIe, all compute in sm_100a tcgen05 kernels. Inputs are
+far larger than L2 (activations are GBs), so no explicit L2 flush is needed.
+N > 1: data parallel, one process per GPU, per-rank batch 256 (weak scaling),
+NCCL all-reduce of the weight gradients every step; time = max over ranks.
+
+--impl reference times the reference's CPU path on this host: the compiled
+reference simulator's planning (dynamic_select + simulate, oracle/_ref) plus
+the CPU numeric training step restated in oracle/numeric.py (torch CPU fp32,
+all host threads) on a bounded sample batch.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GIB12 = 12884901888
+METRIC = "VGG-16 b256 train images/sec & peak GPU mem (vDNN_all/conv/dyn vs no-offload)"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- helpers ----
+def gemm_flops(g):
+    """Algorithmic GEMM FLOPs of one iteration: conv fprop +
+    wgrad + dgrad (no dgrad when the input is the raw INPUT), FC 3x fprop."""
+    import paper_1602_08124_b200 as V
+    cm = V.CostModel()
+    total = 0.0
+    for l in g.layers():
+        if l.kind not in (V.LayerKind.Conv, V.LayerKind.Fc):
+            continue
+        f = cm.flops(g, l.id, False)
+        raw = all(g.layer(q).kind == V.LayerKind.Input for q in l.inputs)
+        total += f * (2 if raw else 3)
+    return total
+
+
+def memory_bound_bytes(g):
+    """Algorithmic bytes of the memory-bound kernels per iteration:
+    ReLU 2Y fwd + 3Y bwd; pool (X+Y) fwd + (2X+2Y) bwd; SGD 12 B/param."""
+    import paper_1602_08124_b200 as V
+    cm = V.CostModel()
+    b = 0
+    for l in g.layers():
+        if l.kind == V.LayerKind.Actv:
+            y = cm.tensor_bytes_of(g.shape(l.id))
+            b += 5 * y
+        elif l.kind == V.LayerKind.Pool:
+            y = cm.tensor_bytes_of(g.shape(l.id))
+            x = sum(cm.tensor_bytes_of(g.shape(q)) for q in l.inputs)
+            b += 3 * (x + y)
+        b += 3 * cm.weight_bytes(g, l.id)
+    return b
+
+
+def link_bandwidth(device: int, nbytes: int = 1 << 30):
+    """Pinned cudaMemcpyAsync GB/s per direction (host-link roofline)."""
+    import torch
+    h = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
+    d = torch.empty(nbytes // 4, dtype=torch.float32, device=f"cuda:{device}")
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(3):
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            e.synchronize()
+            best = max(best, nbytes / (s.elapsed_time(e) * 1e-3) / 1e9)
+        out[name + "_gbs"] = round(best, 2)
+    del h, d
+    return out
+
+
+# ---------------------------------------------------------------- our arm ----
+def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
+    import numpy as np
+    import torch
+    import paper_1602_08124_b200 as V
+    from paper_1602_08124_b200.dist import DataParallel, max_over_ranks
+
+    g = V.build_preset(args.net, args.batch) if args.extra == 0 else V.extend_vgg(args.extra, args.batch)
+    cm = V.CostModel()
+    cap = args.capacity
+    if policy == "dyn":
+        sel = V.dynamic_select(g, cap, cm)
+        if sel.decision is None:
+            return {"policy": policy, "verdict": "untrainable"}
+        d = sel.decision
+    elif policy == "all":
+        d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+    elif policy == "conv":
+        d = V.static_decision(V.PolicyKind.VdnnConv, V.AlgoMode.MemoryOptimal, g, cm)
+    else:  # no-offload baseline(p) with the device's capacity as the budget
+        d = V.static_decision(V.PolicyKind.Baseline, V.AlgoMode.PerfOptimal, g, cm)
+        free, total = torch.cuda.mem_get_info(device)
+        cap = int(free - (6 << 30))
+    plan = V.simulate(g, d, cm, cap)
+    if not plan.pass_:
+        return {"policy": policy, "label": d.label, "verdict": plan.verdict(), "capacity": cap}
+    s = V.Session(g, d, cm, cap, device=device, record_timeline=True, external_grads=world > 1,
+                  precise_fp32=args.precise)
+    dp = DataParallel(s, world, device) if world > 1 else None
+
+    def one(want_loss=False):
+        return dp.step(args.lr, want_loss) if dp else s.step(args.lr, want_loss=want_loss)
+
+    stream = torch.cuda.ExternalStream(s.stream, device=f"cuda:{device}")
+    s.synthetic_batch(1234 + device)
+    for _ in range(args.warmup):
+        one()
+    s.synchronize()
+    torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    l0 = V.kernel_launch_count()
+    with sampler_cls(device) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            one()
+        ev1.record(stream)
+        ev1.synchronize()
+    launches = V.kernel_launch_count() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms, world, device=f"cuda:{device}")
+    imgs = args.batch * world / (ms * 1e-3)
+    loss = s.step(args.lr, want_loss=True) if not dp else dp.step(args.lr, True)
+
+    # per-layer measured times of that last step
+    fwd_ms, bwd_ms = s.layer_times()
+    m = s.measured_report()
+    conv_ms = sum(fwd_ms[l.id] + bwd_ms[l.id] for l in g.layers() if l.kind in (V.LayerKind.Conv, V.LayerKind.Fc))
+    mem_ms = sum(fwd_ms[l.id] + bwd_ms[l.id] for l in g.layers()
+                 if l.kind in (V.LayerKind.Actv, V.LayerKind.Pool))
+    flops = gemm_flops(g)
+    conv_tflops = flops / (conv_ms * 1e-3) / 1e12 if conv_ms > 0 else None
+    off_ms = sum((e.end - e.start) for e in m.events if e.kind == V.EventKind.Offload) * 1e-6
+    pre_ms = sum((e.end - e.start) for e in m.events if e.kind == V.EventKind.Prefetch) * 1e-6
+    free, total = torch.cuda.mem_get_info(device)
+    res = {
+        "policy": policy, "label": d.label, "verdict": "PASS", "capacity_bytes": cap,
+        "images_per_s": round(imgs, 2), "ms_per_step": round(ms, 3), "loss": loss,
+        "peak_pool_bytes": plan.max_mem_bytes, "arena_bytes": s.arena_info()["arena_bytes"],
+        "device_used_bytes": total - free,
+        "offload_bytes_per_iter": plan.offload_traffic_bytes, "prefetch_bytes_per_iter": plan.prefetch_traffic_bytes,
+        "d2h_gbs": round(plan.offload_traffic_bytes / (off_ms * 1e-3) / 1e9, 2) if off_ms > 0 else None,
+        "h2d_gbs": round(plan.prefetch_traffic_bytes / (pre_ms * 1e-3) / 1e9, 2) if pre_ms > 0 else None,
+        "exposed_transfer_ms": round((m.stall_fwd_offload_ns + m.stall_bwd_prefetch_ns) * 1e-6, 3),
+        "conv_fc_ms": round(conv_ms, 3), "memory_bound_ms": round(mem_ms, 3),
+        "conv_fc_tflops": round(conv_tflops, 1) if conv_tflops else None,
+        "gpu_launches": launches, "clocks": clk.summary(),
+        "signature": plan.signature(),
+    }
+    if want_e2e:
+        # end to end through the public API: pinned host batch -> device every
+        # step, loss read back every step
+        sh = g.shape(0)
+        rng = np.random.default_rng(99 + device)
+        imgs_h = torch.from_numpy(rng.uniform(-1, 1, size=(sh.n, sh.h, sh.w, sh.c)).astype(np.float32)).pin_memory()
+        ls = g.shape(g.layer(g.size() - 1).inputs[0])
+        labs_h = torch.from_numpy(rng.integers(0, ls.c, size=sh.n).astype(np.int32)).pin_memory()
+        for _ in range(2):
+            s.set_batch_ptr(imgs_h.data_ptr(), labs_h.data_ptr())
+            one(True)
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            s.set_batch_ptr(imgs_h.data_ptr(), labs_h.data_ptr())
+            one(True)
+        e1.record(stream)
+        e1.synchronize()
+        wall = (time.perf_counter() - t0) / args.steps
+        ems = max(e0.elapsed_time(e1) / args.steps, wall * 1e3)
+        ems = max_over_ranks(ems, world, device=f"cuda:{device}")
+        res["e2e"] = {"value": round(args.batch * world / (ems * 1e-3), 2), "unit": "images/s",
+                      "h2d_bytes_per_step": imgs_h.numel() * 4 + labs_h.numel() * 4, "d2h_bytes_per_step": 4,
+                      "ms_per_step": round(ems, 3)}
+    res["_flops"] = flops
+    res["_conv_ms"] = conv_ms
+    del s
+    torch.cuda.synchronize(device)
+    return res
+
+
+def cpu_baseline_sample(args, seconds_target=15.0):
+    """Reference CPU path on this host: the compiled reference planner
+    (dynamic_select + simulate, oracle/_ref) + the numeric restatement of one
+    training iteration (torch CPU fp32, all threads) on a small batch."""
+    import numpy as np
+    import torch
+    import paper_1602_08124_b200 as V
+    from oracle import numeric, refsim
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    sample_batch = args.cpu_sample_batch
+    g = V.build_preset(args.net, sample_batch) if args.extra == 0 else V.extend_vgg(args.extra, sample_batch)
+    gfull = V.build_preset(args.net, args.batch) if args.extra == 0 else V.extend_vgg(args.extra, args.batch)
+    plan_s = refsim.time_plan(gfull.spec(), args.capacity, 20) if refsim.available() else 0.0
+    w = numeric.he_weights(g, V.CostModel())
+    sh = g.shape(0)
+    rng = np.random.default_rng(5)
+    images = rng.uniform(-1, 1, size=(sh.n, sh.h, sh.w, sh.c)).astype(np.float32)
+    ls = g.shape(g.layer(g.size() - 1).inputs[0])
+    labels = rng.integers(0, ls.c, size=sh.n).astype(np.int32)
+    t0 = time.perf_counter()
+    numeric.train_step(g, w, images, labels, args.lr, dtype=torch.float32)
+    step_s = time.perf_counter() - t0
+    return {"value": round(sample_batch / (step_s + plan_s), 3), "unit": "images/s", "cores": cores,
+            "kind": "port",
+            "sample": (f"{args.net} batch {sample_batch}: reference planner (oracle/_ref dynamic_select+simulate "
+                       f"at b{args.batch}, {plan_s * 1e3:.2f} ms) + CPU numeric fwd/bwd/SGD step "
+                       f"(oracle/numeric.py, torch fp32, {cores} threads, {step_s:.2f} s)")}, step_s + plan_s
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = []
+    for i in range(args.warmup + args.steps):
+        base, secs = cpu_baseline_sample(args)
+        if i >= args.warmup:
+            steps.append(secs)
+    ms = statistics.mean(steps) * 1e3
+    value = args.cpu_sample_batch / (ms * 1e-3)
+    base["value"] = round(value, 3)
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "images/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.net} batch {args.batch} vDNN_dyn @ {args.capacity} B (CPU sample batch "
+                                   f"{args.cpu_sample_batch})", "global_batch": args.cpu_sample_batch},
+            "cpu_baseline": base,
+            "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--net", default="vgg16")
+    ap.add_argument("--extra", type=int, default=0, help="extend_vgg extra conv layers (400 -> VGG-416)")
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--capacity", type=int, default=GIB12)
+    ap.add_argument("--policies", default="dyn,all,conv,none")
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--precise", action="store_true", help="3xTF32 fp32-accurate contractions")
+    ap.add_argument("--cpu-sample-batch", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    from paper_1602_08124_b200.dist import env_rank
+    rank, local, world = env_rank()
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    device = local
+    torch.cuda.set_device(device)
+    peaks, peaks_src = load_peaks()
+    link = link_bandwidth(device)
+
+    results = {}
+    for p in [x for x in args.policies.split(",") if x]:
+        results[p] = run_policy(p, args, device, world, peaks, want_e2e=(p == "dyn"), sampler_cls=ClockSampler)
+
+    head = results.get("dyn") or next(iter(results.values()))
+    tf32_peak = float(peaks.get("bf16_tflops_sustained", 1400.0)) / 2.0
+    line = {
+        "metric": METRIC, "value": head.get("images_per_s"), "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": head.get("ms_per_step"),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 (tf32 tensor cores)" if not args.precise else "f32 (3xtf32)",
+        "data": "synthetic (U[-1,1) NHWC images, uniform labels, He-normal init)",
+        "config": {"workload": f"{args.net}{'' if args.extra == 0 else '+' + str(args.extra)} batch {args.batch}/GPU, "
+                               f"vDNN_dyn under {args.capacity} B HBM budget ({head.get('label')})",
+                   "global_batch": args.batch * world, "per_gpu_batch": args.batch,
+                   "capacity_bytes": args.capacity, "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (activation maps are GBs); no flush needed"},
+        "e2e": head.get("e2e"),
+        "gpu_launches": head.get("gpu_launches"),
+        "clocks": head.get("clocks"),
+        "peak_gpu_mem_bytes": head.get("peak_pool_bytes"),
+        "device_used_bytes": head.get("device_used_bytes"),
+    }
+    if head.get("_conv_ms"):
+        ach = head["_flops"] / (head["_conv_ms"] * 1e-3) / 1e12
+        line["roofline"] = {"bound": "tensor", "kernel": "tc_conv_kernel (all conv/FC fprop+dgrad+wgrad launches)",
+                            "achieved": round(ach, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
+                            "frac": round(ach / tf32_peak, 4), "traffic": None,
+                            "peak_note": f"TF32 dense = {peaks_src} bf16 sustained / 2"}
+    line["host_link"] = dict(link, **{
+        "offload_bytes_per_iter": head.get("offload_bytes_per_iter"),
+        "d2h_gbs_in_run": head.get("d2h_gbs"), "h2d_gbs_in_run": head.get("h2d_gbs"),
+        "exposed_transfer_ms": head.get("exposed_transfer_ms")})
+    pol = {}
+    for k, r in results.items():
+        pol[k] = {kk: vv for kk, vv in r.items() if not kk.startswith("_") and kk not in ("clocks", "e2e")}
+    if "none" in results and results["none"].get("images_per_s") and head.get("images_per_s"):
+        line["slowdown_vs_no_offload"] = round(results["none"]["ms_per_step"] and
+                                               head["ms_per_step"] / results["none"]["ms_per_step"], 4)
+    line["policies"] = pol
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base, _ = cpu_baseline_sample(args)
+        line["cpu_baseline"] = base
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -277,6 +277,8 @@ vdnn_status vdnn_session_grad_buffer(vdnn_session* s, int32_t layer, void** dev_
 vdnn_status vdnn_session_get_grads(vdnn_session* s, int32_t layer, float* host, size_t count);
 /* Apply SGD from the gradient arena (after an external allreduce). */
 vdnn_status vdnn_session_apply_grads(vdnn_session* s, float lr, float grad_scale);
+/* Use a caller-owned device buffer (>= grad_arena count floats) as the gradient arena. */
+vdnn_status vdnn_session_set_grad_arena(vdnn_session* s, void* dev_ptr, size_t count);
 /* Whole-gradient-arena pointer for a single bucketed allreduce. */
 vdnn_status vdnn_session_grad_arena(vdnn_session* s, void** dev_ptr, size_t* count);
 /* Compute stream (cudaStream_t) for interop. */

@@ -831,6 +831,9 @@ class Session:
         _call("vdnn_session_get_grads", self.handle, int(layer), out.ctypes.data_as(C.c_void_p), C.c_size_t(n))
         return out
 
+    def set_grad_arena(self, dev_ptr: int, count: int) -> None:
+        _call("vdnn_session_set_grad_arena", self.handle, C.c_void_p(dev_ptr), C.c_size_t(count))
+
     def apply_grads(self, lr: float, scale: float = 1.0) -> None:
         _call("vdnn_session_apply_grads", self.handle, C.c_float(lr), C.c_float(scale))
 

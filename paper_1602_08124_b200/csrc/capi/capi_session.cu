@@ -163,6 +163,12 @@ vdnn_status vdnn_session_grad_arena(vdnn_session* s, void** ptr, size_t* count) 
     return VDNN_OK;
   });
 }
+vdnn_status vdnn_session_set_grad_arena(vdnn_session* s, void* ptr, size_t count) {
+  return guard([&] {
+    S(s).set_grad_arena(static_cast<float*>(ptr), count);
+    return VDNN_OK;
+  });
+}
 vdnn_status vdnn_session_get_grads(vdnn_session* s, int32_t layer, float* host, size_t count) {
   return guard([&] {
     void* p = nullptr;

@@ -175,7 +175,7 @@ Session::~Session() {
   cudaFree(labels_);
   if (pinned_loss_) cudaFreeHost(pinned_loss_);
   if (splitk_) cudaFree(splitk_);
-  if (grads_) cudaFree(grads_);
+  if (grads_ && grads_owned_) cudaFree(grads_);
   if (cs_) cudaStreamDestroy(cs_);
   if (ms_) cudaStreamDestroy(ms_);
 }
@@ -674,6 +674,15 @@ void Session::grad_buffer(int layer, void** ptr, size_t* count) {
 void Session::grad_arena(void** ptr, size_t* count) {
   *ptr = grads_;
   *count = grads_count_;
+}
+
+void Session::set_grad_arena(float* ptr, size_t count) {
+  if (!o_.external_grads) throw PlanError(Err::Generic, "session was created without external_grads");
+  if (!ptr || count < grads_count_) throw PlanError(Err::Generic, "gradient arena too small");
+  synchronize();
+  if (grads_ && grads_owned_) cudaFree(grads_);
+  grads_ = ptr;
+  grads_owned_ = false;
 }
 
 void Session::apply_grads(float lr, float scale) {

@@ -83,6 +83,7 @@ class Session {
   void grad_buffer(int layer, void** ptr, size_t* count);
   void grad_arena(void** ptr, size_t* count);
   void apply_grads(float lr, float scale);
+  void set_grad_arena(float* ptr, size_t count);
 
   const vdnnp::Report& plan() const { return plan_; }
   u64 arena_bytes() const { return arena_bytes_; }
@@ -127,6 +128,7 @@ class Session {
   float* splitk_ = nullptr;
   size_t splitk_bytes_ = 0;
   float* grads_ = nullptr;       // external gradient arena
+  bool grads_owned_ = true;
   std::vector<u64> grad_off_;    // per layer float offset into grads_
   size_t grads_count_ = 0;
   float* pinned_loss_ = nullptr;
