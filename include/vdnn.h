@@ -304,6 +304,8 @@ vdnn_status vdnn_kernel_conv_wgrad(const vdnn_conv_desc* d, const float* dy, flo
 size_t vdnn_kernel_conv_wgrad_ws_bytes(const vdnn_conv_desc* d);
 /* Calling-thread switch for the kernel-level conv entry points: 1 = 3xTF32 (fp32-accurate), 0 = TF32. */
 void vdnn_kernel_set_precise(int32_t on);
+/* Calling-thread switch: 1 = TMA producers where eligible (default), 0 = cp.async gathers everywhere. */
+void vdnn_kernel_set_tma(int32_t on);
 vdnn_status vdnn_kernel_maxpool_fwd(const vdnn_conv_desc* d, int32_t window, int32_t stride, float* y, void* stream);
 vdnn_status vdnn_kernel_maxpool_bwd(const vdnn_conv_desc* d, int32_t window, int32_t stride, const float* y,
                                     const float* dy, void* stream);

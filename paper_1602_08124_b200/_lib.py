@@ -136,6 +136,8 @@ def lib() -> C.CDLL:
         _lib.vdnn_kernel_conv_wgrad_ws_bytes.argtypes = [C.c_void_p]
         _lib.vdnn_kernel_set_precise.restype = None
         _lib.vdnn_kernel_set_precise.argtypes = [C.c_int32]
+        _lib.vdnn_kernel_set_tma.restype = None
+        _lib.vdnn_kernel_set_tma.argtypes = [C.c_int32]
         if hasattr(_lib, "vdnn_session_plan"):
             _lib.vdnn_session_plan.restype = C.c_void_p
             _lib.vdnn_session_plan.argtypes = [C.c_void_p]

@@ -37,6 +37,7 @@ extern "C" {
 
 uint64_t vdnn_kernel_launch_count(void) { return vdnnk::launch_count(); }
 void vdnn_kernel_set_precise(int32_t on) { vdnnk::set_precise(on != 0); }
+void vdnn_kernel_set_tma(int32_t on) { vdnnk::set_tma(on != 0); }
 
 vdnn_status vdnn_kernel_conv_fprop(const vdnn_conv_desc* d, const float* w, const float* bias, float* y,
                                    void* stream) {

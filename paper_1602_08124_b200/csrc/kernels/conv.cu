@@ -1,4 +1,6 @@
 // Launchers for the tcgen05 implicit-GEMM conv engine (tc_conv.cuh).
+#include <cuda.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cstring>
@@ -10,7 +12,7 @@ namespace vdnnk {
 
 namespace {
 std::atomic<uint64_t> g_launches{0};
-constexpr int kStages = 4;
+constexpr int kStages = 3;         // 3 x 32 KB (BN=128): two CTAs per SM overlap mainloop and epilogue
 constexpr int kStagesPrecise = 3;
 constexpr int kNumSms = 148;
 
@@ -66,32 +68,120 @@ bool build_common(const ConvArgs& a, ConvParams& p) {
   return true;
 }
 
-template <int BN, int STAGES, bool PRECISE>
-cudaError_t launch_bn(const ConvParams& p, int splits, cudaStream_t st) {
+// ---------------------------------------------------------- tensor maps ---
+using PfnTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+using PfnIm2col = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                               CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                               CUtensorMapFloatOOBfill);
+
+void* driver_fn(const char* name) {
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return f;
+}
+
+bool encode_tiled(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                  const cuuint32_t* box, CUtensorMapSwizzle sw) {
+  static PfnTiled fn = reinterpret_cast<PfnTiled>(driver_fn("cuTensorMapEncodeTiled"));
+  if (!fn) return false;
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<cuuint32_t>(rank), const_cast<void*>(base), dims,
+            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// NHWC [n][h][w][c] as an im2col source: windows of k x k with padding `pad`
+// and stride `stride`; `pixels` rows of 32 channels per load.
+bool encode_im2col(CUtensorMap* m, const void* base, int n, int h, int w, int c, int k, int stride, int pad,
+                   int pixels, CUtensorMapSwizzle sw) {
+  static PfnIm2col fn = reinterpret_cast<PfnIm2col>(driver_fn("cuTensorMapEncodeIm2col"));
+  if (!fn) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
+                              static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 4, static_cast<cuuint64_t>(w) * c * 4,
+                                 static_cast<cuuint64_t>(h) * w * c * 4};
+  const int lower[2] = {-pad, -pad};
+  const int upper[2] = {pad - (k - 1), pad - (k - 1)};
+  const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, lower, upper, 32,
+            static_cast<cuuint32_t>(pixels), es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Build the two maps of the TMA producer; false = use the cp.async gathers.
+template <int BN>
+bool make_maps(const ConvParams& p, CUtensorMap* ta, CUtensorMap* tb) {
+  if (p.nseg != 1 || !p.vec_in || !p.vec_out || p.kh != p.kw) return false;
+  const float* x = p.seg[0].x;
+  if (p.kind == kFprop) {
+    if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, kBM, CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.KK), static_cast<cuuint64_t>(p.Cout)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.KK) * 4};
+    const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(BN)};
+    return encode_tiled(tb, p.w, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  if (p.kind == kDgrad) {
+    if (p.stride != 1) return false;
+    if (!encode_im2col(ta, p.dy, p.N, p.Ho, p.Wo, p.Cout, p.kh, 1, p.kh - 1 - p.pad, kBM,
+                       CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+    const int taps = p.kh * p.kw;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.C), static_cast<cuuint64_t>(taps),
+                                static_cast<cuuint64_t>(p.Cout)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.C) * 4, static_cast<cuuint64_t>(taps) * p.C * 4};
+    const cuuint32_t box[3] = {32, 1, 32};
+    return encode_tiled(tb, p.w, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  }
+  if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    return false;
+  const int64_t P = static_cast<int64_t>(p.N) * p.Ho * p.Wo;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.Cout), static_cast<cuuint64_t>(P)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.Cout) * 4};
+  const cuuint32_t box[2] = {32, 32};
+  return encode_tiled(tb, p.dy, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+}
+
+thread_local bool g_precise = false;
+thread_local bool g_no_tma = false;
+
+template <int BN, int STAGES, bool PRECISE, bool TMA>
+cudaError_t launch_bn(const ConvParams& p, const CUtensorMap& ta, const CUtensorMap& tb, int splits,
+                      cudaStream_t st) {
   using L = TcSmem<BN, STAGES, PRECISE>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, STAGES, PRECISE>,
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, STAGES, PRECISE, TMA>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid((p.M + kBM - 1) / kBM, (p.Ncols + BN - 1) / BN, splits);
-  tc_conv_kernel<BN, STAGES, PRECISE><<<grid, 160, L::kTotal, st>>>(p);
+  tc_conv_kernel<BN, STAGES, PRECISE, TMA><<<grid, 160, L::kTotal, st>>>(p, ta, tb);
   count_launch();
   return cudaGetLastError();
 }
 
-thread_local bool g_precise = false;
-
 cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
+  alignas(64) CUtensorMap ta, tb;
+  std::memset(&ta, 0, sizeof(ta));
+  std::memset(&tb, 0, sizeof(tb));
   if (g_precise) {
-    if (p.Ncols <= 64) return launch_bn<64, kStagesPrecise, true>(p, splits, st);
-    return launch_bn<128, kStagesPrecise, true>(p, splits, st);
+    if (p.Ncols <= 64) return launch_bn<64, kStagesPrecise, true, false>(p, ta, tb, splits, st);
+    return launch_bn<128, kStagesPrecise, true, false>(p, ta, tb, splits, st);
   }
-  if (p.Ncols <= 64) return launch_bn<64, kStages, false>(p, splits, st);
-  return launch_bn<128, kStages, false>(p, splits, st);
+  if (p.Ncols <= 64) {
+    if (!g_no_tma && make_maps<64>(p, &ta, &tb)) return launch_bn<64, kStages, false, true>(p, ta, tb, splits, st);
+    return launch_bn<64, kStages, false, false>(p, ta, tb, splits, st);
+  }
+  if (!g_no_tma && make_maps<128>(p, &ta, &tb)) return launch_bn<128, kStages, false, true>(p, ta, tb, splits, st);
+  return launch_bn<128, kStages, false, false>(p, ta, tb, splits, st);
 }
 
 int pick_bn(int ncols) { return ncols <= 64 ? 64 : 128; }
@@ -102,6 +192,7 @@ int wgrad_rows(const ConvParams& p) { return p.vec_in ? p.kh * p.kw * p.nchunk *
 
 uint64_t launch_count() { return g_launches.load(); }
 void set_precise(bool on) { g_precise = on; }
+void set_tma(bool on) { g_no_tma = !on; }
 bool precise() { return g_precise; }
 void count_launch(uint64_t k) { g_launches.fetch_add(k); }
 

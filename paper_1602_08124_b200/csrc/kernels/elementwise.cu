@@ -163,12 +163,15 @@ __device__ __forceinline__ int pool_seg(const PoolDev& d, int c) {
 }
 
 // Y[n][oh][ow][c] = max over the window (row-major scan, first max wins).
+// Vectorised over 4 channels when every segment's C % 4 == 0 (VEC=4).
+template <int VEC>
 __global__ void maxpool_fwd_kernel(const __grid_constant__ PoolDev d, float* __restrict__ y) {
-  const size_t total = static_cast<size_t>(d.n) * d.ho * d.wo * d.ctot;
+  const int cv = d.ctot / VEC;
+  const size_t total = static_cast<size_t>(d.n) * d.ho * d.wo * cv;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(i % d.ctot);
-    size_t t = i / d.ctot;
+    const int c = static_cast<int>(i % cv) * VEC;
+    size_t t = i / cv;
     const int ow = static_cast<int>(t % d.wo);
     t /= d.wo;
     const int oh = static_cast<int>(t % d.ho);
@@ -177,34 +180,109 @@ __global__ void maxpool_fwd_kernel(const __grid_constant__ PoolDev d, float* __r
     const int cl = c - d.cbase[s];
     const float* x = d.x[s];
     const int C = d.c[s];
-    float m = -FLT_MAX;
+    float m[VEC];
     bool first = true;
     for (int r = 0; r < d.window; ++r) {
-      const int ih = oh * d.stride + r;
+      const float* row = x + ((static_cast<size_t>(n) * d.h + oh * d.stride + r) * d.w + ow * d.stride) * C + cl;
       for (int q = 0; q < d.window; ++q) {
-        const int iw = ow * d.stride + q;
-        const float v = x[((static_cast<size_t>(n) * d.h + ih) * d.w + iw) * C + cl];
-        if (first || v > m) {
-          m = v;
-          first = false;
+        float v[VEC];
+        if constexpr (VEC == 4) {
+          const float4 f = *reinterpret_cast<const float4*>(row + static_cast<size_t>(q) * C);
+          v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        } else {
+          v[0] = row[static_cast<size_t>(q) * C];
         }
+#pragma unroll
+        for (int k = 0; k < VEC; ++k)
+          if (first || v[k] > m[k]) m[k] = v[k];
+        first = false;
       }
     }
-    y[i] = m;
+    float* out = y + (((static_cast<size_t>(n) * d.ho + oh) * d.wo + ow) * d.ctot + c);
+    if constexpr (VEC == 4)
+      *reinterpret_cast<float4*>(out) = make_float4(m[0], m[1], m[2], m[3]);
+    else
+      out[0] = m[0];
   }
+}
+
+static bool pool_vec4(const PoolDev& d) {
+  for (int i = 0; i < d.nseg; ++i)
+    if (d.c[i] % 4 != 0) return false;
+  return true;
 }
 
 cudaError_t maxpool_fwd(const PoolArgs& a, float* y, cudaStream_t st) {
   const PoolDev d = to_dev(a);
   const size_t total = static_cast<size_t>(d.n) * d.ho * d.wo * d.ctot;
   if (total == 0) return cudaSuccess;
-  maxpool_fwd_kernel<<<grid_for(total, 4), kThreads, 0, st>>>(d, y);
+  if (pool_vec4(d))
+    maxpool_fwd_kernel<4><<<grid_for(total / 4, 2), kThreads, 0, st>>>(d, y);
+  else
+    maxpool_fwd_kernel<1><<<grid_for(total, 4), kThreads, 0, st>>>(d, y);
   count_launch();
   return cudaGetLastError();
 }
 
-// Gather form (deterministic): every input element sums dY over the windows
-// whose first-maximum position it is.
+// Non-overlapping windows (stride >= window): one thread per output element
+// (x VEC channels) finds the first maximum and scatters dY to it, zeros to the
+// rest of its window -- every covered input written exactly once, no atomics.
+template <int VEC>
+__global__ void maxpool_bwd_scatter_kernel(const __grid_constant__ PoolDev d, const float* __restrict__ y,
+                                           const float* __restrict__ dy) {
+  const int cv = d.ctot / VEC;
+  const size_t total = static_cast<size_t>(d.n) * d.ho * d.wo * cv;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % cv) * VEC;
+    size_t t = i / cv;
+    const int ow = static_cast<int>(t % d.wo);
+    t /= d.wo;
+    const int oh = static_cast<int>(t % d.ho);
+    const int n = static_cast<int>(t / d.ho);
+    const int s = pool_seg(d, c);
+    float* dx = d.dx[s];
+    if (dx == nullptr) continue;
+    const int cl = c - d.cbase[s];
+    const float* x = d.x[s];
+    const int C = d.c[s];
+    const size_t oidx = ((static_cast<size_t>(n) * d.ho + oh) * d.wo + ow) * d.ctot + c;
+    float ym[VEC], g[VEC];
+    bool done[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+      ym[k] = y[oidx + k];
+      g[k] = dy[oidx + k];
+      done[k] = false;
+    }
+    for (int r = 0; r < d.window; ++r) {
+      const size_t rowoff = ((static_cast<size_t>(n) * d.h + oh * d.stride + r) * d.w + ow * d.stride) * C + cl;
+      for (int q = 0; q < d.window; ++q) {
+        const size_t off = rowoff + static_cast<size_t>(q) * C;
+        float v[VEC], o[VEC];
+        if constexpr (VEC == 4) {
+          const float4 f = *reinterpret_cast<const float4*>(x + off);
+          v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        } else {
+          v[0] = x[off];
+        }
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          const bool hit = !done[k] && v[k] == ym[k];
+          o[k] = hit ? g[k] : 0.f;
+          done[k] = done[k] || hit;
+        }
+        if constexpr (VEC == 4)
+          *reinterpret_cast<float4*>(dx + off) = make_float4(o[0], o[1], o[2], o[3]);
+        else
+          dx[off] = o[0];
+      }
+    }
+  }
+}
+
+// Overlapping windows: gather form (deterministic): every input element sums
+// dY over the windows whose first-maximum position it is.
 __global__ void maxpool_bwd_kernel(const __grid_constant__ PoolDev d, const float* __restrict__ y,
                                    const float* __restrict__ dy) {
   const size_t total = static_cast<size_t>(d.n) * d.h * d.w * d.ctot;
@@ -259,7 +337,24 @@ cudaError_t maxpool_bwd(const PoolArgs& a, const float* y, const float* dy, cuda
   const PoolDev d = to_dev(a);
   const size_t total = static_cast<size_t>(d.n) * d.h * d.w * d.ctot;
   if (total == 0) return cudaSuccess;
-  maxpool_bwd_kernel<<<grid_for(total, 4), kThreads, 0, st>>>(d, y, dy);
+  if (d.stride >= d.window) {
+    // inputs no window covers (floor-mode remainder, or stride > window) get 0
+    const bool gaps = d.stride > d.window || (d.h - d.window) % d.stride != 0 || (d.w - d.window) % d.stride != 0 ||
+                      d.ho * d.stride + (d.window - d.stride) < d.h || d.wo * d.stride + (d.window - d.stride) < d.w;
+    if (gaps)
+      for (int i = 0; i < d.nseg; ++i)
+        if (d.dx[i]) {
+          cudaError_t e = cudaMemsetAsync(d.dx[i], 0, static_cast<size_t>(d.n) * d.h * d.w * d.c[i] * sizeof(float), st);
+          if (e != cudaSuccess) return e;
+        }
+    const size_t outs = static_cast<size_t>(d.n) * d.ho * d.wo * d.ctot;
+    if (pool_vec4(d))
+      maxpool_bwd_scatter_kernel<4><<<grid_for(outs / 4, 2), kThreads, 0, st>>>(d, y, dy);
+    else
+      maxpool_bwd_scatter_kernel<1><<<grid_for(outs, 4), kThreads, 0, st>>>(d, y, dy);
+  } else {
+    maxpool_bwd_kernel<<<grid_for(total, 4), kThreads, 0, st>>>(d, y, dy);
+  }
   count_launch();
   return cudaGetLastError();
 }

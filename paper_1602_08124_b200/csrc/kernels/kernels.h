@@ -32,6 +32,8 @@ struct ConvArgs {
 // (hi*hi + hi*lo + lo*hi), i.e. fp32-accurate products.
 void set_precise(bool on);
 bool precise();
+// TMA producers (im2col / tiled tensor maps) where eligible; off = cp.async gathers everywhere.
+void set_tma(bool on);
 cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
                        cudaStream_t st);
 cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st);

@@ -26,8 +26,10 @@
 //   warp 4    : TMEM allocator + single-thread tcgen05.mma issuer; each
 //               stage is released with tcgen05.commit -> EMPTY barrier.
 #pragma once
-#include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <cstdint>
 
 namespace vdnnk {
 
@@ -103,6 +105,33 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_
 __device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+// im2col: coordinates (c, w, h, n) of the first window's top-left corner in
+// input space (may be negative = padding), filter-tap offsets (w, h).
+__device__ __forceinline__ void tma_load_im2col(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c, int w,
+                                                int h, int n, uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -590,8 +619,52 @@ __device__ __forceinline__ void split_lo(uint32_t hi, uint32_t lo, int tid) {
   }
 }
 
-template <int BN, int STAGES, bool PRECISE>
-__global__ void __launch_bounds__(160, 1) tc_conv_kernel(const __grid_constant__ ConvParams p) {
+// TMA producer (single thread). A: im2col (fprop: X, dgrad: dY, 128-pixel
+// columns, SWIZZLE_128B = K-major canonical; wgrad: X, 32-pixel columns per
+// (tap, 32-channel) chunk, SWIZZLE_128B_ATOM_32B = MN-major canonical).
+// B: tiled (fprop: W [Cout][KK] K-major; dgrad: W as (Cin, taps, Cout)
+// MN-major chunks; wgrad: dY [P][Cout] MN-major chunks).
+template <int BN>
+__device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap* ta, const CUtensorMap* tb, int m0,
+                                          int n0, int kb, uint32_t sa, uint32_t sb, uint32_t bar) {
+  if (p.kind == kFprop) {
+    const int tap = kb / p.nchunk, ck = kb - tap * p.nchunk;
+    const int r = tap / p.kw, s = tap - r * p.kw;
+    const Pix q = decode_pix(m0, p.Ho, p.Wo);
+    tma_load_im2col(sa, ta, bar, ck * 32, q.w * p.stride - p.pad, q.h * p.stride - p.pad, q.n,
+                    static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+    tma_load_2d(sb, tb, bar, tap * p.C + ck * 32, n0);
+  } else if (p.kind == kDgrad) {
+    const int nck = (p.Cout + 31) >> 5;
+    const int tap = kb / nck, co0 = (kb - tap * nck) * 32;
+    const int r = tap / p.kw, s = tap - r * p.kw;
+    const int padh = p.kh - 1 - p.pad, padw = p.kw - 1 - p.pad;
+    const Pix q = decode_pix(m0, p.H, p.W);
+    tma_load_im2col(sa, ta, bar, co0, q.w - padw, q.h - padh, q.n, static_cast<uint16_t>(s),
+                    static_cast<uint16_t>(r));
+    const int ftap = (p.kh - 1 - r) * p.kw + (p.kw - 1 - s);
+#pragma unroll
+    for (int mc = 0; mc < BN / 32; ++mc) tma_load_3d(sb + mc * 4096, tb, bar, n0 + mc * 32, ftap, co0);
+  } else {
+    const int p0 = kb * kBK;
+    const Pix q = decode_pix(p0, p.Ho, p.Wo);
+#pragma unroll
+    for (int mc = 0; mc < kBM / 32; ++mc) {
+      const int vc = (m0 >> 5) + mc;
+      const int tap = vc / p.nchunk, ck = vc - tap * p.nchunk;
+      const int r = tap / p.kw, s = tap - r * p.kw;
+      tma_load_im2col(sa + mc * 4096, ta, bar, ck * 32, q.w * p.stride - p.pad, q.h * p.stride - p.pad, q.n,
+                      static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+    }
+#pragma unroll
+    for (int mc = 0; mc < BN / 32; ++mc) tma_load_2d(sb + mc * 4096, tb, bar, n0 + mc * 32, p0);
+  }
+}
+
+template <int BN, int STAGES, bool PRECISE, bool TMA>
+__global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__ ConvParams p,
+                                                         const __grid_constant__ CUtensorMap tma_a,
+                                                         const __grid_constant__ CUtensorMap tma_b) {
   extern __shared__ uint8_t smem_raw[];
   using L = TcSmem<BN, STAGES, PRECISE>;
   const uint32_t raw = smem_u32(smem_raw);
@@ -615,7 +688,7 @@ __global__ void __launch_bounds__(160, 1) tc_conv_kernel(const __grid_constant__
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), 128);  // 128 producer arrivals (async cp.async arrive or plain arrive)
+      mbar_init(full_bar(s), TMA ? 1 : 128);  // TMA: one expect_tx arrive; else 128 producer arrivals
       mbar_init(empty_bar(s), 1);
     }
     mbar_init(accum_bar, 1);
@@ -635,7 +708,23 @@ __global__ void __launch_bounds__(160, 1) tc_conv_kernel(const __grid_constant__
   if (warp < 4) {
     // ---------------- producers ----------------
     const int tid = threadIdx.x;
-    for (int it = 0; it < nkb; ++it) {
+    if constexpr (TMA) {
+      if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+        constexpr uint32_t kBytes = L::kABytes + L::kBBytes;
+        for (int it = 0; it < nkb; ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          if (it >= STAGES) mbar_wait(empty_bar(s), ph ^ 1);
+          const uint32_t sa = base + s * L::kStage;
+          mbar_expect_tx(full_bar(s), kBytes);
+          tma_issue<BN>(p, &tma_a, &tma_b, m0, n0, kb_begin + it, sa, sa + L::kABytes, full_bar(s));
+        }
+      }
+      __syncwarp();
+    }
+    for (int it = 0; !TMA && it < nkb; ++it) {
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;
       if (it >= STAGES) mbar_wait(empty_bar(s), ph ^ 1);
@@ -648,7 +737,7 @@ __global__ void __launch_bounds__(160, 1) tc_conv_kernel(const __grid_constant__
         Gather<BN>::dgrad(p, m0, n0, kb, sa, sb, tid);
       else
         Gather<BN>::wgrad(p, m0, n0, kb, sa, sb, tid);
-      if constexpr (!PRECISE) {
+      if constexpr (!PRECISE || TMA) {
         cp_async_arrive_noinc(full_bar(s));
       } else {
         // one stage of lag: split the previous stage once every producer's copies landed
@@ -664,7 +753,7 @@ __global__ void __launch_bounds__(160, 1) tc_conv_kernel(const __grid_constant__
         }
       }
     }
-    if constexpr (PRECISE) {
+    if constexpr (PRECISE && !TMA) {
       cp_async_wait<0>();
       producers_sync();
       if (nkb > 0) {

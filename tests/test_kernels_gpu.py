@@ -69,14 +69,19 @@ CASES = [
     (8, 1, 1, [4096], 1000, 1, 1, 0),         # AlexNet FC8 as 1x1
     (2, 27, 27, [64], 192, 5, 1, 2),          # AlexNet conv2
     (2, 13, 13, [384], 256, 3, 1, 1),         # AlexNet conv4
+    (3, 17, 17, [64], 96, 3, 2, 1),           # strided (fprop/wgrad only)
+    (2, 10, 10, [48], 36, 5, 1, 2),           # channels not multiples of 32
+    (300, 1, 1, [64], 20, 1, 1, 0),           # M spans several tiles of a 1x1 "image"
 ]
 
 
-@pytest.fixture(params=[False, True], ids=["tf32", "fp32"])
+@pytest.fixture(params=["tf32-tma", "tf32-cpasync", "fp32"])
 def precise(request):
-    L.lib().vdnn_kernel_set_precise(int(request.param))
-    yield request.param
+    L.lib().vdnn_kernel_set_precise(int(request.param == "fp32"))
+    L.lib().vdnn_kernel_set_tma(int(request.param != "tf32-cpasync"))
+    yield request.param == "fp32"
     L.lib().vdnn_kernel_set_precise(0)
+    L.lib().vdnn_kernel_set_tma(1)
 
 
 @pytest.mark.parametrize("case", CASES)

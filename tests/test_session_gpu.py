@@ -199,8 +199,8 @@ def test_dyn_under_tight_budget_and_measured_log_replays_clean():
     _need_gpu()
     g = V.build_preset("vgg16", 8)
     cm = V.CostModel()
-    oracle_run = V.simulate_oracle(g, cm)
-    cap = int(oracle_run.max_mem_bytes * 0.55)
+    floor = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+    cap = int(V.simulate(g, floor, cm, V.KUNLIMITED_BYTES).max_mem_bytes * 1.05)
     sel = V.dynamic_select(g, cap, cm)
     assert sel.decision is not None and sel.decision.label != "baseline(p)"
     s = V.Session(g, sel.decision, cm, cap, record_timeline=True)
