@@ -113,12 +113,21 @@ bool encode_im2col(CUtensorMap* m, const void* base, int n, int h, int w, int c,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Build the two maps of the TMA producer; false = use the cp.async gathers.
+// 2D output map [rows][cols] for the TMA-store epilogue (128-row x 32-col boxes).
+bool encode_out(CUtensorMap* m, const void* base, int64_t rows, int cols) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 4};
+  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kBM)};
+  return encode_tiled(m, base, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// Build the maps of the TMA producer (and output); false = cp.async gathers.
 template <int BN>
-bool make_maps(const ConvParams& p, CUtensorMap* ta, CUtensorMap* tb) {
+bool make_maps(const ConvParams& p, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* tc) {
   if (p.nseg != 1 || !p.vec_in || !p.vec_out || p.kh != p.kw) return false;
   const float* x = p.seg[0].x;
   if (p.kind == kFprop) {
+    if (!encode_out(tc, p.y, p.M, p.Cout)) return false;
     if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, kBM, CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.KK), static_cast<cuuint64_t>(p.Cout)};
@@ -127,7 +136,8 @@ bool make_maps(const ConvParams& p, CUtensorMap* ta, CUtensorMap* tb) {
     return encode_tiled(tb, p.w, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   if (p.kind == kDgrad) {
-    if (p.stride != 1) return false;
+    if (p.stride != 1 || p.seg[0].dx == nullptr) return false;
+    if (!encode_out(tc, p.seg[0].dx, p.M, p.C)) return false;
     if (!encode_im2col(ta, p.dy, p.N, p.Ho, p.Wo, p.Cout, p.kh, 1, p.kh - 1 - p.pad, kBM,
                        CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
@@ -151,8 +161,8 @@ thread_local bool g_precise = false;
 thread_local bool g_no_tma = false;
 
 template <int BN, int STAGES, bool PRECISE, bool TMA>
-cudaError_t launch_bn(const ConvParams& p, const CUtensorMap& ta, const CUtensorMap& tb, int splits,
-                      cudaStream_t st) {
+cudaError_t launch_bn(const ConvParams& p, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                      int splits, cudaStream_t st) {
   using L = TcSmem<BN, STAGES, PRECISE>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -161,27 +171,31 @@ cudaError_t launch_bn(const ConvParams& p, const CUtensorMap& ta, const CUtensor
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid((p.M + kBM - 1) / kBM, (p.Ncols + BN - 1) / BN, splits);
-  tc_conv_kernel<BN, STAGES, PRECISE, TMA><<<grid, 160, L::kTotal, st>>>(p, ta, tb);
+  const unsigned tiles = static_cast<unsigned>((p.M + kBM - 1) / kBM) * static_cast<unsigned>((p.Ncols + BN - 1) / BN);
+  dim3 grid(tiles, 1, splits);
+  tc_conv_kernel<BN, STAGES, PRECISE, TMA><<<grid, 160, L::kTotal, st>>>(p, ta, tb, tc);
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
-  alignas(64) CUtensorMap ta, tb;
+  alignas(64) CUtensorMap ta, tb, tc;
   std::memset(&ta, 0, sizeof(ta));
   std::memset(&tb, 0, sizeof(tb));
+  std::memset(&tc, 0, sizeof(tc));
   if (g_precise) {
-    if (p.Ncols <= 64) return launch_bn<64, kStagesPrecise, true, false>(p, ta, tb, splits, st);
-    return launch_bn<128, kStagesPrecise, true, false>(p, ta, tb, splits, st);
+    if (p.Ncols <= 64) return launch_bn<64, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
+    return launch_bn<128, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
   }
   if (p.Ncols <= 64) {
-    if (!g_no_tma && make_maps<64>(p, &ta, &tb)) return launch_bn<64, kStages, false, true>(p, ta, tb, splits, st);
-    return launch_bn<64, kStages, false, false>(p, ta, tb, splits, st);
+    if (!g_no_tma && make_maps<64>(p, &ta, &tb, &tc))
+      return launch_bn<64, kStages, false, true>(p, ta, tb, tc, splits, st);
+    return launch_bn<64, kStages, false, false>(p, ta, tb, tc, splits, st);
   }
-  if (!g_no_tma && make_maps<128>(p, &ta, &tb)) return launch_bn<128, kStages, false, true>(p, ta, tb, splits, st);
-  return launch_bn<128, kStages, false, false>(p, ta, tb, splits, st);
+  if (!g_no_tma && make_maps<128>(p, &ta, &tb, &tc))
+    return launch_bn<128, kStages, false, true>(p, ta, tb, tc, splits, st);
+  return launch_bn<128, kStages, false, false>(p, ta, tb, tc, splits, st);
 }
 
 int pick_bn(int ncols) { return ncols <= 64 ? 64 : 128; }

@@ -96,6 +96,32 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Long waits (epilogue warps waiting for the whole main loop): let the
+// hardware suspend the thread instead of spinning on issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000000u)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y, bool add) {
+  if (add)
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(src), "r"(x), "r"(y)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map), "r"(src),
+                 "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_and_drain() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
@@ -664,7 +690,8 @@ __device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap
 template <int BN, int STAGES, bool PRECISE, bool TMA>
 __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__ ConvParams p,
                                                          const __grid_constant__ CUtensorMap tma_a,
-                                                         const __grid_constant__ CUtensorMap tma_b) {
+                                                         const __grid_constant__ CUtensorMap tma_b,
+                                                         const __grid_constant__ CUtensorMap tma_c) {
   extern __shared__ uint8_t smem_raw[];
   using L = TcSmem<BN, STAGES, PRECISE>;
   const uint32_t raw = smem_u32(smem_raw);
@@ -679,8 +706,11 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kBM;
-  const int n0 = blockIdx.y * BN;
+  // linear tile index with the N tiles of one M tile adjacent, so the A
+  // (activation) tile is read from DRAM once and re-hit in L2
+  const int ntn = (p.Ncols + BN - 1) / BN;
+  const int m0 = static_cast<int>(blockIdx.x / ntn) * kBM;
+  const int n0 = static_cast<int>(blockIdx.x % ntn) * BN;
   const int kb_begin = blockIdx.z * p.kb_per_split;
   int kb_end = kb_begin + p.kb_per_split;
   if (kb_end > p.kblocks) kb_end = p.kblocks;
@@ -765,11 +795,44 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
       }
     }
     // ---------------- epilogue ----------------
-    mbar_wait(accum_bar, 0);
+    mbar_wait_sleep(accum_bar, 0);
     tc_fence_after();
+    __syncwarp();
     const int row = warp * 32 + lane;
     const int m = m0 + row;
     const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    if (TMA && p.kind != kWgrad) {
+      // Stage the 128 x BN tile in the idle pipeline buffers as BN/32
+      // SWIZZLE_128B boxes (128 rows x 128 B) and write it with TMA stores
+      // (reduce-add for accumulation): fully coalesced, clipped at M / Cout.
+#pragma unroll 1
+      for (int cg = 0; cg < BN / 32; ++cg) {
+        float v[32];
+        tmem_ld32(taddr + cg * 32, v);
+        const int nb = n0 + cg * 32;
+        if (nkb <= 0) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        if (p.kind == kFprop && p.bias) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += (nb + i < p.Cout) ? p.bias[nb + i] : 0.f;
+        }
+        const uint32_t rowaddr = base + cg * 16384 + row * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + (((j ^ (row & 7)) & 7) << 4)),
+                       "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                       : "memory");
+      }
+      fence_proxy_async();
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (threadIdx.x == 0) {
+        for (int cg = 0; cg < BN / 32; ++cg)
+          if (n0 + cg * 32 < p.Ncols) tma_store_2d(&tma_c, base + cg * 16384, n0 + cg * 32, m0, p.epi == kEpiAccum);
+        bulk_commit_and_drain();
+      }
+    } else {
 #pragma unroll 1
     for (int cg = 0; cg < BN / 32; ++cg) {
       float v[32];
@@ -826,21 +889,23 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
               if (i < c.valid) dst[i] = (p.epi == kEpiAccum ? dst[i] : 0.f) + v[i];
           }
         } else {
-#pragma unroll 4
+#pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int ci = nb + i;
-            if (ci >= p.C) break;
-            const Seg sg = p.seg[seg_of(p, ci)];
-            if (!sg.dx) continue;
-            float* dst = sg.dx + static_cast<int64_t>(m) * sg.C + (ci - sg.cbase);
-            *dst = (p.epi == kEpiAccum ? *dst : 0.f) + v[i];
+            if (ci < p.C) {
+              const Seg sg = p.seg[seg_of(p, ci)];
+              if (sg.dx) {
+                float* dst = sg.dx + static_cast<int64_t>(m) * sg.C + (ci - sg.cbase);
+                *dst = (p.epi == kEpiAccum ? *dst : 0.f) + v[i];
+              }
+            }
           }
         }
       } else {
         // WGRAD: row m = weight column (virtual), columns = co.
         if (p.epi == kEpiPartial) {
           float* dst = p.out + static_cast<int64_t>(blockIdx.z) * p.Ncols * p.M;
-#pragma unroll 4
+#pragma unroll
           for (int i = 0; i < 32; ++i)
             if (nb + i < p.Cout) dst[static_cast<int64_t>(nb + i) * p.M + m] = v[i];
         } else {
@@ -848,19 +913,20 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
           const int widx = wgrad_widx(p, m, valid);
           if (!valid) continue;
           if (p.epi == kEpiSgd) {
-#pragma unroll 4
+#pragma unroll
             for (int i = 0; i < 32; ++i)
               if (nb + i < p.Cout) {
                 float* w = p.w_mut + static_cast<int64_t>(nb + i) * p.KK + widx;
                 *w -= p.lr * v[i];
               }
           } else {
-#pragma unroll 4
+#pragma unroll
             for (int i = 0; i < 32; ++i)
               if (nb + i < p.Cout) p.out[static_cast<int64_t>(nb + i) * p.KK + widx] = v[i];
           }
         }
       }
+    }
     }
   } else if (warp == 4) {
     // ---------------- MMA issuer ----------------

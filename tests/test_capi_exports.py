@@ -1,0 +1,39 @@
+"""The C ABI library loads on a CPU-only host and exports every symbol that
+include/vdnn.h declares (no compute calls: those need a GPU)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+from paper_1602_08124_b200 import _lib as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared():
+    with open(os.path.join(ROOT, "include", "vdnn.h")) as f:
+        src = re.sub(r"/\*.*?\*/", "", f.read(), flags=re.S)
+    return sorted(set(re.findall(r"\b(vdnn_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported():
+    lib = L.lib()
+    names = declared()
+    assert len(names) > 60
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert missing == [], missing
+
+
+def test_only_the_c_abi_is_exported():
+    out = subprocess.run(["nm", "-D", "--defined-only", L.LIB_PATH], capture_output=True, text=True).stdout
+    syms = [l.split()[-1] for l in out.splitlines() if l.strip()]
+    assert syms and all(s.startswith("vdnn_") for s in syms), [s for s in syms if not s.startswith("vdnn_")][:5]
+
+
+def test_errors_are_status_codes_not_crashes():
+    lib = L.lib()
+    g = C.c_void_p()
+    assert lib.vdnn_preset(b"nope", C.c_uint64(4), C.byref(g)) == L.UNKNOWN_PRESET
+    assert b"unknown network preset" in lib.vdnn_last_error()
+    assert lib.vdnn_extend_vgg(150, C.c_uint64(4), C.byref(g)) == L.INVALID_DEPTH
+    assert lib.vdnn_version().startswith(b"vdnn-b200")

@@ -1,0 +1,51 @@
+"""Host-side logic of the data-parallel path on CPU (gloo, world_size 2):
+gradient averaging and max-over-ranks timing used by bench.py."""
+import os
+import socket
+
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1602_08124_b200.dist import allreduce_mean_, max_over_ranks
+    g = torch.full((1000,), float(rank + 1))
+    allreduce_mean_(g, world)
+    t = max_over_ranks(10.0 + rank, world)
+    q.put((rank, float(g[0]), float(g[-1]), t))
+    dist.destroy_process_group()
+
+
+def test_allreduce_mean_and_max_over_ranks():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    assert [r[1] for r in res] == [1.5, 1.5] and [r[2] for r in res] == [1.5, 1.5]
+    assert [r[3] for r in res] == [11.0, 11.0]
+
+
+def test_env_rank_defaults(monkeypatch):
+    from paper_1602_08124_b200.dist import env_rank
+    for k in ("RANK", "LOCAL_RANK", "WORLD_SIZE"):
+        monkeypatch.delenv(k, raising=False)
+    assert env_rank() == (0, 0, 1)
