@@ -209,6 +209,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     fwd_ms, bwd_ms = s.layer_times()
     m = s.measured_report()
     conv_ms = sum(fwd_ms[l.id] + bwd_ms[l.id] for l in g.layers() if l.kind in (V.LayerKind.Conv, V.LayerKind.Fc))
+    kernel_ms = sum(fwd_ms) + sum(bwd_ms)
     mem_ms = sum(fwd_ms[l.id] + bwd_ms[l.id] for l in g.layers()
                  if l.kind in (V.LayerKind.Actv, V.LayerKind.Pool))
     flops = gemm_flops(g)
@@ -224,7 +225,9 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         "offload_bytes_per_iter": plan.offload_traffic_bytes, "prefetch_bytes_per_iter": plan.prefetch_traffic_bytes,
         "d2h_gbs": round(plan.offload_traffic_bytes / (off_ms * 1e-3) / 1e9, 2) if off_ms > 0 else None,
         "h2d_gbs": round(plan.prefetch_traffic_bytes / (pre_ms * 1e-3) / 1e9, 2) if pre_ms > 0 else None,
-        "exposed_transfer_ms": round((m.stall_fwd_offload_ns + m.stall_bwd_prefetch_ns) * 1e-6, 3),
+        # compute-stream time not covered by layer kernels = waiting on offload/prefetch copies
+        "exposed_transfer_ms": round(max(0.0, ms - kernel_ms), 3) if world == 1 else None,
+        "kernel_ms": round(kernel_ms, 3),
         "conv_fc_ms": round(conv_ms, 3), "memory_bound_ms": round(mem_ms, 3),
         "conv_fc_tflops": round(conv_tflops, 1) if conv_tflops else None,
         "gpu_launches": launches, "clocks": clk.summary(),

@@ -202,6 +202,24 @@ int pick_bn(int ncols) { return ncols <= 64 ? 64 : 128; }
 
 int wgrad_rows(const ConvParams& p) { return p.vec_in ? p.kh * p.kw * p.nchunk * 32 : p.KK; }
 
+// Split-K factor for WGRAD: minimise waves/split (per-CTA work is ~K/s, the
+// grid runs in ceil(tiles*s / slots) waves of `slots` resident CTAs), at
+// least 8 K blocks per split; ties go to fewer splits (less partial traffic).
+int pick_splits(int tiles, int kblocks, int slots) {
+  int best = 1;
+  double best_t = 1e30;
+  const int smax = std::max(1, std::min(128, kblocks / 8));
+  for (int s = 1; s <= smax; ++s) {
+    const double waves = static_cast<double>((static_cast<int64_t>(tiles) * s + slots - 1) / slots);
+    const double t = waves / s + 1e-3 * s;
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = s;
+    }
+  }
+  return best;
+}
+
 }  // namespace
 
 uint64_t launch_count() { return g_launches.load(); }
@@ -249,8 +267,7 @@ size_t conv_wgrad_ws_bytes(const ConvArgs& a) {
   const int tiles = ((M + kBM - 1) / kBM) * ((a.cout + bn - 1) / bn);
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
   const int kblocks = static_cast<int>((P + kBK - 1) / kBK);
-  int splits = std::max(1, (2 * kNumSms + tiles - 1) / tiles);
-  splits = std::min(splits, std::max(1, kblocks / 8));
+  const int splits = pick_splits(tiles, kblocks, 2 * kNumSms);
   if (splits <= 1) return 0;
   return static_cast<size_t>(splits) * M * a.cout * sizeof(float);
 }
@@ -288,8 +305,7 @@ cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float l
   p.kblocks = static_cast<int>((P + kBK - 1) / kBK);
   const int bn = pick_bn(a.cout);
   const int tiles = ((p.M + kBM - 1) / kBM) * ((a.cout + bn - 1) / bn);
-  int splits = std::max(1, (2 * kNumSms + tiles - 1) / tiles);
-  splits = std::min(splits, std::max(1, p.kblocks / 8));
+  int splits = pick_splits(tiles, p.kblocks, 2 * kNumSms);
   const size_t per = static_cast<size_t>(p.M) * a.cout * sizeof(float);
   if (ws == nullptr || per == 0) splits = 1;
   else splits = static_cast<int>(std::min<size_t>(splits, ws_bytes / per));
