@@ -37,6 +37,7 @@ bool build_common(const ConvArgs& a, ConvParams& p) {
     p.seg[i].dx = a.dx[i];
     p.seg[i].C = a.c[i];
     p.seg[i].cbase = cb;
+    p.seg[i].mask = a.mask_in[i];
     cb += a.c[i];
     if (a.c[i] % 4 != 0) vec = false;
   }
@@ -233,6 +234,7 @@ cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, flo
   ConvParams p;
   if (!build_common(a, p)) return cudaErrorInvalidValue;
   p.kind = kFprop;
+  p.relu = a.relu_out;
   p.epi = accumulate ? kEpiAccum : kEpiStore;
   p.w = w;
   p.bias = bias;

@@ -131,6 +131,7 @@ struct PoolDev {
   float* dx[kMaxConvSegs];
   int c[kMaxConvSegs];
   int cbase[kMaxConvSegs];
+  int mask[kMaxConvSegs];  // fused ReLU backward: zero where x <= 0
 };
 
 static PoolDev to_dev(const PoolArgs& a) {
@@ -149,6 +150,7 @@ static PoolDev to_dev(const PoolArgs& a) {
     d.dx[i] = a.dx[i];
     d.c[i] = a.c[i];
     d.cbase[i] = cb;
+    d.mask[i] = a.mask_in[i];
     cb += a.c[i];
   }
   d.ctot = cb;
@@ -266,10 +268,11 @@ __global__ void maxpool_bwd_scatter_kernel(const __grid_constant__ PoolDev d, co
         } else {
           v[0] = x[off];
         }
+        const bool msk = d.mask[s] != 0;
 #pragma unroll
         for (int k = 0; k < VEC; ++k) {
           const bool hit = !done[k] && v[k] == ym[k];
-          o[k] = hit ? g[k] : 0.f;
+          o[k] = (hit && (!msk || v[k] > 0.f)) ? g[k] : 0.f;
           done[k] = done[k] || hit;
         }
         if constexpr (VEC == 4)
@@ -329,6 +332,7 @@ __global__ void maxpool_bwd_kernel(const __grid_constant__ PoolDev d, const floa
         if (oh * d.stride + ar == ih && ow * d.stride + aq == iw) g += dy[oidx];
       }
     }
+    if (d.mask[s] && x[((static_cast<size_t>(n) * d.h + ih) * d.w + iw) * C + cl] <= 0.f) g = 0.f;
     d.dx[s][((static_cast<size_t>(n) * d.h + ih) * d.w + iw) * C + cl] = g;
   }
 }

@@ -18,6 +18,8 @@ struct ConvArgs {
   float* dx[kMaxConvSegs] = {};            // segment gradient planes (dgrad), may be null
   int c[kMaxConvSegs] = {};                // segment channels
   int cout = 0, kh = 1, kw = 1, stride = 1, pad = 0;
+  int relu_out = 0;                        // fprop: fused ReLU on the output (the ACTV that follows)
+  int mask_in[kMaxConvSegs] = {};          // dgrad: fused ReLU backward, dX *= (x > 0) per segment
   int ho() const { return (h + 2 * pad - kh) / stride + 1; }
   int wo() const { return (w + 2 * pad - kw) / stride + 1; }
   int cin() const {
@@ -56,6 +58,7 @@ struct PoolArgs {
   const float* x[kMaxConvSegs] = {};
   float* dx[kMaxConvSegs] = {};
   int c[kMaxConvSegs] = {};
+  int mask_in[kMaxConvSegs] = {};          // bwd: fused ReLU backward (x is the ReLU's output)
   int ho() const { return (h - window) / stride + 1; }
   int wo() const { return (w - window) / stride + 1; }
   int ctot() const {

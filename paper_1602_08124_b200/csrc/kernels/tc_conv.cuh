@@ -47,6 +47,7 @@ struct Seg {
   float* dx;        // NHWC gradient plane (dgrad output); nullptr = not materialised
   int C;            // channels of this buffer
   int cbase;        // channel offset inside the concatenated input
+  int mask;         // dgrad: multiply dX by (x > 0) (fused ReLU backward)
 };
 
 // A 32-wide "virtual channel chunk" of the concatenated input (vector mode).
@@ -56,6 +57,7 @@ struct Chunk {
 
 struct ConvParams {
   int kind, epi;
+  int relu;                   // fprop: fused ReLU on the output
   int N, H, W, C;             // input side
   int Ho, Wo, Cout;           // output side
   int kh, kw, stride, pad;
@@ -818,6 +820,28 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += (nb + i < p.Cout) ? p.bias[nb + i] : 0.f;
         }
+        if (p.kind == kFprop && p.relu) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        if (p.kind == kDgrad && p.seg[0].mask && m < p.M && nb < p.C) {
+          // fused ReLU backward: the ReLU's output is this conv's input x
+          const float* xr = p.seg[0].x + static_cast<int64_t>(m) * p.C + nb;
+          if (nb + 32 <= p.C) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + i));
+              v[i] = xv.x > 0.f ? v[i] : 0.f;
+              v[i + 1] = xv.y > 0.f ? v[i + 1] : 0.f;
+              v[i + 2] = xv.z > 0.f ? v[i + 2] : 0.f;
+              v[i + 3] = xv.w > 0.f ? v[i + 3] : 0.f;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (nb + i < p.C) v[i] = xr[i] > 0.f ? v[i] : 0.f;
+          }
+        }
         const uint32_t rowaddr = base + cg * 16384 + row * 128;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -850,6 +874,10 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
           for (int i = 0; i < 32; ++i)
             if (nb + i < p.Cout) v[i] += p.bias[nb + i];
         }
+        if (p.relu) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
         if (p.vec_out && nb + 32 <= p.Cout) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
@@ -873,6 +901,12 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
           const Seg sg = p.seg[c.seg];
           if (!sg.dx) continue;
           float* dst = sg.dx + static_cast<int64_t>(m) * sg.C + c.coff;
+          if (sg.mask) {
+            const float* xr = sg.x + static_cast<int64_t>(m) * sg.C + c.coff;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < c.valid) v[i] = xr[i] > 0.f ? v[i] : 0.f;
+          }
           if (c.valid == 32) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
@@ -896,7 +930,9 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
               const Seg sg = p.seg[seg_of(p, ci)];
               if (sg.dx) {
                 float* dst = sg.dx + static_cast<int64_t>(m) * sg.C + (ci - sg.cbase);
-                *dst = (p.epi == kEpiAccum ? *dst : 0.f) + v[i];
+                float val = v[i];
+                if (sg.mask && sg.x[static_cast<int64_t>(m) * sg.C + (ci - sg.cbase)] <= 0.f) val = 0.f;
+                *dst = (p.epi == kEpiAccum ? *dst : 0.f) + val;
               }
             }
           }

@@ -393,6 +393,7 @@ void Session::build_program() {
         break;
     }
   }
+  fuse_relus();
   if (x_off_ == 0) x_off_ = feat[static_cast<size_t>(input_id_)];
   // the setup allocation of the INPUT layer (first ALLOC X of buffer input_id_)
   for (const Event& e : plan_.events)
@@ -400,6 +401,49 @@ void Session::build_program() {
       x_off_ = e.off;
       break;
     }
+}
+
+// ReLU fusion (bit-identical to running the ACTV kernels):
+//  * FWD: a conv/FC whose only consumer is an ACTV applies max(0, .) in its
+//    epilogue; the ACTV's FWD launches nothing (nothing else reads the
+//    pre-activation values, and the buffer is the same in-place alias).
+//  * BWD: an ACTV whose single incoming gradient plane is written by exactly
+//    one producer step (conv/FC dgrad or pool bwd) that reads the ACTV's
+//    output as its input x gets its mask (x > 0) applied in that producer's
+//    epilogue; the ACTV's BWD launches nothing.
+void Session::fuse_relus() {
+  std::vector<int> fwd_at(static_cast<size_t>(L_), -1), bwd_at(static_cast<size_t>(L_), -1);
+  for (size_t i = 0; i < fwd_.size(); ++i) fwd_at[static_cast<size_t>(fwd_[i].layer)] = static_cast<int>(i);
+  for (size_t i = 0; i < bwd_.size(); ++i) bwd_at[static_cast<size_t>(bwd_[i].layer)] = static_cast<int>(i);
+  for (FwdStep& s : fwd_) {
+    const Node& l = g_.at(s.layer);
+    if (l.kind != Kind::Conv && l.kind != Kind::Fc) continue;
+    const auto& us = g_.users(s.layer);
+    if (us.size() != 1 || g_.at(us[0]).kind != Kind::Actv) continue;
+    const int fa = fwd_at[static_cast<size_t>(us[0])];
+    if (fa < 0) continue;
+    s.relu = true;
+    fwd_[static_cast<size_t>(fa)].skip = true;
+  }
+  // which (producer, plane) steps write each gradient location
+  std::map<u64, std::vector<std::pair<int, int>>> writers;
+  for (size_t i = 0; i < bwd_.size(); ++i)
+    for (size_t j = 0; j < bwd_[i].plane_off.size(); ++j)
+      if (bwd_[i].plane_off[j] != kNoOff) writers[bwd_[i].plane_off[j]].push_back({static_cast<int>(i), static_cast<int>(j)});
+  for (BwdStep& s : bwd_) s.mask_plane.assign(s.plane_off.size(), 0);
+  for (BwdStep& a : bwd_) {
+    if (g_.at(a.layer).kind != Kind::Actv || a.dy_off.size() != 1) continue;
+    auto it = writers.find(a.dy_off[0]);
+    if (it == writers.end() || it->second.size() != 1) continue;
+    const auto [pi, pj] = it->second[0];
+    BwdStep& prod = bwd_[static_cast<size_t>(pi)];
+    const Node& pl = g_.at(prod.layer);
+    if (pl.kind != Kind::Conv && pl.kind != Kind::Fc && pl.kind != Kind::Pool) continue;
+    if (pl.in[static_cast<size_t>(pj)] != a.layer) continue;
+    if (prod.accumulate) continue;
+    prod.mask_plane[static_cast<size_t>(pj)] = 1;
+    a.skip = true;
+  }
 }
 
 // ------------------------------------------------------------- helpers ----
@@ -471,13 +515,14 @@ void Session::run_fwd(const FwdStep& s, float lr) {
   switch (l.kind) {
     case Kind::Conv:
     case Kind::Fc: {
-      const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
+      vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
+      a.relu_out = s.relu ? 1 : 0;
       const float* bias = l.kind == Kind::Fc ? F(s.w_off) + g_.fc_inputs(s.layer) * l.out : nullptr;
       check(vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_), "conv_fprop");
       break;
     }
     case Kind::Actv:
-      check(vdnnk::relu_fwd(F(s.out_off), g_.dims(s.layer).count(), cs_), "relu_fwd");
+      if (!s.skip) check(vdnnk::relu_fwd(F(s.out_off), g_.dims(s.layer).count(), cs_), "relu_fwd");
       break;
     case Kind::Pool: {
       vdnnk::PoolArgs p;
@@ -537,7 +582,8 @@ void Session::run_bwd(const BwdStep& s, float lr) {
     case Kind::Fc: {
       const bool fc = l.kind == Kind::Fc;
       if (!s.plane_off.empty()) {
-        const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off);
+        vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off);
+        for (int i = 0; i < a.nseg; ++i) a.mask_in[i] = s.mask_plane[static_cast<size_t>(i)];
         check(vdnnk::conv_dgrad(a, F(s.w_off), dy, s.accumulate, cs_), "conv_dgrad");
       }
       const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
@@ -570,12 +616,13 @@ void Session::run_bwd(const BwdStep& s, float lr) {
         p.dx[i] = s.plane_off.empty() || s.plane_off[static_cast<size_t>(i)] == kNoOff
                       ? nullptr
                       : F(s.plane_off[static_cast<size_t>(i)]);
+        p.mask_in[i] = s.mask_plane.empty() ? 0 : s.mask_plane[static_cast<size_t>(i)];
       }
       if (!s.plane_off.empty()) check(vdnnk::maxpool_bwd(p, F(s.out_off), dy, cs_), "maxpool_bwd");
       break;
     }
     case Kind::Actv:
-      if (dy)
+      if (dy && !s.skip)
         check(vdnnk::relu_bwd(dy, extra.data(), static_cast<int>(extra.size()), F(s.out_off),
                               g_.dims(s.layer).count(), cs_),
               "relu_bwd");

@@ -47,6 +47,8 @@ struct FwdStep {
   u64 ws_off = 0, ws_bytes = 0;
   std::vector<Transfer> offloads;
   int ev = -1;
+  bool relu = false;  // conv/FC: ReLU of the following ACTV fused into the epilogue
+  bool skip = false;  // ACTV whose ReLU was fused into its producer
 };
 
 struct BwdStep {
@@ -61,6 +63,8 @@ struct BwdStep {
   bool accumulate = false;              // two-buffer fork accumulation
   std::vector<u64> dy_off;              // distinct incoming gradient locations (first = canonical)
   int ev = -1;
+  std::vector<char> mask_plane;         // per input: ReLU backward of that input fused here
+  bool skip = false;                    // ACTV whose backward was fused into its gradient's producer
 };
 
 class Session {
@@ -95,6 +99,7 @@ class Session {
  private:
   float* F(u64 off) const { return reinterpret_cast<float*>(base_ + off); }
   void build_program();
+  void fuse_relus();
   void assign_two_buffer();
   void init_weights();
   void run_fwd(const FwdStep& s, float lr);
