@@ -203,17 +203,21 @@ int pick_bn(int ncols) { return ncols <= 64 ? 64 : 128; }
 
 int wgrad_rows(const ConvParams& p) { return p.vec_in ? p.kh * p.kw * p.nchunk * 32 : p.KK; }
 
-// Split-K factor for WGRAD: minimise waves/split (per-CTA work is ~K/s, the
-// grid runs in ceil(tiles*s / slots) waves of `slots` resident CTAs), at
-// least 8 K blocks per split; ties go to fewer splits (less partial traffic).
-int pick_splits(int tiles, int kblocks, int slots) {
+// Split-K factor for WGRAD from a small time model: the main loop runs in
+// ceil(tiles*s / slots) waves of ceil(kblocks/s) K blocks (~4*BN cycles each
+// at the observed tensor-pipe duty), and every split adds a partial tile
+// written and re-read by the reduce (8 B per output element at HBM speed).
+int pick_splits(int tiles, int kblocks, int slots, int bn, int64_t outputs) {
   int best = 1;
   double best_t = 1e30;
-  const int smax = std::max(1, std::min(128, kblocks / 8));
+  const int smax = std::max(1, std::min(1024, kblocks / 4));
   for (int s = 1; s <= smax; ++s) {
     const double waves = static_cast<double>((static_cast<int64_t>(tiles) * s + slots - 1) / slots);
-    const double t = waves / s + 1e-3 * s;
-    if (t < best_t - 1e-9) {
+    const double kbps = static_cast<double>((kblocks + s - 1) / s);
+    const double t_main = waves * kbps * 4.0 * bn / 1.9e9;
+    const double t_part = s > 1 ? static_cast<double>(s) * static_cast<double>(outputs) * 8.0 / 5e12 : 0.0;
+    const double t = t_main + t_part;
+    if (t < best_t * (1 - 1e-6)) {
       best_t = t;
       best = s;
     }
@@ -269,7 +273,7 @@ size_t conv_wgrad_ws_bytes(const ConvArgs& a) {
   const int tiles = ((M + kBM - 1) / kBM) * ((a.cout + bn - 1) / bn);
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
   const int kblocks = static_cast<int>((P + kBK - 1) / kBK);
-  const int splits = pick_splits(tiles, kblocks, 2 * kNumSms);
+  const int splits = pick_splits(tiles, kblocks, 2 * kNumSms, bn, static_cast<int64_t>(M) * a.cout);
   if (splits <= 1) return 0;
   return static_cast<size_t>(splits) * M * a.cout * sizeof(float);
 }
@@ -307,7 +311,7 @@ cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float l
   p.kblocks = static_cast<int>((P + kBK - 1) / kBK);
   const int bn = pick_bn(a.cout);
   const int tiles = ((p.M + kBM - 1) / kBM) * ((a.cout + bn - 1) / bn);
-  int splits = pick_splits(tiles, p.kblocks, 2 * kNumSms);
+  int splits = pick_splits(tiles, p.kblocks, 2 * kNumSms, bn, static_cast<int64_t>(p.M) * a.cout);
   const size_t per = static_cast<size_t>(p.M) * a.cout * sizeof(float);
   if (ws == nullptr || per == 0) splits = 1;
   else splits = static_cast<int>(std::min<size_t>(splits, ws_bytes / per));
