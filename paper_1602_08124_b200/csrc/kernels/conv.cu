@@ -10,6 +10,12 @@
 
 namespace vdnnk {
 
+bool smallc_eligible(const ConvArgs& a);
+cudaError_t smallc_fprop(const ConvArgs& a, const float* w, float* y, cudaStream_t st);
+size_t smallc_wgrad_ws_bytes(const ConvArgs& a, int* nblocks_out);
+cudaError_t smallc_wgrad(const ConvArgs& a, const float* dy, float* w, float lr, float* dw_out, float* ws,
+                         size_t ws_bytes, cudaStream_t st);
+
 namespace {
 std::atomic<uint64_t> g_launches{0};
 constexpr int kStages = 3;         // 3 x 32 KB (BN=128): two CTAs per SM overlap mainloop and epilogue
@@ -235,6 +241,7 @@ void count_launch(uint64_t k) { g_launches.fetch_add(k); }
 
 cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
                        cudaStream_t st) {
+  if (!accumulate && bias == nullptr && smallc_eligible(a)) return smallc_fprop(a, w, y, st);
   ConvParams p;
   if (!build_common(a, p)) return cudaErrorInvalidValue;
   p.kind = kFprop;
@@ -266,6 +273,7 @@ cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool 
 }
 
 size_t conv_wgrad_ws_bytes(const ConvArgs& a) {
+  if (smallc_eligible(a)) return smallc_wgrad_ws_bytes(a, nullptr);
   ConvParams p;
   if (!build_common(a, p)) return 0;
   const int M = wgrad_rows(p);
@@ -298,6 +306,9 @@ __global__ void wgrad_reduce_kernel(const __grid_constant__ ConvParams p, int sp
 
 cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float lr, float* dw_out, float* ws,
                        size_t ws_bytes, cudaStream_t st) {
+  if (smallc_eligible(a) && ws != nullptr &&
+      ws_bytes >= static_cast<size_t>(a.cout) * a.kh * a.kw * a.c[0] * sizeof(float))
+    return smallc_wgrad(a, dy, w_mut, lr, dw_out, ws, ws_bytes, st);
   ConvParams p;
   if (!build_common(a, p)) return cudaErrorInvalidValue;
   p.kind = kWgrad;

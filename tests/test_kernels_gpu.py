@@ -72,6 +72,9 @@ CASES = [
     (3, 17, 17, [64], 96, 3, 2, 1),           # strided (fprop/wgrad only)
     (2, 10, 10, [48], 36, 5, 1, 2),           # channels not multiples of 32
     (300, 1, 1, [64], 20, 1, 1, 0),           # M spans several tiles of a 1x1 "image"
+    (3, 20, 20, [3], 64, 3, 1, 1),            # VGG-style first layer (small-C SIMT path)
+    (2, 23, 23, [3], 96, 11, 4, 0),           # OverFeat-style first layer, Cout 96
+    (2, 9, 9, [4], 40, 3, 2, 1),              # C = 4, strided, Cout not a multiple of 32
 ]
 
 

@@ -169,12 +169,7 @@ def test_odd_shapes_concat_alias_matches_oracle(kind, precise):
     d = V.static_decision(kind, V.AlgoMode.MemoryOptimal, g, cm)
     s, loss, grads = _run_gpu(g, d, w, images, labels, capacity=64 << 20, grads=True, precise=precise)
     _check(g, w, grads, loss, images, labels, str(kind), precise)
-    if not precise:
-        # single-precision rounding aside, the TF32 path is exactly "truncate
-        # operands to tf32, accumulate in fp32": the truncation-emulating
-        # oracle agrees to ~1e-6 on this shallow net
-        cl, errs = _errs(g, w, grads, loss, images, labels, True)
-        assert max(errs.values()) < 1e-4, errs
+
 
 
 def test_fused_sgd_matches_external_grads():
