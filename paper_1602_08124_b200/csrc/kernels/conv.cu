@@ -3,10 +3,12 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.h"
 #include "tc_conv.cuh"
+#include "tma_maps.h"
 
 namespace vdnnk {
 
@@ -15,12 +17,19 @@ cudaError_t smallc_fprop(const ConvArgs& a, const float* w, float* y, cudaStream
 size_t smallc_wgrad_ws_bytes(const ConvArgs& a, int* nblocks_out);
 cudaError_t smallc_wgrad(const ConvArgs& a, const float* dy, float* w, float lr, float* dw_out, float* ws,
                          size_t ws_bytes, cudaStream_t st);
+bool c3tc_fprop_eligible(const ConvArgs& a);
+bool c3tc_wgrad_eligible(const ConvArgs& a);
+size_t c3tc_wgrad_ws_bytes(const ConvArgs& a);
+cudaError_t c3tc_fprop(const ConvArgs& a, const float* w, float* y, cudaStream_t st);
+cudaError_t c3tc_wgrad(const ConvArgs& a, const float* dy, float* w, float lr, float* dw_out, float* ws,
+                       size_t ws_bytes, cudaStream_t st);
 
 namespace {
 std::atomic<uint64_t> g_launches{0};
 constexpr int kStages = 3;         // 3 x 32 KB (BN=128): two CTAs per SM overlap mainloop and epilogue
 constexpr int kStagesPrecise = 3;
 constexpr int kNumSms = 148;
+constexpr int kStagesWide = 4;     // 4 x 48 KB (BN=256): one CTA per SM
 
 bool build_common(const ConvArgs& a, ConvParams& p) {
   std::memset(&p, 0, sizeof(p));
@@ -75,6 +84,8 @@ bool build_common(const ConvArgs& a, ConvParams& p) {
   return true;
 }
 
+}  // namespace
+
 // ---------------------------------------------------------- tensor maps ---
 using PfnTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -128,9 +139,11 @@ bool encode_out(CUtensorMap* m, const void* base, int64_t rows, int cols) {
   return encode_tiled(m, base, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+namespace {
+
 // Build the maps of the TMA producer (and output); false = cp.async gathers.
 template <int BN>
-bool make_maps(const ConvParams& p, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* tc) {
+bool make_maps(ConvParams& p, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* tc) {
   if (p.nseg != 1 || !p.vec_in || !p.vec_out || p.kh != p.kw) return false;
   const float* x = p.seg[0].x;
   if (p.kind == kFprop) {
@@ -149,6 +162,15 @@ bool make_maps(const ConvParams& p, CUtensorMap* ta, CUtensorMap* tb, CUtensorMa
                        CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
     const int taps = p.kh * p.kw;
+    if (p.C % 32 == 0) {
+      // one load per stage: (32 ci, co, ci-chunk, tap) -> smem [chunk][32 co][32 ci]
+      const cuuint64_t d4[4] = {32, static_cast<cuuint64_t>(p.Cout), static_cast<cuuint64_t>(p.C / 32),
+                                static_cast<cuuint64_t>(taps)};
+      const cuuint64_t s4[3] = {static_cast<cuuint64_t>(taps) * p.C * 4, 128, static_cast<cuuint64_t>(p.C) * 4};
+      const cuuint32_t b4[4] = {32, 32, static_cast<cuuint32_t>(BN / 32), 1};
+      p.tma_b_merged = 1;
+      return encode_tiled(tb, p.w, 4, d4, s4, b4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    }
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.C), static_cast<cuuint64_t>(taps),
                                 static_cast<cuuint64_t>(p.Cout)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.C) * 4, static_cast<cuuint64_t>(taps) * p.C * 4};
@@ -158,10 +180,38 @@ bool make_maps(const ConvParams& p, CUtensorMap* ta, CUtensorMap* tb, CUtensorMa
   if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return false;
   const int64_t P = static_cast<int64_t>(p.N) * p.Ho * p.Wo;
+  if (p.Cout % 32 == 0) {
+    // one load per stage: (32 co, pixel, co-chunk) -> smem [chunk][32 pixels][32 co]
+    const cuuint64_t d3[3] = {32, static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(p.Cout / 32)};
+    const cuuint64_t s3[2] = {static_cast<cuuint64_t>(p.Cout) * 4, 128};
+    const cuuint32_t b3[3] = {32, 32, static_cast<cuuint32_t>(BN / 32)};
+    p.tma_b_merged = 1;
+    return encode_tiled(tb, p.dy, 3, d3, s3, b3, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  }
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.Cout), static_cast<cuuint64_t>(P)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.Cout) * 4};
   const cuuint32_t box[2] = {32, 32};
   return encode_tiled(tb, p.dy, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+}
+
+// Which kinds use BN=256 tiles when the layer is wide enough (bit per kind;
+// VDNN_WIDE_TILES overrides for experiments).
+int wide_mask() {
+  static const int m = [] {
+    const char* e = std::getenv("VDNN_WIDE_TILES");
+    return e ? std::atoi(e) : 7;
+  }();
+  return m;
+}
+bool use_wide(int kind) { return (wide_mask() >> kind) & 1; }
+// wgrad: any layer with >= 256 output channels (split-K keeps the SMs busy);
+// fprop/dgrad: only >= 512 columns with >= 4 waves of wide tiles, so halving
+// the resident CTAs per SM neither starves the grid nor exposes epilogues.
+bool wide_ok(const ConvParams& p) {
+  if (p.Ncols < 256 || !use_wide(p.kind)) return false;
+  if (p.kind == kWgrad) return true;
+  const int64_t tiles = static_cast<int64_t>((p.M + kBM - 1) / kBM) * ((p.Ncols + 255) / 256);
+  return p.Ncols >= 512 && tiles >= 4 * kNumSms;
 }
 
 thread_local bool g_precise = false;
@@ -200,12 +250,19 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
       return launch_bn<64, kStages, false, true>(p, ta, tb, tc, splits, st);
     return launch_bn<64, kStages, false, false>(p, ta, tb, tc, splits, st);
   }
+  if (wide_ok(p) && !g_no_tma && make_maps<256>(p, &ta, &tb, &tc))
+    return launch_bn<256, kStagesWide, false, true>(p, ta, tb, tc, splits, st);
   if (!g_no_tma && make_maps<128>(p, &ta, &tb, &tc))
     return launch_bn<128, kStages, false, true>(p, ta, tb, tc, splits, st);
   return launch_bn<128, kStages, false, false>(p, ta, tb, tc, splits, st);
 }
 
-int pick_bn(int ncols) { return ncols <= 64 ? 64 : 128; }
+// Tile width and resident CTAs the wgrad launch will use (mirrors launch()).
+int pick_bn(int ncols) {
+  if (ncols >= 256 && use_wide(kWgrad) && !g_precise && !g_no_tma) return 256;
+  return ncols <= 64 ? 64 : 128;
+}
+int slots_for(int bn) { return bn > 128 ? kNumSms : 2 * kNumSms; }
 
 int wgrad_rows(const ConvParams& p) { return p.vec_in ? p.kh * p.kw * p.nchunk * 32 : p.KK; }
 
@@ -241,6 +298,7 @@ void count_launch(uint64_t k) { g_launches.fetch_add(k); }
 
 cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
                        cudaStream_t st) {
+  if (!accumulate && bias == nullptr && c3tc_fprop_eligible(a)) return c3tc_fprop(a, w, y, st);
   if (!accumulate && bias == nullptr && smallc_eligible(a)) return smallc_fprop(a, w, y, st);
   ConvParams p;
   if (!build_common(a, p)) return cudaErrorInvalidValue;
@@ -273,7 +331,15 @@ cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool 
 }
 
 size_t conv_wgrad_ws_bytes(const ConvArgs& a) {
-  if (smallc_eligible(a)) return smallc_wgrad_ws_bytes(a, nullptr);
+  if (smallc_eligible(a)) {
+    // either kernel may run (the TF32 / exact-fp32 mode can change per call)
+    size_t b = smallc_wgrad_ws_bytes(a, nullptr);
+    const bool was = g_precise;
+    g_precise = false;
+    if (c3tc_wgrad_eligible(a)) b = std::max(b, c3tc_wgrad_ws_bytes(a));
+    g_precise = was;
+    return b;
+  }
   ConvParams p;
   if (!build_common(a, p)) return 0;
   const int M = wgrad_rows(p);
@@ -281,7 +347,7 @@ size_t conv_wgrad_ws_bytes(const ConvArgs& a) {
   const int tiles = ((M + kBM - 1) / kBM) * ((a.cout + bn - 1) / bn);
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
   const int kblocks = static_cast<int>((P + kBK - 1) / kBK);
-  const int splits = pick_splits(tiles, kblocks, 2 * kNumSms, bn, static_cast<int64_t>(M) * a.cout);
+  const int splits = pick_splits(tiles, kblocks, slots_for(bn), bn, static_cast<int64_t>(M) * a.cout);
   if (splits <= 1) return 0;
   return static_cast<size_t>(splits) * M * a.cout * sizeof(float);
 }
@@ -306,6 +372,9 @@ __global__ void wgrad_reduce_kernel(const __grid_constant__ ConvParams p, int sp
 
 cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float lr, float* dw_out, float* ws,
                        size_t ws_bytes, cudaStream_t st) {
+  if (c3tc_wgrad_eligible(a) && ws != nullptr &&
+      ws_bytes >= static_cast<size_t>(a.cout) * a.kh * a.kw * a.c[0] * sizeof(float))
+    return c3tc_wgrad(a, dy, w_mut, lr, dw_out, ws, ws_bytes, st);
   if (smallc_eligible(a) && ws != nullptr &&
       ws_bytes >= static_cast<size_t>(a.cout) * a.kh * a.kw * a.c[0] * sizeof(float))
     return smallc_wgrad(a, dy, w_mut, lr, dw_out, ws, ws_bytes, st);
@@ -322,7 +391,7 @@ cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float l
   p.kblocks = static_cast<int>((P + kBK - 1) / kBK);
   const int bn = pick_bn(a.cout);
   const int tiles = ((p.M + kBM - 1) / kBM) * ((a.cout + bn - 1) / bn);
-  int splits = pick_splits(tiles, p.kblocks, 2 * kNumSms, bn, static_cast<int64_t>(p.M) * a.cout);
+  int splits = pick_splits(tiles, p.kblocks, slots_for(bn), bn, static_cast<int64_t>(p.M) * a.cout);
   const size_t per = static_cast<size_t>(p.M) * a.cout * sizeof(float);
   if (ws == nullptr || per == 0) splits = 1;
   else splits = static_cast<int>(std::min<size_t>(splits, ws_bytes / per));

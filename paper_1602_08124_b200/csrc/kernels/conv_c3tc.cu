@@ -1,0 +1,473 @@
+// First-layer convolutions on the tensor cores (TF32 mode): C <= 4 input
+// channels and a whole filter window that fits one 32-wide K block
+// (kh*kw*C <= 32, e.g. VGG's 3x3x3 = 27). The im2col row of a pixel is only
+// 27 floats at a 12-byte pixel stride, which TMA cannot address, so threads
+// build the operand rows and the tensor core does the contraction; both
+// kernels are then bound by their one big HBM stream (Y written / dY read).
+//
+//   fprop  Y[p][co] = relu?( sum_k A[p][k] * W[co][k] ),  A[p][k] = im2col(X)
+//          persistent CTAs, 128-pixel tiles: 4 builder warps write A rows
+//          (K-major SWIZZLE_128B) into a 4-stage ring, one thread issues
+//          4 x tcgen05.mma (M=128, N=Cout, K=8) into one of two TMEM
+//          accumulators, 4 epilogue warps drain TMEM -> ReLU -> swizzled smem
+//          -> TMA store, overlapping the next tiles' build and MMA.
+//   wgrad  dW[co][k] = sum_p dY[p][co] * A[p][k]
+//          D[co][k] (M = 128 rows, co < Cout live; N = 32) accumulates over a
+//          contiguous pixel range per CTA: dY tiles arrive by TMA (MN-major
+//          32x32 boxes), eight builder warps each write the A^T rows of every
+//          eighth 32-pixel stage (MN-major SWIZZLE_128B_BASE32B), partials per
+//          CTA are reduced in order (deterministic) with the SGD update fused.
+// The exact-fp32 mode (3xTF32 elsewhere) keeps the SIMT kernels of
+// conv_smallc.cu. FLOPs as the reference counts them:
+// 2*k^2*C*Cout*Ho*Wo*N per pass (cost_model.hpp:100-106).
+#include <algorithm>
+
+#include "kernels.h"
+#include "tc_conv.cuh"
+#include "tma_maps.h"
+
+namespace vdnnk {
+
+bool precise();
+cudaError_t smallc_wgrad_reduce_launch(const float* part, int nparts, int64_t count, float* w, float lr,
+                                       float* dw_out, cudaStream_t st);
+
+namespace {
+
+constexpr int kSms = 148;
+constexpr int kFpStages = 4;
+constexpr int kWgStages = 10;
+
+struct C3Geom {
+  int N, H, W, C, Ho, Wo, Cout, k, stride, pad, KK;
+  int P, HoWo;  // output pixels (host checks P < 2^31)
+};
+
+// Window table (shared memory): element offset of im2col column i relative
+// to the window's top-left input element, and its tap (r, s) for clipping.
+__device__ __forceinline__ void c3_table(const C3Geom& g, int* off, int* rs) {
+  const int i = threadIdx.x;
+  if (i < 32) {
+    if (i < g.KK) {
+      const int tap = i / g.C, c = i - tap * g.C;
+      const int r = tap / g.k, s = tap - r * g.k;
+      off[i] = (r * g.W + s) * g.C + c;
+      rs[i] = r | (s << 8);
+    } else {
+      off[i] = 0;
+      rs[i] = 0;
+    }
+  }
+}
+
+// im2col row of output pixel m: 32 values (columns >= KK and padding -> 0).
+__device__ __forceinline__ void c3_row(const float* __restrict__ x, const C3Geom& g, const int* off, const int* rs,
+                                       int m, float (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = 0.f;
+  if (m >= g.P) return;
+  const int n = m / g.HoWo;
+  const int rem = m - n * g.HoWo;
+  const int oh = rem / g.Wo, ow = rem - oh * g.Wo;
+  const int ih0 = oh * g.stride - g.pad, iw0 = ow * g.stride - g.pad;
+  const int64_t base = ((static_cast<int64_t>(n) * g.H + ih0) * g.W + iw0) * g.C;
+  if (ih0 >= 0 && ih0 + g.k <= g.H && iw0 >= 0 && iw0 + g.k <= g.W) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < g.KK) v[i] = __ldg(x + base + off[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (i < g.KK) {
+        const int ih = ih0 + (rs[i] & 0xff), iw = iw0 + (rs[i] >> 8);
+        if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W) v[i] = __ldg(x + base + off[i]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ fprop ------
+// smem: [B: NB rows x 128 B][A: kFpStages x 16 KB][OUT: 2 x NB/32 x 16 KB][barriers][table]
+// warps 0-3 epilogue, 4-11 builders (two groups of 4 warps taking alternate
+// tiles, one pixel row per thread), 12 MMA (+ TMEM owner). TMEM: 2 x NBP columns.
+constexpr int kFpThreads = 416;
+__global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_kernel(const float* __restrict__ x,
+                                                                   const float* __restrict__ w,
+                                                                   const __grid_constant__ CUtensorMap tma_y,
+                                                                   C3Geom g, int NB, int NBP, int relu) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t sb = base;
+  const uint32_t sa0 = sb + ((NB * 128 + 1023) & ~1023);
+  const uint32_t so = sa0 + kFpStages * 16384;
+  const uint32_t obytes = (NB / 32) * 16384;  // one output staging buffer (double-buffered)
+  const uint32_t bars = so + 2 * obytes;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (kFpStages + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * kFpStages + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * kFpStages + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * kFpStages + 4);
+  int* tab = reinterpret_cast<int*>(smem_raw + (bars + 8u * (2 * kFpStages + 6) - raw));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (g.P + kBM - 1) / kBM;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kFpStages; ++s) {
+      mbar_init(full_bar(s), 128);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  c3_table(g, tab, tab + 32);
+  // weights -> B (row co, K-major swizzled; rows >= Cout and k >= KK are 0)
+  for (int i = threadIdx.x; i < NB * 8; i += blockDim.x) {
+    const int co = i >> 3, j = i & 7;
+    float q[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = j * 4 + e;
+      q[e] = (co < g.Cout && k < g.KK) ? w[static_cast<int64_t>(co) * g.KK + k] : 0.f;
+    }
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(kmaj_addr(sb, co, j)), "f"(q[0]), "f"(q[1]),
+                 "f"(q[2]), "f"(q[3])
+                 : "memory");
+  }
+  fence_proxy_async();
+  if (warp == 12) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(2 * NBP)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  if (warp >= 4 && warp < 12) {
+    // ---------------- builders ----------------
+    const int grp = (warp - 4) >> 2;
+    const int row = (threadIdx.x - 128) & 127;
+    int it = grp;
+    for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += 2 * gridDim.x, it += 2) {
+      const int s = it % kFpStages;
+      if (it >= kFpStages) mbar_wait(empty_bar(s), ((it / kFpStages) & 1) ^ 1);
+      float v[32];
+      c3_row(x, g, tab, tab + 32, tile * kBM + row, v);
+      const uint32_t sa = sa0 + s * 16384;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(kmaj_addr(sa, row, j)), "f"(v[4 * j]),
+                     "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                     : "memory");
+      fence_proxy_async();
+      mbar_arrive(full_bar(s));
+    }
+  } else if (warp == 12) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_tf32(NB, false, false);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int s = it % kFpStages, acc = it & 1;
+        mbar_wait(full_bar(s), (it / kFpStages) & 1);
+        if (it >= 2) mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t sa = sa0 + s * 16384;
+#pragma unroll
+        for (int kk = 0; kk < kBK / 8; ++kk)
+          tc_mma_tf32(tmem + acc * NBP, make_sdesc(sa + kk * 32, 16, 1024, kSw128),
+                      make_sdesc(sb + kk * 32, 16, 1024, kSw128), idesc, kk > 0 ? 1u : 0u);
+        tc_commit(empty_bar(s));
+        tc_commit(tfull_bar(acc));
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue ----------------
+    const int row = warp * 32 + lane;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      // the staging buffer of tile it-2 has been read out by its TMA store
+      if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      const uint32_t ob = so + (it & 1) * obytes;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(tfull_bar(acc), (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + acc * NBP + (static_cast<uint32_t>(warp * 32) << 16);
+      for (int cg = 0; cg < NB / 32; ++cg) {
+        float v[32];
+        tmem_ld32(taddr + cg * 32, v);
+        if (relu) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        const uint32_t rowaddr = ob + cg * 16384 + row * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + (((j ^ (row & 7)) & 7) << 4)),
+                       "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                       : "memory");
+      }
+      tc_fence_before();
+      mbar_arrive(tempty_bar(acc));
+      fence_proxy_async();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 0) {
+        for (int cg = 0; cg < NB / 32; ++cg)
+          if (cg * 32 < g.Cout) tma_store_2d(&tma_y, ob + cg * 16384, cg * 32, tile * kBM, false);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * NBP) : "memory");
+  }
+}
+
+// ------------------------------------------------------------ wgrad ------
+// D[co][k] (M = 128 rows, co < Cout <= 128 live; N = 32 columns = k).
+// smem per stage: [A = dY^T: 4 MN-chunks x 4 KB by one TMA (chunks >= Cout/32 stay 0)]
+//                 [B = im2col^T: 1 MN-chunk x 4 KB, one pixel row per builder lane]
+// warps 0-7 builders (warp w builds stages it = w mod 8; warps < Cout/32 then
+// drain TMEM), warp 8 lane 0 TMA, warp 9 MMA + TMEM.
+constexpr int kWgThreads = 320;
+constexpr uint32_t kWgStage = 16384 + 4096;
+__global__ void __launch_bounds__(kWgThreads, 1) c3tc_wgrad_kernel(const float* __restrict__ x,
+                                                                   const __grid_constant__ CUtensorMap tma_dy,
+                                                                   C3Geom g, int ppb, float* __restrict__ part) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bars = base + kWgStages * kWgStage;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (kWgStages + s); };
+  const uint32_t done_bar = bars + 8u * (2 * kWgStages);
+  const uint32_t tmem_slot = bars + 8u * (2 * kWgStages + 1);
+  int* tab = reinterpret_cast<int*>(smem_raw + (bars + 8u * (2 * kWgStages + 2) - raw));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p_begin = blockIdx.x * ppb;
+  const int p_end = min(p_begin + ppb, g.P);
+  const int nkb = p_end > p_begin ? (p_end - p_begin + kBK - 1) / kBK : 0;
+  const int nchunk = g.Cout / 32;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWgStages; ++s) {
+      mbar_init(full_bar(s), 33);  // the building warp's 32 lanes + the TMA thread's expect_tx arrival
+      mbar_init(empty_bar(s), 1);
+    }
+    mbar_init(done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  c3_table(g, tab, tab + 32);
+  // A chunks >= Cout/32 (M rows the TMA never writes) are zero in every stage
+  const int zbytes = (4 - nchunk) * 4096;
+  for (int s = 0; s < kWgStages; ++s)
+    for (int off = threadIdx.x * 16; off < zbytes; off += blockDim.x * 16)
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + s * kWgStage + nchunk * 4096 + off),
+                   "r"(0)
+                   : "memory");
+  fence_proxy_async();
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(32)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  if (warp < 8) {
+    // ---------------- builders ----------------
+    for (int it = warp; it < nkb; it += 8) {
+      const int s = it % kWgStages;
+      if (it >= kWgStages) mbar_wait(empty_bar(s), ((it / kWgStages) & 1) ^ 1);
+      const int m = p_begin + it * kBK + lane;
+      float v[32];
+      c3_row(x, g, tab, tab + 32, m < p_end ? m : g.P, v);
+      const uint32_t sbb = base + s * kWgStage + 16384;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(mnmaj_addr(sbb, lane, 0, j)), "f"(v[4 * j]),
+                     "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                     : "memory");
+      fence_proxy_async();
+      mbar_arrive(full_bar(s));
+    }
+    // ---------------- epilogue: warp w owns TMEM lanes 32w.. = co ----------------
+    if (warp < nchunk) {
+      mbar_wait_sleep(done_bar, 0);
+      tc_fence_after();
+      float v[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16), v);
+      if (nkb <= 0) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      float* dst = part + (static_cast<int64_t>(blockIdx.x) * g.Cout + warp * 32 + lane) * g.KK;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < g.KK) dst[i] = v[i];
+    }
+  } else if (warp == 8) {
+    // ---------------- TMA producer (dY tiles) ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_dy) : "memory");
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % kWgStages;
+        if (it >= kWgStages) mbar_wait(empty_bar(s), ((it / kWgStages) & 1) ^ 1);
+        mbar_expect_tx(full_bar(s), static_cast<uint32_t>(nchunk * 4096));
+        tma_load_3d(base + s * kWgStage, &tma_dy, full_bar(s), 0, p_begin + it * kBK, 0);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_tf32(32, true, true);
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % kWgStages;
+        mbar_wait(full_bar(s), (it / kWgStages) & 1);
+        tc_fence_after();
+        const uint32_t sa = base + s * kWgStage;
+        const uint32_t sbb = sa + 16384;
+#pragma unroll
+        for (int kk = 0; kk < kBK / 8; ++kk)
+          tc_mma_tf32(tmem, make_sdesc(sa + kk * 1024, 4096, 512, kSw128Base32),
+                      make_sdesc(sbb + kk * 1024, 4096, 512, kSw128Base32), idesc, (it > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(empty_bar(s));
+      }
+      if (nkb > 0)
+        tc_commit(done_bar);
+      else
+        mbar_arrive(done_bar);
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(32) : "memory");
+  }
+}
+
+C3Geom geom_of(const ConvArgs& a) {
+  C3Geom g;
+  g.N = a.n;
+  g.H = a.h;
+  g.W = a.w;
+  g.C = a.c[0];
+  g.Ho = a.ho();
+  g.Wo = a.wo();
+  g.Cout = a.cout;
+  g.k = a.kh;
+  g.stride = a.stride;
+  g.pad = a.pad;
+  g.KK = a.kh * a.kw * a.c[0];
+  g.HoWo = g.Ho * g.Wo;
+  g.P = a.n * g.HoWo;
+  return g;
+}
+
+int pow2_at_least(int v) {
+  int p = 32;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+size_t fprop_smem(int NB) {
+  return 1024 + static_cast<size_t>((NB * 128 + 1023) & ~1023) + kFpStages * 16384 + 2 * (NB / 32) * 16384 + 512;
+}
+size_t wgrad_smem() { return 1024 + static_cast<size_t>(kWgStages) * kWgStage + 512; }
+
+int wgrad_blocks(const C3Geom& g) {
+  // one CTA per SM, at least 256 pixel rows each
+  return std::max(1, std::min(kSms, (g.P + 255) / 256));
+}
+
+bool c3_common(const ConvArgs& a) {
+  const int64_t P = static_cast<int64_t>(a.n) * a.ho() * a.wo();
+  const int64_t X = static_cast<int64_t>(a.n) * a.h * a.w * a.c[0];
+  return !precise() && a.nseg == 1 && a.c[0] <= 4 && a.kh == a.kw && a.kh * a.kw * a.c[0] <= 32 && P > 0 &&
+         P < (int64_t{1} << 31) - kBM && X < (int64_t{1} << 40);
+}
+
+}  // namespace
+
+// TF32 tensor-core eligibility (precise mode stays on the exact SIMT kernels).
+bool c3tc_fprop_eligible(const ConvArgs& a) { return c3_common(a) && a.cout % 4 == 0 && a.cout <= 128; }
+bool c3tc_wgrad_eligible(const ConvArgs& a) { return c3_common(a) && a.cout % 32 == 0 && a.cout <= 128; }
+size_t c3tc_wgrad_ws_bytes(const ConvArgs& a) {
+  const C3Geom g = geom_of(a);
+  return static_cast<size_t>(wgrad_blocks(g)) * g.Cout * g.KK * sizeof(float);
+}
+
+cudaError_t c3tc_fprop(const ConvArgs& a, const float* w, float* y, cudaStream_t st) {
+  const C3Geom g = geom_of(a);
+  if (g.P <= 0) return cudaSuccess;
+  const int NB = (g.Cout + 31) / 32 * 32, NBP = pow2_at_least(NB);
+  alignas(64) CUtensorMap ty;
+  if (!encode_out(&ty, y, g.P, g.Cout)) return cudaErrorInvalidValue;
+  const size_t smem = fprop_smem(NB);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(c3tc_fprop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  const int ntiles = (g.P + kBM - 1) / kBM;
+  const int grid = std::min(kSms, ntiles);
+  c3tc_fprop_kernel<<<grid, kFpThreads, smem, st>>>(a.x[0], w, ty, g, NB, NBP, a.relu_out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t c3tc_wgrad(const ConvArgs& a, const float* dy, float* w, float lr, float* dw_out, float* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  const C3Geom g = geom_of(a);
+  const size_t per = static_cast<size_t>(g.Cout) * g.KK * sizeof(float);
+  int nb = wgrad_blocks(g);
+  if (ws == nullptr || ws_bytes < per) return cudaErrorInvalidValue;
+  nb = static_cast<int>(std::min<size_t>(nb, ws_bytes / per));
+  int ppb = (g.P + nb - 1) / nb;
+  ppb = (ppb + kBK - 1) / kBK * kBK;
+  nb = static_cast<int>((g.P + ppb - 1) / ppb);
+  // dY [P][Cout] as (32 co, pixel, co-chunk): one 32-pixel x NB box per stage, MN-major chunks
+  alignas(64) CUtensorMap tdy;
+  const cuuint64_t d3[3] = {32, static_cast<cuuint64_t>(g.P), static_cast<cuuint64_t>(g.Cout / 32)};
+  const cuuint64_t s3[2] = {static_cast<cuuint64_t>(g.Cout) * 4, 128};
+  const cuuint32_t b3[3] = {32, 32, static_cast<cuuint32_t>(g.Cout / 32)};
+  if (!encode_tiled(&tdy, dy, 3, d3, s3, b3, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
+  const size_t smem = wgrad_smem();
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(c3tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  c3tc_wgrad_kernel<<<nb, kWgThreads, smem, st>>>(a.x[0], tdy, g, ppb, ws);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return smallc_wgrad_reduce_launch(ws, nb, static_cast<int64_t>(g.Cout) * g.KK, w, lr, dw_out, st);
+}
+
+}  // namespace vdnnk

@@ -197,6 +197,14 @@ __global__ void smallc_wgrad_reduce(const float* __restrict__ part, int nparts, 
   }
 }
 
+cudaError_t smallc_wgrad_reduce_launch(const float* part, int nparts, int64_t count, float* w, float lr,
+                                       float* dw_out, cudaStream_t st) {
+  smallc_wgrad_reduce<<<static_cast<int>(std::min<int64_t>((count + 255) / 256, 1184)), 256, 0, st>>>(
+      part, nparts, count, w, lr, dw_out);
+  count_launch();
+  return cudaGetLastError();
+}
+
 bool smallc_eligible(const ConvArgs& a) { return a.nseg == 1 && a.c[0] <= 4 && a.cout >= 1 && a.kh == a.kw; }
 
 size_t smallc_fprop_smem(const ConvArgs& a) {

@@ -68,6 +68,7 @@ struct ConvParams {
   Chunk chunk[kMaxChunks];
   int vec_in;                 // every segment C % 4 == 0: 16-B gathers over input channels
   int vec_out;                // Cout % 4 == 0
+  int tma_b_merged;           // dgrad/wgrad B loaded by one TMA per stage (C or Cout % 32 == 0)
   const float* w;             // weights KRSC
   float* w_mut;               // weights to update in place (SGD epilogue)
   const float* bias;          // FC bias for fprop (may be null)
@@ -147,6 +148,14 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
       "[%2];" ::"r"(dst),
       "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z,
+                                            int w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z), "r"(w)
       : "memory");
 }
 // im2col: coordinates (c, w, h, n) of the first window's top-left corner in
@@ -671,8 +680,10 @@ __device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap
     tma_load_im2col(sa, ta, bar, co0, q.w - padw, q.h - padh, q.n, static_cast<uint16_t>(s),
                     static_cast<uint16_t>(r));
     const int ftap = (p.kh - 1 - r) * p.kw + (p.kw - 1 - s);
-#pragma unroll
-    for (int mc = 0; mc < BN / 32; ++mc) tma_load_3d(sb + mc * 4096, tb, bar, n0 + mc * 32, ftap, co0);
+    if (p.tma_b_merged)
+      tma_load_4d(sb, tb, bar, 0, co0, n0 >> 5, ftap);
+    else
+      for (int mc = 0; mc < BN / 32; ++mc) tma_load_3d(sb + mc * 4096, tb, bar, n0 + mc * 32, ftap, co0);
   } else {
     const int p0 = kb * kBK;
     const Pix q = decode_pix(p0, p.Ho, p.Wo);
@@ -684,13 +695,17 @@ __device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap
       tma_load_im2col(sa + mc * 4096, ta, bar, ck * 32, q.w * p.stride - p.pad, q.h * p.stride - p.pad, q.n,
                       static_cast<uint16_t>(s), static_cast<uint16_t>(r));
     }
-#pragma unroll
-    for (int mc = 0; mc < BN / 32; ++mc) tma_load_2d(sb + mc * 4096, tb, bar, n0 + mc * 32, p0);
+    if (p.tma_b_merged)
+      tma_load_3d(sb, tb, bar, 0, p0, n0 >> 5);
+    else
+      for (int mc = 0; mc < BN / 32; ++mc) tma_load_2d(sb + mc * 4096, tb, bar, n0 + mc * 32, p0);
   }
 }
 
+// BN = 256 tiles (wgrad of wide layers: 43 FLOP per staged byte instead of 32)
+// fill TMEM's 256 columns twice over only at one CTA per SM.
 template <int BN, int STAGES, bool PRECISE, bool TMA>
-__global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__ ConvParams p,
+__global__ void __launch_bounds__(160, (BN > 128 ? 1 : 2)) tc_conv_kernel(const __grid_constant__ ConvParams p,
                                                          const __grid_constant__ CUtensorMap tma_a,
                                                          const __grid_constant__ CUtensorMap tma_b,
                                                          const __grid_constant__ CUtensorMap tma_c) {
@@ -756,7 +771,8 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
       }
       __syncwarp();
     }
-    for (int it = 0; !TMA && it < nkb; ++it) {
+    if constexpr (!TMA)
+    for (int it = 0; it < nkb; ++it) {
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;
       if (it >= STAGES) mbar_wait(empty_bar(s), ph ^ 1);
@@ -879,15 +895,18 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
         }
         if (p.vec_out && nb + 32 <= p.Cout) {
+          if (p.epi == kEpiAccum) {
+            float4 a[8];  // loads in flight together, then the stores
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            if (p.epi == kEpiAccum) {
-              const float4 a = *reinterpret_cast<const float4*>(dst + i);
-              o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
+            for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4*>(dst + 4 * i);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              v[4 * i] += a[i].x; v[4 * i + 1] += a[i].y; v[4 * i + 2] += a[i].z; v[4 * i + 3] += a[i].w;
             }
-            *reinterpret_cast<float4*>(dst + i) = o;
           }
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
@@ -908,15 +927,18 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
               if (i < c.valid) v[i] = xr[i] > 0.f ? v[i] : 0.f;
           }
           if (c.valid == 32) {
+            if (p.epi == kEpiAccum) {
+              float4 a[8];
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-              if (p.epi == kEpiAccum) {
-                const float4 a = *reinterpret_cast<const float4*>(dst + i);
-                o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
+              for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4*>(dst + 4 * i);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                v[4 * i] += a[i].x; v[4 * i + 1] += a[i].y; v[4 * i + 2] += a[i].z; v[4 * i + 3] += a[i].w;
               }
-              *reinterpret_cast<float4*>(dst + i) = o;
             }
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
@@ -949,12 +971,16 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
           const int widx = wgrad_widx(p, m, valid);
           if (!valid) continue;
           if (p.epi == kEpiSgd) {
+            // all 32 loads in flight before the stores (the stores may alias
+            // later loads as far as the compiler knows, which would serialise
+            // 32 DRAM round trips per thread)
+            float* wcol = p.w_mut + static_cast<int64_t>(nb) * p.KK + widx;
+            float wv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) wv[i] = (nb + i < p.Cout) ? wcol[static_cast<int64_t>(i) * p.KK] : 0.f;
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (nb + i < p.Cout) {
-                float* w = p.w_mut + static_cast<int64_t>(nb + i) * p.KK + widx;
-                *w -= p.lr * v[i];
-              }
+              if (nb + i < p.Cout) wcol[static_cast<int64_t>(i) * p.KK] = wv[i] - p.lr * v[i];
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
@@ -966,8 +992,6 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
     }
   } else if (warp == 4) {
     // ---------------- MMA issuer ----------------
-    constexpr bool a_mn_kind_w = true;
-    (void)a_mn_kind_w;
     const bool a_mn = (p.kind == kWgrad);
     const bool b_mn = (p.kind != kFprop);
     const uint32_t idesc = make_idesc_tf32(BN, a_mn, b_mn);
@@ -976,7 +1000,7 @@ __global__ void __launch_bounds__(160, 2) tc_conv_kernel(const __grid_constant__
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
         mbar_wait(full_bar(s), ph);
-        fence_proxy_async();
+        if constexpr (!TMA) fence_proxy_async();  // cp.async/st.shared writes -> async proxy
         tc_fence_after();
         const uint32_t sa = base + s * L::kStage;
         const uint32_t sb = sa + L::kABytes;

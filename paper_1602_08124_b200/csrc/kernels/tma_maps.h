@@ -1,0 +1,15 @@
+// Tensor-map encoders shared by the conv kernels (driver entry points are
+// resolved at run time through cudaGetDriverEntryPoint).
+#pragma once
+#include <cuda.h>
+
+#include <cstdint>
+
+namespace vdnnk {
+bool encode_tiled(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                  const cuuint32_t* box, CUtensorMapSwizzle sw);
+bool encode_im2col(CUtensorMap* m, const void* base, int n, int h, int w, int c, int k, int stride, int pad,
+                   int pixels, CUtensorMapSwizzle sw);
+// 2D [rows][cols] fp32 with 128-row x 32-col SWIZZLE_128B boxes (TMA-store epilogues)
+bool encode_out(CUtensorMap* m, const void* base, int64_t rows, int cols);
+}  // namespace vdnnk

@@ -425,17 +425,22 @@ void Session::fuse_relus() {
     s.relu = true;
     fwd_[static_cast<size_t>(fa)].skip = true;
   }
-  // which (producer, plane) steps write each gradient location
-  std::map<u64, std::vector<std::pair<int, int>>> writers;
-  for (size_t i = 0; i < bwd_.size(); ++i)
-    for (size_t j = 0; j < bwd_[i].plane_off.size(); ++j)
-      if (bwd_[i].plane_off[j] != kNoOff) writers[bwd_[i].plane_off[j]].push_back({static_cast<int>(i), static_cast<int>(j)});
+  // the producer of an ACTV's incoming gradient is the last step before it
+  // (in backward order) that wrote that location: with two-buffer reuse the
+  // same G2 offsets are rewritten by many steps, so "last writer" is the key
   for (BwdStep& s : bwd_) s.mask_plane.assign(s.plane_off.size(), 0);
-  for (BwdStep& a : bwd_) {
+  for (size_t ai = 0; ai < bwd_.size(); ++ai) {
+    BwdStep& a = bwd_[ai];
     if (g_.at(a.layer).kind != Kind::Actv || a.dy_off.size() != 1) continue;
-    auto it = writers.find(a.dy_off[0]);
-    if (it == writers.end() || it->second.size() != 1) continue;
-    const auto [pi, pj] = it->second[0];
+    int pi = -1, pj = -1;
+    for (size_t k = ai; k-- > 0 && pi < 0;)
+      for (size_t j = 0; j < bwd_[k].plane_off.size(); ++j)
+        if (bwd_[k].plane_off[j] == a.dy_off[0]) {
+          pi = static_cast<int>(k);
+          pj = static_cast<int>(j);
+          break;
+        }
+    if (pi < 0) continue;
     BwdStep& prod = bwd_[static_cast<size_t>(pi)];
     const Node& pl = g_.at(prod.layer);
     if (pl.kind != Kind::Conv && pl.kind != Kind::Fc && pl.kind != Kind::Pool) continue;

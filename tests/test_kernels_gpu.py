@@ -75,6 +75,11 @@ CASES = [
     (3, 20, 20, [3], 64, 3, 1, 1),            # VGG-style first layer (small-C SIMT path)
     (2, 23, 23, [3], 96, 11, 4, 0),           # OverFeat-style first layer, Cout 96
     (2, 9, 9, [4], 40, 3, 2, 1),              # C = 4, strided, Cout not a multiple of 32
+    (4, 14, 14, [256], 512, 3, 1, 1),         # wide (BN=256) tiles, several M and N tiles
+    (2, 6, 6, [128], 288, 3, 1, 1),           # wide tiles with a partial second N tile
+    (2, 30, 30, [3], 128, 3, 1, 1),           # first layer on the tensor cores (K = 27 in one block)
+    (4, 17, 17, [2], 32, 3, 2, 1),            # C = 2, strided, Cout 32 (tensor-core first layer)
+    (2, 16, 16, [1], 64, 5, 1, 2),            # C = 1, 5x5 (K = 25)
 ]
 
 
