@@ -306,6 +306,8 @@ size_t vdnn_kernel_conv_wgrad_ws_bytes(const vdnn_conv_desc* d);
 void vdnn_kernel_set_precise(int32_t on);
 /* Calling-thread switch: 1 = TMA producers where eligible (default), 0 = cp.async gathers everywhere. */
 void vdnn_kernel_set_tma(int32_t on);
+/* Measured tcgen05 kind::tf32 ceiling of the current device in TFLOP/s (roofline denominator). */
+vdnn_status vdnn_kernel_tf32_peak(double* tflops);
 vdnn_status vdnn_kernel_maxpool_fwd(const vdnn_conv_desc* d, int32_t window, int32_t stride, float* y, void* stream);
 vdnn_status vdnn_kernel_maxpool_bwd(const vdnn_conv_desc* d, int32_t window, int32_t stride, const float* y,
                                     const float* dy, void* stream);

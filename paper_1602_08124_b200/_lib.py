@@ -138,6 +138,7 @@ def lib() -> C.CDLL:
         _lib.vdnn_kernel_set_precise.argtypes = [C.c_int32]
         _lib.vdnn_kernel_set_tma.restype = None
         _lib.vdnn_kernel_set_tma.argtypes = [C.c_int32]
+        _lib.vdnn_kernel_tf32_peak.argtypes = [C.POINTER(C.c_double)]
         if hasattr(_lib, "vdnn_session_plan"):
             _lib.vdnn_session_plan.restype = C.c_void_p
             _lib.vdnn_session_plan.argtypes = [C.c_void_p]

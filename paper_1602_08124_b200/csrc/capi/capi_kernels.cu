@@ -38,6 +38,10 @@ extern "C" {
 uint64_t vdnn_kernel_launch_count(void) { return vdnnk::launch_count(); }
 void vdnn_kernel_set_precise(int32_t on) { vdnnk::set_precise(on != 0); }
 void vdnn_kernel_set_tma(int32_t on) { vdnnk::set_tma(on != 0); }
+vdnn_status vdnn_kernel_tf32_peak(double* tflops) {
+  if (!tflops) return fail(VDNN_INVALID_ARGUMENT, "null output");
+  return cuda_status(vdnnk::tf32_peak_probe(tflops), "tf32 peak probe");
+}
 
 vdnn_status vdnn_kernel_conv_fprop(const vdnn_conv_desc* d, const float* w, const float* bias, float* y,
                                    void* stream) {

@@ -214,23 +214,46 @@ bool wide_ok(const ConvParams& p) {
   return p.Ncols >= 512 && tiles >= 4 * kNumSms;
 }
 
+// BM = 256 tiles (two M=128 MMAs per K step): bit per kind; VDNN_TALL overrides.
+int tall_mask() {
+  static const int m = [] {
+    const char* e = std::getenv("VDNN_TALL");
+    return e ? std::atoi(e) : 7;
+  }();
+  return m;
+}
+bool tall_deep() {
+  static const bool d = [] {
+    const char* e = std::getenv("VDNN_TALL_DEEP");
+    return e && std::atoi(e) != 0;
+  }();
+  return d;
+}
+// enough tall tiles for at least two waves of one CTA per SM
+bool tall_ok(const ConvParams& p, int bn, int splits) {
+  if (!((tall_mask() >> p.kind) & 1)) return false;
+  if (p.kind == kWgrad && (bn != 256 || static_cast<int64_t>(p.kblocks) * kBK < 100000)) return false;
+  const int64_t tiles = static_cast<int64_t>((p.M + 255) / 256) * ((p.Ncols + bn - 1) / bn) * splits;
+  return tiles >= 2 * kNumSms;
+}
+
 thread_local bool g_precise = false;
 thread_local bool g_no_tma = false;
 
-template <int BN, int STAGES, bool PRECISE, bool TMA>
+template <int BN, int STAGES, bool PRECISE, bool TMA, int BM = kBM>
 cudaError_t launch_bn(const ConvParams& p, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                       int splits, cudaStream_t st) {
-  using L = TcSmem<BN, STAGES, PRECISE>;
+  using L = TcSmem<BN, STAGES, PRECISE, BM>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, STAGES, PRECISE, TMA>,
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, STAGES, PRECISE, TMA, BM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const unsigned tiles = static_cast<unsigned>((p.M + kBM - 1) / kBM) * static_cast<unsigned>((p.Ncols + BN - 1) / BN);
+  const unsigned tiles = static_cast<unsigned>((p.M + BM - 1) / BM) * static_cast<unsigned>((p.Ncols + BN - 1) / BN);
   dim3 grid(tiles, 1, splits);
-  tc_conv_kernel<BN, STAGES, PRECISE, TMA><<<grid, 160, L::kTotal, st>>>(p, ta, tb, tc);
+  tc_conv_kernel<BN, STAGES, PRECISE, TMA, BM><<<grid, 160, L::kTotal, st>>>(p, ta, tb, tc);
   count_launch();
   return cudaGetLastError();
 }
@@ -245,24 +268,45 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
     if (p.Ncols <= 64) return launch_bn<64, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
     return launch_bn<128, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
   }
+  const bool deep = tall_deep();
   if (p.Ncols <= 64) {
-    if (!g_no_tma && make_maps<64>(p, &ta, &tb, &tc))
+    if (!g_no_tma && make_maps<64>(p, &ta, &tb, &tc)) {
+      if (tall_ok(p, 64, splits))
+        return deep ? launch_bn<64, 5, false, true, 256>(p, ta, tb, tc, splits, st)
+                    : launch_bn<64, 2, false, true, 256>(p, ta, tb, tc, splits, st);
       return launch_bn<64, kStages, false, true>(p, ta, tb, tc, splits, st);
+    }
     return launch_bn<64, kStages, false, false>(p, ta, tb, tc, splits, st);
   }
-  if (wide_ok(p) && !g_no_tma && make_maps<256>(p, &ta, &tb, &tc))
+  if (wide_ok(p) && !g_no_tma && make_maps<256>(p, &ta, &tb, &tc)) {
+    if (tall_ok(p, 256, splits)) return launch_bn<256, 3, false, true, 256>(p, ta, tb, tc, splits, st);
     return launch_bn<256, kStagesWide, false, true>(p, ta, tb, tc, splits, st);
-  if (!g_no_tma && make_maps<128>(p, &ta, &tb, &tc))
+  }
+  if (!g_no_tma && make_maps<128>(p, &ta, &tb, &tc)) {
+    if (tall_ok(p, 128, splits))
+      return deep ? launch_bn<128, 4, false, true, 256>(p, ta, tb, tc, splits, st)
+                  : launch_bn<128, 2, false, true, 256>(p, ta, tb, tc, splits, st);
     return launch_bn<128, kStages, false, true>(p, ta, tb, tc, splits, st);
+  }
   return launch_bn<128, kStages, false, false>(p, ta, tb, tc, splits, st);
 }
 
-// Tile width and resident CTAs the wgrad launch will use (mirrors launch()).
-int pick_bn(int ncols) {
-  if (ncols >= 256 && use_wide(kWgrad) && !g_precise && !g_no_tma) return 256;
-  return ncols <= 64 ? 64 : 128;
+// Tile shape and resident CTAs the wgrad launch will use (mirrors launch()).
+struct WCfg {
+  int bn, bm, slots;
+};
+// Tall wgrad tiles pay off only with wide (BN=256) tiles over many pixels
+// (measured: +37% at 56x56x256, neutral at 28x28x512, -5..-20% at 14x14 or
+// with 64/128-wide tiles, where the extra im2col boxes per stage dominate).
+WCfg wgrad_cfg(int ncols, int64_t pixels) {
+  WCfg c;
+  const bool tma = !g_precise && !g_no_tma;
+  c.bn = (ncols >= 256 && use_wide(kWgrad) && tma) ? 256 : (ncols <= 64 ? 64 : 128);
+  c.bm = (tma && ((tall_mask() >> kWgrad) & 1) && c.bn == 256 && pixels >= 100000) ? 256 : kBM;
+  const bool one_per_sm = c.bn > 128 || (c.bm > kBM && tall_deep());
+  c.slots = one_per_sm ? kNumSms : 2 * kNumSms;
+  return c;
 }
-int slots_for(int bn) { return bn > 128 ? kNumSms : 2 * kNumSms; }
 
 int wgrad_rows(const ConvParams& p) { return p.vec_in ? p.kh * p.kw * p.nchunk * 32 : p.KK; }
 
@@ -270,14 +314,14 @@ int wgrad_rows(const ConvParams& p) { return p.vec_in ? p.kh * p.kw * p.nchunk *
 // ceil(tiles*s / slots) waves of ceil(kblocks/s) K blocks (~4*BN cycles each
 // at the observed tensor-pipe duty), and every split adds a partial tile
 // written and re-read by the reduce (8 B per output element at HBM speed).
-int pick_splits(int tiles, int kblocks, int slots, int bn, int64_t outputs) {
+int pick_splits(int tiles, int kblocks, int slots, int work, int64_t outputs) {
   int best = 1;
   double best_t = 1e30;
   const int smax = std::max(1, std::min(1024, kblocks / 4));
   for (int s = 1; s <= smax; ++s) {
     const double waves = static_cast<double>((static_cast<int64_t>(tiles) * s + slots - 1) / slots);
     const double kbps = static_cast<double>((kblocks + s - 1) / s);
-    const double t_main = waves * kbps * 4.0 * bn / 1.9e9;
+    const double t_main = waves * kbps * 4.0 * work / 1.9e9;
     const double t_part = s > 1 ? static_cast<double>(s) * static_cast<double>(outputs) * 8.0 / 5e12 : 0.0;
     const double t = t_main + t_part;
     if (t < best_t * (1 - 1e-6)) {
@@ -343,11 +387,11 @@ size_t conv_wgrad_ws_bytes(const ConvArgs& a) {
   ConvParams p;
   if (!build_common(a, p)) return 0;
   const int M = wgrad_rows(p);
-  const int bn = pick_bn(a.cout);
-  const int tiles = ((M + kBM - 1) / kBM) * ((a.cout + bn - 1) / bn);
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
+  const WCfg c = wgrad_cfg(a.cout, P);
+  const int tiles = ((M + c.bm - 1) / c.bm) * ((a.cout + c.bn - 1) / c.bn);
   const int kblocks = static_cast<int>((P + kBK - 1) / kBK);
-  const int splits = pick_splits(tiles, kblocks, slots_for(bn), bn, static_cast<int64_t>(M) * a.cout);
+  const int splits = pick_splits(tiles, kblocks, c.slots, c.bn * c.bm / kBM, static_cast<int64_t>(M) * a.cout);
   if (splits <= 1) return 0;
   return static_cast<size_t>(splits) * M * a.cout * sizeof(float);
 }
@@ -389,9 +433,9 @@ cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float l
   p.Ncols = a.cout;
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
   p.kblocks = static_cast<int>((P + kBK - 1) / kBK);
-  const int bn = pick_bn(a.cout);
-  const int tiles = ((p.M + kBM - 1) / kBM) * ((a.cout + bn - 1) / bn);
-  int splits = pick_splits(tiles, p.kblocks, slots_for(bn), bn, static_cast<int64_t>(p.M) * a.cout);
+  const WCfg c = wgrad_cfg(a.cout, P);
+  const int tiles = ((p.M + c.bm - 1) / c.bm) * ((a.cout + c.bn - 1) / c.bn);
+  int splits = pick_splits(tiles, p.kblocks, c.slots, c.bn * c.bm / kBM, static_cast<int64_t>(p.M) * a.cout);
   const size_t per = static_cast<size_t>(p.M) * a.cout * sizeof(float);
   if (ws == nullptr || per == 0) splits = 1;
   else splits = static_cast<int>(std::min<size_t>(splits, ws_bytes / per));

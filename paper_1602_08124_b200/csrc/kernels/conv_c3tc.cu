@@ -37,6 +37,7 @@ namespace {
 constexpr int kSms = 148;
 constexpr int kFpStages = 4;
 constexpr int kWgStages = 10;
+constexpr int kPrefetch = 24;  // wgrad: dY stages prefetched into L2 ahead of the ring
 
 struct C3Geom {
   int N, H, W, C, Ho, Wo, Cout, k, stride, pad, KK;
@@ -158,9 +159,9 @@ __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_kernel(const float* 
     int it = grp;
     for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += 2 * gridDim.x, it += 2) {
       const int s = it % kFpStages;
-      if (it >= kFpStages) mbar_wait(empty_bar(s), ((it / kFpStages) & 1) ^ 1);
       float v[32];
-      c3_row(x, g, tab, tab + 32, tile * kBM + row, v);
+      c3_row(x, g, tab, tab + 32, tile * kBM + row, v);  // loads in flight while the stage drains
+      if (it >= kFpStages) mbar_wait(empty_bar(s), ((it / kFpStages) & 1) ^ 1);
       const uint32_t sa = sa0 + s * 16384;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
@@ -296,10 +297,10 @@ __global__ void __launch_bounds__(kWgThreads, 1) c3tc_wgrad_kernel(const float* 
     // ---------------- builders ----------------
     for (int it = warp; it < nkb; it += 8) {
       const int s = it % kWgStages;
-      if (it >= kWgStages) mbar_wait(empty_bar(s), ((it / kWgStages) & 1) ^ 1);
       const int m = p_begin + it * kBK + lane;
       float v[32];
-      c3_row(x, g, tab, tab + 32, m < p_end ? m : g.P, v);
+      c3_row(x, g, tab, tab + 32, m < p_end ? m : g.P, v);  // loads in flight while the stage drains
+      if (it >= kWgStages) mbar_wait(empty_bar(s), ((it / kWgStages) & 1) ^ 1);
       const uint32_t sbb = base + s * kWgStage + 16384;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
@@ -330,6 +331,11 @@ __global__ void __launch_bounds__(kWgThreads, 1) c3tc_wgrad_kernel(const float* 
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_dy) : "memory");
       for (int it = 0; it < nkb; ++it) {
         const int s = it % kWgStages;
+        // warm L2 with the tile kPrefetch stages ahead: the ring's loads then hit L2
+        if (it + kPrefetch < nkb)
+          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(&tma_dy), "r"(0),
+                       "r"(p_begin + (it + kPrefetch) * kBK), "r"(0)
+                       : "memory");
         if (it >= kWgStages) mbar_wait(empty_bar(s), ((it / kWgStages) & 1) ^ 1);
         mbar_expect_tx(full_bar(s), static_cast<uint32_t>(nchunk * 4096));
         tma_load_3d(base + s * kWgStage, &tma_dy, full_bar(s), 0, p_begin + it * kBK, 0);

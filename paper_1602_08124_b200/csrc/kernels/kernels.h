@@ -87,6 +87,8 @@ cudaError_t fill_labels(int32_t* y, size_t n, int classes, uint64_t seed, cudaSt
 // Number of kernel launches issued by the calls above since process start
 // (used by bench.py's gpu_launches claim).
 uint64_t launch_count();
+// Measured TF32 tensor-core ceiling (TFLOP/s) of the current device.
+cudaError_t tf32_peak_probe(double* tflops);
 void count_launch(uint64_t k = 1);
 
 }  // namespace vdnnk

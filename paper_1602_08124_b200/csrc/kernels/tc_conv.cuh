@@ -618,9 +618,9 @@ __device__ __forceinline__ int wgrad_widx(const ConvParams& p, int m, bool& vali
 // tensor core reads from x itself: it truncates to 10 mantissa bits) and the
 // exactly representable residual lo = x - hi kept in a second tile; the
 // accumulator gets A*B + A*B_lo + A_lo*B, i.e. fp32-level products.
-template <int BN, int STAGES, bool PRECISE>
+template <int BN, int STAGES, bool PRECISE, int BM = kBM>
 struct TcSmem {
-  static constexpr int kABytes = kBM * 128;
+  static constexpr int kABytes = BM * 128;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kHalf = kABytes + kBBytes;
   static constexpr int kStage = PRECISE ? 2 * kHalf : kHalf;
@@ -661,24 +661,30 @@ __device__ __forceinline__ void split_lo(uint32_t hi, uint32_t lo, int tid) {
 // (tap, 32-channel) chunk, SWIZZLE_128B_ATOM_32B = MN-major canonical).
 // B: tiled (fprop: W [Cout][KK] K-major; dgrad: W as (Cin, taps, Cout)
 // MN-major chunks; wgrad: dY [P][Cout] MN-major chunks).
-template <int BN>
+template <int BN, int BM>
 __device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap* ta, const CUtensorMap* tb, int m0,
                                           int n0, int kb, uint32_t sa, uint32_t sb, uint32_t bar) {
   if (p.kind == kFprop) {
     const int tap = kb / p.nchunk, ck = kb - tap * p.nchunk;
     const int r = tap / p.kw, s = tap - r * p.kw;
-    const Pix q = decode_pix(m0, p.Ho, p.Wo);
-    tma_load_im2col(sa, ta, bar, ck * 32, q.w * p.stride - p.pad, q.h * p.stride - p.pad, q.n,
-                    static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+#pragma unroll
+    for (int h = 0; h < BM / kBM; ++h) {
+      const Pix q = decode_pix(m0 + h * kBM, p.Ho, p.Wo);
+      tma_load_im2col(sa + h * 16384, ta, bar, ck * 32, q.w * p.stride - p.pad, q.h * p.stride - p.pad, q.n,
+                      static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+    }
     tma_load_2d(sb, tb, bar, tap * p.C + ck * 32, n0);
   } else if (p.kind == kDgrad) {
     const int nck = (p.Cout + 31) >> 5;
     const int tap = kb / nck, co0 = (kb - tap * nck) * 32;
     const int r = tap / p.kw, s = tap - r * p.kw;
     const int padh = p.kh - 1 - p.pad, padw = p.kw - 1 - p.pad;
-    const Pix q = decode_pix(m0, p.H, p.W);
-    tma_load_im2col(sa, ta, bar, co0, q.w - padw, q.h - padh, q.n, static_cast<uint16_t>(s),
-                    static_cast<uint16_t>(r));
+#pragma unroll
+    for (int h = 0; h < BM / kBM; ++h) {
+      const Pix q = decode_pix(m0 + h * kBM, p.H, p.W);
+      tma_load_im2col(sa + h * 16384, ta, bar, co0, q.w - padw, q.h - padh, q.n, static_cast<uint16_t>(s),
+                      static_cast<uint16_t>(r));
+    }
     const int ftap = (p.kh - 1 - r) * p.kw + (p.kw - 1 - s);
     if (p.tma_b_merged)
       tma_load_4d(sb, tb, bar, 0, co0, n0 >> 5, ftap);
@@ -688,7 +694,7 @@ __device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap
     const int p0 = kb * kBK;
     const Pix q = decode_pix(p0, p.Ho, p.Wo);
 #pragma unroll
-    for (int mc = 0; mc < kBM / 32; ++mc) {
+    for (int mc = 0; mc < BM / 32; ++mc) {
       const int vc = (m0 >> 5) + mc;
       const int tap = vc / p.nchunk, ck = vc - tap * p.nchunk;
       const int r = tap / p.kw, s = tap - r * p.kw;
@@ -702,15 +708,21 @@ __device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap
   }
 }
 
-// BN = 256 tiles (wgrad of wide layers: 43 FLOP per staged byte instead of 32)
-// fill TMEM's 256 columns twice over only at one CTA per SM.
-template <int BN, int STAGES, bool PRECISE, bool TMA>
-__global__ void __launch_bounds__(160, (BN > 128 ? 1 : 2)) tc_conv_kernel(const __grid_constant__ ConvParams p,
+// BM x BN output tile per CTA. BM = 256 (TMA path) issues two M=128 MMAs per
+// K step against one B tile, into two TMEM accumulators: 43 (BN=128) or 64
+// (BN=256) FLOP per staged byte instead of 32 / 43, the lever against the L2
+// -> SM fill rate that bounds BM=128 tiles. Two CTAs per SM when the stage
+// ring fits in half the shared memory, else one.
+template <int BN, int STAGES, bool PRECISE, bool TMA, int BM = kBM>
+__global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM>::kTotal <= 116 * 1024 ? 2 : 1))
+    tc_conv_kernel(const __grid_constant__ ConvParams p,
                                                          const __grid_constant__ CUtensorMap tma_a,
                                                          const __grid_constant__ CUtensorMap tma_b,
                                                          const __grid_constant__ CUtensorMap tma_c) {
   extern __shared__ uint8_t smem_raw[];
-  using L = TcSmem<BN, STAGES, PRECISE>;
+  using L = TcSmem<BN, STAGES, PRECISE, BM>;
+  constexpr int kHalves = BM / kBM;
+  constexpr int kTmemCols = BN * kHalves;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   const uint32_t bar_base = base + STAGES * L::kStage;
@@ -726,7 +738,7 @@ __global__ void __launch_bounds__(160, (BN > 128 ? 1 : 2)) tc_conv_kernel(const 
   // linear tile index with the N tiles of one M tile adjacent, so the A
   // (activation) tile is read from DRAM once and re-hit in L2
   const int ntn = (p.Ncols + BN - 1) / BN;
-  const int m0 = static_cast<int>(blockIdx.x / ntn) * kBM;
+  const int m0 = static_cast<int>(blockIdx.x / ntn) * BM;
   const int n0 = static_cast<int>(blockIdx.x % ntn) * BN;
   const int kb_begin = blockIdx.z * p.kb_per_split;
   int kb_end = kb_begin + p.kb_per_split;
@@ -743,7 +755,7 @@ __global__ void __launch_bounds__(160, (BN > 128 ? 1 : 2)) tc_conv_kernel(const 
   }
   if (warp == 4) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
-                 "r"(BN)
+                 "r"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -766,7 +778,7 @@ __global__ void __launch_bounds__(160, (BN > 128 ? 1 : 2)) tc_conv_kernel(const 
           if (it >= STAGES) mbar_wait(empty_bar(s), ph ^ 1);
           const uint32_t sa = base + s * L::kStage;
           mbar_expect_tx(full_bar(s), kBytes);
-          tma_issue<BN>(p, &tma_a, &tma_b, m0, n0, kb_begin + it, sa, sa + L::kABytes, full_bar(s));
+          tma_issue<BN, BM>(p, &tma_a, &tma_b, m0, n0, kb_begin + it, sa, sa + L::kABytes, full_bar(s));
         }
       }
       __syncwarp();
@@ -817,8 +829,10 @@ __global__ void __launch_bounds__(160, (BN > 128 ? 1 : 2)) tc_conv_kernel(const 
     tc_fence_after();
     __syncwarp();
     const int row = warp * 32 + lane;
-    const int m = m0 + row;
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+    for (int h = 0; h < kHalves; ++h) {
+    const int m = m0 + h * kBM + row;
+    const uint32_t taddr = tmem + h * BN + (static_cast<uint32_t>(warp * 32) << 16);
     if (TMA && p.kind != kWgrad) {
       // Stage the 128 x BN tile in the idle pipeline buffers as BN/32
       // SWIZZLE_128B boxes (128 rows x 128 B) and write it with TMA stores
@@ -869,9 +883,11 @@ __global__ void __launch_bounds__(160, (BN > 128 ? 1 : 2)) tc_conv_kernel(const 
       asm volatile("bar.sync 2, 128;" ::: "memory");
       if (threadIdx.x == 0) {
         for (int cg = 0; cg < BN / 32; ++cg)
-          if (n0 + cg * 32 < p.Ncols) tma_store_2d(&tma_c, base + cg * 16384, n0 + cg * 32, m0, p.epi == kEpiAccum);
+          if (n0 + cg * 32 < p.Ncols)
+            tma_store_2d(&tma_c, base + cg * 16384, n0 + cg * 32, m0 + h * kBM, p.epi == kEpiAccum);
         bulk_commit_and_drain();
       }
+      if (kHalves > 1) asm volatile("bar.sync 2, 128;" ::: "memory");  // staging read out before reuse
     } else {
 #pragma unroll 1
     for (int cg = 0; cg < BN / 32; ++cg) {
@@ -990,6 +1006,7 @@ __global__ void __launch_bounds__(160, (BN > 128 ? 1 : 2)) tc_conv_kernel(const 
       }
     }
     }
+    }  // halves
   } else if (warp == 4) {
     // ---------------- MMA issuer ----------------
     const bool a_mn = (p.kind == kWgrad);
@@ -1019,7 +1036,10 @@ __global__ void __launch_bounds__(160, (BN > 128 ? 1 : 2)) tc_conv_kernel(const 
             tc_mma_tf32(tmem, ad, bd + kLo, idesc, 1u);
             tc_mma_tf32(tmem, ad, bd, idesc, 1u);
           } else {
-            tc_mma_tf32(tmem, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+            for (int h = 0; h < kHalves; ++h)  // second M half: A rows 128..255 sit 16 KB above
+              tc_mma_tf32(tmem + h * BN, ad + static_cast<uint64_t>(h * (16384 >> 4)), bd, idesc,
+                          (it > 0 || kk > 0) ? 1u : 0u);
           }
         }
         tc_commit(empty_bar(s));
@@ -1032,7 +1052,7 @@ __global__ void __launch_bounds__(160, (BN > 128 ? 1 : 2)) tc_conv_kernel(const 
   __syncthreads();
   if (warp == 4) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
   }
 }
 
