@@ -172,6 +172,10 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     g = V.build_preset(args.net, args.batch) if args.extra == 0 else V.extend_vgg(args.extra, args.batch)
     cm = V.CostModel()
     cap = args.capacity
+    # "<policy>z": the same plan with zero-value-compressed offload/prefetch
+    compress = policy.endswith("z")
+    if compress:
+        policy = policy[:-1]
     if policy == "dyn":
         sel = V.dynamic_select(g, cap, cm)
         if sel.decision is None:
@@ -189,7 +193,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     if not plan.pass_:
         return {"policy": policy, "label": d.label, "verdict": plan.verdict(), "capacity": cap}
     s = V.Session(g, d, cm, cap, device=device, record_timeline=True, external_grads=world > 1,
-                  precise_fp32=args.precise)
+                  precise_fp32=args.precise, compress_offload=compress)
     dp = DataParallel(s, world, device) if world > 1 else None
 
     def one(want_loss=False):
@@ -203,6 +207,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     torch.cuda.synchronize(device)
     if world > 1:
         torch.distributed.barrier()
+    ts0 = s.transfer_stats()
     l0 = V.kernel_launch_count()
     with sampler_cls(device) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -213,6 +218,8 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         ev1.record(stream)
         ev1.synchronize()
     launches = V.kernel_launch_count() - l0
+    ts1 = s.transfer_stats()
+    wire = {k: (ts1[k] - ts0[k]) // args.steps for k in ts0}
     ms = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms, world, device=f"cuda:{device}")
     imgs = args.batch * world / (ms * 1e-3)
@@ -231,7 +238,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     pre_ms = sum((e.end - e.start) for e in m.events if e.kind == V.EventKind.Prefetch) * 1e-6
     free, total = torch.cuda.mem_get_info(device)
     res = {
-        "policy": policy, "label": d.label, "verdict": "PASS", "capacity_bytes": cap,
+        "policy": policy + ("z" if compress else ""), "label": d.label + (" +zvc" if compress else ""), "verdict": "PASS", "capacity_bytes": cap,
         "images_per_s": round(imgs, 2), "ms_per_step": round(ms, 3), "loss": loss,
         "peak_pool_bytes": plan.max_mem_bytes, "arena_bytes": s.arena_info()["arena_bytes"],
         "device_used_bytes": total - free,
@@ -244,6 +251,10 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         "conv_fc_ms": round(conv_ms, 3), "memory_bound_ms": round(mem_ms, 3),
         "conv_fc_tflops": round(conv_tflops, 1) if conv_tflops else None,
         "gpu_launches": launches, "clocks": clk.summary(),
+        "transfer": "zero-value-compressed via SMs (zero-copy)" if compress else "cudaMemcpyAsync (copy engines)",
+        "offload_wire_bytes_per_iter": wire["offload_wire"], "prefetch_wire_bytes_per_iter": wire["prefetch_wire"],
+        "wire_ratio": round((wire["offload_wire"] + wire["prefetch_wire"]) /
+                            max(1, wire["offload_planned"] + wire["prefetch_planned"]), 4),
         "signature": plan.signature(),
     }
     if want_e2e:
@@ -343,7 +354,8 @@ def main():
     ap.add_argument("--extra", type=int, default=0, help="extend_vgg extra conv layers (400 -> VGG-416)")
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--capacity", type=int, default=GIB12)
-    ap.add_argument("--policies", default="dyn,all,conv,none")
+    ap.add_argument("--policies", default="dyn,dynz,all,conv,none",
+                    help="dyn/all/conv/none; a trailing z = same plan with compressed offload")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--precise", action="store_true", help="3xTF32 fp32-accurate contractions")
     ap.add_argument("--cpu-sample-batch", type=int, default=2)
@@ -406,6 +418,13 @@ def main():
         line["slowdown_vs_no_offload"] = round(results["none"]["ms_per_step"] and
                                                head["ms_per_step"] / results["none"]["ms_per_step"], 4)
     line["policies"] = pol
+    if "dynz" in results and results["dynz"].get("images_per_s"):
+        z = results["dynz"]
+        line["compressed_offload"] = {
+            "policy": "vDNN_dyn, same plan, zero-value-compressed offload/prefetch (lossless, bit-identical)",
+            "images_per_s": z["images_per_s"], "ms_per_step": z["ms_per_step"], "wire_ratio": z.get("wire_ratio"),
+            "speedup_vs_copy_engines": round(z["images_per_s"] / head["images_per_s"], 3)
+            if head.get("images_per_s") else None}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         base, _ = cpu_baseline_sample(args)
         line["cpu_baseline"] = base

@@ -244,6 +244,7 @@ typedef struct vdnn_session_options {
   int32_t record_timeline;   /* 1: record CUDA events per op for a measured report */
   int32_t host_arena;        /* 1: pinned host arena for offloads (required when the plan offloads) */
   int32_t precise_fp32;      /* 1: conv/FC contractions as 3xTF32 (fp32-accurate); 0: TF32 */
+  int32_t compress_offload;  /* 1: offload/prefetch through the SMs in lossless zero-value-compressed form */
 } vdnn_session_options;
 void vdnn_session_options_default(vdnn_session_options* o);
 
@@ -271,6 +272,9 @@ vdnn_status vdnn_session_read_feature(vdnn_session* s, int32_t owner, float* hos
 vdnn_status vdnn_session_measured_report(vdnn_session* s, vdnn_report** out);
 /* Per-layer measured FWD/BWD milliseconds of the last step (needs record_timeline). */
 vdnn_status vdnn_session_layer_times(vdnn_session* s, int32_t n_layers, double* fwd_ms, double* bwd_ms);
+/* Cumulative host-link bytes since creation: wire (what crossed PCIe) and planned (raw) per direction. Syncs. */
+vdnn_status vdnn_session_transfer_stats(vdnn_session* s, uint64_t* offload_wire, uint64_t* prefetch_wire,
+                                        uint64_t* offload_planned, uint64_t* prefetch_planned);
 /* Gradient arena (external_grads=1): device pointer and float count of layer's dW (or 0). */
 vdnn_status vdnn_session_grad_buffer(vdnn_session* s, int32_t layer, void** dev_ptr, size_t* count);
 /* Copy layer's dW (+bias grad for FC) from the gradient arena to host (external_grads=1). */
@@ -306,6 +310,13 @@ size_t vdnn_kernel_conv_wgrad_ws_bytes(const vdnn_conv_desc* d);
 void vdnn_kernel_set_precise(int32_t on);
 /* Calling-thread switch: 1 = TMA producers where eligible (default), 0 = cp.async gathers everywhere. */
 void vdnn_kernel_set_tma(int32_t on);
+/* Lossless zero-value-compressed copy between a device buffer and a mapped pinned host buffer
+   (device-accessible pointer, >= vdnn_kernel_zvc_slot_bytes(4*count) bytes); count % 4 == 0, 16-B aligned.
+   wire (device u64 counter, may be NULL for decompress) accumulates the bytes moved. */
+uint64_t vdnn_kernel_zvc_slot_bytes(uint64_t bytes);
+vdnn_status vdnn_kernel_zvc_compress(const float* src, uint64_t count, void* host_dst, uint64_t* wire, void* stream);
+vdnn_status vdnn_kernel_zvc_decompress(const void* host_src, uint64_t count, float* dst, uint64_t* wire,
+                                       void* stream);
 /* Measured tcgen05 kind::tf32 ceiling of the current device in TFLOP/s (roofline denominator). */
 vdnn_status vdnn_kernel_tf32_peak(double* tflops);
 vdnn_status vdnn_kernel_maxpool_fwd(const vdnn_conv_desc* d, int32_t window, int32_t stride, float* y, void* stream);

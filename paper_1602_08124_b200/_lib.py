@@ -111,6 +111,7 @@ class SessionOptions(C.Structure):
     _fields_ = [
         ("device", C.c_int32), ("weight_seed", C.c_uint64), ("external_grads", C.c_int32),
         ("record_timeline", C.c_int32), ("host_arena", C.c_int32), ("precise_fp32", C.c_int32),
+        ("compress_offload", C.c_int32),
     ]
 
 
@@ -139,6 +140,10 @@ def lib() -> C.CDLL:
         _lib.vdnn_kernel_set_tma.restype = None
         _lib.vdnn_kernel_set_tma.argtypes = [C.c_int32]
         _lib.vdnn_kernel_tf32_peak.argtypes = [C.POINTER(C.c_double)]
+        _lib.vdnn_kernel_zvc_slot_bytes.restype = C.c_uint64
+        _lib.vdnn_kernel_zvc_slot_bytes.argtypes = [C.c_uint64]
+        _lib.vdnn_kernel_zvc_compress.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.vdnn_kernel_zvc_decompress.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
         if hasattr(_lib, "vdnn_session_plan"):
             _lib.vdnn_session_plan.restype = C.c_void_p
             _lib.vdnn_session_plan.argtypes = [C.c_void_p]

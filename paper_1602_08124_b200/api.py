@@ -724,7 +724,11 @@ class Session:
 
     def __init__(self, g: NetworkGraph, decision: PolicyDecision, cost: Optional[CostModel] = None,
                  capacity: int = 12884901888, device: int = 0, weight_seed: int = 5000,
-                 external_grads: bool = False, record_timeline: bool = False, precise_fp32: bool = False):
+                 external_grads: bool = False, record_timeline: bool = False, precise_fp32: bool = False,
+                 compress_offload: bool = False):
+        """compress_offload: move offloads/prefetches through the SMs in a
+        lossless zero-value-compressed form (same schedule, bit-identical
+        restored buffers, fewer bytes on the host link)."""
         self.graph = g
         self.decision = decision
         self.cost = cost or CostModel()
@@ -736,6 +740,7 @@ class Session:
         opt.external_grads = int(external_grads)
         opt.record_timeline = int(record_timeline)
         opt.precise_fp32 = int(precise_fp32)
+        opt.compress_offload = int(compress_offload)
         d = decision._handle(g)
         c = self.cost._c()
         h = C.c_void_p()
@@ -755,6 +760,14 @@ class Session:
         _call("vdnn_session_arena_info", self.handle, C.byref(a), C.byref(lo), C.byref(hb), C.byref(sb))
         return {"arena_bytes": a.value, "arena_base_offset": lo.value, "host_arena_bytes": hb.value,
                 "scratch_bytes": sb.value}
+
+    def transfer_stats(self) -> Dict[str, int]:
+        """Cumulative host-link bytes since creation: what crossed PCIe (wire)
+        and what the plan moved (planned), per direction."""
+        v = [C.c_uint64() for _ in range(4)]
+        _call("vdnn_session_transfer_stats", self.handle, *[C.byref(x) for x in v])
+        return {"offload_wire": v[0].value, "prefetch_wire": v[1].value, "offload_planned": v[2].value,
+                "prefetch_planned": v[3].value}
 
     def set_batch(self, images, labels) -> None:
         """Host arrays: images float32 NHWC [N,H,W,C] (C-contiguous), labels int32 [N]."""

@@ -38,6 +38,24 @@ extern "C" {
 uint64_t vdnn_kernel_launch_count(void) { return vdnnk::launch_count(); }
 void vdnn_kernel_set_precise(int32_t on) { vdnnk::set_precise(on != 0); }
 void vdnn_kernel_set_tma(int32_t on) { vdnnk::set_tma(on != 0); }
+uint64_t vdnn_kernel_zvc_slot_bytes(uint64_t bytes) { return vdnnk::zvc_slot_bytes(bytes); }
+vdnn_status vdnn_kernel_zvc_compress(const float* src, uint64_t count, void* host_dst, uint64_t* wire, void* stream) {
+  if (!src || !host_dst || !wire) return fail(VDNN_INVALID_ARGUMENT, "null argument");
+  if (!vdnnk::zvc_eligible(src, count * 4) || !vdnnk::zvc_eligible(host_dst, 16))
+    return fail(VDNN_INVALID_ARGUMENT, "zvc needs count % 4 == 0 and 16-B aligned buffers");
+  return cuda_status(vdnnk::zvc_compress(src, count, host_dst, reinterpret_cast<unsigned long long*>(wire),
+                                         static_cast<cudaStream_t>(stream)),
+                     "zvc_compress");
+}
+vdnn_status vdnn_kernel_zvc_decompress(const void* host_src, uint64_t count, float* dst, uint64_t* wire,
+                                       void* stream) {
+  if (!host_src || !dst) return fail(VDNN_INVALID_ARGUMENT, "null argument");
+  if (!vdnnk::zvc_eligible(dst, count * 4) || !vdnnk::zvc_eligible(host_src, 16))
+    return fail(VDNN_INVALID_ARGUMENT, "zvc needs count % 4 == 0 and 16-B aligned buffers");
+  return cuda_status(vdnnk::zvc_decompress(host_src, count, dst, reinterpret_cast<unsigned long long*>(wire),
+                                           static_cast<cudaStream_t>(stream)),
+                     "zvc_decompress");
+}
 vdnn_status vdnn_kernel_tf32_peak(double* tflops) {
   if (!tflops) return fail(VDNN_INVALID_ARGUMENT, "null output");
   return cuda_status(vdnnk::tf32_peak_probe(tflops), "tf32 peak probe");

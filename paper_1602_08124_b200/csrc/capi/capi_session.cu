@@ -47,6 +47,7 @@ void vdnn_session_options_default(vdnn_session_options* o) {
   o->record_timeline = 0;
   o->host_arena = 1;
   o->precise_fp32 = 0;
+  o->compress_offload = 0;
 }
 
 vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, const vdnn_cost_model* cm,
@@ -61,6 +62,7 @@ vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, con
       o.record_timeline = opt->record_timeline != 0;
       o.host_arena = opt->host_arena != 0;
       o.precise = opt->precise_fp32 != 0;
+      o.compress_offload = opt->compress_offload != 0;
     }
     if (!g->net.finalized()) throw vdnnp::PlanError(vdnnp::Err::Generic, "graph is not finalized");
     auto* s = new vdnnrt::Session(g->net, d->d, vdnncapi::cost_from(cm), capacity, o);
@@ -148,6 +150,13 @@ vdnn_status vdnn_session_layer_times(vdnn_session* s, int32_t n, double* fwd_ms,
   return guard([&] {
     S(s).synchronize();
     S(s).layer_times(n, fwd_ms, bwd_ms);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_transfer_stats(vdnn_session* s, uint64_t* offload_wire, uint64_t* prefetch_wire,
+                                        uint64_t* offload_planned, uint64_t* prefetch_planned) {
+  return guard([&] {
+    S(s).transfer_stats(offload_wire, prefetch_wire, offload_planned, prefetch_planned);
     return VDNN_OK;
   });
 }

@@ -87,6 +87,17 @@ cudaError_t fill_labels(int32_t* y, size_t n, int classes, uint64_t seed, cudaSt
 // Number of kernel launches issued by the calls above since process start
 // (used by bench.py's gpu_launches claim).
 uint64_t launch_count();
+// Zero-value-compressed transfer between a device buffer and a (zero-copy
+// mapped) pinned host slot; lossless, see zvc.cu for the format. `count`
+// floats (multiple of 4, 16-B aligned); `wire` (device counter, may be null
+// for decompress) accumulates the bytes that crossed the link.
+constexpr int kZvcChunk = 1024;
+constexpr int kZvcSlot = 128 + 4 * kZvcChunk;
+uint64_t zvc_slot_bytes(uint64_t bytes);
+bool zvc_eligible(const void* p, uint64_t bytes);
+cudaError_t zvc_compress(const float* src, uint64_t count, void* host_dst, unsigned long long* wire, cudaStream_t st);
+cudaError_t zvc_decompress(const void* host_src, uint64_t count, float* dst, unsigned long long* wire,
+                           cudaStream_t st);
 // Measured TF32 tensor-core ceiling (TFLOP/s) of the current device.
 cudaError_t tf32_peak_probe(double* tflops);
 void count_launch(uint64_t k = 1);

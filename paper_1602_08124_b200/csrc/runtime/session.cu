@@ -94,12 +94,22 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
   for (const Event& e : plan_.events)
     if (e.kind == Ev::Offload && host_slot_[static_cast<size_t>(e.buffer)] == kNoOff) {
       host_slot_[static_cast<size_t>(e.buffer)] = host_bytes_;
-      host_bytes_ += round_up(e.bytes, 4096);
+      // compressed mode: a slot holds the worst case (every chunk dense + its mask)
+      host_bytes_ += round_up(o_.compress_offload ? std::max<u64>(e.bytes, vdnnk::zvc_slot_bytes(e.bytes)) : e.bytes,
+                              4096);
     }
   if (host_bytes_ > 0) {
     if (!o_.host_arena) throw PlanError(Err::Config, "plan offloads but the host arena is disabled");
-    check(cudaHostAlloc(&host_, host_bytes_, cudaHostAllocDefault), "cudaHostAlloc(host arena)");
+    check(cudaHostAlloc(&host_, host_bytes_, o_.compress_offload ? cudaHostAllocMapped : cudaHostAllocDefault),
+          "cudaHostAlloc(host arena)");
+    if (o_.compress_offload) {
+      void* dv = nullptr;
+      check(cudaHostGetDevicePointer(&dv, host_, 0), "cudaHostGetDevicePointer(host arena)");
+      host_dev_ = static_cast<char*>(dv);
+    }
   }
+  check(cudaMalloc(&wire_, 2 * sizeof(unsigned long long)), "cudaMalloc(wire counters)");
+  check(cudaMemsetAsync(wire_, 0, 2 * sizeof(unsigned long long), cs_), "memset wire counters");
 
   // non-pool scratch
   const u64 n = g_.batch();
@@ -172,6 +182,7 @@ Session::~Session() {
   cudaFree(loss_grad_);
   cudaFree(row_loss_);
   cudaFree(loss_);
+  cudaFree(wire_);
   cudaFree(labels_);
   if (pinned_loss_) cudaFreeHost(pinned_loss_);
   if (splitk_) cudaFree(splitk_);
@@ -511,7 +522,13 @@ void Session::run_fwd(const FwdStep& s, float lr) {
     check(cudaStreamWaitEvent(ms_, start, 0), "wait");
     for (const Transfer& t : s.offloads) {
       if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev)], ms_), "record");
-      check(cudaMemcpyAsync(host_ + t.host_off, base_ + t.dev_off, t.bytes, cudaMemcpyDeviceToHost, ms_), "D2H");
+      if (o_.compress_offload && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes))
+        check(vdnnk::zvc_compress(F(t.dev_off), t.bytes / 4, host_dev_ + t.host_off, wire_, ms_), "zvc offload");
+      else {
+        check(cudaMemcpyAsync(host_ + t.host_off, base_ + t.dev_off, t.bytes, cudaMemcpyDeviceToHost, ms_), "D2H");
+        copy_off_ += t.bytes;
+      }
+      raw_off_ += t.bytes;
       if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev) + 1], ms_), "record");
       check(cudaEventRecord(xfer_ev_[static_cast<size_t>(t.ev)], ms_), "record");
     }
@@ -568,7 +585,14 @@ void Session::run_bwd(const BwdStep& s, float lr) {
     check(cudaStreamWaitEvent(ms_, start, 0), "wait");
     for (const Transfer& t : s.prefetches) {
       if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev)], ms_), "record");
-      check(cudaMemcpyAsync(base_ + t.dev_off, host_ + t.host_off, t.bytes, cudaMemcpyHostToDevice, ms_), "H2D");
+      if (o_.compress_offload && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes))
+        check(vdnnk::zvc_decompress(host_dev_ + t.host_off, t.bytes / 4, F(t.dev_off), wire_ + 1, ms_),
+              "zvc prefetch");
+      else {
+        check(cudaMemcpyAsync(base_ + t.dev_off, host_ + t.host_off, t.bytes, cudaMemcpyHostToDevice, ms_), "H2D");
+        copy_pre_ += t.bytes;
+      }
+      raw_pre_ += t.bytes;
       if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev) + 1], ms_), "record");
       check(cudaEventRecord(xfer_ev_[static_cast<size_t>(t.ev)], ms_), "record");
     }
@@ -660,6 +684,16 @@ void Session::step(float lr, float* loss_host) {
     check(cudaStreamSynchronize(cs_), "sync");
     *loss_host = *pinned_loss_;
   }
+}
+
+void Session::transfer_stats(u64* offload_wire, u64* prefetch_wire, u64* offload_raw, u64* prefetch_raw) {
+  synchronize();
+  unsigned long long w[2] = {0, 0};
+  check(cudaMemcpy(w, wire_, sizeof(w), cudaMemcpyDeviceToHost), "wire counters");
+  if (offload_wire) *offload_wire = w[0] + copy_off_;
+  if (prefetch_wire) *prefetch_wire = w[1] + copy_pre_;
+  if (offload_raw) *offload_raw = raw_off_;
+  if (prefetch_raw) *prefetch_raw = raw_pre_;
 }
 
 void Session::synchronize() {

@@ -22,6 +22,10 @@ struct Options {
   bool record_timeline = false;
   bool host_arena = true;
   bool precise = false;  // 3xTF32 contractions
+  // Offload / prefetch through the SMs in zero-value-compressed form
+  // (kernels/zvc.cu) instead of cudaMemcpyAsync; same schedule, same bytes
+  // restored, fewer bytes on the host link.
+  bool compress_offload = false;
 };
 
 // One gradient plane: the slice of a dX buffer that holds the gradient w.r.t.
@@ -93,6 +97,9 @@ class Session {
   u64 arena_bytes() const { return arena_bytes_; }
   u64 arena_lo() const { return arena_lo_; }
   u64 host_bytes() const { return host_bytes_; }
+  // cumulative bytes that crossed the host link (compressed mode: the wire
+  // form; copy mode: the planned bytes)
+  void transfer_stats(u64* offload_wire, u64* prefetch_wire, u64* offload_raw, u64* prefetch_raw);
   u64 scratch_bytes() const { return scratch_bytes_; }
   cudaStream_t stream() const { return cs_; }
 
@@ -123,7 +130,11 @@ class Session {
   char* base_ = nullptr;
   u64 arena_lo_ = 0, arena_bytes_ = 0;
   char* host_ = nullptr;
+  char* host_dev_ = nullptr;  // device view of the mapped host arena (compressed mode)
   u64 host_bytes_ = 0;
+  unsigned long long* wire_ = nullptr;  // [0] offload, [1] prefetch wire bytes (device counters)
+  u64 raw_off_ = 0, raw_pre_ = 0;       // planned bytes issued so far
+  u64 copy_off_ = 0, copy_pre_ = 0;     // of which moved by cudaMemcpyAsync
   std::vector<u64> host_slot_;  // per owner
   u64 scratch_bytes_ = 0;
   float* loss_grad_ = nullptr;
