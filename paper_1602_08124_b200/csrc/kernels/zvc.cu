@@ -16,6 +16,8 @@
 //   f32 vals[nnz]  lane-major (lane 0's nonzeros in (j, e) order, then lane 1's ...)
 // Only 128 + 4*nnz bytes of a slot are written / read; dense chunks cost
 // +3% (the mask), all-zero chunks 128 B.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace vdnnk {
@@ -122,9 +124,17 @@ __global__ void __launch_bounds__(kWarps * 32) zvc_decompress_kernel(const uint8
 // Enough resident warps to keep ~50 GB/s of PCIe requests in flight, few
 // enough (and light enough: 33 KB smem, 256 threads) to co-reside with the
 // conv kernels on the compute stream.
+int zvc_max_grid() {
+  static const int g = [] {
+    const char* e = std::getenv("VDNN_ZVC_GRID");
+    return e ? std::atoi(e) : 32;
+  }();
+  return g;
+}
 int zvc_grid(int64_t nchunks) {
   const int64_t want = (nchunks + kWarps - 1) / kWarps;
-  return static_cast<int>(want < 64 ? (want < 1 ? 1 : want) : 64);
+  const int cap = zvc_max_grid();
+  return static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
 }
 
 }  // namespace

@@ -325,6 +325,7 @@ void Session::build_program() {
         t.dev_off = feat[b];
         t.host_off = host_slot_[b];
         t.ev = xfer++;
+        t.zvc = compressible(e.buffer) && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes);
         fwd_.back().offloads.push_back(t);
         break;
       }
@@ -336,6 +337,7 @@ void Session::build_program() {
         t.dev_off = feat[b];  // the ALLOC logged just before on the memory stream
         t.host_off = host_slot_[b];
         t.ev = xfer++;
+        t.zvc = compressible(e.buffer) && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes);
         pending.push_back(t);
         break;
       }
@@ -412,6 +414,17 @@ void Session::build_program() {
       x_off_ = e.off;
       break;
     }
+}
+
+// Compressed mode moves a buffer through the SMs only when it holds ReLU
+// outputs (its owner feeds an in-place ACTV), about half zeros; dense maps
+// (raw images, max-pool outputs: ~94% nonzero) keep the copy engines, which
+// move dense bytes ~10% faster than SM-driven PCIe stores/loads.
+bool Session::compressible(int owner) const {
+  if (!o_.compress_offload) return false;
+  for (int u : g_.users(owner))
+    if (g_.at(u).kind == Kind::Actv) return true;
+  return false;
 }
 
 // ReLU fusion (bit-identical to running the ACTV kernels):
@@ -522,7 +535,7 @@ void Session::run_fwd(const FwdStep& s, float lr) {
     check(cudaStreamWaitEvent(ms_, start, 0), "wait");
     for (const Transfer& t : s.offloads) {
       if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev)], ms_), "record");
-      if (o_.compress_offload && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes))
+      if (t.zvc)
         check(vdnnk::zvc_compress(F(t.dev_off), t.bytes / 4, host_dev_ + t.host_off, wire_, ms_), "zvc offload");
       else {
         check(cudaMemcpyAsync(host_ + t.host_off, base_ + t.dev_off, t.bytes, cudaMemcpyDeviceToHost, ms_), "D2H");
@@ -585,7 +598,7 @@ void Session::run_bwd(const BwdStep& s, float lr) {
     check(cudaStreamWaitEvent(ms_, start, 0), "wait");
     for (const Transfer& t : s.prefetches) {
       if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev)], ms_), "record");
-      if (o_.compress_offload && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes))
+      if (t.zvc)
         check(vdnnk::zvc_decompress(host_dev_ + t.host_off, t.bytes / 4, F(t.dev_off), wire_ + 1, ms_),
               "zvc prefetch");
       else {

@@ -41,6 +41,7 @@ struct Transfer {
   u64 dev_off = 0;  // pool offset of the device extent
   u64 host_off = 0;
   int ev = -1;      // timing event pair index
+  bool zvc = false; // compressed mode and the buffer holds ReLU outputs (sparse)
 };
 
 struct FwdStep {
@@ -107,6 +108,7 @@ class Session {
   float* F(u64 off) const { return reinterpret_cast<float*>(base_ + off); }
   void build_program();
   void fuse_relus();
+  bool compressible(int owner) const;
   void assign_two_buffer();
   void init_weights();
   void run_fwd(const FwdStep& s, float lr);
