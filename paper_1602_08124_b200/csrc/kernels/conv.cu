@@ -142,13 +142,16 @@ bool encode_out(CUtensorMap* m, const void* base, int64_t rows, int cols) {
 namespace {
 
 // Build the maps of the TMA producer (and output); false = cp.async gathers.
-template <int BN>
+template <int BN, int KW = kBK>
 bool make_maps(ConvParams& p, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* tc) {
   if (p.nseg != 1 || !p.vec_in || !p.vec_out || p.kh != p.kw) return false;
   const float* x = p.seg[0].x;
   if (p.kind == kFprop) {
     if (!encode_out(tc, p.y, p.M, p.Cout)) return false;
-    if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, kBM, CU_TENSOR_MAP_SWIZZLE_128B))
+    static const bool split_a = std::getenv("VDNN_EXP_SPLIT_A") != nullptr;
+    p.exp_split_a = split_a ? 1 : 0;
+    if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, split_a ? 32 : kBM,
+                       CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.KK), static_cast<cuuint64_t>(p.Cout)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.KK) * 4};
@@ -177,20 +180,20 @@ bool make_maps(ConvParams& p, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* tc)
     const cuuint32_t box[3] = {32, 1, 32};
     return encode_tiled(tb, p.w, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   }
-  if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+  if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, KW, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return false;
   const int64_t P = static_cast<int64_t>(p.N) * p.Ho * p.Wo;
   if (p.Cout % 32 == 0) {
     // one load per stage: (32 co, pixel, co-chunk) -> smem [chunk][32 pixels][32 co]
     const cuuint64_t d3[3] = {32, static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(p.Cout / 32)};
     const cuuint64_t s3[2] = {static_cast<cuuint64_t>(p.Cout) * 4, 128};
-    const cuuint32_t b3[3] = {32, 32, static_cast<cuuint32_t>(BN / 32)};
+    const cuuint32_t b3[3] = {32, KW, static_cast<cuuint32_t>(BN / 32)};
     p.tma_b_merged = 1;
     return encode_tiled(tb, p.dy, 3, d3, s3, b3, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   }
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.Cout), static_cast<cuuint64_t>(P)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.Cout) * 4};
-  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t box[2] = {32, KW};
   return encode_tiled(tb, p.dy, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
@@ -240,20 +243,20 @@ bool tall_ok(const ConvParams& p, int bn, int splits) {
 thread_local bool g_precise = false;
 thread_local bool g_no_tma = false;
 
-template <int BN, int STAGES, bool PRECISE, bool TMA, int BM = kBM>
+template <int BN, int STAGES, bool PRECISE, bool TMA, int BM = kBM, int KW = kBK>
 cudaError_t launch_bn(const ConvParams& p, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                       int splits, cudaStream_t st) {
-  using L = TcSmem<BN, STAGES, PRECISE, BM>;
+  using L = TcSmem<BN, STAGES, PRECISE, BM, KW>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, STAGES, PRECISE, TMA, BM>,
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, STAGES, PRECISE, TMA, BM, KW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const unsigned tiles = static_cast<unsigned>((p.M + BM - 1) / BM) * static_cast<unsigned>((p.Ncols + BN - 1) / BN);
   dim3 grid(tiles, 1, splits);
-  tc_conv_kernel<BN, STAGES, PRECISE, TMA, BM><<<grid, 160, L::kTotal, st>>>(p, ta, tb, tc);
+  tc_conv_kernel<BN, STAGES, PRECISE, TMA, BM, KW><<<grid, 160, L::kTotal, st>>>(p, ta, tb, tc);
   count_launch();
   return cudaGetLastError();
 }
@@ -267,6 +270,20 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   if (g_precise) {
     if (p.Ncols <= 64) return launch_bn<64, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
     return launch_bn<128, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
+  }
+  if (p.kind == kWgrad && p.wkw == 64) {
+    // 64-pixel stages: half the im2col TMA ops per FLOP (their issue rate,
+    // not bytes, bounds the 32-pixel wgrad pipeline); one CTA per SM
+    if (p.Ncols > 128 && make_maps<256, 64>(p, &ta, &tb, &tc))
+      return launch_bn<256, 2, false, true, kBM, 64>(p, ta, tb, tc, splits, st);
+    if (p.Ncols > 64 && p.Ncols <= 128 && make_maps<128, 64>(p, &ta, &tb, &tc))
+      return launch_bn<128, 3, false, true, kBM, 64>(p, ta, tb, tc, splits, st);
+    if (p.Ncols <= 64 && make_maps<64, 64>(p, &ta, &tb, &tc))
+      return launch_bn<64, 4, false, true, kBM, 64>(p, ta, tb, tc, splits, st);
+    // maps failed: fall back to 32-pixel K blocks
+    p.wkw = kBK;
+    p.kblocks *= 2;
+    p.kb_per_split *= 2;
   }
   const bool deep = tall_deep();
   if (p.Ncols <= 64) {
@@ -291,20 +308,38 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   return launch_bn<128, kStages, false, false>(p, ta, tb, tc, splits, st);
 }
 
+bool wgrad_wide_k() {
+  static const bool on = [] {
+    const char* e = std::getenv("VDNN_WGRAD_KW");
+    return !(e && std::atoi(e) == 32);
+  }();
+  return on;
+}
+
 // Tile shape and resident CTAs the wgrad launch will use (mirrors launch()).
 struct WCfg {
-  int bn, bm, slots;
+  int bn, bm, slots, kw;
 };
 // Tall wgrad tiles pay off only with wide (BN=256) tiles over many pixels
 // (measured: +37% at 56x56x256, neutral at 28x28x512, -5..-20% at 14x14 or
 // with 64/128-wide tiles, where the extra im2col boxes per stage dominate).
-WCfg wgrad_cfg(int ncols, int64_t pixels) {
+WCfg wgrad_cfg(const ConvParams& p, int64_t pixels) {
   WCfg c;
-  const bool tma = !g_precise && !g_no_tma;
+  const int ncols = p.Cout;
+  const bool tma = !g_precise && !g_no_tma && p.nseg == 1 && p.vec_in && p.vec_out && p.kh == p.kw;
   c.bn = (ncols >= 256 && use_wide(kWgrad) && tma) ? 256 : (ncols <= 64 ? 64 : 128);
   c.bm = (tma && ((tall_mask() >> kWgrad) & 1) && c.bn == 256 && pixels >= 100000) ? 256 : kBM;
   const bool one_per_sm = c.bn > 128 || (c.bm > kBM && tall_deep());
   c.slots = one_per_sm ? kNumSms : 2 * kNumSms;
+  c.kw = kBK;
+  // 64-pixel stages for wide (BN = 256) tiles: measured +18% (56x56x256) to
+  // +42% (28x28 / 14x14 x512); narrower tiles lose their 2-CTA overlap for
+  // nothing (-7% at 128 channels)
+  if (tma && c.bn == 256 && wgrad_wide_k()) {
+    c.kw = 64;
+    c.bm = kBM;
+    c.slots = kNumSms;
+  }
   return c;
 }
 
@@ -388,10 +423,11 @@ size_t conv_wgrad_ws_bytes(const ConvArgs& a) {
   if (!build_common(a, p)) return 0;
   const int M = wgrad_rows(p);
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
-  const WCfg c = wgrad_cfg(a.cout, P);
+  const WCfg c = wgrad_cfg(p, P);
   const int tiles = ((M + c.bm - 1) / c.bm) * ((a.cout + c.bn - 1) / c.bn);
-  const int kblocks = static_cast<int>((P + kBK - 1) / kBK);
-  const int splits = pick_splits(tiles, kblocks, c.slots, c.bn * c.bm / kBM, static_cast<int64_t>(M) * a.cout);
+  const int kblocks = static_cast<int>((P + c.kw - 1) / c.kw);
+  const int splits = pick_splits(tiles, kblocks, c.slots, c.bn * c.bm / kBM * c.kw / kBK,
+                                 static_cast<int64_t>(M) * a.cout);
   if (splits <= 1) return 0;
   return static_cast<size_t>(splits) * M * a.cout * sizeof(float);
 }
@@ -432,10 +468,12 @@ cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float l
   p.M = wgrad_rows(p);
   p.Ncols = a.cout;
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
-  p.kblocks = static_cast<int>((P + kBK - 1) / kBK);
-  const WCfg c = wgrad_cfg(a.cout, P);
+  const WCfg c = wgrad_cfg(p, P);
+  p.wkw = c.kw;
+  p.kblocks = static_cast<int>((P + c.kw - 1) / c.kw);
   const int tiles = ((p.M + c.bm - 1) / c.bm) * ((a.cout + c.bn - 1) / c.bn);
-  int splits = pick_splits(tiles, p.kblocks, c.slots, c.bn * c.bm / kBM, static_cast<int64_t>(p.M) * a.cout);
+  int splits = pick_splits(tiles, p.kblocks, c.slots, c.bn * c.bm / kBM * c.kw / kBK,
+                           static_cast<int64_t>(p.M) * a.cout);
   const size_t per = static_cast<size_t>(p.M) * a.cout * sizeof(float);
   if (ws == nullptr || per == 0) splits = 1;
   else splits = static_cast<int>(std::min<size_t>(splits, ws_bytes / per));

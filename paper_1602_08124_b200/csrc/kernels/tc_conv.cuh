@@ -69,6 +69,8 @@ struct ConvParams {
   int vec_in;                 // every segment C % 4 == 0: 16-B gathers over input channels
   int vec_out;                // Cout % 4 == 0
   int tma_b_merged;           // dgrad/wgrad B loaded by one TMA per stage (C or Cout % 32 == 0)
+  int exp_split_a;            // experiment: fprop A as 4 x 32-pixel im2col boxes
+  int wkw;                    // wgrad: pixels (K) per stage (32, or 64 on the TMA path)
   const float* w;             // weights KRSC
   float* w_mut;               // weights to update in place (SGD epilogue)
   const float* bias;          // FC bias for fprop (may be null)
@@ -618,10 +620,10 @@ __device__ __forceinline__ int wgrad_widx(const ConvParams& p, int m, bool& vali
 // tensor core reads from x itself: it truncates to 10 mantissa bits) and the
 // exactly representable residual lo = x - hi kept in a second tile; the
 // accumulator gets A*B + A*B_lo + A_lo*B, i.e. fp32-level products.
-template <int BN, int STAGES, bool PRECISE, int BM = kBM>
+template <int BN, int STAGES, bool PRECISE, int BM = kBM, int KW = kBK>
 struct TcSmem {
-  static constexpr int kABytes = BM * 128;
-  static constexpr int kBBytes = BN * 128;
+  static constexpr int kABytes = BM * KW * 4;
+  static constexpr int kBBytes = BN * KW * 4;
   static constexpr int kHalf = kABytes + kBBytes;
   static constexpr int kStage = PRECISE ? 2 * kHalf : kHalf;
   static constexpr int kTotal = STAGES * kStage + 1024 /*align slack*/ + 256 /*barriers*/;
@@ -661,7 +663,7 @@ __device__ __forceinline__ void split_lo(uint32_t hi, uint32_t lo, int tid) {
 // (tap, 32-channel) chunk, SWIZZLE_128B_ATOM_32B = MN-major canonical).
 // B: tiled (fprop: W [Cout][KK] K-major; dgrad: W as (Cin, taps, Cout)
 // MN-major chunks; wgrad: dY [P][Cout] MN-major chunks).
-template <int BN, int BM>
+template <int BN, int BM, int KW>
 __device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap* ta, const CUtensorMap* tb, int m0,
                                           int n0, int kb, uint32_t sa, uint32_t sb, uint32_t bar) {
   if (p.kind == kFprop) {
@@ -669,6 +671,14 @@ __device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap
     const int r = tap / p.kw, s = tap - r * p.kw;
 #pragma unroll
     for (int h = 0; h < BM / kBM; ++h) {
+      if (p.exp_split_a) {
+        for (int e = 0; e < 4; ++e) {
+          const Pix q = decode_pix(m0 + h * kBM + 32 * e, p.Ho, p.Wo);
+          tma_load_im2col(sa + h * 16384 + e * 4096, ta, bar, ck * 32, q.w * p.stride - p.pad,
+                          q.h * p.stride - p.pad, q.n, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+        }
+        continue;
+      }
       const Pix q = decode_pix(m0 + h * kBM, p.Ho, p.Wo);
       tma_load_im2col(sa + h * 16384, ta, bar, ck * 32, q.w * p.stride - p.pad, q.h * p.stride - p.pad, q.n,
                       static_cast<uint16_t>(s), static_cast<uint16_t>(r));
@@ -691,20 +701,22 @@ __device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap
     else
       for (int mc = 0; mc < BN / 32; ++mc) tma_load_3d(sb + mc * 4096, tb, bar, n0 + mc * 32, ftap, co0);
   } else {
-    const int p0 = kb * kBK;
+    // KW pixels per stage: every MN chunk (32 channels / 32 output channels)
+    // is KW K-rows of 128 B, chunks KW*128 B apart (the descriptors' LBO)
+    const int p0 = kb * KW;
     const Pix q = decode_pix(p0, p.Ho, p.Wo);
 #pragma unroll
     for (int mc = 0; mc < BM / 32; ++mc) {
       const int vc = (m0 >> 5) + mc;
       const int tap = vc / p.nchunk, ck = vc - tap * p.nchunk;
       const int r = tap / p.kw, s = tap - r * p.kw;
-      tma_load_im2col(sa + mc * 4096, ta, bar, ck * 32, q.w * p.stride - p.pad, q.h * p.stride - p.pad, q.n,
+      tma_load_im2col(sa + mc * (KW * 128), ta, bar, ck * 32, q.w * p.stride - p.pad, q.h * p.stride - p.pad, q.n,
                       static_cast<uint16_t>(s), static_cast<uint16_t>(r));
     }
     if (p.tma_b_merged)
       tma_load_3d(sb, tb, bar, 0, p0, n0 >> 5);
     else
-      for (int mc = 0; mc < BN / 32; ++mc) tma_load_2d(sb + mc * 4096, tb, bar, n0 + mc * 32, p0);
+      for (int mc = 0; mc < BN / 32; ++mc) tma_load_2d(sb + mc * (KW * 128), tb, bar, n0 + mc * 32, p0);
   }
 }
 
@@ -713,14 +725,15 @@ __device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap
 // (BN=256) FLOP per staged byte instead of 32 / 43, the lever against the L2
 // -> SM fill rate that bounds BM=128 tiles. Two CTAs per SM when the stage
 // ring fits in half the shared memory, else one.
-template <int BN, int STAGES, bool PRECISE, bool TMA, int BM = kBM>
-__global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM>::kTotal <= 116 * 1024 ? 2 : 1))
+template <int BN, int STAGES, bool PRECISE, bool TMA, int BM = kBM, int KW = kBK>
+__global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTotal <= 116 * 1024 ? 2 : 1))
     tc_conv_kernel(const __grid_constant__ ConvParams p,
                                                          const __grid_constant__ CUtensorMap tma_a,
                                                          const __grid_constant__ CUtensorMap tma_b,
                                                          const __grid_constant__ CUtensorMap tma_c) {
   extern __shared__ uint8_t smem_raw[];
-  using L = TcSmem<BN, STAGES, PRECISE, BM>;
+  using L = TcSmem<BN, STAGES, PRECISE, BM, KW>;
+  static_assert(KW == kBK || TMA, "wide K stages are TMA-wgrad only");
   constexpr int kHalves = BM / kBM;
   constexpr int kTmemCols = BN * kHalves;
   const uint32_t raw = smem_u32(smem_raw);
@@ -778,7 +791,7 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM>::kTotal 
           if (it >= STAGES) mbar_wait(empty_bar(s), ph ^ 1);
           const uint32_t sa = base + s * L::kStage;
           mbar_expect_tx(full_bar(s), kBytes);
-          tma_issue<BN, BM>(p, &tma_a, &tma_b, m0, n0, kb_begin + it, sa, sa + L::kABytes, full_bar(s));
+          tma_issue<BN, BM, KW>(p, &tma_a, &tma_b, m0, n0, kb_begin + it, sa, sa + L::kABytes, full_bar(s));
         }
       }
       __syncwarp();
@@ -1022,11 +1035,12 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM>::kTotal 
         const uint32_t sa = base + s * L::kStage;
         const uint32_t sb = sa + L::kABytes;
 #pragma unroll
-        for (int kk = 0; kk < kBK / 8; ++kk) {
-          // K-major: advance 32 B inside the swizzled row; MN-major: next 8 K rows.
-          const uint64_t ad = a_mn ? make_sdesc(sa + kk * 1024, 4096, 512, kSw128Base32)
+        for (int kk = 0; kk < KW / 8; ++kk) {
+          // K-major: advance 32 B inside the swizzled row; MN-major: next 8 K
+          // rows (MN chunks KW*128 B apart).
+          const uint64_t ad = a_mn ? make_sdesc(sa + kk * 1024, KW * 128, 512, kSw128Base32)
                                    : make_sdesc(sa + kk * 32, 16, 1024, kSw128);
-          const uint64_t bd = b_mn ? make_sdesc(sb + kk * 1024, 4096, 512, kSw128Base32)
+          const uint64_t bd = b_mn ? make_sdesc(sb + kk * 1024, KW * 128, 512, kSw128Base32)
                                    : make_sdesc(sb + kk * 32, 16, 1024, kSw128);
           if constexpr (PRECISE) {
             // lo tiles sit kHalf bytes above the hi tiles with identical layout:
@@ -1038,7 +1052,7 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM>::kTotal 
           } else {
 #pragma unroll
             for (int h = 0; h < kHalves; ++h)  // second M half: A rows 128..255 sit 16 KB above
-              tc_mma_tf32(tmem + h * BN, ad + static_cast<uint64_t>(h * (16384 >> 4)), bd, idesc,
+              tc_mma_tf32(tmem + h * BN, ad + static_cast<uint64_t>(h * ((kBM * KW * 4) >> 4)), bd, idesc,
                           (it > 0 || kk > 0) ? 1u : 0u);
           }
         }
