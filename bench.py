@@ -37,6 +37,17 @@ METRIC = "VGG-16 b256 train images/sec & peak GPU mem (vDNN_all/conv/dyn vs no-o
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+def conv_traffic():
+    """Mean DRAM bytes per conv-engine launch from the committed ncu capture
+    (profiles/r01_conv_traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_conv_traffic.json")
+    try:
+        with open(path) as f:
+            return int(json.load(f)["conv_dram_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def measured_tf32_peak(peaks, peaks_src):
     """The TF32 roofline denominator: the tcgen05 kind::tf32 issue ceiling
     measured on this device (vdnn_kernel_tf32_peak: M128 N256 K8 MMAs back to
@@ -405,8 +416,10 @@ def main():
         ach = head["_flops"] / (head["_conv_ms"] * 1e-3) / 1e12
         line["roofline"] = {"bound": "tensor", "kernel": "tc_conv_kernel (all conv/FC fprop+dgrad+wgrad launches)",
                             "achieved": round(ach, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
-                            "frac": round(ach / tf32_peak, 4), "traffic": None,
-                            "peak_note": peak_note}
+                            "frac": round(ach / tf32_peak, 4), "traffic": conv_traffic(),
+                            "peak_note": peak_note,
+                            "traffic_note": "DRAM read+write bytes per conv-engine launch (mean over one dyn step), "
+                                            "ncu capture profiles/r01_conv_traffic.json"}
     line["host_link"] = dict(link, **{
         "offload_bytes_per_iter": head.get("offload_bytes_per_iter"),
         "d2h_gbs_in_run": head.get("d2h_gbs"), "h2d_gbs_in_run": head.get("h2d_gbs"),
