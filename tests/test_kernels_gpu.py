@@ -235,3 +235,41 @@ def test_relu_and_softmax():
     lr_.backward()
     assert abs(loss.item() - lr_.item()) < 1e-5 * max(1.0, abs(lr_.item()))
     torch.testing.assert_close(grad.double().cpu(), zr.grad, rtol=1e-4, atol=1e-7)
+
+
+# Shapes large enough to select the production tile variants: tall (BM=256)
+# 128/64-wide tiles, wide (BN=256) tall tiles, 64-pixel wgrad stages, split-K
+# over hundreds of CTAs. Reference: torch float64 on the GPU (same op).
+LARGE = [
+    (32, 56, 56, 64, 128),    # fprop tall BN=128, dgrad tall BN=64, wgrad BN=128
+    (64, 56, 56, 256, 256),   # fprop/dgrad wide+tall (BN=256, BM=256), wgrad BN=256 KW=64
+]
+
+
+@pytest.mark.parametrize("shape", LARGE)
+def test_conv_production_tiles(shape):
+    dev = _dev()
+    n, h, w, c, cout = shape
+    g = torch.Generator(device=dev).manual_seed(n + c)
+    x = torch.randn(n, h, w, c, device=dev, generator=g)
+    wt = torch.randn(cout, 3, 3, c, device=dev, generator=g) * (2.0 / (9 * c)) ** 0.5
+    dy = torch.randn(n, h, w, cout, device=dev, generator=g)
+    xr = x.double().permute(0, 3, 1, 2).requires_grad_(True)
+    wr = wt.double().permute(0, 3, 1, 2).requires_grad_(True)
+    yr = torch.nn.functional.conv2d(xr, wr, padding=1)
+    yr.backward(dy.double().permute(0, 3, 1, 2))
+    y = torch.empty(n, h, w, cout, device=dev)
+    dx = torch.full_like(x, float("nan"))
+    d = _desc(n, h, w, [x], [c], cout, 3, 1, 1, [dx])
+    L.call("vdnn_kernel_conv_fprop", C.byref(d), C.c_void_p(wt.data_ptr()), None, C.c_void_p(y.data_ptr()), None)
+    L.call("vdnn_kernel_conv_dgrad", C.byref(d), C.c_void_p(wt.data_ptr()), C.c_void_p(dy.data_ptr()), 0, None)
+    ws_bytes = L.lib().vdnn_kernel_conv_wgrad_ws_bytes(C.byref(d))
+    ws = torch.empty(max(ws_bytes // 4, 1), device=dev)
+    dw = torch.full_like(wt, float("nan"))
+    L.call("vdnn_kernel_conv_wgrad", C.byref(d), C.c_void_p(dy.data_ptr()), C.c_void_p(wt.data_ptr()),
+           C.c_float(0.0), C.c_void_p(dw.data_ptr()), C.c_void_p(ws.data_ptr()), C.c_size_t(ws_bytes), None)
+    torch.cuda.synchronize()
+    for got, ref in ((y, yr.detach().permute(0, 2, 3, 1)), (dx, xr.grad.permute(0, 2, 3, 1)),
+                     (dw, wr.grad.permute(0, 2, 3, 1))):
+        err = (got.double() - ref).abs().max().item() / ref.abs().max().item()
+        assert err < TF32_TOL, err
