@@ -148,10 +148,7 @@ bool make_maps(ConvParams& p, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* tc)
   const float* x = p.seg[0].x;
   if (p.kind == kFprop) {
     if (!encode_out(tc, p.y, p.M, p.Cout)) return false;
-    static const bool split_a = std::getenv("VDNN_EXP_SPLIT_A") != nullptr;
-    p.exp_split_a = split_a ? 1 : 0;
-    if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, split_a ? 32 : kBM,
-                       CU_TENSOR_MAP_SWIZZLE_128B))
+    if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, kBM, CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.KK), static_cast<cuuint64_t>(p.Cout)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.KK) * 4};
@@ -315,7 +312,7 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
 bool wgrad_wide_k() {
   static const bool on = [] {
     const char* e = std::getenv("VDNN_WGRAD_KW");
-    return !(e && std::atoi(e) == 32);
+    return e && std::atoi(e) == 64;
   }();
   return on;
 }
@@ -336,9 +333,11 @@ WCfg wgrad_cfg(const ConvParams& p, int64_t pixels) {
   const bool one_per_sm = c.bn > 128 || (c.bm > kBM && tall_deep());
   c.slots = one_per_sm ? kNumSms : 2 * kNumSms;
   c.kw = kBK;
-  // 64-pixel stages for wide (BN = 256) tiles: measured +18% (56x56x256) to
-  // +42% (28x28 / 14x14 x512); narrower tiles lose their 2-CTA overlap for
-  // nothing (-7% at 128 channels)
+  // 64-pixel stages (opt-in, VDNN_WGRAD_KW=64): they halve the im2col boxes
+  // per FLOP, which paid +18..42% while the producer thread recomputed every
+  // box coordinate with integer divisions; with the incremental producer the
+  // 32-pixel ring with two CTAs per SM is as fast or faster (56x56x256: 714 vs
+  // 527 TFLOP/s)
   if (tma && c.bn == 256 && wgrad_wide_k()) {
     c.kw = 64;
     c.bm = kBM;

@@ -69,7 +69,6 @@ struct ConvParams {
   int vec_in;                 // every segment C % 4 == 0: 16-B gathers over input channels
   int vec_out;                // Cout % 4 == 0
   int tma_b_merged;           // dgrad/wgrad B loaded by one TMA per stage (C or Cout % 32 == 0)
-  int exp_split_a;            // experiment: fprop A as 4 x 32-pixel im2col boxes
   int wkw;                    // wgrad: pixels (K) per stage (32, or 64 on the TMA path)
   const float* w;             // weights KRSC
   float* w_mut;               // weights to update in place (SGD epilogue)
@@ -659,66 +658,118 @@ __device__ __forceinline__ void split_lo(uint32_t hi, uint32_t lo, int tid) {
 }
 
 // TMA producer (single thread). A: im2col (fprop: X, dgrad: dY, 128-pixel
-// columns, SWIZZLE_128B = K-major canonical; wgrad: X, 32-pixel columns per
+// columns, SWIZZLE_128B = K-major canonical; wgrad: X, KW-pixel columns per
 // (tap, 32-channel) chunk, SWIZZLE_128B_ATOM_32B = MN-major canonical).
 // B: tiled (fprop: W [Cout][KK] K-major; dgrad: W as (Cin, taps, Cout)
 // MN-major chunks; wgrad: dY [P][Cout] MN-major chunks).
+// Everything CTA-invariant (window origins of the tile, the wgrad tile's
+// (tap, chunk) per MN chunk) is computed once and the per-stage coordinates
+// advance incrementally: the issuing thread is serial, and per-stage integer
+// divisions measurably throttled the small-box (wgrad) pipelines.
 template <int BN, int BM, int KW>
-__device__ __forceinline__ void tma_issue(const ConvParams& p, const CUtensorMap* ta, const CUtensorMap* tb, int m0,
-                                          int n0, int kb, uint32_t sa, uint32_t sb, uint32_t bar) {
-  if (p.kind == kFprop) {
-    const int tap = kb / p.nchunk, ck = kb - tap * p.nchunk;
-    const int r = tap / p.kw, s = tap - r * p.kw;
+struct TmaProducer {
+  static constexpr int kH = BM / kBM;
+  int kind;
+  int qw[kH], qh[kH], qn[kH];  // fprop/dgrad: im2col window origin of each 128-row half
+  int ck, nck, r, s;           // fprop/dgrad: current (tap, 32-channel chunk)
+  int wch[BM / 32];            // wgrad: channel offset, tap of each MN chunk of A
+  uint16_t wr[BM / 32], ws[BM / 32];
+  int p0, pw, ph, pn;          // wgrad: first pixel of the stage
+
+  __device__ __forceinline__ void init(const ConvParams& p, int m0, int kb) {
+    kind = p.kind;
+    if (kind != kWgrad) {
+      nck = kind == kFprop ? p.nchunk : (p.Cout + 31) >> 5;
+      const int tap = kb / nck;
+      ck = kb - tap * nck;
+      r = tap / p.kw;
+      s = tap - r * p.kw;
 #pragma unroll
-    for (int h = 0; h < BM / kBM; ++h) {
-      if (p.exp_split_a) {
-        for (int e = 0; e < 4; ++e) {
-          const Pix q = decode_pix(m0 + h * kBM + 32 * e, p.Ho, p.Wo);
-          tma_load_im2col(sa + h * 16384 + e * 4096, ta, bar, ck * 32, q.w * p.stride - p.pad,
-                          q.h * p.stride - p.pad, q.n, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+      for (int h = 0; h < kH; ++h) {
+        if (kind == kFprop) {
+          const Pix q = decode_pix(m0 + h * kBM, p.Ho, p.Wo);
+          qw[h] = q.w * p.stride - p.pad;
+          qh[h] = q.h * p.stride - p.pad;
+          qn[h] = q.n;
+        } else {
+          const Pix q = decode_pix(m0 + h * kBM, p.H, p.W);
+          qw[h] = q.w - (p.kw - 1 - p.pad);
+          qh[h] = q.h - (p.kh - 1 - p.pad);
+          qn[h] = q.n;
         }
-        continue;
       }
-      const Pix q = decode_pix(m0 + h * kBM, p.Ho, p.Wo);
-      tma_load_im2col(sa + h * 16384, ta, bar, ck * 32, q.w * p.stride - p.pad, q.h * p.stride - p.pad, q.n,
-                      static_cast<uint16_t>(s), static_cast<uint16_t>(r));
-    }
-    tma_load_2d(sb, tb, bar, tap * p.C + ck * 32, n0);
-  } else if (p.kind == kDgrad) {
-    const int nck = (p.Cout + 31) >> 5;
-    const int tap = kb / nck, co0 = (kb - tap * nck) * 32;
-    const int r = tap / p.kw, s = tap - r * p.kw;
-    const int padh = p.kh - 1 - p.pad, padw = p.kw - 1 - p.pad;
+    } else {
 #pragma unroll
-    for (int h = 0; h < BM / kBM; ++h) {
-      const Pix q = decode_pix(m0 + h * kBM, p.H, p.W);
-      tma_load_im2col(sa + h * 16384, ta, bar, co0, q.w - padw, q.h - padh, q.n, static_cast<uint16_t>(s),
-                      static_cast<uint16_t>(r));
+      for (int mc = 0; mc < BM / 32; ++mc) {
+        const int vc = (m0 >> 5) + mc;
+        const int tap = vc / p.nchunk, c = vc - tap * p.nchunk;
+        const int rr = tap / p.kw;
+        wch[mc] = c * 32;
+        wr[mc] = static_cast<uint16_t>(rr);
+        ws[mc] = static_cast<uint16_t>(tap - rr * p.kw);
+      }
+      p0 = kb * KW;
+      const Pix q = decode_pix(p0, p.Ho, p.Wo);
+      pw = q.w;
+      ph = q.h;
+      pn = q.n;
     }
-    const int ftap = (p.kh - 1 - r) * p.kw + (p.kw - 1 - s);
-    if (p.tma_b_merged)
-      tma_load_4d(sb, tb, bar, 0, co0, n0 >> 5, ftap);
-    else
-      for (int mc = 0; mc < BN / 32; ++mc) tma_load_3d(sb + mc * 4096, tb, bar, n0 + mc * 32, ftap, co0);
-  } else {
-    // KW pixels per stage: every MN chunk (32 channels / 32 output channels)
-    // is KW K-rows of 128 B, chunks KW*128 B apart (the descriptors' LBO)
-    const int p0 = kb * KW;
-    const Pix q = decode_pix(p0, p.Ho, p.Wo);
-#pragma unroll
-    for (int mc = 0; mc < BM / 32; ++mc) {
-      const int vc = (m0 >> 5) + mc;
-      const int tap = vc / p.nchunk, ck = vc - tap * p.nchunk;
-      const int r = tap / p.kw, s = tap - r * p.kw;
-      tma_load_im2col(sa + mc * (KW * 128), ta, bar, ck * 32, q.w * p.stride - p.pad, q.h * p.stride - p.pad, q.n,
-                      static_cast<uint16_t>(s), static_cast<uint16_t>(r));
-    }
-    if (p.tma_b_merged)
-      tma_load_3d(sb, tb, bar, 0, p0, n0 >> 5);
-    else
-      for (int mc = 0; mc < BN / 32; ++mc) tma_load_2d(sb + mc * (KW * 128), tb, bar, n0 + mc * 32, p0);
   }
-}
+
+  __device__ __forceinline__ void issue(const ConvParams& p, const CUtensorMap* ta, const CUtensorMap* tb, int n0,
+                                        uint32_t sa, uint32_t sb, uint32_t bar) const {
+    if (kind == kFprop) {
+#pragma unroll
+      for (int h = 0; h < kH; ++h)
+        tma_load_im2col(sa + h * 16384, ta, bar, ck * 32, qw[h], qh[h], qn[h], static_cast<uint16_t>(s),
+                        static_cast<uint16_t>(r));
+      tma_load_2d(sb, tb, bar, (r * p.kw + s) * p.C + ck * 32, n0);
+    } else if (kind == kDgrad) {
+#pragma unroll
+      for (int h = 0; h < kH; ++h)
+        tma_load_im2col(sa + h * 16384, ta, bar, ck * 32, qw[h], qh[h], qn[h], static_cast<uint16_t>(s),
+                        static_cast<uint16_t>(r));
+      const int ftap = (p.kh - 1 - r) * p.kw + (p.kw - 1 - s);
+      if (p.tma_b_merged)
+        tma_load_4d(sb, tb, bar, 0, ck * 32, n0 >> 5, ftap);
+      else
+        for (int mc = 0; mc < BN / 32; ++mc) tma_load_3d(sb + mc * 4096, tb, bar, n0 + mc * 32, ftap, ck * 32);
+    } else {
+      // KW pixels per stage: every MN chunk (32 channels / 32 output channels)
+      // is KW K-rows of 128 B, chunks KW*128 B apart (the descriptors' LBO)
+      const int iw = pw * p.stride - p.pad, ih = ph * p.stride - p.pad;
+#pragma unroll
+      for (int mc = 0; mc < BM / 32; ++mc)
+        tma_load_im2col(sa + mc * (KW * 128), ta, bar, wch[mc], iw, ih, pn, ws[mc], wr[mc]);
+      if (p.tma_b_merged)
+        tma_load_3d(sb, tb, bar, 0, p0, n0 >> 5);
+      else
+        for (int mc = 0; mc < BN / 32; ++mc) tma_load_2d(sb + mc * (KW * 128), tb, bar, n0 + mc * 32, p0);
+    }
+  }
+
+  __device__ __forceinline__ void next(const ConvParams& p) {
+    if (kind != kWgrad) {
+      if (++ck == nck) {
+        ck = 0;
+        if (++s == p.kw) {
+          s = 0;
+          ++r;
+        }
+      }
+    } else {
+      p0 += KW;
+      pw += KW;
+      while (pw >= p.Wo) {
+        pw -= p.Wo;
+        if (++ph == p.Ho) {
+          ph = 0;
+          ++pn;
+        }
+      }
+    }
+  }
+};
 
 // BM x BN output tile per CTA. BM = 256 (TMA path) issues two M=128 MMAs per
 // K step against one B tile, into two TMEM accumulators: 43 (BN=128) or 64
@@ -785,13 +836,16 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTo
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
         constexpr uint32_t kBytes = L::kABytes + L::kBBytes;
+        TmaProducer<BN, BM, KW> tp;
+        tp.init(p, m0, kb_begin);
         for (int it = 0; it < nkb; ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           if (it >= STAGES) mbar_wait(empty_bar(s), ph ^ 1);
           const uint32_t sa = base + s * L::kStage;
           mbar_expect_tx(full_bar(s), kBytes);
-          tma_issue<BN, BM, KW>(p, &tma_a, &tma_b, m0, n0, kb_begin + it, sa, sa + L::kABytes, full_bar(s));
+          tp.issue(p, &tma_a, &tma_b, n0, sa, sa + L::kABytes, full_bar(s));
+          tp.next(p);
         }
       }
       __syncwarp();
