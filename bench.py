@@ -55,9 +55,14 @@ def measured_tf32_peak(peaks, peaks_src):
     entry; its bf16 figure / 2 is the fallback if the probe fails."""
     import ctypes as C
     from paper_1602_08124_b200 import _lib as L
-    v = C.c_double(0.0)
-    if L.lib().vdnn_kernel_tf32_peak(C.byref(v)) == 0 and v.value > 0:
-        return v.value, "measured live: tcgen05.mma kind::tf32 M128xN256xK8 issue ceiling, 148 SMs (vdnn_kernel_tf32_peak)"
+    best = 0.0
+    for _ in range(5):  # best of 5 (the first runs can see a cold power/clock state)
+        v = C.c_double(0.0)
+        if L.lib().vdnn_kernel_tf32_peak(C.byref(v)) == 0:
+            best = max(best, v.value)
+    if best > 0:
+        return best, ("measured live (best of 5): tcgen05.mma kind::tf32 M128xN256xK8 issue ceiling, "
+                      "148 SMs (vdnn_kernel_tf32_peak)")
     return float(peaks.get("bf16_tflops_sustained", 1400.0)) / 2.0, f"fallback: {peaks_src} bf16 sustained / 2"
 
 
