@@ -8,6 +8,7 @@
 
 #include "kernels.h"
 #include "tc_conv.cuh"
+#include "tc_conv_persist.cuh"
 #include "tma_maps.h"
 
 namespace vdnnk {
@@ -262,6 +263,39 @@ cudaError_t launch_bn(const ConvParams& p, const CUtensorMap& ta, const CUtensor
   return cudaGetLastError();
 }
 
+template <int BN, int BM, int STAGES>
+cudaError_t launch_persist(const ConvParams& p, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                           cudaStream_t st) {
+  using L = PersistSmem<BN, BM, STAGES>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_persist_kernel<BN, BM, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((p.M + BM - 1) / BM) * ((p.Ncols + BN - 1) / BN);
+  tc_conv_persist_kernel<BN, BM, STAGES><<<std::min(tiles, kNumSms), 192, L::kTotal, st>>>(p, ta, tb, tc);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Persistent kernel selection. Measured (VGG-16 b256 shapes) against the
+// one-tile-per-CTA tall/wide kernels: fprop with 128 output columns +8..11%
+// (L2-bound at ~43 FLOP/B either way; the persistent ring removes per-tile
+// fills), 64 columns +2%, dgrad 64 columns -16%, >= 256 columns -4..-10%
+// (its BN=256 tile is BM=128 to keep two TMEM accumulator sets).
+// VDNN_PERSIST=0 disables, =2 forces it for every fprop/dgrad.
+bool use_persist(const ConvParams& p) {
+  static const int mode = [] {
+    const char* e = std::getenv("VDNN_PERSIST");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (mode == 0) return false;
+  if (mode == 2) return true;
+  return p.kind == kFprop && p.Ncols > 64 && p.Ncols <= 128;
+}
+
 cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
   alignas(64) CUtensorMap ta, tb, tc;
@@ -285,6 +319,19 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
     p.wkw = kBK;
     p.kblocks *= 2;
     p.kb_per_split *= 2;
+  }
+  if (p.kind != kWgrad && splits == 1 && use_persist(p) && !g_no_tma) {
+    if (p.Ncols <= 64) {
+      if (make_maps<64>(p, &ta, &tb, &tc)) return launch_persist<64, 256, 4>(p, ta, tb, tc, st);
+    } else if (p.Ncols <= 128) {
+      if (make_maps<128>(p, &ta, &tb, &tc)) return launch_persist<128, 256, 4>(p, ta, tb, tc, st);
+    } else if (make_maps<256>(p, &ta, &tb, &tc)) {
+      return launch_persist<256, 128, 4>(p, ta, tb, tc, st);
+    }
+    std::memset(&ta, 0, sizeof(ta));
+    std::memset(&tb, 0, sizeof(tb));
+    std::memset(&tc, 0, sizeof(tc));
+    p.tma_b_merged = 0;
   }
   const bool deep = tall_deep();
   if (p.Ncols <= 64) {
