@@ -82,6 +82,12 @@ void vdnn_graph_destroy(vdnn_graph* g);
 vdnn_status vdnn_graph_add_input(vdnn_graph* g, uint64_t c, uint64_t h, uint64_t w, int32_t* id);
 vdnn_status vdnn_graph_add_conv(vdnn_graph* g, const int32_t* inputs, int32_t n_inputs, uint64_t out_channels,
                                 uint64_t kernel, uint64_t stride, uint64_t pad, int32_t join, int32_t* id);
+/* Generic NetworkGraph::add_layer (net_graph.hpp:109-113) as used by the INI inline-layer front-end
+   (config.hpp:194-235): kind 0..5 = input, conv, actv, pool, fc, loss; params per kind as
+   conv (kernel, stride, pad, out), pool (window, stride), fc (out), input (c, h, w). Arity and
+   parameter checks happen at finalize, as in the reference. */
+vdnn_status vdnn_graph_add_layer(vdnn_graph* g, int32_t kind, const int32_t* inputs, int32_t n_inputs, uint64_t p0,
+                                 uint64_t p1, uint64_t p2, uint64_t p3, int32_t join, int32_t* id);
 vdnn_status vdnn_graph_add_actv(vdnn_graph* g, int32_t input, int32_t* id);
 vdnn_status vdnn_graph_add_pool(vdnn_graph* g, const int32_t* inputs, int32_t n_inputs, uint64_t window,
                                 uint64_t stride, int32_t join, int32_t* id);

@@ -79,3 +79,47 @@ def fuzz(seed: int, trials: int) -> dict:
 def time_plan(graph_spec: str, capacity: int, iters: int) -> float:
     """Seconds per reference dynamic_select + simulate (single thread)."""
     return lib().vref_time_plan(graph_spec.encode(), C.c_ulonglong(capacity), int(iters))
+
+
+# ---- front-end / artefact formats (oracle/_ref/libvdnnref_fmt.so, needs nlohmann) ----
+LIB_FMT = os.path.join(_HERE, "_ref", "libvdnnref_fmt.so")
+_fmt = None
+
+
+def fmt_available() -> bool:
+    return os.path.exists(LIB_FMT)
+
+
+def _fmt_lib():
+    global _fmt
+    if _fmt is None:
+        _fmt = C.CDLL(LIB_FMT)
+        for n in ("vref_fmt_config", "vref_fmt_graph_to_json", "vref_fmt_graph_from_json", "vref_fmt_report"):
+            getattr(_fmt, n).restype = C.c_void_p
+        _fmt.vref_fmt_free.argtypes = [C.c_void_p]
+    return _fmt
+
+
+def _fmt_take(p) -> str:
+    s = C.cast(p, C.c_char_p).value.decode()
+    _fmt_lib().vref_fmt_free(p)
+    return s
+
+
+def fmt_config(path: str) -> dict:
+    """Reference load_config(path) + build_network: all fields, graph as a spec (or error)."""
+    return json.loads(_fmt_take(_fmt_lib().vref_fmt_config(path.encode())))
+
+
+def fmt_graph_to_json(graph_spec: str) -> dict:
+    return json.loads(_fmt_take(_fmt_lib().vref_fmt_graph_to_json(graph_spec.encode())))
+
+
+def fmt_graph_from_json(text: str) -> str:
+    """Reference graph_from_json -> spec (or a JSON error object string)."""
+    return _fmt_take(_fmt_lib().vref_fmt_graph_from_json(text.encode()))
+
+
+def fmt_report(graph_spec: str, capacity: int) -> dict:
+    """Reference decision_to_json + report_to_json of dynamic_select/simulate."""
+    return json.loads(_fmt_take(_fmt_lib().vref_fmt_report(graph_spec.encode(), C.c_ulonglong(capacity))))

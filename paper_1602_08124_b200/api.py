@@ -194,6 +194,18 @@ class NetworkGraph:
               C.c_uint64(stride), C.c_uint64(pad), int(join), C.byref(out))
         return out.value
 
+    def add_layer(self, kind: "LayerKind", inputs: Sequence[int] = (), params: Sequence[int] = (),
+                  join: "JoinRule" = None) -> int:
+        """NetworkGraph::add_layer (net_graph.hpp:109-113): any kind with any
+        input list; params per kind = conv (kernel, stride, pad, out), pool
+        (window, stride), fc (out,), input (c, h, w). Checked at finalize."""
+        arr, n = self._ins(inputs)
+        p = list(params) + [0] * (4 - len(params))
+        out = C.c_int32()
+        _call("vdnn_graph_add_layer", self._h, int(kind), arr, n, *[C.c_uint64(int(v)) for v in p[:4]],
+              int(join if join is not None else JoinRule.Concat), C.byref(out))
+        return out.value
+
     def add_actv(self, inp: int) -> int:
         out = C.c_int32()
         _call("vdnn_graph_add_actv", self._h, int(inp), C.byref(out))

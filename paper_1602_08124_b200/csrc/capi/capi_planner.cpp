@@ -134,6 +134,41 @@ vdnn_status vdnn_graph_add_conv(vdnn_graph* g, const int32_t* in, int32_t n, uin
     return VDNN_OK;
   });
 }
+vdnn_status vdnn_graph_add_layer(vdnn_graph* g, int32_t kind, const int32_t* in, int32_t n, uint64_t p0, uint64_t p1,
+                                 uint64_t p2, uint64_t p3, int32_t join, int32_t* id) {
+  return guard([&] {
+    if (kind < 0 || kind > 5) throw vdnnp::PlanError(vdnnp::Err::Config, "unknown layer kind");
+    vdnnp::Node d;
+    d.kind = static_cast<vdnnp::Kind>(kind);
+    d.in = inputs_of(in, n);
+    d.join = join_of(join);
+    switch (d.kind) {
+      case vdnnp::Kind::Conv:
+        d.k = p0;
+        d.s = p1;
+        d.p = p2;
+        d.out = p3;
+        break;
+      case vdnnp::Kind::Pool:
+        d.k = p0;
+        d.s = p1;
+        break;
+      case vdnnp::Kind::Fc:
+        d.out = p0;
+        break;
+      case vdnnp::Kind::Input:
+        d.ic = p0;
+        d.ih = p1;
+        d.iw = p2;
+        break;
+      default:
+        break;
+    }
+    const int r = g->net.add(std::move(d));
+    if (id) *id = r;
+    return VDNN_OK;
+  });
+}
 vdnn_status vdnn_graph_add_actv(vdnn_graph* g, int32_t input, int32_t* id) {
   return guard([&] {
     const int r = g->net.actv(input);

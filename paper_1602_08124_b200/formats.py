@@ -48,25 +48,29 @@ def graph_to_json(g: V.NetworkGraph) -> Dict:
 
 
 def graph_from_json(j: Dict) -> V.NetworkGraph:
-    g = V.NetworkGraph(int(j["batch"]))
-    for e in j["layers"]:
-        kind = e["kind"]
-        ins = [int(x) for x in e.get("inputs", [])]
-        join = V.JoinRule.Elementwise if e.get("join") == "eltwise" else V.JoinRule.Concat
-        if kind == "input":
-            g.add_input(e["c"], e["h"], e["w"])
-        elif kind == "conv":
-            g.add_conv(ins, e["out_channels"], e["kernel"], e["stride"], e["pad"], join)
-        elif kind == "actv":
-            g.add_actv(ins[0])
-        elif kind == "pool":
-            g.add_pool(ins, e["window"], e["stride"], join)
-        elif kind == "fc":
-            g.add_fc(ins, e["out_features"], join)
-        elif kind == "loss":
-            g.add_loss(ins[0])
-        else:
-            raise V.ConfigError(9, "unknown layer kind: " + kind)
+    """report.hpp:80-111: generic add_layer per entry, checked at finalize."""
+    try:
+        g = V.NetworkGraph(int(j["batch"]))
+        for e in j["layers"]:
+            kind = e["kind"]
+            if kind not in _KIND:
+                raise V.ConfigError(9, "unknown layer kind: " + str(kind))
+            k = V.LayerKind(_KIND.index(kind))
+            ins = [int(x) for x in e.get("inputs", [])]
+            join = V.JoinRule.Elementwise if e.get("join") == "eltwise" else V.JoinRule.Concat
+            if k == V.LayerKind.Conv:
+                params = (e["kernel"], e["stride"], e["pad"], e["out_channels"])
+            elif k == V.LayerKind.Pool:
+                params = (e["window"], e["stride"])
+            elif k == V.LayerKind.Fc:
+                params = (e["out_features"],)
+            elif k == V.LayerKind.Input:
+                params = (e["c"], e["h"], e["w"])
+            else:
+                params = ()
+            g.add_layer(k, ins, [int(x) for x in params], join)
+    except KeyError as ex:
+        raise V.ConfigError(9, f"graph json: missing key {ex}")
     return g.finalize()
 
 
