@@ -10,8 +10,10 @@ batch 256 per GPU on synthetic data (U[-1,1) NHWC images, uniform labels,
 He-normal weights), replaying the bit-exact vDNN plan on the B200: offload and
 prefetch copies over PCIe, all compute in sm_100a tcgen05 kernels. Inputs are
 far larger than L2 (activations are GBs), so no explicit L2 flush is needed.
-N > 1: data parallel, one process per GPU, per-rank batch 256 (weak scaling),
-NCCL all-reduce of the weight gradients every step; time = max over ranks.
+N > 1: data parallel, one process per GPU, per-rank batch 256 (weak scaling);
+every step the weight gradients are exchanged by the fused peer-memory
+reduce + SGD + broadcast kernel (VDNN_DP=nccl: NCCL all-reduce + SGD
+instead); time = max over ranks.
 
 --impl reference times the reference's CPU path on this host: the compiled
 reference simulator's planning (dynamic_select + simulate, oracle/_ref) plus
@@ -183,7 +185,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     import numpy as np
     import torch
     import paper_1602_08124_b200 as V
-    from paper_1602_08124_b200.dist import DataParallel, max_over_ranks
+    from paper_1602_08124_b200.dist import make_data_parallel, max_over_ranks
 
     g = V.build_preset(args.net, args.batch) if args.extra == 0 else V.extend_vgg(args.extra, args.batch)
     cm = V.CostModel()
@@ -210,7 +212,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         return {"policy": policy, "label": d.label, "verdict": plan.verdict(), "capacity": cap}
     s = V.Session(g, d, cm, cap, device=device, record_timeline=True, external_grads=world > 1,
                   precise_fp32=args.precise, compress_offload=compress)
-    dp = DataParallel(s, world, device) if world > 1 else None
+    dp = make_data_parallel(s, world, device) if world > 1 else None
 
     def one(want_loss=False):
         return dp.step(args.lr, want_loss) if dp else s.step(args.lr, want_loss=want_loss)
@@ -272,6 +274,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         "wire_ratio": round((wire["offload_wire"] + wire["prefetch_wire"]) /
                             max(1, wire["offload_planned"] + wire["prefetch_planned"]), 4),
         "signature": plan.signature(),
+        "dp_exchange": (dp.mode if dp else None),
     }
     if want_e2e:
         # end to end through the public API: pinned host batch -> device every
@@ -410,6 +413,7 @@ def main():
                                f"vDNN_dyn under {args.capacity} B HBM budget ({head.get('label')})",
                    "global_batch": args.batch * world, "per_gpu_batch": args.batch,
                    "capacity_bytes": args.capacity, "parallelism": f"dp{world}",
+                   "gradient_exchange": (None if world == 1 else head.get("dp_exchange")),
                    "l2": "inputs larger than L2 (activation maps are GBs); no flush needed"},
         "e2e": head.get("e2e"),
         "gpu_launches": head.get("gpu_launches"),

@@ -291,6 +291,24 @@ vdnn_status vdnn_session_apply_grads(vdnn_session* s, float lr, float grad_scale
 vdnn_status vdnn_session_set_grad_arena(vdnn_session* s, void* dev_ptr, size_t count);
 /* Whole-gradient-arena pointer for a single bucketed allreduce. */
 vdnn_status vdnn_session_grad_arena(vdnn_session* s, void** dev_ptr, size_t* count);
+/* Data-parallel exchange over peer memory (NVLink P2P through CUDA IPC), the
+ * fused replacement of "NCCL all-reduce of the gradient arena + apply_grads":
+ * each rank exports a handle (needs external_grads=1 and the session-owned
+ * gradient arena), the caller all-gathers the handles by any means, every
+ * rank attaches with the full array (index = rank), then after each
+ * vdnn_session_step every rank calls vdnn_session_peer_exchange, which on the
+ * compute stream waits for all ranks, reduces 1/N of the gradients from all
+ * ranks in rank order, applies w -= lr*scale*sum and writes the new weights
+ * into every rank's arena, then waits for all ranks again. All ranks must run
+ * the same plan (checked) and call exchange the same number of times. */
+typedef struct vdnn_peer_handle {
+  uint8_t arena[64], grads[64], signal[64]; /* cudaIpcMemHandle_t */
+  uint64_t arena_lo, arena_bytes, grads_count;
+} vdnn_peer_handle;
+vdnn_status vdnn_session_peer_export(vdnn_session* s, vdnn_peer_handle* out);
+vdnn_status vdnn_session_peer_attach(vdnn_session* s, int32_t rank, int32_t world, const vdnn_peer_handle* all);
+vdnn_status vdnn_session_peer_exchange(vdnn_session* s, float lr, float grad_scale);
+vdnn_status vdnn_session_peer_detach(vdnn_session* s);
 /* Compute stream (cudaStream_t) for interop. */
 vdnn_status vdnn_session_stream(vdnn_session* s, void** stream);
 uint64_t vdnn_kernel_launch_count(void);

@@ -115,6 +115,14 @@ class SessionOptions(C.Structure):
     ]
 
 
+class PeerHandle(C.Structure):
+    """vdnn_peer_handle: three CUDA IPC handles + the layout they must agree on."""
+    _fields_ = [
+        ("arena", C.c_uint8 * 64), ("grads", C.c_uint8 * 64), ("signal", C.c_uint8 * 64),
+        ("arena_lo", C.c_uint64), ("arena_bytes", C.c_uint64), ("grads_count", C.c_uint64),
+    ]
+
+
 class ConvDesc(C.Structure):
     _fields_ = [
         ("n", C.c_int32), ("h", C.c_int32), ("w", C.c_int32), ("nseg", C.c_int32),

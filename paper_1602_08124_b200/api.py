@@ -862,6 +862,27 @@ class Session:
     def apply_grads(self, lr: float, scale: float = 1.0) -> None:
         _call("vdnn_session_apply_grads", self.handle, C.c_float(lr), C.c_float(scale))
 
+    # -- data-parallel exchange over peer memory (vdnn_session_peer_*) --
+    def peer_export(self) -> bytes:
+        """This rank's IPC handles (opaque bytes, to be all-gathered)."""
+        h = L.PeerHandle()
+        _call("vdnn_session_peer_export", self.handle, C.byref(h))
+        return bytes(h)
+
+    def peer_attach(self, rank: int, handles: List[bytes]) -> None:
+        """Map every rank's arenas (handles[i] = rank i's peer_export())."""
+        arr = (L.PeerHandle * len(handles))()
+        for i, b in enumerate(handles):
+            C.memmove(C.byref(arr[i]), b, C.sizeof(L.PeerHandle))
+        _call("vdnn_session_peer_attach", self.handle, C.c_int32(rank), C.c_int32(len(handles)), arr)
+
+    def peer_exchange(self, lr: float, scale: float = 1.0) -> None:
+        """Fused all-reduce + SGD + weight broadcast on the compute stream."""
+        _call("vdnn_session_peer_exchange", self.handle, C.c_float(lr), C.c_float(scale))
+
+    def peer_detach(self) -> None:
+        _call("vdnn_session_peer_detach", self.handle)
+
     @property
     def stream(self) -> int:
         p = C.c_void_p()

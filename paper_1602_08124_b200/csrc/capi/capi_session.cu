@@ -3,6 +3,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../runtime/session.h"
 #include "capi_common.h"
@@ -193,6 +194,47 @@ vdnn_status vdnn_session_get_grads(vdnn_session* s, int32_t layer, float* host, 
 vdnn_status vdnn_session_apply_grads(vdnn_session* s, float lr, float scale) {
   return guard([&] {
     S(s).apply_grads(lr, scale);
+    return VDNN_OK;
+  });
+}
+static_assert(sizeof(cudaIpcMemHandle_t) == 64, "vdnn_peer_handle assumes 64-byte IPC handles");
+vdnn_status vdnn_session_peer_export(vdnn_session* s, vdnn_peer_handle* out) {
+  return guard([&] {
+    const auto h = S(s).peer_export();
+    std::memcpy(out->arena, &h.arena, 64);
+    std::memcpy(out->grads, &h.grads, 64);
+    std::memcpy(out->signal, &h.signal, 64);
+    out->arena_lo = h.arena_lo;
+    out->arena_bytes = h.arena_bytes;
+    out->grads_count = h.grads_count;
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_peer_attach(vdnn_session* s, int32_t rank, int32_t world, const vdnn_peer_handle* all) {
+  return guard([&] {
+    if (world < 1 || world > 8 || !all) throw vdnnp::PlanError(vdnnp::Err::Generic, "peer_attach: 1..8 ranks");
+    std::vector<vdnnrt::Session::PeerHandle> v(static_cast<size_t>(world));
+    for (int p = 0; p < world; ++p) {
+      std::memcpy(&v[p].arena, all[p].arena, 64);
+      std::memcpy(&v[p].grads, all[p].grads, 64);
+      std::memcpy(&v[p].signal, all[p].signal, 64);
+      v[p].arena_lo = all[p].arena_lo;
+      v[p].arena_bytes = all[p].arena_bytes;
+      v[p].grads_count = all[p].grads_count;
+    }
+    S(s).peer_attach(rank, world, v.data());
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_peer_exchange(vdnn_session* s, float lr, float scale) {
+  return guard([&] {
+    S(s).peer_exchange(lr, scale);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_peer_detach(vdnn_session* s) {
+  return guard([&] {
+    S(s).peer_detach();
     return VDNN_OK;
   });
 }

@@ -98,6 +98,26 @@ bool zvc_eligible(const void* p, uint64_t bytes);
 cudaError_t zvc_compress(const float* src, uint64_t count, void* host_dst, unsigned long long* wire, cudaStream_t st);
 cudaError_t zvc_decompress(const void* host_src, uint64_t count, float* dst, unsigned long long* wire,
                            cudaStream_t st);
+// Data-parallel exchange over peer memory (peer.cu): barrier flags and the
+// fused reduce + SGD + broadcast of the weight gradients.
+constexpr int kPeerMaxRanks = 8;
+struct PeerChunk {
+  uint64_t w_off;   // byte offset of the weights from the arena base (identical on every rank)
+  uint64_t g_off;   // float offset into the gradient arena
+  uint32_t count;   // floats
+  uint32_t pad;
+};
+struct PeerArgs {
+  int world = 1, rank = 0;
+  char* arena[kPeerMaxRanks] = {};                 // per-rank arena base (local or IPC-mapped)
+  const float* grads[kPeerMaxRanks] = {};          // per-rank gradient arena
+  unsigned long long* signal[kPeerMaxRanks] = {};  // per-rank flags [2 phases][kPeerMaxRanks]
+  const PeerChunk* chunks = nullptr;               // this rank's share (device memory)
+  int nchunks = 0;
+  float step = 0.f;                                // lr * grad_scale
+};
+cudaError_t peer_barrier(const PeerArgs& a, unsigned long long epoch, int phase, cudaStream_t st);
+cudaError_t peer_reduce_sgd(const PeerArgs& a, cudaStream_t st);
 // Measured TF32 tensor-core ceiling (TFLOP/s) of the current device.
 cudaError_t tf32_peak_probe(double* tflops);
 void count_launch(uint64_t k = 1);

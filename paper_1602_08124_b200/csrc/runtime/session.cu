@@ -31,7 +31,6 @@ namespace vdnnrt {
 using namespace vdnnp;
 
 namespace {
-constexpr u64 kNoOff = ~u64{0};
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -177,6 +176,8 @@ Session::~Session() {
   for (auto e : xfer_ev_) cudaEventDestroy(e);
   if (ev_iter_) cudaEventDestroy(ev_iter_);
   if (ev_sync_) cudaEventDestroy(ev_sync_);
+  peer_detach();
+  if (signal_) cudaFree(signal_);
   cudaFree(arena_);
   if (host_) cudaFreeHost(host_);
   cudaFree(loss_grad_);

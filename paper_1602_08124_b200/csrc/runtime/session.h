@@ -15,6 +15,8 @@ namespace vdnnrt {
 using vdnnp::i64;
 using vdnnp::u64;
 
+constexpr u64 kNoOff = ~u64{0};  // "no buffer" offset
+
 struct Options {
   int device = 0;
   u64 weight_seed = 5000;
@@ -93,6 +95,18 @@ class Session {
   void grad_arena(void** ptr, size_t* count);
   void apply_grads(float lr, float scale);
   void set_grad_arena(float* ptr, size_t count);
+  // Data-parallel exchange over peer memory (runtime/peer.cu): export this
+  // session's arena / gradient arena / signal words as CUDA IPC handles, map
+  // every peer's, then run the fused reduce + SGD + broadcast each step.
+  struct PeerHandle {
+    cudaIpcMemHandle_t arena, grads, signal;
+    u64 arena_lo, arena_bytes, grads_count;
+  };
+  PeerHandle peer_export();
+  void peer_attach(int rank, int world, const PeerHandle* all);
+  void peer_exchange(float lr, float scale);
+  void peer_detach();
+  int peer_world() const { return peer_world_; }
 
   const vdnnp::Report& plan() const { return plan_; }
   u64 arena_bytes() const { return arena_bytes_; }
@@ -150,6 +164,12 @@ class Session {
   std::vector<u64> grad_off_;    // per layer float offset into grads_
   size_t grads_count_ = 0;
   float* pinned_loss_ = nullptr;
+  unsigned long long* signal_ = nullptr;  // peer barrier flags [2][kPeerMaxRanks]
+  vdnnk::PeerArgs peer_{};
+  vdnnk::PeerChunk* peer_chunks_ = nullptr;
+  std::vector<void*> peer_maps_;          // IPC-opened pointers (closed on detach)
+  int peer_world_ = 0;
+  unsigned long long peer_epoch_ = 0;
 
   u64 x_off_ = 0;                // INPUT feature extent (setup allocation)
   std::vector<u64> w_off_;       // per layer weight offset

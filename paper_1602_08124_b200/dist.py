@@ -1,6 +1,15 @@
-"""Data-parallel training over NCCL: one process per GPU, each rank running its
-own vDNN plan (identical per-rank schedule, weak scaling), weight gradients
-averaged with one bucketed all-reduce over the session's gradient arena.
+"""Data-parallel training: one process per GPU, each rank running its own vDNN
+plan (identical per-rank schedule, weak scaling). Two exchange paths:
+
+* ``PeerDataParallel`` (default): the fused peer-memory exchange of
+  ``csrc/kernels/peer.cu`` -- every rank's arenas are mapped into every other
+  rank through CUDA IPC; one kernel per rank reduces its 1/N share of the
+  gradients from all ranks over NVLink, applies SGD and stores the new weights
+  into every rank's arena (reduce-scatter + update + all-gather in one pass,
+  bracketed by two flag barriers). torch.distributed only carries the
+  handles.
+* ``DataParallel``: one bucketed NCCL all-reduce over the session's gradient
+  arena followed by the SGD kernels (the library baseline).
 
 The reference has no multi-GPU path; BASELINE.json's config 5
 (VGG-416 b32 per GPU at 2/4/8 GPUs) asks for this one exchange step. The
@@ -39,8 +48,74 @@ def max_over_ranks(value: float, world: int, device=None) -> float:
     return float(t.item())
 
 
+def make_data_parallel(session, world: int, device: int, mode: Optional[str] = None, group=None):
+    """The exchange path for ``world`` ranks: ``mode`` "peer" (fused P2P
+    kernel), "nccl", or None = $VDNN_DP, default "peer"."""
+    mode = mode or os.environ.get("VDNN_DP", "peer")
+    if mode == "peer":
+        try:
+            return PeerDataParallel(session, world, group=group)
+        except PeerUnavailable as e:  # every rank agreed to fall back (no P2P between these GPUs)
+            import sys
+            print(f"[vdnn] peer exchange unavailable ({e}); using NCCL all-reduce", file=sys.stderr)
+            mode = "nccl"
+    if mode == "nccl":
+        return DataParallel(session, world, device, group=group)
+    raise ValueError(f"unknown data-parallel mode {mode!r}")
+
+
+class PeerUnavailable(RuntimeError):
+    """Some rank could not map its peers' arenas (raised on every rank)."""
+
+
+class PeerDataParallel:
+    """Fused peer-memory gradient exchange + SGD (vdnn_session_peer_*). Wraps a
+    Session created with external_grads=True; every rank of the process group
+    must construct it (the IPC handles are all-gathered over ``group``)."""
+
+    mode = "peer"
+
+    def __init__(self, session, world: int, group=None):
+        import torch.distributed as dist
+        self.s = session
+        self.world = world
+        h = session.peer_export()
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, h, group=group)
+            rank = dist.get_rank(group)
+        else:
+            handles, rank = [h], 0
+        err = None
+        try:
+            session.peer_attach(rank, handles)
+        except Exception as e:  # e.g. cudaIpcOpenMemHandle refused (no P2P path)
+            err = repr(e)
+        errs = [err]
+        if world > 1:  # all ranks attach or none does: a lone attached rank would wait in the barrier
+            errs = [None] * world
+            dist.all_gather_object(errs, err, group=group)
+        bad = [f"rank {r}: {e}" for r, e in enumerate(errs) if e]
+        if bad:
+            session.peer_detach()
+            raise PeerUnavailable("; ".join(bad))
+
+    def step(self, lr: float, want_loss: bool = False) -> Optional[float]:
+        # the exchange is enqueued after the step's kernels; the loss read
+        # (want_loss) happens inside step(), before the exchange completes
+        loss = self.s.step(lr, want_loss=want_loss)
+        self.s.peer_exchange(lr, 1.0 / self.world)
+        return loss
+
+    def close(self) -> None:
+        self.s.peer_detach()
+
+
 class DataParallel:
-    """Wraps a Session created with external_grads=True."""
+    """NCCL all-reduce of the gradient arena, then SGD. Wraps a Session
+    created with external_grads=True."""
+
+    mode = "nccl"
 
     def __init__(self, session, world: int, device: int, group=None):
         import torch

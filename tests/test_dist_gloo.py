@@ -49,3 +49,63 @@ def test_env_rank_defaults(monkeypatch):
     for k in ("RANK", "LOCAL_RANK", "WORLD_SIZE"):
         monkeypatch.delenv(k, raising=False)
     assert env_rank() == (0, 0, 1)
+
+
+def test_make_data_parallel_rejects_unknown_mode():
+    from paper_1602_08124_b200.dist import make_data_parallel
+    with pytest.raises(ValueError):
+        make_data_parallel(None, 2, 0, mode="ring")
+
+
+class _FakeSession:
+    """Stands in for Session in the host-side peer-attach protocol."""
+
+    def __init__(self, rank, fail_rank):
+        self.rank, self.fail_rank = rank, fail_rank
+        self.attached = None
+        self.detached = False
+
+    def peer_export(self):
+        return bytes([self.rank]) * 8
+
+    def peer_attach(self, rank, handles):
+        if rank == self.fail_rank:
+            raise RuntimeError("cudaIpcOpenMemHandle refused")
+        self.attached = (rank, list(handles))
+
+    def peer_detach(self):
+        self.detached = True
+
+
+def _peer_worker(rank, world, port, fail_rank, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1602_08124_b200.dist import PeerDataParallel, PeerUnavailable
+    s = _FakeSession(rank, fail_rank)
+    try:
+        PeerDataParallel(s, world)
+        q.put((rank, "ok", s.attached, s.detached))
+    except PeerUnavailable as e:
+        q.put((rank, "unavailable:" + str(e), s.attached, s.detached))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_peer_attach_all_or_none(fail_rank):
+    """Handles are all-gathered in rank order; if any rank fails to attach,
+    every rank detaches and raises (nobody is left waiting in a barrier)."""
+    world = 3
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_peer_worker, args=(r, world, port, fail_rank, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    for rank, status, attached, detached in res:
+        if fail_rank < 0:
+            assert status == "ok" and attached == (rank, [bytes([r]) * 8 for r in range(world)]) and not detached
+        else:
+            assert status.startswith("unavailable:") and "rank 1" in status and detached

@@ -1,0 +1,144 @@
+"""Fused peer-memory gradient exchange (csrc/kernels/peer.cu): reduce 1/N of
+the gradients from every rank over P2P, SGD, store the new weights into every
+rank's arena -- checked against the host-side reduction of the same
+gradients.
+
+The driver's GPU box has one B200, so the multi-rank cases run N processes on
+the SAME device: CUDA IPC maps each process's arenas into the others exactly
+as across GPUs (only the link differs), and the flag barriers synchronise
+separate contexts. Handles travel over gloo.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+LR = 0.05
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _session(V, numeric, g, cm, external=True):
+    d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+    s = V.Session(g, d, cm, 64 << 20, external_grads=external)
+    w = numeric.he_weights(g, cm, seed=31)
+    for k, v in w.items():
+        s.set_weights(k, v)
+    return s, w
+
+
+def _batch(g, seed):
+    sh = g.shape(0)
+    rng = np.random.default_rng(seed)
+    images = rng.uniform(-1, 1, size=(sh.n, sh.h, sh.w, sh.c)).astype(np.float32)
+    labels = rng.integers(0, 10, size=sh.n).astype(np.int32)
+    return images, labels
+
+
+def test_peer_exchange_world1_equals_apply_grads():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1602_08124_b200 as V
+    from oracle import numeric
+    g = V.build_preset("inception_toy", 8)
+    cm = V.CostModel()
+    images, labels = _batch(g, 41)
+    outs = []
+    for peer in (False, True):
+        s, w = _session(V, numeric, g, cm)
+        s.set_batch(images, labels)
+        if peer:
+            s.peer_attach(0, [s.peer_export()])
+            s.step(LR, want_loss=False)
+            s.peer_exchange(LR, 1.0)
+        else:
+            s.step(LR, want_loss=False)
+            s.apply_grads(LR, 1.0)
+        s.synchronize()
+        outs.append({k: s.get_weights(k) for k in w})
+        if peer:
+            s.peer_detach()
+        del s
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[1][k]), k  # same SGD expression, bit-identical
+
+
+def _worker(rank, world, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_1602_08124_b200 as V
+        from oracle import numeric
+        from paper_1602_08124_b200.dist import PeerDataParallel
+        g = V.build_preset("inception_toy", 8)
+        cm = V.CostModel()
+        s, w = _session(V, numeric, g, cm)
+        dp = PeerDataParallel(s, world)
+        report = []
+        for it in range(2):
+            images, labels = _batch(g, 100 + 10 * it + rank)
+            s.set_batch(images, labels)
+            w0 = {k: s.get_weights(k) for k in w}
+            s.step(LR, want_loss=False)
+            s.synchronize()
+            grads = {k: s.get_grads(k) for k in w}
+            all_grads = [None] * world
+            dist.all_gather_object(all_grads, grads)
+            s.peer_exchange(LR, 1.0 / world)
+            s.synchronize()
+            w1 = {k: s.get_weights(k) for k in w}
+            all_w1 = [None] * world
+            dist.all_gather_object(all_w1, w1)
+            err = 0.0
+            same = True
+            for k in w:
+                acc = all_grads[0][k].copy()
+                for p in range(1, world):
+                    acc = acc + all_grads[p][k]  # rank order, fp32
+                # the kernel's step = float(lr) * float(1/N), then one fused
+                # multiply-add w - step*sum: exact in float64, rounded once
+                step = np.float32(np.float32(LR) * np.float32(1.0 / world))
+                ref = (w0[k].astype(np.float64) - np.float64(step) * acc.astype(np.float64)).astype(np.float32)
+                ulps = np.abs(w1[k] - ref) / np.spacing(np.maximum(np.abs(ref), np.float32(1e-30)))
+                err = max(err, float(np.max(ulps)))
+                same = same and all(np.array_equal(all_w1[p][k], w1[k]) for p in range(world))
+            report.append((err, same))
+        dp.close()
+        q.put((rank, report, None))
+        dist.destroy_process_group()
+    except Exception as e:  # surfaced by the parent
+        q.put((rank, None, repr(e)))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_exchange_multiprocess_same_device(world):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, report, exc in res:
+        assert exc is None, (rank, exc)
+        for err, same in report:
+            assert err <= 1.0, (rank, err)  # within one ulp of the fused reference
+            assert same, rank  # every rank holds bit-identical weights

@@ -59,6 +59,19 @@ def main():
     print(f"{'kernel':58s} {'n':>4s} {'ms':>9s} {'share':>6s} {'DRAM MB/launch':>15s}")
     for name, (n, t, rd, wr) in sorted(agg.items(), key=lambda x: -x[1][1]):
         print(f"{name[:58]:58s} {n:4d} {t:9.3f} {t / tot:6.1%} {(rd + wr) / n / 1e6:15.1f}")
+    if "--traffic-json" in sys.argv:
+        # DRAM bytes per conv-engine launch (bench.py's roofline "traffic")
+        import json
+        conv = [k for k in step if "tc_conv" in k["name"] or "c3tc" in k["name"]]
+        byt = sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0) for k in conv)
+        out = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+                         "--clock-control none, python bench.py --policies dyn --steps 1 --warmup 3 (last step): "
+                         + path.split("/")[-1],
+               "conv_launches": len(conv), "conv_dram_bytes_per_launch": byt / max(1, len(conv)),
+               "conv_ms_serialized": sum(k.get("gpu__time_duration.sum", 0) for k in conv),
+               "step_kernel_ms_serialized": tot}
+        with open(sys.argv[sys.argv.index("--traffic-json") + 1], "w") as f:
+            json.dump(out, f, indent=1)
 
 
 if __name__ == "__main__":
