@@ -9,6 +9,7 @@
 #include "kernels.h"
 #include "tc_conv.cuh"
 #include "tc_conv_persist.cuh"
+#include "tc_conv_halo.cuh"
 #include "tma_maps.h"
 
 namespace vdnnk {
@@ -296,8 +297,112 @@ bool use_persist(const ConvParams& p) {
   return p.kind == kFprop && p.Ncols > 64 && p.Ncols <= 128;
 }
 
+// Halo-reuse kernel (tc_conv_halo.cuh) for stride-1 k x k (k >= 3) FPROP /
+// DGRAD over one NHWC tensor with 32-multiple channels, when the padded input
+// row fits a TMA box (<= 256 pixels) and >= 75% of the 256 virtual rows of a
+// tile are real outputs. VDNN_HALO=0 disables.
+bool halo_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VDNN_HALO");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+bool halo_params(const ConvParams& p, HaloParams& h) {
+  if (!halo_enabled() || (p.kind != kFprop && p.kind != kDgrad)) return false;
+  if (p.nseg != 1 || !p.vec_in || p.stride != 1 || p.kh != p.kw || p.kh < 3) return false;
+  if (p.C % 32 != 0 || p.Cout % 32 != 0) return false;
+  std::memset(&h, 0, sizeof(h));
+  h.kind = p.kind;
+  h.N = p.N;
+  h.kh = p.kh;
+  h.kw = p.kw;
+  if (p.kind == kFprop) {
+    h.Hin = p.H, h.Win = p.W, h.Cin = p.C, h.pad = p.pad;
+    h.Hout = p.Ho, h.Wout = p.Wo, h.Cout = p.Cout;
+    h.out = p.y;
+    h.relu = p.relu;
+  } else {
+    if (p.seg[0].dx == nullptr || p.pad > p.kh - 1) return false;
+    h.Hin = p.Ho, h.Win = p.Wo, h.Cin = p.Cout, h.pad = p.kh - 1 - p.pad;
+    h.Hout = p.H, h.Wout = p.W, h.Cout = p.C;
+    h.out = p.seg[0].dx;
+    h.mask_x = p.seg[0].mask ? p.seg[0].x : nullptr;
+  }
+  // Where it wins (measured, VGG-16 b256 shapes): <= 128 output columns over
+  // >= 128 input channels, or 64 output columns (224x224x64 fprop/dgrad
+  // 356 -> 416 TFLOP/s, 112x112x128 599 -> 627, 112x112 dgrad 128 -> 64
+  // 243 -> 344). With 256+ columns the im2col BN=256 tiles are faster: the
+  // tensor core's shared-memory operand reads (64 wavefronts per
+  // M128xN128xK8, measured 87% busy) bound N=128 tiles, and N=256 MMAs read A
+  // once per 256 columns.
+  if (h.Cout > 128 || (h.Cout > 64 && h.Cin < 128)) return false;
+  h.accum = p.epi == kEpiAccum;
+  h.P = h.Win + 2 * h.pad;
+  if (h.P > 256 || h.Wout + h.kw - 1 != h.P) return false;
+  h.TH = 256 / h.P;
+  if (4 * h.TH * h.Wout < 3 * 256) return false;
+  h.nck = h.Cin / 32;
+  h.tiles_h = (h.Hout + h.TH - 1) / h.TH;
+  return true;
+}
+
+template <int BN, int AS, int BS, int KW>
+cudaError_t launch_halo(HaloParams& h, const ConvParams& p, cudaStream_t st) {
+  using L = HaloSmem<BN, AS, BS>;
+  alignas(64) CUtensorMap ta, tb;
+  std::memset(&ta, 0, sizeof(ta));
+  std::memset(&tb, 0, sizeof(tb));
+  const float* src = p.kind == kFprop ? p.seg[0].x : p.dy;
+  {
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(h.Cin), static_cast<cuuint64_t>(h.Win),
+                                static_cast<cuuint64_t>(h.Hin), static_cast<cuuint64_t>(h.N)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(h.Cin) * 4, static_cast<cuuint64_t>(h.Win) * h.Cin * 4,
+                                   static_cast<cuuint64_t>(h.Hin) * h.Win * h.Cin * 4};
+    const cuuint32_t box[4] = {32, static_cast<cuuint32_t>(h.P), static_cast<cuuint32_t>(h.TH), 1};
+    if (!encode_tiled(&ta, src, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorNotSupported;
+  }
+  if (p.kind == kFprop) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.KK), static_cast<cuuint64_t>(p.Cout)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.KK) * 4};
+    const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(BN)};
+    if (!encode_tiled(&tb, p.w, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorNotSupported;
+  } else {
+    const int taps = p.kh * p.kw;
+    const cuuint64_t d4[4] = {32, static_cast<cuuint64_t>(p.Cout), static_cast<cuuint64_t>(p.C / 32),
+                              static_cast<cuuint64_t>(taps)};
+    const cuuint64_t s4[3] = {static_cast<cuuint64_t>(taps) * p.C * 4, 128, static_cast<cuuint64_t>(p.C) * 4};
+    const cuuint32_t b4[4] = {32, 32, static_cast<cuuint32_t>(BN / 32), 1};
+    if (!encode_tiled(&tb, p.w, 4, d4, s4, b4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorNotSupported;
+  }
+  h.ntn = (h.Cout + BN - 1) / BN;
+  h.ntiles = h.N * h.tiles_h * h.ntn;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_halo_kernel<BN, AS, BS, KW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         L::kTotal);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  tc_conv_halo_kernel<BN, AS, BS, KW><<<std::min(h.ntiles, kNumSms), 192, L::kTotal, st>>>(h, ta, tb);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
+  if (!g_precise && !g_no_tma && splits == 1) {
+    HaloParams h;
+    if (halo_params(p, h)) {
+      cudaError_t e = cudaErrorNotSupported;
+      if (h.kw == 3)
+        e = p.Ncols <= 64 ? launch_halo<64, 4, 8, 3>(h, p, st) : launch_halo<128, 3, 7, 3>(h, p, st);
+      else if (h.kw == 5)
+        e = p.Ncols <= 64 ? launch_halo<64, 4, 8, 5>(h, p, st) : launch_halo<128, 3, 7, 5>(h, p, st);
+      if (e != cudaErrorNotSupported) return e;
+    }
+  }
   alignas(64) CUtensorMap ta, tb, tc;
   std::memset(&ta, 0, sizeof(ta));
   std::memset(&tb, 0, sizeof(tb));

@@ -243,6 +243,11 @@ def test_relu_and_softmax():
 LARGE = [
     (32, 56, 56, 64, 128),    # fprop tall BN=128, dgrad tall BN=64, wgrad BN=128
     (64, 56, 56, 256, 256),   # fprop/dgrad wide+tall (BN=256, BM=256), wgrad BN=256 KW=64
+    # halo-reuse fprop/dgrad (tc_conv_halo.cuh): one padded row per tile (P = 226),
+    # two rows (P = 114), eight rows (P = 30)
+    (2, 224, 224, 64, 64),
+    (4, 112, 112, 128, 128),
+    (8, 28, 28, 512, 512),
 ]
 
 
