@@ -1082,18 +1082,23 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTo
     }  // halves
   } else if (warp == 4) {
     // ---------------- MMA issuer ----------------
+    // The whole warp runs the loop so the descriptors are warp-uniform
+    // (uniform registers, no per-MMA waterfall loop); one elected lane
+    // issues. Issued from lane 0 alone, each MMA cost ~10-20 instructions,
+    // which bounded the N<=128 tiles.
     const bool a_mn = (p.kind == kWgrad);
     const bool b_mn = (p.kind != kFprop);
     const uint32_t idesc = make_idesc_tf32(BN, a_mn, b_mn);
-    if (lane == 0) {
-      for (int it = 0; it < nkb; ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(full_bar(s), ph);
-        if constexpr (!TMA) fence_proxy_async();  // cp.async/st.shared writes -> async proxy
-        tc_fence_after();
-        const uint32_t sa = base + s * L::kStage;
-        const uint32_t sb = sa + L::kABytes;
+    const bool leader = elect_one();
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      mbar_wait(full_bar(s), ph);
+      if constexpr (!TMA) fence_proxy_async();  // cp.async/st.shared writes -> async proxy
+      tc_fence_after();
+      const uint32_t sa = base + s * L::kStage;
+      const uint32_t sb = sa + L::kABytes;
+      if (leader) {
 #pragma unroll
         for (int kk = 0; kk < KW / 8; ++kk) {
           // K-major: advance 32 B inside the swizzled row; MN-major: next 8 K
@@ -1118,8 +1123,9 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTo
         }
         tc_commit(empty_bar(s));
       }
-      tc_commit(accum_bar);
+      __syncwarp();
     }
+    if (leader) tc_commit(accum_bar);
     __syncwarp();
   }
   tc_fence_before();

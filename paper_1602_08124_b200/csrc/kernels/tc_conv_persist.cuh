@@ -100,21 +100,23 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
     __syncwarp();
   } else if (warp == 4) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_tf32(BN, false, p.kind != kFprop);
-      const bool b_mn = p.kind != kFprop;
-      int it = 0, lt = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
-        const int acc = lt & 1;
-        if (lt >= 2) mbar_wait(tempty_bar(acc), ((lt >> 1) & 1) ^ 1);
+    // whole warp in the loop (warp-uniform descriptors), one elected lane issues
+    const uint32_t idesc = make_idesc_tf32(BN, false, p.kind != kFprop);
+    const bool b_mn = p.kind != kFprop;
+    const bool leader = elect_one();
+    int it = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      if (lt >= 2) mbar_wait(tempty_bar(acc), ((lt >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d0 = tmem + acc * L::kAccCols;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(full_bar(s), (it / STAGES) & 1);
         tc_fence_after();
-        const uint32_t d0 = tmem + acc * L::kAccCols;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(full_bar(s), (it / STAGES) & 1);
-          tc_fence_after();
-          const uint32_t sa = base + s * L::kStage;
-          const uint32_t sb = sa + L::kABytes;
+        const uint32_t sa = base + s * L::kStage;
+        const uint32_t sb = sa + L::kABytes;
+        if (leader) {
 #pragma unroll
           for (int kk = 0; kk < kBK / 8; ++kk) {
             const uint64_t ad = make_sdesc(sa + kk * 32, 16, 1024, kSw128);
@@ -127,10 +129,11 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
           }
           tc_commit(empty_bar(s));
         }
-        tc_commit(tfull_bar(acc));
+        __syncwarp();
       }
+      if (leader) tc_commit(tfull_bar(acc));
+      __syncwarp();
     }
-    __syncwarp();
   } else {
     // ---------------- epilogue ----------------
     const int row = warp * 32 + lane;
