@@ -330,6 +330,12 @@ vdnn_status vdnn_kernel_conv_dgrad(const vdnn_conv_desc* d, const float* w, cons
 vdnn_status vdnn_kernel_conv_wgrad(const vdnn_conv_desc* d, const float* dy, float* w, float lr, float* dw_out,
                                    float* ws, size_t ws_bytes, void* stream);
 size_t vdnn_kernel_conv_wgrad_ws_bytes(const vdnn_conv_desc* d);
+/* fprop with a workspace: outputs with fewer tiles than SMs (FC layers) run a deterministic split-K
+   (partial slabs + ordered reduce with the bias/ReLU epilogue). ws_bytes >= vdnn_kernel_conv_fprop_ws_bytes
+   uses the full split (0 when the shape does not split). */
+vdnn_status vdnn_kernel_conv_fprop_ws(const vdnn_conv_desc* d, const float* w, const float* bias, float* y, float* ws,
+                                      size_t ws_bytes, void* stream);
+size_t vdnn_kernel_conv_fprop_ws_bytes(const vdnn_conv_desc* d);
 /* Calling-thread switch for the kernel-level conv entry points: 1 = 3xTF32 (fp32-accurate), 0 = TF32. */
 void vdnn_kernel_set_precise(int32_t on);
 /* Calling-thread switch: 1 = TMA producers where eligible (default), 0 = cp.async gathers everywhere. */

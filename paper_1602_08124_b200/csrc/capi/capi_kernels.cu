@@ -85,6 +85,19 @@ vdnn_status vdnn_kernel_conv_wgrad(const vdnn_conv_desc* d, const float* dy, flo
                      "conv_wgrad");
 }
 
+vdnn_status vdnn_kernel_conv_fprop_ws(const vdnn_conv_desc* d, const float* w, const float* bias, float* y, float* ws,
+                                      size_t ws_bytes, void* stream) {
+  vdnnk::ConvArgs a;
+  if (!to_args(d, a)) return fail(VDNN_INVALID_ARGUMENT, "bad conv descriptor");
+  return cuda_status(vdnnk::conv_fprop(a, w, bias, y, false, static_cast<cudaStream_t>(stream), ws, ws_bytes),
+                     "conv_fprop");
+}
+size_t vdnn_kernel_conv_fprop_ws_bytes(const vdnn_conv_desc* d) {
+  vdnnk::ConvArgs a;
+  if (!to_args(d, a)) return 0;
+  return vdnnk::conv_fprop_ws_bytes(a);
+}
+
 size_t vdnn_kernel_conv_wgrad_ws_bytes(const vdnn_conv_desc* d) {
   vdnnk::ConvArgs a;
   if (!to_args(d, a)) return 0;

@@ -141,6 +141,15 @@ bool encode_out(CUtensorMap* m, const void* base, int64_t rows, int cols) {
   return encode_tiled(m, base, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+// 3D [splits][rows][cols] fp32 partial-sum slabs (split-K fprop), 128 x 32 boxes.
+bool encode_out3(CUtensorMap* m, const void* base, int splits, int64_t rows, int cols) {
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(splits)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 4, static_cast<cuuint64_t>(rows) * cols * 4};
+  const cuuint32_t box[3] = {32, static_cast<cuuint32_t>(kBM), 1};
+  return encode_tiled(m, base, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 namespace {
 
 // Build the maps of the TMA producer (and output); false = cp.async gathers.
@@ -149,7 +158,11 @@ bool make_maps(ConvParams& p, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* tc)
   if (p.nseg != 1 || !p.vec_in || !p.vec_out || p.kh != p.kw) return false;
   const float* x = p.seg[0].x;
   if (p.kind == kFprop) {
-    if (!encode_out(tc, p.y, p.M, p.Cout)) return false;
+    if (p.epi == kEpiPartial) {
+      if (!encode_out3(tc, p.out, p.splits, p.M, p.Cout)) return false;
+    } else if (!encode_out(tc, p.y, p.M, p.Cout)) {
+      return false;
+    }
     if (!encode_im2col(ta, x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, kBM, CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.KK), static_cast<cuuint64_t>(p.Cout)};
@@ -211,7 +224,7 @@ bool use_wide(int kind) { return (wide_mask() >> kind) & 1; }
 // the resident CTAs per SM neither starves the grid nor exposes epilogues.
 bool wide_ok(const ConvParams& p) {
   if (p.Ncols < 256 || !use_wide(p.kind)) return false;
-  if (p.kind == kWgrad) return true;
+  if (p.kind == kWgrad) return static_cast<int64_t>(p.kblocks) * p.wkw >= 2048;  // mirrors wgrad_cfg
   const int64_t tiles = static_cast<int64_t>((p.M + kBM - 1) / kBM) * ((p.Ncols + 255) / 256);
   static const int min_cols = [] {
     const char* e = std::getenv("VDNN_WIDE_MIN");
@@ -411,6 +424,12 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
     if (p.Ncols <= 64) return launch_bn<64, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
     return launch_bn<128, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
   }
+  if (p.kind == kFprop && p.epi == kEpiPartial) {
+    // split-K fprop (FC layers: few output tiles, long K): BN=128 TMA tiles,
+    // partial slabs through the 3-D output map
+    if (make_maps<128>(p, &ta, &tb, &tc)) return launch_bn<128, kStages, false, true>(p, ta, tb, tc, splits, st);
+    return cudaErrorNotSupported;
+  }
   if (p.kind == kWgrad && p.wkw == 64) {
     // 64-pixel stages: half the im2col TMA ops per FLOP (their issue rate,
     // not bytes, bounds the 32-pixel wgrad pipeline); one CTA per SM
@@ -480,7 +499,10 @@ WCfg wgrad_cfg(const ConvParams& p, int64_t pixels) {
   WCfg c;
   const int ncols = p.Cout;
   const bool tma = !g_precise && !g_no_tma && p.nseg == 1 && p.vec_in && p.vec_out && p.kh == p.kw;
-  c.bn = (ncols >= 256 && use_wide(kWgrad) && tma) ? 256 : (ncols <= 64 ? 64 : 128);
+  // A short reduction (FC layers: K = batch) makes every tile mostly
+  // epilogue (the SGD read-modify-write of its weights); BN=128 tiles run two
+  // CTAs per SM so one CTA's epilogue overlaps the other's loads and MMAs.
+  c.bn = (ncols >= 256 && use_wide(kWgrad) && tma && pixels >= 2048) ? 256 : (ncols <= 64 ? 64 : 128);
   c.bm = (tma && ((tall_mask() >> kWgrad) & 1) && c.bn == 256 && pixels >= 100000) ? 256 : kBM;
   const bool one_per_sm = c.bn > 128 || (c.bm > kBM && tall_deep());
   c.slots = one_per_sm ? kNumSms : 2 * kNumSms;
@@ -530,12 +552,9 @@ void set_tma(bool on) { g_no_tma = !on; }
 bool precise() { return g_precise; }
 void count_launch(uint64_t k) { g_launches.fetch_add(k); }
 
-cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
-                       cudaStream_t st) {
-  if (!accumulate && bias == nullptr && c3tc_fprop_eligible(a)) return c3tc_fprop(a, w, y, st);
-  if (!accumulate && bias == nullptr && smallc_eligible(a)) return smallc_fprop(a, w, y, st);
-  ConvParams p;
-  if (!build_common(a, p)) return cudaErrorInvalidValue;
+namespace {
+bool fprop_params(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate, ConvParams& p) {
+  if (!build_common(a, p)) return false;
   p.kind = kFprop;
   p.relu = a.relu_out;
   p.epi = accumulate ? kEpiAccum : kEpiStore;
@@ -546,7 +565,87 @@ cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, flo
   p.Ncols = a.cout;
   p.kblocks = p.vec_in ? a.kh * a.kw * p.nchunk : (p.KK + kBK - 1) / kBK;
   p.kb_per_split = p.kblocks;
-  return launch(p, 1, st);
+  return true;
+}
+
+// Split-K factor for FPROP: only when the output has fewer BN=128 tiles than
+// SMs (FC layers at small batch: FC6 of VGG-16 b256 is 2 x 32 tiles over a
+// 25,088-long reduction) and the operands take the TMA path. Same time model
+// as WGRAD, two CTAs per SM.
+int fprop_splits(const ConvParams& p) {
+  if (g_precise || g_no_tma || p.epi != kEpiStore || p.nseg != 1 || !p.vec_in || !p.vec_out || p.kh != p.kw)
+    return 1;
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ncols + 127) / 128);
+  if (tiles >= kNumSms || p.kblocks < 64) return 1;
+  return pick_splits(tiles, p.kblocks, 2 * kNumSms, 128, static_cast<int64_t>(p.M) * p.Cout);
+}
+
+__global__ void fprop_reduce_kernel(const float* __restrict__ part, int splits, int64_t m, int cout,
+                                    const float* __restrict__ bias, int relu, float* __restrict__ y) {
+  const int64_t total4 = m * cout / 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 s = reinterpret_cast<const float4*>(part)[i];
+    for (int z = 1; z < splits; ++z) {  // fixed order: deterministic
+      const float4 q = reinterpret_cast<const float4*>(part + z * m * cout)[i];
+      s.x += q.x;
+      s.y += q.y;
+      s.z += q.z;
+      s.w += q.w;
+    }
+    if (bias) {
+      const int o = static_cast<int>((i * 4) % cout);
+      s.x += bias[o];
+      s.y += bias[o + 1];
+      s.z += bias[o + 2];
+      s.w += bias[o + 3];
+    }
+    if (relu) {
+      s.x = fmaxf(s.x, 0.f);
+      s.y = fmaxf(s.y, 0.f);
+      s.z = fmaxf(s.z, 0.f);
+      s.w = fmaxf(s.w, 0.f);
+    }
+    reinterpret_cast<float4*>(y)[i] = s;
+  }
+}
+}  // namespace
+
+size_t conv_fprop_ws_bytes(const ConvArgs& a) {
+  if (c3tc_fprop_eligible(a) || smallc_eligible(a)) return 0;
+  ConvParams p;
+  if (!fprop_params(a, nullptr, nullptr, nullptr, false, p)) return 0;
+  const int s = fprop_splits(p);
+  return s > 1 ? static_cast<size_t>(s) * p.M * p.Cout * sizeof(float) : 0;
+}
+
+cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
+                       cudaStream_t st, float* ws, size_t ws_bytes) {
+  if (!accumulate && bias == nullptr && c3tc_fprop_eligible(a)) return c3tc_fprop(a, w, y, st);
+  if (!accumulate && bias == nullptr && smallc_eligible(a)) return smallc_fprop(a, w, y, st);
+  ConvParams p;
+  if (!fprop_params(a, w, bias, y, accumulate, p)) return cudaErrorInvalidValue;
+  int splits = ws ? fprop_splits(p) : 1;
+  const size_t per = static_cast<size_t>(p.M) * p.Cout * sizeof(float);
+  if (splits > 1) splits = static_cast<int>(std::min<size_t>(splits, ws_bytes / per));
+  if (splits > 1) {
+    p.kb_per_split = (p.kblocks + splits - 1) / splits;
+    splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;
+  }
+  if (splits <= 1) {
+    p.kb_per_split = p.kblocks;
+    return launch(p, 1, st);
+  }
+  p.epi = kEpiPartial;
+  p.out = ws;
+  p.splits = splits;
+  cudaError_t e = launch(p, splits, st);
+  if (e != cudaSuccess) return e;
+  const int64_t total4 = static_cast<int64_t>(p.M) * p.Cout / 4;
+  const int blocks = static_cast<int>(std::min<int64_t>((total4 + 255) / 256, 4 * kNumSms));
+  fprop_reduce_kernel<<<blocks, 256, 0, st>>>(ws, splits, p.M, p.Cout, bias, p.relu, y);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st) {

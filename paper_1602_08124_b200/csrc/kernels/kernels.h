@@ -36,8 +36,11 @@ void set_precise(bool on);
 bool precise();
 // TMA producers (im2col / tiled tensor maps) where eligible; off = cp.async gathers everywhere.
 void set_tma(bool on);
+// `ws` (optional, conv_fprop_ws_bytes(a) bytes) enables a deterministic
+// split-K for outputs with fewer tiles than SMs (FC layers).
 cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
-                       cudaStream_t st);
+                       cudaStream_t st, float* ws = nullptr, size_t ws_bytes = 0);
+size_t conv_fprop_ws_bytes(const ConvArgs& a);
 cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st);
 // Weight gradient. If dw_out is null: fused SGD  w_mut -= lr * dW.
 // Otherwise dW is written to dw_out (KRSC layout) and w_mut is untouched.

@@ -79,6 +79,7 @@ struct ConvParams {
   float lr;
   // GEMM geometry
   int M, Ncols, kblocks, kb_per_split;
+  int splits;                 // split-K fprop: number of partial slabs
   int KK;                     // kh*kw*C: weight row length
 };
 
@@ -121,6 +122,11 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map), "r"(src),
                  "r"(x), "r"(y)
                  : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map), "r"(src),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
 }
 __device__ __forceinline__ void bulk_commit_and_drain() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -919,11 +925,12 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTo
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0.f;
         }
-        if (p.kind == kFprop && p.bias) {
+        const bool partial = p.epi == kEpiPartial;  // split-K fprop: raw partial sums
+        if (p.kind == kFprop && p.bias && !partial) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += (nb + i < p.Cout) ? p.bias[nb + i] : 0.f;
         }
-        if (p.kind == kFprop && p.relu) {
+        if (p.kind == kFprop && p.relu && !partial) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
         }
@@ -956,8 +963,12 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTo
       asm volatile("bar.sync 2, 128;" ::: "memory");
       if (threadIdx.x == 0) {
         for (int cg = 0; cg < BN / 32; ++cg)
-          if (n0 + cg * 32 < p.Ncols)
-            tma_store_2d(&tma_c, base + cg * 16384, n0 + cg * 32, m0 + h * kBM, p.epi == kEpiAccum);
+          if (n0 + cg * 32 < p.Ncols) {
+            if (p.epi == kEpiPartial)  // split z's slab of the [splits][M][Cout] partials
+              tma_store_3d(&tma_c, base + cg * 16384, n0 + cg * 32, m0 + h * kBM, static_cast<int>(blockIdx.z));
+            else
+              tma_store_2d(&tma_c, base + cg * 16384, n0 + cg * 32, m0 + h * kBM, p.epi == kEpiAccum);
+          }
         bulk_commit_and_drain();
       }
       if (kHalves > 1) asm volatile("bar.sync 2, 128;" ::: "memory");  // staging read out before reuse

@@ -129,6 +129,11 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
     if (l.kind != Kind::Conv && l.kind != Kind::Fc) continue;
     need = std::max(need, vdnnk::conv_wgrad_ws_bytes(conv_args(s.layer, s.in_off, nullptr)));
   }
+  for (const FwdStep& s : fwd_) {  // split-K FC fprop partials share the buffer
+    const Node& l = g_.at(s.layer);
+    if (l.kind != Kind::Conv && l.kind != Kind::Fc) continue;
+    need = std::max(need, vdnnk::conv_fprop_ws_bytes(conv_args(s.layer, s.in_off, nullptr)));
+  }
   splitk_bytes_ = std::min<size_t>(need, size_t{256} << 20);
   if (splitk_bytes_ > 0) check(cudaMalloc(&splitk_, splitk_bytes_), "cudaMalloc(split-K)");
   scratch_bytes_ += splitk_bytes_;
@@ -554,7 +559,7 @@ void Session::run_fwd(const FwdStep& s, float lr) {
       vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
       a.relu_out = s.relu ? 1 : 0;
       const float* bias = l.kind == Kind::Fc ? F(s.w_off) + g_.fc_inputs(s.layer) * l.out : nullptr;
-      check(vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_), "conv_fprop");
+      check(vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_, splitk_, splitk_bytes_), "conv_fprop");
       break;
     }
     case Kind::Actv:

@@ -123,6 +123,14 @@ def _conv_case(case):
     torch.cuda.synchronize()
     xr, wr, yr = _ref_conv(xs, wt, stride, pad)
     _close(y, yr.permute(0, 2, 3, 1))
+    fws = L.lib().vdnn_kernel_conv_fprop_ws_bytes(C.byref(d))
+    if fws > 0:  # split-K fprop (few output tiles, long reduction)
+        ws = torch.empty(fws // 4, device=dev)
+        y2 = torch.full_like(y, float("nan"))
+        L.call("vdnn_kernel_conv_fprop_ws", C.byref(d), C.c_void_p(wt.data_ptr()), None, C.c_void_p(y2.data_ptr()),
+               C.c_void_p(ws.data_ptr()), C.c_size_t(fws), None)
+        torch.cuda.synchronize()
+        _close(y2, yr.permute(0, 2, 3, 1))
 
     dy = torch.randn(n, ho, wo, cout, generator=g).to(dev)
     yr.backward(dy.double().cpu().permute(0, 3, 1, 2))
@@ -235,6 +243,36 @@ def test_relu_and_softmax():
     lr_.backward()
     assert abs(loss.item() - lr_.item()) < 1e-5 * max(1.0, abs(lr_.item()))
     torch.testing.assert_close(grad.double().cpu(), zr.grad, rtol=1e-4, atol=1e-7)
+
+
+def test_fc_fprop_split_k_with_bias():
+    """VGG-16 FC6 at batch 256 (2 x 32 output tiles over K = 25,088): the
+    split-K partial slabs + ordered reduce with the fused bias, against the
+    unsplit kernel and a float64 reference; deterministic across calls."""
+    dev = _dev()
+    n, k, o = 256, 25088, 4096
+    g = torch.Generator(device=dev).manual_seed(7)
+    x = torch.randn(n, 1, 1, k, device=dev, generator=g)
+    wt = torch.randn(o, 1, 1, k, device=dev, generator=g) * (2.0 / k) ** 0.5
+    b = torch.randn(o, device=dev, generator=g)
+    d = _desc(n, 1, 1, [x], [k], o, 1, 1, 0)
+    fws = L.lib().vdnn_kernel_conv_fprop_ws_bytes(C.byref(d))
+    assert fws > 0
+    ws = torch.empty(fws // 4, device=dev)
+    outs = []
+    for _ in range(2):
+        y = torch.full((n, 1, 1, o), float("nan"), device=dev)
+        L.call("vdnn_kernel_conv_fprop_ws", C.byref(d), C.c_void_p(wt.data_ptr()), C.c_void_p(b.data_ptr()),
+               C.c_void_p(y.data_ptr()), C.c_void_p(ws.data_ptr()), C.c_size_t(fws), None)
+        outs.append(y)
+    y1 = torch.empty_like(outs[0])
+    L.call("vdnn_kernel_conv_fprop", C.byref(d), C.c_void_p(wt.data_ptr()), C.c_void_p(b.data_ptr()),
+           C.c_void_p(y1.data_ptr()), None)
+    torch.cuda.synchronize()
+    ref = (x.double().reshape(n, k) @ wt.double().reshape(o, k).T + b.double()).reshape(n, 1, 1, o)
+    assert torch.equal(outs[0], outs[1])
+    _close(outs[0], ref)
+    _close(y1, ref)
 
 
 # Shapes large enough to select the production tile variants: tall (BM=256)
