@@ -208,6 +208,40 @@ __global__ void maxpool_fwd_kernel(const __grid_constant__ PoolDev d, float* __r
   }
 }
 
+// 2x2 / stride-2 windows over one NHWC tensor (every VGG pool): one output
+// row per blockIdx.y, 4 channels per thread, the four window loads issued
+// before any compare (the generic loop serialises them), 32-bit index math.
+// Same scan order and strict '>' as the generic kernel: bit-identical output.
+__global__ void __launch_bounds__(256) maxpool2x2_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int h,
+                                                            int w, int c, int ho, int wo) {
+  const int cv = c >> 2;
+  const int row = blockIdx.y;  // n * ho + oh
+  const int n = row / ho, oh = row - n * ho;
+  const float4* x0 = reinterpret_cast<const float4*>(x + (static_cast<size_t>(n) * h + 2 * oh) * w * c);
+  const float4* x1 = x0 + static_cast<size_t>(w) * cv;
+  float4* yr = reinterpret_cast<float4*>(y + static_cast<size_t>(row) * wo * c);
+  const int per_row = wo * cv;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < per_row; i += gridDim.x * blockDim.x) {
+    const int ow = i / cv, c4 = i - ow * cv;
+    const int off = 2 * ow * cv + c4;
+    const float4 a = __ldcs(x0 + off), b = __ldcs(x0 + off + cv), e = __ldcs(x1 + off), f = __ldcs(x1 + off + cv);
+    float4 m = a;
+    m.x = b.x > m.x ? b.x : m.x;
+    m.y = b.y > m.y ? b.y : m.y;
+    m.z = b.z > m.z ? b.z : m.z;
+    m.w = b.w > m.w ? b.w : m.w;
+    m.x = e.x > m.x ? e.x : m.x;
+    m.y = e.y > m.y ? e.y : m.y;
+    m.z = e.z > m.z ? e.z : m.z;
+    m.w = e.w > m.w ? e.w : m.w;
+    m.x = f.x > m.x ? f.x : m.x;
+    m.y = f.y > m.y ? f.y : m.y;
+    m.z = f.z > m.z ? f.z : m.z;
+    m.w = f.w > m.w ? f.w : m.w;
+    yr[i] = m;
+  }
+}
+
 static bool pool_vec4(const PoolDev& d) {
   for (int i = 0; i < d.nseg; ++i)
     if (d.c[i] % 4 != 0) return false;
@@ -218,6 +252,14 @@ cudaError_t maxpool_fwd(const PoolArgs& a, float* y, cudaStream_t st) {
   const PoolDev d = to_dev(a);
   const size_t total = static_cast<size_t>(d.n) * d.ho * d.wo * d.ctot;
   if (total == 0) return cudaSuccess;
+  if (d.nseg == 1 && d.window == 2 && d.stride == 2 && d.c[0] % 4 == 0 &&
+      static_cast<int64_t>(d.n) * d.ho <= 65535) {
+    const int per_row = d.wo * d.c[0] / 4;
+    const dim3 grid(static_cast<unsigned>((per_row + 255) / 256), static_cast<unsigned>(d.n * d.ho));
+    maxpool2x2_fwd_kernel<<<grid, 256, 0, st>>>(d.x[0], y, d.h, d.w, d.c[0], d.ho, d.wo);
+    count_launch();
+    return cudaGetLastError();
+  }
   if (pool_vec4(d))
     maxpool_fwd_kernel<4><<<grid_for(total / 4, 2), kThreads, 0, st>>>(d, y);
   else
