@@ -10,6 +10,7 @@
 #include "tc_conv.cuh"
 #include "tc_conv_persist.cuh"
 #include "tc_conv_halo.cuh"
+#include "tc_conv_pair.cuh"
 #include "tma_maps.h"
 
 namespace vdnnk {
@@ -403,8 +404,53 @@ cudaError_t launch_halo(HaloParams& h, const ConvParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// CTA-pair kernel (tc_conv_pair.cuh) for FPROP / DGRAD with >= 256 output
+// columns and at least two tiles of 256 x 256 per pair. VDNN_PAIR=0 disables.
+bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VDNN_PAIR");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <int STAGES>
+cudaError_t launch_pair(ConvParams& p, cudaStream_t st) {
+  using L = PairSmem<STAGES>;
+  alignas(64) CUtensorMap ta, tb, tc;
+  std::memset(&ta, 0, sizeof(ta));
+  std::memset(&tb, 0, sizeof(tb));
+  std::memset(&tc, 0, sizeof(tc));
+  // per-CTA halves: 128 A rows, 128 B rows (fprop) / 4 MN chunks (dgrad)
+  if (!make_maps<128>(p, &ta, &tb, &tc)) return cudaErrorNotSupported;
+  if (p.kind == kDgrad && !p.tma_b_merged) return cudaErrorNotSupported;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(tc_conv_pair_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((p.M + 255) / 256) * ((p.Ncols + 255) / 256);
+  const int grid = 2 * std::min(tiles, kNumSms / 2);
+  tc_conv_pair_kernel<STAGES><<<grid, 192, L::kTotal, st>>>(p, ta, tb, tc);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
+  if (!g_precise && !g_no_tma && splits == 1 && pair_enabled() && (p.kind == kFprop || p.kind == kDgrad) &&
+      p.epi != kEpiPartial && p.Ncols >= 256 && p.Ncols % 128 == 0 &&
+      static_cast<int64_t>((p.M + 255) / 256) * (p.Ncols / 256) >= kNumSms) {
+    static const int stages = [] {
+      const char* e = std::getenv("VDNN_PAIR_STAGES");
+      return e ? std::atoi(e) : 5;
+    }();
+    const cudaError_t e = stages == 6 ? launch_pair<6>(p, st) : launch_pair<5>(p, st);
+    if (e != cudaErrorNotSupported) return e;
+    p.tma_b_merged = 0;
+  }
   if (!g_precise && !g_no_tma && splits == 1) {
     HaloParams h;
     if (halo_params(p, h)) {

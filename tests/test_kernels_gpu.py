@@ -286,6 +286,10 @@ LARGE = [
     (2, 224, 224, 64, 64),
     (4, 112, 112, 128, 128),
     (8, 28, 28, 512, 512),
+    # CTA-pair (cta_group::2) fprop/dgrad: 256 x 256 tiles over >= 148 tiles,
+    # and a 384-column layer whose second tile leaves the peer's B half empty
+    (32, 28, 28, 512, 512),
+    (64, 28, 28, 384, 384),
 ]
 
 
