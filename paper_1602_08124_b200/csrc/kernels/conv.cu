@@ -438,8 +438,35 @@ cudaError_t launch_pair(ConvParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int STAGES, int KW>
+cudaError_t launch_wgrad_pair(ConvParams& p, int splits, cudaStream_t st) {
+  using L = WgradPairSmem<STAGES, KW>;
+  alignas(64) CUtensorMap ta, tb, tc;
+  std::memset(&ta, 0, sizeof(ta));
+  std::memset(&tb, 0, sizeof(tb));
+  std::memset(&tc, 0, sizeof(tc));
+  if (!make_maps<128, KW>(p, &ta, &tb, &tc)) return cudaErrorNotSupported;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_wgrad_pair_kernel<STAGES, KW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         L::kTotal);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int work = ((p.M + 255) / 256) * ((p.Ncols + 255) / 256) * splits;
+  const int grid = 2 * std::min(work, kNumSms / 2);
+  tc_wgrad_pair_kernel<STAGES, KW><<<grid, 192, L::kTotal, st>>>(p, ta, tb, splits);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
+  if (p.kind == kWgrad && p.use_pair && !g_precise && !g_no_tma) {
+    const cudaError_t e = p.wkw == 64 ? launch_wgrad_pair<3, 64>(p, splits, st) : launch_wgrad_pair<6, kBK>(p, splits, st);
+    if (e != cudaErrorNotSupported) return e;
+    p.tma_b_merged = 0;
+  }
   if (!g_precise && !g_no_tma && splits == 1 && pair_enabled() && (p.kind == kFprop || p.kind == kDgrad) &&
       p.epi != kEpiPartial && p.Ncols >= 256 && p.Ncols % 128 == 0 &&
       static_cast<int64_t>((p.M + 255) / 256) * (p.Ncols / 256) >= kNumSms) {
@@ -537,10 +564,13 @@ bool wgrad_wide_k() {
 // Tile shape and resident CTAs the wgrad launch will use (mirrors launch()).
 struct WCfg {
   int bn, bm, slots, kw;
+  bool pair;
 };
 // Tall wgrad tiles pay off only with wide (BN=256) tiles over many pixels
 // (measured: +37% at 56x56x256, neutral at 28x28x512, -5..-20% at 14x14 or
 // with 64/128-wide tiles, where the extra im2col boxes per stage dominate).
+int wgrad_rows(const ConvParams& p) { return p.vec_in ? p.kh * p.kw * p.nchunk * 32 : p.KK; }
+
 WCfg wgrad_cfg(const ConvParams& p, int64_t pixels) {
   WCfg c;
   const int ncols = p.Cout;
@@ -553,6 +583,20 @@ WCfg wgrad_cfg(const ConvParams& p, int64_t pixels) {
   const bool one_per_sm = c.bn > 128 || (c.bm > kBM && tall_deep());
   c.slots = one_per_sm ? kNumSms : 2 * kNumSms;
   c.kw = kBK;
+  c.pair = false;
+  // CTA pair (M = 256 weight rows x N = 256 output channels per pair)
+  if (tma && pair_enabled() && ncols >= 256 && pixels >= 2048 && wgrad_rows(p) >= 256) {
+    c.pair = true;
+    c.bn = 256;
+    c.bm = 256;
+    c.slots = kNumSms / 2;
+    static const int kw = [] {
+      const char* e = std::getenv("VDNN_PAIR_WGRAD_KW");
+      return e ? std::atoi(e) : 64;
+    }();
+    c.kw = kw == 32 ? kBK : 64;
+    return c;
+  }
   // 64-pixel stages (opt-in, VDNN_WGRAD_KW=64): they halve the im2col boxes
   // per FLOP, which paid +18..42% while the producer thread recomputed every
   // box coordinate with integer divisions; with the incremental producer the
@@ -566,7 +610,6 @@ WCfg wgrad_cfg(const ConvParams& p, int64_t pixels) {
   return c;
 }
 
-int wgrad_rows(const ConvParams& p) { return p.vec_in ? p.kh * p.kw * p.nchunk * 32 : p.KK; }
 
 // Split-K factor for WGRAD from a small time model: the main loop runs in
 // ceil(tiles*s / slots) waves of ceil(kblocks/s) K blocks (~4*BN cycles each
@@ -770,6 +813,7 @@ cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float l
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
   const WCfg c = wgrad_cfg(p, P);
   p.wkw = c.kw;
+  p.use_pair = c.pair ? 1 : 0;
   p.kblocks = static_cast<int>((P + c.kw - 1) / c.kw);
   const int tiles = ((p.M + c.bm - 1) / c.bm) * ((a.cout + c.bn - 1) / c.bn);
   int splits = pick_splits(tiles, p.kblocks, c.slots, c.bn * c.bm / kBM * c.kw / kBK,

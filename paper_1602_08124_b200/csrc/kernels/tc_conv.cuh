@@ -80,6 +80,7 @@ struct ConvParams {
   // GEMM geometry
   int M, Ncols, kblocks, kb_per_split;
   int splits;                 // split-K fprop: number of partial slabs
+  int use_pair;               // wgrad: CTA-pair kernel (tc_conv_pair.cuh)
   int KK;                     // kh*kw*C: weight row length
 };
 

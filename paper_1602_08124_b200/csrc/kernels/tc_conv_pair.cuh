@@ -80,6 +80,15 @@ __device__ __forceinline__ void tma_load_im2col_pair(uint32_t dst, const CUtenso
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y,
+                                                 int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
 template <int STAGES>
 struct PairSmem {
   static constexpr int kABytes = kBM * 128;  // this CTA's 128 A rows x 32 fp32
@@ -282,6 +291,207 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();  // the peer's MMAs / barrier traffic into this CTA are over
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+// WGRAD on a CTA pair: D[(tap, ci)][co] over M = 256 weight rows (CTA rank r
+// holds rows m0 + 128r: four 32-row MN chunks of X im2col boxes) x N = 256
+// output channels (rank r holds dY columns n0 + 128r), K = KW pixels per
+// stage, both operands MN-major. Work items are (tile, split) pairs walked
+// persistently; the epilogue writes split-K partials or applies SGD / writes
+// dW exactly like tc_conv_kernel's WGRAD epilogue.
+template <int STAGES, int KW>
+struct WgradPairSmem {
+  static constexpr int kABytes = kBM * KW * 4;
+  static constexpr int kBBytes = 128 * KW * 4;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kTotal = STAGES * kStage + 1024 + 256;
+  static constexpr int kAccCols = 256;
+};
+
+template <int STAGES, int KW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    tc_wgrad_pair_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tma_a,
+                         const __grid_constant__ CUtensorMap tma_b, int splits) {
+  using L = WgradPairSmem<STAGES, KW>;
+  constexpr int BN = 256;
+  constexpr int kTmemCols = 2 * L::kAccCols;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bars = base + STAGES * L::kStage;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * STAGES + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * STAGES + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = static_cast<int>(blockIdx.x >> 1), npairs = static_cast<int>(gridDim.x >> 1);
+  const int ntn = (p.Ncols + BN - 1) / BN;
+  const int nwork = ((p.M + 255) / 256) * ntn * splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  // split-major order: the pairs running concurrently share one pixel range
+  // (same split) across tiles, so its X / dY rows are read from DRAM once and
+  // re-hit in L2 (tile-major order re-read them once per tile)
+  const int ntiles = ((p.M + 255) / 256) * ntn;
+  auto decode = [&](int w, int& m0, int& n0, int& z, int& kb0, int& kb1) {
+    z = w / ntiles;
+    const int tile = w - z * ntiles;
+    m0 = (tile / ntn) * 256 + static_cast<int>(rank) * kBM;
+    n0 = (tile % ntn) * BN;
+    kb0 = z * p.kb_per_split;
+    kb1 = kb0 + p.kb_per_split < p.kblocks ? kb0 + p.kb_per_split : p.kblocks;
+  };
+
+  if (warp == 5) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+      int it = 0;
+      for (int w = pair; w < nwork; w += npairs) {
+        int m0, n0, z, kb0, kb1;
+        decode(w, m0, n0, z, kb0, kb1);
+        const int nb = n0 + static_cast<int>(rank) * 128;
+        TmaProducer<128, kBM, KW> tp;
+        tp.init(p, m0, kb0);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
+          const uint32_t sa = base + s * L::kStage, sb = sa + L::kABytes;
+          const uint32_t lbar = map_to_rank(full_bar(s), 0);
+          if (rank == 0) mbar_expect_tx(full_bar(s), 2 * L::kStage);
+          const int iw = tp.pw * p.stride - p.pad, ih = tp.ph * p.stride - p.pad;
+#pragma unroll
+          for (int mc = 0; mc < kBM / 32; ++mc)
+            tma_load_im2col_pair(sa + mc * (KW * 128), &tma_a, lbar, tp.wch[mc], iw, ih, tp.pn, tp.ws[mc],
+                                 tp.wr[mc]);
+          if (p.tma_b_merged)
+            tma_load_3d_pair(sb, &tma_b, lbar, 0, tp.p0, nb >> 5);
+          else
+            for (int mc = 0; mc < 4; ++mc) tma_load_2d_pair(sb + mc * (KW * 128), &tma_b, lbar, nb + mc * 32, tp.p0);
+          tp.next(p);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    // ---------------- MMA issuer (leader CTA) ----------------
+    if (rank == 0) {
+      const uint32_t idesc = (make_idesc_tf32(BN, true, true) & ~(0x1Fu << 24)) | ((256u >> 4) << 24);
+      const bool leader = elect_one();
+      int it = 0, lt = 0;
+      for (int w = pair; w < nwork; w += npairs, ++lt) {
+        int m0, n0, z, kb0, kb1;
+        decode(w, m0, n0, z, kb0, kb1);
+        const int acc = lt & 1;
+        if (lt >= 2) mbar_wait(tempty_bar(acc), ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem + acc * L::kAccCols;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(full_bar(s), (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = base + s * L::kStage, sb = sa + L::kABytes;
+          if (leader) {
+#pragma unroll
+            for (int kk = 0; kk < KW / 8; ++kk)
+              tc_mma_tf32_pair(d0, make_sdesc(sa + kk * 1024, KW * 128, 512, kSw128Base32),
+                               make_sdesc(sb + kk * 1024, KW * 128, 512, kSw128Base32), idesc,
+                               (kb > kb0 || kk > 0) ? 1u : 0u);
+            tc_commit_pair(empty_bar(s));
+          }
+          __syncwarp();
+        }
+        if (leader) tc_commit_pair(tfull_bar(acc));
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int row = warp * 32 + lane;
+    const uint32_t ltempty0 = map_to_rank(tempty_bar(0), 0), ltempty1 = map_to_rank(tempty_bar(1), 0);
+    int lt = 0;
+    for (int w = pair; w < nwork; w += npairs, ++lt) {
+      int m0, n0, z, kb0, kb1;
+      decode(w, m0, n0, z, kb0, kb1);
+      const int acc = lt & 1;
+      mbar_wait_sleep(tfull_bar(acc), (lt >> 1) & 1);
+      tc_fence_after();
+      const int m = m0 + row;
+      const uint32_t taddr = tmem + acc * L::kAccCols + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+      for (int cg = 0; cg < BN / 32; ++cg) {
+        float v[32];
+        tmem_ld32(taddr + cg * 32, v);
+        if (cg == BN / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive_cluster(acc ? ltempty1 : ltempty0);
+        }
+        if (kb1 <= kb0) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        if (m >= p.M) continue;
+        const int nb = n0 + cg * 32;
+        if (nb >= p.Cout) continue;
+        if (p.epi == kEpiPartial) {
+          float* dst = p.out + static_cast<int64_t>(z) * p.Ncols * p.M;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (nb + i < p.Cout) dst[static_cast<int64_t>(nb + i) * p.M + m] = v[i];
+        } else {
+          bool valid;
+          const int widx = wgrad_widx(p, m, valid);
+          if (!valid) continue;
+          if (p.epi == kEpiSgd) {
+            float* wcol = p.w_mut + static_cast<int64_t>(nb) * p.KK + widx;
+            float wv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) wv[i] = (nb + i < p.Cout) ? wcol[static_cast<int64_t>(i) * p.KK] : 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (nb + i < p.Cout) wcol[static_cast<int64_t>(i) * p.KK] = wv[i] - p.lr * v[i];
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (nb + i < p.Cout) p.out[static_cast<int64_t>(nb + i) * p.KK + widx] = v[i];
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
   if (warp == 4) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");

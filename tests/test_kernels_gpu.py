@@ -320,3 +320,12 @@ def test_conv_production_tiles(shape):
                      (dw, wr.grad.permute(0, 2, 3, 1))):
         err = (got.double() - ref).abs().max().item() / ref.abs().max().item()
         assert err < TF32_TOL, err
+    # fused SGD epilogue (w -= lr * dW), same split-K workspace
+    lr = 1e-3
+    w2 = wt.clone()
+    L.call("vdnn_kernel_conv_wgrad", C.byref(d), C.c_void_p(dy.data_ptr()), C.c_void_p(w2.data_ptr()),
+           C.c_float(lr), None, C.c_void_p(ws.data_ptr()), C.c_size_t(ws_bytes), None)
+    torch.cuda.synchronize()
+    gref = wr.grad.permute(0, 2, 3, 1)
+    diff = (w2.double() - (wt.double() - lr * gref)).abs().max().item()
+    assert diff < TF32_TOL * lr * gref.abs().max().item() + 2e-7 * wt.abs().max().item(), diff
