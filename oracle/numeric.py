@@ -63,9 +63,12 @@ def tf32(t: torch.Tensor) -> torch.Tensor:
 
 
 def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np.ndarray, lr: float,
-               dtype=torch.float64, tf32_operands: bool = False
+               dtype=torch.float64, tf32_operands: bool = False, device: str = "cpu"
                ) -> Tuple[float, Dict[int, np.ndarray], Dict[int, np.ndarray]]:
     """Returns (loss, updated weights, weight gradients).
+
+    device="cuda" evaluates the same float64 restatement with torch on the GPU
+    (test infrastructure for network sizes the CPU cannot finish quickly).
 
     tf32_operands=True rounds both operands of every conv/FC contraction the
     way kind::tf32 reads them (fp32 values stay fp32 between layers); this is
@@ -74,7 +77,7 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
     L = layers_of(g)
     N = len(L)
     buf: Dict[int, torch.Tensor] = {}
-    W = {k: torch.tensor(v, dtype=dtype) for k, v in weights.items()}
+    W = {k: torch.tensor(v, dtype=dtype, device=device) for k, v in weights.items()}
     grads: Dict[int, torch.Tensor] = {}
 
     def cat_in(l: Layer, flatten: bool = False):
@@ -96,7 +99,7 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
     loss = 0.0
     for l in L:
         if l.kind == INPUT:
-            buf[l.id] = torch.tensor(images, dtype=dtype).reshape(_nhwc(l.shape))
+            buf[l.id] = torch.tensor(images, dtype=dtype, device=device).reshape(_nhwc(l.shape))
         elif l.kind == CONV:
             k, s, p, cout = l.params
             x = cat_in(l).permute(0, 3, 1, 2)
@@ -119,12 +122,12 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
             buf[l.id] = (q(x) @ q(w).t() + b).reshape(_nhwc(l.shape))
         elif l.kind == LOSS:
             z = buf[owner(L, l.inputs[0])].reshape(l.shape[0], -1)
-            lab = torch.tensor(labels, dtype=torch.long)
+            lab = torch.tensor(labels, dtype=torch.long, device=device)
             lse = torch.logsumexp(z, dim=1)
-            loss = float((lse - z[torch.arange(z.shape[0]), lab]).mean())
+            loss = float((lse - z[torch.arange(z.shape[0], device=z.device), lab]).mean())
             pr = torch.softmax(z, dim=1)
             oh = torch.zeros_like(pr)
-            oh[torch.arange(z.shape[0]), lab] = 1.0
+            oh[torch.arange(z.shape[0], device=z.device), lab] = 1.0
             gscratch = (pr - oh) / z.shape[0]
 
     # ---------------- backward
@@ -232,7 +235,8 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
             y.backward(dy.permute(0, 3, 1, 2))
             if produces(l):
                 set_planes(l, x.grad.permute(0, 2, 3, 1), False)
-    return loss, {k: v.numpy().astype(np.float32) for k, v in W.items()}, {k: v.numpy() for k, v in grads.items()}
+    return (loss, {k: v.cpu().numpy().astype(np.float32) for k, v in W.items()},
+            {k: v.cpu().numpy() for k, v in grads.items()})
 
 
 def he_weights(g, cost, seed: int = 5000) -> Dict[int, np.ndarray]:

@@ -438,24 +438,24 @@ cudaError_t launch_pair(ConvParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int STAGES, int KW>
+template <int STAGES, int KW, int PN>
 cudaError_t launch_wgrad_pair(ConvParams& p, int splits, cudaStream_t st) {
-  using L = WgradPairSmem<STAGES, KW>;
+  using L = WgradPairSmem<STAGES, KW, PN>;
   alignas(64) CUtensorMap ta, tb, tc;
   std::memset(&ta, 0, sizeof(ta));
   std::memset(&tb, 0, sizeof(tb));
   std::memset(&tc, 0, sizeof(tc));
-  if (!make_maps<128, KW>(p, &ta, &tb, &tc)) return cudaErrorNotSupported;
+  if (!make_maps<PN / 2, KW>(p, &ta, &tb, &tc)) return cudaErrorNotSupported;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_wgrad_pair_kernel<STAGES, KW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         L::kTotal);
+    cudaError_t e = cudaFuncSetAttribute(tc_wgrad_pair_kernel<STAGES, KW, PN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int work = ((p.M + 255) / 256) * ((p.Ncols + 255) / 256) * splits;
+  const int work = ((p.M + 255) / 256) * ((p.Ncols + PN - 1) / PN) * splits;
   const int grid = 2 * std::min(work, kNumSms / 2);
-  tc_wgrad_pair_kernel<STAGES, KW><<<grid, 192, L::kTotal, st>>>(p, ta, tb, splits);
+  tc_wgrad_pair_kernel<STAGES, KW, PN><<<grid, 192, L::kTotal, st>>>(p, ta, tb, splits);
   count_launch();
   return cudaGetLastError();
 }
@@ -463,7 +463,13 @@ cudaError_t launch_wgrad_pair(ConvParams& p, int splits, cudaStream_t st) {
 cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
   if (p.kind == kWgrad && p.use_pair && !g_precise && !g_no_tma) {
-    const cudaError_t e = p.wkw == 64 ? launch_wgrad_pair<3, 64>(p, splits, st) : launch_wgrad_pair<6, kBK>(p, splits, st);
+    cudaError_t e = cudaErrorNotSupported;
+    if (p.Ncols >= 256)
+      e = p.wkw == 64 ? launch_wgrad_pair<3, 64, 256>(p, splits, st) : launch_wgrad_pair<6, kBK, 256>(p, splits, st);
+    else if (p.Ncols >= 128)
+      e = launch_wgrad_pair<4, 64, 128>(p, splits, st);
+    else
+      e = launch_wgrad_pair<5, 64, 64>(p, splits, st);
     if (e != cudaErrorNotSupported) return e;
     p.tma_b_merged = 0;
   }
@@ -585,16 +591,20 @@ WCfg wgrad_cfg(const ConvParams& p, int64_t pixels) {
   c.kw = kBK;
   c.pair = false;
   // CTA pair (M = 256 weight rows x N = 256 output channels per pair)
-  if (tma && pair_enabled() && ncols >= 256 && pixels >= 2048 && wgrad_rows(p) >= 256) {
+  static const int pair_min = [] {  // narrowest layer that takes the pair wgrad (VDNN_PAIR_WGRAD_MIN)
+    const char* e = std::getenv("VDNN_PAIR_WGRAD_MIN");
+    return e ? std::atoi(e) : 256;
+  }();
+  if (tma && pair_enabled() && ncols >= pair_min && pixels >= 2048 && wgrad_rows(p) >= 256) {
     c.pair = true;
-    c.bn = 256;
+    c.bn = ncols >= 256 ? 256 : (ncols >= 128 ? 128 : 64);
     c.bm = 256;
     c.slots = kNumSms / 2;
     static const int kw = [] {
       const char* e = std::getenv("VDNN_PAIR_WGRAD_KW");
       return e ? std::atoi(e) : 64;
     }();
-    c.kw = kw == 32 ? kBK : 64;
+    c.kw = (kw == 32 && c.bn == 256) ? kBK : 64;
     return c;
   }
   // 64-pixel stages (opt-in, VDNN_WGRAD_KW=64): they halve the im2col boxes

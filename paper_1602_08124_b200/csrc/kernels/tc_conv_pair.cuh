@@ -303,21 +303,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 // stage, both operands MN-major. Work items are (tile, split) pairs walked
 // persistently; the epilogue writes split-K partials or applies SGD / writes
 // dW exactly like tc_conv_kernel's WGRAD epilogue.
-template <int STAGES, int KW>
+template <int STAGES, int KW, int PN>
 struct WgradPairSmem {
   static constexpr int kABytes = kBM * KW * 4;
-  static constexpr int kBBytes = 128 * KW * 4;
+  static constexpr int kBBytes = (PN / 2) * KW * 4;  // this CTA's half of the PN output channels
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kTotal = STAGES * kStage + 1024 + 256;
-  static constexpr int kAccCols = 256;
+  static constexpr int kAccCols = PN < 32 ? 32 : PN;
 };
 
-template <int STAGES, int KW>
+// PN = output channels per pair MMA (N): 256, 128 or 64; each CTA stages PN/2.
+template <int STAGES, int KW, int PN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     tc_wgrad_pair_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tma_a,
                          const __grid_constant__ CUtensorMap tma_b, int splits) {
-  using L = WgradPairSmem<STAGES, KW>;
-  constexpr int BN = 256;
+  using L = WgradPairSmem<STAGES, KW, PN>;
+  constexpr int BN = PN;
   constexpr int kTmemCols = 2 * L::kAccCols;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -380,8 +381,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       for (int w = pair; w < nwork; w += npairs) {
         int m0, n0, z, kb0, kb1;
         decode(w, m0, n0, z, kb0, kb1);
-        const int nb = n0 + static_cast<int>(rank) * 128;
-        TmaProducer<128, kBM, KW> tp;
+        const int nb = n0 + static_cast<int>(rank) * (PN / 2);
+        TmaProducer<PN / 2, kBM, KW> tp;
         tp.init(p, m0, kb0);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
@@ -397,7 +398,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           if (p.tma_b_merged)
             tma_load_3d_pair(sb, &tma_b, lbar, 0, tp.p0, nb >> 5);
           else
-            for (int mc = 0; mc < 4; ++mc) tma_load_2d_pair(sb + mc * (KW * 128), &tma_b, lbar, nb + mc * 32, tp.p0);
+            for (int mc = 0; mc < PN / 64; ++mc)
+              tma_load_2d_pair(sb + mc * (KW * 128), &tma_b, lbar, nb + mc * 32, tp.p0);
           tp.next(p);
         }
       }
