@@ -207,6 +207,10 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         d = V.static_decision(V.PolicyKind.Baseline, V.AlgoMode.PerfOptimal, g, cm)
         free, total = torch.cuda.mem_get_info(device)
         cap = int(free - (6 << 30))
+        if world > 1:  # one plan on every rank (the peer exchange maps weights by offset)
+            t = torch.tensor([cap], dtype=torch.int64, device=f"cuda:{device}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+            cap = int(t.item())
     plan = V.simulate(g, d, cm, cap)
     if not plan.pass_:
         return {"policy": policy, "label": d.label, "verdict": plan.verdict(), "capacity": cap}

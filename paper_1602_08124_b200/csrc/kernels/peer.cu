@@ -19,7 +19,7 @@
 // Barriers are flag words: rank r writes `epoch` into slot [phase][r] of every
 // rank's signal array with a system-scope release store and waits until all
 // N slots of its own array reach `epoch` (acquire loads). A wait that exceeds
-// 60 s traps instead of hanging the device.
+// 120 s traps instead of hanging the device.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -56,7 +56,7 @@ __global__ void peer_barrier_kernel(PeerArgs a, unsigned long long epoch, int ph
   const unsigned long long* mine = a.signal[a.rank] + phase * kPeerMaxRanks + p;
   const unsigned long long t0 = globaltimer();
   while (ld_acquire_sys(mine) < epoch) {
-    if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();  // a peer never arrived
+    if (globaltimer() - t0 > 120ull * 1000000000ull) __trap();  // a peer never arrived
     __nanosleep(64);
   }
 }
