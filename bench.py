@@ -208,7 +208,8 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         free, total = torch.cuda.mem_get_info(device)
         cap = int(free - (6 << 30))
         if world > 1:  # one plan on every rank (the peer exchange maps weights by offset)
-            t = torch.tensor([cap], dtype=torch.int64, device=f"cuda:{device}")
+            t = torch.tensor([cap], dtype=torch.int64,
+                             device="cpu" if torch.distributed.get_backend() == "gloo" else f"cuda:{device}")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
             cap = int(t.item())
     plan = V.simulate(g, d, cm, cap)
@@ -394,8 +395,15 @@ def main():
     from paper_1602_08124_b200.dist import env_rank
     rank, local, world = env_rank()
     if world > 1:
-        torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if os.environ.get("VDNN_BENCH_SAME_DEVICE") == "1":
+            # test hook: every rank on cuda:0 (the one-GPU box), gloo for the
+            # host collectives; the peer exchange still runs over CUDA IPC
+            local = 0
+            torch.cuda.set_device(0)
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     device = local
     torch.cuda.set_device(device)
     peaks, peaks_src = load_peaks()

@@ -142,3 +142,26 @@ def test_peer_exchange_multiprocess_same_device(world):
         for err, same in report:
             assert err <= 1.0, (rank, err)  # within one ulp of the fused reference
             assert same, rank  # every rank holds bit-identical weights
+
+
+def test_bench_two_ranks_same_device_peer_exchange():
+    """bench.py's N>1 path end to end (torchrun, 2 ranks): on the one-GPU box
+    both ranks share cuda:0 (VDNN_BENCH_SAME_DEVICE=1 -> gloo for the host
+    collectives); the gradient exchange is the fused peer kernel."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VDNN_BENCH_SAME_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--net", "alexnet", "--batch", "32", "--policies", "dyn", "--steps", "1", "--warmup", "3",
+           "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert line["config"]["gradient_exchange"] == "peer"
+    assert line["policies"]["dyn"]["dp_exchange"] == "peer"
