@@ -414,9 +414,9 @@ bool pair_enabled() {
   return on;
 }
 
-template <int STAGES>
+template <int STAGES, int KB>
 cudaError_t launch_pair(ConvParams& p, cudaStream_t st) {
-  using L = PairSmem<STAGES>;
+  using L = PairSmem<STAGES, KB>;
   alignas(64) CUtensorMap ta, tb, tc;
   std::memset(&ta, 0, sizeof(ta));
   std::memset(&tb, 0, sizeof(tb));
@@ -427,13 +427,13 @@ cudaError_t launch_pair(ConvParams& p, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e =
-        cudaFuncSetAttribute(tc_conv_pair_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+        cudaFuncSetAttribute(tc_conv_pair_kernel<STAGES, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int tiles = ((p.M + 255) / 256) * ((p.Ncols + 255) / 256);
   const int grid = 2 * std::min(tiles, kNumSms / 2);
-  tc_conv_pair_kernel<STAGES><<<grid, 192, L::kTotal, st>>>(p, ta, tb, tc);
+  tc_conv_pair_kernel<STAGES, KB><<<grid, 192, L::kTotal, st>>>(p, ta, tb, tc);
   count_launch();
   return cudaGetLastError();
 }
@@ -480,7 +480,11 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
       const char* e = std::getenv("VDNN_PAIR_STAGES");
       return e ? std::atoi(e) : 5;
     }();
-    const cudaError_t e = stages == 6 ? launch_pair<6>(p, st) : launch_pair<5>(p, st);
+    cudaError_t e;
+    if (stages == 3 && p.kblocks % 2 == 0)
+      e = launch_pair<3, 2>(p, st);  // 64-channel (2 k-block) stages
+    else
+      e = stages == 6 ? launch_pair<6, 1>(p, st) : launch_pair<5, 1>(p, st);
     if (e != cudaErrorNotSupported) return e;
     p.tma_b_merged = 0;
   }

@@ -89,21 +89,22 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
       : "memory");
 }
 
-template <int STAGES>
+template <int STAGES, int KB = 1>
 struct PairSmem {
-  static constexpr int kABytes = kBM * 128;  // this CTA's 128 A rows x 32 fp32
-  static constexpr int kBBytes = 128 * 128;  // this CTA's half of B: 128 rows (or 4 MN chunks) x 32 fp32
+  static constexpr int kABytes = KB * kBM * 128;  // this CTA's 128 A rows x 32 fp32, per k-block
+  static constexpr int kBBytes = KB * 128 * 128;  // this CTA's half of B: 128 rows (or 4 MN chunks) x 32 fp32
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kOut = 2 * 16384;
   static constexpr int kTotal = STAGES * kStage + kOut + 1024 + 256;
   static constexpr int kAccCols = 256;
 };
 
-template <int STAGES>
+// KB = k-blocks (32 channels each) per pipeline stage; p.kblocks % KB == 0.
+template <int STAGES, int KB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     tc_conv_pair_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tma_a,
                         const __grid_constant__ CUtensorMap tma_b, const __grid_constant__ CUtensorMap tma_c) {
-  using L = PairSmem<STAGES>;
+  using L = PairSmem<STAGES, KB>;
   constexpr int BN = 256;
   constexpr int kTmemCols = 2 * L::kAccCols;
   extern __shared__ uint8_t smem_raw[];
@@ -122,7 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   const int pair = static_cast<int>(blockIdx.x >> 1), npairs = static_cast<int>(gridDim.x >> 1);
   const int ntn = (p.Ncols + BN - 1) / BN;
   const int ntiles = ((p.M + 255) / 256) * ntn;
-  const int nkb = p.kblocks;
+  const int nkb = p.kblocks / KB;  // pipeline stages per tile
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -173,14 +174,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           // serialised the ring (measured 0.9 us per stage).
           const uint32_t lbar = map_to_rank(full_bar(s), 0);
           if (rank == 0) mbar_expect_tx(full_bar(s), 2 * L::kStage);
-          // A: im2col rows of this CTA's half
-          tma_load_im2col_pair(sa, &tma_a, lbar, tp.ck * 32, tp.qw[0], tp.qh[0], tp.qn[0],
-                               static_cast<uint16_t>(tp.s), static_cast<uint16_t>(tp.r));
-          if (p.kind == kFprop) {
-            tma_load_2d_pair(sb, &tma_b, lbar, (tp.r * p.kw + tp.s) * p.C + tp.ck * 32, nb);
-          } else {
-            const int ftap = (p.kh - 1 - tp.r) * p.kw + (p.kw - 1 - tp.s);
-            tma_load_4d_pair(sb, &tma_b, lbar, 0, tp.ck * 32, nb >> 5, ftap);
+#pragma unroll
+          for (int j = 0; j < KB; ++j) {
+            if (j > 0) tp.next(p);
+            // A: im2col rows of this CTA's half; B: this CTA's half of the columns
+            tma_load_im2col_pair(sa + j * 16384, &tma_a, lbar, tp.ck * 32, tp.qw[0], tp.qh[0], tp.qn[0],
+                                 static_cast<uint16_t>(tp.s), static_cast<uint16_t>(tp.r));
+            if (p.kind == kFprop) {
+              tma_load_2d_pair(sb + j * 16384, &tma_b, lbar, (tp.r * p.kw + tp.s) * p.C + tp.ck * 32, nb);
+            } else {
+              const int ftap = (p.kh - 1 - tp.r) * p.kw + (p.kw - 1 - tp.s);
+              tma_load_4d_pair(sb + j * 16384, &tma_b, lbar, 0, tp.ck * 32, nb >> 5, ftap);
+            }
           }
           tp.next(p);
         }
@@ -206,12 +211,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           const uint32_t sa = base + s * L::kStage, sb = sa + L::kABytes;
           if (leader) {
 #pragma unroll
-            for (int kk = 0; kk < kBK / 8; ++kk) {
-              const uint64_t ad = make_sdesc(sa + kk * 32, 16, 1024, kSw128);
-              const uint64_t bd = b_mn ? make_sdesc(sb + kk * 1024, 4096, 512, kSw128Base32)
-                                       : make_sdesc(sb + kk * 32, 16, 1024, kSw128);
-              tc_mma_tf32_pair(d0, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-            }
+            for (int j = 0; j < KB; ++j)
+#pragma unroll
+              for (int kk = 0; kk < kBK / 8; ++kk) {
+                const uint64_t ad = make_sdesc(sa + j * 16384 + kk * 32, 16, 1024, kSw128);
+                const uint64_t bd = b_mn ? make_sdesc(sb + j * 16384 + kk * 1024, 4096, 512, kSw128Base32)
+                                         : make_sdesc(sb + j * 16384 + kk * 32, 16, 1024, kSw128);
+                tc_mma_tf32_pair(d0, ad, bd, idesc, (kb > 0 || j > 0 || kk > 0) ? 1u : 0u);
+              }
             tc_commit_pair(empty_bar(s));
           }
           __syncwarp();

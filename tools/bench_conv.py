@@ -8,7 +8,7 @@ shapes = [(256, 224, 224, 64, 64), (256, 112, 112, 128, 128), (256, 56, 56, 256,
           (256, 14, 14, 512, 512), (256, 112, 112, 64, 128)]
 if len(sys.argv) > 1 and sys.argv[1] == "notma":
     L.lib().vdnn_kernel_set_tma(0)
-def t(fn, n=5):
+def t(fn, n=int(__import__("os").environ.get("REPS", "5"))):
     fn(); torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
