@@ -190,10 +190,15 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     g = V.build_preset(args.net, args.batch) if args.extra == 0 else V.extend_vgg(args.extra, args.batch)
     cm = V.CostModel()
     cap = args.capacity
-    # "<policy>z": the same plan with zero-value-compressed offload/prefetch
+    # "<policy>z": the same plan with zero-value-compressed offload/prefetch;
+    # "<policy>p": the same plan offloading into the ring neighbour's spare
+    # HBM over NVLink (data parallel only: a peer GPU is the offload target)
     compress = policy.endswith("z")
-    if compress:
+    peer_target = policy.endswith("p")
+    if compress or peer_target:
         policy = policy[:-1]
+    if peer_target and world < 2:
+        return {"policy": policy + "p", "verdict": "skipped: a peer-HBM offload target needs >= 2 GPUs"}
     if policy == "dyn":
         sel = V.dynamic_select(g, cap, cm)
         if sel.decision is None:
@@ -216,7 +221,11 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     if not plan.pass_:
         return {"policy": policy, "label": d.label, "verdict": plan.verdict(), "capacity": cap}
     s = V.Session(g, d, cm, cap, device=device, record_timeline=True, external_grads=world > 1,
-                  precise_fp32=args.precise, compress_offload=compress)
+                  precise_fp32=args.precise, compress_offload=compress,
+                  offload_target="device" if peer_target else "host")
+    if peer_target:
+        from paper_1602_08124_b200.dist import ring_spill
+        ring_spill(s, world)
     dp = make_data_parallel(s, world, device) if world > 1 else None
 
     def one(want_loss=False):
@@ -261,7 +270,9 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     pre_ms = sum((e.end - e.start) for e in m.events if e.kind == V.EventKind.Prefetch) * 1e-6
     free, total = torch.cuda.mem_get_info(device)
     res = {
-        "policy": policy + ("z" if compress else ""), "label": d.label + (" +zvc" if compress else ""), "verdict": "PASS", "capacity_bytes": cap,
+        "policy": policy + ("z" if compress else "") + ("p" if peer_target else ""),
+        "label": d.label + (" +zvc" if compress else "") + (" ->peer HBM" if peer_target else ""),
+        "verdict": "PASS", "capacity_bytes": cap,
         "images_per_s": round(imgs, 2), "ms_per_step": round(ms, 3), "loss": loss,
         "peak_pool_bytes": plan.max_mem_bytes, "arena_bytes": s.arena_info()["arena_bytes"],
         "device_used_bytes": total - free,
@@ -274,7 +285,9 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         "conv_fc_ms": round(conv_ms, 3), "memory_bound_ms": round(mem_ms, 3),
         "conv_fc_tflops": round(conv_tflops, 1) if conv_tflops else None,
         "gpu_launches": launches, "clocks": clk.summary(),
-        "transfer": "zero-value-compressed via SMs (zero-copy)" if compress else "cudaMemcpyAsync (copy engines)",
+        "transfer": ("zero-value-compressed via SMs (zero-copy)" if compress else
+                     "cudaMemcpyAsync to the ring neighbour's HBM (NVLink peer copies)" if peer_target else
+                     "cudaMemcpyAsync (copy engines)"),
         "offload_wire_bytes_per_iter": wire["offload_wire"], "prefetch_wire_bytes_per_iter": wire["prefetch_wire"],
         "wire_ratio": round((wire["offload_wire"] + wire["prefetch_wire"]) /
                             max(1, wire["offload_planned"] + wire["prefetch_planned"]), 4),
@@ -378,8 +391,9 @@ def main():
     ap.add_argument("--extra", type=int, default=0, help="extend_vgg extra conv layers (400 -> VGG-416)")
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--capacity", type=int, default=GIB12)
-    ap.add_argument("--policies", default="dyn,dynz,all,conv,none",
-                    help="dyn/all/conv/none; a trailing z = same plan with compressed offload")
+    ap.add_argument("--policies", default=None,
+                    help="dyn/all/conv/none; a trailing z = same plan with compressed offload, a trailing p = "
+                         "offload into a peer GPU's HBM (N > 1). Default: dyn,dynz,all,conv,none (+ dynp at N > 1)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--precise", action="store_true", help="3xTF32 fp32-accurate contractions")
     ap.add_argument("--cpu-sample-batch", type=int, default=2)
@@ -409,6 +423,8 @@ def main():
     peaks, peaks_src = load_peaks()
     link = link_bandwidth(device)
 
+    if args.policies is None:
+        args.policies = "dyn,dynz,all,conv,none" if world == 1 else "dyn,dynp,dynz,all,conv,none"
     results = {}
     for p in [x for x in args.policies.split(",") if x]:
         results[p] = run_policy(p, args, device, world, peaks, want_e2e=(p == "dyn"), sampler_cls=ClockSampler)
@@ -459,6 +475,14 @@ def main():
             "images_per_s": z["images_per_s"], "ms_per_step": z["ms_per_step"], "wire_ratio": z.get("wire_ratio"),
             "speedup_vs_copy_engines": round(z["images_per_s"] / head["images_per_s"], 3)
             if head.get("images_per_s") else None}
+    if "dynp" in results and results["dynp"].get("images_per_s"):
+        z = results["dynp"]
+        line["peer_hbm_offload"] = {
+            "policy": "vDNN_dyn, same plan, offload target = ring neighbour's spare HBM (NVLink peer copies)",
+            "images_per_s": z["images_per_s"], "ms_per_step": z["ms_per_step"],
+            "offload_gbs": z.get("d2h_gbs"), "prefetch_gbs": z.get("h2d_gbs"),
+            "slowdown_vs_no_offload": (round(z["ms_per_step"] / results["none"]["ms_per_step"], 4)
+                                       if results.get("none", {}).get("ms_per_step") else None)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         base, _ = cpu_baseline_sample(args)
         line["cpu_baseline"] = base

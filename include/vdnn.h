@@ -251,6 +251,8 @@ typedef struct vdnn_session_options {
   int32_t host_arena;        /* 1: pinned host arena for offloads (required when the plan offloads) */
   int32_t precise_fp32;      /* 1: conv/FC contractions as 3xTF32 (fp32-accurate); 0: TF32 */
   int32_t compress_offload;  /* 1: offload/prefetch through the SMs in lossless zero-value-compressed form */
+  int32_t offload_target;    /* 0: pinned host arena (PCIe); 1: a device buffer set with
+                                vdnn_session_set_offload_buffer / _spill_attach (e.g. a peer GPU's HBM) */
 } vdnn_session_options;
 void vdnn_session_options_default(vdnn_session_options* o);
 
@@ -309,6 +311,13 @@ vdnn_status vdnn_session_peer_export(vdnn_session* s, vdnn_peer_handle* out);
 vdnn_status vdnn_session_peer_attach(vdnn_session* s, int32_t rank, int32_t world, const vdnn_peer_handle* all);
 vdnn_status vdnn_session_peer_exchange(vdnn_session* s, float lr, float grad_scale);
 vdnn_status vdnn_session_peer_detach(vdnn_session* s);
+/* Device offload target (offload_target = 1): the bytes the offload slots need; use a caller-provided
+ * device buffer, or host a spill buffer for a peer (export its CUDA IPC handle) and offload into a
+ * peer's spill buffer (attach its handle) -- offloads then travel over NVLink instead of PCIe. */
+vdnn_status vdnn_session_offload_bytes(vdnn_session* s, uint64_t* bytes);
+vdnn_status vdnn_session_set_offload_buffer(vdnn_session* s, void* dev_ptr, uint64_t bytes);
+vdnn_status vdnn_session_spill_export(vdnn_session* s, uint8_t ipc_handle[64]);
+vdnn_status vdnn_session_spill_attach(vdnn_session* s, const uint8_t ipc_handle[64]);
 /* Compute stream (cudaStream_t) for interop. */
 vdnn_status vdnn_session_stream(vdnn_session* s, void** stream);
 uint64_t vdnn_kernel_launch_count(void);

@@ -737,10 +737,15 @@ class Session:
     def __init__(self, g: NetworkGraph, decision: PolicyDecision, cost: Optional[CostModel] = None,
                  capacity: int = 12884901888, device: int = 0, weight_seed: int = 5000,
                  external_grads: bool = False, record_timeline: bool = False, precise_fp32: bool = False,
-                 compress_offload: bool = False):
+                 compress_offload: bool = False, offload_target: str = "host"):
         """compress_offload: move offloads/prefetches through the SMs in a
         lossless zero-value-compressed form (same schedule, bit-identical
-        restored buffers, fewer bytes on the host link)."""
+        restored buffers, fewer bytes on the host link).
+        offload_target: "host" (pinned host memory over PCIe, the reference's
+        model) or "device" (a device buffer given to set_offload_buffer, or a
+        peer GPU's spill buffer via spill_export / spill_attach: NVLink)."""
+        if offload_target not in ("host", "device"):
+            raise ValueError(f"offload_target must be 'host' or 'device', not {offload_target!r}")
         self.graph = g
         self.decision = decision
         self.cost = cost or CostModel()
@@ -753,6 +758,7 @@ class Session:
         opt.record_timeline = int(record_timeline)
         opt.precise_fp32 = int(precise_fp32)
         opt.compress_offload = int(compress_offload)
+        opt.offload_target = 0 if offload_target == "host" else 1
         d = decision._handle(g)
         c = self.cost._c()
         h = C.c_void_p()
@@ -861,6 +867,26 @@ class Session:
 
     def apply_grads(self, lr: float, scale: float = 1.0) -> None:
         _call("vdnn_session_apply_grads", self.handle, C.c_float(lr), C.c_float(scale))
+
+    # -- device offload target (offload_target="device") --
+    def offload_bytes(self) -> int:
+        v = C.c_uint64()
+        _call("vdnn_session_offload_bytes", self.handle, C.byref(v))
+        return v.value
+
+    def set_offload_buffer(self, dev_ptr: int, nbytes: int) -> None:
+        _call("vdnn_session_set_offload_buffer", self.handle, C.c_void_p(dev_ptr), C.c_uint64(nbytes))
+
+    def spill_export(self) -> bytes:
+        """Allocate this rank's spill buffer (offload_bytes) and return its IPC handle."""
+        h = (C.c_uint8 * 64)()
+        _call("vdnn_session_spill_export", self.handle, h)
+        return bytes(h)
+
+    def spill_attach(self, handle: bytes) -> None:
+        """Offload into the spill buffer a peer exported (NVLink instead of PCIe)."""
+        h = (C.c_uint8 * 64).from_buffer_copy(handle)
+        _call("vdnn_session_spill_attach", self.handle, h)
 
     # -- data-parallel exchange over peer memory (vdnn_session_peer_*) --
     def peer_export(self) -> bytes:

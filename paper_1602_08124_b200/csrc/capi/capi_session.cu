@@ -49,6 +49,7 @@ void vdnn_session_options_default(vdnn_session_options* o) {
   o->host_arena = 1;
   o->precise_fp32 = 0;
   o->compress_offload = 0;
+  o->offload_target = 0;
 }
 
 vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, const vdnn_cost_model* cm,
@@ -64,6 +65,7 @@ vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, con
       o.host_arena = opt->host_arena != 0;
       o.precise = opt->precise_fp32 != 0;
       o.compress_offload = opt->compress_offload != 0;
+      o.offload_target = opt->offload_target;
     }
     if (!g->net.finalized()) throw vdnnp::PlanError(vdnnp::Err::Generic, "graph is not finalized");
     auto* s = new vdnnrt::Session(g->net, d->d, vdnncapi::cost_from(cm), capacity, o);
@@ -235,6 +237,33 @@ vdnn_status vdnn_session_peer_exchange(vdnn_session* s, float lr, float scale) {
 vdnn_status vdnn_session_peer_detach(vdnn_session* s) {
   return guard([&] {
     S(s).peer_detach();
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_offload_bytes(vdnn_session* s, uint64_t* bytes) {
+  return guard([&] {
+    *bytes = S(s).offload_bytes();
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_set_offload_buffer(vdnn_session* s, void* dev_ptr, uint64_t bytes) {
+  return guard([&] {
+    S(s).set_offload_buffer(dev_ptr, bytes);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_spill_export(vdnn_session* s, uint8_t ipc_handle[64]) {
+  return guard([&] {
+    const cudaIpcMemHandle_t h = S(s).spill_export();
+    std::memcpy(ipc_handle, &h, 64);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_spill_attach(vdnn_session* s, const uint8_t ipc_handle[64]) {
+  return guard([&] {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, 64);
+    S(s).spill_attach(h);
     return VDNN_OK;
   });
 }

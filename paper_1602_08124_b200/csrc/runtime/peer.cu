@@ -125,4 +125,31 @@ void Session::peer_detach() {
   peer_world_ = 0;
 }
 
+// ------------------------------------------------ device offload target ----
+void Session::set_offload_buffer(void* dev_ptr, u64 bytes) {
+  if (o_.offload_target == 0) throw PlanError(Err::Config, "session offloads to the pinned host arena");
+  if (!dev_ptr || bytes < host_bytes_) throw PlanError(Err::Generic, "offload buffer missing or too small");
+  synchronize();
+  host_ = static_cast<char*>(dev_ptr);
+}
+
+cudaIpcMemHandle_t Session::spill_export() {
+  if (!spill_) {
+    check(cudaMalloc(&spill_, std::max<u64>(host_bytes_, 4096)), "cudaMalloc(spill buffer)");
+    scratch_bytes_ += std::max<u64>(host_bytes_, 4096);
+  }
+  cudaIpcMemHandle_t h;
+  check(cudaIpcGetMemHandle(&h, spill_), "cudaIpcGetMemHandle(spill)");
+  return h;
+}
+
+void Session::spill_attach(const cudaIpcMemHandle_t& h) {
+  if (o_.offload_target == 0) throw PlanError(Err::Config, "session offloads to the pinned host arena");
+  synchronize();
+  if (spill_map_) cudaIpcCloseMemHandle(spill_map_);
+  spill_map_ = nullptr;
+  check(cudaIpcOpenMemHandle(&spill_map_, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(spill)");
+  host_ = static_cast<char*>(spill_map_);
+}
+
 }  // namespace vdnnrt

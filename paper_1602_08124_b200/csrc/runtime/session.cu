@@ -97,10 +97,13 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
       host_bytes_ += round_up(o_.compress_offload ? std::max<u64>(e.bytes, vdnnk::zvc_slot_bytes(e.bytes)) : e.bytes,
                               4096);
     }
-  if (host_bytes_ > 0) {
+  if (o_.offload_target != 0 && o_.compress_offload)
+    throw PlanError(Err::Config, "compressed offload targets the pinned host arena only");
+  if (host_bytes_ > 0 && o_.offload_target == 0) {
     if (!o_.host_arena) throw PlanError(Err::Config, "plan offloads but the host arena is disabled");
     check(cudaHostAlloc(&host_, host_bytes_, o_.compress_offload ? cudaHostAllocMapped : cudaHostAllocDefault),
           "cudaHostAlloc(host arena)");
+    host_owned_ = true;
     if (o_.compress_offload) {
       void* dv = nullptr;
       check(cudaHostGetDevicePointer(&dv, host_, 0), "cudaHostGetDevicePointer(host arena)");
@@ -184,7 +187,9 @@ Session::~Session() {
   peer_detach();
   if (signal_) cudaFree(signal_);
   cudaFree(arena_);
-  if (host_) cudaFreeHost(host_);
+  if (host_ && host_owned_) cudaFreeHost(host_);
+  if (spill_map_) cudaIpcCloseMemHandle(spill_map_);
+  if (spill_) cudaFree(spill_);
   cudaFree(loss_grad_);
   cudaFree(row_loss_);
   cudaFree(loss_);
@@ -544,7 +549,7 @@ void Session::run_fwd(const FwdStep& s, float lr) {
       if (t.zvc)
         check(vdnnk::zvc_compress(F(t.dev_off), t.bytes / 4, host_dev_ + t.host_off, wire_, ms_), "zvc offload");
       else {
-        check(cudaMemcpyAsync(host_ + t.host_off, base_ + t.dev_off, t.bytes, cudaMemcpyDeviceToHost, ms_), "D2H");
+        check(cudaMemcpyAsync(host_ + t.host_off, base_ + t.dev_off, t.bytes, cudaMemcpyDefault, ms_), "offload copy");
         copy_off_ += t.bytes;
       }
       raw_off_ += t.bytes;
@@ -608,7 +613,7 @@ void Session::run_bwd(const BwdStep& s, float lr) {
         check(vdnnk::zvc_decompress(host_dev_ + t.host_off, t.bytes / 4, F(t.dev_off), wire_ + 1, ms_),
               "zvc prefetch");
       else {
-        check(cudaMemcpyAsync(base_ + t.dev_off, host_ + t.host_off, t.bytes, cudaMemcpyHostToDevice, ms_), "H2D");
+        check(cudaMemcpyAsync(base_ + t.dev_off, host_ + t.host_off, t.bytes, cudaMemcpyDefault, ms_), "prefetch copy");
         copy_pre_ += t.bytes;
       }
       raw_pre_ += t.bytes;
@@ -690,6 +695,8 @@ void Session::run_bwd(const BwdStep& s, float lr) {
 }
 
 void Session::step(float lr, float* loss_host) {
+  if (host_bytes_ > 0 && !host_)
+    throw PlanError(Err::Config, "the plan offloads but no offload buffer is set (set_offload_buffer / spill_attach)");
   timed_ = o_.record_timeline;
   vdnnk::set_precise(o_.precise);
   if (timed_) check(cudaEventRecord(ev_iter_, cs_), "record");

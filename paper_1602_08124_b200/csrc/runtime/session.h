@@ -28,6 +28,11 @@ struct Options {
   // (kernels/zvc.cu) instead of cudaMemcpyAsync; same schedule, same bytes
   // restored, fewer bytes on the host link.
   bool compress_offload = false;
+  // Where offloaded feature maps go: 0 = the pinned host arena (PCIe, the
+  // reference's model); 1 = a device buffer set later with
+  // set_offload_buffer / spill_attach (e.g. a peer GPU's spare HBM over
+  // NVLink). Same schedule, same slots, same sync rules.
+  int offload_target = 0;
 };
 
 // One gradient plane: the slice of a dX buffer that holds the gradient w.r.t.
@@ -107,6 +112,12 @@ class Session {
   void peer_exchange(float lr, float scale);
   void peer_detach();
   int peer_world() const { return peer_world_; }
+  // Device offload target (Options::offload_target = 1): bytes the slots need,
+  // a caller-provided device buffer, or a peer's spill buffer through IPC.
+  u64 offload_bytes() const { return host_bytes_; }
+  void set_offload_buffer(void* dev_ptr, u64 bytes);
+  cudaIpcMemHandle_t spill_export();       // allocates this rank's spill buffer (offload_bytes) for a peer
+  void spill_attach(const cudaIpcMemHandle_t& h);  // offload into a peer's spill buffer
 
   const vdnnp::Report& plan() const { return plan_; }
   u64 arena_bytes() const { return arena_bytes_; }
@@ -168,6 +179,9 @@ class Session {
   vdnnk::PeerArgs peer_{};
   vdnnk::PeerChunk* peer_chunks_ = nullptr;
   std::vector<void*> peer_maps_;          // IPC-opened pointers (closed on detach)
+  bool host_owned_ = false;               // host_ is our cudaHostAlloc (else a device target)
+  void* spill_ = nullptr;                 // buffer this rank hosts for a peer's offloads
+  void* spill_map_ = nullptr;             // IPC mapping of the peer's spill buffer (our target)
   int peer_world_ = 0;
   unsigned long long peer_epoch_ = 0;
 

@@ -66,6 +66,25 @@ def make_data_parallel(session, world: int, device: int, mode: Optional[str] = N
     raise ValueError(f"unknown data-parallel mode {mode!r}")
 
 
+def ring_spill(session, world: int, group=None) -> int:
+    """Peer-HBM offload target for data-parallel runs: every rank hosts a
+    spill buffer (its own plan's offload bytes; the plans are identical) and
+    offloads into the buffer of rank (r + 1) % world, so offload/prefetch
+    copies travel over NVLink to a neighbour's spare HBM instead of PCIe.
+    The session must be created with offload_target="device". Returns the
+    neighbour rank."""
+    import torch.distributed as dist
+    if world < 2:
+        raise ValueError("a peer offload target needs at least two ranks")
+    h = session.spill_export()
+    handles = [None] * world
+    dist.all_gather_object(handles, h, group=group)
+    rank = dist.get_rank(group)
+    peer = (rank + 1) % world
+    session.spill_attach(handles[peer])
+    return peer
+
+
 class PeerUnavailable(RuntimeError):
     """Some rank could not map its peers' arenas (raised on every rank)."""
 

@@ -123,6 +123,79 @@ def _worker(rank, world, port, q):
         q.put((rank, None, repr(e)))
 
 
+def _spill_worker(rank, world, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_1602_08124_b200 as V
+        from oracle import numeric
+        from paper_1602_08124_b200.dist import PeerDataParallel, ring_spill
+        g = V.build_preset("alexnet", 4)
+        cm = V.CostModel()
+        d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+        w = numeric.he_weights(g, cm, seed=51)
+        images, labels = _batch(g, 60 + rank)
+        labels = labels % 1000
+        # data parallel, offloads into the ring neighbour's spill buffer
+        s = V.Session(g, d, cm, 1 << 30, external_grads=True, offload_target="device", record_timeline=True)
+        for k, v in w.items():
+            s.set_weights(k, v)
+        peer = ring_spill(s, world)
+        dp = PeerDataParallel(s, world)
+        s.set_batch(images, labels)
+        s.step(LR, want_loss=False)
+        s.synchronize()
+        grads = {k: s.get_grads(k) for k in w}
+        s.peer_exchange(LR, 1.0 / world)
+        s.synchronize()
+        after = {k: s.get_weights(k) for k in w}
+        clean = V.replay_check(s.measured_report(), g, d, 1 << 30) == []
+        dist.barrier()  # every rank done with its neighbour's spill buffer
+        dp.close()
+        del s
+        # the same batch through the pinned host arena: identical gradients
+        s2 = V.Session(g, d, cm, 1 << 30, external_grads=True)
+        for k, v in w.items():
+            s2.set_weights(k, v)
+        s2.set_batch(images, labels)
+        s2.step(LR, want_loss=False)
+        s2.synchronize()
+        same_grads = all(np.array_equal(s2.get_grads(k), grads[k]) for k in w)
+        all_after = [None] * world
+        dist.all_gather_object(all_after, after)
+        same_w = all(np.array_equal(all_after[p][k], after[k]) for p in range(world) for k in w)
+        q.put((rank, (peer, clean, same_grads, same_w), None))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, None, repr(e)))
+
+
+def test_ring_spill_offload_multiprocess_same_device():
+    """Peer-HBM offload target: each rank offloads into its ring neighbour's
+    spill buffer (CUDA IPC; over NVLink between GPUs), together with the
+    fused gradient exchange. Gradients equal the pinned-host-arena run bit
+    for bit, the measured log replays clean, and ranks end identical."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_spill_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, rep, exc in res:
+        assert exc is None, (rank, exc)
+        peer, clean, same_grads, same_w = rep
+        assert peer == (rank + 1) % world and clean and same_grads and same_w, (rank, rep)
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_peer_exchange_multiprocess_same_device(world):
     if not torch.cuda.is_available():
@@ -147,7 +220,8 @@ def test_peer_exchange_multiprocess_same_device(world):
 def test_bench_two_ranks_same_device_peer_exchange():
     """bench.py's N>1 path end to end (torchrun, 2 ranks): on the one-GPU box
     both ranks share cuda:0 (VDNN_BENCH_SAME_DEVICE=1 -> gloo for the host
-    collectives); the gradient exchange is the fused peer kernel."""
+    collectives); the gradient exchange is the fused peer kernel, and the
+    dynp policy offloads into the neighbour rank's spill buffer."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import json
@@ -157,7 +231,7 @@ def test_bench_two_ranks_same_device_peer_exchange():
     env = dict(os.environ, VDNN_BENCH_SAME_DEVICE="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
-           "--net", "alexnet", "--batch", "32", "--policies", "dyn", "--steps", "1", "--warmup", "3",
+           "--net", "alexnet", "--batch", "32", "--policies", "dyn,dynp,none", "--steps", "1", "--warmup", "3",
            "--no-cpu-baseline"]
     out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -165,3 +239,6 @@ def test_bench_two_ranks_same_device_peer_exchange():
     assert line["n_gpus"] == 2 and line["value"] > 0
     assert line["config"]["gradient_exchange"] == "peer"
     assert line["policies"]["dyn"]["dp_exchange"] == "peer"
+    # the same plan offloading into the ring neighbour's HBM
+    assert line["policies"]["dynp"]["signature"] == line["policies"]["dyn"]["signature"]
+    assert line["peer_hbm_offload"]["images_per_s"] > 0

@@ -255,3 +255,49 @@ def test_vgg16_b32_production_kernels_match_oracle():
     assert loss_b == loss
     for k in w:
         assert np.array_equal(grads_b[k], grads[k]), f"layer {k}"
+
+
+def test_device_offload_target_is_bit_identical():
+    """offload_target="device": the same plan's offloads/prefetches go to a
+    device buffer (the stand-in for a peer GPU's HBM) instead of pinned host
+    memory -- same slots, same sync rules, so identical weights, and the
+    measured log still replays clean."""
+    _need_gpu()
+    g = V.build_preset("alexnet", 8)
+    cm = V.CostModel()
+    w = numeric.he_weights(g, cm, seed=13)
+    images, labels = _batch(g, seed=14)
+    d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+    outs = []
+    for target in ("host", "device"):
+        s = V.Session(g, d, cm, 4 << 30, record_timeline=True, offload_target=target)
+        spill = None
+        if target == "device":
+            n = s.offload_bytes()
+            assert n > 0
+            spill = torch.empty(n // 4 + 1, dtype=torch.float32, device="cuda")
+            s.set_offload_buffer(spill.data_ptr(), spill.numel() * 4)
+        for k, v in w.items():
+            s.set_weights(k, v)
+        s.set_batch(images, labels)
+        loss = s.step(LR)
+        loss2 = s.step(LR)
+        outs.append((loss, loss2, {k: s.get_weights(k) for k in w}))
+        assert V.replay_check(s.measured_report(), g, d, 4 << 30) == []
+        del s, spill
+    assert outs[0][0] == outs[1][0] and outs[0][1] == outs[1][1]
+    for k in w:
+        assert np.array_equal(outs[0][2][k], outs[1][2][k]), k
+
+
+def test_device_offload_target_requires_a_buffer():
+    _need_gpu()
+    g = V.build_preset("alexnet", 4)
+    cm = V.CostModel()
+    d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+    s = V.Session(g, d, cm, 4 << 30, offload_target="device")
+    s.synthetic_batch(3)
+    with pytest.raises(V.VdnnError):
+        s.step(LR)
+    with pytest.raises(V.VdnnError):
+        V.Session(g, d, cm, 4 << 30, offload_target="device", compress_offload=True)
