@@ -414,9 +414,9 @@ bool pair_enabled() {
   return on;
 }
 
-template <int STAGES, int KB>
+template <int STAGES, int KB, int NOUT = 2>
 cudaError_t launch_pair(ConvParams& p, cudaStream_t st) {
-  using L = PairSmem<STAGES, KB>;
+  using L = PairSmem<STAGES, KB, NOUT>;
   alignas(64) CUtensorMap ta, tb, tc;
   std::memset(&ta, 0, sizeof(ta));
   std::memset(&tb, 0, sizeof(tb));
@@ -427,13 +427,14 @@ cudaError_t launch_pair(ConvParams& p, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e =
-        cudaFuncSetAttribute(tc_conv_pair_kernel<STAGES, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+        cudaFuncSetAttribute(tc_conv_pair_kernel<STAGES, KB, NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int tiles = ((p.M + 255) / 256) * ((p.Ncols + 255) / 256);
   const int grid = 2 * std::min(tiles, kNumSms / 2);
-  tc_conv_pair_kernel<STAGES, KB><<<grid, 192, L::kTotal, st>>>(p, ta, tb, tc);
+  tc_conv_pair_kernel<STAGES, KB, NOUT><<<grid, 192, L::kTotal, st>>>(p, ta, tb, tc);
   count_launch();
   return cudaGetLastError();
 }
@@ -483,8 +484,11 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
     cudaError_t e;
     if (stages == 3 && p.kblocks % 2 == 0)
       e = launch_pair<3, 2>(p, st);  // 64-channel (2 k-block) stages
-    else
-      e = stages == 6 ? launch_pair<6, 1>(p, st) : launch_pair<5, 1>(p, st);
+    else if (stages == 6)
+      e = launch_pair<6, 1>(p, st);
+    else  // default: 5 stages, four TMA-store staging boxes (3 stores in flight: the 56x56x256
+          // tiles' epilogue is as long as their 72-k-block main loop; measured -6% there)
+      e = launch_pair<5, 1, 4>(p, st);
     if (e != cudaErrorNotSupported) return e;
     p.tma_b_merged = 0;
   }

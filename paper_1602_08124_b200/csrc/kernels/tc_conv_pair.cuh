@@ -89,22 +89,22 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
       : "memory");
 }
 
-template <int STAGES, int KB = 1>
+template <int STAGES, int KB = 1, int NOUT = 2>
 struct PairSmem {
   static constexpr int kABytes = KB * kBM * 128;  // this CTA's 128 A rows x 32 fp32, per k-block
   static constexpr int kBBytes = KB * 128 * 128;  // this CTA's half of B: 128 rows (or 4 MN chunks) x 32 fp32
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kOut = 2 * 16384;
+  static constexpr int kOut = NOUT * 16384;  // TMA-store staging boxes (128 rows x 32 columns)
   static constexpr int kTotal = STAGES * kStage + kOut + 1024 + 256;
   static constexpr int kAccCols = 256;
 };
 
 // KB = k-blocks (32 channels each) per pipeline stage; p.kblocks % KB == 0.
-template <int STAGES, int KB>
+template <int STAGES, int KB, int NOUT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     tc_conv_pair_kernel(const __grid_constant__ ConvParams p, const __grid_constant__ CUtensorMap tma_a,
                         const __grid_constant__ CUtensorMap tma_b, const __grid_constant__ CUtensorMap tma_c) {
-  using L = PairSmem<STAGES, KB>;
+  using L = PairSmem<STAGES, KB, NOUT>;
   constexpr int BN = 256;
   constexpr int kTmemCols = 2 * L::kAccCols;
   extern __shared__ uint8_t smem_raw[];
@@ -275,10 +275,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
               if (nb + i < p.C) v[i] = xr[i] > 0.f ? v[i] : 0.f;
           }
         }
-        // box buffer (box & 1) was last used two boxes ago: its TMA store must have read it
-        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        // box buffer (box % NOUT) was last used NOUT boxes ago: its TMA store must have read it
+        if (threadIdx.x == 0) {
+          if constexpr (NOUT == 4)
+            asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        const uint32_t ob = obuf + (box & 1) * 16384;
+        const uint32_t ob = obuf + (box % NOUT) * 16384;
         const uint32_t rowaddr = ob + row * 128;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
