@@ -320,6 +320,15 @@ def test_conv_production_tiles(shape):
                      (dw, wr.grad.permute(0, 2, 3, 1))):
         err = (got.double() - ref).abs().max().item() / ref.abs().max().item()
         assert err < TF32_TOL, err
+    # accumulating dgrad (two-buffer fork accumulation): dx_acc = base + dX
+    base = torch.randn_like(x)
+    dxa = base.clone()
+    da = _desc(n, h, w, [x], [c], cout, 3, 1, 1, [dxa])
+    L.call("vdnn_kernel_conv_dgrad", C.byref(da), C.c_void_p(wt.data_ptr()), C.c_void_p(dy.data_ptr()), 1, None)
+    torch.cuda.synchronize()
+    refa = base.double() + xr.grad.permute(0, 2, 3, 1)
+    err = (dxa.double() - refa).abs().max().item() / refa.abs().max().item()
+    assert err < TF32_TOL, err
     # fused SGD epilogue (w -= lr * dW), same split-K workspace
     lr = 1e-3
     w2 = wt.clone()
