@@ -729,7 +729,10 @@ size_t conv_fprop_ws_bytes(const ConvArgs& a) {
 cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
                        cudaStream_t st, float* ws, size_t ws_bytes) {
   if (!accumulate && bias == nullptr && c3tc_fprop_eligible(a)) return c3tc_fprop(a, w, y, st);
-  if (!accumulate && bias == nullptr && smallc_eligible(a)) return smallc_fprop(a, w, y, st);
+  // SIMT first layer only in the exact-fp32 mode: in TF32 mode the windows
+  // c3tc does not take (AlexNet / OverFeat 11x11x3, K = 363) run on the
+  // tensor-core engine with cp.async gathers (measured 8.8 TFLOP/s SIMT)
+  if (!accumulate && bias == nullptr && smallc_eligible(a) && g_precise) return smallc_fprop(a, w, y, st);
   ConvParams p;
   if (!fprop_params(a, w, bias, y, accumulate, p)) return cudaErrorInvalidValue;
   int splits = ws ? fprop_splits(p) : 1;
@@ -780,8 +783,9 @@ size_t conv_wgrad_ws_bytes(const ConvArgs& a) {
     g_precise = was;
     return b;
   }
+  const size_t first = 0;
   ConvParams p;
-  if (!build_common(a, p)) return 0;
+  if (!build_common(a, p)) return first;
   const int M = wgrad_rows(p);
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
   const WCfg c = wgrad_cfg(p, P);
@@ -789,8 +793,8 @@ size_t conv_wgrad_ws_bytes(const ConvArgs& a) {
   const int kblocks = static_cast<int>((P + c.kw - 1) / c.kw);
   const int splits = pick_splits(tiles, kblocks, c.slots, c.bn * c.bm / kBM * c.kw / kBK,
                                  static_cast<int64_t>(M) * a.cout);
-  if (splits <= 1) return 0;
-  return static_cast<size_t>(splits) * M * a.cout * sizeof(float);
+  if (splits <= 1) return first;
+  return std::max(first, static_cast<size_t>(splits) * M * a.cout * sizeof(float));
 }
 
 __global__ void wgrad_reduce_kernel(const __grid_constant__ ConvParams p, int splits) {
@@ -816,6 +820,9 @@ cudaError_t conv_wgrad(const ConvArgs& a, const float* dy, float* w_mut, float l
   if (c3tc_wgrad_eligible(a) && ws != nullptr &&
       ws_bytes >= static_cast<size_t>(a.cout) * a.kh * a.kw * a.c[0] * sizeof(float))
     return c3tc_wgrad(a, dy, w_mut, lr, dw_out, ws, ws_bytes, st);
+  // first-layer wgrad outside c3tc: the SIMT kernel (smem-resident weights,
+  // hoisted window decode) beats the engine's scalar 4-byte gathers there
+  // (AlexNet 11x11x3: 1.03 vs 1.71 ms)
   if (smallc_eligible(a) && ws != nullptr &&
       ws_bytes >= static_cast<size_t>(a.cout) * a.kh * a.kw * a.c[0] * sizeof(float))
     return smallc_wgrad(a, dy, w_mut, lr, dw_out, ws, ws_bytes, st);

@@ -187,7 +187,8 @@ def test_wgrad_split_k_large_reduction():
     _close(dw, wr.grad.permute(0, 2, 3, 1))
 
 
-@pytest.mark.parametrize("window,stride,segs", [(3, 2, [64]), (2, 2, [16, 8]), (2, 2, [3]), (2, 2, [64])])
+@pytest.mark.parametrize("window,stride,segs", [(3, 2, [64]), (3, 2, [16, 8]), (3, 2, [3]), (2, 2, [16, 8]), (2, 2, [3]),
+                                               (2, 2, [64])])
 def test_maxpool(window, stride, segs):
     dev = _dev()
     n, h, w = 2, 13, 13
