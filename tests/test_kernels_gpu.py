@@ -339,3 +339,32 @@ def test_conv_production_tiles(shape):
     gref = wr.grad.permute(0, 2, 3, 1)
     diff = (w2.double() - (wt.double() - lr * gref)).abs().max().item()
     assert diff < TF32_TOL * lr * gref.abs().max().item() + 2e-7 * wt.abs().max().item(), diff
+
+
+@pytest.mark.parametrize("n,h,cout", [(16, 227, 64), (8, 231, 96)])
+def test_first_layer_big_window_tensor_cores(n, h, cout):
+    """AlexNet / OverFeat conv1 (11x11x3, stride 4, K = 363 = 12 K blocks) on
+    the multi-K-block first-layer tensor-core kernels (fprop + wgrad with the
+    ordered partial reduce), against float64 torch on the GPU."""
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(h)
+    x = torch.randn(n, h, h, 3, device=dev, generator=g)
+    wt = torch.randn(cout, 11, 11, 3, device=dev, generator=g) * (2.0 / 363) ** 0.5
+    ho = (h - 11) // 4 + 1
+    dy = torch.randn(n, ho, ho, cout, device=dev, generator=g)
+    xr = x.double().permute(0, 3, 1, 2)
+    wr = wt.double().permute(0, 3, 1, 2).requires_grad_(True)
+    yr = torch.nn.functional.conv2d(xr, wr, stride=4)
+    yr.backward(dy.double().permute(0, 3, 1, 2))
+    y = torch.full((n, ho, ho, cout), float("nan"), device=dev)
+    d = _desc(n, h, h, [x], [3], cout, 11, 4, 0)
+    L.call("vdnn_kernel_conv_fprop", C.byref(d), C.c_void_p(wt.data_ptr()), None, C.c_void_p(y.data_ptr()), None)
+    ws_bytes = L.lib().vdnn_kernel_conv_wgrad_ws_bytes(C.byref(d))
+    ws = torch.empty(max(ws_bytes // 4, 1), device=dev)
+    dw = torch.full_like(wt, float("nan"))
+    L.call("vdnn_kernel_conv_wgrad", C.byref(d), C.c_void_p(dy.data_ptr()), C.c_void_p(wt.data_ptr()),
+           C.c_float(0.0), C.c_void_p(dw.data_ptr()), C.c_void_p(ws.data_ptr()), C.c_size_t(ws_bytes), None)
+    torch.cuda.synchronize()
+    for got, ref in ((y, yr.detach().permute(0, 2, 3, 1)), (dw, wr.grad.permute(0, 2, 3, 1))):
+        err = (got.double() - ref).abs().max().item() / ref.abs().max().item()
+        assert err < TF32_TOL, err
