@@ -450,6 +450,60 @@ __global__ void maxpool_bwd_gather4_kernel(const __grid_constant__ PoolDev d, co
   }
 }
 
+// Overlapping windows with window <= 2*stride (AlexNet/OverFeat 3x3/2):
+// deterministic scatter in four passes over the window parity classes
+// (oh % 2, ow % 2) -- windows of one class never overlap, so each pass adds
+// dY to its windows' first-maximum positions without races, in a fixed
+// order. 4 channels per thread; dX zeroed first. The fused ReLU backward
+// skips positions whose input is <= 0 (they end 0, as the mask demands).
+__global__ void maxpool_bwd_class_kernel(const __grid_constant__ PoolDev d, const float* __restrict__ dy, int ph,
+                                         int pw) {
+  const int cv = d.ctot / 4;
+  const int hoc = (d.ho - ph + 1) / 2, woc = (d.wo - pw + 1) / 2;  // windows of this class
+  const size_t total = static_cast<size_t>(d.n) * hoc * woc * cv;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % cv) * 4;
+    size_t t = i / cv;
+    const int ow = 2 * static_cast<int>(t % woc) + pw;
+    t /= woc;
+    const int oh = 2 * static_cast<int>(t % hoc) + ph;
+    const int n = static_cast<int>(t / hoc);
+    const int s = pool_seg(d, c);
+    float* dx = d.dx[s];
+    if (dx == nullptr) continue;
+    const int cl = c - d.cbase[s];
+    const float* x = d.x[s];
+    const int C = d.c[s];
+    float m[4];
+    int arg[4] = {0, 0, 0, 0};
+    for (int r = 0; r < d.window; ++r) {
+      const float* row = x + ((static_cast<size_t>(n) * d.h + oh * d.stride + r) * d.w + ow * d.stride) * C + cl;
+      for (int q = 0; q < d.window; ++q) {
+        const float4 v4 = *reinterpret_cast<const float4*>(row + static_cast<size_t>(q) * C);
+        const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+        const int pos = r * d.window + q;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (pos == 0 || v[k] > m[k]) {
+            m[k] = v[k];
+            arg[k] = pos;
+          }
+      }
+    }
+    const size_t oidx = ((static_cast<size_t>(n) * d.ho + oh) * d.wo + ow) * d.ctot + c;
+    const float4 d4 = *reinterpret_cast<const float4*>(dy + oidx);
+    const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (d.mask[s] && m[k] <= 0.f) continue;
+      const int r = arg[k] / d.window, q = arg[k] - r * d.window;
+      float* dst = dx + ((static_cast<size_t>(n) * d.h + oh * d.stride + r) * d.w + ow * d.stride + q) * C + cl + k;
+      *dst += dv[k];
+    }
+  }
+}
+
 cudaError_t maxpool_bwd(const PoolArgs& a, const float* y, const float* dy, cudaStream_t st) {
   const PoolDev d = to_dev(a);
   const size_t total = static_cast<size_t>(d.n) * d.h * d.w * d.ctot;
@@ -469,6 +523,19 @@ cudaError_t maxpool_bwd(const PoolArgs& a, const float* y, const float* dy, cuda
       maxpool_bwd_scatter_kernel<4><<<grid_for(outs / 4, 2), kThreads, 0, st>>>(d, y, dy);
     else
       maxpool_bwd_scatter_kernel<1><<<grid_for(outs, 4), kThreads, 0, st>>>(d, y, dy);
+  } else if (pool_vec4(d) && d.window <= 2 * d.stride) {
+    for (int i = 0; i < d.nseg; ++i)
+      if (d.dx[i]) {
+        cudaError_t e = cudaMemsetAsync(d.dx[i], 0, static_cast<size_t>(d.n) * d.h * d.w * d.c[i] * sizeof(float), st);
+        if (e != cudaSuccess) return e;
+      }
+    const size_t wins = static_cast<size_t>(d.n) * d.ho * d.wo * d.ctot / 4;
+    for (int ph = 0; ph < 2; ++ph)
+      for (int pw = 0; pw < 2; ++pw) {
+        maxpool_bwd_class_kernel<<<grid_for(wins / 4 + 1, 2), kThreads, 0, st>>>(d, dy, ph, pw);
+        count_launch();
+      }
+    return cudaGetLastError();
   } else if (pool_vec4(d)) {
     maxpool_bwd_gather4_kernel<<<grid_for(total / 4, 2), kThreads, 0, st>>>(d, y, dy);
   } else {
