@@ -426,6 +426,11 @@ def main():
     torch.cuda.set_device(device)
     peaks, peaks_src = load_peaks()
     link = link_bandwidth(device)
+    # the TF32 ceiling is probed first, on a cool GPU at full clocks: the dyn
+    # step's conv kernels run at those clocks (the link-bound step leaves the
+    # GPU mostly idle), while a probe after the no-offload run measured the
+    # power-capped clock (835 vs 1,095 TFLOP/s)
+    tf32_peak, peak_note = measured_tf32_peak(peaks, peaks_src)
 
     if args.policies is None:
         args.policies = "dyn,dynz,all,conv,none" if world == 1 else "dyn,dynp,dynz,all,conv,none"
@@ -434,7 +439,6 @@ def main():
         results[p] = run_policy(p, args, device, world, peaks, want_e2e=(p == "dyn"), sampler_cls=ClockSampler)
 
     head = results.get("dyn") or next(iter(results.values()))
-    tf32_peak, peak_note = measured_tf32_peak(peaks, peaks_src)
     line = {
         "metric": METRIC, "value": head.get("images_per_s"), "unit": "images/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head.get("ms_per_step"),
