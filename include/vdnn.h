@@ -267,6 +267,11 @@ vdnn_status vdnn_session_arena_info(const vdnn_session* s, uint64_t* arena_bytes
 vdnn_status vdnn_session_set_batch_host(vdnn_session* s, const float* images, const int32_t* labels);
 vdnn_status vdnn_session_set_batch_device(vdnn_session* s, const float* images, const int32_t* labels);
 vdnn_status vdnn_session_synthetic_batch(vdnn_session* s, uint64_t seed);
+/* Input pipeline: stage the NEXT batch (pinned host pointers) on a separate stream while the current
+ * step runs; the next vdnn_session_step consumes it. Pair with vdnn_session_step(s, lr, NULL) +
+ * vdnn_session_read_loss so the host does not wait on the loss before staging the next batch. */
+vdnn_status vdnn_session_prefetch_batch_host(vdnn_session* s, const float* images, const int32_t* labels);
+vdnn_status vdnn_session_read_loss(vdnn_session* s, float* loss);
 /* Weights: per layer, KRSC conv / [out][in]+bias FC; float count = weight_bytes/4. */
 vdnn_status vdnn_session_get_weights(vdnn_session* s, int32_t layer, float* host, size_t count);
 vdnn_status vdnn_session_set_weights(vdnn_session* s, int32_t layer, const float* host, size_t count);

@@ -800,6 +800,16 @@ class Session:
         fn = "vdnn_session_set_batch_device" if device else "vdnn_session_set_batch_host"
         _call(fn, self.handle, C.c_void_p(images_ptr), C.c_void_p(labels_ptr))
 
+    def prefetch_batch_ptr(self, images_ptr: int, labels_ptr: int) -> None:
+        """Stage the NEXT batch from pinned host memory on the input stream
+        (overlapping the running step); the next step() consumes it."""
+        _call("vdnn_session_prefetch_batch_host", self.handle, C.c_void_p(images_ptr), C.c_void_p(labels_ptr))
+
+    def read_loss(self) -> float:
+        """Loss of the last step (after step(want_loss=False))."""
+        _call("vdnn_session_read_loss", self.handle, C.byref(self._loss))
+        return float(self._loss.value)
+
     def synthetic_batch(self, seed: int = 1234) -> None:
         _call("vdnn_session_synthetic_batch", self.handle, C.c_uint64(seed))
 

@@ -240,6 +240,19 @@ vdnn_status vdnn_session_peer_detach(vdnn_session* s) {
     return VDNN_OK;
   });
 }
+vdnn_status vdnn_session_prefetch_batch_host(vdnn_session* s, const float* images, const int32_t* labels) {
+  return guard([&] {
+    S(s).prefetch_batch_host(images, labels);
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_read_loss(vdnn_session* s, float* loss) {
+  return guard([&] {
+    if (!loss) throw vdnnp::PlanError(vdnnp::Err::Generic, "null loss pointer");
+    *loss = S(s).read_loss();
+    return VDNN_OK;
+  });
+}
 vdnn_status vdnn_session_offload_bytes(vdnn_session* s, uint64_t* bytes) {
   return guard([&] {
     *bytes = S(s).offload_bytes();

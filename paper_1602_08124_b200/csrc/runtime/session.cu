@@ -184,6 +184,11 @@ Session::~Session() {
   for (auto e : xfer_ev_) cudaEventDestroy(e);
   if (ev_iter_) cudaEventDestroy(ev_iter_);
   if (ev_sync_) cudaEventDestroy(ev_sync_);
+  if (in_stream_) cudaStreamSynchronize(in_stream_);
+  if (staged_ready_) cudaEventDestroy(staged_ready_);
+  if (staging_free_) cudaEventDestroy(staging_free_);
+  if (staging_) cudaFree(staging_);
+  if (in_stream_) cudaStreamDestroy(in_stream_);
   peer_detach();
   if (signal_) cudaFree(signal_);
   cudaFree(arena_);
@@ -699,6 +704,16 @@ void Session::step(float lr, float* loss_host) {
     throw PlanError(Err::Config, "the plan offloads but no offload buffer is set (set_offload_buffer / spill_attach)");
   timed_ = o_.record_timeline;
   vdnnk::set_precise(o_.precise);
+  if (has_staged_) {  // the batch prefetch_batch_host staged: into the INPUT extent, then free the buffer
+    const u64 bytes = lv_.feat[static_cast<size_t>(input_id_)];
+    check(cudaStreamWaitEvent(cs_, staged_ready_, 0), "wait");
+    if (staged_images_) check(cudaMemcpyAsync(F(x_off_), staging_, bytes, cudaMemcpyDeviceToDevice, cs_), "images D2D");
+    if (staged_labels_)
+      check(cudaMemcpyAsync(labels_, staging_ + bytes, static_cast<u64>(g_.batch()) * 4, cudaMemcpyDeviceToDevice, cs_),
+            "labels D2D");
+    check(cudaEventRecord(staging_free_, cs_), "record");
+    has_staged_ = false;
+  }
   if (timed_) check(cudaEventRecord(ev_iter_, cs_), "record");
   // the memory stream never runs ahead into a new iteration
   check(cudaEventRecord(ev_sync_, cs_), "record");
@@ -737,6 +752,34 @@ void Session::set_batch_device(const float* images, const int32_t* labels) {
   const u64 bytes = lv_.feat[static_cast<size_t>(input_id_)];
   if (images) check(cudaMemcpyAsync(F(x_off_), images, bytes, cudaMemcpyDeviceToDevice, cs_), "images D2D");
   if (labels) check(cudaMemcpyAsync(labels_, labels, g_.batch() * 4, cudaMemcpyDeviceToDevice, cs_), "labels D2D");
+}
+
+void Session::prefetch_batch_host(const float* images, const int32_t* labels) {
+  const u64 bytes = lv_.feat[static_cast<size_t>(input_id_)];
+  const u64 lbytes = static_cast<u64>(g_.batch()) * 4;
+  if (!in_stream_) {
+    check(cudaStreamCreateWithFlags(&in_stream_, cudaStreamNonBlocking), "stream");
+    check(cudaMalloc(&staging_, bytes + lbytes), "cudaMalloc(input staging)");
+    scratch_bytes_ += bytes + lbytes;
+    check(cudaEventCreateWithFlags(&staged_ready_, cudaEventDisableTiming), "event");
+    check(cudaEventCreateWithFlags(&staging_free_, cudaEventDisableTiming), "event");
+    check(cudaEventRecord(staging_free_, cs_), "record");
+  }
+  if (has_staged_) throw PlanError(Err::Generic, "a prefetched batch is already waiting for the next step");
+  // the previous staged batch has been copied out of the buffer
+  check(cudaStreamWaitEvent(in_stream_, staging_free_, 0), "wait");
+  if (images) check(cudaMemcpyAsync(staging_, images, bytes, cudaMemcpyHostToDevice, in_stream_), "images H2D");
+  if (labels) check(cudaMemcpyAsync(staging_ + bytes, labels, lbytes, cudaMemcpyHostToDevice, in_stream_), "labels H2D");
+  check(cudaEventRecord(staged_ready_, in_stream_), "record");
+  has_staged_ = true;
+  staged_images_ = images != nullptr;
+  staged_labels_ = labels != nullptr;
+}
+
+float Session::read_loss() {
+  check(cudaMemcpyAsync(pinned_loss_, loss_, 4, cudaMemcpyDeviceToHost, cs_), "loss D2H");
+  check(cudaStreamSynchronize(cs_), "sync");
+  return *pinned_loss_;
 }
 
 void Session::synthetic_batch(u64 seed) {

@@ -88,6 +88,13 @@ class Session {
 
   void set_batch_host(const float* images, const int32_t* labels);
   void set_batch_device(const float* images, const int32_t* labels);
+  // Input pipeline: stage the NEXT batch from pinned host memory into a
+  // device staging buffer on a separate stream (overlapping the running
+  // step); the next step() moves it into the INPUT extent first thing.
+  void prefetch_batch_host(const float* images, const int32_t* labels);
+  // Loss of the last step (D2H + sync), for callers that issue step()
+  // without reading the loss and prefetch the next batch first.
+  float read_loss();
   void synthetic_batch(u64 seed);
   void get_weights(int layer, float* host, size_t count);
   void set_weights(int layer, const float* host, size_t count);
@@ -175,6 +182,10 @@ class Session {
   std::vector<u64> grad_off_;    // per layer float offset into grads_
   size_t grads_count_ = 0;
   float* pinned_loss_ = nullptr;
+  cudaStream_t in_stream_ = nullptr;      // input pipeline stream (prefetch_batch_host)
+  char* staging_ = nullptr;               // next batch: images then labels
+  cudaEvent_t staged_ready_ = nullptr, staging_free_ = nullptr;
+  bool has_staged_ = false, staged_images_ = false, staged_labels_ = false;
   unsigned long long* signal_ = nullptr;  // peer barrier flags [2][kPeerMaxRanks]
   vdnnk::PeerArgs peer_{};
   vdnnk::PeerChunk* peer_chunks_ = nullptr;

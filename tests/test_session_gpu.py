@@ -301,3 +301,38 @@ def test_device_offload_target_requires_a_buffer():
         s.step(LR)
     with pytest.raises(V.VdnnError):
         V.Session(g, d, cm, 4 << 30, offload_target="device", compress_offload=True)
+
+
+def test_prefetched_batches_match_set_batch():
+    """Input pipeline: batches staged with prefetch_batch_ptr (pinned host ->
+    device on the input stream, overlapping the running step) give the same
+    weights and losses as set_batch before every step."""
+    _need_gpu()
+    g = V.build_preset("alexnet", 4)
+    cm = V.CostModel()
+    w = numeric.he_weights(g, cm, seed=71)
+    d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+    batches = [_batch(g, seed=72 + i) for i in range(3)]
+    pinned = [(torch.from_numpy(im).pin_memory(), torch.from_numpy(lb).pin_memory()) for im, lb in batches]
+    outs = []
+    for mode in ("set", "prefetch"):
+        s = V.Session(g, d, cm, 4 << 30)
+        for k, v in w.items():
+            s.set_weights(k, v)
+        losses = []
+        if mode == "set":
+            for im, lb in batches:
+                s.set_batch(im, lb)
+                losses.append(s.step(LR))
+        else:
+            s.prefetch_batch_ptr(pinned[0][0].data_ptr(), pinned[0][1].data_ptr())
+            for i in range(3):
+                s.step(LR, want_loss=False)
+                if i + 1 < 3:
+                    s.prefetch_batch_ptr(pinned[i + 1][0].data_ptr(), pinned[i + 1][1].data_ptr())
+                losses.append(s.read_loss())
+        outs.append((losses, {k: s.get_weights(k) for k in w}))
+        del s
+    assert outs[0][0] == outs[1][0]
+    for k in w:
+        assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
