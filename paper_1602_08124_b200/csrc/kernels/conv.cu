@@ -406,6 +406,16 @@ cudaError_t launch_halo(HaloParams& h, const ConvParams& p, cudaStream_t st) {
 
 // CTA-pair kernel (tc_conv_pair.cuh) for FPROP / DGRAD with >= 256 output
 // columns and at least two tiles of 256 x 256 per pair. VDNN_PAIR=0 disables.
+// 64-column wgrad: 4-stage rings (2 CTAs / SM still fit) -- the short
+// per-stage MMA work (4 x M128N64K8) leaves 3-stage rings latency-bound
+bool wgrad_deep64() {
+  static const bool on = [] {
+    const char* e = std::getenv("VDNN_WGRAD_DEEP64");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool pair_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("VDNN_PAIR");
@@ -550,6 +560,7 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
       if (tall_ok(p, 64, splits))
         return deep ? launch_bn<64, 5, false, true, 256>(p, ta, tb, tc, splits, st)
                     : launch_bn<64, 2, false, true, 256>(p, ta, tb, tc, splits, st);
+      if (p.kind == kWgrad && wgrad_deep64()) return launch_bn<64, 4, false, true>(p, ta, tb, tc, splits, st);
       return launch_bn<64, kStages, false, true>(p, ta, tb, tc, splits, st);
     }
     return launch_bn<64, kStages, false, false>(p, ta, tb, tc, splits, st);
