@@ -21,7 +21,13 @@
  *   replay_check                     replay.hpp:95-304       -> vdnn_replay_check
  *
  * and the B200 training executor that *runs* a plan (vdnn_session_*), plus
- * kernel-level entry points (vdnn_kernel_*) used by the parity tests.
+ * kernel-level entry points (vdnn_kernel_*) used by the parity tests. The
+ * executor's extensions have no reference counterpart (the reference only
+ * times the schedule): the data-parallel exchange (vdnn_session_peer_*:
+ * the reference is single-GPU), the device / peer-HBM offload
+ * target (vdnn_session_set_offload_buffer, _spill_*: a LinkProfile other than
+ * PCIe, cost_model.hpp:22-30), compressed offload (compress_offload) and the
+ * input pipeline (vdnn_session_prefetch_batch_host).
  *
  * Conventions: every call returns vdnn_status; the message of the last
  * failure on the calling thread is vdnn_last_error(). OOM is not an error:
