@@ -308,16 +308,22 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         labs_h = torch.from_numpy(rng.integers(0, ls.c, size=sh.n).astype(np.int32)).pin_memory()
         # input pipeline: each step's batch is staged (pinned host -> device)
         # on the session's input stream while the previous step runs; the
-        # step moves it into the INPUT extent, the loss is read back after the
-        # next batch was queued
+        # step moves it into the INPUT extent; every step's loss is read back,
+        # pipelined one step behind (queue now, wait after the next step was
+        # enqueued) so the host never idles the GPU
+        pending = []
+
         def e2e_step():
             one(False)
+            pending.append(s.queue_loss())
             s.prefetch_batch_ptr(imgs_h.data_ptr(), labs_h.data_ptr())
-            return s.read_loss()
+            if len(pending) > 1:
+                s.wait_loss(pending.pop(0))
 
         s.prefetch_batch_ptr(imgs_h.data_ptr(), labs_h.data_ptr())
         for _ in range(2):
             e2e_step()
+        s.wait_loss(pending.pop(0))
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
@@ -326,6 +332,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         e0.record(stream)
         for _ in range(args.steps):
             e2e_step()
+        s.wait_loss(pending.pop(0))  # the last step's loss is read back inside the timed region
         e1.record(stream)
         e1.synchronize()
         wall = (time.perf_counter() - t0) / args.steps

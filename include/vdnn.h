@@ -278,6 +278,9 @@ vdnn_status vdnn_session_synthetic_batch(vdnn_session* s, uint64_t seed);
  * vdnn_session_read_loss so the host does not wait on the loss before staging the next batch. */
 vdnn_status vdnn_session_prefetch_batch_host(vdnn_session* s, const float* images, const int32_t* labels);
 vdnn_status vdnn_session_read_loss(vdnn_session* s, float* loss);
+/* Pipelined loss readback: queue the last step's loss (ticket), wait for it later (<= 4 outstanding). */
+vdnn_status vdnn_session_queue_loss(vdnn_session* s, int64_t* ticket);
+vdnn_status vdnn_session_wait_loss(vdnn_session* s, int64_t ticket, float* loss);
 /* Weights: per layer, KRSC conv / [out][in]+bias FC; float count = weight_bytes/4. */
 vdnn_status vdnn_session_get_weights(vdnn_session* s, int32_t layer, float* host, size_t count);
 vdnn_status vdnn_session_set_weights(vdnn_session* s, int32_t layer, const float* host, size_t count);

@@ -810,6 +810,17 @@ class Session:
         _call("vdnn_session_read_loss", self.handle, C.byref(self._loss))
         return float(self._loss.value)
 
+    def queue_loss(self) -> int:
+        """Queue the D2H of the last step's loss; returns a ticket for wait_loss."""
+        t = C.c_int64()
+        _call("vdnn_session_queue_loss", self.handle, C.byref(t))
+        return t.value
+
+    def wait_loss(self, ticket: int) -> float:
+        v = C.c_float()
+        _call("vdnn_session_wait_loss", self.handle, C.c_int64(ticket), C.byref(v))
+        return float(v.value)
+
     def synthetic_batch(self, seed: int = 1234) -> None:
         _call("vdnn_session_synthetic_batch", self.handle, C.c_uint64(seed))
 

@@ -253,6 +253,18 @@ vdnn_status vdnn_session_read_loss(vdnn_session* s, float* loss) {
     return VDNN_OK;
   });
 }
+vdnn_status vdnn_session_queue_loss(vdnn_session* s, int64_t* ticket) {
+  return guard([&] {
+    *ticket = S(s).queue_loss();
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_wait_loss(vdnn_session* s, int64_t ticket, float* loss) {
+  return guard([&] {
+    *loss = S(s).wait_loss(ticket);
+    return VDNN_OK;
+  });
+}
 vdnn_status vdnn_session_offload_bytes(vdnn_session* s, uint64_t* bytes) {
   return guard([&] {
     *bytes = S(s).offload_bytes();

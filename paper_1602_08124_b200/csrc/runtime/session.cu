@@ -168,6 +168,11 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
     t0_ev_.resize(nsteps);
     for (auto& e : t0_ev_) check(cudaEventCreate(&e), "event");
     check(cudaEventCreate(&ev_iter_), "event");
+    ev_prev_.resize(ev_.size());
+    for (auto& e : ev_prev_) check(cudaEventCreate(&e), "event");
+    t0_ev_prev_.resize(nsteps);
+    for (auto& e : t0_ev_prev_) check(cudaEventCreate(&e), "event");
+    check(cudaEventCreate(&ev_iter_prev_), "event");
   }
   check(cudaEventCreateWithFlags(&ev_sync_, cudaEventDisableTiming), "event");
 
@@ -181,6 +186,9 @@ Session::~Session() {
   for (auto e : ev_) cudaEventDestroy(e);
   for (auto e : step_ev_) cudaEventDestroy(e);
   for (auto e : t0_ev_) cudaEventDestroy(e);
+  for (auto e : ev_prev_) cudaEventDestroy(e);
+  for (auto e : t0_ev_prev_) cudaEventDestroy(e);
+  if (ev_iter_prev_) cudaEventDestroy(ev_iter_prev_);
   for (auto e : xfer_ev_) cudaEventDestroy(e);
   if (ev_iter_) cudaEventDestroy(ev_iter_);
   if (ev_sync_) cudaEventDestroy(ev_sync_);
@@ -188,6 +196,9 @@ Session::~Session() {
   if (staged_ready_) cudaEventDestroy(staged_ready_);
   if (staging_free_) cudaEventDestroy(staging_free_);
   if (staging_) cudaFree(staging_);
+  for (auto e : loss_ev_)
+    if (e) cudaEventDestroy(e);
+  if (loss_ring_) cudaFreeHost(loss_ring_);
   if (in_stream_) cudaStreamDestroy(in_stream_);
   peer_detach();
   if (signal_) cudaFree(signal_);
@@ -704,6 +715,11 @@ void Session::step(float lr, float* loss_host) {
     throw PlanError(Err::Config, "the plan offloads but no offload buffer is set (set_offload_buffer / spill_attach)");
   timed_ = o_.record_timeline;
   vdnnk::set_precise(o_.precise);
+  if (timed_) {  // this step records into the set the step before last used (see session.h)
+    std::swap(ev_, ev_prev_);
+    std::swap(t0_ev_, t0_ev_prev_);
+    std::swap(ev_iter_, ev_iter_prev_);
+  }
   if (has_staged_) {  // the batch prefetch_batch_host staged: into the INPUT extent, then free the buffer
     const u64 bytes = lv_.feat[static_cast<size_t>(input_id_)];
     check(cudaStreamWaitEvent(cs_, staged_ready_, 0), "wait");
@@ -774,6 +790,26 @@ void Session::prefetch_batch_host(const float* images, const int32_t* labels) {
   has_staged_ = true;
   staged_images_ = images != nullptr;
   staged_labels_ = labels != nullptr;
+}
+
+int64_t Session::queue_loss() {
+  if (!loss_ring_) {
+    check(cudaHostAlloc(&loss_ring_, kLossRing * sizeof(float), cudaHostAllocDefault), "cudaHostAlloc(loss ring)");
+    for (auto& e : loss_ev_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  }
+  const int64_t t = loss_tickets_++;
+  const int slot = static_cast<int>(t % kLossRing);
+  check(cudaMemcpyAsync(loss_ring_ + slot, loss_, 4, cudaMemcpyDeviceToHost, cs_), "loss D2H");
+  check(cudaEventRecord(loss_ev_[slot], cs_), "record");
+  return t;
+}
+
+float Session::wait_loss(int64_t ticket) {
+  if (ticket < 0 || ticket >= loss_tickets_ || ticket < loss_tickets_ - kLossRing)
+    throw PlanError(Err::Generic, "loss ticket out of range (at most 4 outstanding)");
+  const int slot = static_cast<int>(ticket % kLossRing);
+  check(cudaEventSynchronize(loss_ev_[slot]), "sync");
+  return loss_ring_[slot];
 }
 
 float Session::read_loss() {

@@ -95,6 +95,11 @@ class Session {
   // Loss of the last step (D2H + sync), for callers that issue step()
   // without reading the loss and prefetch the next batch first.
   float read_loss();
+  // Pipelined loss readback: queue the D2H of the last step's loss into a
+  // pinned ring slot (returns a ticket) and wait for it later, so the host
+  // can enqueue the next step before the previous loss arrives.
+  int64_t queue_loss();
+  float wait_loss(int64_t ticket);
   void synthetic_batch(u64 seed);
   void get_weights(int layer, float* host, size_t count);
   void set_weights(int layer, const float* host, size_t count);
@@ -186,6 +191,10 @@ class Session {
   char* staging_ = nullptr;               // next batch: images then labels
   cudaEvent_t staged_ready_ = nullptr, staging_free_ = nullptr;
   bool has_staged_ = false, staged_images_ = false, staged_labels_ = false;
+  static constexpr int kLossRing = 4;
+  float* loss_ring_ = nullptr;            // pinned, kLossRing slots
+  cudaEvent_t loss_ev_[kLossRing] = {};
+  int64_t loss_tickets_ = 0;
   unsigned long long* signal_ = nullptr;  // peer barrier flags [2][kPeerMaxRanks]
   vdnnk::PeerArgs peer_{};
   vdnnk::PeerChunk* peer_chunks_ = nullptr;
@@ -207,6 +216,11 @@ class Session {
   // timing
   std::vector<cudaEvent_t> ev_;  // pairs: [2i] start, [2i+1] end
   cudaEvent_t ev_iter_ = nullptr;
+  // the previous step's timing events: steps alternate between two sets so
+  // the host can enqueue step k+1 while step k's events are still pending
+  // (re-recording in-flight timing events stalled the host ~1 step)
+  std::vector<cudaEvent_t> ev_prev_, t0_ev_prev_;
+  cudaEvent_t ev_iter_prev_ = nullptr;
   cudaEvent_t ev_sync_ = nullptr;
   std::vector<cudaEvent_t> step_ev_;  // compute-side step-start events (cross-stream gating)
   std::vector<cudaEvent_t> t0_ev_;    // timed step-start events (record_timeline)

@@ -315,7 +315,7 @@ def test_prefetched_batches_match_set_batch():
     batches = [_batch(g, seed=72 + i) for i in range(3)]
     pinned = [(torch.from_numpy(im).pin_memory(), torch.from_numpy(lb).pin_memory()) for im, lb in batches]
     outs = []
-    for mode in ("set", "prefetch"):
+    for mode in ("set", "prefetch", "pipelined"):
         s = V.Session(g, d, cm, 4 << 30)
         for k, v in w.items():
             s.set_weights(k, v)
@@ -324,15 +324,25 @@ def test_prefetched_batches_match_set_batch():
             for im, lb in batches:
                 s.set_batch(im, lb)
                 losses.append(s.step(LR))
-        else:
+        elif mode == "prefetch":
             s.prefetch_batch_ptr(pinned[0][0].data_ptr(), pinned[0][1].data_ptr())
             for i in range(3):
                 s.step(LR, want_loss=False)
                 if i + 1 < 3:
                     s.prefetch_batch_ptr(pinned[i + 1][0].data_ptr(), pinned[i + 1][1].data_ptr())
                 losses.append(s.read_loss())
+        else:  # loss readback pipelined one step behind (queue_loss / wait_loss)
+            s.prefetch_batch_ptr(pinned[0][0].data_ptr(), pinned[0][1].data_ptr())
+            tickets = []
+            for i in range(3):
+                s.step(LR, want_loss=False)
+                tickets.append(s.queue_loss())
+                if i + 1 < 3:
+                    s.prefetch_batch_ptr(pinned[i + 1][0].data_ptr(), pinned[i + 1][1].data_ptr())
+            losses = [s.wait_loss(t) for t in tickets]
         outs.append((losses, {k: s.get_weights(k) for k in w}))
         del s
-    assert outs[0][0] == outs[1][0]
-    for k in w:
-        assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
+    for o in outs[1:]:
+        assert o[0] == outs[0][0]
+        for k in w:
+            assert np.array_equal(o[1][k], outs[0][1][k]), k
