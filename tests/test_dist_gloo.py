@@ -109,3 +109,49 @@ def test_peer_attach_all_or_none(fail_rank):
             assert status == "ok" and attached == (rank, [bytes([r]) * 8 for r in range(world)]) and not detached
         else:
             assert status.startswith("unavailable:") and "rank 1" in status and detached
+
+
+class _FakeSpillSession:
+    def __init__(self, rank):
+        self.rank = rank
+        self.attached = None
+
+    def spill_export(self):
+        return bytes([0xA0 + self.rank]) * 64
+
+    def spill_attach(self, handle):
+        self.attached = handle
+
+
+def _spill_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1602_08124_b200.dist import ring_spill
+    s = _FakeSpillSession(rank)
+    peer = ring_spill(s, world)
+    q.put((rank, peer, s.attached))
+    dist.destroy_process_group()
+
+
+def test_ring_spill_routes_each_rank_to_its_neighbour():
+    """Peer-HBM offload target: rank r offloads into rank (r+1) % N's spill
+    buffer (the handle it attaches is the neighbour's export)."""
+    world = 3
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_spill_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    for rank, peer, attached in res:
+        assert peer == (rank + 1) % world
+        assert attached == bytes([0xA0 + peer]) * 64
+
+
+def test_ring_spill_needs_two_ranks():
+    from paper_1602_08124_b200.dist import ring_spill
+    with pytest.raises(ValueError):
+        ring_spill(_FakeSpillSession(0), 1)
