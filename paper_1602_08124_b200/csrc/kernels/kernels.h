@@ -95,7 +95,7 @@ uint64_t launch_count();
 // floats (multiple of 4, 16-B aligned); `wire` (device counter, may be null
 // for decompress) accumulates the bytes that crossed the link.
 constexpr int kZvcChunk = 1024;
-constexpr int kZvcSlot = 128 + 4 * kZvcChunk;
+constexpr int kZvcSlot = 128 + 16 + 4 * kZvcChunk;  // mask + header + dense values (worst case)
 uint64_t zvc_slot_bytes(uint64_t bytes);
 bool zvc_eligible(const void* p, uint64_t bytes);
 cudaError_t zvc_compress(const float* src, uint64_t count, void* host_dst, unsigned long long* wire, cudaStream_t st);

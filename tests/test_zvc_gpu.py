@@ -13,6 +13,29 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
+def _pad16(b):
+    return (b + 15) // 16 * 16
+
+
+def _expected_wire(x):
+    """Bytes the v2 format moves (zvc.cu): per 1024-value chunk the mask and a
+    16-B header, then either the raw nonzeros or -- when the nonzeros' top
+    bytes span <= 15 -- their low 3 bytes plus a 4-bit top-byte offset."""
+    u = x.view(torch.int32).cpu().numpy().view(np.uint32)
+    n = u.size
+    u = np.concatenate([u, np.zeros((-n) % 1024, dtype=np.uint32)]).reshape(-1, 1024)
+    total = 0
+    for row in u:
+        nzv = row[row != 0]
+        nnz = nzv.size
+        top = nzv >> 24
+        if nnz and int(top.max()) - int(top.min()) <= 15:
+            total += 144 + _pad16(3 * nnz) + _pad16((nnz + 1) // 2)
+        else:
+            total += 144 + _pad16(4 * nnz)
+    return total
+
+
 def _roundtrip(x):
     n = x.numel()
     lib = L.lib()
@@ -27,10 +50,8 @@ def _roundtrip(x):
                                           C.c_void_p(wire.data_ptr() + 8), None) == 0, lib.vdnn_last_error()
     torch.cuda.synchronize()
     assert torch.equal(x.view(torch.int32), y.view(torch.int32)), "round trip not bit-exact"
-    nnz = int((x.view(torch.int32) != 0).sum())
-    chunks = (n + 1023) // 1024
     w = wire.cpu().tolist()
-    assert w[0] == w[1] == 128 * chunks + 4 * nnz
+    assert w[0] == w[1] == _expected_wire(x)
     return w[0]
 
 
@@ -45,14 +66,30 @@ def test_zvc_special_values():
     vals = torch.tensor([0.0, -0.0, float("nan"), float("inf"), -float("inf"), 1e-45, -1e-45, 3.0] * 512,
                         device="cuda")
     w = _roundtrip(vals)
-    assert w == 128 * 4 + 4 * (vals.numel() - 512)  # only +0.0 is dropped (-0.0 is a value)
+    # only +0.0 is dropped (-0.0 is a value); mixed signs / exponents: raw mode
+    assert w == 4 * 144 + 4 * (vals.numel() - 512)
 
 
 def test_zvc_all_zero_and_dense():
     z = torch.zeros(1 << 16, device="cuda")
-    assert _roundtrip(z) == 128 * 64
-    d = torch.rand(1 << 16, device="cuda") + 1.0
-    assert _roundtrip(d) == 128 * 64 + 4 * (1 << 16)
+    assert _roundtrip(z) == 144 * 64
+    d = torch.rand(1 << 16, device="cuda") + 1.0  # [1, 2): one top byte -> packed mode, 3.5 B per value
+    assert _roundtrip(d) == 144 * 64 + 64 * (3072 + 512)
+
+
+def test_zvc_packed_mode_edge_cases():
+    """Top-byte span exactly 15 (packed) and 16 (raw), odd nonzero counts."""
+    base = torch.tensor([1.0], device="cuda").view(torch.int32)
+    rows = []
+    for span, nnz in ((15, 1023), (16, 1001), (0, 1), (7, 3)):
+        t = torch.zeros(1024, dtype=torch.int32, device="cuda")
+        idx = torch.randperm(1024, device="cuda")[:nnz]
+        tops = torch.arange(nnz, device="cuda") % (span + 1)
+        vals = (base + (tops << 24) - (0 << 24)) | (torch.arange(nnz, device="cuda", dtype=torch.int32) & 0xFFFFFF)
+        t[idx] = vals.to(torch.int32)
+        rows.append(t)
+    x = torch.cat(rows).view(torch.float32)
+    _roundtrip(x)
 
 
 def _train(g, d, cap, compress, steps=2):
