@@ -447,8 +447,12 @@ void Session::build_program() {
 // outputs (its owner feeds an in-place ACTV), about half zeros; dense maps
 // (raw images, max-pool outputs: ~94% nonzero) keep the copy engines, which
 // move dense bytes ~10% faster than SM-driven PCIe stores/loads.
+// ReLU outputs (~35% nonzero on VGG-16) and max-pool outputs (the max of
+// ReLU windows: ~50% zeros, tools/zvc_stats.py) go through the compressing
+// kernels; dense maps (the input images) keep the copy engines.
 bool Session::compressible(int owner) const {
   if (!o_.compress_offload) return false;
+  if (g_.at(owner).kind == Kind::Pool) return true;
   for (int u : g_.users(owner))
     if (g_.at(u).kind == Kind::Actv) return true;
   return false;

@@ -17,7 +17,7 @@ for _ in range(3):
 s.step(0.01)
 tot_raw = tot_zvc = tot_nib = 0
 for l in g.layers():
-    if l.kind != V.LayerKind.Conv:
+    if l.kind not in (V.LayerKind.Conv, V.LayerKind.Pool):
         continue
     sh = g.shape(l.id)
     n = sh.n * sh.c * sh.h * sh.w
@@ -35,6 +35,6 @@ for l in g.layers():
     tot_raw += 4 * chunks.size
     tot_zvc += zvc.sum()
     tot_nib += nib.sum()
-    print(f"L{l.id:2d} {sh.c:4d}x{sh.h:3d}: zeros {1 - nz.mean():.3f}  chunks with top-byte span<=15: "
+    print(f"L{l.id:2d} {'pool' if l.kind == V.LayerKind.Pool else 'conv'} {sh.c:4d}x{sh.h:3d}: zeros {1 - nz.mean():.3f}  chunks with top-byte span<=15: "
           f"{(span <= 15).mean():.3f}  zvc {zvc.sum() / (4 * chunks.size):.3f}  +nibble {nib.sum() / (4 * chunks.size):.3f}")
 print(f"all conv outputs: zvc {tot_zvc / tot_raw:.3f}  zvc+nibble {tot_nib / tot_raw:.3f}")
