@@ -439,7 +439,13 @@ __global__ void __launch_bounds__(kWgThreads, 1) c3tc_wgrad_kernel(const float* 
 // the same builders: W [Cout][KK] rows are not 16-B aligned at KK = 363, so
 // it is not resident -- 12 x NB x 128 B would not fit next to the ring).
 constexpr int kMkFpStages = 4;
-__global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_mk_kernel(const float* __restrict__ x,
+// builder groups take stages round-robin: group spacing (kMkGroups) must not
+// exceed the ring depth for the parity waits to stay unambiguous
+constexpr int kMkGroups = 4;
+constexpr int kMkMmaWarp = 4 + 4 * kMkGroups;
+constexpr int kFpMkThreads = 32 * (kMkMmaWarp + 1);
+static_assert(kMkGroups <= kMkFpStages, "builder spacing must fit the ring");
+__global__ void __launch_bounds__(kFpMkThreads, 1) c3tc_fprop_mk_kernel(const float* __restrict__ x,
                                                                       const float* __restrict__ w,
                                                                       const __grid_constant__ CUtensorMap tma_y,
                                                                       C3Geom g, int NB, int NBP, int KB, int relu) {
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_mk_kernel(const floa
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   c3_table_mk(g, KB, tab, tab + kMkMaxKB * 32);
-  if (warp == 12) {
+  if (warp == kMkMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
                  "r"(2 * NBP)
                  : "memory");
@@ -487,8 +493,8 @@ __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_mk_kernel(const floa
   const int* off = tab;
   const int* rs = tab + kMkMaxKB * 32;
 
-  if (warp >= 4 && warp < 12) {
-    // ---------------- builders: two groups of 4 warps take alternate STAGES ----------------
+  if (warp >= 4 && warp < kMkMmaWarp) {
+    // ---------------- builders: kMkGroups groups of 4 warps take stages round-robin ----------------
     // (mbarrier parity waits are only unambiguous if a builder's consecutive
     // stages are at most kMkFpStages apart: alternating whole 12-stage tiles
     // let a group wait on a slot two phases back -- wrong data, measured)
@@ -498,7 +504,7 @@ __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_mk_kernel(const floa
     C3Pix q{};
     const int total = ((ntiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
                        static_cast<int>(gridDim.x)) * KB;
-    for (int it = grp; it < total; it += 2) {
+    for (int it = grp; it < total; it += kMkGroups) {
       const int tl = it / KB, kb = it - tl * KB;
       if (tl != cur_tl) {
         cur_tl = tl;
@@ -525,7 +531,7 @@ __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_mk_kernel(const floa
       fence_proxy_async();
       mbar_arrive(full_bar(s));
     }
-  } else if (warp == 12) {
+  } else if (warp == kMkMmaWarp) {
     // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
     const uint32_t idesc = make_idesc_tf32(NB, false, false);
     const bool leader = elect_one();
@@ -591,7 +597,7 @@ __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_mk_kernel(const floa
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 12) {
+  if (warp == kMkMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * NBP) : "memory");
   }
@@ -832,7 +838,7 @@ cudaError_t c3tc_fprop(const ConvArgs& a, const float* w, float* y, cudaStream_t
       attr_mk = smem;
     }
     const int ntiles = (g.P + kBM - 1) / kBM;
-    c3tc_fprop_mk_kernel<<<std::min(kSms, ntiles), kFpThreads, smem, st>>>(a.x[0], w, ty, g, NB, NBP, KB,
+    c3tc_fprop_mk_kernel<<<std::min(kSms, ntiles), kFpMkThreads, smem, st>>>(a.x[0], w, ty, g, NB, NBP, KB,
                                                                             a.relu_out);
     count_launch();
     return cudaGetLastError();
