@@ -259,6 +259,8 @@ typedef struct vdnn_session_options {
   int32_t compress_offload;  /* 1: offload/prefetch through the SMs in lossless zero-value-compressed form */
   int32_t offload_target;    /* 0: pinned host arena (PCIe); 1: a device buffer set with
                                 vdnn_session_set_offload_buffer / _spill_attach (e.g. a peer GPU's HBM) */
+  int32_t cuda_graph;        /* 1: replay each step as one CUDA graph (captured on the 2nd step, re-captured
+                                when lr changes) */
 } vdnn_session_options;
 void vdnn_session_options_default(vdnn_session_options* o);
 

@@ -737,13 +737,15 @@ class Session:
     def __init__(self, g: NetworkGraph, decision: PolicyDecision, cost: Optional[CostModel] = None,
                  capacity: int = 12884901888, device: int = 0, weight_seed: int = 5000,
                  external_grads: bool = False, record_timeline: bool = False, precise_fp32: bool = False,
-                 compress_offload: bool = False, offload_target: str = "host"):
+                 compress_offload: bool = False, offload_target: str = "host", cuda_graph: bool = False):
         """compress_offload: move offloads/prefetches through the SMs in a
         lossless zero-value-compressed form (same schedule, bit-identical
         restored buffers, fewer bytes on the host link).
         offload_target: "host" (pinned host memory over PCIe, the reference's
         model) or "device" (a device buffer given to set_offload_buffer, or a
-        peer GPU's spill buffer via spill_export / spill_attach: NVLink)."""
+        peer GPU's spill buffer via spill_export / spill_attach: NVLink).
+        cuda_graph: replay each step as one CUDA graph (captured on the second
+        step; re-captured when lr changes)."""
         if offload_target not in ("host", "device"):
             raise ValueError(f"offload_target must be 'host' or 'device', not {offload_target!r}")
         self.graph = g
@@ -759,6 +761,7 @@ class Session:
         opt.precise_fp32 = int(precise_fp32)
         opt.compress_offload = int(compress_offload)
         opt.offload_target = 0 if offload_target == "host" else 1
+        opt.cuda_graph = int(cuda_graph)
         d = decision._handle(g)
         c = self.cost._c()
         h = C.c_void_p()

@@ -50,6 +50,7 @@ void vdnn_session_options_default(vdnn_session_options* o) {
   o->precise_fp32 = 0;
   o->compress_offload = 0;
   o->offload_target = 0;
+  o->cuda_graph = 0;
 }
 
 vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, const vdnn_cost_model* cm,
@@ -66,6 +67,7 @@ vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, con
       o.precise = opt->precise_fp32 != 0;
       o.compress_offload = opt->compress_offload != 0;
       o.offload_target = opt->offload_target;
+      o.cuda_graph = opt->cuda_graph != 0;
     }
     if (!g->net.finalized()) throw vdnnp::PlanError(vdnnp::Err::Generic, "graph is not finalized");
     auto* s = new vdnnrt::Session(g->net, d->d, vdnncapi::cost_from(cm), capacity, o);

@@ -183,6 +183,7 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
 Session::~Session() {
   if (cs_) cudaStreamSynchronize(cs_);
   if (ms_) cudaStreamSynchronize(ms_);
+  if (gexec_) cudaGraphExecDestroy(gexec_);  // before the events its nodes record
   for (auto e : ev_) cudaEventDestroy(e);
   for (auto e : step_ev_) cudaEventDestroy(e);
   for (auto e : t0_ev_) cudaEventDestroy(e);
@@ -216,6 +217,7 @@ Session::~Session() {
   if (grads_ && grads_owned_) cudaFree(grads_);
   if (cs_) cudaStreamDestroy(cs_);
   if (ms_) cudaStreamDestroy(ms_);
+  cudaGetLastError();  // leave no stale error from the teardown calls for the next session
 }
 
 // ------------------------------------------------------------- program ----
@@ -719,7 +721,7 @@ void Session::step(float lr, float* loss_host) {
     throw PlanError(Err::Config, "the plan offloads but no offload buffer is set (set_offload_buffer / spill_attach)");
   timed_ = o_.record_timeline;
   vdnnk::set_precise(o_.precise);
-  if (timed_) {  // this step records into the set the step before last used (see session.h)
+  if (timed_ && !o_.cuda_graph) {  // this step records into the set the step before last used (see session.h)
     std::swap(ev_, ev_prev_);
     std::swap(t0_ev_, t0_ev_prev_);
     std::swap(ev_iter_, ev_iter_prev_);
@@ -734,12 +736,46 @@ void Session::step(float lr, float* loss_host) {
     check(cudaEventRecord(staging_free_, cs_), "record");
     has_staged_ = false;
   }
-  if (timed_) check(cudaEventRecord(ev_iter_, cs_), "record");
-  // the memory stream never runs ahead into a new iteration
-  check(cudaEventRecord(ev_sync_, cs_), "record");
-  check(cudaStreamWaitEvent(ms_, ev_sync_, 0), "wait");
-  for (const FwdStep& s : fwd_) run_fwd(s, lr);
-  for (const BwdStep& s : bwd_) run_bwd(s, lr);
+  if (!o_.cuda_graph || eager_steps_ < 1) {
+    enqueue_step(lr);
+    ++eager_steps_;
+  } else {
+    bool captured_now = false;
+    if (!gexec_ || lr != graph_lr_) {
+      captured_now = true;
+      if (gexec_) cudaGraphExecDestroy(gexec_);
+      gexec_ = nullptr;
+      const u64 c0 = copy_off_, c1 = copy_pre_, r0 = raw_off_, r1 = raw_pre_, l0 = vdnnk::launch_count();
+      cudaGraph_t graph = nullptr;
+      check(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeThreadLocal), "begin capture");
+      try {
+        enqueue_step(lr);
+      } catch (...) {
+        cudaStreamEndCapture(cs_, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      check(cudaStreamEndCapture(cs_, &graph), "end capture");
+      const cudaError_t e = cudaGraphInstantiate(&gexec_, graph, 0);
+      cudaGraphDestroy(graph);
+      check(e, "graph instantiate");
+      graph_lr_ = lr;
+      g_copy_off_ = copy_off_ - c0;
+      g_copy_pre_ = copy_pre_ - c1;
+      g_raw_off_ = raw_off_ - r0;
+      g_raw_pre_ = raw_pre_ - r1;
+      g_launches_ = vdnnk::launch_count() - l0;
+      copy_off_ = c0, copy_pre_ = c1, raw_off_ = r0, raw_pre_ = r1;  // re-added per launch below
+    }
+    check(cudaGraphLaunch(gexec_, cs_), "graph launch");
+    copy_off_ += g_copy_off_;
+    copy_pre_ += g_copy_pre_;
+    raw_off_ += g_raw_off_;
+    raw_pre_ += g_raw_pre_;
+    // the captured kernels were counted while capturing; every later replay launches them again
+    if (captured_now) captured_now = false;
+    else vdnnk::count_launch(g_launches_);
+  }
   if (loss_host) {
     check(cudaMemcpyAsync(pinned_loss_, loss_, 4, cudaMemcpyDeviceToHost, cs_), "loss D2H");
     check(cudaStreamSynchronize(cs_), "sync");
@@ -814,6 +850,16 @@ float Session::wait_loss(int64_t ticket) {
   const int slot = static_cast<int>(ticket % kLossRing);
   check(cudaEventSynchronize(loss_ev_[slot]), "sync");
   return loss_ring_[slot];
+}
+
+// One iteration's stream work (both streams; in graph mode this is what gets captured).
+void Session::enqueue_step(float lr) {
+  if (timed_) check(cudaEventRecord(ev_iter_, cs_), "record");
+  // the memory stream never runs ahead into a new iteration
+  check(cudaEventRecord(ev_sync_, cs_), "record");
+  check(cudaStreamWaitEvent(ms_, ev_sync_, 0), "wait");
+  for (const FwdStep& s : fwd_) run_fwd(s, lr);
+  for (const BwdStep& s : bwd_) run_bwd(s, lr);
 }
 
 float Session::read_loss() {
@@ -900,7 +946,10 @@ vdnnp::Report Session::measured_report() const {
   if (ev_.empty()) throw PlanError(Err::Generic, "session was created without record_timeline");
   auto ns = [&](cudaEvent_t e) -> i64 {
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, ev_iter_, e) != cudaSuccess) return 0;
+    if (cudaEventElapsedTime(&ms, ev_iter_, e) != cudaSuccess) {
+      cudaGetLastError();  // do not leave a stale error for the next launch check
+      return 0;
+    }
     return std::max<i64>(0, static_cast<i64>(std::llround(static_cast<double>(ms) * 1e6)));
   };
   const size_t nst = fwd_.size() + bwd_.size();
@@ -1040,7 +1089,10 @@ void Session::layer_times(int n, double* fwd_ms, double* bwd_ms) const {
   }
   auto el = [&](size_t k) {
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev_[2 * k], ev_[2 * k + 1]);
+    if (cudaEventElapsedTime(&ms, ev_[2 * k], ev_[2 * k + 1]) != cudaSuccess) {
+      cudaGetLastError();
+      return 0.0;
+    }
     return static_cast<double>(ms);
   };
   for (const FwdStep& s : fwd_)

@@ -33,6 +33,10 @@ struct Options {
   // set_offload_buffer / spill_attach (e.g. a peer GPU's spare HBM over
   // NVLink). Same schedule, same slots, same sync rules.
   int offload_target = 0;
+  // Replay each training step as one CUDA graph (captured on the second
+  // step, re-captured when lr changes): both streams' work, the transfers and
+  // their event gating become graph nodes; one launch per step.
+  bool cuda_graph = false;
 };
 
 // One gradient plane: the slice of a dX buffer that holds the gradient w.r.t.
@@ -200,6 +204,12 @@ class Session {
   vdnnk::PeerChunk* peer_chunks_ = nullptr;
   std::vector<void*> peer_maps_;          // IPC-opened pointers (closed on detach)
   bool host_owned_ = false;               // host_ is our cudaHostAlloc (else a device target)
+  // CUDA graph mode
+  cudaGraphExec_t gexec_ = nullptr;
+  float graph_lr_ = 0.f;
+  int eager_steps_ = 0;
+  u64 g_copy_off_ = 0, g_copy_pre_ = 0, g_raw_off_ = 0, g_raw_pre_ = 0, g_launches_ = 0;  // per-step deltas
+  void enqueue_step(float lr);
   void* spill_ = nullptr;                 // buffer this rank hosts for a peer's offloads
   void* spill_map_ = nullptr;             // IPC mapping of the peer's spill buffer (our target)
   int peer_world_ = 0;

@@ -346,3 +346,35 @@ def test_prefetched_batches_match_set_batch():
         assert o[0] == outs[0][0]
         for k in w:
             assert np.array_equal(o[1][k], outs[0][1][k]), k
+
+
+@pytest.mark.parametrize("compress", [False, True], ids=["copy-engines", "zvc"])
+def test_cuda_graph_steps_are_bit_identical(compress):
+    """cuda_graph=True: the step is captured once (second step) and replayed
+    as one CUDA graph -- both streams, the offload/prefetch copies and their
+    event gating -- and re-captured when lr changes. Weights, losses, transfer
+    accounting and the measured log equal the eager run."""
+    _need_gpu()
+    g = V.build_preset("alexnet", 4)
+    cm = V.CostModel()
+    w = numeric.he_weights(g, cm, seed=81)
+    images, labels = _batch(g, seed=82)
+    d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+    outs = []
+    for graph in (False, True):
+        s = V.Session(g, d, cm, 4 << 30, record_timeline=True, compress_offload=compress, cuda_graph=graph)
+        for k, v in w.items():
+            s.set_weights(k, v)
+        s.set_batch(images, labels)
+        l0 = V.kernel_launch_count()
+        losses = [s.step(LR) for _ in range(3)] + [s.step(LR / 2) for _ in range(2)]
+        launches = V.kernel_launch_count() - l0
+        stats = s.transfer_stats()
+        assert V.replay_check(s.measured_report(), g, d, 4 << 30) == []
+        outs.append((losses, {k: s.get_weights(k) for k in w}, stats, launches))
+        del s
+    assert outs[0][0] == outs[1][0]
+    for k in w:
+        assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
+    assert outs[0][2] == outs[1][2]
+    assert outs[0][3] == outs[1][3]
