@@ -278,3 +278,197 @@ __global__ void __launch_bounds__(192, 1) tc_conv_halo_kernel(const __grid_const
 }
 
 }  // namespace vdnnk
+
+namespace vdnnk {
+
+// ------------------------------------------------------- halo WGRAD -------
+// dW[co][r][s][ci] = sum_p dY[p][co] * X[p + r*P + s][ci] on the virtual
+// pixel grid (pitch P = W + 2*pad; dY is 0 on the garbage columns x >= Wout,
+// which TMA's out-of-bounds fill provides). One pipeline unit is one virtual
+// output row: B = that dY row (Cout/32 MN-major chunks of P pixel rows), and
+// per (tap row r, 32-channel chunk c) of this CTA's group one TMA box of the
+// padded input row y + r. The M = 128 rows of an MMA are the four shifted
+// views s = 0..3 of that ONE staged box (MN-major chunks LBO = 128 B apart:
+// A[(s, ci)][k] = X[k + s][ci]; tools/halo_mn_probe.cu) -- s = 3 is unused
+// for 3x3, so 96 of 128 rows are useful, but every input row is staged once
+// per (r, c) instead of once per tap (the im2col wgrad stages it 9 times).
+// A CTA owns a group of (r, c) blocks (G x Cout TMEM columns) and a range of
+// rows, and writes its split-K partial; wgrad_reduce_kernel sums them.
+struct HaloWgParams {
+  int N, H, W, C, Cout, kh, kw, pad, P, Kp, Hout, Wout, nck;
+  int G, ngroups, rows_per, nrows, M;
+  int AS, BS;              // ring depths (A: one padded input row per (r, c); B: one dY row)
+  uint32_t a_slot, b_slot; // bytes per slot (1024-aligned)
+  float* part;             // [splits][Cout][M]
+};
+constexpr int kHwMaxAS = 4, kHwMaxBS = 2;
+inline uint32_t halo_wg_a_slot(int Kp) { return ((static_cast<uint32_t>(Kp) + 8) * 128 + 1023u) & ~1023u; }
+inline uint32_t halo_wg_b_slot(int Kp, int bn) { return ((static_cast<uint32_t>(bn / 32) * Kp * 128) + 1023u) & ~1023u; }
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1) tc_wgrad_halo_kernel(const __grid_constant__ HaloWgParams p,
+                                                               const __grid_constant__ CUtensorMap tma_x,
+                                                               const __grid_constant__ CUtensorMap tma_dy) {
+  const int AS = p.AS, BS = p.BS;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bslots = base + AS * p.a_slot;
+  const uint32_t bars = bslots + BS * p.b_slot;
+  auto full_a = [&](int s) { return bars + 8u * s; };
+  auto empty_a = [&](int s) { return bars + 8u * (AS + s); };
+  auto full_b = [&](int s) { return bars + 8u * (2 * AS + s); };
+  auto empty_b = [&](int s) { return bars + 8u * (2 * AS + BS + s); };
+  const uint32_t done_bar = bars + 8u * (2 * AS + 2 * BS);
+  const uint32_t tmem_slot = bars + 8u * (2 * AS + 2 * BS + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int z = blockIdx.x / p.ngroups, grp = blockIdx.x - z * p.ngroups;
+  const int g0 = grp * p.G;
+  const int G = min(p.G, p.kh * p.nck - g0);  // (r, c) blocks of this CTA: index j -> block g0 + j
+  const int row0 = z * p.rows_per;
+  const int row1 = min(row0 + p.rows_per, p.nrows);
+  const int nrows = max(0, row1 - row0);
+  const int ncol = G * BN;
+  int tcols = 32;
+  while (tcols < ncol) tcols <<= 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(full_a(s), 1);
+      mbar_init(empty_a(s), 1);
+    }
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(full_b(s), 1);
+      mbar_init(empty_b(s), 1);
+    }
+    mbar_init(done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // rows the boxes never write: B rows [P, Kp) must be 0 (they meet A rows of
+  // garbage pixels), A rows [P, Kp + 8) must be finite
+  for (int s = 0; s < AS; ++s)
+    for (uint32_t o = p.P * 128 + threadIdx.x * 16; o < p.a_slot; o += blockDim.x * 16)
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + s * p.a_slot + o), "r"(0) : "memory");
+  for (int s = 0; s < BS; ++s)
+    for (int ch = 0; ch < BN / 32; ++ch)
+      for (int o = p.P * 128 + threadIdx.x * 16; o < p.Kp * 128; o += blockDim.x * 16)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(bslots + s * p.b_slot + ch * p.Kp * 128 + o),
+                     "r"(0)
+                     : "memory");
+  fence_proxy_async();
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  if (warp == 5) {
+    // ---------------- TMA producer (one thread, in consumption order) ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_x) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_dy) : "memory");
+      int sa = 0, sb = 0;
+      uint32_t pha = 1, phb = 1;
+      const uint32_t abytes = static_cast<uint32_t>(p.P) * 128, bbytes = (BN / 32) * abytes;
+      for (int row = row0; row < row1; ++row) {
+        const int n = row / p.Hout, y = row - n * p.Hout;
+        mbar_wait(empty_b(sb), phb);
+        mbar_expect_tx(full_b(sb), bbytes);
+        for (int ch = 0; ch < BN / 32; ++ch)
+          tma_load_4d(bslots + sb * p.b_slot + ch * p.Kp * 128, &tma_dy, full_b(sb), ch * 32, 0, y, n);
+        if (++sb == BS) {
+          sb = 0;
+          phb ^= 1;
+        }
+        for (int j = 0; j < G; ++j) {
+          const int blk = g0 + j, r = blk / p.nck, c = blk - r * p.nck;
+          mbar_wait(empty_a(sa), pha);
+          mbar_expect_tx(full_a(sa), abytes);
+          tma_load_4d(base + sa * p.a_slot, &tma_x, full_a(sa), c * 32, -p.pad, y + r - p.pad, n);
+          if (++sa == AS) {
+            sa = 0;
+            pha ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = make_idesc_tf32(BN, true, true);
+    const bool leader = elect_one();
+    const int ksteps = p.Kp / 8;
+    const uint32_t lbo_b = static_cast<uint32_t>(p.Kp) * 128;
+    int sa = 0, sb = 0;
+    uint32_t pha = 0, phb = 0;
+    for (int i = 0; i < nrows; ++i) {
+      mbar_wait(full_b(sb), phb);
+      tc_fence_after();
+      const uint32_t b0 = bslots + sb * p.b_slot;
+      for (int j = 0; j < G; ++j) {
+        mbar_wait(full_a(sa), pha);
+        tc_fence_after();
+        const uint32_t a0 = base + sa * p.a_slot;
+        if (leader) {
+          for (int kk = 0; kk < ksteps; ++kk)
+            tc_mma_tf32(tmem + j * BN, make_sdesc(a0 + kk * 1024, 128, 512, kSw128Base32),
+                        make_sdesc(b0 + kk * 1024, lbo_b, 512, kSw128Base32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(empty_a(sa));
+        }
+        __syncwarp();
+        if (++sa == AS) {
+          sa = 0;
+          pha ^= 1;
+        }
+      }
+      if (leader) tc_commit(empty_b(sb));
+      __syncwarp();
+      if (++sb == BS) {
+        sb = 0;
+        phb ^= 1;
+      }
+    }
+    if (leader) {
+      if (nrows > 0)
+        tc_commit(done_bar);
+      else
+        mbar_arrive(done_bar);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: warp w = shift s, lane = ci ----------------
+    mbar_wait_sleep(done_bar, 0);
+    tc_fence_after();
+    const int s = warp;
+    for (int j = 0; j < G; ++j) {
+      const int blk = g0 + j, r = blk / p.nck, c = blk - r * p.nck;
+      const int m = ((r * p.kw + s) * p.nck + c) * 32 + lane;
+      for (int cg = 0; cg < BN / 32; ++cg) {
+        float v[32];
+        tmem_ld32(tmem + j * BN + cg * 32 + (static_cast<uint32_t>(warp * 32) << 16), v);
+        if (s >= p.kw) continue;  // the fourth shifted view (taps past the kernel)
+        if (nrows <= 0) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = 0.f;
+        }
+        float* dst = p.part + static_cast<int64_t>(z) * p.Cout * p.M;
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (cg * 32 + q < p.Cout) dst[static_cast<int64_t>(cg * 32 + q) * p.M + m] = v[q];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
+  }
+}
+
+}  // namespace vdnnk
