@@ -361,6 +361,11 @@ size_t vdnn_kernel_conv_wgrad_ws_bytes(const vdnn_conv_desc* d);
 vdnn_status vdnn_kernel_conv_fprop_ws(const vdnn_conv_desc* d, const float* w, const float* bias, float* y, float* ws,
                                       size_t ws_bytes, void* stream);
 size_t vdnn_kernel_conv_fprop_ws_bytes(const vdnn_conv_desc* d);
+/* dgrad with a workspace: FC layers (1x1 filter over a 1x1 image) with fewer dX tiles than SMs run the same
+   deterministic split-K (partial slabs + ordered reduce with the ReLU mask and accumulation). */
+vdnn_status vdnn_kernel_conv_dgrad_ws(const vdnn_conv_desc* d, const float* w, const float* dy, int32_t accumulate,
+                                      float* ws, size_t ws_bytes, void* stream);
+size_t vdnn_kernel_conv_dgrad_ws_bytes(const vdnn_conv_desc* d);
 /* Calling-thread switch for the kernel-level conv entry points: 1 = 3xTF32 (fp32-accurate), 0 = TF32. */
 void vdnn_kernel_set_precise(int32_t on);
 /* Calling-thread switch: 1 = TMA producers where eligible (default), 0 = cp.async gathers everywhere. */

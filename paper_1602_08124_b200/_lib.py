@@ -145,6 +145,8 @@ def lib() -> C.CDLL:
         _lib.vdnn_kernel_conv_wgrad_ws_bytes.argtypes = [C.c_void_p]
         _lib.vdnn_kernel_conv_fprop_ws_bytes.restype = C.c_size_t
         _lib.vdnn_kernel_conv_fprop_ws_bytes.argtypes = [C.c_void_p]
+        _lib.vdnn_kernel_conv_dgrad_ws_bytes.restype = C.c_size_t
+        _lib.vdnn_kernel_conv_dgrad_ws_bytes.argtypes = [C.c_void_p]
         _lib.vdnn_kernel_set_precise.restype = None
         _lib.vdnn_kernel_set_precise.argtypes = [C.c_int32]
         _lib.vdnn_kernel_set_tma.restype = None

@@ -98,6 +98,20 @@ size_t vdnn_kernel_conv_fprop_ws_bytes(const vdnn_conv_desc* d) {
   return vdnnk::conv_fprop_ws_bytes(a);
 }
 
+vdnn_status vdnn_kernel_conv_dgrad_ws(const vdnn_conv_desc* d, const float* w, const float* dy, int32_t accumulate,
+                                      float* ws, size_t ws_bytes, void* stream) {
+  vdnnk::ConvArgs a;
+  if (!to_args(d, a)) return fail(VDNN_INVALID_ARGUMENT, "bad conv descriptor");
+  if (a.stride != 1) return fail(VDNN_UNSUPPORTED, "dgrad implemented for stride 1 only");
+  return cuda_status(
+      vdnnk::conv_dgrad(a, w, dy, accumulate != 0, static_cast<cudaStream_t>(stream), ws, ws_bytes), "conv_dgrad");
+}
+size_t vdnn_kernel_conv_dgrad_ws_bytes(const vdnn_conv_desc* d) {
+  vdnnk::ConvArgs a;
+  if (!to_args(d, a)) return 0;
+  return vdnnk::conv_dgrad_ws_bytes(a);
+}
+
 size_t vdnn_kernel_conv_wgrad_ws_bytes(const vdnn_conv_desc* d) {
   vdnnk::ConvArgs a;
   if (!to_args(d, a)) return 0;

@@ -173,7 +173,11 @@ bool make_maps(ConvParams& p, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* tc)
   }
   if (p.kind == kDgrad) {
     if (p.stride != 1 || p.seg[0].dx == nullptr) return false;
-    if (!encode_out(tc, p.seg[0].dx, p.M, p.C)) return false;
+    if (p.epi == kEpiPartial) {
+      if (!encode_out3(tc, p.out, p.splits, p.M, p.C)) return false;
+    } else if (!encode_out(tc, p.seg[0].dx, p.M, p.C)) {
+      return false;
+    }
     if (!encode_im2col(ta, p.dy, p.N, p.Ho, p.Wo, p.Cout, p.kh, 1, p.kh - 1 - p.pad, kBM,
                        CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
@@ -521,7 +525,7 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
     if (p.Ncols <= 64) return launch_bn<64, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
     return launch_bn<128, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
   }
-  if (p.kind == kFprop && p.epi == kEpiPartial) {
+  if ((p.kind == kFprop || p.kind == kDgrad) && p.epi == kEpiPartial) {
     // split-K fprop (FC layers: few output tiles, long K): BN=128 TMA tiles,
     // partial slabs through the 3-D output map
     if (make_maps<128>(p, &ta, &tb, &tc)) return launch_bn<128, kStages, false, true>(p, ta, tb, tc, splits, st);
@@ -769,10 +773,9 @@ cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, flo
   return cudaGetLastError();
 }
 
-cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st) {
-  ConvParams p;
-  if (!build_common(a, p)) return cudaErrorInvalidValue;
-  if (a.stride != 1) return cudaErrorNotSupported;
+namespace {
+bool dgrad_params(const ConvArgs& a, const float* w, const float* dy, bool accumulate, ConvParams& p) {
+  if (!build_common(a, p)) return false;
   p.kind = kDgrad;
   p.epi = accumulate ? kEpiAccum : kEpiStore;
   p.w = w;
@@ -781,7 +784,89 @@ cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool 
   p.Ncols = p.vec_in ? p.nchunk * 32 : p.C;
   p.kblocks = p.vec_out ? a.kh * a.kw * ((a.cout + 31) / 32) : (a.kh * a.kw * a.cout + kBK - 1) / kBK;
   p.kb_per_split = p.kblocks;
-  return launch(p, 1, st);
+  return true;
+}
+
+// Split-K for DGRAD of FC layers (1x1 over a 1x1 image) with fewer BN=128
+// output tiles than SMs: AlexNet FC6 dX is 128 x 9,216 = 72 tiles over a
+// 4,096-long reduction. Partials + ordered reduce (mask, accumulation).
+int dgrad_splits(const ConvParams& p) {
+  if (g_precise || g_no_tma || p.nseg != 1 || !p.vec_in || !p.vec_out || p.kh != 1 || p.kw != 1 || p.H != 1 ||
+      p.W != 1 || p.C % 32 != 0)
+    return 1;
+  static const bool off = std::getenv("VDNN_NO_DGRAD_SPLIT") != nullptr;  // A/B switch
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ncols + 127) / 128);
+  if (off || tiles >= kNumSms || p.kblocks < 64) return 1;
+  return pick_splits(tiles, p.kblocks, 2 * kNumSms, 128, static_cast<int64_t>(p.M) * p.C);
+}
+
+__global__ void dgrad_reduce_kernel(const float* __restrict__ part, int splits, int64_t m, int c,
+                                    const float* __restrict__ mask_x, int accumulate, float* __restrict__ dx) {
+  const int64_t total4 = m * c / 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 s = reinterpret_cast<const float4*>(part)[i];
+    for (int z = 1; z < splits; ++z) {  // fixed order: deterministic
+      const float4 q = reinterpret_cast<const float4*>(part + z * m * c)[i];
+      s.x += q.x;
+      s.y += q.y;
+      s.z += q.z;
+      s.w += q.w;
+    }
+    if (mask_x) {
+      const float4 xv = reinterpret_cast<const float4*>(mask_x)[i];
+      s.x = xv.x > 0.f ? s.x : 0.f;
+      s.y = xv.y > 0.f ? s.y : 0.f;
+      s.z = xv.z > 0.f ? s.z : 0.f;
+      s.w = xv.w > 0.f ? s.w : 0.f;
+    }
+    if (accumulate) {
+      const float4 o = reinterpret_cast<const float4*>(dx)[i];
+      s.x += o.x;
+      s.y += o.y;
+      s.z += o.z;
+      s.w += o.w;
+    }
+    reinterpret_cast<float4*>(dx)[i] = s;
+  }
+}
+}  // namespace
+
+size_t conv_dgrad_ws_bytes(const ConvArgs& a) {
+  ConvParams p;
+  if (a.stride != 1 || !dgrad_params(a, nullptr, nullptr, false, p)) return 0;
+  const int s = dgrad_splits(p);
+  return s > 1 ? static_cast<size_t>(s) * p.M * p.C * sizeof(float) : 0;
+}
+
+cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st,
+                       float* ws, size_t ws_bytes) {
+  ConvParams p;
+  if (!dgrad_params(a, w, dy, accumulate, p)) return cudaErrorInvalidValue;
+  if (a.stride != 1) return cudaErrorNotSupported;
+  int splits = (ws && p.seg[0].dx) ? dgrad_splits(p) : 1;
+  const size_t per = static_cast<size_t>(p.M) * p.C * sizeof(float);
+  if (splits > 1) splits = static_cast<int>(std::min<size_t>(splits, ws_bytes / per));
+  if (splits > 1) {
+    p.kb_per_split = (p.kblocks + splits - 1) / splits;
+    splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;
+  }
+  if (splits <= 1) {
+    p.kb_per_split = p.kblocks;
+    return launch(p, 1, st);
+  }
+  const bool accum = p.epi == kEpiAccum;
+  p.epi = kEpiPartial;
+  p.out = ws;
+  p.splits = splits;
+  cudaError_t e = launch(p, splits, st);
+  if (e != cudaSuccess) return e;
+  const int64_t total4 = static_cast<int64_t>(p.M) * p.C / 4;
+  const int blocks = static_cast<int>(std::min<int64_t>((total4 + 255) / 256, 4 * kNumSms));
+  dgrad_reduce_kernel<<<blocks, 256, 0, st>>>(ws, splits, p.M, p.C, p.seg[0].mask ? p.seg[0].x : nullptr,
+                                              accum ? 1 : 0, p.seg[0].dx);
+  count_launch();
+  return cudaGetLastError();
 }
 
 namespace {

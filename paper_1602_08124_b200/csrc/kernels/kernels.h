@@ -41,7 +41,11 @@ void set_tma(bool on);
 cudaError_t conv_fprop(const ConvArgs& a, const float* w, const float* bias, float* y, bool accumulate,
                        cudaStream_t st, float* ws = nullptr, size_t ws_bytes = 0);
 size_t conv_fprop_ws_bytes(const ConvArgs& a);
-cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st);
+// `ws` (optional, conv_dgrad_ws_bytes(a) bytes): deterministic split-K for FC
+// layers with fewer output tiles than SMs.
+cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st,
+                       float* ws = nullptr, size_t ws_bytes = 0);
+size_t conv_dgrad_ws_bytes(const ConvArgs& a);
 // Weight gradient. If dw_out is null: fused SGD  w_mut -= lr * dW.
 // Otherwise dW is written to dw_out (KRSC layout) and w_mut is untouched.
 // `ws` holds split-K partials; pass conv_wgrad_ws_bytes(a) bytes (or less:

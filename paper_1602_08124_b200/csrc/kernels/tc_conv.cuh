@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTo
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
         }
-        if (p.kind == kDgrad && p.seg[0].mask && m < p.M && nb < p.C) {
+        if (p.kind == kDgrad && p.seg[0].mask && !partial && m < p.M && nb < p.C) {
           // fused ReLU backward: the ReLU's output is this conv's input x
           const float* xr = p.seg[0].x + static_cast<int64_t>(m) * p.C + nb;
           if (nb + 32 <= p.C) {

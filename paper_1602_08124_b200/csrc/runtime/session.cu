@@ -131,6 +131,7 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
     const Node& l = g_.at(s.layer);
     if (l.kind != Kind::Conv && l.kind != Kind::Fc) continue;
     need = std::max(need, vdnnk::conv_wgrad_ws_bytes(conv_args(s.layer, s.in_off, nullptr)));
+    need = std::max(need, vdnnk::conv_dgrad_ws_bytes(conv_args(s.layer, s.in_off, nullptr)));
   }
   for (const FwdStep& s : fwd_) {  // split-K FC fprop partials share the buffer
     const Node& l = g_.at(s.layer);
@@ -659,7 +660,7 @@ void Session::run_bwd(const BwdStep& s, float lr) {
       if (!s.plane_off.empty()) {
         vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off);
         for (int i = 0; i < a.nseg; ++i) a.mask_in[i] = s.mask_plane[static_cast<size_t>(i)];
-        check(vdnnk::conv_dgrad(a, F(s.w_off), dy, s.accumulate, cs_), "conv_dgrad");
+        check(vdnnk::conv_dgrad(a, F(s.w_off), dy, s.accumulate, cs_, splitk_, splitk_bytes_), "conv_dgrad");
       }
       const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
       // split-K partials live in a fixed non-pool scratch so the reduction

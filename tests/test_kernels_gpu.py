@@ -276,6 +276,44 @@ def test_fc_fprop_split_k_with_bias():
     _close(y1, ref)
 
 
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_fc_dgrad_split_k(accumulate):
+    """AlexNet FC6 dX at batch 128 (1 x 72 tiles over K = 4,096): split-K
+    partial slabs + ordered reduce, plain and accumulating (branch-join)
+    mode, against the unsplit kernel and a float64 reference; deterministic
+    across calls. (The fused ReLU mask is a session-level flag: covered by
+    the VGG-16 session parity test, whose FC7 dX splits.)"""
+    dev = _dev()
+    n, k, o = 128, 9216, 4096
+    g = torch.Generator(device=dev).manual_seed(11)
+    x = torch.randn(n, 1, 1, k, device=dev, generator=g)
+    wt = torch.randn(o, 1, 1, k, device=dev, generator=g) * (2.0 / k) ** 0.5
+    dy = torch.randn(n, 1, 1, o, device=dev, generator=g)
+    base = torch.randn(n, 1, 1, k, device=dev, generator=g)
+    d = _desc(n, 1, 1, [x], [k], o, 1, 1, 0)
+    ws_bytes = L.lib().vdnn_kernel_conv_dgrad_ws_bytes(C.byref(d))
+    assert ws_bytes > 0
+    ws = torch.empty(ws_bytes // 4, device=dev)
+    outs = []
+    for use_ws in (True, True, False):
+        dx = base.clone() if accumulate else torch.full_like(x, float("nan"))
+        dd = _desc(n, 1, 1, [x], [k], o, 1, 1, 0, [dx])
+        if use_ws:
+            L.call("vdnn_kernel_conv_dgrad_ws", C.byref(dd), C.c_void_p(wt.data_ptr()), C.c_void_p(dy.data_ptr()),
+                   1 if accumulate else 0, C.c_void_p(ws.data_ptr()), C.c_size_t(ws_bytes), None)
+        else:
+            L.call("vdnn_kernel_conv_dgrad", C.byref(dd), C.c_void_p(wt.data_ptr()), C.c_void_p(dy.data_ptr()),
+                   1 if accumulate else 0, None)
+        outs.append(dx)
+    torch.cuda.synchronize()
+    ref = (dy.double().reshape(n, o) @ wt.double().reshape(o, k)).reshape(n, 1, 1, k)
+    if accumulate:
+        ref = ref + base.double()
+    assert torch.equal(outs[0], outs[1])
+    _close(outs[0], ref)
+    _close(outs[2], ref)
+
+
 # Shapes large enough to select the production tile variants: tall (BM=256)
 # 128/64-wide tiles, wide (BN=256) tall tiles, 64-pixel wgrad stages, split-K
 # over hundreds of CTAs. Reference: torch float64 on the GPU (same op).
