@@ -11,6 +11,7 @@
 #include "tc_conv_persist.cuh"
 #include "tc_conv_halo.cuh"
 #include "tc_conv_pair.cuh"
+#include "tc_conv_halo_pair.cuh"
 #include "tma_maps.h"
 
 namespace vdnnk {
@@ -408,6 +409,63 @@ cudaError_t launch_halo(HaloParams& h, const ConvParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Halo kernel on a CTA pair (tc_conv_halo_pair.cuh): same maps, B boxes of
+// BN/2 rows per CTA. VDNN_HALO_PAIR=0 selects the single-CTA halo kernel.
+bool halo_pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VDNN_HALO_PAIR");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <int BN, int AS, int BS, int KW, bool RESB = false>
+cudaError_t launch_halo_pair(HaloParams& h, const ConvParams& p, cudaStream_t st) {
+  using L = HaloPairSmem<BN, AS, BS>;
+  const int smem = RESB ? L::total(h.nck * h.kh * KW) : L::kTotal;
+  if (smem > 227 * 1024 || (RESB && h.Cout != BN)) return cudaErrorNotSupported;
+  alignas(64) CUtensorMap ta, tb;
+  std::memset(&ta, 0, sizeof(ta));
+  std::memset(&tb, 0, sizeof(tb));
+  const float* src = p.kind == kFprop ? p.seg[0].x : p.dy;
+  {
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(h.Cin), static_cast<cuuint64_t>(h.Win),
+                                static_cast<cuuint64_t>(h.Hin), static_cast<cuuint64_t>(h.N)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(h.Cin) * 4, static_cast<cuuint64_t>(h.Win) * h.Cin * 4,
+                                   static_cast<cuuint64_t>(h.Hin) * h.Win * h.Cin * 4};
+    const cuuint32_t box[4] = {32, static_cast<cuuint32_t>(h.P), static_cast<cuuint32_t>(h.TH), 1};
+    if (!encode_tiled(&ta, src, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorNotSupported;
+  }
+  if (p.kind == kFprop) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.KK), static_cast<cuuint64_t>(p.Cout)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.KK) * 4};
+    const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(BN / 2)};
+    if (!encode_tiled(&tb, p.w, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorNotSupported;
+  } else {
+    const int taps = p.kh * p.kw;
+    const cuuint64_t d4[4] = {32, static_cast<cuuint64_t>(p.Cout), static_cast<cuuint64_t>(p.C / 32),
+                              static_cast<cuuint64_t>(taps)};
+    const cuuint64_t s4[3] = {static_cast<cuuint64_t>(taps) * p.C * 4, 128, static_cast<cuuint64_t>(p.C) * 4};
+    const cuuint32_t b4[4] = {32, 32, static_cast<cuuint32_t>(BN / 64), 1};
+    if (!encode_tiled(&tb, p.w, 4, d4, s4, b4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorNotSupported;
+  }
+  if (h.Cout % BN != 0) return cudaErrorNotSupported;  // each CTA stages BN/2 whole B rows
+  h.ntn = h.Cout / BN;
+  const int ntiles = h.N * ((h.tiles_h + 1) / 2) * h.ntn;
+  h.ntiles = ntiles;
+  static int attr_smem = 0;
+  if (smem > attr_smem) {
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_halo_pair_kernel<BN, AS, BS, KW, RESB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_smem = smem;
+  }
+  const int grid = 2 * std::min(ntiles, kNumSms / 2);
+  tc_conv_halo_pair_kernel<BN, AS, BS, KW, RESB><<<grid, 192, smem, st>>>(h, ta, tb);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // CTA-pair kernel (tc_conv_pair.cuh) for FPROP / DGRAD with >= 256 output
 // columns and at least two tiles of 256 x 256 per pair. VDNN_PAIR=0 disables.
 // 64-column wgrad: 4-stage rings (2 CTAs / SM still fit) -- the short
@@ -510,6 +568,15 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
     HaloParams h;
     if (halo_params(p, h)) {
       cudaError_t e = cudaErrorNotSupported;
+      static const bool resb = [] {
+        const char* e = std::getenv("VDNN_HALO_RESB");
+        return !e || std::atoi(e) != 0;
+      }();
+      if (h.kw == 3 && halo_pair_enabled() && resb && h.Cout == 64)  // filter half resident (<= 2 chunks)
+        e = launch_halo_pair<64, 4, 1, 3, true>(h, p, st);
+      if (e == cudaErrorNotSupported && h.kw == 3 && halo_pair_enabled())
+        e = h.Cout <= 64 ? launch_halo_pair<64, 5, 8, 3>(h, p, st) : launch_halo_pair<128, 4, 7, 3>(h, p, st);
+      if (e != cudaErrorNotSupported) return e;
       if (h.kw == 3)
         e = p.Ncols <= 64 ? launch_halo<64, 4, 8, 3>(h, p, st) : launch_halo<128, 3, 7, 3>(h, p, st);
       else if (h.kw == 5)

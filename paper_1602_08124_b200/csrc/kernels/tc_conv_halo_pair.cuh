@@ -1,0 +1,295 @@
+// CTA-pair (cta_group::2) variant of the halo-reuse FPROP / DGRAD kernel
+// (tc_conv_halo.cuh; included by conv.cu after tc_conv_pair.cuh).
+//
+// Why: the halo kernel's N = 64 / 128 MMAs are bound by the tensor core's
+// shared-memory operand reads (ncu: TC wavefronts 78-83% busy, tensor pipe
+// 48-56%): per M128 x N x K8 MMA a single SM reads 4 KB of A and N x 32 B of
+// B. On a CTA pair each SM keeps its own 128 A rows but only HALF of B (the
+// pair exchanges the halves), so per SM and MMA of the same FLOPs it reads
+// 4 KB + N x 16 B: 6 -> 5 KB at N = 64, 8 -> 6 KB at N = 128.
+//
+//   cluster (2,1,1); rank 0 = leader. Pair tile = (image n, row-tile pair
+//   thp, column block tn): CTA rank r owns output rows th = 2*thp + r (TH rows
+//   of the virtual pitch-P grid, two M=256 pair MMAs per tap: h = 0, 1) and
+//   stages its own padded input box plus B rows n0 + r*BN/2. A rank-1 tile past
+//   the last row tile computes on TMA zero fill and stores nothing.
+//   warps 0-3 : epilogue of this CTA's 256 virtual rows (as tc_conv_halo)
+//   warp 4    : TMEM alloc (cta_group::2); in the leader the MMA issuer
+//   warp 5    : TMA producer; both CTAs' loads complete on the LEADER's full
+//               barriers (.cta_group::2 TMA), the leader's single arrive
+//               expects both CTAs' bytes; empty / tfull barriers are
+//               multicast commits; tempty counts 256 arrivals in the leader.
+// RESB: when one CTA's half of the whole filter fits next to the A ring
+// (64 -> 64 channels: 9 taps x 2 chunks x 4 KB = 72 KB), B is loaded once per
+// CTA and stays resident: the per-tile B stream (as many L2 -> SM bytes as
+// the A boxes at 64 columns) disappears.
+#pragma once
+
+namespace vdnnk {
+
+template <int BN, int AS, int BS>
+struct HaloPairSmem {
+  static constexpr int kASlot = 33 * 1024;       // >= 258 rows x 128 B
+  static constexpr int kBSlot = (BN / 2) * 128;  // this CTA's half of B
+  static constexpr int kTotal = AS * kASlot + BS * kBSlot + 1024 + 256;
+  static int total(int nbslots) { return AS * kASlot + nbslots * kBSlot + 1024 + 256; }
+  static constexpr int kAccCols = 2 * BN;  // h = 0, 1
+  static_assert(2 * kAccCols <= 512, "two accumulator sets must fit TMEM");
+};
+
+template <int BN, int AS, int BS, int KW, bool RESB = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    tc_conv_halo_pair_kernel(const __grid_constant__ HaloParams p, const __grid_constant__ CUtensorMap tma_a,
+                             const __grid_constant__ CUtensorMap tma_b) {
+  using L = HaloPairSmem<BN, AS, BS>;
+  constexpr int kTmemCols = 2 * L::kAccCols;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bslots = base + AS * L::kASlot;
+  const int nbslots = RESB ? p.nck * p.kh * KW : BS;
+  const uint32_t bars = bslots + static_cast<uint32_t>(nbslots) * L::kBSlot;
+  auto full_a = [&](int s) { return bars + 8u * s; };
+  auto empty_a = [&](int s) { return bars + 8u * (AS + s); };
+  auto full_b = [&](int s) { return bars + 8u * (2 * AS + s); };
+  auto empty_b = [&](int s) { return bars + 8u * (2 * AS + BS + s); };
+  auto tfull = [&](int a) { return bars + 8u * (2 * AS + 2 * BS + a); };
+  auto tempty = [&](int a) { return bars + 8u * (2 * AS + 2 * BS + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * AS + 2 * BS + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = static_cast<int>(blockIdx.x >> 1), npairs = static_cast<int>(gridDim.x >> 1);
+  const int tiles_hp = (p.tiles_h + 1) >> 1;
+  const int ntiles = p.N * tiles_hp * p.ntn;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(full_a(s), 1);
+      mbar_init(empty_a(s), 1);
+    }
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(full_b(s), 1);
+      mbar_init(empty_b(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  const uint32_t abytes = static_cast<uint32_t>(p.TH * p.P * 128);
+  if (warp == 5) {
+    // ---------------- TMA producer (this CTA's rows and B half) ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+      int sa = 0, sb = 0;
+      uint32_t pha = 1, phb = 1;  // the first pass over each ring does not wait
+      if constexpr (RESB) {  // the whole filter half, once, on full_b(0)
+        const int nb = static_cast<int>(rank) * (BN / 2);
+        if (rank == 0) mbar_expect_tx(full_b(0), 2u * nbslots * L::kBSlot);
+        const uint32_t lb = map_to_rank(full_b(0), 0);
+        for (int c = 0; c < p.nck; ++c)
+          for (int r = 0; r < p.kh; ++r)
+            for (int s = 0; s < KW; ++s) {
+              const uint32_t dst = bslots + ((c * p.kh + r) * KW + s) * L::kBSlot;
+              if (p.kind == kFprop) {
+                tma_load_2d_pair(dst, &tma_b, lb, (r * KW + s) * p.Cin + c * 32, nb);
+              } else {
+                const int ftap = (p.kh - 1 - r) * KW + (KW - 1 - s);
+                tma_load_4d_pair(dst, &tma_b, lb, 0, c * 32, nb >> 5, ftap);
+              }
+            }
+      }
+      for (int tile = pair; tile < ntiles; tile += npairs) {
+        const int tn = tile % p.ntn, t2 = tile / p.ntn;
+        const int thp = t2 % tiles_hp, n = t2 / tiles_hp;
+        const int y0 = (2 * thp + static_cast<int>(rank)) * p.TH;
+        const int nb = tn * BN + static_cast<int>(rank) * (BN / 2);
+        for (int c = 0; c < p.nck; ++c) {
+          for (int r = 0; r < p.kh; ++r) {
+            mbar_wait(empty_a(sa), pha);
+            // only the leader arrives (expecting both CTAs' bytes); see tc_conv_pair.cuh
+            if (rank == 0) mbar_expect_tx(full_a(sa), 2 * abytes);
+            tma_load_4d_pair(base + sa * L::kASlot, &tma_a, map_to_rank(full_a(sa), 0), c * 32, -p.pad,
+                             y0 + r - p.pad, n);
+            if (++sa == AS) {
+              sa = 0;
+              pha ^= 1;
+            }
+            if constexpr (!RESB) {
+#pragma unroll
+              for (int s = 0; s < KW; ++s) {
+                mbar_wait(empty_b(sb), phb);
+                if (rank == 0) mbar_expect_tx(full_b(sb), 2 * L::kBSlot);
+                const uint32_t lb = map_to_rank(full_b(sb), 0);
+                if (p.kind == kFprop) {
+                  tma_load_2d_pair(bslots + sb * L::kBSlot, &tma_b, lb, (r * KW + s) * p.Cin + c * 32, nb);
+                } else {
+                  const int ftap = (p.kh - 1 - r) * KW + (KW - 1 - s);
+                  tma_load_4d_pair(bslots + sb * L::kBSlot, &tma_b, lb, 0, c * 32, nb >> 5, ftap);
+                }
+                if (++sb == BS) {
+                  sb = 0;
+                  phb ^= 1;
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    // ---------------- MMA issuer (leader CTA) ----------------
+    if (rank == 0) {
+      const bool leader = elect_one();
+      const bool b_mn = p.kind != kFprop;
+      const uint32_t idesc = (make_idesc_tf32(BN, false, b_mn) & ~(0x1Fu << 24)) | ((256u >> 4) << 24);
+      const uint64_t adesc0 = make_sdesc(base, 16, 1024, kSw128);
+      const uint64_t bdesc0 =
+          b_mn ? make_sdesc(bslots, 4096, 512, kSw128Base32) : make_sdesc(bslots, 16, 1024, kSw128);
+      const uint32_t kstep_b = b_mn ? (1024 >> 4) : (32 >> 4);
+      int sa = 0, sb = 0, lt = 0;
+      uint32_t pha = 0, phb = 0;
+      const int nstage = p.nck * p.kh;
+      if constexpr (RESB) mbar_wait(full_b(0), 0);
+      for (int tile = pair; tile < ntiles; tile += npairs, ++lt) {
+        const int acc = lt & 1;
+        if (lt >= 2) mbar_wait(tempty(acc), ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem + acc * L::kAccCols;
+        uint32_t first = 1;
+        for (int st = 0; st < nstage; ++st) {
+          mbar_wait(full_a(sa), pha);
+          tc_fence_after();
+          const uint64_t ad = adesc0 + static_cast<uint64_t>((sa * L::kASlot) >> 4);
+#pragma unroll
+          for (int s = 0; s < KW; ++s) {
+            if constexpr (RESB) {
+              sb = st * KW + s;
+            } else {
+              mbar_wait(full_b(sb), phb);
+            }
+            tc_fence_after();
+            const uint64_t bd = bdesc0 + static_cast<uint64_t>((sb * L::kBSlot) >> 4);
+            if (leader) {
+#pragma unroll
+              for (int kk = 0; kk < kBK / 8; ++kk) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  tc_mma_tf32_pair(d0 + h * BN, ad + static_cast<uint64_t>(((h * kBM + s) * 128 + kk * 32) >> 4),
+                                   bd + static_cast<uint64_t>(kk * kstep_b), idesc,
+                                   (first && kk == 0) ? 0u : 1u);
+              }
+              if constexpr (!RESB) tc_commit_pair(empty_b(sb));
+            }
+            __syncwarp();
+            first = 0;
+            if (RESB) continue;
+            if (++sb == BS) {
+              sb = 0;
+              phb ^= 1;
+            }
+          }
+          if (leader) tc_commit_pair(empty_a(sa));
+          __syncwarp();
+          if (++sa == AS) {
+            sa = 0;
+            pha ^= 1;
+          }
+        }
+        if (leader) tc_commit_pair(tfull(acc));
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue (this CTA's 256 virtual rows) ----------------
+    const int row = warp * 32 + lane;
+    const uint32_t ltempty0 = map_to_rank(tempty(0), 0), ltempty1 = map_to_rank(tempty(1), 0);
+    int lt = 0;
+    for (int tile = pair; tile < ntiles; tile += npairs, ++lt) {
+      const int acc = lt & 1;
+      const int tn = tile % p.ntn, t2 = tile / p.ntn;
+      const int thp = t2 % tiles_hp, n = t2 / tiles_hp;
+      const int y0 = (2 * thp + static_cast<int>(rank)) * p.TH, n0 = tn * BN;
+      mbar_wait_sleep(tfull(acc), (lt >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int v = h * kBM + row;
+        const int yl = v / p.P, x = v - yl * p.P, y = y0 + yl;
+        const bool valid = yl < p.TH && x < p.Wout && y < p.Hout;
+        const int64_t pix = (static_cast<int64_t>(n) * p.Hout + y) * p.Wout + x;
+        const uint32_t taddr = tmem + acc * L::kAccCols + h * BN + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+        for (int cg = 0; cg < BN / 32; ++cg) {
+          float vals[32];
+          tmem_ld32(taddr + cg * 32, vals);
+          if (h == 1 && cg == BN / 32 - 1) {
+            // last TMEM read of this accumulator set: release it to the leader's MMA warp
+            tc_fence_before();
+            mbar_arrive_cluster(acc ? ltempty1 : ltempty0);
+          }
+          const int nb = n0 + cg * 32;
+          if (!valid || nb >= p.Cout) continue;
+          if (p.relu) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) vals[i] = fmaxf(vals[i], 0.f);
+          }
+          if (p.mask_x) {
+            const float4* xr = reinterpret_cast<const float4*>(p.mask_x + pix * p.Cout + nb);
+            float4 xv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xv[i] = __ldg(xr + i);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              vals[4 * i] = xv[i].x > 0.f ? vals[4 * i] : 0.f;
+              vals[4 * i + 1] = xv[i].y > 0.f ? vals[4 * i + 1] : 0.f;
+              vals[4 * i + 2] = xv[i].z > 0.f ? vals[4 * i + 2] : 0.f;
+              vals[4 * i + 3] = xv[i].w > 0.f ? vals[4 * i + 3] : 0.f;
+            }
+          }
+          float4* dst = reinterpret_cast<float4*>(p.out + pix * p.Cout + nb);
+          if (p.accum) {
+            float4 a[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = dst[i];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              vals[4 * i] += a[i].x;
+              vals[4 * i + 1] += a[i].y;
+              vals[4 * i + 2] += a[i].z;
+              vals[4 * i + 3] += a[i].w;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(vals[4 * i], vals[4 * i + 1], vals[4 * i + 2], vals[4 * i + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's MMAs / barrier traffic into this CTA are over
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+}  // namespace vdnnk

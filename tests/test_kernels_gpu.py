@@ -325,6 +325,11 @@ LARGE = [
     (2, 224, 224, 64, 64),
     (4, 112, 112, 128, 128),
     (8, 28, 28, 512, 512),
+    # halo on a CTA pair (tc_conv_halo_pair.cuh) with an odd number of row
+    # tiles (P = 26, TH = 9: 3 per image), so a rank-1 CTA computes past the
+    # last row tile and must store nothing
+    (3, 24, 24, 128, 128),
+    (3, 24, 24, 64, 64),
     # CTA-pair (cta_group::2) fprop/dgrad: 256 x 256 tiles over >= 148 tiles,
     # and a 384-column layer whose second tile leaves the peer's B half empty
     (32, 28, 28, 512, 512),
@@ -377,6 +382,48 @@ def test_conv_production_tiles(shape):
     gref = wr.grad.permute(0, 2, 3, 1)
     diff = (w2.double() - (wt.double() - lr * gref)).abs().max().item()
     assert diff < TF32_TOL * lr * gref.abs().max().item() + 2e-7 * wt.abs().max().item(), diff
+
+
+_HALO_SNIPPET = r"""
+import ctypes as C, sys, torch
+sys.path.insert(0, {root!r})
+from paper_1602_08124_b200 import _lib as L
+n, h, c, cout = {shape!r}
+g = torch.Generator(device="cuda").manual_seed(3)
+x = torch.randn(n, h, h, c, device="cuda", generator=g)
+wt = torch.randn(cout, 3, 3, c, device="cuda", generator=g) * (2.0 / (9 * c)) ** 0.5
+dy = torch.randn(n, h, h, cout, device="cuda", generator=g)
+y = torch.empty(n, h, h, cout, device="cuda")
+dx = torch.empty_like(x)
+d = L.ConvDesc(); d.n, d.h, d.w, d.nseg = n, h, h, 1
+d.x[0] = x.data_ptr(); d.dx[0] = dx.data_ptr(); d.c[0] = c
+d.cout, d.kh, d.kw, d.stride, d.pad = cout, 3, 3, 1, 1
+L.call("vdnn_kernel_conv_fprop", C.byref(d), C.c_void_p(wt.data_ptr()), None, C.c_void_p(y.data_ptr()), None)
+L.call("vdnn_kernel_conv_dgrad", C.byref(d), C.c_void_p(wt.data_ptr()), C.c_void_p(dy.data_ptr()), 0, None)
+torch.cuda.synchronize()
+torch.save({{"y": y.cpu(), "dx": dx.cpu()}}, {out!r})
+"""
+
+
+@pytest.mark.parametrize("shape", [(2, 224, 64, 64), (3, 24, 128, 128), (4, 56, 128, 64)])
+def test_halo_pair_bit_identical_to_single_cta(shape, tmp_path):
+    """The CTA-pair halo kernel accumulates every output in the same K order
+    as the single-CTA halo kernel: fprop and dgrad outputs are bit-identical
+    (VDNN_HALO_PAIR=0 selects the single-CTA kernel in a child process)."""
+    import os
+    import subprocess
+    import sys
+    _dev()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        out = str(tmp_path / f"halo{flag}.pt")
+        env = dict(os.environ, VDNN_HALO_PAIR=flag)
+        subprocess.run([sys.executable, "-c", _HALO_SNIPPET.format(root=root, shape=shape, out=out)], env=env,
+                       check=True, timeout=300)
+        outs.append(torch.load(out))
+    assert torch.equal(outs[0]["y"], outs[1]["y"])
+    assert torch.equal(outs[0]["dx"], outs[1]["dx"])
 
 
 @pytest.mark.parametrize("n,h,cout", [(16, 227, 64), (8, 231, 96)])

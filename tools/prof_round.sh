@@ -2,13 +2,14 @@
 # the other BASELINE configs, launch list of one dyn step with DRAM bytes,
 # per-layer times, and full ncu captures of the top conv kernels.
 set -x
-timeout 600 python bench.py > gpurun_out/bench_r01s2.json 2> gpurun_out/bench_r01s2.err
+LABEL=${LABEL:-r01s3}
+timeout 600 python bench.py > gpurun_out/bench_${LABEL}.json 2> gpurun_out/bench_${LABEL}.err
 for net in alexnet overfeat inception_toy; do
   timeout 300 python bench.py --net $net --batch 128 --policies dyn,all,conv,none --no-cpu-baseline > gpurun_out/bench_$net.json 2> gpurun_out/bench_$net.err
 done
 timeout 900 python bench.py --extra 400 --batch 32 --policies dyn,none --steps 2 --no-cpu-baseline > gpurun_out/bench_vgg416.json 2> gpurun_out/bench_vgg416.err
 python tools/prof_layers.py vgg16 256 none > gpurun_out/layers_none.txt 2>&1
 python tools/prof_layers.py alexnet 128 none > gpurun_out/layers_alexnet.txt 2>&1
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r01s2_launches_dyn.csv python bench.py --policies dyn --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"tc_conv_pair|tc_wgrad_pair|tc_conv_halo" --launch-skip 0 --launch-count 3 -o gpurun_out/r01s2_full python tools/one_step.py vgg16 256 none > gpurun_out/ncu_full.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/${LABEL}_launches_dyn.csv python bench.py --policies dyn --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"tc_conv_pair|tc_wgrad_pair|tc_conv_halo|tc_wgrad_halo|c3tc" --launch-skip 0 --launch-count 7 -o gpurun_out/${LABEL}_full python tools/one_step.py vgg16 256 none > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
