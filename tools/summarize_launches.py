@@ -39,9 +39,10 @@ def main():
     per = int(sys.argv[sys.argv.index("--per-step") + 1]) if "--per-step" in sys.argv else None
     ks = load(path)
     # steps start with the first layer's fprop; take the last complete step
-    # before the tf32 probe (the probe runs after the timed policies)
+    # (bench.py runs the tf32 probe before the policies: drop it and
+    # everything before it)
     probe = [i for i, k in enumerate(ks) if "tf32_peak" in k["name"]]
-    ks = ks[:probe[0]] if probe else ks
+    ks = ks[probe[-1] + 1:] if probe else ks
     first = sys.argv[sys.argv.index("--first") + 1] if "--first" in sys.argv else "c3tc_fprop"
     starts = [i for i, k in enumerate(ks) if first in k["name"]]
     step = ks[starts[-2]:starts[-1]] if len(starts) >= 2 else ks[starts[-1]:]
@@ -62,7 +63,7 @@ def main():
     if "--traffic-json" in sys.argv:
         # DRAM bytes per conv-engine launch (bench.py's roofline "traffic")
         import json
-        conv = [k for k in step if "tc_conv" in k["name"] or "c3tc" in k["name"]]
+        conv = [k for k in step if k["name"].startswith("void tc_") or "c3tc" in k["name"]]
         byt = sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0) for k in conv)
         out = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                          "--clock-control none, python bench.py --policies dyn --steps 1 --warmup 3 (last step): "
