@@ -193,7 +193,9 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     # "<policy>z": the same plan with zero-value-compressed offload/prefetch;
     # "<policy>p": the same plan offloading into the ring neighbour's spare
     # HBM over NVLink (data parallel only: a peer GPU is the offload target)
-    compress = policy.endswith("z")
+    # "<policy>t": compressed, and maps read in backward only by TF32
+    # contractions / ReLU masks travel TF32-exact (bit-identical step)
+    compress = "tf32" if policy.endswith("t") else policy.endswith("z")
     peer_target = policy.endswith("p")
     if compress or peer_target:
         policy = policy[:-1]
@@ -270,8 +272,9 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     pre_ms = sum((e.end - e.start) for e in m.events if e.kind == V.EventKind.Prefetch) * 1e-6
     free, total = torch.cuda.mem_get_info(device)
     res = {
-        "policy": policy + ("z" if compress else "") + ("p" if peer_target else ""),
-        "label": d.label + (" +zvc" if compress else "") + (" ->peer HBM" if peer_target else ""),
+        "policy": policy + ({"tf32": "t", True: "z"}.get(compress, "")) + ("p" if peer_target else ""),
+        "label": d.label + ({"tf32": " +zvc/tf32-exact", True: " +zvc"}.get(compress, ""))
+                 + (" ->peer HBM" if peer_target else ""),
         "verdict": "PASS", "capacity_bytes": cap,
         "images_per_s": round(imgs, 2), "ms_per_step": round(ms, 3), "loss": loss,
         "peak_pool_bytes": plan.max_mem_bytes, "arena_bytes": s.arena_info()["arena_bytes"],
@@ -411,7 +414,8 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--capacity", type=int, default=GIB12)
     ap.add_argument("--policies", default=None,
-                    help="dyn/all/conv/none; a trailing z = same plan with compressed offload, a trailing p = "
+                    help="dyn/all/conv/none; a trailing z = same plan with compressed offload, t = compressed with "
+                         "TF32-exact values where only TF32 contractions read the map, a trailing p = "
                          "offload into a peer GPU's HBM (N > 1). Default: dyn,dynz,all,conv,none (+ dynp at N > 1)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--precise", action="store_true", help="3xTF32 fp32-accurate contractions")
@@ -448,7 +452,7 @@ def main():
     tf32_peak, peak_note = measured_tf32_peak(peaks, peaks_src)
 
     if args.policies is None:
-        args.policies = "dyn,dynz,all,conv,none" if world == 1 else "dyn,dynp,dynz,all,conv,none"
+        args.policies = "dyn,dynz,dynt,all,conv,none" if world == 1 else "dyn,dynp,dynz,all,conv,none"
     results = {}
     for p in [x for x in args.policies.split(",") if x]:
         results[p] = run_policy(p, args, device, world, peaks, want_e2e=(p == "dyn"), sampler_cls=ClockSampler)
@@ -497,6 +501,14 @@ def main():
         z = results["dynz"]
         line["compressed_offload"] = {
             "policy": "vDNN_dyn, same plan, zero-value-compressed offload/prefetch (lossless, bit-identical)",
+            "images_per_s": z["images_per_s"], "ms_per_step": z["ms_per_step"], "wire_ratio": z.get("wire_ratio"),
+            "speedup_vs_copy_engines": round(z["images_per_s"] / head["images_per_s"], 3)
+            if head.get("images_per_s") else None}
+    if "dynt" in results and results["dynt"].get("images_per_s"):
+        z = results["dynt"]
+        line["tf32_exact_offload"] = {
+            "policy": "vDNN_dyn, same plan, compressed offload/prefetch; maps read in backward only by TF32 "
+                      "contractions and ReLU masks travel TF32-exact (bit-identical training step)",
             "images_per_s": z["images_per_s"], "ms_per_step": z["ms_per_step"], "wire_ratio": z.get("wire_ratio"),
             "speedup_vs_copy_engines": round(z["images_per_s"] / head["images_per_s"], 3)
             if head.get("images_per_s") else None}

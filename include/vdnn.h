@@ -256,7 +256,9 @@ typedef struct vdnn_session_options {
   int32_t record_timeline;   /* 1: record CUDA events per op for a measured report */
   int32_t host_arena;        /* 1: pinned host arena for offloads (required when the plan offloads) */
   int32_t precise_fp32;      /* 1: conv/FC contractions as 3xTF32 (fp32-accurate); 0: TF32 */
-  int32_t compress_offload;  /* 1: offload/prefetch through the SMs in lossless zero-value-compressed form */
+  int32_t compress_offload;  /* 1: offload/prefetch through the SMs in lossless zero-value-compressed form;
+                                2: as 1, and maps read in backward only by TF32 contractions and ReLU masks
+                                travel TF32-exact (bit-identical training step; not with precise_fp32) */
   int32_t offload_target;    /* 0: pinned host arena (PCIe); 1: a device buffer set with
                                 vdnn_session_set_offload_buffer / _spill_attach (e.g. a peer GPU's HBM) */
   int32_t cuda_graph;        /* 1: replay each step as one CUDA graph (captured on the 2nd step, re-captured
@@ -375,6 +377,11 @@ void vdnn_kernel_set_tma(int32_t on);
    wire (device u64 counter, may be NULL for decompress) accumulates the bytes moved. */
 uint64_t vdnn_kernel_zvc_slot_bytes(uint64_t bytes);
 vdnn_status vdnn_kernel_zvc_compress(const float* src, uint64_t count, void* host_dst, uint64_t* wire, void* stream);
+/* As vdnn_kernel_zvc_compress, but nonzeros may travel TF32-exact (sign, exponent, top 10 mantissa bits;
+   the low 13 bits -- ignored by tcgen05 kind::tf32 -- are dropped). Chunks holding a nonzero that would
+   truncate to +-0 or an Inf/NaN stay lossless. */
+vdnn_status vdnn_kernel_zvc_compress_tf32(const float* src, uint64_t count, void* host_dst, uint64_t* wire,
+                                          void* stream);
 vdnn_status vdnn_kernel_zvc_decompress(const void* host_src, uint64_t count, float* dst, uint64_t* wire,
                                        void* stream);
 /* Measured tcgen05 kind::tf32 ceiling of the current device in TFLOP/s (roofline denominator). */

@@ -155,6 +155,7 @@ def lib() -> C.CDLL:
         _lib.vdnn_kernel_zvc_slot_bytes.restype = C.c_uint64
         _lib.vdnn_kernel_zvc_slot_bytes.argtypes = [C.c_uint64]
         _lib.vdnn_kernel_zvc_compress.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.vdnn_kernel_zvc_compress_tf32.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.vdnn_kernel_zvc_decompress.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
         if hasattr(_lib, "vdnn_session_plan"):
             _lib.vdnn_session_plan.restype = C.c_void_p

@@ -737,10 +737,13 @@ class Session:
     def __init__(self, g: NetworkGraph, decision: PolicyDecision, cost: Optional[CostModel] = None,
                  capacity: int = 12884901888, device: int = 0, weight_seed: int = 5000,
                  external_grads: bool = False, record_timeline: bool = False, precise_fp32: bool = False,
-                 compress_offload: bool = False, offload_target: str = "host", cuda_graph: bool = False):
+                 compress_offload=False, offload_target: str = "host", cuda_graph: bool = False):
         """compress_offload: move offloads/prefetches through the SMs in a
         lossless zero-value-compressed form (same schedule, bit-identical
-        restored buffers, fewer bytes on the host link).
+        restored buffers, fewer bytes on the host link). "tf32": the same,
+        and maps whose backward readers are only TF32 contractions and ReLU
+        masks travel TF32-exact (the 13 low mantissa bits the tensor core
+        ignores are dropped; the training step stays bit-identical).
         offload_target: "host" (pinned host memory over PCIe, the reference's
         model) or "device" (a device buffer given to set_offload_buffer, or a
         peer GPU's spill buffer via spill_export / spill_attach: NVLink).
@@ -759,7 +762,9 @@ class Session:
         opt.external_grads = int(external_grads)
         opt.record_timeline = int(record_timeline)
         opt.precise_fp32 = int(precise_fp32)
-        opt.compress_offload = int(compress_offload)
+        if compress_offload not in (False, True, 0, 1, "zvc", "tf32"):
+            raise ValueError(f"compress_offload must be a bool, 'zvc' or 'tf32', not {compress_offload!r}")
+        opt.compress_offload = 2 if compress_offload == "tf32" else int(bool(compress_offload))
         opt.offload_target = 0 if offload_target == "host" else 1
         opt.cuda_graph = int(cuda_graph)
         d = decision._handle(g)

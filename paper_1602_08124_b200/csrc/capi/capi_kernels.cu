@@ -47,6 +47,15 @@ vdnn_status vdnn_kernel_zvc_compress(const float* src, uint64_t count, void* hos
                                          static_cast<cudaStream_t>(stream)),
                      "zvc_compress");
 }
+vdnn_status vdnn_kernel_zvc_compress_tf32(const float* src, uint64_t count, void* host_dst, uint64_t* wire,
+                                          void* stream) {
+  if (!src || !host_dst || !wire) return fail(VDNN_INVALID_ARGUMENT, "null argument");
+  if (!vdnnk::zvc_eligible(src, count * 4) || !vdnnk::zvc_eligible(host_dst, 16))
+    return fail(VDNN_INVALID_ARGUMENT, "zvc needs count % 4 == 0 and 16-B aligned buffers");
+  return cuda_status(vdnnk::zvc_compress(src, count, host_dst, reinterpret_cast<unsigned long long*>(wire),
+                                         static_cast<cudaStream_t>(stream), true),
+                     "zvc_compress_tf32");
+}
 vdnn_status vdnn_kernel_zvc_decompress(const void* host_src, uint64_t count, float* dst, uint64_t* wire,
                                        void* stream) {
   if (!host_src || !dst) return fail(VDNN_INVALID_ARGUMENT, "null argument");

@@ -65,7 +65,9 @@ vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, con
       o.record_timeline = opt->record_timeline != 0;
       o.host_arena = opt->host_arena != 0;
       o.precise = opt->precise_fp32 != 0;
-      o.compress_offload = opt->compress_offload != 0;
+      if (opt->compress_offload < 0 || opt->compress_offload > 2)
+        throw vdnnp::PlanError(vdnnp::Err::Config, "compress_offload must be 0, 1 or 2");
+      o.compress_offload = opt->compress_offload;
       o.offload_target = opt->offload_target;
       o.cuda_graph = opt->cuda_graph != 0;
     }

@@ -102,7 +102,9 @@ constexpr int kZvcChunk = 1024;
 constexpr int kZvcSlot = 128 + 16 + 4 * kZvcChunk;  // mask + header + dense values (worst case)
 uint64_t zvc_slot_bytes(uint64_t bytes);
 bool zvc_eligible(const void* p, uint64_t bytes);
-cudaError_t zvc_compress(const float* src, uint64_t count, void* host_dst, unsigned long long* wire, cudaStream_t st);
+// tf32 = true: nonzeros may travel TF32-exact (low 13 mantissa bits dropped; zvc.cu mode 2)
+cudaError_t zvc_compress(const float* src, uint64_t count, void* host_dst, unsigned long long* wire, cudaStream_t st,
+                         bool tf32 = false);
 cudaError_t zvc_decompress(const void* host_src, uint64_t count, float* dst, unsigned long long* wire,
                            cudaStream_t st);
 // Data-parallel exchange over peer memory (peer.cu): barrier flags and the

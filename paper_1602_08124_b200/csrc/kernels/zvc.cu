@@ -20,6 +20,14 @@
 //           two per byte, padded to 16 B) -- chosen when a chunk's top bytes span <= 15, which
 //           holds for every chunk of the VGG-16 offload set measured (tools/zvc_stats.py):
 //           3.5 B per nonzero instead of 4, wire 0.44 -> 0.39 of the raw bytes.
+//   mode 2 (TF32-exact transfers, only when the caller asks for it): each nonzero as one u16 =
+//           (4-bit top-byte offset << 11) | the next 11 bits (exponent LSB + the 10 TF32 mantissa
+//           bits). The low 13 mantissa bits are dropped: the tcgen05 kind::tf32 MMA ignores them
+//           (measured: tools/tf32_trunc_probe.py -- fprop and wgrad outputs on X and on X with those
+//           bits cleared are bit-identical), so for a map whose only backward readers are TF32
+//           contractions and ReLU masks the training step is bit-identical. A chunk falls back to
+//           mode 1 / 0 if a nonzero would truncate to +-0 (a denormal: the ReLU mask x > 0 must
+//           survive) or is Inf/NaN. 2 B per nonzero instead of 3.5.
 // Only the header and the padded payload cross the link; a dense chunk costs
 // +3.5% (mask + header), an all-zero chunk 144 B.
 #include <cstdlib>
@@ -56,7 +64,7 @@ __device__ __forceinline__ void warp_copy_out(const float* st, uint8_t* out, uin
 
 __global__ void __launch_bounds__(kWarps * 32) zvc_compress_kernel(const float4* __restrict__ src, int64_t n4,
                                                                    uint8_t* __restrict__ dst,
-                                                                   unsigned long long* __restrict__ wire) {
+                                                                   unsigned long long* __restrict__ wire, int tf32) {
   __shared__ __align__(16) float stage[kWarps][kZvcChunk + 4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nchunks = (n4 + kZvcChunk / 4 - 1) / (kZvcChunk / 4);
@@ -72,6 +80,7 @@ __global__ void __launch_bounds__(kWarps * 32) zvc_compress_kernel(const float4*
       v[j] = i < n4 ? __ldcs(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     uint32_t mask = 0, tmin = 255, tmax = 0;
+    bool inexact = false;  // a nonzero that TF32 truncation would not represent (denormal -> 0, Inf/NaN)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t q[4] = {__float_as_uint(v[j].x), __float_as_uint(v[j].y), __float_as_uint(v[j].z),
@@ -82,8 +91,10 @@ __global__ void __launch_bounds__(kWarps * 32) zvc_compress_kernel(const float4*
           mask |= 1u << (4 * j + e);
           tmin = min(tmin, q[e] >> 24);
           tmax = max(tmax, q[e] >> 24);
+          inexact |= ((q[e] & 0x7FFFE000u) == 0u) || ((q[e] & 0x7F800000u) == 0x7F800000u);
         }
     }
+    inexact = __any_sync(0xffffffffu, inexact);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
@@ -101,12 +112,31 @@ __global__ void __launch_bounds__(kWarps * 32) zvc_compress_kernel(const float4*
     __syncwarp();
     uint8_t* out = dst + c * kZvcSlot;
     reinterpret_cast<uint32_t*>(out)[lane] = mask;
-    const uint32_t mode = (total > 0 && tmax - tmin <= 15u) ? 1u : 0u;
+    const bool narrow = total > 0 && tmax - tmin <= 15u;
+    const uint32_t mode = narrow ? ((tf32 && !inexact) ? 2u : 1u) : 0u;
     if (lane == 0)
       *reinterpret_cast<uint4*>(out + 128) = make_uint4(mode, tmin, total, 0u);
     uint32_t payload;
     if (mode == 0) {
       payload = pad16(4 * total);
+      warp_copy_out(st, out + 128 + kHdr, payload, lane);
+    } else if (mode == 2) {
+      // values into registers first, then the u16 codes in place
+      uint32_t w[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t k2 = lane + 32u * i;
+        w[i] = k2 < total ? __float_as_uint(st[k2]) : 0u;
+      }
+      __syncwarp();
+      uint16_t* pk = reinterpret_cast<uint16_t*>(st);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t k2 = lane + 32u * i;
+        if (k2 < total) pk[k2] = static_cast<uint16_t>((((w[i] >> 24) - tmin) << 11) | ((w[i] >> 13) & 0x7FFu));
+      }
+      __syncwarp();
+      payload = pad16(2 * total);
       warp_copy_out(st, out + 128 + kHdr, payload, lane);
     } else {
       // pack in place: each lane reads its value pairs (2p, 2p+1) into
@@ -164,14 +194,31 @@ __global__ void __launch_bounds__(kWarps * 32) zvc_decompress_kernel(const uint8
     const uint4 hdr = __ldcs(reinterpret_cast<const uint4*>(in + 128));
     uint32_t total;
     uint32_t k = warp_excl_scan(__popc(mask), total);
-    const uint32_t payload = hdr.x == 0 ? pad16(4 * total) : pad16(3 * total) + pad16((total + 1) / 2);
+    const uint32_t payload = hdr.x == 0   ? pad16(4 * total)
+                             : hdr.x == 2 ? pad16(2 * total)
+                                          : pad16(3 * total) + pad16((total + 1) / 2);
     {
       const float4* i4 = reinterpret_cast<const float4*>(in + 128 + kHdr);
       float4* st4 = reinterpret_cast<float4*>(st);
       for (uint32_t i = lane; i < payload / 16; i += 32) st4[i] = __ldcs(i4 + i);
     }
     __syncwarp();
-    if (hdr.x == 1) {  // unpack to floats in place (read every pair into registers first)
+    if (hdr.x == 2) {  // u16 codes -> TF32-exact floats in place (codes into registers first)
+      const uint16_t* pk = reinterpret_cast<const uint16_t*>(st);
+      uint32_t w[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t k2 = lane + 32u * i;
+        w[i] = k2 < total ? pk[k2] : 0u;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t k2 = lane + 32u * i;
+        if (k2 < total) st[k2] = __uint_as_float((((w[i] >> 11) + hdr.y) << 24) | ((w[i] & 0x7FFu) << 13));
+      }
+      __syncwarp();
+    } else if (hdr.x == 1) {  // unpack to floats in place (read every pair into registers first)
       const uint8_t* pk = reinterpret_cast<const uint8_t*>(st);
       const uint32_t off3 = pad16(3 * total), npairs = (total + 1) / 2;
       uint32_t w[32];
@@ -240,13 +287,14 @@ bool zvc_eligible(const void* p, uint64_t bytes) {
   return bytes > 0 && bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 }
 
-cudaError_t zvc_compress(const float* src, uint64_t count, void* dst, unsigned long long* wire, cudaStream_t st) {
+cudaError_t zvc_compress(const float* src, uint64_t count, void* dst, unsigned long long* wire, cudaStream_t st,
+                         bool tf32) {
   if (count == 0) return cudaSuccess;
   if (count % 4 != 0) return cudaErrorInvalidValue;
   const int64_t n4 = static_cast<int64_t>(count / 4);
   const int64_t nchunks = (n4 + kZvcChunk / 4 - 1) / (kZvcChunk / 4);
   zvc_compress_kernel<<<zvc_grid(nchunks), kWarps * 32, 0, st>>>(reinterpret_cast<const float4*>(src), n4,
-                                                                  static_cast<uint8_t*>(dst), wire);
+                                                                  static_cast<uint8_t*>(dst), wire, tf32 ? 1 : 0);
   count_launch();
   return cudaGetLastError();
 }

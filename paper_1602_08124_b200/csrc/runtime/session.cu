@@ -356,6 +356,7 @@ void Session::build_program() {
         t.host_off = host_slot_[b];
         t.ev = xfer++;
         t.zvc = compressible(e.buffer) && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes);
+        t.tf32 = t.zvc && o_.compress_offload == 2 && tf32_exact_ok(e.buffer);
         fwd_.back().offloads.push_back(t);
         break;
       }
@@ -368,6 +369,7 @@ void Session::build_program() {
         t.host_off = host_slot_[b];
         t.ev = xfer++;
         t.zvc = compressible(e.buffer) && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes);
+        t.tf32 = t.zvc && o_.compress_offload == 2 && tf32_exact_ok(e.buffer);
         pending.push_back(t);
         break;
       }
@@ -453,6 +455,31 @@ void Session::build_program() {
 // ReLU outputs (~35% nonzero on VGG-16) and max-pool outputs (the max of
 // ReLU windows: ~50% zeros, tools/zvc_stats.py) go through the compressing
 // kernels; dense maps (the input images) keep the copy engines.
+// Mode 2: a map may travel TF32-exact when everything that reads it in the
+// backward pass consumes it only through a tcgen05 kind::tf32 contraction
+// (conv / FC wgrad operand) or a ReLU mask (x > 0, preserved: zvc.cu keeps
+// any chunk with a would-be-zero denormal lossless): its readers, through
+// in-place ACTV aliases, are conv layers with > 4 input channels (C <= 4
+// layers may run SIMT kernels) and FC layers. Max-pool backward locates the
+// max by equality of X and Y, so pool inputs and outputs stay lossless.
+bool Session::tf32_exact_ok(int owner) const {
+  if (o_.precise || (g_.at(owner).kind != Kind::Conv && g_.at(owner).kind != Kind::Fc)) return false;
+  std::vector<int> todo(g_.users(owner).begin(), g_.users(owner).end());
+  while (!todo.empty()) {
+    const int u = todo.back();
+    todo.pop_back();
+    const Node& n = g_.at(u);
+    if (n.kind == Kind::Actv) {
+      todo.insert(todo.end(), g_.users(u).begin(), g_.users(u).end());
+    } else if (n.kind == Kind::Conv) {
+      if (g_.in_dims(u).c <= 4) return false;
+    } else if (n.kind != Kind::Fc) {
+      return false;
+    }
+  }
+  return true;
+}
+
 bool Session::compressible(int owner) const {
   if (!o_.compress_offload) return false;
   if (g_.at(owner).kind == Kind::Pool) return true;
@@ -570,7 +597,8 @@ void Session::run_fwd(const FwdStep& s, float lr) {
     for (const Transfer& t : s.offloads) {
       if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev)], ms_), "record");
       if (t.zvc)
-        check(vdnnk::zvc_compress(F(t.dev_off), t.bytes / 4, host_dev_ + t.host_off, wire_, ms_), "zvc offload");
+        check(vdnnk::zvc_compress(F(t.dev_off), t.bytes / 4, host_dev_ + t.host_off, wire_, ms_, t.tf32),
+              "zvc offload");
       else {
         check(cudaMemcpyAsync(host_ + t.host_off, base_ + t.dev_off, t.bytes, cudaMemcpyDefault, ms_), "offload copy");
         copy_off_ += t.bytes;

@@ -25,9 +25,12 @@ struct Options {
   bool host_arena = true;
   bool precise = false;  // 3xTF32 contractions
   // Offload / prefetch through the SMs in zero-value-compressed form
-  // (kernels/zvc.cu) instead of cudaMemcpyAsync; same schedule, same bytes
-  // restored, fewer bytes on the host link.
-  bool compress_offload = false;
+  // (kernels/zvc.cu) instead of cudaMemcpyAsync; same schedule, fewer bytes
+  // on the host link. 1: lossless (every byte restored). 2: additionally,
+  // maps whose only backward readers are TF32 contractions (conv/FC wgrad
+  // operands) and ReLU masks travel TF32-exact (the 13 mantissa bits the
+  // tensor core ignores are dropped): the training step stays bit-identical.
+  int compress_offload = 0;
   // Where offloaded feature maps go: 0 = the pinned host arena (PCIe, the
   // reference's model); 1 = a device buffer set later with
   // set_offload_buffer / spill_attach (e.g. a peer GPU's spare HBM over
@@ -53,6 +56,7 @@ struct Transfer {
   u64 host_off = 0;
   int ev = -1;      // timing event pair index
   bool zvc = false; // compressed mode and the buffer holds ReLU outputs (sparse)
+  bool tf32 = false; // compressed mode 2 and only TF32 consumers read it in backward
 };
 
 struct FwdStep {
@@ -150,6 +154,7 @@ class Session {
   void build_program();
   void fuse_relus();
   bool compressible(int owner) const;
+  bool tf32_exact_ok(int owner) const;
   void assign_two_buffer();
   void init_weights();
   void run_fwd(const FwdStep& s, float lr);

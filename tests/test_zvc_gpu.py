@@ -17,22 +17,33 @@ def _pad16(b):
     return (b + 15) // 16 * 16
 
 
-def _expected_wire(x):
-    """Bytes the v2 format moves (zvc.cu): per 1024-value chunk the mask and a
-    16-B header, then either the raw nonzeros or -- when the nonzeros' top
-    bytes span <= 15 -- their low 3 bytes plus a 4-bit top-byte offset."""
+def _chunk_modes(x, tf32=False):
+    """Per 1024-value chunk: (mode, nnz) as zvc.cu chooses them."""
     u = x.view(torch.int32).cpu().numpy().view(np.uint32)
     n = u.size
     u = np.concatenate([u, np.zeros((-n) % 1024, dtype=np.uint32)]).reshape(-1, 1024)
-    total = 0
+    out = []
     for row in u:
         nzv = row[row != 0]
         nnz = nzv.size
         top = nzv >> 24
+        inexact = bool(np.any((nzv & 0x7FFFE000) == 0) or np.any((nzv & 0x7F800000) == 0x7F800000))
         if nnz and int(top.max()) - int(top.min()) <= 15:
-            total += 144 + _pad16(3 * nnz) + _pad16((nnz + 1) // 2)
+            out.append((2 if tf32 and not inexact else 1, nnz))
         else:
-            total += 144 + _pad16(4 * nnz)
+            out.append((0, nnz))
+    return out
+
+
+def _expected_wire(x, tf32=False):
+    """Bytes the v2 format moves (zvc.cu): per 1024-value chunk the mask and a
+    16-B header, then either the raw nonzeros, or -- when the nonzeros' top
+    bytes span <= 15 -- their low 3 bytes plus a 4-bit top-byte offset, or
+    (TF32-exact transfers) one u16 per nonzero."""
+    total = 0
+    for mode, nnz in _chunk_modes(x, tf32):
+        total += 144 + (_pad16(2 * nnz) if mode == 2 else
+                        _pad16(3 * nnz) + _pad16((nnz + 1) // 2) if mode == 1 else _pad16(4 * nnz))
     return total
 
 
@@ -92,6 +103,90 @@ def test_zvc_packed_mode_edge_cases():
     _roundtrip(x)
 
 
+def _roundtrip_tf32(x):
+    """TF32-exact transfer: mode-2 chunks come back with the low 13 mantissa
+    bits cleared, every other chunk bit-exact; wire bytes per the model."""
+    n = x.numel()
+    lib = L.lib()
+    slot = lib.vdnn_kernel_zvc_slot_bytes(C.c_uint64(4 * n))
+    host = torch.empty(slot // 4 + 4, dtype=torch.float32).pin_memory()
+    host.fill_(float("nan"))
+    wire = torch.zeros(2, dtype=torch.int64, device="cuda")
+    y = torch.full_like(x, 7.0)
+    assert lib.vdnn_kernel_zvc_compress_tf32(C.c_void_p(x.data_ptr()), C.c_uint64(n), C.c_void_p(host.data_ptr()),
+                                             C.c_void_p(wire.data_ptr()), None) == 0, lib.vdnn_last_error()
+    assert lib.vdnn_kernel_zvc_decompress(C.c_void_p(host.data_ptr()), C.c_uint64(n), C.c_void_p(y.data_ptr()),
+                                          C.c_void_p(wire.data_ptr() + 8), None) == 0, lib.vdnn_last_error()
+    torch.cuda.synchronize()
+    modes = _chunk_modes(x, tf32=True)
+    xi = x.view(torch.int32).cpu()
+    want = xi.clone()
+    for c, (mode, _) in enumerate(modes):
+        if mode == 2:
+            want[c * 1024:(c + 1) * 1024] &= ~0x1FFF
+    assert torch.equal(y.view(torch.int32).cpu(), want)
+    w = wire.cpu().tolist()
+    assert w[0] == w[1] == _expected_wire(x, tf32=True)
+    return w[0], modes
+
+
+@pytest.mark.parametrize("n", [1024, 4096 * 3 + 8, 1 << 20])
+def test_zvc_tf32_exact_relu_like(n):
+    g = torch.Generator(device="cuda").manual_seed(n + 1)
+    x = torch.relu(torch.randn(n, device="cuda", generator=g))
+    w, modes = _roundtrip_tf32(x)
+    assert all(m == 2 for m, nnz in modes if nnz)
+    assert w < _expected_wire(x)  # 2 B per nonzero instead of 3.5
+
+
+def test_zvc_tf32_exact_keeps_denormals_and_specials_lossless():
+    """Chunks whose top bytes span <= 15 but that hold a nonzero TF32
+    truncation cannot represent stay in the lossless packed mode: a positive
+    denormal next to tiny normals (truncation would zero it and flip the ReLU
+    mask), +Inf / a NaN payload next to huge normals."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    r = torch.rand(4096, device="cuda", generator=g) + 1.0
+    x = torch.cat([r[:1024] * 2.0 ** -120, r[1024:2048] * 2.0 ** 120, r[2048:3072] * 2.0 ** 120,
+                   torch.relu(r[3072:] - 1.5)])
+    xi = x.view(torch.int32)
+    xi[5] = 1                   # positive denormal
+    xi[1024 + 7] = 0x7F800000   # +Inf
+    xi[2048 + 9] = 0x7FC00001   # NaN with a payload
+    _, modes = _roundtrip_tf32(x)
+    assert [m for m, _ in modes] == [1, 1, 1, 2]
+
+
+def test_tf32_operands_truncate():
+    """The premise of TF32-exact transfers: the tensor core ignores the 13 low
+    mantissa bits of fp32 operands, so a conv on X and on X with those bits
+    cleared gives bit-identical fprop and wgrad outputs."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(2)
+    n, h, c, co = 4, 28, 64, 128
+    x = torch.relu(torch.randn(n, h, h, c, device=dev, generator=g))
+    xt = (x.view(torch.int32) & ~0x1FFF).view(torch.float32)
+    wt = torch.randn(co, 3, 3, c, device=dev, generator=g) * 0.05
+    dy = torch.randn(n, h, h, co, device=dev, generator=g)
+    outs = []
+    for xx in (x, xt):
+        d = L.ConvDesc()
+        d.n, d.h, d.w, d.nseg = n, h, h, 1
+        d.x[0] = xx.data_ptr()
+        d.c[0] = c
+        d.cout, d.kh, d.kw, d.stride, d.pad = co, 3, 3, 1, 1
+        y = torch.empty(n, h, h, co, device=dev)
+        L.call("vdnn_kernel_conv_fprop", C.byref(d), C.c_void_p(wt.data_ptr()), None, C.c_void_p(y.data_ptr()), None)
+        wsb = L.lib().vdnn_kernel_conv_wgrad_ws_bytes(C.byref(d))
+        ws = torch.empty(max(wsb // 4, 1), device=dev)
+        dw = torch.empty_like(wt)
+        L.call("vdnn_kernel_conv_wgrad", C.byref(d), C.c_void_p(dy.data_ptr()), C.c_void_p(wt.data_ptr()),
+               C.c_float(0.0), C.c_void_p(dw.data_ptr()), C.c_void_p(ws.data_ptr()), C.c_size_t(wsb), None)
+        torch.cuda.synchronize()
+        outs.append((y, dw))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+
+
 def _train(g, d, cap, compress, steps=2):
     s = V.Session(g, d, V.CostModel(), cap, compress_offload=compress)
     s.synthetic_batch(7)
@@ -115,3 +210,22 @@ def test_compressed_session_bit_identical(net, batch):
     assert t0["offload_wire"] == t0["offload_planned"]          # copy engines move the planned bytes
     assert t1["offload_wire"] == t1["prefetch_wire"]             # what went out comes back
     assert t1["offload_wire"] < t1["offload_planned"]            # ReLU maps are sparse
+
+
+@pytest.mark.parametrize("net,batch", [("alexnet", 16), ("inception_toy", 16)])
+def test_tf32_exact_session_bit_identical(net, batch):
+    """compress_offload="tf32": maps read in backward only by TF32
+    contractions and ReLU masks travel TF32-exact; losses and weights after
+    two steps equal the copy-engine run bit for bit, with fewer wire bytes
+    than the lossless format."""
+    g = V.build_preset(net, batch)
+    d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, V.CostModel())
+    cap = 8 << 30
+    l0, w0, _, _ = _train(g, d, cap, False)
+    _, _, t1, _ = _train(g, d, cap, True)
+    l2, w2, t2, _ = _train(g, d, cap, "tf32")
+    assert l0 == l2
+    for a, b in zip(w0, w2):
+        assert np.array_equal(a.view(np.int32), b.view(np.int32))
+    assert t2["offload_wire"] == t2["prefetch_wire"]
+    assert t2["offload_wire"] < t1["offload_wire"]
