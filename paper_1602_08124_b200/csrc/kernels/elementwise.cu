@@ -268,12 +268,82 @@ cudaError_t maxpool_fwd(const PoolArgs& a, float* y, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// The backward kernels do not read Y: each recomputes its window's maximum
+// from X with the forward's rule (row-major scan, strict '>'), which gives
+// Y's exact value, and routes dY to the first position equal to it -- the
+// same position as comparing with the stored Y (a NaN maximum matches
+// nothing either way). Saves the Y read, and a pool output whose other
+// backward readers are TF32 contractions may travel TF32-exact (zvc.cu).
+template <int VEC>
+__device__ __forceinline__ void window_max(const float* x, size_t rowoff0, size_t row_pitch, int C, int window,
+                                           float (&m)[VEC]) {
+  bool first = true;
+  for (int r = 0; r < window; ++r) {
+    const size_t rowoff = rowoff0 + static_cast<size_t>(r) * row_pitch;
+    for (int q = 0; q < window; ++q) {
+      float v[VEC];
+      if constexpr (VEC == 4) {
+        const float4 f = *reinterpret_cast<const float4*>(x + rowoff + static_cast<size_t>(q) * C);
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+      } else {
+        v[0] = x[rowoff + static_cast<size_t>(q) * C];
+      }
+#pragma unroll
+      for (int k = 0; k < VEC; ++k)
+        if (first || v[k] > m[k]) m[k] = v[k];
+      first = false;
+    }
+  }
+}
+
+// 2x2 / stride 2 over one NHWC tensor (every VGG pool): the four window loads
+// in registers, the forward's compare order, first equal position wins.
+__global__ void __launch_bounds__(256) maxpool2x2_bwd_kernel(const float* __restrict__ x, float* __restrict__ dx,
+                                                            const float* __restrict__ dy, int h, int w, int c,
+                                                            int ho, int wo, int msk) {
+  const int cv = c >> 2;
+  const int row = blockIdx.y;  // n * ho + oh
+  const int n = row / ho, oh = row - n * ho;
+  const size_t base0 = (static_cast<size_t>(n) * h + 2 * oh) * w * cv;
+  const float4* x0 = reinterpret_cast<const float4*>(x) + base0;
+  const float4* x1 = x0 + static_cast<size_t>(w) * cv;
+  float4* d0 = reinterpret_cast<float4*>(dx) + base0;
+  float4* d1 = d0 + static_cast<size_t>(w) * cv;
+  const float4* dyr = reinterpret_cast<const float4*>(dy + static_cast<size_t>(row) * wo * c);
+  const int per_row = wo * cv;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < per_row; i += gridDim.x * blockDim.x) {
+    const int ow = i / cv, c4 = i - ow * cv;
+    const int off = 2 * ow * cv + c4;
+    const float4 a = __ldcs(x0 + off), b = __ldcs(x0 + off + cv), e = __ldcs(x1 + off), f = __ldcs(x1 + off + cv);
+    const float4 g = __ldcs(dyr + i);
+    const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w}, ev[4] = {e.x, e.y, e.z, e.w},
+                fv[4] = {f.x, f.y, f.z, f.w}, gv[4] = {g.x, g.y, g.z, g.w};
+    float oa[4], ob[4], oe[4], of[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float m = av[k];
+      m = bv[k] > m ? bv[k] : m;
+      m = ev[k] > m ? ev[k] : m;
+      m = fv[k] > m ? fv[k] : m;
+      const bool ha = av[k] == m, hb = !ha && bv[k] == m, he = !ha && !hb && ev[k] == m,
+                 hf = !ha && !hb && !he && fv[k] == m;
+      oa[k] = (ha && (!msk || av[k] > 0.f)) ? gv[k] : 0.f;
+      ob[k] = (hb && (!msk || bv[k] > 0.f)) ? gv[k] : 0.f;
+      oe[k] = (he && (!msk || ev[k] > 0.f)) ? gv[k] : 0.f;
+      of[k] = (hf && (!msk || fv[k] > 0.f)) ? gv[k] : 0.f;
+    }
+    d0[off] = make_float4(oa[0], oa[1], oa[2], oa[3]);
+    d0[off + cv] = make_float4(ob[0], ob[1], ob[2], ob[3]);
+    d1[off] = make_float4(oe[0], oe[1], oe[2], oe[3]);
+    d1[off + cv] = make_float4(of[0], of[1], of[2], of[3]);
+  }
+}
+
 // Non-overlapping windows (stride >= window): one thread per output element
 // (x VEC channels) finds the first maximum and scatters dY to it, zeros to the
 // rest of its window -- every covered input written exactly once, no atomics.
 template <int VEC>
-__global__ void maxpool_bwd_scatter_kernel(const __grid_constant__ PoolDev d, const float* __restrict__ y,
-                                           const float* __restrict__ dy) {
+__global__ void maxpool_bwd_scatter_kernel(const __grid_constant__ PoolDev d, const float* __restrict__ dy) {
   const int cv = d.ctot / VEC;
   const size_t total = static_cast<size_t>(d.n) * d.ho * d.wo * cv;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
@@ -293,9 +363,10 @@ __global__ void maxpool_bwd_scatter_kernel(const __grid_constant__ PoolDev d, co
     const size_t oidx = ((static_cast<size_t>(n) * d.ho + oh) * d.wo + ow) * d.ctot + c;
     float ym[VEC], g[VEC];
     bool done[VEC];
+    window_max<VEC>(x, ((static_cast<size_t>(n) * d.h + oh * d.stride) * d.w + ow * d.stride) * C + cl,
+                    static_cast<size_t>(d.w) * C, C, d.window, ym);
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {
-      ym[k] = y[oidx + k];
       g[k] = dy[oidx + k];
       done[k] = false;
     }
@@ -328,8 +399,7 @@ __global__ void maxpool_bwd_scatter_kernel(const __grid_constant__ PoolDev d, co
 
 // Overlapping windows: gather form (deterministic): every input element sums
 // dY over the windows whose first-maximum position it is.
-__global__ void maxpool_bwd_kernel(const __grid_constant__ PoolDev d, const float* __restrict__ y,
-                                   const float* __restrict__ dy) {
+__global__ void maxpool_bwd_kernel(const __grid_constant__ PoolDev d, const float* __restrict__ dy) {
   const size_t total = static_cast<size_t>(d.n) * d.h * d.w * d.ctot;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -357,7 +427,10 @@ __global__ void maxpool_bwd_kernel(const __grid_constant__ PoolDev d, const floa
     for (int oh = oh_lo; oh <= oh_hi; ++oh) {
       for (int ow = ow_lo; ow <= ow_hi; ++ow) {
         const size_t oidx = ((static_cast<size_t>(n) * d.ho + oh) * d.wo + ow) * d.ctot + c;
-        const float ym = y[oidx];
+        float ymv[1];
+        window_max<1>(x, ((static_cast<size_t>(n) * d.h + oh * d.stride) * d.w + ow * d.stride) * C + cl,
+                      static_cast<size_t>(d.w) * C, C, d.window, ymv);
+        const float ym = ymv[0];
         // first position in row-major window order holding the max
         int ar = -1, aq = -1;
         for (int r = 0; r < d.window && ar < 0; ++r) {
@@ -384,8 +457,7 @@ __global__ void maxpool_bwd_kernel(const __grid_constant__ PoolDev d, const floa
 // once all four channels found their argmax. The scalar kernel rescanned up to
 // 9 window elements per covering window with 4-byte loads (AlexNet 55x55x64
 // pool: 1.05 ms for ~0.25 GB of traffic).
-__global__ void maxpool_bwd_gather4_kernel(const __grid_constant__ PoolDev d, const float* __restrict__ y,
-                                           const float* __restrict__ dy) {
+__global__ void maxpool_bwd_gather4_kernel(const __grid_constant__ PoolDev d, const float* __restrict__ dy) {
   const int cv = d.ctot / 4;
   const size_t total = static_cast<size_t>(d.n) * d.h * d.w * cv;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
@@ -413,8 +485,9 @@ __global__ void maxpool_bwd_gather4_kernel(const __grid_constant__ PoolDev d, co
     for (int oh = oh_lo; oh <= oh_hi; ++oh) {
       for (int ow = ow_lo; ow <= ow_hi; ++ow) {
         const size_t oidx = ((static_cast<size_t>(n) * d.ho + oh) * d.wo + ow) * d.ctot + c;
-        const float4 y4 = *reinterpret_cast<const float4*>(y + oidx);
-        const float ym[4] = {y4.x, y4.y, y4.z, y4.w};
+        float ym[4];
+        window_max<4>(x, ((static_cast<size_t>(n) * d.h + oh * d.stride) * d.w + ow * d.stride) * C + cl,
+                      static_cast<size_t>(d.w) * C, C, d.window, ym);
         int arg[4] = {-1, -1, -1, -1};  // r * window + q of the first maximum, per channel
         int left = 4;
         for (int r = 0; r < d.window && left > 0; ++r) {
@@ -496,6 +569,7 @@ __global__ void maxpool_bwd_class_kernel(const __grid_constant__ PoolDev d, cons
     const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      if (m[k] != m[k]) continue;  // NaN maximum: no position equals it
       if (d.mask[s] && m[k] <= 0.f) continue;
       const int r = arg[k] / d.window, q = arg[k] - r * d.window;
       float* dst = dx + ((static_cast<size_t>(n) * d.h + oh * d.stride + r) * d.w + ow * d.stride + q) * C + cl + k;
@@ -519,10 +593,16 @@ cudaError_t maxpool_bwd(const PoolArgs& a, const float* y, const float* dy, cuda
           if (e != cudaSuccess) return e;
         }
     const size_t outs = static_cast<size_t>(d.n) * d.ho * d.wo * d.ctot;
-    if (pool_vec4(d))
-      maxpool_bwd_scatter_kernel<4><<<grid_for(outs / 4, 2), kThreads, 0, st>>>(d, y, dy);
-    else
-      maxpool_bwd_scatter_kernel<1><<<grid_for(outs, 4), kThreads, 0, st>>>(d, y, dy);
+    if (!gaps && d.nseg == 1 && d.window == 2 && d.stride == 2 && d.c[0] % 4 == 0 && d.dx[0] &&
+        static_cast<int64_t>(d.n) * d.ho <= 65535) {
+      const int per_row = d.wo * d.c[0] / 4;
+      const dim3 grid(static_cast<unsigned>((per_row + 255) / 256), static_cast<unsigned>(d.n * d.ho));
+      maxpool2x2_bwd_kernel<<<grid, 256, 0, st>>>(d.x[0], d.dx[0], dy, d.h, d.w, d.c[0], d.ho, d.wo, d.mask[0]);
+    } else if (pool_vec4(d)) {
+      maxpool_bwd_scatter_kernel<4><<<grid_for(outs / 4, 2), kThreads, 0, st>>>(d, dy);
+    } else {
+      maxpool_bwd_scatter_kernel<1><<<grid_for(outs, 4), kThreads, 0, st>>>(d, dy);
+    }
   } else if (pool_vec4(d) && d.window <= 2 * d.stride) {
     for (int i = 0; i < d.nseg; ++i)
       if (d.dx[i]) {
@@ -537,9 +617,9 @@ cudaError_t maxpool_bwd(const PoolArgs& a, const float* y, const float* dy, cuda
       }
     return cudaGetLastError();
   } else if (pool_vec4(d)) {
-    maxpool_bwd_gather4_kernel<<<grid_for(total / 4, 2), kThreads, 0, st>>>(d, y, dy);
+    maxpool_bwd_gather4_kernel<<<grid_for(total / 4, 2), kThreads, 0, st>>>(d, dy);
   } else {
-    maxpool_bwd_kernel<<<grid_for(total, 4), kThreads, 0, st>>>(d, y, dy);
+    maxpool_bwd_kernel<<<grid_for(total, 4), kThreads, 0, st>>>(d, dy);
   }
   count_launch();
   return cudaGetLastError();

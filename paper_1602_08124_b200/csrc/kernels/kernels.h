@@ -75,6 +75,8 @@ struct PoolArgs {
   }
 };
 cudaError_t maxpool_fwd(const PoolArgs& a, float* y, cudaStream_t st);
+// `y` (the reference's operand set: X, Y, dY) is not read: the kernels
+// recompute each window's maximum from X with the forward's rule.
 cudaError_t maxpool_bwd(const PoolArgs& a, const float* y, const float* dy, cudaStream_t st);
 // Mean softmax cross-entropy over n rows of k logits. Writes the gradient
 // (softmax - onehot)/n into grad_scratch, the per-row loss into row_loss and

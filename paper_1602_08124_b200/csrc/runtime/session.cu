@@ -460,10 +460,13 @@ void Session::build_program() {
 // (conv / FC wgrad operand) or a ReLU mask (x > 0, preserved: zvc.cu keeps
 // any chunk with a would-be-zero denormal lossless): its readers, through
 // in-place ACTV aliases, are conv layers with > 4 input channels (C <= 4
-// layers may run SIMT kernels) and FC layers. Max-pool backward locates the
-// max by equality of X and Y, so pool inputs and outputs stay lossless.
+// layers may run SIMT kernels) and FC layers. A max-pool's backward routes
+// dY by the window maximum of its input X, so pool inputs stay lossless;
+// pool outputs qualify (the pool backward recomputes the maximum from X and
+// does not read Y, elementwise.cu).
 bool Session::tf32_exact_ok(int owner) const {
-  if (o_.precise || (g_.at(owner).kind != Kind::Conv && g_.at(owner).kind != Kind::Fc)) return false;
+  const Kind k = g_.at(owner).kind;
+  if (o_.precise || (k != Kind::Conv && k != Kind::Fc && k != Kind::Pool)) return false;
   std::vector<int> todo(g_.users(owner).begin(), g_.users(owner).end());
   while (!todo.empty()) {
     const int u = todo.back();

@@ -187,11 +187,15 @@ def test_wgrad_split_k_large_reduction():
     _close(dw, wr.grad.permute(0, 2, 3, 1))
 
 
-@pytest.mark.parametrize("window,stride,segs", [(3, 2, [64]), (3, 2, [16, 8]), (3, 2, [3]), (2, 2, [16, 8]), (2, 2, [3]),
-                                               (2, 2, [64])])
-def test_maxpool(window, stride, segs):
+@pytest.mark.parametrize("window,stride,segs,h", [(3, 2, [64], 13), (3, 2, [16, 8], 13), (3, 2, [3], 13),
+                                                 (2, 2, [16, 8], 13), (2, 2, [3], 13), (2, 2, [64], 13),
+                                                 (2, 2, [64], 14), (3, 3, [8], 12)])
+def test_maxpool(window, stride, segs, h):
+    """Forward and backward against torch (ties from ReLU zeros on purpose).
+    The backward gets a NaN-filled Y: the kernels recompute each window's
+    maximum from X and must not read it."""
     dev = _dev()
-    n, h, w = 2, 13, 13
+    n, w = 2, h
     g = torch.Generator().manual_seed(3)
     # ties on purpose: relu'd inputs have many zeros
     xs = [torch.relu(torch.randn(n, h, w, c, generator=g)).to(dev) for c in segs]
@@ -207,6 +211,7 @@ def test_maxpool(window, stride, segs):
     dy = torch.randn(n, ho, wo, ct, generator=g).to(dev)
     dxs = [torch.full_like(t, float("nan")) for t in xs]
     d2 = _desc(n, h, w, xs, segs, 0, 1, 1, 0, dxs)
+    y.fill_(float("nan"))
     L.call("vdnn_kernel_maxpool_bwd", C.byref(d2), window, stride, C.c_void_p(y.data_ptr()),
            C.c_void_p(dy.data_ptr()), None)
     torch.cuda.synchronize()
