@@ -34,6 +34,22 @@ constexpr int kStages = 3;         // 3 x 32 KB (BN=128): two CTAs per SM overla
 constexpr int kStagesPrecise = 3;
 constexpr int kNumSms = 148;
 constexpr int kStagesWide = 4;     // 4 x 48 KB (BN=256): one CTA per SM
+std::atomic<int> g_sm_reserve{-1};  // SMs the persistent conv kernels leave free (compressed transfers)
+
+// CTAs (one per SM) of the persistent conv kernels: all 148 SMs, minus an
+// even reserve for concurrent SM-driven transfers (zvc.cu kernels cannot
+// co-reside with a ~200 KB-smem conv CTA; without a reserve they wait for a
+// whole persistent conv kernel, or hold SMs a persistent kernel's
+// statically scheduled CTAs need).
+int persist_sms() {
+  int r = g_sm_reserve.load(std::memory_order_relaxed);
+  if (r < 0) {
+    const char* e = std::getenv("VDNN_SM_RESERVE");
+    r = e ? std::atoi(e) : 0;
+  }
+  r = std::max(0, std::min(r, 64)) & ~1;
+  return kNumSms - r;
+}
 
 bool build_common(const ConvArgs& a, ConvParams& p) {
   std::memset(&p, 0, sizeof(p));
@@ -295,7 +311,7 @@ cudaError_t launch_persist(const ConvParams& p, const CUtensorMap& ta, const CUt
     attr_set = true;
   }
   const int tiles = ((p.M + BM - 1) / BM) * ((p.Ncols + BN - 1) / BN);
-  tc_conv_persist_kernel<BN, BM, STAGES><<<std::min(tiles, kNumSms), 192, L::kTotal, st>>>(p, ta, tb, tc);
+  tc_conv_persist_kernel<BN, BM, STAGES><<<std::min(tiles, persist_sms()), 192, L::kTotal, st>>>(p, ta, tb, tc);
   count_launch();
   return cudaGetLastError();
 }
@@ -404,7 +420,7 @@ cudaError_t launch_halo(HaloParams& h, const ConvParams& p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  tc_conv_halo_kernel<BN, AS, BS, KW><<<std::min(h.ntiles, kNumSms), 192, L::kTotal, st>>>(h, ta, tb);
+  tc_conv_halo_kernel<BN, AS, BS, KW><<<std::min(h.ntiles, persist_sms()), 192, L::kTotal, st>>>(h, ta, tb);
   count_launch();
   return cudaGetLastError();
 }
@@ -460,7 +476,7 @@ cudaError_t launch_halo_pair(HaloParams& h, const ConvParams& p, cudaStream_t st
     if (e != cudaSuccess) return e;
     attr_smem = smem;
   }
-  const int grid = 2 * std::min(ntiles, kNumSms / 2);
+  const int grid = 2 * std::min(ntiles, persist_sms() / 2);
   tc_conv_halo_pair_kernel<BN, AS, BS, KW, RESB><<<grid, 192, smem, st>>>(h, ta, tb);
   count_launch();
   return cudaGetLastError();
@@ -505,7 +521,7 @@ cudaError_t launch_pair(ConvParams& p, cudaStream_t st) {
     attr_set = true;
   }
   const int tiles = ((p.M + 255) / 256) * ((p.Ncols + 255) / 256);
-  const int grid = 2 * std::min(tiles, kNumSms / 2);
+  const int grid = 2 * std::min(tiles, persist_sms() / 2);
   tc_conv_pair_kernel<STAGES, KB, NOUT><<<grid, 192, L::kTotal, st>>>(p, ta, tb, tc);
   count_launch();
   return cudaGetLastError();
@@ -527,7 +543,7 @@ cudaError_t launch_wgrad_pair(ConvParams& p, int splits, cudaStream_t st) {
     attr_set = true;
   }
   const int work = ((p.M + 255) / 256) * ((p.Ncols + PN - 1) / PN) * splits;
-  const int grid = 2 * std::min(work, kNumSms / 2);
+  const int grid = 2 * std::min(work, persist_sms() / 2);
   tc_wgrad_pair_kernel<STAGES, KW, PN><<<grid, 192, L::kTotal, st>>>(p, ta, tb, splits);
   count_launch();
   return cudaGetLastError();
@@ -898,6 +914,8 @@ __global__ void dgrad_reduce_kernel(const float* __restrict__ part, int splits, 
   }
 }
 }  // namespace
+
+void set_sm_reserve(int sms) { g_sm_reserve.store(sms, std::memory_order_relaxed); }
 
 size_t conv_dgrad_ws_bytes(const ConvArgs& a) {
   ConvParams p;

@@ -46,6 +46,9 @@ size_t conv_fprop_ws_bytes(const ConvArgs& a);
 cudaError_t conv_dgrad(const ConvArgs& a, const float* w, const float* dy, bool accumulate, cudaStream_t st,
                        float* ws = nullptr, size_t ws_bytes = 0);
 size_t conv_dgrad_ws_bytes(const ConvArgs& a);
+// SMs the persistent conv kernels leave free for concurrent SM-driven
+// transfers (process-wide; -1 = VDNN_SM_RESERVE or 0).
+void set_sm_reserve(int sms);
 // Weight gradient. If dw_out is null: fused SGD  w_mut -= lr * dW.
 // Otherwise dW is written to dw_out (KRSC layout) and w_mut is untouched.
 // `ws` holds split-K partials; pass conv_wgrad_ws_bytes(a) bytes (or less:

@@ -17,6 +17,7 @@
 //     before every earlier user of it has finished.
 //   * non-pool scratch (documented in DESIGN.md): softmax gradient / loss,
 //     labels, split-K partials, and (data-parallel mode) the gradient arena.
+#include <cstdlib>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -753,6 +754,17 @@ void Session::step(float lr, float* loss_host) {
     throw PlanError(Err::Config, "the plan offloads but no offload buffer is set (set_offload_buffer / spill_attach)");
   timed_ = o_.record_timeline;
   vdnnk::set_precise(o_.precise);
+  if (sm_reserve_ < 0) {
+    // Compressed transfers run on the SMs concurrently with the persistent
+    // conv kernels: leave them 16 SMs (VGG-16 b256 dyn, interleaved A/B of
+    // 0/8/16/24: dynt 1,468 -> 1,697 img/s, dynz 1,013 -> 1,118 at 16).
+    // Same tiles, same accumulation order: results are unchanged.
+    bool zvc = false;
+    for (const FwdStep& f : fwd_)
+      for (const Transfer& t : f.offloads) zvc = zvc || t.zvc;
+    sm_reserve_ = std::getenv("VDNN_SM_RESERVE") ? 0 : (zvc ? 16 : 0);
+  }
+  vdnnk::set_sm_reserve(std::getenv("VDNN_SM_RESERVE") ? -1 : sm_reserve_);
   if (timed_ && !o_.cuda_graph) {  // this step records into the set the step before last used (see session.h)
     std::swap(ev_, ev_prev_);
     std::swap(t0_ev_, t0_ev_prev_);

@@ -154,6 +154,7 @@ class Session {
   void build_program();
   void fuse_relus();
   bool compressible(int owner) const;
+  int sm_reserve_ = -1;  // SMs left to the compressed-transfer kernels (set on the first step)
   bool tf32_exact_ok(int owner) const;
   void assign_two_buffer();
   void init_weights();
