@@ -37,3 +37,25 @@ def test_errors_are_status_codes_not_crashes():
     assert b"unknown network preset" in lib.vdnn_last_error()
     assert lib.vdnn_extend_vgg(150, C.c_uint64(4), C.byref(g)) == L.INVALID_DEPTH
     assert lib.vdnn_version().startswith(b"vdnn-b200")
+
+
+def test_session_option_validation_before_any_device_work():
+    """Bad transfer-mode options are rejected up front (no GPU needed): the
+    Python mirror raises ValueError, the C ABI returns a CONFIG status."""
+    import pytest
+    import paper_1602_08124_b200 as V
+    g = V.build_preset("alexnet", 4)
+    d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, V.CostModel())
+    with pytest.raises(ValueError):
+        V.Session(g, d, compress_offload="bf16")
+    with pytest.raises(ValueError):
+        V.Session(g, d, offload_target="nvme")
+    opt = L.SessionOptions()
+    L.lib().vdnn_session_options_default(C.byref(opt))
+    assert opt.compress_offload == 0
+    opt.compress_offload = 3
+    s = C.c_void_p()
+    dd = d._handle(g)
+    cm = V.CostModel()._c()
+    st = L.lib().vdnn_session_create(g.handle, dd.h, C.byref(cm), C.c_uint64(1 << 30), C.byref(opt), C.byref(s))
+    assert st != 0 and b"compress_offload" in L.lib().vdnn_last_error()
