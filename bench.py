@@ -416,7 +416,7 @@ def main():
     ap.add_argument("--policies", default=None,
                     help="dyn/all/conv/none; a trailing z = same plan with compressed offload, t = compressed with "
                          "TF32-exact values where only TF32 contractions read the map, a trailing p = "
-                         "offload into a peer GPU's HBM (N > 1). Default: dyn,dynz,all,conv,none (+ dynp at N > 1)")
+                         "offload into a peer GPU's HBM (N > 1). Default: dyn,dynz,dynt,all,conv,none (+ dynp at N > 1)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--precise", action="store_true", help="3xTF32 fp32-accurate contractions")
     ap.add_argument("--cpu-sample-batch", type=int, default=2)
@@ -452,7 +452,7 @@ def main():
     tf32_peak, peak_note = measured_tf32_peak(peaks, peaks_src)
 
     if args.policies is None:
-        args.policies = "dyn,dynz,dynt,all,conv,none" if world == 1 else "dyn,dynp,dynz,all,conv,none"
+        args.policies = "dyn,dynz,dynt,all,conv,none" if world == 1 else "dyn,dynp,dynz,dynt,all,conv,none"
     results = {}
     for p in [x for x in args.policies.split(",") if x]:
         results[p] = run_policy(p, args, device, world, peaks, want_e2e=(p == "dyn"), sampler_cls=ClockSampler)
