@@ -378,3 +378,57 @@ def test_cuda_graph_steps_are_bit_identical(compress):
         assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
     assert outs[0][2] == outs[1][2]
     assert outs[0][3] == outs[1][3]
+
+
+def test_vgg16_b256_headline_plan_full_size():
+    """BASELINE config 4 at full size: VGG-16 b256 under the 12 GiB budget.
+    The dyn decision and schedule are the reference's (vdnn-conv+greedy,
+    signature 2188dd2e41bf52e2 in tests/golden/vgg16_b256.json); the measured
+    event log of the real run keeps every planned pool offset and replays
+    clean; one training step with copy-engine transfers, with TF32-exact
+    compressed transfers, and without offload (32.7 GB pool) gives the same
+    loss and the same updated weights bit for bit (size-independent
+    properties at the size the headline is quoted on)."""
+    _need_gpu()
+    import gc
+    import hashlib
+    import torch
+    g = V.build_preset("vgg16", 256)
+    cm = V.CostModel()
+    cap = 12884901888
+    sel = V.dynamic_select(g, cap, cm)
+    d = sel.decision
+    assert d.label == "vdnn-conv+greedy"
+
+    def run(decision, capacity, **kw):
+        s = V.Session(g, decision, cm, capacity, **kw)
+        s.synthetic_batch(7)
+        loss = s.step(LR)
+        h = hashlib.sha256()
+        for l in g.layers():
+            if l.kind in (V.LayerKind.Conv, V.LayerKind.Fc):
+                h.update(np.ascontiguousarray(s.get_weights(l.id)).tobytes())
+        return s, loss, h.hexdigest()
+
+    s, loss_dyn, w_dyn = run(d, cap, record_timeline=True)
+    assert s.plan.signature() == "2188dd2e41bf52e2"
+    assert s.arena_info()["arena_bytes"] <= cap
+    m = s.measured_report()
+    assert m.offload_traffic_bytes == s.plan.offload_traffic_bytes == 10635706368
+    assert [e.offset for e in m.events] == [e.offset for e in s.plan.events]
+    assert V.replay_check(m, g, d, cap) == []
+    del s, m
+    gc.collect()
+    s, loss_t, w_t = run(d, cap, compress_offload="tf32")
+    st = s.transfer_stats()
+    assert st["offload_wire"] < 0.4 * st["offload_planned"]
+    del s
+    gc.collect()
+    free, _ = torch.cuda.mem_get_info()
+    db = V.static_decision(V.PolicyKind.Baseline, V.AlgoMode.PerfOptimal, g, cm)
+    s, loss_b, w_b = run(db, int(free - (6 << 30)))
+    del s
+    gc.collect()
+    assert np.isfinite(loss_dyn)
+    assert loss_dyn == loss_t == loss_b
+    assert w_dyn == w_t == w_b
