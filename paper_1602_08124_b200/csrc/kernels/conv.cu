@@ -986,10 +986,24 @@ bool halo_wg_params(const ConvParams& p, HaloWgParams& h, int& bn, size_t& smem)
   h.G = (nblk + h.ngroups - 1) / h.ngroups;
   h.nrows = h.N * h.Hout;
   int splits = std::max(1, kNumSms / h.ngroups);
+  // CTA pair (tc_conv_halo_pair.cuh): 64 channels, the blocks split evenly
+  // between the two CTAs, one row range per pair
+  static const bool pair_wg = [] {
+    const char* e = std::getenv("VDNN_HALO_PAIR_WGRAD");
+    return !e || std::atoi(e) != 0;
+  }();
+  h.pair = (pair_wg && halo_pair_enabled() && p.Cout == 64 && nblk % 2 == 0 && nblk / 2 * 64 <= 512) ? 1 : 0;
+  if (h.pair) {
+    // a fixed item count (4 per pair of a full grid): partials and reduce
+    // order do not depend on the grid an SM reserve leaves
+    h.ngroups = 1;
+    h.G = nblk / 2;
+    splits = 4 * (kNumSms / 2);
+  }
   h.rows_per = (h.nrows + splits - 1) / splits;
   h.M = p.kh * p.kw * h.nck * 32;
   h.a_slot = halo_wg_a_slot(h.Kp);
-  h.b_slot = halo_wg_b_slot(h.Kp, bn);
+  h.b_slot = halo_wg_b_slot(h.Kp, h.pair ? 32 : bn);
   h.BS = 2;
   const size_t fixed = 1024 + 256 + static_cast<size_t>(h.BS) * h.b_slot;
   if (fixed + 2 * static_cast<size_t>(h.a_slot) > kSmemLimit) return false;
@@ -1021,6 +1035,19 @@ cudaError_t launch_halo_wgrad(HaloWgParams& h, size_t smem, const ConvParams& p,
     const cuuint32_t box[4] = {32, static_cast<cuuint32_t>(h.P), 1, 1};
     if (!encode_tiled(&tdy, p.dy, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
       return cudaErrorNotSupported;
+  }
+  if (h.pair) {
+    static bool pattr = false;
+    if (!pattr) {
+      cudaError_t e = cudaFuncSetAttribute(tc_wgrad_halo_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(kSmemLimit));
+      if (e != cudaSuccess) return e;
+      pattr = true;
+    }
+    const int items = halo_wg_splits(h);
+    tc_wgrad_halo_pair_kernel<<<2 * std::min(items, persist_sms() / 2), 192, smem, st>>>(h, tx, tdy, items);
+    count_launch();
+    return cudaGetLastError();
   }
   static size_t attr = 0;
   if (smem > attr) {

@@ -298,6 +298,7 @@ struct HaloWgParams {
   int N, H, W, C, Cout, kh, kw, pad, P, Kp, Hout, Wout, nck;
   int G, ngroups, rows_per, nrows, M;
   int AS, BS;              // ring depths (A: one padded input row per (r, c); B: one dY row)
+  int pair;                // 1: tc_wgrad_halo_pair_kernel (G blocks per CTA, splits = pairs)
   uint32_t a_slot, b_slot; // bytes per slot (1024-aligned)
   float* part;             // [splits][Cout][M]
 };

@@ -293,3 +293,201 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 }
 
 }  // namespace vdnnk
+
+namespace vdnnk {
+
+// Halo WGRAD (tc_conv_halo.cuh) on a CTA pair, 64 output channels: a work
+// item is a range of rows; CTA rank r of the pair owns (r, c) blocks
+// g0 = r*G .. (its 128 M rows per MMA: the four shifted views of its staged
+// input row) and stages dY channels 32r..32r+31 of each row (its half of B).
+// One M256 x N64 pair MMA per K step covers two blocks: per SM the tensor
+// core reads 4 KB of A + 1 KB of B instead of 4 + 2 KB (the single-CTA
+// kernel is operand-read bound: ncu TC wavefronts 83%, tensor pipe 55%).
+// Persistent over a FIXED number of items (the split-K partials and their
+// reduce order do not depend on how many SMs the grid got, e.g. with an SM
+// reserve for compressed transfers), two TMEM accumulator sets so item i's
+// epilogue overlaps item i+1's main loop. Both CTAs walk the same items and
+// G blocks per row in lockstep; loads complete on the leader's barriers,
+// releases are multicast commits (see tc_conv_pair.cuh).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    tc_wgrad_halo_pair_kernel(const __grid_constant__ HaloWgParams p, const __grid_constant__ CUtensorMap tma_x,
+                              const __grid_constant__ CUtensorMap tma_dy, int nitems) {
+  constexpr int BN = 64;
+  const int AS = p.AS, BS = p.BS;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bslots = base + AS * p.a_slot;
+  const uint32_t bars = bslots + BS * p.b_slot;
+  auto full_a = [&](int s) { return bars + 8u * s; };
+  auto empty_a = [&](int s) { return bars + 8u * (AS + s); };
+  auto full_b = [&](int s) { return bars + 8u * (2 * AS + s); };
+  auto empty_b = [&](int s) { return bars + 8u * (2 * AS + BS + s); };
+  auto tfull = [&](int a) { return bars + 8u * (2 * AS + 2 * BS + a); };
+  auto tempty = [&](int a) { return bars + 8u * (2 * AS + 2 * BS + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * AS + 2 * BS + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = static_cast<int>(blockIdx.x >> 1), npairs = static_cast<int>(gridDim.x >> 1);
+  const int G = p.G;
+  const int g0 = static_cast<int>(rank) * G;
+  int acc_cols = 32;
+  while (acc_cols < G * BN) acc_cols <<= 1;
+  const int tcols = 2 * acc_cols;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(full_a(s), 1);
+      mbar_init(empty_a(s), 1);
+    }
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(full_b(s), 1);
+      mbar_init(empty_b(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // rows the boxes never write: B rows [P, Kp) must be 0, A rows [P, Kp + 8) finite
+  for (int s = 0; s < AS; ++s)
+    for (uint32_t o = p.P * 128 + threadIdx.x * 16; o < p.a_slot; o += blockDim.x * 16)
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + s * p.a_slot + o), "r"(0) : "memory");
+  for (int s = 0; s < BS; ++s)
+    for (int o = p.P * 128 + threadIdx.x * 16; o < p.Kp * 128; o += blockDim.x * 16)
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(bslots + s * p.b_slot + o), "r"(0) : "memory");
+  fence_proxy_async();
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  if (warp == 5) {
+    // ---------------- TMA producer (this CTA's dY half and input rows) ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_x) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_dy) : "memory");
+      int sa = 0, sb = 0;
+      uint32_t pha = 1, phb = 1;
+      const uint32_t bytes = static_cast<uint32_t>(p.P) * 128;
+      for (int item = pair; item < nitems; item += npairs) {
+        const int row0 = item * p.rows_per, row1 = min(row0 + p.rows_per, p.nrows);
+        for (int row = row0; row < row1; ++row) {
+          const int n = row / p.Hout, y = row - n * p.Hout;
+          mbar_wait(empty_b(sb), phb);
+          if (rank == 0) mbar_expect_tx(full_b(sb), 2 * bytes);
+          tma_load_4d_pair(bslots + sb * p.b_slot, &tma_dy, map_to_rank(full_b(sb), 0),
+                           static_cast<int>(rank) * 32, 0, y, n);
+          if (++sb == BS) {
+            sb = 0;
+            phb ^= 1;
+          }
+          for (int j = 0; j < G; ++j) {
+            const int blk = g0 + j, r = blk / p.nck, c = blk - r * p.nck;
+            mbar_wait(empty_a(sa), pha);
+            if (rank == 0) mbar_expect_tx(full_a(sa), 2 * bytes);
+            tma_load_4d_pair(base + sa * p.a_slot, &tma_x, map_to_rank(full_a(sa), 0), c * 32, -p.pad,
+                             y + r - p.pad, n);
+            if (++sa == AS) {
+              sa = 0;
+              pha ^= 1;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    // ---------------- MMA issuer (leader) ----------------
+    if (rank == 0) {
+      const uint32_t idesc = (make_idesc_tf32(BN, true, true) & ~(0x1Fu << 24)) | ((256u >> 4) << 24);
+      const bool leader = elect_one();
+      const int ksteps = p.Kp / 8;
+      const uint32_t lbo_b = static_cast<uint32_t>(p.Kp) * 128;
+      int sa = 0, sb = 0, lt = 0;
+      uint32_t pha = 0, phb = 0;
+      for (int item = pair; item < nitems; item += npairs, ++lt) {
+        const int acc = lt & 1;
+        if (lt >= 2) mbar_wait(tempty(acc), ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem + acc * acc_cols;
+        const int nrows = min(p.rows_per, p.nrows - item * p.rows_per);
+        for (int i = 0; i < nrows; ++i) {
+          mbar_wait(full_b(sb), phb);
+          tc_fence_after();
+          const uint32_t b0 = bslots + sb * p.b_slot;
+          for (int j = 0; j < G; ++j) {
+            mbar_wait(full_a(sa), pha);
+            tc_fence_after();
+            const uint32_t a0 = base + sa * p.a_slot;
+            if (leader) {
+              for (int kk = 0; kk < ksteps; ++kk)
+                tc_mma_tf32_pair(d0 + j * BN, make_sdesc(a0 + kk * 1024, 128, 512, kSw128Base32),
+                                 make_sdesc(b0 + kk * 1024, lbo_b, 512, kSw128Base32), idesc,
+                                 (i > 0 || kk > 0) ? 1u : 0u);
+              tc_commit_pair(empty_a(sa));
+            }
+            __syncwarp();
+            if (++sa == AS) {
+              sa = 0;
+              pha ^= 1;
+            }
+          }
+          if (leader) tc_commit_pair(empty_b(sb));
+          __syncwarp();
+          if (++sb == BS) {
+            sb = 0;
+            phb ^= 1;
+          }
+        }
+        if (leader) tc_commit_pair(tfull(acc));
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue: warp w = shift s, lane = ci ----------------
+    const uint32_t lt0 = map_to_rank(tempty(0), 0), lt1 = map_to_rank(tempty(1), 0);
+    const int s = warp;
+    int lt = 0;
+    for (int item = pair; item < nitems; item += npairs, ++lt) {
+      const int acc = lt & 1;
+      mbar_wait_sleep(tfull(acc), (lt >> 1) & 1);
+      tc_fence_after();
+      float* dst = p.part + static_cast<int64_t>(item) * p.Cout * p.M;
+      for (int j = 0; j < G; ++j) {
+        const int blk = g0 + j, r = blk / p.nck, c = blk - r * p.nck;
+        const int m = ((r * p.kw + s) * p.nck + c) * 32 + lane;
+        for (int cg = 0; cg < BN / 32; ++cg) {
+          float v[32];
+          tmem_ld32(tmem + acc * acc_cols + j * BN + cg * 32 + (static_cast<uint32_t>(warp * 32) << 16), v);
+          if (j == G - 1 && cg == BN / 32 - 1) {
+            // last TMEM read of this accumulator set: release it to the leader's MMA warp
+            tc_fence_before();
+            mbar_arrive_cluster(acc ? lt1 : lt0);
+          }
+          if (s >= p.kw) continue;  // the fourth shifted view (taps past the kernel)
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (cg * 32 + q < p.Cout) dst[static_cast<int64_t>(cg * 32 + q) * p.M + m] = v[q];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
+  }
+}
+
+}  // namespace vdnnk
