@@ -145,6 +145,15 @@ def _conv_case(case):
         for t, c in zip(dxs, segs):
             _close(t, gx[..., off:off + c])
             off += c
+        dws = L.lib().vdnn_kernel_conv_dgrad_ws_bytes(C.byref(d2))
+        if dws > 0:  # split-K dgrad (few dX tiles, long reduction)
+            wsd = torch.empty(dws // 4, device=dev)
+            dx2 = [torch.full_like(t, float("nan")) for t in xs]
+            d3 = _desc(n, h, w, xs, segs, cout, k, stride, pad, dx2)
+            L.call("vdnn_kernel_conv_dgrad_ws", C.byref(d3), C.c_void_p(wt.data_ptr()), C.c_void_p(dy.data_ptr()),
+                   0, C.c_void_p(wsd.data_ptr()), C.c_size_t(dws), None)
+            torch.cuda.synchronize()
+            _close(dx2[0], gx)
     # wgrad with dW output (no SGD), with and without split-K workspace
     for use_ws in (False, True):
         dw = torch.full_like(wt, float("nan"))
