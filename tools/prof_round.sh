@@ -7,7 +7,7 @@ timeout 600 python bench.py > gpurun_out/bench_${LABEL}.json 2> gpurun_out/bench
 for net in alexnet overfeat inception_toy; do
   timeout 300 python bench.py --net $net --batch 128 --policies dyn,all,conv,none --no-cpu-baseline > gpurun_out/bench_$net.json 2> gpurun_out/bench_$net.err
 done
-timeout 900 python bench.py --extra 400 --batch 32 --policies dyn,none --steps 2 --no-cpu-baseline > gpurun_out/bench_vgg416.json 2> gpurun_out/bench_vgg416.err
+timeout 1200 python bench.py --extra 400 --batch 32 --policies dyn,dynt,none --steps 2 --no-cpu-baseline > gpurun_out/bench_vgg416.json 2> gpurun_out/bench_vgg416.err
 python tools/prof_layers.py vgg16 256 none > gpurun_out/layers_none.txt 2>&1
 python tools/prof_layers.py alexnet 128 none > gpurun_out/layers_alexnet.txt 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/${LABEL}_launches_dyn.csv python bench.py --policies dyn --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
