@@ -478,7 +478,7 @@ def main():
     }
     if head.get("_conv_ms"):
         ach = head["_flops"] / (head["_conv_ms"] * 1e-3) / 1e12
-        line["roofline"] = {"bound": "tensor", "kernel": "tcgen05 conv engine (tc_conv / tc_conv_halo / tc_conv_persist / c3tc kernels: every conv+FC fprop, dgrad, wgrad launch)",
+        line["roofline"] = {"bound": "tensor", "kernel": "tcgen05 conv engine (tc_conv_pair / tc_wgrad_pair / tc_conv_halo_pair / tc_wgrad_halo_pair / tc_conv / tc_conv_persist / c3tc kernels: every conv+FC fprop, dgrad, wgrad launch)",
                             "achieved": round(ach, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
                             "frac": round(ach / tf32_peak, 4), "traffic": conv_traffic(),
                             "peak_note": peak_note,
