@@ -242,3 +242,28 @@ def test_bench_two_ranks_same_device_peer_exchange():
     # the same plan offloading into the ring neighbour's HBM
     assert line["policies"]["dynp"]["signature"] == line["policies"]["dyn"]["signature"]
     assert line["peer_hbm_offload"]["images_per_s"] > 0
+
+
+def test_bench_two_ranks_compressed_transfers_bit_identical():
+    """N>1 with the compressed transfer modes (in bench.py's multi-GPU default
+    policies): under a budget that makes vDNN_dyn offload, copy-engine,
+    lossless-compressed and TF32-exact transfers give the same loss on 2 ranks
+    with the fused peer gradient exchange."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VDNN_BENCH_SAME_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--net", "alexnet", "--batch", "32", "--capacity", "271494988", "--policies", "dyn,dynz,dynt",
+           "--steps", "1", "--warmup", "3", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    pol = line["policies"]
+    assert pol["dyn"]["offload_bytes_per_iter"] > 0
+    assert pol["dyn"]["loss"] == pol["dynz"]["loss"] == pol["dynt"]["loss"]
+    assert pol["dynt"]["wire_ratio"] < pol["dynz"]["wire_ratio"] < 1.0
