@@ -59,3 +59,17 @@ def test_session_option_validation_before_any_device_work():
     cm = V.CostModel()._c()
     st = L.lib().vdnn_session_create(g.handle, dd.h, C.byref(cm), C.c_uint64(1 << 30), C.byref(opt), C.byref(s))
     assert st != 0 and b"compress_offload" in L.lib().vdnn_last_error()
+
+
+def test_kernel_entry_points_reject_bad_arguments_without_a_device():
+    """The workspace / TF32-exact kernel entry points validate their
+    arguments before touching CUDA: a strided dgrad is UNSUPPORTED, null
+    buffers are INVALID_ARGUMENT."""
+    lib = L.lib()
+    d = L.ConvDesc()
+    d.n, d.h, d.w, d.nseg = 2, 8, 8, 1
+    d.c[0] = 32
+    d.cout, d.kh, d.kw, d.stride, d.pad = 32, 3, 3, 2, 1
+    assert lib.vdnn_kernel_conv_dgrad_ws(C.byref(d), None, None, 0, None, C.c_size_t(0), None) == L.UNSUPPORTED
+    assert lib.vdnn_kernel_zvc_compress_tf32(None, C.c_uint64(4), None, None, None) == L.INVALID_ARGUMENT
+    assert b"null" in lib.vdnn_last_error()
