@@ -243,6 +243,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         torch.distributed.barrier()
     ts0 = s.transfer_stats()
     l0 = V.kernel_launch_count()
+    s.pause_timeline(True)  # no per-op timing events inside the timed region (one more step records them below)
     with sampler_cls(device) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
@@ -257,6 +258,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     ms = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms, world, device=f"cuda:{device}")
     imgs = args.batch * world / (ms * 1e-3)
+    s.pause_timeline(False)
     loss = s.step(args.lr, want_loss=True) if not dp else dp.step(args.lr, True)
 
     # per-layer measured times of that last step
@@ -323,6 +325,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
             if len(pending) > 1:
                 s.wait_loss(pending.pop(0))
 
+        s.pause_timeline(True)
         s.prefetch_batch_ptr(imgs_h.data_ptr(), labs_h.data_ptr())
         for _ in range(2):
             e2e_step()

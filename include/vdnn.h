@@ -292,6 +292,9 @@ vdnn_status vdnn_session_set_weights(vdnn_session* s, int32_t layer, const float
 vdnn_status vdnn_session_step(vdnn_session* s, float lr, float* loss_host);
 /* Forward only (for tests); leaves logits readable via vdnn_session_read_buffer. */
 vdnn_status vdnn_session_synchronize(vdnn_session* s);
+/* record_timeline sessions: 1 = skip the per-op timing events on the following steps (benchmark loops:
+   they cost ~10% on small nets), 0 = record again; reports describe the last step recorded. */
+vdnn_status vdnn_session_pause_timeline(vdnn_session* s, int32_t paused);
 /* Copy a feature buffer (owner layer) or gradient buffer to host as of the last step (debug/tests). */
 vdnn_status vdnn_session_read_feature(vdnn_session* s, int32_t owner, float* host, size_t count);
 /* Measured report of the last step: plan events with CUDA-event timestamps. */

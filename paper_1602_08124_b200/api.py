@@ -842,6 +842,11 @@ class Session:
     def synchronize(self) -> None:
         _call("vdnn_session_synchronize", self.handle)
 
+    def pause_timeline(self, paused: bool = True) -> None:
+        """record_timeline sessions: skip (or resume) the per-op timing events;
+        measured_report / layer_times describe the last step recorded."""
+        _call("vdnn_session_pause_timeline", self.handle, C.c_int32(int(paused)))
+
     def weight_count(self, layer: int) -> int:
         return self.cost.weight_bytes(self.graph, layer) // 4
 

@@ -134,6 +134,12 @@ vdnn_status vdnn_session_step(vdnn_session* s, float lr, float* loss_host) {
     return VDNN_OK;
   });
 }
+vdnn_status vdnn_session_pause_timeline(vdnn_session* s, int32_t paused) {
+  return guard([&] {
+    S(s).pause_timeline(paused != 0);
+    return VDNN_OK;
+  });
+}
 vdnn_status vdnn_session_synchronize(vdnn_session* s) {
   return guard([&] {
     S(s).synchronize();

@@ -752,7 +752,7 @@ void Session::run_bwd(const BwdStep& s, float lr) {
 void Session::step(float lr, float* loss_host) {
   if (host_bytes_ > 0 && !host_)
     throw PlanError(Err::Config, "the plan offloads but no offload buffer is set (set_offload_buffer / spill_attach)");
-  timed_ = o_.record_timeline;
+  timed_ = o_.record_timeline && !timeline_paused_;
   vdnnk::set_precise(o_.precise);
   if (sm_reserve_ < 0) {
     // Compressed transfers run on the SMs concurrently with the persistent

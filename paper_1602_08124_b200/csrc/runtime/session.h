@@ -242,6 +242,13 @@ class Session {
   std::vector<cudaEvent_t> t0_ev_;    // timed step-start events (record_timeline)
   std::vector<cudaEvent_t> xfer_ev_;  // per transfer completion
   bool timed_ = false;
+  bool timeline_paused_ = false;  // record_timeline sessions: skip the per-op events (timed benchmark loops)
+
+ public:
+  // Pause / resume the per-op CUDA events of a record_timeline session; the
+  // measured report and layer times then describe the last step run with
+  // them on.
+  void pause_timeline(bool paused) { timeline_paused_ = paused; }
 };
 
 }  // namespace vdnnrt
