@@ -1,7 +1,8 @@
 """Where is the host link idle in a vDNN_dyn step? From the measured event
 log of one VGG-16 b256 step under 12 GiB: the union of OFFLOAD/PREFETCH
 intervals vs the step, and the compute events that run while no transfer
-is in flight (the exposed compute): python tools/link_idle.py [net] [batch] [capacity]"""
+is in flight (the exposed compute):
+python tools/link_idle.py [net] [batch] [capacity] [compress: 0 | zvc | tf32]"""
 import sys
 
 sys.path.insert(0, ".")
@@ -10,10 +11,12 @@ import paper_1602_08124_b200 as V
 net = sys.argv[1] if len(sys.argv) > 1 else "vgg16"
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 cap = int(sys.argv[3]) if len(sys.argv) > 3 else 12884901888
+comp = sys.argv[4] if len(sys.argv) > 4 else "0"
+comp = {"0": False, "zvc": True, "tf32": "tf32"}[comp]
 g = V.build_preset(net, batch)
 cm = V.CostModel()
 d = V.dynamic_select(g, cap, cm).decision
-s = V.Session(g, d, cm, cap, record_timeline=True)
+s = V.Session(g, d, cm, cap, record_timeline=True, compress_offload=comp)
 s.synthetic_batch(1)
 for _ in range(3):
     s.step(0.01, want_loss=False)
