@@ -299,19 +299,19 @@ cudaError_t launch_bn(const ConvParams& p, const CUtensorMap& ta, const CUtensor
   return cudaGetLastError();
 }
 
-template <int BN, int BM, int STAGES>
+template <int BN, int BM, int STAGES, bool WG = false>
 cudaError_t launch_persist(const ConvParams& p, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                            cudaStream_t st) {
   using L = PersistSmem<BN, BM, STAGES>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_conv_persist_kernel<BN, BM, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_persist_kernel<BN, BM, STAGES, WG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int tiles = ((p.M + BM - 1) / BM) * ((p.Ncols + BN - 1) / BN);
-  tc_conv_persist_kernel<BN, BM, STAGES><<<std::min(tiles, persist_sms()), 192, L::kTotal, st>>>(p, ta, tb, tc);
+  tc_conv_persist_kernel<BN, BM, STAGES, WG><<<std::min(tiles, persist_sms()), 192, L::kTotal, st>>>(p, ta, tb, tc);
   count_launch();
   return cudaGetLastError();
 }
@@ -330,6 +330,19 @@ bool use_persist(const ConvParams& p) {
   if (mode == 0) return false;
   if (mode == 2) return true;
   return p.kind == kFprop && p.Ncols > 64 && p.Ncols <= 128;
+}
+
+// Persistent WGRAD (tc_conv_persist.cuh, WG) for short reductions: at most
+// 32 K blocks (FC layers: K = batch) over at least two waves of 256 x 128
+// tiles. VDNN_PERSIST_WGRAD=0 disables.
+bool persist_wgrad(const ConvParams& p) {
+  static const bool on = [] {
+    const char* e = std::getenv("VDNN_PERSIST_WGRAD");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || g_precise || g_no_tma || p.Ncols < 128 || p.kblocks > 32) return false;
+  const int64_t tiles = static_cast<int64_t>((p.M + 255) / 256) * ((p.Ncols + 127) / 128);
+  return tiles >= 2 * kNumSms;
 }
 
 // Halo-reuse kernel (tc_conv_halo.cuh) for stride-1 k x k (k >= 3) FPROP /
@@ -627,6 +640,29 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
     p.wkw = kBK;
     p.kblocks *= 2;
     p.kb_per_split *= 2;
+  }
+  if (p.kind == kWgrad && splits == 1 && persist_wgrad(p) && p.wkw == kBK && p.epi != kEpiPartial) {
+    // short-reduction wgrad (FC layers): persistent, SGD epilogue overlapped;
+    // for FC layers the SGD goes through TMA boxes of W (tma_c)
+    if (make_maps<128>(p, &ta, &tb, &tc)) {
+      p.sgd_tma = 0;
+      static const bool sgd_tma = [] {
+        const char* e = std::getenv("VDNN_SGD_TMA");
+        return !e || std::atoi(e) != 0;
+      }();
+      if (sgd_tma && p.epi == kEpiSgd && p.kh == 1 && p.kw == 1 && p.H == 1 && p.W == 1 && p.nseg == 1 &&
+          p.C % 32 == 0 && p.KK % 4 == 0) {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.KK), static_cast<cuuint64_t>(p.Cout)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.KK) * 4};
+        const cuuint32_t box[2] = {128, 32};
+        if (encode_tiled(&tc, p.w_mut, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE)) p.sgd_tma = 1;
+      }
+      return launch_persist<128, 256, 4, true>(p, ta, tb, tc, st);
+    }
+    std::memset(&ta, 0, sizeof(ta));
+    std::memset(&tb, 0, sizeof(tb));
+    std::memset(&tc, 0, sizeof(tc));
+    p.tma_b_merged = 0;
   }
   if (p.kind != kWgrad && splits == 1 && use_persist(p) && !g_no_tma) {
     if (p.Ncols <= 64) {

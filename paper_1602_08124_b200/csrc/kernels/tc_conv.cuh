@@ -82,6 +82,7 @@ struct ConvParams {
   int splits;                 // split-K fprop: number of partial slabs
   int use_pair;               // wgrad: CTA-pair kernel (tc_conv_pair.cuh)
   int KK;                     // kh*kw*C: weight row length
+  int sgd_tma;                // persistent FC wgrad: SGD epilogue through TMA boxes of W (map in tma_c)
 };
 
 // ------------------------------------------------------------------ PTX ----

@@ -15,6 +15,12 @@
 //
 // smem: [STAGES x (A BM x 128 B | B BN x 128 B)] [2 x 16 KB output boxes] [barriers]
 // TMEM: 2 x (BM/128) x BN fp32 columns (<= 512).
+//
+// WG = true: WGRAD with a short reduction (FC layers: K = batch, 8 K blocks
+// at b256), unsplit. One tile per CTA paid a launch, a pipeline fill and
+// TMEM setup for every 256 x 128 block of weights; here the fused SGD
+// epilogue (w -= lr * dW, the weight read + write that bounds these layers)
+// of tile t overlaps tile t+1's loads and MMAs. Both operands MN-major.
 #pragma once
 
 namespace vdnnk {
@@ -30,7 +36,7 @@ struct PersistSmem {
   static_assert(2 * kAccCols <= 512, "two accumulator sets must fit TMEM");
 };
 
-template <int BN, int BM, int STAGES>
+template <int BN, int BM, int STAGES, bool WG = false>
 __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_constant__ ConvParams p,
                                                                  const __grid_constant__ CUtensorMap tma_a,
                                                                  const __grid_constant__ CUtensorMap tma_b,
@@ -48,6 +54,7 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
   auto tfull_bar = [&](int a) { return bars + 8u * (2 * STAGES + a); };
   auto tempty_bar = [&](int a) { return bars + 8u * (2 * STAGES + 2 + a); };
   const uint32_t tmem_slot = bars + 8u * (2 * STAGES + 4);
+  auto wbar = [&](int b) { return bars + 8u * (2 * STAGES + 5 + b); };  // WG + sgd_tma: W box loads
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntn = (p.Ncols + BN - 1) / BN;
@@ -62,6 +69,7 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), 128);
+      mbar_init(wbar(a), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -101,7 +109,7 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
   } else if (warp == 4) {
     // ---------------- MMA issuer ----------------
     // whole warp in the loop (warp-uniform descriptors), one elected lane issues
-    const uint32_t idesc = make_idesc_tf32(BN, false, p.kind != kFprop);
+    const uint32_t idesc = make_idesc_tf32(BN, WG, p.kind != kFprop);
     const bool b_mn = p.kind != kFprop;
     const bool leader = elect_one();
     int it = 0, lt = 0;
@@ -119,7 +127,8 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
         if (leader) {
 #pragma unroll
           for (int kk = 0; kk < kBK / 8; ++kk) {
-            const uint64_t ad = make_sdesc(sa + kk * 32, 16, 1024, kSw128);
+            const uint64_t ad = WG ? make_sdesc(sa + kk * 1024, kBK * 128, 512, kSw128Base32)
+                                   : make_sdesc(sa + kk * 32, 16, 1024, kSw128);
             const uint64_t bd = b_mn ? make_sdesc(sb + kk * 1024, 4096, 512, kSw128Base32)
                                      : make_sdesc(sb + kk * 32, 16, 1024, kSw128);
 #pragma unroll
@@ -156,6 +165,55 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
             // last TMEM read of this accumulator set: hand it back to the MMA warp
             tc_fence_before();
             mbar_arrive(tempty_bar(acc));
+          }
+          if constexpr (WG) {
+            if (p.sgd_tma) {
+              // FC layer: W[nb .. nb+31][m0 + h*128 .. +127] as one TMA box
+              // (16 KB, unswizzled [32 co][128 k]); SGD in shared memory, TMA
+              // store back -- the weight traffic runs asynchronously instead
+              // of 32 dependent loads per thread
+              const int b = box & 1;
+              const uint32_t ob = obuf + b * 16384;
+              if (threadIdx.x == 0) {
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // box b's last store read it
+                mbar_expect_tx(wbar(b), 16384);
+                tma_load_2d(ob, &tma_c, wbar(b), m0 + h * kBM, nb);
+              }
+              mbar_wait(wbar(b), (box >> 1) & 1);
+              const uint32_t col = ob + row * 4;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                float w;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(w) : "r"(col + i * 512) : "memory");
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(col + i * 512), "f"(w - p.lr * v[i]) : "memory");
+              }
+              fence_proxy_async();
+              asm volatile("bar.sync 1, 128;" ::: "memory");
+              if (threadIdx.x == 0) {
+                tma_store_2d(&tma_c, ob, m0 + h * kBM, nb, false);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              }
+              continue;
+            }
+            // row m = weight column, v[i] = dW of output channel nb + i
+            bool valid;
+            const int widx = wgrad_widx(p, m, valid);
+            if (valid) {
+              if (p.epi == kEpiSgd) {
+                float* wcol = p.w_mut + static_cast<int64_t>(nb) * p.KK + widx;
+                float wv[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) wv[i] = (nb + i < p.Cout) ? wcol[static_cast<int64_t>(i) * p.KK] : 0.f;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (nb + i < p.Cout) wcol[static_cast<int64_t>(i) * p.KK] = wv[i] - p.lr * v[i];
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (nb + i < p.Cout) p.out[static_cast<int64_t>(nb + i) * p.KK + widx] = v[i];
+              }
+            }
+            continue;
           }
           if (p.kind == kFprop && p.bias) {
 #pragma unroll
@@ -201,7 +259,7 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
         }
       }
     }
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if ((!WG || p.sgd_tma) && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
