@@ -302,7 +302,7 @@ cudaError_t launch_bn(const ConvParams& p, const CUtensorMap& ta, const CUtensor
 template <int BN, int BM, int STAGES, bool WG = false>
 cudaError_t launch_persist(const ConvParams& p, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                            cudaStream_t st) {
-  using L = PersistSmem<BN, BM, STAGES>;
+  using L = PersistSmem<BN, BM, STAGES, WG ? 4 : 2>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(tc_conv_persist_kernel<BN, BM, STAGES, WG>,
@@ -657,7 +657,7 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
         const cuuint32_t box[2] = {128, 32};
         if (encode_tiled(&tc, p.w_mut, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE)) p.sgd_tma = 1;
       }
-      return launch_persist<128, 256, 4, true>(p, ta, tb, tc, st);
+      return launch_persist<128, 256, 3, true>(p, ta, tb, tc, st);
     }
     std::memset(&ta, 0, sizeof(ta));
     std::memset(&tb, 0, sizeof(tb));

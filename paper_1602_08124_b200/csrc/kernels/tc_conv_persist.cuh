@@ -25,12 +25,12 @@
 
 namespace vdnnk {
 
-template <int BN, int BM, int STAGES>
+template <int BN, int BM, int STAGES, int NOUT = 2>
 struct PersistSmem {
   static constexpr int kABytes = BM * 128;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kOut = 2 * 16384;
+  static constexpr int kOut = NOUT * 16384;
   static constexpr int kTotal = STAGES * kStage + kOut + 1024 + 256;
   static constexpr int kAccCols = (BM / kBM) * BN;  // one accumulator set
   static_assert(2 * kAccCols <= 512, "two accumulator sets must fit TMEM");
@@ -41,7 +41,9 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
                                                                  const __grid_constant__ CUtensorMap tma_a,
                                                                  const __grid_constant__ CUtensorMap tma_b,
                                                                  const __grid_constant__ CUtensorMap tma_c) {
-  using L = PersistSmem<BN, BM, STAGES>;
+  // WG: four 16 KB W boxes (three loads ahead of the SGD math)
+  constexpr int kNout = WG ? 4 : 2;
+  using L = PersistSmem<BN, BM, STAGES, kNout>;
   constexpr int kHalves = BM / kBM;
   constexpr int kTmemCols = 2 * L::kAccCols;
   extern __shared__ uint8_t smem_raw[];
@@ -54,7 +56,7 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
   auto tfull_bar = [&](int a) { return bars + 8u * (2 * STAGES + a); };
   auto tempty_bar = [&](int a) { return bars + 8u * (2 * STAGES + 2 + a); };
   const uint32_t tmem_slot = bars + 8u * (2 * STAGES + 4);
-  auto wbar = [&](int b) { return bars + 8u * (2 * STAGES + 5 + b); };  // WG + sgd_tma: W box loads
+  auto wbar = [&](int b) { return bars + 8u * (2 * STAGES + 5 + b); };  // WG + sgd_tma: W box loads (4)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntn = (p.Ncols + BN - 1) / BN;
@@ -69,8 +71,8 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), 128);
-      mbar_init(wbar(a), 1);
     }
+    for (int b = 0; b < 4; ++b) mbar_init(wbar(b), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 4) {
@@ -147,6 +149,19 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
     // ---------------- epilogue ----------------
     const int row = warp * 32 + lane;
     int lt = 0, box = 0;
+    // WG + sgd_tma: W box g (global order: tile, half, 32-column group) goes
+    // to buffer g % 4; the load of box g + 3 is issued once box g's store is out
+    constexpr int kPerTile = kHalves * (BN / 32);
+    auto issue_w = [&](int g) {
+      const int t = static_cast<int>(blockIdx.x) + (g / kPerTile) * static_cast<int>(gridDim.x);
+      if (t >= ntiles) return;
+      const int j = g % kPerTile, hh = j / (BN / 32), cc = j - hh * (BN / 32);
+      const int km = (t / ntn) * BM + hh * kBM, co = (t % ntn) * BN + cc * 32;
+      mbar_expect_tx(wbar(g & 3), 16384);
+      tma_load_2d(obuf + (g & 3) * 16384, &tma_c, wbar(g & 3), km, co);
+    };
+    if (WG && p.sgd_tma && threadIdx.x == 0)
+      for (int g = 0; g < 3; ++g) issue_w(g);
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
       const int acc = lt & 1;
       const int m0 = (tile / ntn) * BM, n0 = (tile % ntn) * BN;
@@ -170,16 +185,11 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
             if (p.sgd_tma) {
               // FC layer: W[nb .. nb+31][m0 + h*128 .. +127] as one TMA box
               // (16 KB, unswizzled [32 co][128 k]); SGD in shared memory, TMA
-              // store back -- the weight traffic runs asynchronously instead
-              // of 32 dependent loads per thread
-              const int b = box & 1;
+              // store back -- the weight traffic runs asynchronously (three
+              // box loads in flight) instead of 32 dependent loads per thread
+              const int b = box & 3;
               const uint32_t ob = obuf + b * 16384;
-              if (threadIdx.x == 0) {
-                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // box b's last store read it
-                mbar_expect_tx(wbar(b), 16384);
-                tma_load_2d(ob, &tma_c, wbar(b), m0 + h * kBM, nb);
-              }
-              mbar_wait(wbar(b), (box >> 1) & 1);
+              mbar_wait(wbar(b), (box >> 2) & 1);
               const uint32_t col = ob + row * 4;
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
@@ -192,6 +202,9 @@ __global__ void __launch_bounds__(192, 1) tc_conv_persist_kernel(const __grid_co
               if (threadIdx.x == 0) {
                 tma_store_2d(&tma_c, ob, m0 + h * kBM, nb, false);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                // buffer (box + 3) & 3 held box - 1, whose store must have read it
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                issue_w(box + 3);
               }
               continue;
             }
