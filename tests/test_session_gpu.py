@@ -432,3 +432,30 @@ def test_vgg16_b256_headline_plan_full_size():
     assert np.isfinite(loss_dyn)
     assert loss_dyn == loss_t == loss_b
     assert w_dyn == w_t == w_b
+
+
+def test_pause_timeline_keeps_numbers_and_reports_last_recorded_step():
+    """pause_timeline skips the per-op events (benchmark loops) without
+    changing results; after resuming, the measured report and layer times
+    describe the last recorded step and still replay clean."""
+    _need_gpu()
+    g = V.build_preset("alexnet", 16)
+    cm = V.CostModel()
+    d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+    cap = 4 << 30
+    losses = []
+    for pause in (False, True):
+        s = V.Session(g, d, cm, cap, record_timeline=True)
+        s.synthetic_batch(5)
+        s.step(LR)
+        s.pause_timeline(pause)
+        s.step(LR)
+        s.step(LR)
+        s.pause_timeline(False)
+        losses.append(s.step(LR))
+        f, b = s.layer_times()
+        assert sum(f) > 0 and sum(b) > 0
+        m = s.measured_report()
+        assert V.replay_check(m, g, d, cap) == []
+        del s
+    assert losses[0] == losses[1]
