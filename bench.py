@@ -354,6 +354,9 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     return res
 
 
+_CPU_WARM = False
+
+
 def cpu_baseline_sample(args, seconds_target=15.0):
     """Reference CPU path on this host: the compiled reference planner
     (dynamic_select + simulate, oracle/_ref) + the numeric restatement of one
@@ -374,6 +377,15 @@ def cpu_baseline_sample(args, seconds_target=15.0):
     images = rng.uniform(-1, 1, size=(sh.n, sh.h, sh.w, sh.c)).astype(np.float32)
     ls = g.shape(g.layer(g.size() - 1).inputs[0])
     labels = rng.integers(0, ls.c, size=sh.n).astype(np.int32)
+    global _CPU_WARM
+    if not _CPU_WARM:  # first call: torch CPU thread pool / allocator warm-up on a tiny batch, untimed
+        gw = V.build_preset(args.net, 2) if args.extra == 0 else V.extend_vgg(args.extra, 2)
+        shw = gw.shape(0)
+        lsw = gw.shape(gw.layer(gw.size() - 1).inputs[0])
+        numeric.train_step(gw, numeric.he_weights(gw, V.CostModel()),
+                           rng.uniform(-1, 1, size=(shw.n, shw.h, shw.w, shw.c)).astype(np.float32),
+                           rng.integers(0, lsw.c, size=shw.n).astype(np.int32), args.lr, dtype=torch.float32)
+        _CPU_WARM = True
     t0 = time.perf_counter()
     numeric.train_step(g, w, images, labels, args.lr, dtype=torch.float32)
     step_s = time.perf_counter() - t0
@@ -422,7 +434,8 @@ def main():
                          "offload into a peer GPU's HBM (N > 1). Default: dyn,dynz,dynt,all,conv,none (+ dynp at N > 1)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--precise", action="store_true", help="3xTF32 fp32-accurate contractions")
-    ap.add_argument("--cpu-sample-batch", type=int, default=2)
+    ap.add_argument("--cpu-sample-batch", type=int, default=96,
+                    help="images in the CPU reference sample (~7 s of CPU work for VGG-16 b96 on 16 cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
