@@ -13,5 +13,5 @@ python tools/prof_layers.py alexnet 128 none > gpurun_out/layers_alexnet.txt 2>&
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/${LABEL}_launches_dyn.csv python bench.py --policies dyn --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"tc_conv_pair|tc_wgrad_pair|tc_conv_halo|tc_wgrad_halo|c3tc" --launch-skip 0 --launch-count 7 -o gpurun_out/${LABEL}_full python tools/one_step.py vgg16 256 none > gpurun_out/ncu_full.log 2>&1
 # backward-pass kernels (one launch each): pair wgrad, pair-halo wgrad, first-layer wgrad, persistent FC wgrad, pool bwd
-ncu --set full --clock-control none --import-source on -k regex:"tc_wgrad_pair|tc_wgrad_halo_pair|c3tc_wgrad|tc_conv_persist_kernel<128, 256, 3, true>|maxpool2x2_bwd" --launch-count 6 -o gpurun_out/${LABEL}_full_bwd python tools/one_step.py vgg16 256 none > gpurun_out/ncu_full_bwd.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"tc_wgrad_pair|tc_wgrad_halo_pair|c3tc_wgrad|tc_conv_persist|maxpool2x2_bwd" --launch-skip 0 --launch-count 12 -o gpurun_out/${LABEL}_full_bwd python tools/one_step.py vgg16 256 none > gpurun_out/ncu_full_bwd.log 2>&1
 ls -la gpurun_out
