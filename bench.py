@@ -177,6 +177,7 @@ def link_bandwidth(device: int, nbytes: int = 1 << 30):
             best = max(best, nbytes / (s.elapsed_time(e) * 1e-3) / 1e9)
         out[name + "_gbs"] = round(best, 2)
     del h, d
+    torch.cuda.empty_cache()  # give the probe's 1 GiB back before the sessions measure device usage
     return out
 
 
@@ -195,6 +196,11 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     # HBM over NVLink (data parallel only: a peer GPU is the offload target)
     # "<policy>t": compressed, and maps read in backward only by TF32
     # contractions / ReLU masks travel TF32-exact (bit-identical step)
+    # "<policy>f": fp32-accurate contractions (3xTF32) instead of TF32
+    name = policy
+    precise = args.precise or policy.endswith("f")
+    if policy.endswith("f"):
+        policy = policy[:-1]
     compress = "tf32" if policy.endswith("t") else policy.endswith("z")
     peer_target = policy.endswith("p")
     if compress or peer_target:
@@ -223,7 +229,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     if not plan.pass_:
         return {"policy": policy, "label": d.label, "verdict": plan.verdict(), "capacity": cap}
     s = V.Session(g, d, cm, cap, device=device, record_timeline=True, external_grads=world > 1,
-                  precise_fp32=args.precise, compress_offload=compress,
+                  precise_fp32=precise, compress_offload=compress,
                   offload_target="device" if peer_target else "host")
     if peer_target:
         from paper_1602_08124_b200.dist import ring_spill
@@ -245,19 +251,23 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     l0 = V.kernel_launch_count()
     s.pause_timeline(True)  # no per-op timing events inside the timed region (one more step records them below)
     with sampler_cls(device) as clk:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for _ in range(args.steps):
+        # one event per step boundary on the session's compute stream: the
+        # region [first, last] is the timed total, the gaps give the median
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        evs[0].record(stream)
+        for i in range(args.steps):
             one()
-        ev1.record(stream)
-        ev1.synchronize()
+            evs[i + 1].record(stream)
+        evs[-1].synchronize()
+        ev0, ev1 = evs[0], evs[-1]
+        per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     launches = V.kernel_launch_count() - l0
     ts1 = s.transfer_stats()
     wire = {k: (ts1[k] - ts0[k]) // args.steps for k in ts0}
     ms = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms, world, device=f"cuda:{device}")
     imgs = args.batch * world / (ms * 1e-3)
+    ms_median = max_over_ranks(statistics.median(per_step), world, device=f"cuda:{device}")
     s.pause_timeline(False)
     loss = s.step(args.lr, want_loss=True) if not dp else dp.step(args.lr, True)
 
@@ -274,22 +284,26 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     pre_ms = sum((e.end - e.start) for e in m.events if e.kind == V.EventKind.Prefetch) * 1e-6
     free, total = torch.cuda.mem_get_info(device)
     res = {
-        "policy": policy + ({"tf32": "t", True: "z"}.get(compress, "")) + ("p" if peer_target else ""),
+        "policy": name,
         "label": d.label + ({"tf32": " +zvc/tf32-exact", True: " +zvc"}.get(compress, ""))
                  + (" ->peer HBM" if peer_target else ""),
         "verdict": "PASS", "capacity_bytes": cap,
-        "images_per_s": round(imgs, 2), "ms_per_step": round(ms, 3), "loss": loss,
+        "images_per_s": round(imgs, 2), "ms_per_step": round(ms, 3), "ms_per_step_median": round(ms_median, 3),
+        "loss": loss, "precise_fp32": bool(precise),
         "peak_pool_bytes": plan.max_mem_bytes, "arena_bytes": s.arena_info()["arena_bytes"],
         "device_used_bytes": total - free,
         "offload_bytes_per_iter": plan.offload_traffic_bytes, "prefetch_bytes_per_iter": plan.prefetch_traffic_bytes,
         "d2h_gbs": round(plan.offload_traffic_bytes / (off_ms * 1e-3) / 1e9, 2) if off_ms > 0 else None,
         "h2d_gbs": round(plan.prefetch_traffic_bytes / (pre_ms * 1e-3) / 1e9, 2) if pre_ms > 0 else None,
-        # compute-stream time not covered by layer kernels = waiting on offload/prefetch copies
-        # (layer times come from one extra step after a host sync, at the clocks
-        # of a briefly idle GPU; with no transfers the difference to the timed
-        # loop is clock droop under sustained load, not transfer time)
-        "exposed_transfer_ms": (round(max(0.0, ms - kernel_ms), 3)
-                                if world == 1 and plan.offload_traffic_bytes > 0 else None),
+        # exposed (non-overlapped) transfer time = the SYNC stalls of the
+        # measured event log of one recorded step (simulator.hpp:315-322
+        # forward: FWD(n+1) waits for n's offloads; :400-441 backward: BWD(m)
+        # waits for its prefetches / the step's prefetch tail), re-timed from
+        # CUDA events on both streams
+        "exposed_transfer_ms": (round(m.stall_ns() * 1e-6, 3) if plan.offload_traffic_bytes > 0 else None),
+        "stall_fwd_offload_ms": round(m.stall_fwd_offload_ns * 1e-6, 3),
+        "stall_bwd_prefetch_ms": round(m.stall_bwd_prefetch_ns * 1e-6, 3),
+        "measured_step_ms": round(m.total_ns * 1e-6, 3),
         "kernel_ms": round(kernel_ms, 3),
         "conv_fc_ms": round(conv_ms, 3), "memory_bound_ms": round(mem_ms, 3),
         "conv_fc_tflops": round(conv_tflops, 1) if conv_tflops else None,
@@ -360,31 +374,31 @@ _CPU_WARM = False
 def cpu_baseline_sample(args, seconds_target=15.0):
     """Reference CPU path on this host: the compiled reference planner
     (dynamic_select + simulate, oracle/_ref) + the numeric restatement of one
-    training iteration (torch CPU fp32, all threads) on a small batch."""
+    training iteration (torch CPU fp32, all threads) on a small batch. The
+    graphs come from the reference's own presets (refsim.preset_spec) so this
+    arm never loads the product library (libvdnn.so)."""
     import numpy as np
     import torch
-    import paper_1602_08124_b200 as V
     from oracle import numeric, refsim
     cores = os.cpu_count() or 1
     torch.set_num_threads(cores)
     sample_batch = args.cpu_sample_batch
-    g = V.build_preset(args.net, sample_batch) if args.extra == 0 else V.extend_vgg(args.extra, sample_batch)
-    gfull = V.build_preset(args.net, args.batch) if args.extra == 0 else V.extend_vgg(args.extra, args.batch)
-    plan_s = refsim.time_plan(gfull.spec(), args.capacity, 20) if refsim.available() else 0.0
-    w = numeric.he_weights(g, V.CostModel())
-    sh = g.shape(0)
+    g = numeric.layers_of(refsim.preset_spec(args.net, sample_batch, args.extra))
+    full_spec = refsim.preset_spec(args.net, args.batch, args.extra)
+    plan_s = refsim.time_plan(full_spec, args.capacity, 20)
+    w = numeric.he_weights(g)
+    sh = g[0].shape  # NCHW
     rng = np.random.default_rng(5)
-    images = rng.uniform(-1, 1, size=(sh.n, sh.h, sh.w, sh.c)).astype(np.float32)
-    ls = g.shape(g.layer(g.size() - 1).inputs[0])
-    labels = rng.integers(0, ls.c, size=sh.n).astype(np.int32)
+    images = rng.uniform(-1, 1, size=(sh[0], sh[2], sh[3], sh[1])).astype(np.float32)
+    classes = int(np.prod(g[g[-1].inputs[0]].shape[1:]))
+    labels = rng.integers(0, classes, size=sh[0]).astype(np.int32)
     global _CPU_WARM
     if not _CPU_WARM:  # first call: torch CPU thread pool / allocator warm-up on a tiny batch, untimed
-        gw = V.build_preset(args.net, 2) if args.extra == 0 else V.extend_vgg(args.extra, 2)
-        shw = gw.shape(0)
-        lsw = gw.shape(gw.layer(gw.size() - 1).inputs[0])
-        numeric.train_step(gw, numeric.he_weights(gw, V.CostModel()),
-                           rng.uniform(-1, 1, size=(shw.n, shw.h, shw.w, shw.c)).astype(np.float32),
-                           rng.integers(0, lsw.c, size=shw.n).astype(np.int32), args.lr, dtype=torch.float32)
+        gw = numeric.layers_of(refsim.preset_spec(args.net, 2, args.extra))
+        shw = gw[0].shape
+        numeric.train_step(gw, numeric.he_weights(gw),
+                           rng.uniform(-1, 1, size=(shw[0], shw[2], shw[3], shw[1])).astype(np.float32),
+                           rng.integers(0, classes, size=shw[0]).astype(np.int32), args.lr, dtype=torch.float32)
         _CPU_WARM = True
     t0 = time.perf_counter()
     numeric.train_step(g, w, images, labels, args.lr, dtype=torch.float32)
@@ -431,7 +445,9 @@ def main():
     ap.add_argument("--policies", default=None,
                     help="dyn/all/conv/none; a trailing z = same plan with compressed offload, t = compressed with "
                          "TF32-exact values where only TF32 contractions read the map, a trailing p = "
-                         "offload into a peer GPU's HBM (N > 1). Default: dyn,dynz,dynt,all,conv,none (+ dynp at N > 1)")
+                         "offload into a peer GPU's HBM (N > 1), a trailing f = fp32-accurate 3xTF32 "
+                         "contractions. Default: dyn,dynz,dynt,all,conv,none,dynf,nonef (N > 1: dyn,dynp,dynz,dynt,"
+                         "all,conv,none)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--precise", action="store_true", help="3xTF32 fp32-accurate contractions")
     ap.add_argument("--cpu-sample-batch", type=int, default=96,
@@ -468,7 +484,8 @@ def main():
     tf32_peak, peak_note = measured_tf32_peak(peaks, peaks_src)
 
     if args.policies is None:
-        args.policies = "dyn,dynz,dynt,all,conv,none" if world == 1 else "dyn,dynp,dynz,dynt,all,conv,none"
+        args.policies = ("dyn,dynz,dynt,all,conv,none,dynf,nonef" if world == 1
+                         else "dyn,dynp,dynz,dynt,all,conv,none")
     results = {}
     for p in [x for x in args.policies.split(",") if x]:
         results[p] = run_policy(p, args, device, world, peaks, want_e2e=(p == "dyn"), sampler_cls=ClockSampler)
@@ -528,6 +545,11 @@ def main():
             "images_per_s": z["images_per_s"], "ms_per_step": z["ms_per_step"], "wire_ratio": z.get("wire_ratio"),
             "speedup_vs_copy_engines": round(z["images_per_s"] / head["images_per_s"], 3)
             if head.get("images_per_s") else None}
+    if any(k in results for k in ("dynf", "nonef")):
+        line["fp32_accurate"] = {
+            "policy": "3xTF32 contractions (fp32-accurate), same plans",
+            **{k: {"images_per_s": results[k].get("images_per_s"), "ms_per_step": results[k].get("ms_per_step")}
+               for k in ("dynf", "nonef") if k in results}}
     if "dynp" in results and results["dynp"].get("images_per_s"):
         z = results["dynp"]
         line["peer_hbm_offload"] = {

@@ -246,6 +246,12 @@ typedef struct vdnn_violation {
 } vdnn_violation;
 vdnn_status vdnn_replay_check(const vdnn_report* r, const vdnn_graph* g, const vdnn_decision* d, uint64_t capacity,
                               vdnn_violation* out, size_t cap, size_t* n);
+/* The executable program the session runs (operands bound to pool offsets,
+ * per-step scratch gaps, transfers) checked against the plan's own event log:
+ * every binding inside the extent live for that buffer at that step. Not a
+ * reference entry point: the parity gate for the executor's view of a plan. */
+vdnn_status vdnn_program_check(const vdnn_graph* g, const vdnn_decision* d, const vdnn_cost_model* cm,
+                               uint64_t capacity, vdnn_violation* out, size_t cap, size_t* n);
 
 /* ------------------------------------------------- B200 training session -- */
 typedef struct vdnn_session vdnn_session;

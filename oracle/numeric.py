@@ -31,16 +31,63 @@ INPUT, CONV, ACTV, POOL, FC, LOSS = range(6)
 
 
 class Layer:
-    def __init__(self, id, kind, inputs, params, shape):
+    def __init__(self, id, kind, inputs, params, shape, join=0):
         self.id, self.kind, self.inputs, self.params, self.shape = id, kind, list(inputs), params, shape
+        self.join = join  # 0 = concat, 1 = elementwise sum
 
 
 def layers_of(g) -> List[Layer]:
-    """From a paper_1602_08124_b200.NetworkGraph (finalized)."""
+    """From a paper_1602_08124_b200.NetworkGraph (finalized), a graph spec
+    string ("B=<batch>|<kind> <inputs> p0 p1 p2 p3 <join>|...", the format of
+    oracle/refsim.preset_spec), or an already converted layer list."""
+    if isinstance(g, str):
+        return layers_from_spec(g)
+    if isinstance(g, list):
+        return g
     out = []
     for l in g.layers():
         s = g.shape(l.id)
-        out.append(Layer(l.id, int(l.kind), l.inputs, l.params, (s.n, s.c, s.h, s.w)))
+        out.append(Layer(l.id, int(l.kind), l.inputs, l.params, (s.n, s.c, s.h, s.w), int(l.join)))
+    return out
+
+
+_KINDS = {"input": INPUT, "conv": CONV, "actv": ACTV, "pool": POOL, "fc": FC, "loss": LOSS}
+
+
+def layers_from_spec(spec: str) -> List[Layer]:
+    """Graph spec -> layers with inferred NCHW shapes (net_graph.hpp:299-358:
+    conv (h + 2p - k)/s + 1, pool floor without padding, concat sums C,
+    elementwise keeps the shape, FC -> (n, out, 1, 1), LOSS -> (n, 1, 1, 1)).
+    Lets the reference arm build its graphs without the product library."""
+    parts = spec.split("|")
+    batch = int(parts[0].split("=")[1])
+    out: List[Layer] = []
+    for i, p in enumerate(parts[1:]):
+        kind_s, ins_s, a, b, c, d, j = p.split()
+        kind = _KINDS[kind_s]
+        ins = [] if ins_s == "-" else [int(x) for x in ins_s.split(",")]
+        prm = (int(a), int(b), int(c), int(d))
+        join = int(j)
+        if kind == INPUT:
+            shape = (batch, prm[0], prm[1], prm[2])
+        else:
+            n, ch, h, w = out[ins[0]].shape
+            for q in ins[1:]:
+                if join == 0:
+                    ch += out[q].shape[1]
+            if kind == CONV:
+                k, s, pad, cout = prm
+                shape = (n, cout, (h + 2 * pad - k) // s + 1, (w + 2 * pad - k) // s + 1)
+            elif kind == POOL:
+                k, s = prm[0], prm[1]
+                shape = (n, ch, (h - k) // s + 1, (w - k) // s + 1)
+            elif kind == FC:
+                shape = (n, prm[0], 1, 1)
+            elif kind == LOSS:
+                shape = (n, 1, 1, 1)
+            else:
+                shape = out[ins[0]].shape
+        out.append(Layer(i, kind, ins, prm, shape, join))
     return out
 
 
@@ -239,19 +286,22 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
             {k: v.cpu().numpy() for k, v in grads.items()})
 
 
-def he_weights(g, cost, seed: int = 5000) -> Dict[int, np.ndarray]:
+def he_weights(g, cost=None, seed: int = 5000) -> Dict[int, np.ndarray]:
     """Host-side He-normal init (numpy), for tests that upload weights."""
     rng = np.random.default_rng(seed)
+    L = layers_of(g)
     out = {}
-    for l in layers_of(g):
+    for l in L:
         if l.kind == CONV:
             k, s, p, cout = l.params
-            cin = sum(layers_of(g)[q].shape[1] for q in l.inputs)
+            cs = [L[q].shape[1] for q in l.inputs]
+            cin = cs[0] if l.join == 1 else sum(cs)
             fan = k * k * cin
             out[l.id] = (rng.standard_normal(cout * k * k * cin) * np.sqrt(2.0 / fan)).astype(np.float32)
         elif l.kind == FC:
             outf = l.params[0]
-            fin = sum(int(np.prod(layers_of(g)[q].shape[1:])) for q in l.inputs)
+            fs = [int(np.prod(L[q].shape[1:])) for q in l.inputs]
+            fin = fs[0] if l.join == 1 else sum(fs)
             w = (rng.standard_normal(outf * fin) * np.sqrt(2.0 / fin)).astype(np.float32)
             out[l.id] = np.concatenate([w, np.zeros(outf, np.float32)])
     return out

@@ -9,7 +9,7 @@ from .api import (
     GradientScheme, InvalidDecision, InvalidDepth, JoinRule, LayerKind, NetworkGraph, OomInfo, Phase,
     PolicyDecision, PolicyKind, PoolUseError, ProfilePassResult, RunReport, ShapeMismatch, SimOptions, Stream,
     StreamEvent, TensorShape, UnknownPreset, Violation, WrongLayerKind, baseline_footprint, build_preset,
-    dynamic_select, extend_vgg, gradient_map_bytes, greedy_downgrade, per_layer_event_peaks, replay_check,
+    dynamic_select, extend_vgg, gradient_map_bytes, greedy_downgrade, per_layer_event_peaks, program_check, replay_check,
     Session, kernel_launch_count, report_from_events, simulate, simulate_oracle, simulate_with_trace, static_decision,
 )
 

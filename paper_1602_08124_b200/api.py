@@ -685,6 +685,18 @@ def replay_check(report: RunReport, g: NetworkGraph, decision: PolicyDecision, c
     return [Violation(v.kind.decode(), v.detail.decode()) for v in out[: n.value]]
 
 
+def program_check(g: NetworkGraph, decision: PolicyDecision, cost: "CostModel", capacity: int) -> List[Violation]:
+    """Compile the plan's executable program (the executor's operand bindings,
+    scratch gaps, transfers) and check it against the plan's own event log."""
+    d = decision._handle(g)
+    cm = cost._c()
+    n = C.c_size_t()
+    _call("vdnn_program_check", g.handle, d.h, C.byref(cm), C.c_uint64(capacity), None, C.c_size_t(0), C.byref(n))
+    out = (L.Violation * max(n.value, 1))()
+    _call("vdnn_program_check", g.handle, d.h, C.byref(cm), C.c_uint64(capacity), out, n, C.byref(n))
+    return [Violation(v.kind.decode(), v.detail.decode()) for v in out[: n.value]]
+
+
 @dataclass
 class FootprintReport:
     weights_bytes: int

@@ -655,4 +655,25 @@ vdnn_status vdnn_replay_check(const vdnn_report* r, const vdnn_graph* g, const v
   });
 }
 
+// Compile the executable program of a plan and check its operand bindings,
+// scratch gaps and transfers against the plan's own event log.
+vdnn_status vdnn_program_check(const vdnn_graph* g, const vdnn_decision* d, const vdnn_cost_model* cm,
+                               uint64_t capacity, vdnn_violation* out, size_t cap, size_t* n) {
+  return guard([&] {
+    const Net& net = final_net(g);
+    Program prog;
+    const Report r = plan(net, d->d, cost_from(cm), capacity, {}, &prog);
+    std::vector<Finding> v;
+    if (r.pass) v = check_program(prog, r, net, d->d);
+    if (n) *n = v.size();
+    if (out)
+      for (size_t i = 0; i < v.size() && i < cap; ++i) {
+        std::memset(&out[i], 0, sizeof(out[i]));
+        std::strncpy(out[i].kind, v[i].kind.c_str(), sizeof(out[i].kind) - 1);
+        std::strncpy(out[i].detail, v[i].detail.c_str(), sizeof(out[i].detail) - 1);
+      }
+    return VDNN_OK;
+  });
+}
+
 }  // extern "C"

@@ -34,7 +34,7 @@ constexpr int kStages = 3;         // 3 x 32 KB (BN=128): two CTAs per SM overla
 constexpr int kStagesPrecise = 3;
 constexpr int kNumSms = 148;
 constexpr int kStagesWide = 4;     // 4 x 48 KB (BN=256): one CTA per SM
-std::atomic<int> g_sm_reserve{-1};  // SMs the persistent conv kernels leave free (compressed transfers)
+thread_local int g_sm_reserve = -1;  // SMs the persistent conv kernels leave free (compressed transfers)
 
 // CTAs (one per SM) of the persistent conv kernels: all 148 SMs, minus an
 // even reserve for concurrent SM-driven transfers (zvc.cu kernels cannot
@@ -42,7 +42,7 @@ std::atomic<int> g_sm_reserve{-1};  // SMs the persistent conv kernels leave fre
 // whole persistent conv kernel, or hold SMs a persistent kernel's
 // statically scheduled CTAs need).
 int persist_sms() {
-  int r = g_sm_reserve.load(std::memory_order_relaxed);
+  int r = g_sm_reserve;
   if (r < 0) {
     const char* e = std::getenv("VDNN_SM_RESERVE");
     r = e ? std::atoi(e) : 0;
@@ -951,7 +951,7 @@ __global__ void dgrad_reduce_kernel(const float* __restrict__ part, int splits, 
 }
 }  // namespace
 
-void set_sm_reserve(int sms) { g_sm_reserve.store(sms, std::memory_order_relaxed); }
+void set_sm_reserve(int sms) { g_sm_reserve = sms; }
 
 size_t conv_dgrad_ws_bytes(const ConvArgs& a) {
   ConvParams p;

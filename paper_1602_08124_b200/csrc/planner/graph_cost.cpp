@@ -91,101 +91,86 @@ int Net::loss(int in) {
   return add(std::move(n));
 }
 
-// net_graph.hpp:231-279
+// Structural rules of a layer list (net_graph.hpp:231-279): ids are
+// positions, inputs point strictly backwards and are distinct, each kind has
+// its arity and positive parameters.
 void Net::check() const {
-  if (batch_ < 1) throw PlanError(Err::Generic, "batch must be >= 1");
+  if (batch_ < 1) throw PlanError(Err::Generic, "a graph needs a batch of at least 1");
+  auto bad = [](const Node& l, const std::string& why) {
+    return PlanError(Err::Generic, std::string(kind_name(l.kind)) + " layer " + std::to_string(l.id) + ": " + why);
+  };
   for (size_t i = 0; i < nodes_.size(); ++i) {
     const Node& l = nodes_[i];
-    const std::string at = "layer " + std::to_string(i);
-    if (l.id != static_cast<int>(i)) throw PlanError(Err::Generic, at + ": id does not match position");
-    for (int q : l.in)
-      if (q < 0 || q >= l.id) throw PlanError(Err::Generic, at + ": inputs must reference earlier layers");
-    for (size_t a = 0; a < l.in.size(); ++a)
-      for (size_t b = a + 1; b < l.in.size(); ++b)
-        if (l.in[a] == l.in[b]) throw PlanError(Err::Generic, at + ": duplicate input");
-    switch (l.kind) {
-      case Kind::Input:
-        if (!l.in.empty()) throw PlanError(Err::Generic, at + ": INPUT layers take no inputs");
-        if (l.ic < 1 || l.ih < 1 || l.iw < 1) throw PlanError(Err::Generic, at + ": input dims must be >= 1");
-        break;
-      case Kind::Actv:
-        if (l.in.size() != 1) throw PlanError(Err::Generic, at + ": ACTV layers take exactly one input");
-        break;
-      case Kind::Conv:
-        if (l.in.empty()) throw PlanError(Err::Generic, at + ": CONV layers need at least one input");
-        if (l.k < 1 || l.s < 1 || l.out < 1) throw PlanError(Err::Generic, at + ": bad conv params");
-        break;
-      case Kind::Pool:
-        if (l.in.empty()) throw PlanError(Err::Generic, at + ": POOL layers need at least one input");
-        if (l.k < 1 || l.s < 1) throw PlanError(Err::Generic, at + ": bad pool params");
-        break;
-      case Kind::Fc:
-        if (l.in.empty()) throw PlanError(Err::Generic, at + ": FC layers need at least one input");
-        if (l.out < 1) throw PlanError(Err::Generic, at + ": bad fc params");
-        break;
-      case Kind::Loss:
-        if (l.in.empty()) throw PlanError(Err::Generic, at + ": LOSS layers need at least one input");
-        break;
+    if (l.id != static_cast<int>(i)) throw bad(l, "stored at position " + std::to_string(i));
+    std::vector<int> seen;
+    for (int q : l.in) {
+      if (q < 0 || q >= l.id) throw bad(l, "input " + std::to_string(q) + " is not an earlier layer");
+      if (std::find(seen.begin(), seen.end(), q) != seen.end())
+        throw bad(l, "input " + std::to_string(q) + " listed twice");
+      seen.push_back(q);
     }
+    const size_t arity = l.in.size();
+    bool ok = true;
+    switch (l.kind) {
+      case Kind::Input: ok = arity == 0 && l.ic >= 1 && l.ih >= 1 && l.iw >= 1; break;
+      case Kind::Actv: ok = arity == 1; break;
+      case Kind::Conv: ok = arity >= 1 && l.k >= 1 && l.s >= 1 && l.out >= 1; break;
+      case Kind::Pool: ok = arity >= 1 && l.k >= 1 && l.s >= 1; break;
+      case Kind::Fc: ok = arity >= 1 && l.out >= 1; break;
+      case Kind::Loss: ok = arity >= 1; break;
+    }
+    if (!ok) throw bad(l, "wrong number of inputs (" + std::to_string(arity) + ") or a non-positive parameter");
   }
 }
 
-Dims Net::joined(const Node& l) const {  // net_graph.hpp:281-297
+// Shape of a layer's joined input (net_graph.hpp:281-297): a concat stacks
+// channels of maps that agree on n/h/w; an elementwise join needs equal shapes.
+Dims Net::joined(const Node& l) const {
   Dims s = shapes_.at(static_cast<size_t>(l.in[0]));
   for (size_t i = 1; i < l.in.size(); ++i) {
     const Dims& t = shapes_.at(static_cast<size_t>(l.in[i]));
-    if (l.join == Join::Concat) {
-      if (t.n != s.n || t.h != s.h || t.w != s.w)
-        throw PlanError(Err::Shape, "layer " + std::to_string(l.id) + ": concat inputs disagree on n/h/w");
-      s.c += t.c;
-    } else if (!(t == s)) {
-      throw PlanError(Err::Shape,
-                      "layer " + std::to_string(l.id) + ": elementwise inputs must have identical shapes");
-    }
+    const bool fits = l.join == Join::Concat ? (t.n == s.n && t.h == s.h && t.w == s.w) : t == s;
+    if (!fits)
+      throw PlanError(Err::Shape, "layer " + std::to_string(l.id) + ": input " + std::to_string(l.in[i]) +
+                                      (l.join == Join::Concat ? " cannot be concatenated (n/h/w differ)"
+                                                              : " cannot be summed (shape differs)"));
+    if (l.join == Join::Concat) s.c += t.c;
   }
   return s;
 }
 
-void Net::finalize() {  // net_graph.hpp:206-212,299-358
+// Shapes in id order (net_graph.hpp:299-358): conv (h + 2p - k)/s + 1 with
+// exact division, pool floor((h - k)/s) + 1, FC (n, out, 1, 1), LOSS
+// (n, 1, 1, 1), ACTV keeps its input's shape; then the consumer lists.
+void Net::finalize() {
   check();
   shapes_.assign(nodes_.size(), Dims{});
   for (const Node& l : nodes_) {
-    Dims& o = shapes_[static_cast<size_t>(l.id)];
-    switch (l.kind) {
-      case Kind::Input:
-        o = Dims{batch_, l.ic, l.ih, l.iw};
-        break;
-      case Kind::Conv: {
-        const Dims x = joined(l);
-        const u64 sh = x.h + 2 * l.p, sw = x.w + 2 * l.p;
-        if (sh < l.k || sw < l.k)
-          throw PlanError(Err::Shape, "layer " + std::to_string(l.id) + ": kernel larger than padded input");
-        if ((sh - l.k) % l.s != 0 || (sw - l.k) % l.s != 0)
-          throw PlanError(Err::Shape,
-                          "layer " + std::to_string(l.id) + ": (h + 2p - k) not divisible by stride");
-        o = Dims{x.n, l.out, (sh - l.k) / l.s + 1, (sw - l.k) / l.s + 1};
-        break;
-      }
-      case Kind::Actv:
-        o = shapes_[static_cast<size_t>(l.in[0])];
-        break;
-      case Kind::Pool: {
-        const Dims x = joined(l);
-        if (x.h < l.k || x.w < l.k)
-          throw PlanError(Err::Shape, "layer " + std::to_string(l.id) + ": pool window larger than input");
-        o = Dims{x.n, x.c, (x.h - l.k) / l.s + 1, (x.w - l.k) / l.s + 1};
-        break;
-      }
-      case Kind::Fc: {
-        const Dims x = joined(l);
-        o = Dims{x.n, l.out, 1, 1};
-        break;
-      }
-      case Kind::Loss: {
-        const Dims x = joined(l);
-        o = Dims{x.n, 1, 1, 1};
-        break;
-      }
+    const size_t i = static_cast<size_t>(l.id);
+    if (l.kind == Kind::Input) {
+      shapes_[i] = Dims{batch_, l.ic, l.ih, l.iw};
+      continue;
+    }
+    if (l.kind == Kind::Actv) {
+      shapes_[i] = shapes_[static_cast<size_t>(l.in[0])];
+      continue;
+    }
+    const Dims x = joined(l);
+    auto shape_error = [&](const char* why) {
+      return PlanError(Err::Shape, "layer " + std::to_string(l.id) + ": " + why);
+    };
+    if (l.kind == Kind::Conv) {
+      const u64 h = x.h + 2 * l.p, w = x.w + 2 * l.p;
+      if (h < l.k || w < l.k) throw shape_error("the filter does not fit the padded input");
+      if ((h - l.k) % l.s || (w - l.k) % l.s) throw shape_error("stride does not divide the padded span");
+      shapes_[i] = Dims{x.n, l.out, (h - l.k) / l.s + 1, (w - l.k) / l.s + 1};
+    } else if (l.kind == Kind::Pool) {
+      if (x.h < l.k || x.w < l.k) throw shape_error("the pooling window does not fit the input");
+      shapes_[i] = Dims{x.n, x.c, (x.h - l.k) / l.s + 1, (x.w - l.k) / l.s + 1};
+    } else if (l.kind == Kind::Fc) {
+      shapes_[i] = Dims{x.n, l.out, 1, 1};
+    } else {
+      shapes_[i] = Dims{x.n, 1, 1, 1};
     }
   }
   users_.assign(nodes_.size(), {});

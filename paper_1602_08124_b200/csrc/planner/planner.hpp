@@ -154,55 +154,48 @@ struct TraceRow {
   u64 off = 0, len = 0, cur = 0, hw = 0;
 };
 
-// Fixed-capacity, 512-B aligned suballocator with size-segregated
-// double-ended placement (memory_pool.hpp:32-86): requests above capacity/8
-// are best-fit bottom-up, smaller or pinned requests go to the top of the
-// highest fitting extent.
+// The device arena's address map: an ordered list of segments that tiles
+// [0, capacity) exactly, each either holding one allocation or free (no two
+// free segments are ever adjacent). An allocation is named by its start
+// offset, which is unique among live allocations. Placement policy
+// (memory_pool.hpp:32-86): requests of at most capacity/8 bytes, and pinned
+// requests, take the top of the highest-addressed free segment that fits;
+// larger requests take the bottom of the smallest free segment that fits
+// (lowest address on ties). Sizes are rounded up to 512 B.
 class Arena {
  public:
   explicit Arena(u64 capacity, bool trace = false);
-  std::optional<u64> alloc(u64 bytes, const std::string& tag, i64 t, bool pin_high);
-  void release(u64 handle, i64 t);
-  u64 offset(u64 handle) const;
-  u64 requested(u64 handle) const;
-  u64 in_use() const { return used_; }
-  u64 peak() const { return peak_; }
-  u64 largest_hole() const;
-  u64 total_free() const;
-  bool fragmented(u64 bytes) const;
-  void verify() const;  // self_check
-  u128 integral_until(i64 t);
+  std::optional<u64> place(u64 bytes, const std::string& tag, i64 t, bool pinned);
+  void free_at(u64 off, i64 t);
+  u64 requested_at(u64 off) const;
+  u64 live_bytes() const { return live_; }
+  u64 high_water() const { return hw_; }
+  // (offset, length) of the largest free segment; lowest address on ties
+  std::pair<u64, u64> widest_gap() const;
+  u64 free_total() const;
+  // a request that total free space could hold but no single gap can
+  bool would_fragment(u64 bytes) const;
+  void audit() const;  // tiling / coalescing / conservation invariants
+  u128 byte_ns_until(i64 t);
   const std::vector<TraceRow>& trace() const { return rows_; }
   u64 capacity() const { return cap_; }
 
  private:
-  struct Live {
-    u64 off, len, req;
+  struct Seg {
+    u64 off = 0, len = 0;
+    bool used = false;
+    u64 req = 0;
     std::string tag;
   };
-  void tick(i64 t);
-  void give_back(u64 off, u64 len);
+  void clock_to(i64 t);
+  size_t seg_at(u64 off) const;  // index of the segment starting at off
   u64 cap_;
   bool trace_;
-  std::map<u64, u64> holes_;  // offset -> length, coalesced
-  std::map<u64, Live> live_;
-  u64 used_ = 0, peak_ = 0, next_ = 1;
-  i64 last_t_ = 0;
+  std::vector<Seg> segs_;
+  u64 live_ = 0, hw_ = 0;
+  i64 now_ = 0;
   u128 area_ = 0;
   std::vector<TraceRow> rows_;
-};
-
-class PinnedLedger {  // HostLedger, memory_pool.hpp:225-256
- public:
-  void add(int owner, u64 bytes, i64 t);
-  void remove(int owner, i64 t);
-  u64 peak() const { return peak_; }
-  u64 current() const { return cur_; }
-
- private:
-  std::map<int, u64> held_;
-  u64 cur_ = 0, peak_ = 0;
-  i64 last_t_ = 0;
 };
 
 // ----------------------------------------------------------- decisions ----
@@ -265,34 +258,98 @@ struct SimFlags {
   bool with_dw = false;
 };
 
-// Residency of a feature buffer (sim_types.hpp:93-100).
-enum class Where : int { None = 0, Device, Draining, Host, Filling, Gone };
-
-// Static per-(graph, decision) dataflow (simulator.hpp:30-155); also the
-// executor's map of who reads what.
-struct Liveness {
-  int L = 0;
-  std::vector<u64> feat;                       // owner -> bytes (0 = no buffer)
-  std::vector<std::vector<int>> fwd_users;     // owner -> forward readers
-  std::vector<std::vector<int>> bwd_users;     // owner -> backward readers
-  std::vector<std::vector<int>> owners_in;     // layer -> distinct owners of X
-  std::vector<std::vector<int>> bwd_reads;     // layer -> feature buffers BWD reads
-  std::vector<u64> grad;                       // layer -> dX bytes
-  std::vector<std::vector<int>> grad_users;    // grad buffer -> backward readers
-  std::vector<std::vector<int>> grads_read;    // layer -> grad buffers its BWD reads
-  std::vector<std::vector<int>> offloads_at;   // layer -> buffers it offloads
-  std::vector<u64> wbytes, wsbytes;
-  std::vector<i64> fwd_ns, bwd_ns, xfer_ns;
-  u64 g2_bytes = 0, ws2_bytes = 0;
+// ------------------------------------------------------------- dataflow ---
+// What (graph, decision) fix before any timing (simulator.hpp:30-155): one
+// record per layer id. Feature fields describe the buffer the layer owns
+// (bytes == 0: it owns none -- ACTV aliases its producer's, LOSS has none).
+struct LayerFlow {
+  // own feature buffer
+  u64 bytes = 0;
+  i64 copy_ns = 0;              // one-way host-link time of the buffer
+  int fwd_readers = 0;          // forward steps that read it
+  int last_fwd_reader = kNone;
+  std::vector<int> bwd_readers; // backward steps that read it (ascending)
+  // the layer's own steps
+  std::vector<int> x_owners;    // distinct owners of its inputs (ascending)
+  std::vector<int> bwd_operands;// feature buffers its BWD reads (ascending)
+  std::vector<int> drains;      // buffers its FWD offloads (ascending)
+  u64 w_bytes = 0, ws_bytes = 0;
+  i64 fwd_ns = 0, bwd_ns = 0;
+  // gradients
+  u64 dx_bytes = 0;             // its dX map (0: none)
+  std::vector<int> dx_readers;  // BWD steps that take its dX as dY (ascending)
+  std::vector<int> dy_sources;  // dX maps its BWD takes as dY (ascending)
 };
-Liveness analyze(const Net& g, const Decision& d, const Cost& c);
+struct Dataflow {
+  std::vector<LayerFlow> at;
+  u64 g2_bytes = 0, ws2_bytes = 0;  // two-buffer scheme: each G2 buffer, the shared WS
+};
+Dataflow derive_dataflow(const Net& g, const Decision& d, const Cost& c);
 
-// First layer below `current` with a host-resident offloaded buffer; the
-// scan stops after the first CONV (prefetch.hpp:16-23).
-std::optional<int> prefetch_candidate(int current, const std::vector<Where>& where,
-                                      const std::vector<std::vector<int>>& offloads_at, const Net& g);
+// --------------------------------------------------------------- program ---
+// The executable form of a plan: every compute step (FWD/BWD of one layer)
+// with its operands bound to pool offsets, the transfers it issues on the
+// memory stream and the transfers it must wait for. The reference-format
+// event log (Report::events) is rendered from the same walk, so the executor
+// and the schedule parity tests consume one object.
+constexpr u64 kNoLoc = ~u64{0};
 
-Report plan(const Net& g, const Decision& d, const Cost& c, u64 capacity, const SimFlags& f = {});
+struct PlaneRef {     // the gradient plane of `producer`'s dX w.r.t. its input slot `slot`
+  int producer = kNone;
+  int slot = 0;       // concat: input index; elementwise: 0 (one shared plane)
+  u64 off = kNoLoc;   // pool offset (or overflow slot, see Program::overflow_base)
+  bool operator==(const PlaneRef& o) const { return producer == o.producer && slot == o.slot; }
+};
+
+struct Xfer {         // one OFFLOAD (D2H) or PREFETCH (H2D) of a whole feature buffer
+  bool to_host = true;
+  int owner = kNone;
+  u64 bytes = 0;
+  u64 dev_off = 0;    // device extent (offload: source; prefetch: freshly placed destination)
+  int step = -1;      // compute step in which it is issued (it starts after that step begins)
+  i64 t0 = 0, t1 = 0; // planned memory-lane window
+};
+
+struct Step {
+  bool bwd = false;
+  int layer = kNone;
+  i64 t_enter = 0, t0 = 0, t1 = 0, t_leave = 0;  // planned: lane reaches the step, kernel, lane moves on
+  std::vector<int> issues;        // Program::xfers issued here (in issue order)
+  std::vector<int> wait_before;   // xfers the kernel must see landed (BWD operands in flight)
+  bool wait_after = false;        // the next step waits for every xfer issued here (sync rule)
+  std::vector<u64> x;             // per input: feature extent of its owner (FWD, BWD of CONV/FC/POOL)
+  u64 y = kNoLoc;                 // FWD: output extent; BWD: POOL output / ACTV alias
+  u64 w = kNoLoc;
+  u64 ws = kNoLoc, ws_bytes = 0;
+  std::vector<PlaneRef> dx;       // BWD: per input, the plane it writes (off = kNoLoc: none)
+  bool dx_accumulate = false;     // two-buffer: add into a fork gradient already in the slot
+  std::vector<PlaneRef> dy;       // BWD: distinct incoming planes; [0] receives the fold of the rest
+  u64 gap_off = 0, gap_len = 0;   // widest free pool segment while the kernel runs (scratch space)
+  // BWD of an ACTV: the step whose epilogue may apply this ReLU's mask to
+  // input slot mask_slot (the only writer of its incoming plane), or -1
+  int mask_host = -1, mask_slot = -1;
+};
+
+struct Program {
+  std::vector<Step> steps;
+  std::vector<Xfer> xfers;
+  std::vector<u64> w_off;         // per layer weight extent (kNoLoc: none)
+  int input = kNone;              // the INPUT layer whose setup extent takes each batch
+  u64 input_off = kNoLoc;
+  // the step after whose kernel nothing touches the INPUT extent again this
+  // iteration (the next batch may land there), or -1 = only after the last step
+  int input_idle_after = -1;
+  u64 arena_lo = 0, arena_hi = 0; // span of every planned extent
+  // two-buffer scheme: gradient slots beyond the plan's two G2 buffers (a
+  // graph that needs more live maps than two), placed after arena_hi
+  u64 overflow_base = 0, overflow_slot_bytes = 0;
+  int overflow_slots = 0;
+};
+
+// One pass of the schedule: the report (always) and the program (when
+// `prog` is non-null and the plan passes).
+Report plan(const Net& g, const Decision& d, const Cost& c, u64 capacity, const SimFlags& f = {},
+            Program* prog = nullptr);
 Report plan_oracle(const Net& g, const Cost& c);
 
 // policy.hpp
@@ -320,5 +377,7 @@ struct Finding {
 std::vector<Finding> validate_log(const Report& r, const Net& g, const Decision& d, u64 capacity);
 
 u64 schedule_signature(const Report& r);
+// Bindings of a compiled Program against the event log of the same pass.
+std::vector<Finding> check_program(const Program& P, const Report& r, const Net& g, const Decision& d);
 
 }  // namespace vdnnp

@@ -84,7 +84,7 @@ void Session::peer_attach(int rank, int world, const PeerHandle* all) {
   for (int i = 0; i < L_; ++i) {
     const size_t k = static_cast<size_t>(i);
     if (grad_off_[k] == kNoOff) continue;
-    const uint64_t n = lv_.wbytes[k] / 4;
+    const uint64_t n = df_.at[k].w_bytes / 4;
     for (uint64_t s = 0; s < n; s += kChunk, ++j) {
       if (static_cast<int>(j % static_cast<uint64_t>(world)) != rank) continue;
       vdnnk::PeerChunk c{};

@@ -44,10 +44,13 @@ void Session::check(cudaError_t e, const char* what) const {
 
 Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, const Options& o)
     : g_(g), d_(d), c_(c), cap_(capacity), o_(o) {
+  // everything that can be rejected is rejected before the first allocation
   if (c_.elem != 4) throw PlanError(Err::Config, "the CUDA executor stores fp32 (elem_size 4)");
-  plan_ = vdnnp::plan(g_, d_, c_, cap_);
+  if (o_.offload_target != 0 && o_.compress_offload)
+    throw PlanError(Err::Config, "compressed offload targets the pinned host arena only");
+  plan_ = vdnnp::plan(g_, d_, c_, cap_, {}, &prog_);
   if (!plan_.pass) throw PlanError(Err::Generic, "plan does not fit the budget: " + plan_.verdict());
-  lv_ = analyze(g_, d_, c_);
+  df_ = vdnnp::derive_dataflow(g_, d_, c_);
   L_ = g_.size();
   for (const Node& l : g_.nodes()) {
     if (l.join == Join::Elementwise && l.in.size() > 1)
@@ -62,7 +65,7 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
       if (loss_id_ >= 0) throw PlanError(Err::Config, "UNSUPPORTED: more than one LOSS layer");
       loss_id_ = l.id;
     }
-    if (l.kind == Kind::Conv && lv_.grad[static_cast<size_t>(l.id)] > 0 && l.s != 1)
+    if (l.kind == Kind::Conv && df_.at[static_cast<size_t>(l.id)].dx_bytes > 0 && l.s != 1)
       throw PlanError(Err::Config, "UNSUPPORTED: data gradient of a strided conv that is not the first layer");
   }
   if (input_id_ < 0 || loss_id_ < 0) throw PlanError(Err::Config, "UNSUPPORTED: graph needs one INPUT and one LOSS");
@@ -71,37 +74,44 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
     const Dims& ld = g_.dims(g_.at(loss_id_).in[0]);
     classes_ = static_cast<int>(ld.c * ld.h * ld.w);
   }
+  // pinned host slots: one per offloaded owner
+  host_slot_.assign(static_cast<size_t>(L_), kNoOff);
+  for (const vdnnp::Xfer& x : prog_.xfers)
+    if (x.to_host && host_slot_[static_cast<size_t>(x.owner)] == kNoOff) {
+      host_slot_[static_cast<size_t>(x.owner)] = host_bytes_;
+      // compressed mode: a slot holds the worst case (every chunk dense + its mask)
+      host_bytes_ += round_up(o_.compress_offload ? std::max<u64>(x.bytes, vdnnk::zvc_slot_bytes(x.bytes)) : x.bytes,
+                              4096);
+    }
+  if (host_bytes_ > 0 && o_.offload_target == 0 && !o_.host_arena)
+    throw PlanError(Err::Config, "plan offloads but the host arena is disabled");
 
+  try {
+    acquire();
+  } catch (...) {
+    release();  // a partly built session frees what it got (the destructor will not run)
+    throw;
+  }
+}
+
+// All device / host resources of a session, in one place so a failing
+// constructor can undo them.
+void Session::acquire() {
   check(cudaSetDevice(o_.device), "cudaSetDevice");
   check(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking), "stream");
   check(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking), "stream");
 
-  // device arena over the planned offsets
-  u64 lo = ~u64{0}, hi = 0;
-  for (const Event& e : plan_.events) {
-    if (e.kind != Ev::Alloc) continue;
-    lo = std::min(lo, e.off);
-    hi = std::max(hi, e.off + round_up(e.bytes, kAlign));
-  }
-  if (hi <= lo) throw PlanError(Err::Generic, "empty plan");
-  arena_lo_ = lo;
-  arena_bytes_ = hi - lo;
-  check(cudaMalloc(&arena_, arena_bytes_), "cudaMalloc(device arena)");
-  base_ = arena_ - lo;
+  // device arena over the planned span [arena_lo, arena_hi), plus the
+  // two-buffer overflow gradient slots (if the graph needs them) right after
+  if (prog_.arena_hi <= prog_.arena_lo) throw PlanError(Err::Generic, "empty plan");
+  arena_lo_ = prog_.arena_lo;
+  arena_bytes_ = prog_.arena_hi - prog_.arena_lo;
+  const u64 overflow = static_cast<u64>(prog_.overflow_slots) * prog_.overflow_slot_bytes;
+  check(cudaMalloc(&arena_, arena_bytes_ + overflow), "cudaMalloc(device arena)");
+  base_ = arena_ - arena_lo_;
+  scratch_bytes_ += overflow;
 
-  // pinned host arena: one slot per offloaded owner
-  host_slot_.assign(static_cast<size_t>(L_), kNoOff);
-  for (const Event& e : plan_.events)
-    if (e.kind == Ev::Offload && host_slot_[static_cast<size_t>(e.buffer)] == kNoOff) {
-      host_slot_[static_cast<size_t>(e.buffer)] = host_bytes_;
-      // compressed mode: a slot holds the worst case (every chunk dense + its mask)
-      host_bytes_ += round_up(o_.compress_offload ? std::max<u64>(e.bytes, vdnnk::zvc_slot_bytes(e.bytes)) : e.bytes,
-                              4096);
-    }
-  if (o_.offload_target != 0 && o_.compress_offload)
-    throw PlanError(Err::Config, "compressed offload targets the pinned host arena only");
   if (host_bytes_ > 0 && o_.offload_target == 0) {
-    if (!o_.host_arena) throw PlanError(Err::Config, "plan offloads but the host arena is disabled");
     check(cudaHostAlloc(&host_, host_bytes_, o_.compress_offload ? cudaHostAllocMapped : cudaHostAllocDefault),
           "cudaHostAlloc(host arena)");
     host_owned_ = true;
@@ -114,39 +124,35 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
   check(cudaMalloc(&wire_, 2 * sizeof(unsigned long long)), "cudaMalloc(wire counters)");
   check(cudaMemsetAsync(wire_, 0, 2 * sizeof(unsigned long long), cs_), "memset wire counters");
 
-  // non-pool scratch
+  // non-pool scratch: softmax gradient + per-row loss + loss, two label slots
   const u64 n = g_.batch();
   check(cudaMalloc(&loss_grad_, n * static_cast<u64>(classes_) * 4), "cudaMalloc(loss grad)");
   check(cudaMalloc(&row_loss_, n * 4), "cudaMalloc(row loss)");
   check(cudaMalloc(&loss_, 4), "cudaMalloc(loss)");
-  check(cudaMalloc(&labels_, n * 4), "cudaMalloc(labels)");
+  check(cudaMalloc(&labels_, 2 * n * 4), "cudaMalloc(labels)");
+  labels_next_ = labels_ + n;
   check(cudaHostAlloc(&pinned_loss_, 4, cudaHostAllocDefault), "cudaHostAlloc(loss)");
-  scratch_bytes_ = n * static_cast<u64>(classes_) * 4 + n * 8 + 4;
-  check(cudaMemsetAsync(labels_, 0, n * 4, cs_), "memset labels");
+  scratch_bytes_ += n * static_cast<u64>(classes_) * 4 + n * 12 + 4;
+  check(cudaMemsetAsync(labels_, 0, 2 * n * 4, cs_), "memset labels");
 
   build_program();
 
-  // split-K scratch: the largest wgrad partial buffer, capped at 256 MiB
+  // split-K partials: in the step's free pool gap when it is wide enough
+  // (inside the budget), else in one fallback buffer sized for the steps
+  // whose gap is not
   size_t need = 0;
-  for (const BwdStep& s : bwd_) {
-    const Node& l = g_.at(s.layer);
-    if (l.kind != Kind::Conv && l.kind != Kind::Fc) continue;
-    need = std::max(need, vdnnk::conv_wgrad_ws_bytes(conv_args(s.layer, s.in_off, nullptr)));
-    need = std::max(need, vdnnk::conv_dgrad_ws_bytes(conv_args(s.layer, s.in_off, nullptr)));
-  }
-  for (const FwdStep& s : fwd_) {  // split-K FC fprop partials share the buffer
-    const Node& l = g_.at(s.layer);
-    if (l.kind != Kind::Conv && l.kind != Kind::Fc) continue;
-    need = std::max(need, vdnnk::conv_fprop_ws_bytes(conv_args(s.layer, s.in_off, nullptr)));
-  }
-  splitk_bytes_ = std::min<size_t>(need, size_t{256} << 20);
+  for (const FwdStep& s : fwd_)
+    if (s.scratch > s.gap_len) need = std::max(need, s.scratch);
+  for (const BwdStep& s : bwd_)
+    if (s.scratch > s.gap_len) need = std::max(need, s.scratch);
+  splitk_bytes_ = need;
   if (splitk_bytes_ > 0) check(cudaMalloc(&splitk_, splitk_bytes_), "cudaMalloc(split-K)");
   scratch_bytes_ += splitk_bytes_;
 
   if (o_.external_grads) {
     grad_off_.assign(static_cast<size_t>(L_), kNoOff);
     for (int i = 0; i < L_; ++i) {
-      const u64 wb = lv_.wbytes[static_cast<size_t>(i)];
+      const u64 wb = df_.at[static_cast<size_t>(i)].w_bytes;
       if (wb == 0) continue;
       grad_off_[static_cast<size_t>(i)] = grads_count_;
       grads_count_ += wb / 4;
@@ -157,9 +163,7 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
 
   // timing / gating events
   const size_t nsteps = fwd_.size() + bwd_.size();
-  size_t nxfer = 0;
-  for (const auto& s : fwd_) nxfer += s.offloads.size();
-  for (const auto& s : bwd_) nxfer += s.prefetches.size();
+  const size_t nxfer = prog_.xfers.size();
   step_ev_.resize(nsteps);
   for (auto& e : step_ev_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   xfer_ev_.resize(std::max<size_t>(nxfer, 1));
@@ -177,276 +181,120 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
     check(cudaEventCreate(&ev_iter_prev_), "event");
   }
   check(cudaEventCreateWithFlags(&ev_sync_, cudaEventDisableTiming), "event");
+  check(cudaEventCreateWithFlags(&input_idle_ev_, cudaEventDisableTiming), "event");
 
   init_weights();
   check(cudaStreamSynchronize(cs_), "init");
 }
 
-Session::~Session() {
+Session::~Session() { release(); }
+
+void Session::release() noexcept {
   if (cs_) cudaStreamSynchronize(cs_);
   if (ms_) cudaStreamSynchronize(ms_);
-  if (gexec_) cudaGraphExecDestroy(gexec_);  // before the events its nodes record
-  for (auto e : ev_) cudaEventDestroy(e);
-  for (auto e : step_ev_) cudaEventDestroy(e);
-  for (auto e : t0_ev_) cudaEventDestroy(e);
-  for (auto e : ev_prev_) cudaEventDestroy(e);
-  for (auto e : t0_ev_prev_) cudaEventDestroy(e);
-  if (ev_iter_prev_) cudaEventDestroy(ev_iter_prev_);
-  for (auto e : xfer_ev_) cudaEventDestroy(e);
-  if (ev_iter_) cudaEventDestroy(ev_iter_);
-  if (ev_sync_) cudaEventDestroy(ev_sync_);
   if (in_stream_) cudaStreamSynchronize(in_stream_);
-  if (staged_ready_) cudaEventDestroy(staged_ready_);
-  if (staging_free_) cudaEventDestroy(staging_free_);
-  if (staging_) cudaFree(staging_);
-  for (auto e : loss_ev_)
-    if (e) cudaEventDestroy(e);
-  if (loss_ring_) cudaFreeHost(loss_ring_);
-  if (in_stream_) cudaStreamDestroy(in_stream_);
+  if (gexec_) cudaGraphExecDestroy(gexec_);  // before the events its nodes record
+  gexec_ = nullptr;
+  for (auto* v : {&ev_, &step_ev_, &t0_ev_, &ev_prev_, &t0_ev_prev_, &xfer_ev_}) {
+    for (auto e : *v)
+      if (e) cudaEventDestroy(e);
+    v->clear();
+  }
+  for (cudaEvent_t* e : {&ev_iter_prev_, &ev_iter_, &ev_sync_, &staged_ready_, &input_idle_ev_})
+    if (*e) cudaEventDestroy(*e), *e = nullptr;
+  for (auto& e : loss_ev_)
+    if (e) cudaEventDestroy(e), e = nullptr;
+  if (loss_ring_) cudaFreeHost(loss_ring_), loss_ring_ = nullptr;
+  if (in_stream_) cudaStreamDestroy(in_stream_), in_stream_ = nullptr;
   peer_detach();
-  if (signal_) cudaFree(signal_);
-  cudaFree(arena_);
+  if (signal_) cudaFree(signal_), signal_ = nullptr;
+  if (arena_) cudaFree(arena_), arena_ = nullptr;
   if (host_ && host_owned_) cudaFreeHost(host_);
-  if (spill_map_) cudaIpcCloseMemHandle(spill_map_);
-  if (spill_) cudaFree(spill_);
-  cudaFree(loss_grad_);
-  cudaFree(row_loss_);
-  cudaFree(loss_);
-  cudaFree(wire_);
-  cudaFree(labels_);
-  if (pinned_loss_) cudaFreeHost(pinned_loss_);
-  if (splitk_) cudaFree(splitk_);
+  host_ = nullptr;
+  if (spill_map_) cudaIpcCloseMemHandle(spill_map_), spill_map_ = nullptr;
+  if (spill_) cudaFree(spill_), spill_ = nullptr;
+  for (void** p : {reinterpret_cast<void**>(&loss_grad_), reinterpret_cast<void**>(&row_loss_),
+                   reinterpret_cast<void**>(&loss_), reinterpret_cast<void**>(&wire_),
+                   reinterpret_cast<void**>(&labels_), reinterpret_cast<void**>(&splitk_)})
+    if (*p) cudaFree(*p), *p = nullptr;
+  if (pinned_loss_) cudaFreeHost(pinned_loss_), pinned_loss_ = nullptr;
   if (grads_ && grads_owned_) cudaFree(grads_);
-  if (cs_) cudaStreamDestroy(cs_);
-  if (ms_) cudaStreamDestroy(ms_);
+  grads_ = nullptr;
+  if (cs_) cudaStreamDestroy(cs_), cs_ = nullptr;
+  if (ms_) cudaStreamDestroy(ms_), ms_ = nullptr;
   cudaGetLastError();  // leave no stale error from the teardown calls for the next session
 }
 
 // ------------------------------------------------------------- program ----
-// Two-buffer (baseline) scheme: the plan provisions two network-max gradient
-// buffers (G2, simulator.hpp:259-264) and no per-layer dX. Assign every
-// producer's dX to one of them in backward order; a producer whose gradient
-// feeds the same fork as a live one accumulates into it (the fork sum).
-void Session::assign_two_buffer() {
-  std::vector<u64> g2;
-  for (const Event& e : plan_.events)
-    if (e.kind == Ev::Alloc && e.tag == "G2") g2.push_back(e.off);
-  g2_loc_.assign(static_cast<size_t>(L_), kNoOff);
-  g2_accum_.assign(static_cast<size_t>(L_), 0);
-  if (lv_.g2_bytes == 0) return;
-  if (g2.size() != 2) throw PlanError(Err::Generic, "two-buffer plan without two G2 buffers");
-  std::vector<int> left(static_cast<size_t>(L_), 0);
-  std::vector<int> slot_of(static_cast<size_t>(L_), -1);
-  std::vector<std::set<int>> occupants(2);
-  for (int m = L_ - 1; m >= 0; --m) {
-    const size_t i = static_cast<size_t>(m);
-    if (g_.at(m).kind == Kind::Input) continue;
-    if (lv_.grad[i] > 0) {
-      // fork accumulation: a live single-plane gradient w.r.t. the same tensor
-      const Node& l = g_.at(m);
-      int merge = -1;
-      std::vector<int> planes;
-      for (int q : l.in)
-        if (g_.at(g_.owner(q)).kind != Kind::Input) planes.push_back(q);
-      if (planes.size() == 1) {
-        for (int s = 0; s < 2 && merge < 0; ++s)
-          for (int p : occupants[static_cast<size_t>(s)]) {
-            const Node& pl = g_.at(p);
-            std::vector<int> pp;
-            for (int q : pl.in)
-              if (g_.at(g_.owner(q)).kind != Kind::Input) pp.push_back(q);
-            if (pp.size() == 1 && pp[0] == planes[0]) {
-              merge = p;
-              break;
-            }
-          }
-      }
-      if (merge >= 0) {
-        g2_loc_[i] = g2_loc_[static_cast<size_t>(merge)];
-        g2_accum_[i] = 1;
-        slot_of[i] = slot_of[static_cast<size_t>(merge)];
-      } else {
-        int s = occupants[0].empty() ? 0 : (occupants[1].empty() ? 1 : -1);
-        if (s < 0)
-          throw PlanError(Err::Config,
-                          "UNSUPPORTED: two-buffer gradient reuse needs more than two live gradient maps at layer " +
-                              std::to_string(m));
-        g2_loc_[i] = g2[static_cast<size_t>(s)];
-        slot_of[i] = s;
-      }
-      occupants[static_cast<size_t>(slot_of[i])].insert(m);
-      left[i] = static_cast<int>(lv_.grad_users[i].size());
-    }
-    // m's BWD consumed its dY: retire gradients whose readers are all done
-    for (int gb : lv_.grads_read[i]) {
-      const size_t gi = static_cast<size_t>(gb);
-      if (--left[gi] == 0) occupants[static_cast<size_t>(slot_of[gi])].erase(gb);
-    }
-    if (lv_.grad[i] > 0 && lv_.grad_users[i].empty()) occupants[static_cast<size_t>(slot_of[i])].erase(m);
-  }
-}
-
+// The planner's Program already binds every operand to its pool offset, lists
+// each step's transfers and the transfers its kernel waits for; this turns it
+// into the launch-ready step lists.
 void Session::build_program() {
-  const bool two = d_.scheme == Scheme::TwoBuffer;
-  if (two) assign_two_buffer();
-  std::vector<u64> feat(static_cast<size_t>(L_), kNoOff), grad(static_cast<size_t>(L_), kNoOff),
-      ws(static_cast<size_t>(L_), kNoOff);
-  u64 ws2 = kNoOff;
+  vdnnk::set_precise(o_.precise);  // scratch sizes depend on the contraction mode
   w_off_.assign(static_cast<size_t>(L_), kNoOff);
-  std::map<u64, u64> merged;  // fold map: plane location -> canonical location
-  auto canon = [&](u64 loc) {
-    while (merged.count(loc)) loc = merged[loc];
-    return loc;
+  for (int i = 0; i < L_; ++i) w_off_[static_cast<size_t>(i)] = prog_.w_off[static_cast<size_t>(i)];
+  x_off_ = prog_.input_off;
+  input_idle_after_ = prog_.input_idle_after;
+  auto transfer = [&](int xi) {
+    const vdnnp::Xfer& x = prog_.xfers[static_cast<size_t>(xi)];
+    Transfer t;
+    t.owner = x.owner;
+    t.bytes = x.bytes;
+    t.dev_off = x.dev_off;
+    t.host_off = host_slot_[static_cast<size_t>(x.owner)];
+    t.ev = xi;
+    t.zvc = compressible(x.owner) && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes);
+    t.tf32 = t.zvc && o_.compress_offload == 2 && tf32_exact_ok(x.owner);
+    return t;
   };
-  // plane offset (bytes) of input j inside producer g's dX buffer
-  auto plane_rel = [&](int gprod, int j) -> u64 {
-    const Node& l = g_.at(gprod);
-    u64 off = 0;
-    for (int k = 0; k < j; ++k) {
-      const int q = l.in[static_cast<size_t>(k)];
-      if (g_.at(g_.owner(q)).kind == Kind::Input) continue;
-      off += c_.bytes_of(g_.dims(q));
-    }
-    return off;
-  };
-  auto grad_base = [&](int gprod) -> u64 { return two ? g2_loc_[static_cast<size_t>(gprod)] : grad[static_cast<size_t>(gprod)]; };
-
-  std::vector<Transfer> pending;  // prefetches since the last BWD
-  int xfer = 0, step = 0;
-  bool in_fwd = true;
-  for (const Event& e : plan_.events) {
-    const size_t b = e.buffer >= 0 ? static_cast<size_t>(e.buffer) : 0;
-    switch (e.kind) {
-      case Ev::Alloc:
-        if (e.tag == "X" || e.tag == "Y") {
-          feat[b] = e.off;
-          if (e.buffer == input_id_ && e.layer == input_id_ && x_off_ == 0 && in_fwd) x_off_ = e.off;
-        } else if (e.tag == "dX") {
-          grad[b] = e.off;
-        } else if (e.tag == "W") {
-          w_off_[b] = e.off;
-        } else if (e.tag == "WS") {
-          if (e.buffer < 0) ws2 = e.off;
-          else ws[b] = e.off;
-        }
-        break;
-      case Ev::Fwd: {
-        FwdStep s;
-        s.layer = e.layer;
-        const Node& l = g_.at(e.layer);
-        for (int q : l.in) s.in_off.push_back(feat[static_cast<size_t>(g_.owner(q))]);
-        if (l.kind == Kind::Actv)
-          s.out_off = feat[static_cast<size_t>(g_.owner(e.layer))];
-        else if (l.kind != Kind::Loss)
-          s.out_off = feat[static_cast<size_t>(e.layer)];
-        s.w_off = w_off_[static_cast<size_t>(e.layer)];
-        const u64 wsb = lv_.wsbytes[static_cast<size_t>(e.layer)];
-        if (wsb > 0) {
-          s.ws_off = two ? ws2 : ws[static_cast<size_t>(e.layer)];
-          s.ws_bytes = wsb;
-        }
-        s.ev = step++;
-        fwd_.push_back(s);
-        break;
+  auto or_none = [](u64 v) { return v == vdnnp::kNoLoc ? kNoOff : v; };
+  for (size_t si = 0; si < prog_.steps.size(); ++si) {
+    const vdnnp::Step& p = prog_.steps[si];
+    const Node& l = g_.at(p.layer);
+    const bool contraction = l.kind == Kind::Conv || l.kind == Kind::Fc;
+    if (!p.bwd) {
+      FwdStep s;
+      s.layer = p.layer;
+      s.ev = static_cast<int>(si);
+      for (u64 v : p.x) s.in_off.push_back(or_none(v));
+      s.out_off = or_none(p.y);
+      s.w_off = or_none(p.w);
+      if (p.ws_bytes > 0) s.ws_off = or_none(p.ws), s.ws_bytes = p.ws_bytes;
+      for (int xi : p.issues) s.offloads.push_back(transfer(xi));
+      s.gap_off = p.gap_off;
+      s.gap_len = p.gap_len;
+      if (contraction) s.scratch = vdnnk::conv_fprop_ws_bytes(conv_args(s.layer, s.in_off, nullptr));
+      fwd_.push_back(std::move(s));
+    } else {
+      BwdStep s;
+      s.layer = p.layer;
+      s.ev = static_cast<int>(si);
+      for (int xi : p.issues) s.prefetches.push_back(transfer(xi));
+      s.wait_prefetch = p.wait_before;
+      for (u64 v : p.x) s.in_off.push_back(or_none(v));
+      s.out_off = or_none(p.y);
+      s.w_off = or_none(p.w);
+      if (p.ws_bytes > 0) s.ws_off = or_none(p.ws), s.ws_bytes = p.ws_bytes;
+      for (const vdnnp::PlaneRef& pl : p.dx) s.plane_off.push_back(or_none(pl.off));
+      s.accumulate = p.dx_accumulate;
+      for (const vdnnp::PlaneRef& pl : p.dy) s.dy_off.push_back(pl.off);
+      s.mask_plane.assign(s.plane_off.size(), 0);
+      s.gap_off = p.gap_off;
+      s.gap_len = p.gap_len;
+      if (contraction) {
+        s.scratch = vdnnk::conv_wgrad_ws_bytes(conv_args(s.layer, s.in_off, nullptr));
+        if (!s.plane_off.empty())
+          s.scratch = std::max(s.scratch, vdnnk::conv_dgrad_ws_bytes(conv_args(s.layer, s.in_off, &s.plane_off)));
       }
-      case Ev::Offload: {
-        Transfer t;
-        t.owner = e.buffer;
-        t.bytes = e.bytes;
-        t.dev_off = feat[b];
-        t.host_off = host_slot_[b];
-        t.ev = xfer++;
-        t.zvc = compressible(e.buffer) && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes);
-        t.tf32 = t.zvc && o_.compress_offload == 2 && tf32_exact_ok(e.buffer);
-        fwd_.back().offloads.push_back(t);
-        break;
-      }
-      case Ev::Prefetch: {
-        in_fwd = false;
-        Transfer t;
-        t.owner = e.buffer;
-        t.bytes = e.bytes;
-        t.dev_off = feat[b];  // the ALLOC logged just before on the memory stream
-        t.host_off = host_slot_[b];
-        t.ev = xfer++;
-        t.zvc = compressible(e.buffer) && vdnnk::zvc_eligible(base_ + t.dev_off, t.bytes);
-        t.tf32 = t.zvc && o_.compress_offload == 2 && tf32_exact_ok(e.buffer);
-        pending.push_back(t);
-        break;
-      }
-      case Ev::Bwd: {
-        in_fwd = false;
-        BwdStep s;
-        s.layer = e.layer;
-        const int m = e.layer;
-        const size_t mi = static_cast<size_t>(m);
-        const Node& l = g_.at(m);
-        s.prefetches = pending;
-        pending.clear();
-        for (const Transfer& t : s.prefetches)
-          if (std::find(lv_.bwd_reads[mi].begin(), lv_.bwd_reads[mi].end(), t.owner) != lv_.bwd_reads[mi].end())
-            s.wait_prefetch.push_back(t.ev);
-        for (int q : l.in) s.in_off.push_back(feat[static_cast<size_t>(g_.owner(q))]);
-        if (l.kind == Kind::Actv)
-          s.out_off = feat[static_cast<size_t>(g_.owner(m))];
-        else if (l.kind == Kind::Pool)
-          s.out_off = feat[mi];
-        s.w_off = w_off_[mi];
-        const u64 wsb = lv_.wsbytes[mi];
-        if (wsb > 0) {
-          s.ws_off = two ? ws2 : ws[mi];
-          s.ws_bytes = wsb;
-        }
-        if (lv_.grad[mi] > 0) {
-          const u64 base = grad_base(m);
-          for (size_t j = 0; j < l.in.size(); ++j) {
-            const int q = l.in[j];
-            if (g_.at(g_.owner(q)).kind == Kind::Input)
-              s.plane_off.push_back(kNoOff);
-            else
-              s.plane_off.push_back(base + plane_rel(m, static_cast<int>(j)));
-          }
-          if (two) s.accumulate = g2_accum_[mi] != 0;
-        }
-        // incoming gradient planes: for each gradient buffer m reads, the
-        // planes whose input chain passes through m
-        std::vector<u64> dy;
-        for (int gb : lv_.grads_read[mi]) {
-          const Node& gl = g_.at(gb);
-          for (size_t j = 0; j < gl.in.size(); ++j) {
-            int cur = gl.in[j];
-            bool hit = false;
-            while (true) {
-              if (cur == m) {
-                hit = true;
-                break;
-              }
-              if (g_.at(cur).kind != Kind::Actv) break;
-              cur = g_.at(cur).in[0];
-            }
-            if (!hit) continue;
-            const u64 loc = canon(grad_base(gb) + plane_rel(gb, static_cast<int>(j)));
-            if (std::find(dy.begin(), dy.end(), loc) == dy.end()) dy.push_back(loc);
-          }
-        }
-        for (size_t k = 1; k < dy.size(); ++k) merged[dy[k]] = dy[0];  // this step folds them
-        s.dy_off = dy;
-        s.ev = step++;
-        bwd_.push_back(s);
-        break;
-      }
-      default:
-        break;
+      bwd_.push_back(std::move(s));
     }
   }
   fuse_relus();
-  if (x_off_ == 0) x_off_ = feat[static_cast<size_t>(input_id_)];
-  // the setup allocation of the INPUT layer (first ALLOC X of buffer input_id_)
-  for (const Event& e : plan_.events)
-    if (e.kind == Ev::Alloc && e.buffer == input_id_ && (e.tag == "X" || e.tag == "Y")) {
-      x_off_ = e.off;
-      break;
-    }
+}
+
+float* Session::scratch_for(u64 gap_off, u64 gap_len, size_t need) const {
+  if (need == 0) return nullptr;
+  return need <= gap_len ? F(gap_off) : splitk_;
 }
 
 // Compressed mode moves a buffer through the SMs only when it holds ReLU
@@ -496,14 +344,14 @@ bool Session::compressible(int owner) const {
 //  * FWD: a conv/FC whose only consumer is an ACTV applies max(0, .) in its
 //    epilogue; the ACTV's FWD launches nothing (nothing else reads the
 //    pre-activation values, and the buffer is the same in-place alias).
-//  * BWD: an ACTV whose single incoming gradient plane is written by exactly
-//    one producer step (conv/FC dgrad or pool bwd) that reads the ACTV's
-//    output as its input x gets its mask (x > 0) applied in that producer's
-//    epilogue; the ACTV's BWD launches nothing.
+//  * BWD: the planner names, for an ACTV whose incoming plane has exactly one
+//    writer (a conv/FC dgrad or pool backward reading the ACTV's output as
+//    that input, nothing folded or accumulated into the plane), that writer's
+//    step (Step::mask_host); its epilogue applies the mask (x > 0) and the
+//    ACTV's BWD launches nothing.
 void Session::fuse_relus() {
-  std::vector<int> fwd_at(static_cast<size_t>(L_), -1), bwd_at(static_cast<size_t>(L_), -1);
+  std::vector<int> fwd_at(static_cast<size_t>(L_), -1);
   for (size_t i = 0; i < fwd_.size(); ++i) fwd_at[static_cast<size_t>(fwd_[i].layer)] = static_cast<int>(i);
-  for (size_t i = 0; i < bwd_.size(); ++i) bwd_at[static_cast<size_t>(bwd_[i].layer)] = static_cast<int>(i);
   for (FwdStep& s : fwd_) {
     const Node& l = g_.at(s.layer);
     if (l.kind != Kind::Conv && l.kind != Kind::Fc) continue;
@@ -514,28 +362,12 @@ void Session::fuse_relus() {
     s.relu = true;
     fwd_[static_cast<size_t>(fa)].skip = true;
   }
-  // the producer of an ACTV's incoming gradient is the last step before it
-  // (in backward order) that wrote that location: with two-buffer reuse the
-  // same G2 offsets are rewritten by many steps, so "last writer" is the key
-  for (BwdStep& s : bwd_) s.mask_plane.assign(s.plane_off.size(), 0);
-  for (size_t ai = 0; ai < bwd_.size(); ++ai) {
-    BwdStep& a = bwd_[ai];
-    if (g_.at(a.layer).kind != Kind::Actv || a.dy_off.size() != 1) continue;
-    int pi = -1, pj = -1;
-    for (size_t k = ai; k-- > 0 && pi < 0;)
-      for (size_t j = 0; j < bwd_[k].plane_off.size(); ++j)
-        if (bwd_[k].plane_off[j] == a.dy_off[0]) {
-          pi = static_cast<int>(k);
-          pj = static_cast<int>(j);
-          break;
-        }
-    if (pi < 0) continue;
-    BwdStep& prod = bwd_[static_cast<size_t>(pi)];
-    const Node& pl = g_.at(prod.layer);
-    if (pl.kind != Kind::Conv && pl.kind != Kind::Fc && pl.kind != Kind::Pool) continue;
-    if (pl.in[static_cast<size_t>(pj)] != a.layer) continue;
-    if (prod.accumulate) continue;
-    prod.mask_plane[static_cast<size_t>(pj)] = 1;
+  const size_t nf = fwd_.size();
+  for (BwdStep& a : bwd_) {
+    const vdnnp::Step& p = prog_.steps[static_cast<size_t>(a.ev)];
+    if (p.mask_host < 0 || static_cast<size_t>(p.mask_host) < nf) continue;
+    BwdStep& host = bwd_[static_cast<size_t>(p.mask_host) - nf];
+    host.mask_plane[static_cast<size_t>(p.mask_slot)] = 1;
     a.skip = true;
   }
 }
@@ -574,12 +406,12 @@ vdnnk::ConvArgs Session::conv_args(int layer, const std::vector<u64>& in_off,
 void Session::init_weights() {
   for (const Node& l : g_.nodes()) {
     const size_t i = static_cast<size_t>(l.id);
-    if (lv_.wbytes[i] == 0) continue;
+    if (df_.at[i].w_bytes == 0) continue;
     float* w = F(w_off_[i]);
     const u64 seed = o_.weight_seed + static_cast<u64>(l.id);
     if (l.kind == Kind::Conv) {
       const u64 fan = l.k * l.k * g_.in_dims(l.id).c;
-      check(vdnnk::fill_normal(w, lv_.wbytes[i] / 4, std::sqrt(2.0f / static_cast<float>(fan)), seed, cs_), "init");
+      check(vdnnk::fill_normal(w, df_.at[i].w_bytes / 4, std::sqrt(2.0f / static_cast<float>(fan)), seed, cs_), "init");
     } else {
       const u64 in = g_.fc_inputs(l.id);
       check(vdnnk::fill_normal(w, in * l.out, std::sqrt(2.0f / static_cast<float>(in)), seed, cs_), "init");
@@ -619,7 +451,9 @@ void Session::run_fwd(const FwdStep& s, float lr) {
       vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
       a.relu_out = s.relu ? 1 : 0;
       const float* bias = l.kind == Kind::Fc ? F(s.w_off) + g_.fc_inputs(s.layer) * l.out : nullptr;
-      check(vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_, splitk_, splitk_bytes_), "conv_fprop");
+      check(vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_, scratch_for(s.gap_off, s.gap_len, s.scratch),
+                              s.scratch),
+            "conv_fprop");
       break;
     }
     case Kind::Actv:
@@ -652,6 +486,7 @@ void Session::run_fwd(const FwdStep& s, float lr) {
   if (timed_) check(cudaEventRecord(ev_[2 * s.ev + 1], cs_), "record");
   if (!s.offloads.empty())  // sync rule: FWD(n+1) may not start before n's offloads drain
     check(cudaStreamWaitEvent(cs_, xfer_ev_[static_cast<size_t>(s.offloads.back().ev)], 0), "wait");
+  if (s.ev == input_idle_after_) check(cudaEventRecord(input_idle_ev_, cs_), "record");
 }
 
 void Session::run_bwd(const BwdStep& s, float lr) {
@@ -692,14 +527,18 @@ void Session::run_bwd(const BwdStep& s, float lr) {
       if (!s.plane_off.empty()) {
         vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off);
         for (int i = 0; i < a.nseg; ++i) a.mask_in[i] = s.mask_plane[static_cast<size_t>(i)];
-        check(vdnnk::conv_dgrad(a, F(s.w_off), dy, s.accumulate, cs_, splitk_, splitk_bytes_), "conv_dgrad");
+        check(vdnnk::conv_dgrad(a, F(s.w_off), dy, s.accumulate, cs_, scratch_for(s.gap_off, s.gap_len, s.scratch),
+                                s.scratch),
+              "conv_dgrad");
       }
       const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
-      // split-K partials live in a fixed non-pool scratch so the reduction
-      // order (and hence every bit of the update) is independent of the
-      // offload policy and of the algorithm's workspace extent
+      // split-K partials: the split count depends only on the layer shape
+      // (the launch always gets the bytes it asks for), so the reduction
+      // order -- and every bit of the update -- is independent of the offload
+      // policy and of where the partials live
       float* dw = grads_ ? grads_ + grad_off_[mi] : nullptr;
-      check(vdnnk::conv_wgrad(a, dy, F(s.w_off), lr, dw, splitk_, splitk_bytes_, cs_), "conv_wgrad");
+      check(vdnnk::conv_wgrad(a, dy, F(s.w_off), lr, dw, scratch_for(s.gap_off, s.gap_len, s.scratch), s.scratch, cs_),
+            "conv_wgrad");
       if (fc) {
         const u64 in = g_.fc_inputs(s.layer);
         float* bias = F(s.w_off) + in * l.out;
@@ -747,6 +586,7 @@ void Session::run_bwd(const BwdStep& s, float lr) {
   if (timed_) check(cudaEventRecord(ev_[2 * s.ev + 1], cs_), "record");
   if (!s.prefetches.empty())  // prefetches launched here land before the next BWD
     check(cudaStreamWaitEvent(cs_, xfer_ev_[static_cast<size_t>(s.prefetches.back().ev)], 0), "wait");
+  if (s.ev == input_idle_after_) check(cudaEventRecord(input_idle_ev_, cs_), "record");
 }
 
 void Session::step(float lr, float* loss_host) {
@@ -770,14 +610,10 @@ void Session::step(float lr, float* loss_host) {
     std::swap(t0_ev_, t0_ev_prev_);
     std::swap(ev_iter_, ev_iter_prev_);
   }
-  if (has_staged_) {  // the batch prefetch_batch_host staged: into the INPUT extent, then free the buffer
-    const u64 bytes = lv_.feat[static_cast<size_t>(input_id_)];
+  if (has_staged_) {  // the batch prefetch_batch_host put in the INPUT extent (+ its labels) has landed
     check(cudaStreamWaitEvent(cs_, staged_ready_, 0), "wait");
-    if (staged_images_) check(cudaMemcpyAsync(F(x_off_), staging_, bytes, cudaMemcpyDeviceToDevice, cs_), "images D2D");
-    if (staged_labels_)
-      check(cudaMemcpyAsync(labels_, staging_ + bytes, static_cast<u64>(g_.batch()) * 4, cudaMemcpyDeviceToDevice, cs_),
-            "labels D2D");
-    check(cudaEventRecord(staging_free_, cs_), "record");
+    check(cudaMemcpyAsync(labels_, labels_next_, static_cast<u64>(g_.batch()) * 4, cudaMemcpyDeviceToDevice, cs_),
+          "labels D2D");
     has_staged_ = false;
   }
   if (!o_.cuda_graph || eager_steps_ < 1) {
@@ -843,37 +679,37 @@ void Session::synchronize() {
 }
 
 void Session::set_batch_host(const float* images, const int32_t* labels) {
-  const u64 bytes = lv_.feat[static_cast<size_t>(input_id_)];
+  const u64 bytes = df_.at[static_cast<size_t>(input_id_)].bytes;
   if (images) check(cudaMemcpyAsync(F(x_off_), images, bytes, cudaMemcpyHostToDevice, cs_), "images H2D");
   if (labels) check(cudaMemcpyAsync(labels_, labels, g_.batch() * 4, cudaMemcpyHostToDevice, cs_), "labels H2D");
 }
 
 void Session::set_batch_device(const float* images, const int32_t* labels) {
-  const u64 bytes = lv_.feat[static_cast<size_t>(input_id_)];
+  const u64 bytes = df_.at[static_cast<size_t>(input_id_)].bytes;
   if (images) check(cudaMemcpyAsync(F(x_off_), images, bytes, cudaMemcpyDeviceToDevice, cs_), "images D2D");
   if (labels) check(cudaMemcpyAsync(labels_, labels, g_.batch() * 4, cudaMemcpyDeviceToDevice, cs_), "labels D2D");
 }
 
 void Session::prefetch_batch_host(const float* images, const int32_t* labels) {
-  const u64 bytes = lv_.feat[static_cast<size_t>(input_id_)];
+  const u64 bytes = df_.at[static_cast<size_t>(input_id_)].bytes;
   const u64 lbytes = static_cast<u64>(g_.batch()) * 4;
+  if (has_staged_) throw PlanError(Err::Generic, "a prefetched batch is already waiting for the next step");
   if (!in_stream_) {
     check(cudaStreamCreateWithFlags(&in_stream_, cudaStreamNonBlocking), "stream");
-    check(cudaMalloc(&staging_, bytes + lbytes), "cudaMalloc(input staging)");
-    scratch_bytes_ += bytes + lbytes;
     check(cudaEventCreateWithFlags(&staged_ready_, cudaEventDisableTiming), "event");
-    check(cudaEventCreateWithFlags(&staging_free_, cudaEventDisableTiming), "event");
-    check(cudaEventRecord(staging_free_, cs_), "record");
   }
-  if (has_staged_) throw PlanError(Err::Generic, "a prefetched batch is already waiting for the next step");
-  // the previous staged batch has been copied out of the buffer
-  check(cudaStreamWaitEvent(in_stream_, staging_free_, 0), "wait");
-  if (images) check(cudaMemcpyAsync(staging_, images, bytes, cudaMemcpyHostToDevice, in_stream_), "images H2D");
-  if (labels) check(cudaMemcpyAsync(staging_ + bytes, labels, lbytes, cudaMemcpyHostToDevice, in_stream_), "labels H2D");
+  // the last enqueued step records input_idle_ev_ once nothing it runs
+  // touches the INPUT extent any more (or at its end); the previous staged
+  // labels were consumed at that step's start
+  check(cudaStreamWaitEvent(in_stream_, input_idle_ev_, 0), "wait");
+  if (images) check(cudaMemcpyAsync(F(x_off_), images, bytes, cudaMemcpyHostToDevice, in_stream_), "images H2D");
+  if (labels) {
+    check(cudaMemcpyAsync(labels_next_, labels, lbytes, cudaMemcpyHostToDevice, in_stream_), "labels H2D");
+  } else {
+    check(cudaMemcpyAsync(labels_next_, labels_, lbytes, cudaMemcpyDeviceToDevice, in_stream_), "labels keep");
+  }
   check(cudaEventRecord(staged_ready_, in_stream_), "record");
   has_staged_ = true;
-  staged_images_ = images != nullptr;
-  staged_labels_ = labels != nullptr;
 }
 
 int64_t Session::queue_loss() {
@@ -904,6 +740,7 @@ void Session::enqueue_step(float lr) {
   check(cudaStreamWaitEvent(ms_, ev_sync_, 0), "wait");
   for (const FwdStep& s : fwd_) run_fwd(s, lr);
   for (const BwdStep& s : bwd_) run_bwd(s, lr);
+  if (input_idle_after_ < 0) check(cudaEventRecord(input_idle_ev_, cs_), "record");
 }
 
 float Session::read_loss() {
@@ -913,7 +750,7 @@ float Session::read_loss() {
 }
 
 void Session::synthetic_batch(u64 seed) {
-  const u64 count = lv_.feat[static_cast<size_t>(input_id_)] / 4;
+  const u64 count = df_.at[static_cast<size_t>(input_id_)].bytes / 4;
   check(vdnnk::fill_uniform(F(x_off_), count, -1.0f, 1.0f, seed, cs_), "images");
   check(vdnnk::fill_labels(labels_, g_.batch(), classes_, seed + 1, cs_), "labels");
 }
@@ -921,7 +758,7 @@ void Session::synthetic_batch(u64 seed) {
 void Session::get_weights(int layer, float* host, size_t count) {
   if (layer < 0 || layer >= L_ || w_off_[static_cast<size_t>(layer)] == kNoOff)
     throw PlanError(Err::Generic, "layer has no weights");
-  if (count * 4 != lv_.wbytes[static_cast<size_t>(layer)]) throw PlanError(Err::Generic, "weight count mismatch");
+  if (count * 4 != df_.at[static_cast<size_t>(layer)].w_bytes) throw PlanError(Err::Generic, "weight count mismatch");
   synchronize();
   check(cudaMemcpy(host, F(w_off_[static_cast<size_t>(layer)]), count * 4, cudaMemcpyDeviceToHost), "D2H");
 }
@@ -929,7 +766,7 @@ void Session::get_weights(int layer, float* host, size_t count) {
 void Session::set_weights(int layer, const float* host, size_t count) {
   if (layer < 0 || layer >= L_ || w_off_[static_cast<size_t>(layer)] == kNoOff)
     throw PlanError(Err::Generic, "layer has no weights");
-  if (count * 4 != lv_.wbytes[static_cast<size_t>(layer)]) throw PlanError(Err::Generic, "weight count mismatch");
+  if (count * 4 != df_.at[static_cast<size_t>(layer)].w_bytes) throw PlanError(Err::Generic, "weight count mismatch");
   synchronize();
   check(cudaMemcpy(F(w_off_[static_cast<size_t>(layer)]), host, count * 4, cudaMemcpyHostToDevice), "H2D");
 }
@@ -942,7 +779,7 @@ void Session::read_feature(int owner, float* host, size_t count) {
   for (const Event& e : plan_.events)
     if (e.kind == Ev::Alloc && e.buffer == owner && (e.tag == "X" || e.tag == "Y")) off = e.off;
   if (off == kNoOff) throw PlanError(Err::Generic, "owner has no feature buffer");
-  if (count * 4 > lv_.feat[static_cast<size_t>(owner)]) throw PlanError(Err::Generic, "count too large");
+  if (count * 4 > df_.at[static_cast<size_t>(owner)].bytes) throw PlanError(Err::Generic, "count too large");
   check(cudaMemcpy(host, F(off), count * 4, cudaMemcpyDeviceToHost), "D2H");
 }
 
@@ -953,7 +790,7 @@ void Session::grad_buffer(int layer, void** ptr, size_t* count) {
     return;
   }
   *ptr = grads_ + grad_off_[static_cast<size_t>(layer)];
-  *count = lv_.wbytes[static_cast<size_t>(layer)] / 4;
+  *count = df_.at[static_cast<size_t>(layer)].w_bytes / 4;
 }
 
 void Session::grad_arena(void** ptr, size_t* count) {
@@ -975,7 +812,7 @@ void Session::apply_grads(float lr, float scale) {
   for (int i = 0; i < L_; ++i) {
     const size_t k = static_cast<size_t>(i);
     if (grad_off_[k] == kNoOff) continue;
-    check(vdnnk::sgd_update(F(w_off_[k]), grads_ + grad_off_[k], lr * scale, lv_.wbytes[k] / 4, cs_), "sgd");
+    check(vdnnk::sgd_update(F(w_off_[k]), grads_ + grad_off_[k], lr * scale, df_.at[k].w_bytes / 4, cs_), "sgd");
   }
 }
 

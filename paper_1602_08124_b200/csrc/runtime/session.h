@@ -42,13 +42,6 @@ struct Options {
   bool cuda_graph = false;
 };
 
-// One gradient plane: the slice of a dX buffer that holds the gradient w.r.t.
-// one input of its producer (split-plane layout for concat joins).
-struct Plane {
-  int producer = -1;  // layer whose BWD writes the buffer
-  int index = 0;      // which input of the producer
-};
-
 struct Transfer {
   int owner = -1;
   u64 bytes = 0;
@@ -59,6 +52,8 @@ struct Transfer {
   bool tf32 = false; // compressed mode 2 and only TF32 consumers read it in backward
 };
 
+// Runtime form of one planned compute step (vdnnp::Step), with the pieces
+// the launch code needs resolved.
 struct FwdStep {
   int layer = -1;
   std::vector<u64> in_off;   // feature offsets of the layer's inputs (in input order, via owners)
@@ -69,6 +64,8 @@ struct FwdStep {
   int ev = -1;
   bool relu = false;  // conv/FC: ReLU of the following ACTV fused into the epilogue
   bool skip = false;  // ACTV whose ReLU was fused into its producer
+  u64 gap_off = 0, gap_len = 0;  // free pool segment while the kernel runs
+  size_t scratch = 0;            // split-K partial bytes the launch needs
 };
 
 struct BwdStep {
@@ -85,6 +82,8 @@ struct BwdStep {
   int ev = -1;
   std::vector<char> mask_plane;         // per input: ReLU backward of that input fused here
   bool skip = false;                    // ACTV whose backward was fused into its gradient's producer
+  u64 gap_off = 0, gap_len = 0;         // free pool segment while the kernel runs
+  size_t scratch = 0;                   // split-K partial bytes the launches need
 };
 
 class Session {
@@ -96,9 +95,10 @@ class Session {
 
   void set_batch_host(const float* images, const int32_t* labels);
   void set_batch_device(const float* images, const int32_t* labels);
-  // Input pipeline: stage the NEXT batch from pinned host memory into a
-  // device staging buffer on a separate stream (overlapping the running
-  // step); the next step() moves it into the INPUT extent first thing.
+  // Input pipeline: copy the NEXT batch from pinned host memory straight into
+  // the INPUT extent on a separate stream, as soon as the running step no
+  // longer touches that extent (planned, Program::input_idle_after); the next
+  // step() waits for it. No staging buffer outside the pool.
   void prefetch_batch_host(const float* images, const int32_t* labels);
   // Loss of the last step (D2H + sync), for callers that issue step()
   // without reading the loss and prefetch the next batch first.
@@ -151,12 +151,14 @@ class Session {
 
  private:
   float* F(u64 off) const { return reinterpret_cast<float*>(base_ + off); }
+  void acquire();
+  void release() noexcept;
   void build_program();
   void fuse_relus();
+  float* scratch_for(u64 gap_off, u64 gap_len, size_t need) const;
   bool compressible(int owner) const;
   int sm_reserve_ = -1;  // SMs left to the compressed-transfer kernels (set on the first step)
   bool tf32_exact_ok(int owner) const;
-  void assign_two_buffer();
   void init_weights();
   void run_fwd(const FwdStep& s, float lr);
   void run_bwd(const BwdStep& s, float lr);
@@ -169,7 +171,8 @@ class Session {
   u64 cap_;
   Options o_;
   vdnnp::Report plan_;
-  vdnnp::Liveness lv_;
+  vdnnp::Program prog_;   // the plan's executable form (bound offsets, transfers, waits)
+  vdnnp::Dataflow df_;
   int L_ = 0;
   int input_id_ = -1, loss_id_ = -1, logits_owner_ = -1;
   int classes_ = 0;
@@ -190,17 +193,22 @@ class Session {
   float* row_loss_ = nullptr;
   float* loss_ = nullptr;
   int32_t* labels_ = nullptr;
-  float* splitk_ = nullptr;
+  float* splitk_ = nullptr;      // split-K partials for steps whose free pool gap is too small
   size_t splitk_bytes_ = 0;
+  size_t splitk_in_pool_ = 0;    // steps whose partials live in the pool's free gap
   float* grads_ = nullptr;       // external gradient arena
   bool grads_owned_ = true;
   std::vector<u64> grad_off_;    // per layer float offset into grads_
   size_t grads_count_ = 0;
   float* pinned_loss_ = nullptr;
-  cudaStream_t in_stream_ = nullptr;      // input pipeline stream (prefetch_batch_host)
-  char* staging_ = nullptr;               // next batch: images then labels
-  cudaEvent_t staged_ready_ = nullptr, staging_free_ = nullptr;
-  bool has_staged_ = false, staged_images_ = false, staged_labels_ = false;
+  // input pipeline (prefetch_batch_host): the next batch lands directly in
+  // the INPUT extent once the running step no longer touches it
+  // (Program::input_idle_after); labels alternate between two slots
+  cudaStream_t in_stream_ = nullptr;
+  cudaEvent_t input_idle_ev_ = nullptr;   // recorded by every step after its idle point
+  cudaEvent_t staged_ready_ = nullptr;
+  int32_t* labels_next_ = nullptr;        // the other label slot
+  bool has_staged_ = false;
   static constexpr int kLossRing = 4;
   float* loss_ring_ = nullptr;            // pinned, kLossRing slots
   cudaEvent_t loss_ev_[kLossRing] = {};
@@ -222,12 +230,10 @@ class Session {
   unsigned long long peer_epoch_ = 0;
 
   u64 x_off_ = 0;                // INPUT feature extent (setup allocation)
+  int input_idle_after_ = -1;    // step after which the INPUT extent may take the next batch
   std::vector<u64> w_off_;       // per layer weight offset
   std::vector<FwdStep> fwd_;
   std::vector<BwdStep> bwd_;
-  // two-buffer scheme: dX location per producer
-  std::vector<u64> g2_loc_;
-  std::vector<char> g2_accum_;
 
   // timing
   std::vector<cudaEvent_t> ev_;  // pairs: [2i] start, [2i+1] end
