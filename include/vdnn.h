@@ -347,6 +347,34 @@ vdnn_status vdnn_session_spill_export(vdnn_session* s, uint8_t ipc_handle[64]);
 vdnn_status vdnn_session_spill_attach(vdnn_session* s, const uint8_t ipc_handle[64]);
 /* Compute stream (cudaStream_t) for interop. */
 vdnn_status vdnn_session_stream(vdnn_session* s, void** stream);
+/* Layer-local probe (parity tests; not a reference entry point). During the next vdnn_session_step,
+ * the operands of one compute step -- FWD (bwd = 0) or BWD (bwd = 1) of `layer` -- are copied into a
+ * caller-provided device buffer: what its kernels read, right before they run, and what they wrote,
+ * right after (stream-ordered on the compute stream; one-shot; not in cuda_graph mode). The layout
+ * lists the segments (offset/bytes in the destination) and the fusions the step applies:
+ *   X[i]: input i (NHWC fp32); W: weights (index 1 = after an in-step SGD); Y: output;
+ *   DY: incoming gradient (after the fold of the other planes); DX_BEFORE[i] / DX[i]: gradient plane of
+ *   input i before (two-buffer accumulation) / after; DW: dW (+bias grad) in the gradient arena;
+ *   LOSS_GRAD (N x classes softmax gradient), LOSS (scalar). */
+enum { VDNN_PROBE_X = 0, VDNN_PROBE_W = 1, VDNN_PROBE_Y = 2, VDNN_PROBE_DY = 3, VDNN_PROBE_DX_BEFORE = 4,
+       VDNN_PROBE_DX = 5, VDNN_PROBE_DW = 6, VDNN_PROBE_LOSS_GRAD = 7, VDNN_PROBE_LOSS = 8 };
+#define VDNN_PROBE_MAX_SEGS 40
+typedef struct vdnn_probe_seg {
+  int32_t what, index, after, pad_;
+  uint64_t offset, bytes;
+} vdnn_probe_seg;
+typedef struct vdnn_probe_layout {
+  int32_t nseg;
+  int32_t relu_fused;    /* FWD: the next ACTV's ReLU applied in the epilogue */
+  int32_t accumulate;    /* BWD: dX added into a plane holding a fork gradient */
+  int32_t skip;          /* ACTV fused into a neighbour: launches nothing */
+  uint32_t mask_planes;  /* BWD: bit i = dX[i] masked by (X[i] > 0) in the epilogue */
+  uint32_t pad_;
+  uint64_t total_bytes;
+  vdnn_probe_seg seg[VDNN_PROBE_MAX_SEGS];
+} vdnn_probe_layout;
+vdnn_status vdnn_session_probe_layout(vdnn_session* s, int32_t layer, int32_t bwd, vdnn_probe_layout* out);
+vdnn_status vdnn_session_arm_probe(vdnn_session* s, int32_t layer, int32_t bwd, void* dst_dev, uint64_t dst_bytes);
 uint64_t vdnn_kernel_launch_count(void);
 
 /* ------------------------------------------ kernel-level entry points ---- */

@@ -305,3 +305,166 @@ def he_weights(g, cost=None, seed: int = 5000) -> Dict[int, np.ndarray]:
             w = (rng.standard_normal(outf * fin) * np.sqrt(2.0 / fin)).astype(np.float32)
             out[l.id] = np.concatenate([w, np.zeros(outf, np.float32)])
     return out
+
+
+# ------------------------------------------------------------------------------
+# Layer-local ops (ORACLE ONLY): one layer's FWD or BWD evaluated on the very
+# operands a B200 step's kernels read (Session.probe_step), so every kernel is
+# checked at the single-contraction bound instead of through a whole network.
+# Same definitions as train_step above; the dataflow of each op follows
+# simulator.hpp:90-131 (operands: CONV/FC read X, POOL reads X (+Y), ACTV its
+# aliased Y) and footprint.hpp:60-71 (one gradient plane per non-INPUT input;
+# an elementwise join shares one plane).
+# ------------------------------------------------------------------------------
+
+def _join(l: Layer, xs: List[torch.Tensor], flatten: bool) -> torch.Tensor:
+    parts = [x.reshape(x.shape[0], -1) if flatten else x for x in xs]
+    if l.join == 1 and len(parts) > 1:  # elementwise: sum
+        out = parts[0]
+        for p in parts[1:]:
+            out = out + p
+        return out
+    return torch.cat(parts, dim=1 if flatten else 3)
+
+
+def _split(l: Layer, L: List[Layer], full: torch.Tensor, flatten: bool) -> List[torch.Tensor]:
+    """Gradient w.r.t. the joined input -> per-input planes (elementwise: the
+    same gradient for every input)."""
+    out, off = [], 0
+    for q in l.inputs:
+        n, c, h, w = L[q].shape
+        shape = (full.shape[0], h, w, c)  # the batch may be a leading sample
+        if l.join == 1 and len(l.inputs) > 1:
+            out.append(full.reshape(shape))
+            continue
+        cc = c * h * w if flatten else c
+        part = full[:, off:off + cc] if flatten else full[..., off:off + cc]
+        out.append(part.reshape(shape))
+        off += cc
+    return out
+
+
+def layer_forward(g, layer: int, xs: List[torch.Tensor], w: torch.Tensor = None, relu: bool = False,
+                  labels=None, tf32_operands: bool = False, batch: int = None, dtype=torch.float64):
+    """FWD of one layer. xs: its inputs as NHWC tensors (any float dtype, any
+    device); w: flat weights (KRSC conv, [out][in]+bias FC). relu: the next
+    ACTV's ReLU fused into the epilogue. batch: evaluate only the first
+    `batch` images (every FWD op is separable per image). Returns
+    {"Y": NHWC} or, for LOSS, {"LOSS": scalar, "LOSS_GRAD": [N, classes]}."""
+    L = layers_of(g)
+    l = L[layer]
+    q = tf32 if tf32_operands else (lambda t: t)
+    xs = [x.to(dtype) for x in xs]
+    if batch is not None:
+        xs = [x[:batch] for x in xs]
+    if l.kind == CONV:
+        k, s, p, cout = l.params
+        x = _join(l, xs, False).permute(0, 3, 1, 2)
+        w4 = w.to(dtype).reshape(cout, k, k, x.shape[1]).permute(0, 3, 1, 2)
+        y = Fn.conv2d(q(x), q(w4), stride=s, padding=p).permute(0, 2, 3, 1)
+    elif l.kind == FC:
+        out = l.params[0]
+        x = _join(l, xs, True)
+        fin = x.shape[1]
+        wd = w.to(dtype)
+        y = (q(x) @ q(wd[: out * fin].reshape(out, fin)).t() + wd[out * fin:]).reshape(x.shape[0], 1, 1, out)
+    elif l.kind == POOL:
+        k, s = l.params[0], l.params[1]
+        y = Fn.max_pool2d(_join(l, xs, False).permute(0, 3, 1, 2), k, s).permute(0, 2, 3, 1)
+    elif l.kind == ACTV:
+        y = xs[0]
+    elif l.kind == LOSS:
+        z = xs[0].reshape(xs[0].shape[0], -1)
+        lab = torch.as_tensor(labels, dtype=torch.long, device=z.device)[: z.shape[0]]
+        idx = torch.arange(z.shape[0], device=z.device)
+        loss = (torch.logsumexp(z, dim=1) - z[idx, lab]).mean()
+        pr = torch.softmax(z, dim=1)
+        pr[idx, lab] -= 1.0
+        return {"LOSS": loss, "LOSS_GRAD": pr / z.shape[0]}
+    else:
+        raise ValueError("layer has no FWD op")
+    if relu or l.kind == ACTV:
+        y = torch.relu(y)
+    return {"Y": y.contiguous()}
+
+
+def layer_backward(g, layer: int, xs: List[torch.Tensor], dy: torch.Tensor, w: torch.Tensor = None,
+                   mask: int = 0, dx_before: Dict[int, torch.Tensor] = None, planes=None,
+                   tf32_operands: bool = False, batch: int = None, out_channels=None,
+                   want_dw: bool = True, dtype=torch.float64):
+    """BWD of one layer on the operands its kernels read. dy: incoming gradient
+    (NHWC, the fold of every incoming plane); mask bit i: dX[i] *= (X[i] > 0)
+    (the producer's ReLU backward fused into this epilogue); dx_before[i]:
+    plane contents before an accumulating (two-buffer) write; planes: input
+    slots that have a plane (default: every input). batch: dX of the first
+    `batch` images only (separable per image); out_channels: dW rows to
+    evaluate (dW[co] reads only dY[..., co] -- over the whole batch).
+    Returns {"DX": {i: NHWC}, "DW": flat KRSC / [out][in]+bias rows}."""
+    L = layers_of(g)
+    l = L[layer]
+    q = tf32 if tf32_operands else (lambda t: t)
+    xs = [x.to(dtype) for x in xs]
+    dy = dy.to(dtype)
+    planes = list(range(len(l.inputs))) if planes is None else planes
+    out = {"DX": {}}
+    xb = [x[:batch] for x in xs] if batch is not None else xs
+    dyb = dy[:batch] if batch is not None else dy
+    if l.kind == CONV:
+        k, s, p, cout = l.params
+        x = _join(l, xb, False).permute(0, 3, 1, 2)
+        cin = x.shape[1]
+        w4 = w.to(dtype).reshape(cout, k, k, cin).permute(0, 3, 1, 2)
+        if planes:
+            full = torch.nn.grad.conv2d_input(x.shape, q(w4), q(dyb.permute(0, 3, 1, 2)), stride=s, padding=p)
+            split = _split(l, L, full.permute(0, 2, 3, 1), False)
+            for i in planes:
+                out["DX"][i] = split[i]
+        if want_dw:
+            co = list(range(cout)) if out_channels is None else list(out_channels)
+            xa = _join(l, xs, False).permute(0, 3, 1, 2)
+            dya = dy.permute(0, 3, 1, 2)[:, co]
+            dw = torch.nn.grad.conv2d_weight(q(xa), (len(co), cin, k, k), q(dya), stride=s, padding=p)
+            out["DW"] = dw.permute(0, 2, 3, 1).reshape(len(co), -1)  # rows = selected output channels
+            out["DW_rows"] = co
+    elif l.kind == FC:
+        o = l.params[0]
+        d2 = dyb.reshape(dyb.shape[0], -1)
+        xa = _join(l, xs, True)
+        fin = xa.shape[1]
+        wd = w.to(dtype)[: o * fin].reshape(o, fin)
+        if planes:
+            split = _split(l, L, q(d2) @ q(wd), True)
+            for i in planes:
+                out["DX"][i] = split[i]
+        if want_dw:
+            co = list(range(o)) if out_channels is None else list(out_channels)
+            dfull = dy.reshape(dy.shape[0], -1)[:, co]
+            out["DW"] = q(dfull).t() @ q(xa)
+            out["DB"] = dfull.sum(0)
+            out["DW_rows"] = co
+    elif l.kind == POOL:
+        k, s = l.params[0], l.params[1]
+        x = _join(l, xb, False).permute(0, 3, 1, 2).detach().requires_grad_(True)
+        Fn.max_pool2d(x, k, s).backward(dyb.permute(0, 3, 1, 2))
+        split = _split(l, L, x.grad.permute(0, 2, 3, 1), False)
+        for i in planes:
+            out["DX"][i] = split[i]
+    else:
+        raise ValueError("layer has no BWD contraction/pool op")
+    for i in list(out["DX"].keys()):
+        d = out["DX"][i]
+        if mask >> i & 1:
+            d = torch.where(xb[i] > 0, d, torch.zeros_like(d))
+        if dx_before is not None and i in dx_before:
+            b = dx_before[i].to(dtype)
+            d = d + (b[:batch] if batch is not None else b)
+        out["DX"][i] = d.contiguous()
+    return out
+
+
+def max_rel(gpu: torch.Tensor, ref: torch.Tensor) -> float:
+    """max |gpu - ref| / max |ref| (0 when both are all zero)."""
+    ref = ref.to(torch.float64)
+    d = (gpu.to(torch.float64).reshape(ref.shape) - ref).abs().max().item()
+    m = ref.abs().max().item()
+    return d / m if m > 0 else d

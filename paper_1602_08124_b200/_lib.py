@@ -115,6 +115,21 @@ class SessionOptions(C.Structure):
     ]
 
 
+class ProbeSeg(C.Structure):
+    _fields_ = [("what", C.c_int32), ("index", C.c_int32), ("after", C.c_int32), ("pad_", C.c_int32),
+                ("offset", C.c_uint64), ("bytes", C.c_uint64)]
+
+
+PROBE_MAX_SEGS = 40
+
+
+class ProbeLayout(C.Structure):
+    """vdnn_probe_layout: segments of a layer-local probe and the fusions the step applies."""
+    _fields_ = [("nseg", C.c_int32), ("relu_fused", C.c_int32), ("accumulate", C.c_int32), ("skip", C.c_int32),
+                ("mask_planes", C.c_uint32), ("pad_", C.c_uint32), ("total_bytes", C.c_uint64),
+                ("seg", ProbeSeg * PROBE_MAX_SEGS)]
+
+
 class PeerHandle(C.Structure):
     """vdnn_peer_handle: three CUDA IPC handles + the layout they must agree on."""
     _fields_ = [

@@ -955,6 +955,41 @@ class Session:
     def peer_detach(self) -> None:
         _call("vdnn_session_peer_detach", self.handle)
 
+    # -- layer-local probe (parity tests) --
+    PROBE_NAMES = ("X", "W", "Y", "DY", "DX_BEFORE", "DX", "DW", "LOSS_GRAD", "LOSS")
+
+    def probe_layout(self, layer: int, bwd: bool) -> Dict:
+        """Segments the probe of FWD/BWD(layer) copies, and the fusions that step applies."""
+        lay = L.ProbeLayout()
+        _call("vdnn_session_probe_layout", self.handle, int(layer), int(bool(bwd)), C.byref(lay))
+        segs = [(self.PROBE_NAMES[lay.seg[i].what], lay.seg[i].index, bool(lay.seg[i].after),
+                 lay.seg[i].offset, lay.seg[i].bytes) for i in range(lay.nseg)]
+        return {"segs": segs, "total_bytes": lay.total_bytes, "relu_fused": bool(lay.relu_fused),
+                "accumulate": bool(lay.accumulate), "skip": bool(lay.skip), "mask_planes": lay.mask_planes}
+
+    def probe_step(self, probes, lr: float = 0.01, device: int = 0):
+        """Run one step with layer-local probes armed: probes = [(layer, bwd), ...].
+        Returns (loss, {(layer, bwd): {(name, index[, "after"]): torch fp32 tensor on the device}}):
+        each operand as the step's kernels read it (before) or wrote it (after)."""
+        import torch
+        bufs, lays = {}, {}
+        for layer, bwd in probes:
+            lay = self.probe_layout(layer, bwd)
+            buf = torch.empty(max(1, lay["total_bytes"] // 4), dtype=torch.float32, device=f"cuda:{device}")
+            _call("vdnn_session_arm_probe", self.handle, int(layer), int(bool(bwd)), C.c_void_p(buf.data_ptr()),
+                  C.c_uint64(buf.numel() * 4))
+            bufs[(layer, bwd)], lays[(layer, bwd)] = buf, lay
+        loss = self.step(lr)
+        self.synchronize()
+        out = {}
+        for key, lay in lays.items():
+            d = {"_layout": lay}
+            for name, idx, after, off, nb in lay["segs"]:
+                t = bufs[key][off // 4: off // 4 + nb // 4]
+                d[(name, idx, "after") if (after and name == "W") else (name, idx)] = t
+            out[key] = d
+        return loss, out
+
     @property
     def stream(self) -> int:
         p = C.c_void_p()

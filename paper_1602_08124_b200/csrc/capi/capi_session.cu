@@ -310,3 +310,31 @@ vdnn_status vdnn_session_stream(vdnn_session* s, void** stream) {
 }
 
 }  // extern "C"
+
+vdnn_status vdnn_session_probe_layout(vdnn_session* s, int32_t layer, int32_t bwd, vdnn_probe_layout* out) {
+  return guard([&] {
+    const vdnnrt::Session::ProbeLayout p = S(s).probe_layout(layer, bwd != 0);
+    if (p.segs.size() > VDNN_PROBE_MAX_SEGS) throw vdnnp::PlanError(vdnnp::Err::Generic, "probe: too many segments");
+    std::memset(out, 0, sizeof(*out));
+    out->nseg = static_cast<int32_t>(p.segs.size());
+    out->relu_fused = p.relu;
+    out->accumulate = p.accumulate;
+    out->skip = p.skip;
+    out->mask_planes = p.mask;
+    out->total_bytes = p.total;
+    for (size_t i = 0; i < p.segs.size(); ++i) {
+      out->seg[i].what = p.segs[i].what;
+      out->seg[i].index = p.segs[i].index;
+      out->seg[i].after = p.segs[i].after ? 1 : 0;
+      out->seg[i].offset = p.segs[i].dst;
+      out->seg[i].bytes = p.segs[i].bytes;
+    }
+    return VDNN_OK;
+  });
+}
+vdnn_status vdnn_session_arm_probe(vdnn_session* s, int32_t layer, int32_t bwd, void* dst, uint64_t bytes) {
+  return guard([&] {
+    S(s).arm_probe(layer, bwd != 0, dst, bytes);
+    return VDNN_OK;
+  });
+}

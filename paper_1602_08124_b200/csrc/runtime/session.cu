@@ -445,6 +445,7 @@ void Session::run_fwd(const FwdStep& s, float lr) {
     }
   }
   if (timed_) check(cudaEventRecord(ev_[2 * s.ev], cs_), "record");
+  if (!probes_.empty()) probe_copy(s.ev, false);
   switch (l.kind) {
     case Kind::Conv:
     case Kind::Fc: {
@@ -483,6 +484,7 @@ void Session::run_fwd(const FwdStep& s, float lr) {
     default:
       break;
   }
+  if (!probes_.empty()) probe_copy(s.ev, true);
   if (timed_) check(cudaEventRecord(ev_[2 * s.ev + 1], cs_), "record");
   if (!s.offloads.empty())  // sync rule: FWD(n+1) may not start before n's offloads drain
     check(cudaStreamWaitEvent(cs_, xfer_ev_[static_cast<size_t>(s.offloads.back().ev)], 0), "wait");
@@ -519,6 +521,7 @@ void Session::run_bwd(const BwdStep& s, float lr) {
   for (size_t k = 1; k < s.dy_off.size(); ++k) extra.push_back(F(s.dy_off[k]));
   if (l.kind != Kind::Actv && !extra.empty())
     check(vdnnk::add_into(dy, extra.data(), static_cast<int>(extra.size()), g_.dims(s.layer).count(), cs_), "fold");
+  if (!probes_.empty()) probe_copy(s.ev, false);
 
   switch (l.kind) {
     case Kind::Conv:
@@ -583,6 +586,7 @@ void Session::run_bwd(const BwdStep& s, float lr) {
     default:
       break;
   }
+  if (!probes_.empty()) probe_copy(s.ev, true);
   if (timed_) check(cudaEventRecord(ev_[2 * s.ev + 1], cs_), "record");
   if (!s.prefetches.empty())  // prefetches launched here land before the next BWD
     check(cudaStreamWaitEvent(cs_, xfer_ev_[static_cast<size_t>(s.prefetches.back().ev)], 0), "wait");
@@ -617,7 +621,13 @@ void Session::step(float lr, float* loss_host) {
     has_staged_ = false;
   }
   if (!o_.cuda_graph || eager_steps_ < 1) {
-    enqueue_step(lr);
+    try {
+      enqueue_step(lr);
+    } catch (...) {
+      probes_.clear();
+      throw;
+    }
+    probes_.clear();  // one-shot
     ++eager_steps_;
   } else {
     bool captured_now = false;
@@ -781,6 +791,102 @@ void Session::read_feature(int owner, float* host, size_t count) {
   if (off == kNoOff) throw PlanError(Err::Generic, "owner has no feature buffer");
   if (count * 4 > df_.at[static_cast<size_t>(owner)].bytes) throw PlanError(Err::Generic, "count too large");
   check(cudaMemcpy(host, F(off), count * 4, cudaMemcpyDeviceToHost), "D2H");
+}
+
+Session::ProbeLayout Session::probe_layout(int layer, bool bwd) const {
+  if (layer < 0 || layer >= L_) throw PlanError(Err::Generic, "probe: layer out of range");
+  ProbeLayout p;
+  const Node& l = g_.at(layer);
+  const size_t li = static_cast<size_t>(layer);
+  auto add = [&](int what, int index, u64 bytes, int src, u64 src_off, bool after) {
+    if (bytes == 0) return;
+    ProbeSeg s;
+    s.what = what, s.index = index, s.dst = p.total, s.bytes = bytes, s.src = src, s.src_off = src_off, s.after = after;
+    p.segs.push_back(s);
+    p.total += round_up(bytes, 256);
+  };
+  auto in_bytes = [&](size_t i) { return g_.dims(l.in[i]).count() * 4; };
+  const u64 y_bytes = g_.dims(layer).count() * 4;
+  const bool contraction = l.kind == Kind::Conv || l.kind == Kind::Fc;
+  if (!bwd) {
+    const FwdStep* s = nullptr;
+    for (const FwdStep& f : fwd_)
+      if (f.layer == layer) s = &f;
+    if (!s) throw PlanError(Err::Generic, "probe: layer has no FWD step");
+    p.relu = s->relu ? 1 : 0;
+    p.skip = s->skip ? 1 : 0;
+    for (size_t i = 0; i < s->in_off.size(); ++i)
+      if (l.kind != Kind::Actv) add(kPX, static_cast<int>(i), in_bytes(i), 0, s->in_off[i], false);
+    if (contraction) add(kPW, 0, df_.at[li].w_bytes, 0, s->w_off, false);
+    if (l.kind == Kind::Actv) add(kPX, 0, y_bytes, 0, s->out_off, false);
+    if (l.kind == Kind::Loss) {
+      add(kPLossGrad, 0, g_.batch() * static_cast<u64>(classes_) * 4, 2, 0, true);
+      add(kPLoss, 0, 4, 3, 0, true);
+    } else {
+      add(kPY, 0, y_bytes, 0, s->out_off, true);
+    }
+    return p;
+  }
+  const BwdStep* s = nullptr;
+  for (const BwdStep& b : bwd_)
+    if (b.layer == layer) s = &b;
+  if (!s) throw PlanError(Err::Generic, "probe: layer has no BWD step");
+  p.accumulate = s->accumulate ? 1 : 0;
+  p.skip = s->skip ? 1 : 0;
+  for (size_t i = 0; i < s->mask_plane.size(); ++i)
+    if (s->mask_plane[i]) p.mask |= 1u << i;
+  if (l.kind == Kind::Actv) {
+    add(kPY, 0, y_bytes, 0, s->out_off, false);
+    for (size_t k = 0; k < s->dy_off.size(); ++k) add(kPDY, static_cast<int>(k), y_bytes, 0, s->dy_off[k], false);
+    if (!s->dy_off.empty()) add(kPDX, 0, y_bytes, 0, s->dy_off[0], true);
+    return p;
+  }
+  if (l.kind == Kind::Conv || l.kind == Kind::Fc || l.kind == Kind::Pool)
+    for (size_t i = 0; i < s->in_off.size(); ++i) add(kPX, static_cast<int>(i), in_bytes(i), 0, s->in_off[i], false);
+  if (contraction) add(kPW, 0, df_.at[li].w_bytes, 0, s->w_off, false);
+  if (!s->dy_off.empty()) add(kPDY, 0, y_bytes, 0, s->dy_off[0], false);  // after the fold of the other planes
+  for (size_t i = 0; i < s->plane_off.size(); ++i) {
+    if (s->plane_off[i] == kNoOff) continue;
+    const u64 b = l.kind == Kind::Loss ? g_.dims(l.in[0]).count() * 4 : in_bytes(i);
+    if (s->accumulate) add(kPDXBefore, static_cast<int>(i), b, 0, s->plane_off[i], false);
+    add(kPDX, static_cast<int>(i), b, 0, s->plane_off[i], true);
+  }
+  if (contraction && grads_) add(kPDW, 0, df_.at[li].w_bytes, 1, grad_off_[li], true);
+  if (contraction && !grads_) add(kPW, 1, df_.at[li].w_bytes, 0, s->w_off, true);  // updated weights
+  return p;
+}
+
+void Session::arm_probe(int layer, bool bwd, void* dst, u64 bytes) {
+  if (o_.cuda_graph) throw PlanError(Err::Config, "probes are not available in cuda_graph mode");
+  ArmedProbe a;
+  a.lay = probe_layout(layer, bwd);
+  if (!dst || bytes < a.lay.total) throw PlanError(Err::Generic, "probe: destination buffer too small");
+  a.dst = static_cast<char*>(dst);
+  if (!bwd) {
+    for (const FwdStep& f : fwd_)
+      if (f.layer == layer) a.ev = f.ev;
+  } else {
+    for (const BwdStep& b : bwd_)
+      if (b.layer == layer) a.ev = b.ev;
+  }
+  probes_.push_back(std::move(a));
+}
+
+void Session::probe_copy(int ev, bool after) {
+  for (const ArmedProbe& a : probes_) {
+    if (a.ev != ev) continue;
+    for (const ProbeSeg& s : a.lay.segs) {
+      if (s.after != after) continue;
+      const char* src = nullptr;
+      switch (s.src) {
+        case 0: src = base_ + s.src_off; break;
+        case 1: src = reinterpret_cast<const char*>(grads_ + s.src_off); break;
+        case 2: src = reinterpret_cast<const char*>(loss_grad_); break;
+        default: src = reinterpret_cast<const char*>(loss_); break;
+      }
+      check(cudaMemcpyAsync(a.dst + s.dst, src, s.bytes, cudaMemcpyDefault, cs_), "probe copy");
+    }
+  }
 }
 
 void Session::grad_buffer(int layer, void** ptr, size_t* count) {

@@ -255,6 +255,41 @@ class Session {
   // measured report and layer times then describe the last step run with
   // them on.
   void pause_timeline(bool paused) { timeline_paused_ = paused; }
+
+  // Layer-local probe (parity tests): during the next step, copy the
+  // operands of one compute step (FWD or BWD of one layer) into a
+  // caller-provided device buffer -- what the kernels read, right before they
+  // run, and what they wrote, right after -- so every kernel can be checked
+  // against the oracle op evaluated on the very inputs it saw. The copies are
+  // stream-ordered on the compute stream; probes are one-shot.
+  enum ProbeWhat { kPX = 0, kPW = 1, kPY = 2, kPDY = 3, kPDXBefore = 4, kPDX = 5, kPDW = 6, kPLossGrad = 7,
+                   kPLoss = 8 };
+  struct ProbeSeg {
+    int what = 0, index = 0;  // index: input slot (X, DX) or incoming plane (DY)
+    u64 dst = 0, bytes = 0;   // byte range in the destination buffer
+    int src = 0;              // 0 pool offset, 1 gradient arena (float offset), 2 loss gradient, 3 loss
+    u64 src_off = 0;
+    bool after = false;       // copied after the step's kernels (else before)
+  };
+  struct ProbeLayout {
+    std::vector<ProbeSeg> segs;
+    u64 total = 0;
+    int relu = 0;        // FWD: the following ACTV's ReLU is applied in the epilogue
+    int accumulate = 0;  // BWD: dX added into a plane that already holds a fork gradient
+    unsigned mask = 0;   // BWD: bit i = ReLU-backward mask of input i (x_i > 0) applied in the epilogue
+    int skip = 0;        // ACTV step fused into its neighbour (launches nothing)
+  };
+  ProbeLayout probe_layout(int layer, bool bwd) const;
+  void arm_probe(int layer, bool bwd, void* dst, u64 bytes);
+
+ private:
+  struct ArmedProbe {
+    int ev = -1;
+    ProbeLayout lay;
+    char* dst = nullptr;
+  };
+  std::vector<ArmedProbe> probes_;
+  void probe_copy(int ev, bool after);
 };
 
 }  // namespace vdnnrt

@@ -1,0 +1,145 @@
+"""Layer-local GPU parity at the BASELINE configs' full sizes.
+
+Each config runs under its BASELINE policy and budget with real
+offload/prefetch; probes copy every compute step's operands as its kernels
+read them and its results as they wrote them (Session.probe_step), and each
+FWD / dgrad / wgrad / pool / ReLU / loss result is compared with the float64
+oracle op on those same operands (tests/layer_parity.py, bounds stated
+there): the TF32 contraction against the oracle that reads operands the way
+kind::tf32 does (only the fp32 accumulation order may differ) and against
+plain float64; 3xTF32 against plain float64 with a reduction-length bound.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1602_08124_b200 as V
+from oracle import numeric
+
+import layer_parity as LP
+
+pytestmark = pytest.mark.gpu
+CAP = 12884901888
+OUT = os.environ.get("VDNN_PARITY_OUT")  # optional: write the per-tensor records (profiles/)
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _batch(g, seed):
+    s = g.shape(0)
+    rng = np.random.default_rng(seed)
+    images = rng.uniform(-1, 1, size=(s.n, s.h, s.w, s.c)).astype(np.float32)
+    ls = g.shape(g.layer(g.size() - 1).inputs[0])
+    labels = rng.integers(0, ls.c * ls.h * ls.w, size=s.n).astype(np.int32)
+    return images, labels
+
+
+def _decision(g, cm, policy):
+    if policy == "dyn":
+        return V.dynamic_select(g, CAP, cm).decision
+    kind = {"all": V.PolicyKind.VdnnAll, "conv": V.PolicyKind.VdnnConv, "none": V.PolicyKind.Baseline}[policy]
+    return V.static_decision(kind, V.AlgoMode.MemoryOptimal, g, cm)
+
+
+def _run(name, net, batch, policy, precise, layers=None, extra=0, expect_label=None):
+    _need_gpu()
+    g = V.build_preset(net, batch) if not extra else V.extend_vgg(extra, batch)
+    cm = V.CostModel()
+    d = _decision(g, cm, policy)
+    if expect_label:
+        assert d.label == expect_label
+    s = V.Session(g, d, cm, CAP, external_grads=True, precise_fp32=precise)
+    images, labels = _batch(g, 2024 + batch)
+    s.set_batch(images, labels)
+    s.step(0.01)  # warm step: identical inputs and weights every step (external_grads: no update)
+    recs = LP.check_session(s, g, labels, layers=layers, precise=precise)
+    tag = f"{name} {'fp32' if precise else 'tf32'} {d.label}"
+    print(tag, json.dumps(LP.summarize(recs)))
+    if OUT:
+        with open(os.path.join(OUT, f"parity_{name}_{'fp32' if precise else 'tf32'}.json"), "w") as f:
+            json.dump({"config": tag, "plan_signature": s.plan.signature(), "records": recs}, f, indent=0)
+    assert s.plan.offload_traffic_bytes > 0 or policy in ("dyn", "none")
+    bad = LP.violations(recs, precise)
+    assert not bad, f"{tag}: {len(bad)} violations: " + "; ".join(bad[:8])
+    ops = {r["op"] for r in recs}
+    return recs, ops
+
+
+@pytest.mark.parametrize("precise", [False, True], ids=["tf32", "fp32"])
+def test_vgg16_b256_dyn_every_layer(precise):
+    """BASELINE config 4: VGG-16 b256 under the 12 GiB vDNN_dyn plan."""
+    _, ops = _run("vgg16_b256", "vgg16", 256, "dyn", precise, expect_label="vdnn-conv+greedy")
+    assert {"fprop", "dgrad", "wgrad", "pool_fwd", "pool_bwd"} <= ops
+
+
+@pytest.mark.parametrize("precise", [False, True], ids=["tf32", "fp32"])
+def test_alexnet_b128_vdnn_all_every_layer(precise):
+    """BASELINE config 1: AlexNet b128 under vDNN_all(m)."""
+    _run("alexnet_b128", "alexnet", 128, "all", precise)
+
+
+@pytest.mark.parametrize("precise", [False, True], ids=["tf32", "fp32"])
+def test_overfeat_b128_vdnn_conv_every_layer(precise):
+    """BASELINE config 2: OverFeat b128 under vDNN_conv(m)."""
+    _run("overfeat_b128", "overfeat", 128, "conv", precise)
+
+
+@pytest.mark.parametrize("precise", [False, True], ids=["tf32", "fp32"])
+def test_inception_toy_b128_dyn_every_layer(precise):
+    """BASELINE config 3: inception_toy b128, vDNN_dyn -> baseline(p): the
+    two-buffer gradient scheme with fork accumulation (DX_BEFORE checked)."""
+    recs, _ = _run("inception_toy_b128", "inception_toy", 128, "dyn", precise, expect_label="baseline(p)")
+    assert any(r["tensor"].startswith("DX") for r in recs)
+
+
+def test_vgg416_b32_dyn_sampled_layers():
+    """BASELINE config 5: VGG-416 b32 under the 12 GiB vDNN_dyn plan (all-FFT
+    vdnn-conv(p)); a sample of layers at every resolution plus the classifier."""
+    g = V.extend_vgg(400, 32)
+    L = numeric.layers_of(g)
+    convs = [l.id for l in L if l.kind == numeric.CONV]
+    pools = [l.id for l in L if l.kind == numeric.POOL]
+    fcs = [l.id for l in L if l.kind == numeric.FC]
+    pick = sorted(set(convs[:3] + convs[len(convs) // 2: len(convs) // 2 + 2] + convs[-2:] + pools + fcs
+                      + [L[-1].id]))
+    _run("vgg416_b32", "vgg16", 32, "dyn", False, layers=pick, extra=400, expect_label="vdnn-conv(p)")
+
+
+def test_vgg16_b256_dyn_two_step_loss_matches_oracle():
+    """Whole-network check at the headline size: two training steps (fused
+    wgrad+SGD) of VGG-16 b256 under the 12 GiB vDNN_dyn plan; each step's loss
+    against the float64 oracle network (on the GPU) that reads contraction
+    operands as kind::tf32 does, within 1e-3 relative, and against plain
+    float64 within 1e-2."""
+    _need_gpu()
+    import gc
+    g = V.build_preset("vgg16", 256)
+    cm = V.CostModel()
+    d = V.dynamic_select(g, CAP, cm).decision
+    w = numeric.he_weights(g, cm, seed=77)
+    images, labels = _batch(g, 78)
+    s = V.Session(g, d, cm, CAP)
+    for k, v in w.items():
+        s.set_weights(k, v)
+    s.set_batch(images, labels)
+    gpu = [s.step(0.01), s.step(0.01)]
+    del s
+    gc.collect()
+    torch.cuda.empty_cache()
+    for emu, tol in ((True, 1e-3), (False, 1e-2)):
+        ww, ref = dict(w), []
+        for _ in range(2):
+            l, ww, _ = numeric.train_step(g, ww, images, labels, 0.01, device="cuda", tf32_operands=emu)
+            ref.append(l)
+            gc.collect()
+            torch.cuda.empty_cache()
+        print("vgg16 b256 dyn losses", gpu, "oracle" + (" (tf32 operands)" if emu else ""), ref)
+        for a, b in zip(gpu, ref):
+            assert abs(a - b) <= tol * max(1.0, abs(b)), (gpu, ref, emu)
