@@ -283,6 +283,10 @@ vdnn_status vdnn_session_arena_info(const vdnn_session* s, uint64_t* arena_bytes
 vdnn_status vdnn_session_set_batch_host(vdnn_session* s, const float* images, const int32_t* labels);
 vdnn_status vdnn_session_set_batch_device(vdnn_session* s, const float* images, const int32_t* labels);
 vdnn_status vdnn_session_synthetic_batch(vdnn_session* s, uint64_t seed);
+/* Graphs with several INPUT layers (net_graph.hpp allows any number): images of INPUT layer `layer`
+ * (set_batch_* fills the first INPUT layer; labels are shared by every LOSS head, taken modulo its
+ * class count; the step's loss is the sum over heads). */
+vdnn_status vdnn_session_set_input(vdnn_session* s, int32_t layer, const float* images, int32_t on_device);
 /* Input pipeline: stage the NEXT batch (pinned host pointers) on a separate stream while the current
  * step runs; the next vdnn_session_step consumes it. Pair with vdnn_session_step(s, lr, NULL) +
  * vdnn_session_read_loss so the host does not wait on the loss before staging the next batch. */

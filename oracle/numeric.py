@@ -132,6 +132,11 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
         for q in l.inputs:
             t = buf[owner(L, q)]
             parts.append(t.reshape(t.shape[0], -1) if flatten else t)
+        if l.join == 1 and len(parts) > 1:  # elementwise join: sum (net_graph.hpp:290-296)
+            out = parts[0]
+            for t in parts[1:]:
+                out = out + t
+            return out
         return torch.cat(parts, dim=1 if flatten else 3)
 
     def in_channels(l: Layer, flatten: bool = False):
@@ -145,8 +150,9 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
     gscratch = None
     loss = 0.0
     for l in L:
-        if l.kind == INPUT:
-            buf[l.id] = torch.tensor(images, dtype=dtype, device=device).reshape(_nhwc(l.shape))
+        if l.kind == INPUT:  # several INPUT layers: images = {layer id: array}
+            im = images[l.id] if isinstance(images, dict) else images
+            buf[l.id] = torch.tensor(im, dtype=dtype, device=device).reshape(_nhwc(l.shape))
         elif l.kind == CONV:
             k, s, p, cout = l.params
             x = cat_in(l).permute(0, 3, 1, 2)
@@ -168,14 +174,18 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
             b = W[l.id][out * fin:]
             buf[l.id] = (q(x) @ q(w).t() + b).reshape(_nhwc(l.shape))
         elif l.kind == LOSS:
+            # several LOSS heads: the loss is their sum; each head reads the
+            # shared label vector modulo its class count
             z = buf[owner(L, l.inputs[0])].reshape(l.shape[0], -1)
-            lab = torch.tensor(labels, dtype=torch.long, device=device)
+            lab = torch.tensor(labels, dtype=torch.long, device=device) % z.shape[1]
             lse = torch.logsumexp(z, dim=1)
-            loss = float((lse - z[torch.arange(z.shape[0], device=z.device), lab]).mean())
+            loss += float((lse - z[torch.arange(z.shape[0], device=z.device), lab]).mean())
             pr = torch.softmax(z, dim=1)
             oh = torch.zeros_like(pr)
             oh[torch.arange(z.shape[0], device=z.device), lab] = 1.0
-            gscratch = (pr - oh) / z.shape[0]
+            if gscratch is None:
+                gscratch = {}
+            gscratch[l.id] = (pr - oh) / z.shape[0]
 
     # ---------------- backward
     def produces(l: Layer) -> bool:
@@ -220,11 +230,16 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
         return keys
 
     def set_planes(l: Layer, full: torch.Tensor, flatten: bool):
-        """Split a gradient w.r.t. the concatenated input into per-input planes."""
+        """Split a gradient w.r.t. the concatenated input into per-input planes
+        (elementwise join: every input receives the whole gradient)."""
         off = 0
         cs = in_channels(l, flatten)
         for j, q in enumerate(l.inputs):
             c = cs[j]
+            if l.join == 1 and len(l.inputs) > 1:
+                if L[owner(L, q)].kind != INPUT:
+                    planes[(l.id, j)] = full.reshape(_nhwc(L[q].shape)).contiguous()
+                continue
             if L[owner(L, q)].kind != INPUT:
                 part = full[:, off:off + c] if flatten else full[..., off:off + c]
                 planes[(l.id, j)] = part.reshape(_nhwc(L[q].shape)).contiguous()
@@ -245,8 +260,10 @@ def train_step(g, weights: Dict[int, np.ndarray], images: np.ndarray, labels: np
                 planes[keys[0]] = dy
         if l.kind == LOSS:
             if produces(l):
-                planes[(m, 0)] = gscratch.reshape(_nhwc(L[l.inputs[0]].shape)).clone()
+                planes[(m, 0)] = gscratch[m].reshape(_nhwc(L[l.inputs[0]].shape)).clone()
         elif l.kind == ACTV:
+            if dy is None:  # nothing downstream needs this map's gradient
+                continue
             y = buf[owner(L, m)]
             planes[keys[0]] = torch.where(y > 0, dy, torch.zeros_like(dy))
         elif l.kind == CONV:
@@ -375,7 +392,7 @@ def layer_forward(g, layer: int, xs: List[torch.Tensor], w: torch.Tensor = None,
         y = xs[0]
     elif l.kind == LOSS:
         z = xs[0].reshape(xs[0].shape[0], -1)
-        lab = torch.as_tensor(labels, dtype=torch.long, device=z.device)[: z.shape[0]]
+        lab = torch.as_tensor(labels, dtype=torch.long, device=z.device)[: z.shape[0]] % z.shape[1]
         idx = torch.arange(z.shape[0], device=z.device)
         loss = (torch.logsumexp(z, dim=1) - z[idx, lab]).mean()
         pr = torch.softmax(z, dim=1)

@@ -285,9 +285,30 @@ char* vref_run(const char* graph_spec, const char* cost_spec, const char* dec_sp
   }
 }
 
+static std::string graph_spec_of(const NetworkGraph& g);
+
 char* vref_preset_spec(const char* name, unsigned long long batch, int extra) {
   try {
     NetworkGraph g = extra > 0 ? extend_vgg(extra, batch) : build_preset(name, batch);
+    return dup(graph_spec_of(g));
+  } catch (const std::exception& e) {
+    return dup(std::string("ERROR:") + e.what());
+  }
+}
+
+// The reference fuzz campaign's graph generator (fuzz.hpp:26-63) for one seed:
+// the graphs its differential campaign plans, to be run on the GPU as well.
+char* vref_fuzz_graph(unsigned long long seed, int max_layers) {
+  try {
+    std::mt19937_64 rng(seed);
+    return dup(graph_spec_of(fuzzdetail::random_graph(rng, max_layers)));
+  } catch (const std::exception& e) {
+    return dup(std::string("ERROR:") + e.what());
+  }
+}
+
+static std::string graph_spec_of(const NetworkGraph& g) {
+  {
     std::ostringstream os;
     os << "B=" << g.batch();
     for (const LayerDescriptor& l : g.layers()) {
@@ -301,9 +322,7 @@ char* vref_preset_spec(const char* name, unsigned long long batch, int extra) {
       if (l.input) { p[0] = l.input->c; p[1] = l.input->h; p[2] = l.input->w; }
       os << " " << p[0] << " " << p[1] << " " << p[2] << " " << p[3] << " " << (l.join == JoinRule::Elementwise ? 1 : 0);
     }
-    return dup(os.str());
-  } catch (const std::exception& e) {
-    return dup(std::string("ERROR:") + e.what());
+    return os.str();
   }
 }
 

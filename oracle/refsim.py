@@ -25,7 +25,7 @@ def lib():
     global _lib
     if _lib is None:
         _lib = C.CDLL(LIB)
-        for n in ("vref_run", "vref_preset_spec", "vref_replay", "vref_fuzz"):
+        for n in ("vref_run", "vref_preset_spec", "vref_replay", "vref_fuzz", "vref_fuzz_graph"):
             getattr(_lib, n).restype = C.c_void_p
         _lib.vref_free.argtypes = [C.c_void_p]
         _lib.vref_time_plan.restype = C.c_double
@@ -70,6 +70,14 @@ def replay(graph_spec: str, dec_spec: str, capacity: int, events, max_mem: int, 
     if isinstance(out, dict) and "error" in out:
         raise RuntimeError(out["error"])
     return out
+
+
+def fuzz_graph(seed: int, max_layers: int = 12) -> str:
+    """Graph spec of the reference fuzz generator (fuzz.hpp:26-63) for `seed`."""
+    s = _take(lib().vref_fuzz_graph(C.c_ulonglong(seed), int(max_layers)))
+    if s.startswith("ERROR:"):
+        raise RuntimeError(s)
+    return s
 
 
 def fuzz(seed: int, trials: int) -> dict:

@@ -816,6 +816,14 @@ class Session:
               lb.ctypes.data_as(C.c_void_p))
         self._keep = (im, lb)  # the copy is asynchronous: keep sources alive until the next call
 
+    def set_input(self, layer: int, images) -> None:
+        """Images (float32 NHWC host array) of one INPUT layer of a multi-input graph."""
+        import numpy as np
+        im = np.ascontiguousarray(images, dtype=np.float32)
+        _call("vdnn_session_set_input", self.handle, int(layer), im.ctypes.data_as(C.c_void_p), 0)
+        self._keep_inputs = getattr(self, "_keep_inputs", {})
+        self._keep_inputs[layer] = im  # asynchronous copy: keep the source alive
+
     def set_batch_ptr(self, images_ptr: int, labels_ptr: int, device: bool = False) -> None:
         fn = "vdnn_session_set_batch_device" if device else "vdnn_session_set_batch_host"
         _call(fn, self.handle, C.c_void_p(images_ptr), C.c_void_p(labels_ptr))

@@ -338,3 +338,9 @@ vdnn_status vdnn_session_arm_probe(vdnn_session* s, int32_t layer, int32_t bwd, 
     return VDNN_OK;
   });
 }
+vdnn_status vdnn_session_set_input(vdnn_session* s, int32_t layer, const float* images, int32_t on_device) {
+  return guard([&] {
+    S(s).set_input(layer, images, on_device != 0);
+    return VDNN_OK;
+  });
+}

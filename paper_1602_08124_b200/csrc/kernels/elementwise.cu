@@ -124,6 +124,84 @@ cudaError_t add_into(float* dst, const float* const* src, int nsrc, size_t n, cu
   return cudaGetLastError();
 }
 
+// dst = sum_k src[k], masked by (y > 0) when y != null; dst may be src[0]
+// (element-wise in place). Used for shared gradient planes (an elementwise
+// join's one map is read-only: its readers sum / mask into their own
+// buffer) and for the summed input of an elementwise join.
+__global__ void combine_kernel(float* __restrict__ dst, PtrList src, int nsrc, const float* __restrict__ y, size_t n) {
+  const size_t n4 = n / 4;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float4 v = reinterpret_cast<const float4*>(src.p[0])[i];
+    for (int k = 1; k < nsrc; ++k) {
+      const float4 e = reinterpret_cast<const float4*>(src.p[k])[i];
+      v.x += e.x;
+      v.y += e.y;
+      v.z += e.z;
+      v.w += e.w;
+    }
+    if (y) {
+      const float4 a = reinterpret_cast<const float4*>(y)[i];
+      v.x = a.x > 0.f ? v.x : 0.f;
+      v.y = a.y > 0.f ? v.y : 0.f;
+      v.z = a.z > 0.f ? v.z : 0.f;
+      v.w = a.w > 0.f ? v.w : 0.f;
+    }
+    reinterpret_cast<float4*>(dst)[i] = v;
+  }
+  for (size_t i = n4 * 4 + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float v = src.p[0][i];
+    for (int k = 1; k < nsrc; ++k) v += src.p[k][i];
+    if (y) v = y[i] > 0.f ? v : 0.f;
+    dst[i] = v;
+  }
+}
+
+cudaError_t combine(float* dst, const float* const* src, int nsrc, const float* y, size_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  if (nsrc < 1 || nsrc > 8) return cudaErrorInvalidValue;
+  for (int i = 0; i < nsrc; ++i)
+    if (reinterpret_cast<uintptr_t>(src[i]) % 16) return cudaErrorMisalignedAddress;
+  if (reinterpret_cast<uintptr_t>(dst) % 16 || (y && reinterpret_cast<uintptr_t>(y) % 16))
+    return cudaErrorMisalignedAddress;
+  PtrList pl{};
+  for (int i = 0; i < nsrc; ++i) pl.p[i] = src[i];
+  combine_kernel<<<grid_for(n, 16), kThreads, 0, st>>>(dst, pl, nsrc, y, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Zero insertion for the data gradient of a strided conv: d[n][i][j][c] =
+// dy[n][i/s][j/s][c] where s divides i and j, else 0, over (hd, wd) =
+// ((ho-1)s+1, (wo-1)s+1); a stride-1 dgrad over d with the conv's own pad
+// and kernel then equals the strided conv's dgrad.
+__global__ void dilate_kernel(float* __restrict__ d, const float* __restrict__ dy, int n, int ho, int wo, int c,
+                              int s, int hd, int wd) {
+  const size_t total = static_cast<size_t>(n) * hd * wd * c;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int ch = static_cast<int>(e % c);
+    size_t r = e / c;
+    const int j = static_cast<int>(r % wd);
+    r /= wd;
+    const int i = static_cast<int>(r % hd);
+    const size_t img = r / hd;
+    float v = 0.f;
+    if (i % s == 0 && j % s == 0) v = dy[((img * ho + i / s) * wo + j / s) * c + ch];
+    d[e] = v;
+  }
+}
+
+cudaError_t dilate(float* d, const float* dy, int n, int ho, int wo, int c, int stride, cudaStream_t st) {
+  const int hd = (ho - 1) * stride + 1, wd = (wo - 1) * stride + 1;
+  const size_t total = static_cast<size_t>(n) * hd * wd * c;
+  if (total == 0) return cudaSuccess;
+  dilate_kernel<<<grid_for(total, 4), kThreads, 0, st>>>(d, dy, n, ho, wo, c, stride, hd, wd);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------- max-pool -----
 struct PoolDev {
   int n, h, w, window, stride, ho, wo, nseg, ctot;
@@ -641,7 +719,7 @@ __global__ void softmax_xent_kernel(const float* __restrict__ logits, const int3
   for (int i = lane; i < k; i += 32) s += expf(z[i] - m);
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   const float lse = m + logf(s);
-  const int lab = labels[warp];
+  const int lab = labels[warp] % k;  // several LOSS heads share one label vector
   const float inv_n = 1.0f / static_cast<float>(n);
   for (int i = lane; i < k; i += 32) {
     const float pr = expf(z[i] - lse);
@@ -650,7 +728,7 @@ __global__ void softmax_xent_kernel(const float* __restrict__ logits, const int3
   if (lane == 0) row_loss[warp] = lse - z[lab];
 }
 
-__global__ void mean_kernel(const float* __restrict__ v, int n, float* __restrict__ out) {
+__global__ void mean_kernel(const float* __restrict__ v, int n, float* __restrict__ out, int accumulate) {
   __shared__ float part[256];
   float s = 0.f;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
@@ -660,16 +738,16 @@ __global__ void mean_kernel(const float* __restrict__ v, int n, float* __restric
     if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = part[0] / static_cast<float>(n);
+  if (threadIdx.x == 0) *out = (accumulate ? *out : 0.f) + part[0] / static_cast<float>(n);
 }
 
 cudaError_t softmax_xent_fwd(const float* logits, const int32_t* labels, int n, int k, float* grad_scratch,
-                             float* row_loss, float* loss, cudaStream_t st) {
+                             float* row_loss, float* loss, cudaStream_t st, bool accumulate) {
   if (n <= 0) return cudaSuccess;
   const int threads = 256;
   const int blocks = (n * 32 + threads - 1) / threads;
   softmax_xent_kernel<<<blocks, threads, 0, st>>>(logits, labels, n, k, grad_scratch, row_loss);
-  mean_kernel<<<1, 256, 0, st>>>(row_loss, n, loss);
+  mean_kernel<<<1, 256, 0, st>>>(row_loss, n, loss, accumulate ? 1 : 0);
   count_launch(2);
   return cudaGetLastError();
 }

@@ -62,6 +62,10 @@ cudaError_t relu_fwd(float* y, size_t n, cudaStream_t st);
 // g0 = (g0 + sum extra) * (y > 0); in place on g0.
 cudaError_t relu_bwd(float* g0, const float* const* extra, int nextra, const float* y, size_t n, cudaStream_t st);
 cudaError_t add_into(float* dst, const float* const* src, int nsrc, size_t n, cudaStream_t st);
+// dst = sum src[k] (k < nsrc <= 8), then *= (y > 0) if y; dst may alias src[0]; 16-B aligned.
+cudaError_t combine(float* dst, const float* const* src, int nsrc, const float* y, size_t n, cudaStream_t st);
+// zero-inserted dY of a stride-s conv: ((ho-1)s+1) x ((wo-1)s+1) x c per image
+cudaError_t dilate(float* d, const float* dy, int n, int ho, int wo, int c, int stride, cudaStream_t st);
 struct PoolArgs {
   int n = 0, h = 0, w = 0, window = 2, stride = 2;
   int nseg = 0;
@@ -84,8 +88,10 @@ cudaError_t maxpool_bwd(const PoolArgs& a, const float* y, const float* dy, cuda
 // Mean softmax cross-entropy over n rows of k logits. Writes the gradient
 // (softmax - onehot)/n into grad_scratch, the per-row loss into row_loss and
 // the mean loss into *loss (all device pointers).
+// Labels are taken modulo k (several LOSS heads may share one label vector);
+// accumulate: *loss += mean instead of *loss = mean (the total over heads).
 cudaError_t softmax_xent_fwd(const float* logits, const int32_t* labels, int n, int k, float* grad_scratch,
-                             float* row_loss, float* loss, cudaStream_t st);
+                             float* row_loss, float* loss, cudaStream_t st, bool accumulate = false);
 // bias -= lr * sum_n dy[n][o]   (or db_out[o] = sum when db_out != null)
 cudaError_t bias_grad(const float* dy, int n, int o, float* bias, float lr, float* db_out, cudaStream_t st);
 cudaError_t sgd_update(float* w, const float* g, float lr, size_t n, cudaStream_t st);

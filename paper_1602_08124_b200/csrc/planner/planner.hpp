@@ -328,6 +328,12 @@ struct Step {
   // BWD of an ACTV: the step whose epilogue may apply this ReLU's mask to
   // input slot mask_slot (the only writer of its incoming plane), or -1
   int mask_host = -1, mask_slot = -1;
+  // Shared planes (the one gradient map of an elementwise join, read by every
+  // input's chain: footprint.hpp:67) are read-only. A step whose incoming
+  // planes are all shared does not fold in place: an ACTV writes its masked
+  // sum to a private plane (dx[0], placed after the arena: the reference's
+  // plan has no extent for it), any other layer sums into its scratch gap.
+  bool stage_dy = false;
 };
 
 struct Program {
@@ -344,6 +350,9 @@ struct Program {
   // graph that needs more live maps than two), placed after arena_hi
   u64 overflow_base = 0, overflow_slot_bytes = 0;
   int overflow_slots = 0;
+  // private planes of ACTVs over shared planes (Step::stage_dy), after the
+  // overflow slots: [private_base, private_base + private_bytes)
+  u64 private_base = 0, private_bytes = 0;
 };
 
 // One pass of the schedule: the report (always) and the program (when

@@ -529,12 +529,24 @@ class Compiler {
   int plane_slot(int producer, size_t j) const {
     return g_.at(producer).join == Join::Elementwise ? 0 : static_cast<int>(j);
   }
-  PlaneRef canon(PlaneRef p) const {
-    for (auto it = folded_.find({p.producer, p.slot}); it != folded_.end(); it = folded_.find({p.producer, p.slot}))
+  // A fold is recorded per chain (the buffer owner its steps lead to): a
+  // shared plane folded into one chain's plane stays itself for the others.
+  PlaneRef canon(PlaneRef p, int chain) const {
+    for (auto it = folded_.find({p.producer, p.slot, chain}); it != folded_.end();
+         it = folded_.find({p.producer, p.slot, chain}))
       p.producer = it->second.first, p.slot = it->second.second;
     return p;
   }
+  // the one gradient map of an elementwise join over >= 2 non-INPUT inputs
+  bool shared(const PlaneRef& p) const {
+    const Node& l = g_.at(p.producer);
+    if (l.kind == Kind::Actv || l.join != Join::Elementwise) return false;
+    int n = 0;
+    for (int q : l.in) n += g_.at(g_.owner(q)).kind != Kind::Input;
+    return n >= 2;
+  }
   u64 dx_base(int producer) const {
+    if (auto it = private_plane_.find(producer); it != private_plane_.end()) return it->second;
     if (per_layer_) return loc(dx_at_[static_cast<size_t>(producer)]);
     return g2_slot_.at(static_cast<size_t>(producer));
   }
@@ -557,6 +569,7 @@ class Compiler {
     }
     // incoming planes: of every dX map m reads, the planes whose input chain
     // passes through m; already-folded planes resolve to their fold target
+    const int owner_m = g_.owner(m);
     for (int src : at(m).dy_sources) {
       const Node& sl = g_.at(src);
       for (size_t j = 0; j < sl.in.size(); ++j) {
@@ -564,19 +577,35 @@ class Compiler {
         std::vector<int> chain;
         gradient_consumers(g_, sl.in[j], chain);
         if (std::find(chain.begin(), chain.end(), m) == chain.end()) continue;
-        PlaneRef p = canon(PlaneRef{src, plane_slot(src, j), kNoLoc});
+        PlaneRef p = canon(PlaneRef{src, plane_slot(src, j), kNoLoc}, owner_m);
         if (!per_layer_) {  // two-buffer fork accumulation shares one slot
           auto it = g2_alias_.find(p.producer);
-          if (it != g2_alias_.end()) p = canon(PlaneRef{it->second.first, it->second.second, kNoLoc});
+          if (it != g2_alias_.end()) p = canon(PlaneRef{it->second.first, it->second.second, kNoLoc}, owner_m);
         }
         if (std::find(s.dy.begin(), s.dy.end(), p) != s.dy.end()) continue;
         p.off = dx_base(p.producer) + plane_rel(p.producer, static_cast<size_t>(slot_input(p)));
         s.dy.push_back(p);
       }
     }
-    for (size_t k = 1; k < s.dy.size(); ++k) folded_[{s.dy[k].producer, s.dy[k].slot}] = {s.dy[0].producer, s.dy[0].slot};
+    // the fold goes into a plane of this chain's own when there is one
+    std::stable_partition(s.dy.begin(), s.dy.end(), [&](const PlaneRef& p) { return !shared(p); });
+    if (!s.dy.empty() && shared(s.dy[0])) {
+      if (l.kind == Kind::Actv) {  // masked sum -> a private plane the rest of the chain reads
+        const u64 bytes = c_.bytes_of(g_.dims(m));
+        private_plane_[m] = private_mark_ + private_bytes_;
+        private_bytes_ += round_up(bytes, kAlign);
+        s.dx = {PlaneRef{m, 0, private_plane_[m]}};
+        s.stage_dy = true;
+        for (const PlaneRef& p : s.dy) folded_[{p.producer, p.slot, owner_m}] = {m, 0};
+      } else {
+        s.stage_dy = s.dy.size() > 1;  // the kernels read the sum from the step's scratch
+      }
+    } else {
+      for (size_t k = 1; k < s.dy.size(); ++k)
+        folded_[{s.dy[k].producer, s.dy[k].slot, owner_m}] = {s.dy[0].producer, s.dy[0].slot};
+    }
     bwd_step_of_[m] = static_cast<int>(prog_->steps.size()) - 1;
-    if (l.kind == Kind::Actv && s.dy.size() == 1) find_mask_host(s);
+    if (l.kind == Kind::Actv && s.dy.size() == 1 && !s.stage_dy) find_mask_host(s);
   }
 
   // An ACTV's backward (dY *= (y > 0)) can run in the epilogue of the one
@@ -588,6 +617,7 @@ class Compiler {
     const PlaneRef p = s.dy[0];
     for (const auto& [from, to] : folded_)
       if (to == std::make_pair(p.producer, p.slot)) return;
+    if (shared(p)) return;
     for (const auto& [acc, to] : g2_alias_)
       if (to.first == p.producer) return;
     const Node& pl = g_.at(p.producer);
@@ -714,6 +744,17 @@ class Compiler {
         for (PlaneRef& p : s.dy) fix(p.off);
       }
     }
+    P.private_base = hi + static_cast<u64>(overflow_slots_) * P.overflow_slot_bytes;
+    P.private_bytes = private_bytes_;
+    if (private_bytes_ > 0) {
+      auto fix = [&](u64& off) {
+        if (off != kNoLoc && off >= private_mark_ && off < overflow_mark_) off = off - private_mark_ + P.private_base;
+      };
+      for (Step& s : P.steps) {
+        for (PlaneRef& p : s.dx) fix(p.off);
+        for (PlaneRef& p : s.dy) fix(p.off);
+      }
+    }
     // the INPUT layer's setup extent and the last step that touches it
     for (const Node& l : g_.nodes())
       if (l.kind == Kind::Input && P.input == kNone) P.input = l.id;
@@ -792,7 +833,10 @@ class Compiler {
   i64 ledger_t_ = 0;
   // program binding state
   std::map<int, int> last_in_;                               // owner -> its prefetch xfer
-  std::map<std::pair<int, int>, std::pair<int, int>> folded_;  // plane -> plane it was folded into
+  std::map<std::tuple<int, int, int>, std::pair<int, int>> folded_;  // (plane, chain) -> plane it was folded into
+  std::map<int, u64> private_plane_;                         // ACTV -> its private plane (marker offset)
+  u64 private_bytes_ = 0;
+  static constexpr u64 private_mark_ = u64{1} << 62;
   std::vector<u64> g2_slot_;
   std::vector<char> g2_accum_;
   std::map<int, std::pair<int, int>> g2_alias_;

@@ -304,11 +304,12 @@ std::vector<Finding> check_program(const Program& P, const Report& r, const Net&
         if (s.gap_len > 0 && off < s.gap_off + s.gap_len && s.gap_off < lv.end)
           flag("program-gap", at + " scratch gap overlaps live " + lv.tag + "/" + std::to_string(lv.buffer));
       if (!s.bwd || !per_layer) continue;
+      auto priv = [&](u64 off) { return off >= P.private_base && off < P.private_base + P.private_bytes; };
       for (const PlaneRef& p : s.dx)
-        if (p.off != kNoLoc && (p.producer != s.layer || !inside(p.off, "dX", s.layer)))
+        if (p.off != kNoLoc && (p.producer != s.layer || !(inside(p.off, "dX", s.layer) || priv(p.off))))
           flag("program-plane", at + " writes a plane outside its own dX");
       for (const PlaneRef& p : s.dy)
-        if (!inside(p.off, "dX", p.producer))
+        if (!inside(p.off, "dX", p.producer) && !priv(p.off))
           flag("program-plane", at + " reads plane " + std::to_string(p.producer) + "/" + std::to_string(p.slot) +
                                     " outside the live dX of its producer");
     }

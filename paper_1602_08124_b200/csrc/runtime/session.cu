@@ -52,28 +52,29 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
   if (!plan_.pass) throw PlanError(Err::Generic, "plan does not fit the budget: " + plan_.verdict());
   df_ = vdnnp::derive_dataflow(g_, d_, c_);
   L_ = g_.size();
+  // The reference vocabulary (net_graph.hpp:83,281-321): concat and
+  // elementwise joins, strided convs, any number of INPUT and LOSS layers.
+  loss_classes_.assign(static_cast<size_t>(L_), 0);
+  loss_grad_at_.assign(static_cast<size_t>(L_), 0);
   for (const Node& l : g_.nodes()) {
-    if (l.join == Join::Elementwise && l.in.size() > 1)
-      throw PlanError(Err::Config, "UNSUPPORTED: elementwise joins are not implemented by the CUDA executor");
     if (l.in.size() > static_cast<size_t>(vdnnk::kMaxConvSegs))
       throw PlanError(Err::Config, "UNSUPPORTED: more than 8 inputs to one layer");
     if (l.kind == Kind::Input) {
-      if (input_id_ >= 0) throw PlanError(Err::Config, "UNSUPPORTED: more than one INPUT layer");
-      input_id_ = l.id;
+      if (input_id_ < 0) input_id_ = l.id;
+      inputs_.push_back(l.id);
     }
     if (l.kind == Kind::Loss) {
-      if (loss_id_ >= 0) throw PlanError(Err::Config, "UNSUPPORTED: more than one LOSS layer");
-      loss_id_ = l.id;
+      if (loss_id_ < 0) loss_id_ = l.id;  // the first head writes the loss, later heads add to it
+      const Dims& ld = g_.dims(l.in[0]);
+      const int k = static_cast<int>(ld.c * ld.h * ld.w);
+      loss_classes_[static_cast<size_t>(l.id)] = k;
+      loss_grad_at_[static_cast<size_t>(l.id)] = loss_grad_count_;
+      loss_grad_count_ += g_.batch() * static_cast<u64>(k);
+      classes_ = std::max(classes_, k);
     }
-    if (l.kind == Kind::Conv && df_.at[static_cast<size_t>(l.id)].dx_bytes > 0 && l.s != 1)
-      throw PlanError(Err::Config, "UNSUPPORTED: data gradient of a strided conv that is not the first layer");
   }
-  if (input_id_ < 0 || loss_id_ < 0) throw PlanError(Err::Config, "UNSUPPORTED: graph needs one INPUT and one LOSS");
+  if (input_id_ < 0 || loss_id_ < 0) throw PlanError(Err::Config, "UNSUPPORTED: graph needs an INPUT and a LOSS layer");
   logits_owner_ = g_.owner(g_.at(loss_id_).in[0]);
-  {
-    const Dims& ld = g_.dims(g_.at(loss_id_).in[0]);
-    classes_ = static_cast<int>(ld.c * ld.h * ld.w);
-  }
   // pinned host slots: one per offloaded owner
   host_slot_.assign(static_cast<size_t>(L_), kNoOff);
   for (const vdnnp::Xfer& x : prog_.xfers)
@@ -106,7 +107,10 @@ void Session::acquire() {
   if (prog_.arena_hi <= prog_.arena_lo) throw PlanError(Err::Generic, "empty plan");
   arena_lo_ = prog_.arena_lo;
   arena_bytes_ = prog_.arena_hi - prog_.arena_lo;
-  const u64 overflow = static_cast<u64>(prog_.overflow_slots) * prog_.overflow_slot_bytes;
+  // beyond the planned span (reported as non-pool scratch): two-buffer
+  // overflow gradient slots, then the private planes of ACTVs over shared
+  // elementwise-join maps
+  const u64 overflow = static_cast<u64>(prog_.overflow_slots) * prog_.overflow_slot_bytes + prog_.private_bytes;
   check(cudaMalloc(&arena_, arena_bytes_ + overflow), "cudaMalloc(device arena)");
   base_ = arena_ - arena_lo_;
   scratch_bytes_ += overflow;
@@ -126,13 +130,13 @@ void Session::acquire() {
 
   // non-pool scratch: softmax gradient + per-row loss + loss, two label slots
   const u64 n = g_.batch();
-  check(cudaMalloc(&loss_grad_, n * static_cast<u64>(classes_) * 4), "cudaMalloc(loss grad)");
+  check(cudaMalloc(&loss_grad_, loss_grad_count_ * 4), "cudaMalloc(loss grad)");
   check(cudaMalloc(&row_loss_, n * 4), "cudaMalloc(row loss)");
   check(cudaMalloc(&loss_, 4), "cudaMalloc(loss)");
   check(cudaMalloc(&labels_, 2 * n * 4), "cudaMalloc(labels)");
   labels_next_ = labels_ + n;
   check(cudaHostAlloc(&pinned_loss_, 4, cudaHostAllocDefault), "cudaHostAlloc(loss)");
-  scratch_bytes_ += n * static_cast<u64>(classes_) * 4 + n * 12 + 4;
+  scratch_bytes_ += loss_grad_count_ * 4 + n * 12 + 4;
   check(cudaMemsetAsync(labels_, 0, 2 * n * 4, cs_), "memset labels");
 
   build_program();
@@ -234,7 +238,16 @@ void Session::build_program() {
   w_off_.assign(static_cast<size_t>(L_), kNoOff);
   for (int i = 0; i < L_; ++i) w_off_[static_cast<size_t>(i)] = prog_.w_off[static_cast<size_t>(i)];
   x_off_ = prog_.input_off;
-  input_idle_after_ = prog_.input_idle_after;
+  input_idle_after_ = inputs_.size() == 1 ? prog_.input_idle_after : -1;
+  for (int id : inputs_) {  // setup extents of every INPUT layer
+    u64 off = kNoOff;
+    for (const Event& e : plan_.events)
+      if (e.kind == Ev::Alloc && e.buffer == id && e.tag == "X") {
+        off = e.off;
+        break;
+      }
+    input_off_.push_back(off);
+  }
   auto transfer = [&](int xi) {
     const vdnnp::Xfer& x = prog_.xfers[static_cast<size_t>(xi)];
     Transfer t;
@@ -263,7 +276,11 @@ void Session::build_program() {
       for (int xi : p.issues) s.offloads.push_back(transfer(xi));
       s.gap_off = p.gap_off;
       s.gap_len = p.gap_len;
-      if (contraction) s.scratch = vdnnk::conv_fprop_ws_bytes(conv_args(s.layer, s.in_off, nullptr));
+      const float* probe_x = summed(s.layer) ? F(s.in_off[0]) : nullptr;  // shapes only
+      if (summed(s.layer)) s.sum_bytes = round_up(g_.dims(l.in[0]).count() * 4, 1024);
+      if (contraction) s.part_bytes = vdnnk::conv_fprop_ws_bytes(conv_args(s.layer, s.in_off, nullptr, probe_x));
+      s.part_off = s.sum_bytes;
+      s.scratch = s.part_bytes ? s.part_off + s.part_bytes : s.sum_bytes;
       fwd_.push_back(std::move(s));
     } else {
       BwdStep s;
@@ -281,11 +298,35 @@ void Session::build_program() {
       s.mask_plane.assign(s.plane_off.size(), 0);
       s.gap_off = p.gap_off;
       s.gap_len = p.gap_len;
-      if (contraction) {
-        s.scratch = vdnnk::conv_wgrad_ws_bytes(conv_args(s.layer, s.in_off, nullptr));
-        if (!s.plane_off.empty())
-          s.scratch = std::max(s.scratch, vdnnk::conv_dgrad_ws_bytes(conv_args(s.layer, s.in_off, &s.plane_off)));
+      s.stage_dy = p.stage_dy;
+      if (p.stage_dy && l.kind == Kind::Actv) s.priv_out = p.dx.at(0).off;
+      const bool sum = summed(s.layer) && l.kind != Kind::Actv;
+      const float* probe_x = sum ? F(s.in_off[0]) : nullptr;
+      size_t at = 0;
+      if (sum) s.sum_bytes = round_up(g_.dims(l.in[0]).count() * 4, 1024), at = s.sum_bytes;
+      if (s.stage_dy && l.kind != Kind::Actv) {
+        s.stage_off = at;
+        s.stage_bytes = round_up(g_.dims(s.layer).count() * 4, 1024);
+        at += s.stage_bytes;
       }
+      bool any_plane = false;
+      for (u64 o : s.plane_off) any_plane = any_plane || o != kNoOff;
+      if (l.kind == Kind::Conv && l.s > 1 && any_plane) {  // dgrad through a zero-inserted dY
+        const Dims& y = g_.dims(s.layer);
+        s.dil_off = at;
+        s.dil_bytes = round_up(y.n * ((y.h - 1) * l.s + 1) * ((y.w - 1) * l.s + 1) * y.c * 4, 1024);
+        at += s.dil_bytes;
+      }
+      if (contraction) {
+        s.part_bytes = vdnnk::conv_wgrad_ws_bytes(conv_args(s.layer, s.in_off, nullptr, probe_x));
+        if (any_plane) {
+          vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off, probe_x);
+          a.stride = 1;
+          s.part_bytes = std::max(s.part_bytes, vdnnk::conv_dgrad_ws_bytes(a));
+        }
+      }
+      s.part_off = at;
+      s.scratch = s.part_bytes ? at + s.part_bytes : at;
       bwd_.push_back(std::move(s));
     }
   }
@@ -321,6 +362,7 @@ bool Session::tf32_exact_ok(int owner) const {
     const int u = todo.back();
     todo.pop_back();
     const Node& n = g_.at(u);
+    if (summed(u)) return false;  // a join's sum of truncated maps is not the truncated sum
     if (n.kind == Kind::Actv) {
       todo.insert(todo.end(), g_.users(u).begin(), g_.users(u).end());
     } else if (n.kind == Kind::Conv) {
@@ -373,10 +415,69 @@ void Session::fuse_relus() {
 }
 
 // ------------------------------------------------------------- helpers ----
+bool Session::summed(int layer) const {
+  const Node& l = g_.at(layer);
+  return l.join == Join::Elementwise && l.in.size() > 1;
+}
+
+// X of an elementwise join (net_graph.hpp:290-296: identical shapes) = the
+// sum of its inputs, into the step's scratch.
+void Session::sum_inputs(int layer, const std::vector<u64>& in_off, float* dst) {
+  const Node& l = g_.at(layer);
+  std::vector<const float*> src;
+  for (size_t i = 0; i < l.in.size(); ++i) src.push_back(F(in_off[i]));
+  check(vdnnk::combine(dst, src.data(), static_cast<int>(src.size()), nullptr, g_.dims(l.in[0]).count(), cs_),
+        "join sum");
+}
+
+vdnnk::PoolArgs Session::pool_args(int layer, const std::vector<u64>& in_off, const std::vector<u64>* planes,
+                                   const float* sum_x) const {
+  const Node& l = g_.at(layer);
+  vdnnk::PoolArgs p;
+  const Dims& first = g_.dims(l.in[0]);
+  p.n = static_cast<int>(first.n);
+  p.h = static_cast<int>(first.h);
+  p.w = static_cast<int>(first.w);
+  p.window = static_cast<int>(l.k);
+  p.stride = static_cast<int>(l.s);
+  p.nseg = sum_x ? 1 : static_cast<int>(l.in.size());
+  for (int i = 0; i < p.nseg; ++i) {
+    p.x[i] = sum_x ? sum_x : F(in_off[static_cast<size_t>(i)]);
+    p.c[i] = static_cast<int>(g_.dims(l.in[static_cast<size_t>(i)]).c);
+    p.dx[i] = nullptr;
+  }
+  if (planes) {
+    for (size_t i = 0; i < planes->size(); ++i) {
+      if ((*planes)[i] == kNoOff) continue;
+      const size_t slot = sum_x ? 0 : i;  // a join's one shared map
+      p.dx[slot] = F((*planes)[i]);
+    }
+  }
+  return p;
+}
+
 vdnnk::ConvArgs Session::conv_args(int layer, const std::vector<u64>& in_off,
-                                   const std::vector<u64>* planes) const {
+                                   const std::vector<u64>* planes, const float* sum_x) const {
   const Node& l = g_.at(layer);
   vdnnk::ConvArgs a;
+  if (sum_x) {  // elementwise join: one segment (the summed input), one shared gradient map
+    const Dims& d = g_.dims(l.in[0]);
+    const bool fc = l.kind == Kind::Fc;
+    a.nseg = 1;
+    a.n = static_cast<int>(d.n);
+    a.h = fc ? 1 : static_cast<int>(d.h);
+    a.w = fc ? 1 : static_cast<int>(d.w);
+    a.c[0] = static_cast<int>(fc ? d.c * d.h * d.w : d.c);
+    a.x[0] = sum_x;
+    if (planes)
+      for (u64 o : *planes)
+        if (o != kNoOff && !a.dx[0]) a.dx[0] = F(o);
+    a.cout = static_cast<int>(l.out);
+    a.kh = a.kw = fc ? 1 : static_cast<int>(l.k);
+    a.stride = fc ? 1 : static_cast<int>(l.s);
+    a.pad = fc ? 0 : static_cast<int>(l.p);
+    return a;
+  }
   a.nseg = static_cast<int>(l.in.size());
   const Dims& first = g_.dims(l.in[0]);
   a.n = static_cast<int>(first.n);
@@ -446,41 +547,35 @@ void Session::run_fwd(const FwdStep& s, float lr) {
   }
   if (timed_) check(cudaEventRecord(ev_[2 * s.ev], cs_), "record");
   if (!probes_.empty()) probe_copy(s.ev, false);
+  char* scr = reinterpret_cast<char*>(scratch_for(s.gap_off, s.gap_len, s.scratch));
+  const float* sum_x = nullptr;
+  if (s.sum_bytes) {
+    sum_inputs(s.layer, s.in_off, reinterpret_cast<float*>(scr));
+    sum_x = reinterpret_cast<const float*>(scr);
+  }
+  float* part = s.part_bytes ? reinterpret_cast<float*>(scr + s.part_off) : nullptr;
   switch (l.kind) {
     case Kind::Conv:
     case Kind::Fc: {
-      vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
+      vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, sum_x);
       a.relu_out = s.relu ? 1 : 0;
       const float* bias = l.kind == Kind::Fc ? F(s.w_off) + g_.fc_inputs(s.layer) * l.out : nullptr;
-      check(vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_, scratch_for(s.gap_off, s.gap_len, s.scratch),
-                              s.scratch),
-            "conv_fprop");
+      check(vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_, part, s.part_bytes), "conv_fprop");
       break;
     }
     case Kind::Actv:
       if (!s.skip) check(vdnnk::relu_fwd(F(s.out_off), g_.dims(s.layer).count(), cs_), "relu_fwd");
       break;
-    case Kind::Pool: {
-      vdnnk::PoolArgs p;
-      const Dims& first = g_.dims(l.in[0]);
-      p.n = static_cast<int>(first.n);
-      p.h = static_cast<int>(first.h);
-      p.w = static_cast<int>(first.w);
-      p.window = static_cast<int>(l.k);
-      p.stride = static_cast<int>(l.s);
-      p.nseg = static_cast<int>(l.in.size());
-      for (int i = 0; i < p.nseg; ++i) {
-        p.x[i] = F(s.in_off[static_cast<size_t>(i)]);
-        p.c[i] = static_cast<int>(g_.dims(l.in[static_cast<size_t>(i)]).c);
-      }
-      check(vdnnk::maxpool_fwd(p, F(s.out_off), cs_), "maxpool_fwd");
+    case Kind::Pool:
+      check(vdnnk::maxpool_fwd(pool_args(s.layer, s.in_off, nullptr, sum_x), F(s.out_off), cs_), "maxpool_fwd");
       break;
-    }
-    case Kind::Loss:
-      check(vdnnk::softmax_xent_fwd(F(s.in_off[0]), labels_, static_cast<int>(g_.batch()), classes_, loss_grad_,
-                                    row_loss_, loss_, cs_),
+    case Kind::Loss: {
+      const size_t li = static_cast<size_t>(s.layer);
+      check(vdnnk::softmax_xent_fwd(F(s.in_off[0]), labels_, static_cast<int>(g_.batch()), loss_classes_[li],
+                                    loss_grad_ + loss_grad_at_[li], row_loss_, loss_, cs_, s.layer != loss_id_),
             "softmax_xent");
       break;
+    }
     default:
       break;
   }
@@ -516,32 +611,55 @@ void Session::run_bwd(const BwdStep& s, float lr) {
   for (int ev : s.wait_prefetch) check(cudaStreamWaitEvent(cs_, xfer_ev_[static_cast<size_t>(ev)], 0), "wait");
   if (timed_) check(cudaEventRecord(ev_[2 * s.ev], cs_), "record");
 
+  char* scr = reinterpret_cast<char*>(scratch_for(s.gap_off, s.gap_len, s.scratch));
+  float* part = s.part_bytes ? reinterpret_cast<float*>(scr + s.part_off) : nullptr;
+  const size_t ycount = g_.dims(s.layer).count();
   float* dy = s.dy_off.empty() ? nullptr : F(s.dy_off[0]);
   std::vector<const float*> extra;
   for (size_t k = 1; k < s.dy_off.size(); ++k) extra.push_back(F(s.dy_off[k]));
-  if (l.kind != Kind::Actv && !extra.empty())
-    check(vdnnk::add_into(dy, extra.data(), static_cast<int>(extra.size()), g_.dims(s.layer).count(), cs_), "fold");
+  if (l.kind != Kind::Actv && s.stage_dy) {  // shared planes are read-only: sum into scratch
+    std::vector<const float*> all{dy};
+    all.insert(all.end(), extra.begin(), extra.end());
+    dy = reinterpret_cast<float*>(scr + s.stage_off);
+    check(vdnnk::combine(dy, all.data(), static_cast<int>(all.size()), nullptr, ycount, cs_), "fold (staged)");
+  } else if (l.kind != Kind::Actv && !extra.empty()) {
+    check(vdnnk::add_into(dy, extra.data(), static_cast<int>(extra.size()), ycount, cs_), "fold");
+  }
+  const float* sum_x = nullptr;
+  if (s.sum_bytes) {
+    sum_inputs(s.layer, s.in_off, reinterpret_cast<float*>(scr));
+    sum_x = reinterpret_cast<const float*>(scr);
+  }
   if (!probes_.empty()) probe_copy(s.ev, false);
 
   switch (l.kind) {
     case Kind::Conv:
     case Kind::Fc: {
       const bool fc = l.kind == Kind::Fc;
-      if (!s.plane_off.empty()) {
-        vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off);
-        for (int i = 0; i < a.nseg; ++i) a.mask_in[i] = s.mask_plane[static_cast<size_t>(i)];
-        check(vdnnk::conv_dgrad(a, F(s.w_off), dy, s.accumulate, cs_, scratch_for(s.gap_off, s.gap_len, s.scratch),
-                                s.scratch),
-              "conv_dgrad");
+      bool any_plane = false;
+      for (u64 o : s.plane_off) any_plane = any_plane || o != kNoOff;
+      if (any_plane) {
+        vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off, sum_x);
+        for (int i = 0; i < a.nseg; ++i) a.mask_in[i] = sum_x ? 0 : s.mask_plane[static_cast<size_t>(i)];
+        const float* dyd = dy;
+        if (s.dil_bytes) {  // strided conv: stride-1 dgrad over the zero-inserted dY
+          const Dims& y = g_.dims(s.layer);
+          float* d = reinterpret_cast<float*>(scr + s.dil_off);
+          check(vdnnk::dilate(d, dy, static_cast<int>(y.n), static_cast<int>(y.h), static_cast<int>(y.w),
+                              static_cast<int>(y.c), a.stride, cs_),
+                "dilate dY");
+          a.stride = 1;
+          dyd = d;
+        }
+        check(vdnnk::conv_dgrad(a, F(s.w_off), dyd, s.accumulate, cs_, part, s.part_bytes), "conv_dgrad");
       }
-      const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr);
+      const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, sum_x);
       // split-K partials: the split count depends only on the layer shape
       // (the launch always gets the bytes it asks for), so the reduction
       // order -- and every bit of the update -- is independent of the offload
       // policy and of where the partials live
       float* dw = grads_ ? grads_ + grad_off_[mi] : nullptr;
-      check(vdnnk::conv_wgrad(a, dy, F(s.w_off), lr, dw, scratch_for(s.gap_off, s.gap_len, s.scratch), s.scratch, cs_),
-            "conv_wgrad");
+      check(vdnnk::conv_wgrad(a, dy, F(s.w_off), lr, dw, part, s.part_bytes, cs_), "conv_wgrad");
       if (fc) {
         const u64 in = g_.fc_inputs(s.layer);
         float* bias = F(s.w_off) + in * l.out;
@@ -552,37 +670,34 @@ void Session::run_bwd(const BwdStep& s, float lr) {
       break;
     }
     case Kind::Pool: {
-      vdnnk::PoolArgs p;
-      const Dims& first = g_.dims(l.in[0]);
-      p.n = static_cast<int>(first.n);
-      p.h = static_cast<int>(first.h);
-      p.w = static_cast<int>(first.w);
-      p.window = static_cast<int>(l.k);
-      p.stride = static_cast<int>(l.s);
-      p.nseg = static_cast<int>(l.in.size());
+      vdnnk::PoolArgs p = pool_args(s.layer, s.in_off, &s.plane_off, sum_x);
+      bool any_plane = false;
       for (int i = 0; i < p.nseg; ++i) {
-        p.x[i] = F(s.in_off[static_cast<size_t>(i)]);
-        p.c[i] = static_cast<int>(g_.dims(l.in[static_cast<size_t>(i)]).c);
-        p.dx[i] = s.plane_off.empty() || s.plane_off[static_cast<size_t>(i)] == kNoOff
-                      ? nullptr
-                      : F(s.plane_off[static_cast<size_t>(i)]);
-        p.mask_in[i] = s.mask_plane.empty() ? 0 : s.mask_plane[static_cast<size_t>(i)];
+        p.mask_in[i] = (sum_x || s.mask_plane.empty()) ? 0 : s.mask_plane[static_cast<size_t>(i)];
+        any_plane = any_plane || p.dx[i] != nullptr;
       }
-      if (!s.plane_off.empty()) check(vdnnk::maxpool_bwd(p, F(s.out_off), dy, cs_), "maxpool_bwd");
+      if (any_plane) check(vdnnk::maxpool_bwd(p, F(s.out_off), dy, cs_), "maxpool_bwd");
       break;
     }
     case Kind::Actv:
-      if (dy && !s.skip)
-        check(vdnnk::relu_bwd(dy, extra.data(), static_cast<int>(extra.size()), F(s.out_off),
-                              g_.dims(s.layer).count(), cs_),
+      if (dy && s.priv_out != kNoOff) {  // shared incoming planes: masked sum into the private plane
+        std::vector<const float*> all{dy};
+        all.insert(all.end(), extra.begin(), extra.end());
+        check(vdnnk::combine(F(s.priv_out), all.data(), static_cast<int>(all.size()), F(s.out_off), ycount, cs_),
+              "relu_bwd (private plane)");
+      } else if (dy && !s.skip) {
+        check(vdnnk::relu_bwd(dy, extra.data(), static_cast<int>(extra.size()), F(s.out_off), ycount, cs_),
               "relu_bwd");
+      }
       break;
-    case Kind::Loss:
+    case Kind::Loss: {
+      const size_t li = static_cast<size_t>(s.layer);
       if (!s.plane_off.empty() && s.plane_off[0] != kNoOff)
-        check(cudaMemcpyAsync(F(s.plane_off[0]), loss_grad_, g_.batch() * static_cast<u64>(classes_) * 4,
-                              cudaMemcpyDeviceToDevice, cs_),
+        check(cudaMemcpyAsync(F(s.plane_off[0]), loss_grad_ + loss_grad_at_[li],
+                              g_.batch() * static_cast<u64>(loss_classes_[li]) * 4, cudaMemcpyDeviceToDevice, cs_),
               "loss grad copy");
       break;
+    }
     default:
       break;
   }
@@ -704,6 +819,7 @@ void Session::prefetch_batch_host(const float* images, const int32_t* labels) {
   const u64 bytes = df_.at[static_cast<size_t>(input_id_)].bytes;
   const u64 lbytes = static_cast<u64>(g_.batch()) * 4;
   if (has_staged_) throw PlanError(Err::Generic, "a prefetched batch is already waiting for the next step");
+  if (inputs_.size() != 1) throw PlanError(Err::Config, "prefetch_batch_host needs a graph with one INPUT layer");
   if (!in_stream_) {
     check(cudaStreamCreateWithFlags(&in_stream_, cudaStreamNonBlocking), "stream");
     check(cudaEventCreateWithFlags(&staged_ready_, cudaEventDisableTiming), "event");
@@ -760,9 +876,23 @@ float Session::read_loss() {
 }
 
 void Session::synthetic_batch(u64 seed) {
-  const u64 count = df_.at[static_cast<size_t>(input_id_)].bytes / 4;
-  check(vdnnk::fill_uniform(F(x_off_), count, -1.0f, 1.0f, seed, cs_), "images");
+  for (size_t i = 0; i < inputs_.size(); ++i) {
+    const u64 count = df_.at[static_cast<size_t>(inputs_[i])].bytes / 4;
+    check(vdnnk::fill_uniform(F(input_off_[i]), count, -1.0f, 1.0f, seed + 7919 * i, cs_), "images");
+  }
   check(vdnnk::fill_labels(labels_, g_.batch(), classes_, seed + 1, cs_), "labels");
+}
+
+void Session::set_input(int layer, const float* images, bool device) {
+  for (size_t i = 0; i < inputs_.size(); ++i) {
+    if (inputs_[i] != layer) continue;
+    const u64 bytes = df_.at[static_cast<size_t>(layer)].bytes;
+    check(cudaMemcpyAsync(F(input_off_[i]), images, bytes, device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                          cs_),
+          "images");
+    return;
+  }
+  throw PlanError(Err::Generic, "set_input: not an INPUT layer");
 }
 
 void Session::get_weights(int layer, float* host, size_t count) {
@@ -820,7 +950,7 @@ Session::ProbeLayout Session::probe_layout(int layer, bool bwd) const {
     if (contraction) add(kPW, 0, df_.at[li].w_bytes, 0, s->w_off, false);
     if (l.kind == Kind::Actv) add(kPX, 0, y_bytes, 0, s->out_off, false);
     if (l.kind == Kind::Loss) {
-      add(kPLossGrad, 0, g_.batch() * static_cast<u64>(classes_) * 4, 2, 0, true);
+      add(kPLossGrad, 0, g_.batch() * static_cast<u64>(loss_classes_[li]) * 4, 2, loss_grad_at_[li], true);
       add(kPLoss, 0, 4, 3, 0, true);
     } else {
       add(kPY, 0, y_bytes, 0, s->out_off, true);
@@ -838,13 +968,17 @@ Session::ProbeLayout Session::probe_layout(int layer, bool bwd) const {
   if (l.kind == Kind::Actv) {
     add(kPY, 0, y_bytes, 0, s->out_off, false);
     for (size_t k = 0; k < s->dy_off.size(); ++k) add(kPDY, static_cast<int>(k), y_bytes, 0, s->dy_off[k], false);
-    if (!s->dy_off.empty()) add(kPDX, 0, y_bytes, 0, s->dy_off[0], true);
+    if (!s->dy_off.empty()) add(kPDX, 0, y_bytes, 0, s->priv_out != kNoOff ? s->priv_out : s->dy_off[0], true);
     return p;
   }
   if (l.kind == Kind::Conv || l.kind == Kind::Fc || l.kind == Kind::Pool)
     for (size_t i = 0; i < s->in_off.size(); ++i) add(kPX, static_cast<int>(i), in_bytes(i), 0, s->in_off[i], false);
   if (contraction) add(kPW, 0, df_.at[li].w_bytes, 0, s->w_off, false);
-  if (!s->dy_off.empty()) add(kPDY, 0, y_bytes, 0, s->dy_off[0], false);  // after the fold of the other planes
+  if (s->stage_dy) {  // shared planes stay as they are: every incoming plane (the kernels read their sum)
+    for (size_t k = 0; k < s->dy_off.size(); ++k) add(kPDY, static_cast<int>(k), y_bytes, 0, s->dy_off[k], false);
+  } else if (!s->dy_off.empty()) {
+    add(kPDY, 0, y_bytes, 0, s->dy_off[0], false);  // after the fold of the other planes
+  }
   for (size_t i = 0; i < s->plane_off.size(); ++i) {
     if (s->plane_off[i] == kNoOff) continue;
     const u64 b = l.kind == Kind::Loss ? g_.dims(l.in[0]).count() * 4 : in_bytes(i);
@@ -881,7 +1015,7 @@ void Session::probe_copy(int ev, bool after) {
       switch (s.src) {
         case 0: src = base_ + s.src_off; break;
         case 1: src = reinterpret_cast<const char*>(grads_ + s.src_off); break;
-        case 2: src = reinterpret_cast<const char*>(loss_grad_); break;
+        case 2: src = reinterpret_cast<const char*>(loss_grad_ + s.src_off); break;
         default: src = reinterpret_cast<const char*>(loss_); break;
       }
       check(cudaMemcpyAsync(a.dst + s.dst, src, s.bytes, cudaMemcpyDefault, cs_), "probe copy");

@@ -65,7 +65,11 @@ struct FwdStep {
   bool relu = false;  // conv/FC: ReLU of the following ACTV fused into the epilogue
   bool skip = false;  // ACTV whose ReLU was fused into its producer
   u64 gap_off = 0, gap_len = 0;  // free pool segment while the kernel runs
-  size_t scratch = 0;            // split-K partial bytes the launch needs
+  // step scratch (the free gap when it is wide enough, else the fallback
+  // buffer): [summed elementwise-join input | split-K partials]
+  size_t scratch = 0;
+  size_t sum_bytes = 0;          // elementwise join: the summed input X
+  size_t part_off = 0, part_bytes = 0;
 };
 
 struct BwdStep {
@@ -83,7 +87,15 @@ struct BwdStep {
   std::vector<char> mask_plane;         // per input: ReLU backward of that input fused here
   bool skip = false;                    // ACTV whose backward was fused into its gradient's producer
   u64 gap_off = 0, gap_len = 0;         // free pool segment while the kernel runs
-  size_t scratch = 0;                   // split-K partial bytes the launches need
+  // incoming planes all shared (elementwise join map, read-only): ACTV
+  // writes the masked sum to its private plane priv_out, other layers read
+  // the sum from scratch
+  bool stage_dy = false;
+  u64 priv_out = kNoOff;
+  // step scratch: [summed join input | staged dY | zero-inserted dY (strided
+  // conv dgrad) | split-K partials]
+  size_t scratch = 0;
+  size_t sum_bytes = 0, stage_off = 0, stage_bytes = 0, dil_off = 0, dil_bytes = 0, part_off = 0, part_bytes = 0;
 };
 
 class Session {
@@ -95,6 +107,8 @@ class Session {
 
   void set_batch_host(const float* images, const int32_t* labels);
   void set_batch_device(const float* images, const int32_t* labels);
+  // Graphs with several INPUT layers: images of one of them (layer id).
+  void set_input(int layer, const float* images, bool device);
   // Input pipeline: copy the NEXT batch from pinned host memory straight into
   // the INPUT extent on a separate stream, as soon as the running step no
   // longer touches that extent (planned, Program::input_idle_after); the next
@@ -162,7 +176,13 @@ class Session {
   void init_weights();
   void run_fwd(const FwdStep& s, float lr);
   void run_bwd(const BwdStep& s, float lr);
-  vdnnk::ConvArgs conv_args(int layer, const std::vector<u64>& in_off, const std::vector<u64>* planes) const;
+  // sum_x: the summed input of an elementwise join (one segment, shared plane)
+  vdnnk::ConvArgs conv_args(int layer, const std::vector<u64>& in_off, const std::vector<u64>* planes,
+                            const float* sum_x = nullptr) const;
+  vdnnk::PoolArgs pool_args(int layer, const std::vector<u64>& in_off, const std::vector<u64>* planes,
+                            const float* sum_x) const;
+  bool summed(int layer) const;  // elementwise join over >= 2 inputs
+  void sum_inputs(int layer, const std::vector<u64>& in_off, float* dst);
   void check(cudaError_t e, const char* what) const;
 
   vdnnp::Net g_;
@@ -175,7 +195,12 @@ class Session {
   vdnnp::Dataflow df_;
   int L_ = 0;
   int input_id_ = -1, loss_id_ = -1, logits_owner_ = -1;
-  int classes_ = 0;
+  int classes_ = 0;                 // max over LOSS heads (synthetic labels)
+  std::vector<int> inputs_;         // INPUT layers (ids ascending) and their setup extents
+  std::vector<u64> input_off_;
+  std::vector<int> loss_classes_;   // per layer (LOSS heads only)
+  std::vector<u64> loss_grad_at_;   // per layer: float offset of its softmax gradient in loss_grad_
+  u64 loss_grad_count_ = 0;
 
   cudaStream_t cs_ = nullptr, ms_ = nullptr;
   char* arena_ = nullptr;

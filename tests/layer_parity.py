@@ -132,9 +132,12 @@ def _compare(g, L, i, bwd, d, labels, precise) -> List[Dict]:
         if l.kind == numeric.LOSS:
             r = numeric.layer_forward(g, i, xs, labels=labels)
             n = xs[0].shape[0]
-            e1 = abs(float(d[("LOSS", 0)][0]) - float(r["LOSS"])) / max(1.0, abs(float(r["LOSS"])))
             e2 = numeric.max_rel(d[("LOSS_GRAD", 0)].reshape(n, -1), r["LOSS_GRAD"])
-            return [_rec(l, "fwd", "LOSS", 1, e1, e1), _rec(l, "fwd", "LOSS_GRAD", 1, e2, e2)]
+            out = [_rec(l, "fwd", "LOSS_GRAD", 1, e2, e2)]
+            if i == min(x.id for x in L if x.kind == numeric.LOSS):  # later heads add to the loss
+                e1 = abs(float(d[("LOSS", 0)][0]) - float(r["LOSS"])) / max(1.0, abs(float(r["LOSS"])))
+                out.append(_rec(l, "fwd", "LOSS", 1, e1, e1))
+            return out
         nb = _sample_batch(l, L)
         y = d[("Y", 0)].reshape(numeric._nhwc(l.shape))[:nb]
         r_plain = numeric.layer_forward(g, i, xs, w, relu=lay["relu_fused"], batch=nb)["Y"]
@@ -155,9 +158,12 @@ def _compare(g, L, i, bwd, d, labels, precise) -> List[Dict]:
     if l.kind == numeric.LOSS:
         return out  # copies the FWD's gradient (checked there)
     xs = [d[("X", j)].reshape(numeric._nhwc(sh)) for j, sh in enumerate(shapes)]
-    dy = d[("DY", 0)].reshape(numeric._nhwc(l.shape))
+    ndy = sum(1 for sg in lay["segs"] if sg[0] == "DY")  # > 1: shared planes the kernels read the sum of
+    dy = sum(d[("DY", k)].to(torch.float64) for k in range(ndy)).reshape(numeric._nhwc(l.shape))
     w = d.get(("W", 0))
     planes = sorted(k[1] for k in d if isinstance(k, tuple) and k[0] == "DX")
+    if l.join == 1 and len(l.inputs) > 1:  # one shared map: every probed DX segment is the same extent
+        planes = planes[:1]
     before = {j: d[("DX_BEFORE", j)].reshape(numeric._nhwc(shapes[j])) for j in planes if ("DX_BEFORE", j) in d}
     contraction = l.kind in (numeric.CONV, numeric.FC)
     nb = _sample_batch(l, L)
@@ -232,7 +238,10 @@ def violations(recs: List[Dict], precise: bool) -> List[str]:
             if r["err_plain"] > tol:
                 bad.append(f"L{r['layer']} {r['op']} {r['tensor']} K={r['K']}: {r['err_plain']:.3e} > {tol:.2e}")
         else:
-            if r["err_emu"] > TF32_EMU_TOL[r["op"]]:
+            # small contractions may run on fp32-exact SIMT / rounding paths
+            # (first layers with C <= 4, tiny wgrad): more accurate than TF32
+            # truncation, so they meet the fp32 bound against float64 instead
+            if r["err_emu"] > TF32_EMU_TOL[r["op"]] and r["err_plain"] > fp32_tol(r["K"]):
                 bad.append(f"L{r['layer']} {r['op']} {r['tensor']} K={r['K']}: vs tf32-operand oracle "
                            f"{r['err_emu']:.3e} > {TF32_EMU_TOL[r['op']]:.1e}")
             if r["err_plain"] > TF32_PLAIN_TOL:

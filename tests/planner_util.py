@@ -116,3 +116,74 @@ def compare_case(spec_graph: str, case: dict, cost_spec: str = "") -> None:
     for k in want:
         assert got[k] == want[k], f"{case['decision_spec']} @ {case['capacity']}: field {k} differs"
     assert [v.kind for v in V.replay_check(r, g, d, cap)] == ref["report"]["violations"]
+
+
+def vocab_spec(rng) -> str:
+    """A random graph over the reference's whole vocabulary (net_graph.hpp:83,
+    281-321): elementwise joins of ReLU branches (read-only shared gradient
+    maps), concat joins, strided convs (exact divisibility), overlapping and
+    non-overlapping pools, two INPUT layers, an auxiliary LOSS head, an FC over
+    an elementwise join. Spec format of graph_from_spec."""
+    batch = 2 + rng.randrange(3)
+    h = rng.choice([9, 12, 15, 16])
+    layers, shape = [], {}
+
+    def add(s, sh=None):
+        layers.append(s)
+        shape[len(layers) - 1] = sh
+        return len(layers) - 1
+
+    c0 = rng.choice([3, 4, 8])
+    inputs = [add(f"input - {c0} {h} {h} 0 0", (c0, h, h))]
+    if rng.randrange(2):  # a second INPUT layer, concatenated with the first
+        c1 = rng.choice([1, 4])
+        inputs.append(add(f"input - {c1} {h} {h} 0 0", (c1, h, h)))
+    c = rng.choice([8, 16, 32])
+    prev = add(f"conv {','.join(map(str, inputs))} 3 1 1 {c} 0", (c, h, h))
+    prev = add(f"actv {prev} 0 0 0 0 0", shape[prev])
+    aux_done = False
+    for _ in range(4 + rng.randrange(3)):
+        c, hh, _w = shape[prev]
+        r = rng.randrange(6)
+        if r == 0:  # elementwise join of two branches, at least one a ReLU chain
+            oc = rng.choice([4, 8, 32])
+            a = add(f"conv {prev} 3 1 1 {oc} 0", (oc, hh, hh))
+            a = add(f"actv {a} 0 0 0 0 0", shape[a])
+            b = add(f"conv {prev} 1 1 0 {oc} 0", (oc, hh, hh))
+            if rng.randrange(2):
+                b = add(f"actv {b} 0 0 0 0 0", shape[b])
+            k, oc2 = rng.choice([1, 3]), rng.choice([8, 16])
+            prev = add(f"conv {a},{b} {k} 1 {k // 2} {oc2} 1", (oc2, hh, hh))
+        elif r == 1 and hh >= 5:  # strided conv: (h + 2p - k) divisible by the stride
+            k, p = rng.choice([(3, 1), (1, 0)]) if hh % 2 else rng.choice([(2, 0), (4, 1)])
+            oc = rng.choice([8, 16, 32])
+            ho = (hh + 2 * p - k) // 2 + 1
+            prev = add(f"conv {prev} {k} 2 {p} {oc} 0", (oc, ho, ho))
+            prev = add(f"actv {prev} 0 0 0 0 0", shape[prev])
+        elif r == 2 and hh >= 4:
+            win = rng.choice([2, 3])
+            ho = (hh - win) // 2 + 1
+            prev = add(f"pool {prev} {win} 2 0 0 0", (c, ho, ho))
+        elif r == 3:  # concat fork/join
+            oa = rng.choice([4, 8])
+            a = add(f"conv {prev} 1 1 0 {oa} 0", (oa, hh, hh))
+            b = add(f"actv {prev} 0 0 0 0 0", shape[prev])
+            oc = rng.choice([8, 16])
+            prev = add(f"conv {a},{b} 3 1 1 {oc} 0", (oc, hh, hh))
+        elif r == 4 and not aux_done:  # auxiliary LOSS head
+            f = add(f"fc {prev} {rng.choice([5, 10])} 0 0 0 0")
+            add(f"loss {f} 0 0 0 0 0")
+            aux_done = True
+        else:
+            oc = rng.choice([8, 16, 32, 64])
+            prev = add(f"conv {prev} 3 1 1 {oc} 0", (oc, hh, hh))
+            prev = add(f"actv {prev} 0 0 0 0 0", shape[prev])
+    if rng.randrange(2):  # classifier over an elementwise join of two FC branches
+        a = add(f"fc {prev} 16 0 0 0 0")
+        a = add(f"actv {a} 0 0 0 0 0")
+        b = add(f"fc {prev} 16 0 0 0 0")
+        prev = add(f"fc {a},{b} 10 0 0 0 1")
+    else:
+        prev = add(f"fc {prev} 10 0 0 0 0")
+    add(f"loss {prev} 0 0 0 0 0")
+    return f"B={batch}|" + "|".join(layers)

@@ -117,7 +117,9 @@ def test_vgg16_b256_dyn_two_step_loss_matches_oracle():
     wgrad+SGD) of VGG-16 b256 under the 12 GiB vDNN_dyn plan; each step's loss
     against the float64 oracle network (on the GPU) that reads contraction
     operands as kind::tf32 does, within 1e-3 relative, and against plain
-    float64 within 1e-2."""
+    float64 within 1e-2. lr = 1e-3: at 1e-2 this init diverges (loss 11.9 ->
+    24.9) and the second step's loss amplifies accumulation-order noise
+    (measured 3e-3 apart), which says nothing about the kernels."""
     _need_gpu()
     import gc
     g = V.build_preset("vgg16", 256)
@@ -129,14 +131,14 @@ def test_vgg16_b256_dyn_two_step_loss_matches_oracle():
     for k, v in w.items():
         s.set_weights(k, v)
     s.set_batch(images, labels)
-    gpu = [s.step(0.01), s.step(0.01)]
+    gpu = [s.step(1e-3), s.step(1e-3)]
     del s
     gc.collect()
     torch.cuda.empty_cache()
     for emu, tol in ((True, 1e-3), (False, 1e-2)):
         ww, ref = dict(w), []
         for _ in range(2):
-            l, ww, _ = numeric.train_step(g, ww, images, labels, 0.01, device="cuda", tf32_operands=emu)
+            l, ww, _ = numeric.train_step(g, ww, images, labels, 1e-3, device="cuda", tf32_operands=emu)
             ref.append(l)
             gc.collect()
             torch.cuda.empty_cache()

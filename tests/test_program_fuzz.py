@@ -14,7 +14,7 @@ import random
 import pytest
 
 import paper_1602_08124_b200 as V
-from planner_util import graph_from_spec
+from planner_util import graph_from_spec, vocab_spec
 
 
 def fork_heavy_spec(rng: random.Random, max_layers: int = 16) -> str:
@@ -110,3 +110,28 @@ def test_program_bindings_on_presets():
             c = cap if d.gradient_scheme == V.GradientScheme.PerLayer else 1 << 40
             if V.simulate(g, d, cm, c).pass_:
                 assert V.program_check(g, d, cm, c) == [], (net, d.label)
+
+
+def test_program_bindings_on_full_vocabulary_graphs():
+    """Elementwise joins over ReLU chains (shared maps read-only, private
+    planes), strided convs, several INPUT and LOSS layers: the compiled
+    program binds every operand inside its live extent (private planes sit
+    after the arena), and the generator emits every construct."""
+    rng = random.Random(4242)
+    cm = V.CostModel()
+    seen = {"eltwise": 0, "stride": 0, "inputs": 0, "losses": 0, "private": 0}
+    for _ in range(60):
+        spec = vocab_spec(rng)
+        g = graph_from_spec(spec)
+        layers = spec.split("|")[1:]
+        seen["eltwise"] += any(p.startswith("conv") and p.endswith(" 1") and "," in p.split()[1] for p in layers)
+        seen["stride"] += any(p.startswith("conv") and p.split()[3] == "2" for p in layers)
+        seen["inputs"] += sum(p.startswith("input") for p in layers) > 1
+        seen["losses"] += sum(p.startswith("loss") for p in layers) > 1
+        fp = V.simulate_oracle(g, cm).max_mem_bytes
+        for d in decisions(g, cm):
+            for cap in (int(fp * rng.uniform(0.5, 1.5)), 1 << 40):
+                if not V.simulate(g, d, cm, cap).pass_:
+                    continue
+                assert V.program_check(g, d, cm, cap) == [], (spec, d.label, cap)
+    assert all(v > 0 for k, v in seen.items() if k != "private"), seen
