@@ -117,6 +117,7 @@ void Session::peer_exchange(float lr, float scale) {
 void Session::peer_detach() {
   if (peer_world_ == 0 && peer_maps_.empty() && !peer_chunks_) return;
   if (cs_) cudaStreamSynchronize(cs_);
+  drop_graph();
   for (void* m : peer_maps_) cudaIpcCloseMemHandle(m);
   peer_maps_.clear();
   if (peer_chunks_) cudaFree(peer_chunks_);
@@ -130,6 +131,7 @@ void Session::set_offload_buffer(void* dev_ptr, u64 bytes) {
   if (o_.offload_target == 0) throw PlanError(Err::Config, "session offloads to the pinned host arena");
   if (!dev_ptr || bytes < host_bytes_) throw PlanError(Err::Generic, "offload buffer missing or too small");
   synchronize();
+  drop_graph();
   host_ = static_cast<char*>(dev_ptr);
 }
 
@@ -146,6 +148,7 @@ cudaIpcMemHandle_t Session::spill_export() {
 void Session::spill_attach(const cudaIpcMemHandle_t& h) {
   if (o_.offload_target == 0) throw PlanError(Err::Config, "session offloads to the pinned host arena");
   synchronize();
+  drop_graph();
   if (spill_map_) cudaIpcCloseMemHandle(spill_map_);
   spill_map_ = nullptr;
   check(cudaIpcOpenMemHandle(&spill_map_, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(spill)");

@@ -1042,6 +1042,7 @@ void Session::set_grad_arena(float* ptr, size_t count) {
   if (!o_.external_grads) throw PlanError(Err::Generic, "session was created without external_grads");
   if (!ptr || count < grads_count_) throw PlanError(Err::Generic, "gradient arena too small");
   synchronize();
+  drop_graph();
   if (grads_ && grads_owned_) cudaFree(grads_);
   grads_ = ptr;
   grads_owned_ = false;

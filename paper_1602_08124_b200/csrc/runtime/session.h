@@ -249,6 +249,13 @@ class Session {
   int eager_steps_ = 0;
   u64 g_copy_off_ = 0, g_copy_pre_ = 0, g_raw_off_ = 0, g_raw_pre_ = 0, g_launches_ = 0;  // per-step deltas
   void enqueue_step(float lr);
+  // A pointer the captured step reads or writes changed: re-capture (after
+  // one eager step) instead of replaying into the old buffer.
+  void drop_graph() noexcept {
+    if (gexec_) cudaGraphExecDestroy(gexec_);
+    gexec_ = nullptr;
+    eager_steps_ = 0;
+  }
   void* spill_ = nullptr;                 // buffer this rank hosts for a peer's offloads
   void* spill_map_ = nullptr;             // IPC mapping of the peer's spill buffer (our target)
   int peer_world_ = 0;
