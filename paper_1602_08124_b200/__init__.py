@@ -10,7 +10,7 @@ from .api import (
     PolicyDecision, PolicyKind, PoolUseError, ProfilePassResult, RunReport, ShapeMismatch, SimOptions, Stream,
     StreamEvent, TensorShape, UnknownPreset, Violation, WrongLayerKind, baseline_footprint, build_preset,
     dynamic_select, extend_vgg, gradient_map_bytes, greedy_downgrade, per_layer_event_peaks, program_check, replay_check,
-    Session, kernel_launch_count, report_from_events, simulate, simulate_oracle, simulate_with_trace, static_decision,
+    Session, from_bf16_bits, kernel_launch_count, to_bf16_bits, report_from_events, simulate, simulate_oracle, simulate_with_trace, static_decision,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -788,6 +788,15 @@ class Session:
         self._plan_keepalive = self._own
         self.batch = g.batch
         self._loss = C.c_float()
+        # storage format of every pool tensor (cost_model.hpp:69): fp32, or bf16 at elem_size 2
+        self.bf16 = self.cost.elem_size == 2
+        self.elem_size = 2 if self.bf16 else 4
+
+    def _storage(self, a):
+        """Host array -> the session's storage format (fp32, or bf16 bit patterns)."""
+        import numpy as np
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        return to_bf16_bits(a) if self.bf16 else a
 
     @property
     def handle(self):
@@ -808,9 +817,10 @@ class Session:
                 "prefetch_planned": v[3].value}
 
     def set_batch(self, images, labels) -> None:
-        """Host arrays: images float32 NHWC [N,H,W,C] (C-contiguous), labels int32 [N]."""
+        """Host arrays: images float32 NHWC [N,H,W,C] (C-contiguous; rounded to
+        bf16 for an elem_size-2 session), labels int32 [N]."""
         import numpy as np
-        im = np.ascontiguousarray(images, dtype=np.float32)
+        im = self._storage(images)
         lb = np.ascontiguousarray(labels, dtype=np.int32)
         _call("vdnn_session_set_batch_host", self.handle, im.ctypes.data_as(C.c_void_p),
               lb.ctypes.data_as(C.c_void_p))
@@ -818,8 +828,7 @@ class Session:
 
     def set_input(self, layer: int, images) -> None:
         """Images (float32 NHWC host array) of one INPUT layer of a multi-input graph."""
-        import numpy as np
-        im = np.ascontiguousarray(images, dtype=np.float32)
+        im = self._storage(images)
         _call("vdnn_session_set_input", self.handle, int(layer), im.ctypes.data_as(C.c_void_p), 0)
         self._keep_inputs = getattr(self, "_keep_inputs", {})
         self._keep_inputs[layer] = im  # asynchronous copy: keep the source alive
@@ -868,7 +877,7 @@ class Session:
         _call("vdnn_session_pause_timeline", self.handle, C.c_int32(int(paused)))
 
     def weight_count(self, layer: int) -> int:
-        return self.cost.weight_bytes(self.graph, layer) // 4
+        return self.cost.weight_bytes(self.graph, layer) // self.elem_size
 
     def get_weights(self, layer: int):
         import numpy as np
@@ -978,14 +987,15 @@ class Session:
     def probe_step(self, probes, lr: float = 0.01, device: int = 0):
         """Run one step with layer-local probes armed: probes = [(layer, bwd), ...].
         Returns (loss, {(layer, bwd): {(name, index[, "after"]): torch fp32 tensor on the device}}):
-        each operand as the step's kernels read it (before) or wrote it (after)."""
+        each operand as the step's kernels read it (before) or wrote it (after). Pool tensors of a
+        bf16 session are widened exactly to fp32; DW (the fp32 gradient arena) and LOSS are fp32."""
         import torch
         bufs, lays = {}, {}
         for layer, bwd in probes:
             lay = self.probe_layout(layer, bwd)
-            buf = torch.empty(max(1, lay["total_bytes"] // 4), dtype=torch.float32, device=f"cuda:{device}")
+            buf = torch.empty(max(4, lay["total_bytes"]), dtype=torch.uint8, device=f"cuda:{device}")
             _call("vdnn_session_arm_probe", self.handle, int(layer), int(bool(bwd)), C.c_void_p(buf.data_ptr()),
-                  C.c_uint64(buf.numel() * 4))
+                  C.c_uint64(buf.numel()))
             bufs[(layer, bwd)], lays[(layer, bwd)] = buf, lay
         loss = self.step(lr)
         self.synchronize()
@@ -993,7 +1003,11 @@ class Session:
         for key, lay in lays.items():
             d = {"_layout": lay}
             for name, idx, after, off, nb in lay["segs"]:
-                t = bufs[key][off // 4: off // 4 + nb // 4]
+                raw = bufs[key][off: off + nb]
+                if self.bf16 and name not in ("DW", "LOSS"):
+                    t = raw.view(torch.bfloat16).float()
+                else:
+                    t = raw.view(torch.float32)
                 d[(name, idx, "after") if (after and name == "W") else (name, idx)] = t
             out[key] = d
         return loss, out
@@ -1003,6 +1017,23 @@ class Session:
         p = C.c_void_p()
         _call("vdnn_session_stream", self.handle, C.byref(p))
         return p.value or 0
+
+
+def to_bf16_bits(a):
+    """float32 array -> uint16 bf16 bit patterns, round to nearest even (NaN kept NaN)."""
+    import numpy as np
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    r = ((u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) >> np.uint32(16)).astype(np.uint16)
+    nan = (u & np.uint32(0x7FFFFFFF)) > np.uint32(0x7F800000)
+    if nan.any():
+        r[nan] = ((u[nan] >> np.uint32(16)) | np.uint32(0x40)).astype(np.uint16)
+    return r
+
+
+def from_bf16_bits(b):
+    """uint16 bf16 bit patterns -> float32 (exact)."""
+    import numpy as np
+    return (np.ascontiguousarray(b, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
 
 
 def kernel_launch_count() -> int:

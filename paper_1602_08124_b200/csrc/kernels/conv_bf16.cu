@@ -1,0 +1,323 @@
+// Launchers for the BF16-storage conv engine (tcb_conv.cuh): fprop / dgrad /
+// wgrad of every CONV and FC layer when the plan stores 2-byte elements
+// (cost_model.hpp:69). Split-K partials are fp32 and reduced in a fixed order
+// (deterministic, independent of where the partials live), as in conv.cu.
+#include <algorithm>
+#include <cstring>
+
+#include "kernels.h"
+#include "tcb_conv.cuh"
+
+namespace vdnnk {
+
+namespace {
+constexpr int kNumSmsB = 148;
+constexpr int kStagesB = 3;  // 3 x 32 KB (BN = 128) or 4 x 24 KB (BN = 64): two CTAs per SM
+
+bool build_common_b(const ConvArgs& a, ConvParamsB& p) {
+  std::memset(&p, 0, sizeof(p));
+  if (a.nseg < 1 || a.nseg > kMaxSegs) return false;
+  p.N = a.n;
+  p.H = a.h;
+  p.W = a.w;
+  p.Ho = a.ho();
+  p.Wo = a.wo();
+  p.Cout = a.cout;
+  p.kh = a.kh;
+  p.kw = a.kw;
+  p.stride = a.stride;
+  p.pad = a.pad;
+  p.nseg = a.nseg;
+  int cb = 0;
+  bool vec = true;
+  for (int i = 0; i < a.nseg; ++i) {
+    p.seg[i].x = reinterpret_cast<const bf16*>(a.x[i]);
+    p.seg[i].dx = reinterpret_cast<bf16*>(a.dx[i]);
+    p.seg[i].C = a.c[i];
+    p.seg[i].cbase = cb;
+    p.seg[i].mask = a.mask_in[i];
+    cb += a.c[i];
+    if (a.c[i] % 8 != 0) vec = false;
+  }
+  p.C = cb;
+  p.KK = a.kh * a.kw * cb;
+  int nch = 0;
+  if (vec && a.nseg == 1) {
+    p.chunk_arith = 1;
+    nch = (cb + 63) / 64;
+  } else if (vec) {
+    for (int i = 0; i < a.nseg && vec; ++i)
+      for (int c0 = 0; c0 < a.c[i]; c0 += 64) {
+        if (nch >= kMaxChunksB) {
+          vec = false;
+          break;
+        }
+        Chunk& c = p.chunk[nch++];
+        c.seg = i;
+        c.coff = c0;
+        c.valid = std::min(64, a.c[i] - c0);
+        c.cbase = p.seg[i].cbase + c0;
+      }
+  }
+  p.vec_in = vec ? 1 : 0;
+  p.nchunk = vec ? nch : 0;
+  p.vec_out = (a.cout % 8 == 0) ? 1 : 0;
+  return true;
+}
+
+template <int BN, int STAGES>
+cudaError_t launch_b(const ConvParamsB& p, int splits, cudaStream_t st) {
+  using L = TcbSmem<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(tcb_conv_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ncols + BN - 1) / BN);
+  const dim3 grid(static_cast<unsigned>(tiles), 1, static_cast<unsigned>(splits));
+  tcb_conv_kernel<BN, STAGES><<<grid, 160, L::kTotal, st>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+int tile_n(int ncols) { return ncols <= 64 ? 64 : 128; }
+
+cudaError_t launch_any(const ConvParamsB& p, int splits, cudaStream_t st) {
+  if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
+  if (tile_n(p.Ncols) == 64) return launch_b<64, 4>(p, splits, st);
+  return launch_b<128, kStagesB>(p, splits, st);
+}
+
+// Split-K factor (same time model as conv.cu's pick_splits): waves of
+// ceil(kblocks / s) K blocks against the partial slabs' write + re-read.
+int pick_splits_b(int tiles, int kblocks, int bn, int64_t outputs) {
+  const int slots = 2 * kNumSmsB;
+  int best = 1;
+  double best_t = 1e30;
+  const int smax = std::max(1, std::min(1024, kblocks / 4));
+  for (int s = 1; s <= smax; ++s) {
+    const double waves = static_cast<double>((static_cast<int64_t>(tiles) * s + slots - 1) / slots);
+    const double kbps = static_cast<double>((kblocks + s - 1) / s);
+    const double t_main = waves * kbps * 4.0 * bn / 1.9e9;
+    const double t_part = s > 1 ? static_cast<double>(s) * static_cast<double>(outputs) * 8.0 / 5e12 : 0.0;
+    const double t = t_main + t_part;
+    if (t < best_t * (1 - 1e-6)) {
+      best_t = t;
+      best = s;
+    }
+  }
+  return best;
+}
+
+int clamp_splits(ConvParamsB& p, int splits, size_t per, size_t ws_bytes) {
+  if (splits > 1) splits = static_cast<int>(std::min<size_t>(splits, per ? ws_bytes / per : 1));
+  if (splits < 1) splits = 1;
+  p.kb_per_split = (p.kblocks + splits - 1) / splits;
+  return (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;
+}
+
+// ----------------------------------------------------------------- FPROP ---
+bool fprop_params_b(const ConvArgs& a, const void* w, const void* bias, void* y, bool accumulate, ConvParamsB& p) {
+  if (!build_common_b(a, p)) return false;
+  p.kind = kFprop;
+  p.relu = a.relu_out;
+  p.epi = accumulate ? kEpiAccum : kEpiStore;
+  p.w = static_cast<const bf16*>(w);
+  p.bias = static_cast<const bf16*>(bias);
+  p.y = static_cast<bf16*>(y);
+  p.M = a.n * p.Ho * p.Wo;
+  p.Ncols = a.cout;
+  p.kblocks = p.vec_in ? a.kh * a.kw * p.nchunk : (p.KK + kBKb - 1) / kBKb;
+  p.kb_per_split = p.kblocks;
+  return true;
+}
+
+// FC layers at small batch: fewer output tiles than SMs over a long reduction.
+int fprop_splits_b(const ConvParamsB& p) {
+  if (p.epi != kEpiStore || p.nseg != 1 || !p.vec_in || !p.vec_out) return 1;
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ncols + tile_n(p.Ncols) - 1) / tile_n(p.Ncols));
+  if (tiles >= kNumSmsB || p.kblocks < 32) return 1;
+  return pick_splits_b(tiles, p.kblocks, tile_n(p.Ncols), static_cast<int64_t>(p.M) * p.Cout);
+}
+
+__global__ void fprop_reduce_b_kernel(const float* __restrict__ part, int splits, int64_t m, int cout,
+                                      const bf16* __restrict__ bias, int relu, bf16* __restrict__ y) {
+  const int64_t total = m * cout;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float s = part[i];
+    for (int z = 1; z < splits; ++z) s += part[z * total + i];  // fixed order: deterministic
+    if (bias) s += __bfloat162float(bias[i % cout]);
+    if (relu) s = fmaxf(s, 0.f);
+    y[i] = __float2bfloat16_rn(s);
+  }
+}
+
+// ----------------------------------------------------------------- DGRAD ---
+bool dgrad_params_b(const ConvArgs& a, const void* w, const void* dy, bool accumulate, ConvParamsB& p) {
+  if (!build_common_b(a, p)) return false;
+  p.kind = kDgrad;
+  p.epi = accumulate ? kEpiAccum : kEpiStore;
+  p.w = static_cast<const bf16*>(w);
+  p.dy = static_cast<const bf16*>(dy);
+  p.M = a.n * a.h * a.w;
+  p.Ncols = p.vec_in ? p.nchunk * 64 : p.C;
+  p.kblocks = p.vec_out ? a.kh * a.kw * ((a.cout + 63) / 64) : (a.kh * a.kw * a.cout + kBKb - 1) / kBKb;
+  p.kb_per_split = p.kblocks;
+  return true;
+}
+
+int dgrad_splits_b(const ConvParamsB& p) {
+  if (p.nseg != 1 || !p.vec_in || !p.vec_out || p.kh != 1 || p.kw != 1 || p.H != 1 || p.W != 1 || p.C % 64 != 0)
+    return 1;
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ncols + tile_n(p.Ncols) - 1) / tile_n(p.Ncols));
+  if (tiles >= kNumSmsB || p.kblocks < 32) return 1;
+  return pick_splits_b(tiles, p.kblocks, tile_n(p.Ncols), static_cast<int64_t>(p.M) * p.C);
+}
+
+__global__ void dgrad_reduce_b_kernel(const float* __restrict__ part, int splits, int64_t m, int c,
+                                      const bf16* __restrict__ mask_x, int accumulate, bf16* __restrict__ dx) {
+  const int64_t total = m * c;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float s = part[i];
+    for (int z = 1; z < splits; ++z) s += part[z * total + i];
+    if (mask_x && !(__bfloat162float(mask_x[i]) > 0.f)) s = 0.f;
+    if (accumulate) s += __bfloat162float(dx[i]);
+    dx[i] = __float2bfloat16_rn(s);
+  }
+}
+
+// ----------------------------------------------------------------- WGRAD ---
+int wgrad_rows_b(const ConvParamsB& p) { return p.vec_in ? p.kh * p.kw * p.nchunk * 64 : p.KK; }
+
+int wgrad_splits_b(const ConvParamsB& p, int M, int64_t P) {
+  const int bn = tile_n(p.Cout);
+  const int tiles = ((M + kBM - 1) / kBM) * ((p.Cout + bn - 1) / bn);
+  const int kblocks = static_cast<int>((P + kBKb - 1) / kBKb);
+  return pick_splits_b(tiles, kblocks, bn, static_cast<int64_t>(M) * p.Cout);
+}
+
+__global__ void wgrad_reduce_b_kernel(const __grid_constant__ ConvParamsB p, int splits, float* __restrict__ dw) {
+  const int64_t total = static_cast<int64_t>(p.Cout) * p.M;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(idx % p.M);
+    const int co = static_cast<int>(idx / p.M);
+    bool valid;
+    const int widx = wgrad_widx_b(p, m, valid);
+    if (!valid) continue;
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += p.out[static_cast<int64_t>(k) * total + idx];
+    const int64_t at = static_cast<int64_t>(co) * p.KK + widx;
+    if (dw)
+      dw[at] = s;
+    else
+      p.w_mut[at] = __float2bfloat16_rn(__bfloat162float(p.w_mut[at]) - p.lr * s);
+  }
+}
+
+int reduce_blocks(int64_t total) { return static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kNumSmsB)); }
+}  // namespace
+
+size_t conv_fprop_ws_bytes_bf16(const ConvArgs& a) {
+  ConvParamsB p;
+  if (!fprop_params_b(a, nullptr, nullptr, nullptr, false, p)) return 0;
+  const int s = fprop_splits_b(p);
+  return s > 1 ? static_cast<size_t>(s) * p.M * p.Cout * sizeof(float) : 0;
+}
+
+cudaError_t conv_fprop_bf16(const ConvArgs& a, const void* w, const void* bias, void* y, bool accumulate,
+                            cudaStream_t st, float* ws, size_t ws_bytes) {
+  ConvParamsB p;
+  if (!fprop_params_b(a, w, bias, y, accumulate, p)) return cudaErrorInvalidValue;
+  const size_t per = static_cast<size_t>(p.M) * p.Cout * sizeof(float);
+  const int splits = clamp_splits(p, ws ? fprop_splits_b(p) : 1, per, ws_bytes);
+  if (splits <= 1) {
+    p.kb_per_split = p.kblocks;
+    return launch_any(p, 1, st);
+  }
+  p.epi = kEpiPartial;
+  p.out = ws;
+  cudaError_t e = launch_any(p, splits, st);
+  if (e != cudaSuccess) return e;
+  const int64_t total = static_cast<int64_t>(p.M) * p.Cout;
+  fprop_reduce_b_kernel<<<reduce_blocks(total), 256, 0, st>>>(ws, splits, p.M, p.Cout, p.bias, p.relu, p.y);
+  count_launch();
+  return cudaGetLastError();
+}
+
+size_t conv_dgrad_ws_bytes_bf16(const ConvArgs& a) {
+  ConvParamsB p;
+  if (a.stride != 1 || !dgrad_params_b(a, nullptr, nullptr, false, p)) return 0;
+  const int s = dgrad_splits_b(p);
+  return s > 1 ? static_cast<size_t>(s) * p.M * p.C * sizeof(float) : 0;
+}
+
+cudaError_t conv_dgrad_bf16(const ConvArgs& a, const void* w, const void* dy, bool accumulate, cudaStream_t st,
+                            float* ws, size_t ws_bytes) {
+  ConvParamsB p;
+  if (!dgrad_params_b(a, w, dy, accumulate, p)) return cudaErrorInvalidValue;
+  if (a.stride != 1) return cudaErrorNotSupported;
+  const size_t per = static_cast<size_t>(p.M) * p.C * sizeof(float);
+  const int splits = clamp_splits(p, (ws && p.seg[0].dx) ? dgrad_splits_b(p) : 1, per, ws_bytes);
+  if (splits <= 1) {
+    p.kb_per_split = p.kblocks;
+    return launch_any(p, 1, st);
+  }
+  const bool accum = p.epi == kEpiAccum;
+  p.epi = kEpiPartial;
+  p.out = ws;
+  cudaError_t e = launch_any(p, splits, st);
+  if (e != cudaSuccess) return e;
+  const int64_t total = static_cast<int64_t>(p.M) * p.C;
+  dgrad_reduce_b_kernel<<<reduce_blocks(total), 256, 0, st>>>(ws, splits, p.M, p.C,
+                                                               p.seg[0].mask ? p.seg[0].x : nullptr, accum ? 1 : 0,
+                                                               p.seg[0].dx);
+  count_launch();
+  return cudaGetLastError();
+}
+
+size_t conv_wgrad_ws_bytes_bf16(const ConvArgs& a) {
+  ConvParamsB p;
+  if (!build_common_b(a, p)) return 0;
+  const int M = wgrad_rows_b(p);
+  const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
+  const int s = wgrad_splits_b(p, M, P);
+  return s > 1 ? static_cast<size_t>(s) * M * a.cout * sizeof(float) : 0;
+}
+
+cudaError_t conv_wgrad_bf16(const ConvArgs& a, const void* dy, void* w_mut, float lr, float* dw_out, float* ws,
+                            size_t ws_bytes, cudaStream_t st) {
+  ConvParamsB p;
+  if (!build_common_b(a, p)) return cudaErrorInvalidValue;
+  p.kind = kWgrad;
+  p.dy = static_cast<const bf16*>(dy);
+  p.w = static_cast<const bf16*>(w_mut);
+  p.w_mut = static_cast<bf16*>(w_mut);
+  p.lr = lr;
+  p.M = wgrad_rows_b(p);
+  p.Ncols = a.cout;
+  const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
+  p.kblocks = static_cast<int>((P + kBKb - 1) / kBKb);
+  const size_t per = static_cast<size_t>(p.M) * a.cout * sizeof(float);
+  const int splits = clamp_splits(p, ws ? wgrad_splits_b(p, p.M, P) : 1, per, ws_bytes);
+  if (splits <= 1) {
+    p.epi = dw_out ? kEpiGrad : kEpiSgd;
+    p.out = dw_out;
+    p.kb_per_split = p.kblocks;
+    return launch_any(p, 1, st);
+  }
+  p.epi = kEpiPartial;
+  p.out = ws;
+  cudaError_t e = launch_any(p, splits, st);
+  if (e != cudaSuccess) return e;
+  const int64_t total = static_cast<int64_t>(p.Cout) * p.M;
+  wgrad_reduce_b_kernel<<<reduce_blocks(total), 256, 0, st>>>(p, splits, dw_out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace vdnnk

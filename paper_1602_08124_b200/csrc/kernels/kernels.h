@@ -142,4 +142,37 @@ cudaError_t peer_reduce_sgd(const PeerArgs& a, cudaStream_t st);
 cudaError_t tf32_peak_probe(double* tflops);
 void count_launch(uint64_t k = 1);
 
+// ---- BF16 storage (the reference's elem_size = 2, cost_model.hpp:69) ------
+// Same operations over bf16 tensors (tcb_conv.cuh, conv_bf16.cu,
+// elementwise_bf16.cu): tcgen05 kind::f16 contractions with fp32 TMEM
+// accumulation, memory-bound ops in fp32 registers, one round-to-nearest-even
+// per stored value. ConvArgs / PoolArgs pointers address bf16 data here; the
+// split-K workspaces, the optional dW / db outputs and the SGD gradient
+// arena are fp32.
+cudaError_t conv_fprop_bf16(const ConvArgs& a, const void* w, const void* bias, void* y, bool accumulate,
+                            cudaStream_t st, float* ws = nullptr, size_t ws_bytes = 0);
+size_t conv_fprop_ws_bytes_bf16(const ConvArgs& a);
+cudaError_t conv_dgrad_bf16(const ConvArgs& a, const void* w, const void* dy, bool accumulate, cudaStream_t st,
+                            float* ws = nullptr, size_t ws_bytes = 0);
+size_t conv_dgrad_ws_bytes_bf16(const ConvArgs& a);
+cudaError_t conv_wgrad_bf16(const ConvArgs& a, const void* dy, void* w_mut, float lr, float* dw_out, float* ws,
+                            size_t ws_bytes, cudaStream_t st);
+size_t conv_wgrad_ws_bytes_bf16(const ConvArgs& a);
+cudaError_t relu_fwd_bf16(void* y, size_t n, cudaStream_t st);
+cudaError_t relu_bwd_bf16(void* g0, const void* const* extra, int nextra, const void* y, size_t n, cudaStream_t st);
+cudaError_t add_into_bf16(void* dst, const void* const* src, int nsrc, size_t n, cudaStream_t st);
+cudaError_t combine_bf16(void* dst, const void* const* src, int nsrc, const void* y, size_t n, cudaStream_t st);
+cudaError_t dilate_bf16(void* d, const void* dy, int n, int ho, int wo, int c, int stride, cudaStream_t st);
+cudaError_t maxpool_fwd_bf16(const PoolArgs& a, void* y, cudaStream_t st);
+cudaError_t maxpool_bwd_bf16(const PoolArgs& a, const void* dy, cudaStream_t st);
+cudaError_t softmax_xent_fwd_bf16(const void* logits, const int32_t* labels, int n, int k, void* grad_scratch,
+                                  float* row_loss, float* loss, cudaStream_t st, bool accumulate = false);
+cudaError_t bias_grad_bf16(const void* dy, int n, int o, void* bias, float lr, float* db_out, cudaStream_t st);
+cudaError_t sgd_update_bf16(void* w, const float* g, float lr, size_t n, cudaStream_t st);
+cudaError_t fill_normal_bf16(void* w, size_t n, float stddev, uint64_t seed, cudaStream_t st);
+cudaError_t fill_uniform_bf16(void* x, size_t n, float lo, float hi, uint64_t seed, cudaStream_t st);
+cudaError_t fill_const_bf16(void* x, size_t n, float v, cudaStream_t st);
+cudaError_t f32_to_bf16(void* dst, const float* src, size_t n, cudaStream_t st);
+cudaError_t bf16_to_f32(float* dst, const void* src, size_t n, cudaStream_t st);
+
 }  // namespace vdnnk

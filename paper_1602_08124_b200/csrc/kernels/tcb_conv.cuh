@@ -1,0 +1,673 @@
+// BF16-storage implicit-GEMM convolution engine (tcgen05 kind::f16, fp32
+// accumulation in TMEM) for the reference's elem_size = 2 mode
+// (/root/reference/proj/include/vdnnsim/cost_model.hpp:69, config.hpp:112):
+// every feature map, gradient map and weight the planner sizes at 2 bytes per
+// element is stored as bf16; products are exact in fp32 and accumulate in
+// fp32; each result is rounded once (round-to-nearest-even) when it is stored.
+//
+// Same three contractions as the fp32 engine (tc_conv.cuh):
+//   FPROP  Y[p][co]         = sum_{r,s,ci} X[p@(r,s)][ci] * W[co][r][s][ci]
+//   DGRAD  dX[p][ci]        = sum_{r,s,co} dY[p@(r',s')][co] * W[co][k-1-r'][k-1-s'][ci]   (stride 1)
+//   WGRAD  dW[(r,s,ci)][co] = sum_{p} X[p@(r,s)][ci] * dY[p][co]
+//
+// One 128 x BN output tile per CTA, split-K over grid.z. A 128-byte operand
+// row holds 64 bf16, so one stage carries twice the K depth of an fp32 stage
+// in the same bytes (4 MMAs of K = 16 per stage):
+//   warps 0-3 : producers. K-major rows (im2col of X or dY, K-major W) and
+//               MN-major rows (W^T for dgrad, X^T / dY^T for wgrad: K = 64
+//               rows of 64 MN elements per 8 KB chunk) are gathered with
+//               16-byte cp.async when every channel count is a multiple of 8,
+//               else element by element (first layers, odd channel counts),
+//               into the UMMA SWIZZLE_128B canonical layouts; after the main
+//               loop the same warps run the epilogue (tcgen05.ld 32x32b).
+//   warp 4    : TMEM allocator + single-thread tcgen05.mma issuer; stages are
+//               released with tcgen05.commit -> EMPTY barrier.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "tc_conv.cuh"
+
+namespace vdnnk {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int kBKb = 64;         // bf16 per K block = one 128-B swizzle row
+constexpr int kMaxChunksB = 96;
+
+struct BSeg {
+  const bf16* x;  // NHWC [N][H][W][C]
+  bf16* dx;       // NHWC gradient plane (dgrad output); nullptr = not materialised
+  int C, cbase, mask;
+};
+
+struct ConvParamsB {
+  int kind, epi, relu;
+  int N, H, W, C;
+  int Ho, Wo, Cout;
+  int kh, kw, stride, pad;
+  int nseg;
+  BSeg seg[kMaxSegs];
+  int nchunk, chunk_arith;         // 64-wide virtual channel chunks (arith: single segment)
+  Chunk chunk[kMaxChunksB];
+  int vec_in, vec_out;             // every segment C % 8 == 0 / Cout % 8 == 0: 16-B gathers
+  const bf16* w;                   // KRSC
+  bf16* w_mut;                     // SGD epilogue target
+  const bf16* bias;                // FC bias (fprop)
+  const bf16* dy;
+  bf16* y;
+  float* out;                      // fp32 dW (kEpiGrad) or split-K partials (kEpiPartial)
+  float lr;
+  int M, Ncols, kblocks, kb_per_split, KK;
+};
+
+__device__ __forceinline__ Chunk chunk_at_b(const ConvParamsB& p, int i) {
+  if (p.chunk_arith) {
+    Chunk c;
+    c.seg = 0;
+    c.coff = static_cast<int32_t>(i * 64);
+    const int v = p.C - i * 64;
+    c.valid = static_cast<int32_t>(v < 64 ? v : 64);
+    c.cbase = c.coff;
+    return c;
+  }
+  return p.chunk[i];
+}
+
+__device__ __forceinline__ int seg_of_b(const ConvParamsB& p, int c) {
+  int s = 0;
+#pragma unroll 1
+  for (int i = 1; i < p.nseg; ++i)
+    if (c >= p.seg[i].cbase) s = i;
+  return s;
+}
+
+// MN-major SWIZZLE_128B tile: chunk mc = 64 MN elements x 64 K rows (8 KB),
+// K row k at 128 B; the 16-B granule j is XORed with (k % 8).
+__device__ __forceinline__ uint32_t mnb_addr(uint32_t base, int k, int mc, int j) {
+  return base + mc * 8192 + k * 128 + (((j ^ (k & 7)) & 7) << 4);
+}
+
+__device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+__device__ __forceinline__ uint16_t ld_bits(const bf16* p) { return __bfloat16_as_ushort(__ldg(p)); }
+
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// kind::f16 instruction descriptor: bf16 A/B, fp32 D, M = 128.
+__host__ __device__ constexpr uint32_t make_idesc_bf16(int n, bool a_mn_major, bool b_mn_major) {
+  return (1u << 4)                       // D format f32
+         | (1u << 7)                     // A format bf16
+         | (1u << 10)                    // B format bf16
+         | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
+}
+
+// Whether a stage's gathers include element-wise st.shared writes (then the
+// producer fences them into the async proxy before arriving).
+__device__ __forceinline__ bool scalar_gathers(const ConvParamsB& p) {
+  if (p.kind == kFprop) return !p.vec_in;
+  if (p.kind == kDgrad) return !p.vec_in || !p.vec_out;
+  return !p.vec_in || !p.vec_out;
+}
+
+template <int BN>
+struct GatherB {
+  // ---- FPROP: A = im2col rows (pixel) x 64 channels, B = W rows (co) x 64 channels (both K-major)
+  __device__ static void fprop(const ConvParamsB& p, int m0, int n0, int kb, uint32_t sa, uint32_t sb, int tid) {
+    if (p.vec_in) {
+      const int tap = kb / p.nchunk, ck = kb - tap * p.nchunk;
+      const int r = tap / p.kw, s = tap - r * p.kw;
+      const Chunk c = chunk_at_b(p, ck);
+      const BSeg sg = p.seg[c.seg];
+      const int j = tid & 7;
+      const bool jv = (j * 8) < c.valid;
+#pragma unroll 4
+      for (int i = 0; i < kBM / 16; ++i) {
+        const int row = (tid >> 3) + 16 * i;
+        const int m = m0 + row;
+        const bf16* src = sg.x;
+        uint32_t bytes = 0;
+        if (m < p.M && jv) {
+          const Pix q = decode_pix(m, p.Ho, p.Wo);
+          const int ih = q.h * p.stride - p.pad + r, iw = q.w * p.stride - p.pad + s;
+          if (ih >= 0 && ih < p.H && iw >= 0 && iw < p.W) {
+            src = sg.x + ((static_cast<int64_t>(q.n) * p.H + ih) * p.W + iw) * sg.C + c.coff + j * 8;
+            bytes = 16;
+          }
+        }
+        cp_async16(kmaj_addr(sa, row, j), src, bytes);
+      }
+#pragma unroll 4
+      for (int i = 0; i < BN / 16; ++i) {
+        const int row = (tid >> 3) + 16 * i;
+        const int co = n0 + row;
+        const bf16* src = p.w;
+        uint32_t bytes = 0;
+        if (co < p.Cout && jv) {
+          src = p.w + static_cast<int64_t>(co) * p.KK + tap * p.C + c.cbase + j * 8;
+          bytes = 16;
+        }
+        cp_async16(kmaj_addr(sb, row, j), src, bytes);
+      }
+    } else {
+      // flat K = (r, s, c) over the concatenated channels; one bf16 per lane
+      const int e = tid & 63;
+      const int k = kb * kBKb + e;
+      const bool kv = k < p.KK;
+      int r = 0, s = 0, c = 0, sgi = 0;
+      if (kv) {
+        const int tap = k / p.C;
+        c = k - tap * p.C;
+        r = tap / p.kw;
+        s = tap - r * p.kw;
+        sgi = seg_of_b(p, c);
+      }
+      const BSeg sg = p.seg[sgi];
+      const int cl = c - sg.cbase;
+      const uint32_t eoff = (e & 7) * 2;
+#pragma unroll 4
+      for (int i = 0; i < kBM / 2; ++i) {
+        const int row = (tid >> 6) + 2 * i;
+        const int m = m0 + row;
+        uint16_t v = 0;
+        if (kv && m < p.M) {
+          const Pix q = decode_pix(m, p.Ho, p.Wo);
+          const int ih = q.h * p.stride - p.pad + r, iw = q.w * p.stride - p.pad + s;
+          if (ih >= 0 && ih < p.H && iw >= 0 && iw < p.W)
+            v = ld_bits(sg.x + ((static_cast<int64_t>(q.n) * p.H + ih) * p.W + iw) * sg.C + cl);
+        }
+        st_shared_u16(kmaj_addr(sa, row, e >> 3) + eoff, v);
+      }
+#pragma unroll 4
+      for (int i = 0; i < BN / 2; ++i) {
+        const int row = (tid >> 6) + 2 * i;
+        const int co = n0 + row;
+        uint16_t v = 0;
+        if (kv && co < p.Cout) v = ld_bits(p.w + static_cast<int64_t>(co) * p.KK + k);
+        st_shared_u16(kmaj_addr(sb, row, e >> 3) + eoff, v);
+      }
+    }
+  }
+
+  // ---- DGRAD (stride 1): A = im2col of dY over the input grid (pad' = k-1-pad),
+  // K-major over co; B = W^T, MN-major: K rows = co, MN = virtual input channel.
+  __device__ static void dgrad(const ConvParamsB& p, int m0, int n0, int kb, uint32_t sa, uint32_t sb, int tid) {
+    const int padh = p.kh - 1 - p.pad, padw = p.kw - 1 - p.pad;
+    const int nck = (p.Cout + 63) >> 6;
+    const int tap = p.vec_out ? kb / nck : 0;
+    const int co0 = p.vec_out ? (kb - tap * nck) * 64 : 0;
+    const int KD = p.kh * p.kw * p.Cout;
+    if (p.vec_out) {
+      const int r = tap / p.kw, s = tap - r * p.kw;
+      const int j = tid & 7;
+      const bool jv = (co0 + j * 8) < p.Cout;
+#pragma unroll 4
+      for (int i = 0; i < kBM / 16; ++i) {
+        const int row = (tid >> 3) + 16 * i;
+        const int m = m0 + row;
+        const bf16* src = p.dy;
+        uint32_t bytes = 0;
+        if (m < p.M && jv) {
+          const Pix q = decode_pix(m, p.H, p.W);
+          const int oh = q.h - padh + r, ow = q.w - padw + s;
+          if (oh >= 0 && oh < p.Ho && ow >= 0 && ow < p.Wo) {
+            src = p.dy + ((static_cast<int64_t>(q.n) * p.Ho + oh) * p.Wo + ow) * p.Cout + co0 + j * 8;
+            bytes = 16;
+          }
+        }
+        cp_async16(kmaj_addr(sa, row, j), src, bytes);
+      }
+    } else {
+      const int e = tid & 63;
+      const int k = kb * kBKb + e;
+      const bool kv = k < KD;
+      int r = 0, s = 0, co = 0;
+      if (kv) {
+        const int t = k / p.Cout;
+        co = k - t * p.Cout;
+        r = t / p.kw;
+        s = t - r * p.kw;
+      }
+      const uint32_t eoff = (e & 7) * 2;
+#pragma unroll 4
+      for (int i = 0; i < kBM / 2; ++i) {
+        const int row = (tid >> 6) + 2 * i;
+        const int m = m0 + row;
+        uint16_t v = 0;
+        if (kv && m < p.M) {
+          const Pix q = decode_pix(m, p.H, p.W);
+          const int oh = q.h - padh + r, ow = q.w - padw + s;
+          if (oh >= 0 && oh < p.Ho && ow >= 0 && ow < p.Wo)
+            v = ld_bits(p.dy + ((static_cast<int64_t>(q.n) * p.Ho + oh) * p.Wo + ow) * p.Cout + co);
+        }
+        st_shared_u16(kmaj_addr(sa, row, e >> 3) + eoff, v);
+      }
+    }
+    // B: row (k, mc) holds W[co(k)][flipped tap][virtual ci chunk mc]
+    auto kdecode = [&](int k, int& co, int& rr, int& ss) {
+      if (p.vec_out) {
+        co = co0 + k;
+        rr = tap / p.kw;
+        ss = tap - rr * p.kw;
+        return co < p.Cout;
+      }
+      const int kf = kb * kBKb + k;
+      const bool kv = kf < KD;
+      const int t = kv ? kf / p.Cout : 0;
+      co = kv ? kf - t * p.Cout : 0;
+      rr = t / p.kw;
+      ss = t - rr * p.kw;
+      return kv;
+    };
+    if (p.vec_in) {
+      const int j = tid & 7;
+#pragma unroll 2
+      for (int i = 0; i < BN / 16; ++i) {
+        const int q = (tid >> 3) + 16 * i;
+        const int k = q & 63, mc = q >> 6;
+        int co, rr, ss;
+        const bool kv = kdecode(k, co, rr, ss);
+        const int vc = (n0 >> 6) + mc;
+        const bf16* src = p.w;
+        uint32_t bytes = 0;
+        if (kv && vc < p.nchunk) {
+          const Chunk c = chunk_at_b(p, vc);
+          if (j * 8 < c.valid) {
+            const int ftap = (p.kh - 1 - rr) * p.kw + (p.kw - 1 - ss);
+            src = p.w + static_cast<int64_t>(co) * p.KK + ftap * p.C + c.cbase + j * 8;
+            bytes = 16;
+          }
+        }
+        cp_async16(mnb_addr(sb, k, mc, j), src, bytes);
+      }
+    } else {
+      const int e = tid & 63;
+      const uint32_t eoff = (e & 7) * 2;
+#pragma unroll 2
+      for (int i = 0; i < BN / 2; ++i) {
+        const int q = (tid >> 6) + 2 * i;
+        const int k = q & 63, mc = q >> 6;
+        int co, rr, ss;
+        const bool kv = kdecode(k, co, rr, ss);
+        const int ci = n0 + mc * 64 + e;
+        uint16_t v = 0;
+        if (kv && ci < p.C) {
+          const int ftap = (p.kh - 1 - rr) * p.kw + (p.kw - 1 - ss);
+          v = ld_bits(p.w + static_cast<int64_t>(co) * p.KK + ftap * p.C + ci);
+        }
+        st_shared_u16(mnb_addr(sb, k, mc, e >> 3) + eoff, v);
+      }
+    }
+  }
+
+  // ---- WGRAD: GEMM M = virtual (r,s,ci) weight columns, N = co, K = output pixels.
+  // A: X_col^T, MN-major (K row = pixel, MN = weight column); B: dY^T, MN-major.
+  __device__ static void wgrad(const ConvParamsB& p, int m0, int n0, int kb, uint32_t sa, uint32_t sb, int tid) {
+    const int P = p.N * p.Ho * p.Wo;
+    if (p.vec_in) {
+      const int j = tid & 7;
+#pragma unroll 2
+      for (int i = 0; i < kBM / 16; ++i) {
+        const int q = (tid >> 3) + 16 * i;
+        const int k = q & 63, mc = q >> 6;
+        const int pix = kb * kBKb + k;
+        const int vcol = (m0 >> 6) + mc;
+        const bf16* src = p.w;
+        uint32_t bytes = 0;
+        if (pix < P && vcol < p.kh * p.kw * p.nchunk) {
+          const int tap = vcol / p.nchunk, ck = vcol - tap * p.nchunk;
+          const Chunk c = chunk_at_b(p, ck);
+          if (j * 8 < c.valid) {
+            const int r = tap / p.kw, s = tap - r * p.kw;
+            const Pix x = decode_pix(pix, p.Ho, p.Wo);
+            const int ih = x.h * p.stride - p.pad + r, iw = x.w * p.stride - p.pad + s;
+            if (ih >= 0 && ih < p.H && iw >= 0 && iw < p.W) {
+              const BSeg sg = p.seg[c.seg];
+              src = sg.x + ((static_cast<int64_t>(x.n) * p.H + ih) * p.W + iw) * sg.C + c.coff + j * 8;
+              bytes = 16;
+            }
+          }
+        }
+        cp_async16(mnb_addr(sa, k, mc, j), src, bytes);
+      }
+    } else {
+      const int e = tid & 63;
+      const uint32_t eoff = (e & 7) * 2;
+#pragma unroll 2
+      for (int i = 0; i < kBM / 2; ++i) {
+        const int q = (tid >> 6) + 2 * i;
+        const int k = q & 63, mc = q >> 6;
+        const int pix = kb * kBKb + k;
+        const int col = m0 + mc * 64 + e;  // flat (r, s, c)
+        uint16_t v = 0;
+        if (pix < P && col < p.KK) {
+          const int tap = col / p.C, c = col - tap * p.C;
+          const int r = tap / p.kw, s = tap - r * p.kw;
+          const Pix x = decode_pix(pix, p.Ho, p.Wo);
+          const int ih = x.h * p.stride - p.pad + r, iw = x.w * p.stride - p.pad + s;
+          if (ih >= 0 && ih < p.H && iw >= 0 && iw < p.W) {
+            const BSeg sg = p.seg[seg_of_b(p, c)];
+            v = ld_bits(sg.x + ((static_cast<int64_t>(x.n) * p.H + ih) * p.W + iw) * sg.C + (c - sg.cbase));
+          }
+        }
+        st_shared_u16(mnb_addr(sa, k, mc, e >> 3) + eoff, v);
+      }
+    }
+    if (p.vec_out) {
+      const int j = tid & 7;
+#pragma unroll 2
+      for (int i = 0; i < BN / 16; ++i) {
+        const int q = (tid >> 3) + 16 * i;
+        const int k = q & 63, mc = q >> 6;
+        const int pix = kb * kBKb + k;
+        const int co = n0 + mc * 64 + j * 8;
+        const bf16* src = p.dy;
+        uint32_t bytes = 0;
+        if (pix < P && co < p.Cout) {
+          src = p.dy + static_cast<int64_t>(pix) * p.Cout + co;
+          bytes = 16;
+        }
+        cp_async16(mnb_addr(sb, k, mc, j), src, bytes);
+      }
+    } else {
+      const int e = tid & 63;
+      const uint32_t eoff = (e & 7) * 2;
+#pragma unroll 2
+      for (int i = 0; i < BN / 2; ++i) {
+        const int q = (tid >> 6) + 2 * i;
+        const int k = q & 63, mc = q >> 6;
+        const int pix = kb * kBKb + k;
+        const int co = n0 + mc * 64 + e;
+        uint16_t v = 0;
+        if (pix < P && co < p.Cout) v = ld_bits(p.dy + static_cast<int64_t>(pix) * p.Cout + co);
+        st_shared_u16(mnb_addr(sb, k, mc, e >> 3) + eoff, v);
+      }
+    }
+  }
+};
+
+// Weight-row index of a wgrad GEMM row m (virtual (tap, 64-chunk, lane) or flat).
+__device__ __forceinline__ int wgrad_widx_b(const ConvParamsB& p, int m, bool& valid) {
+  if (p.vec_in) {
+    const int vcol = m >> 6, lane = m & 63;
+    const int tap = vcol / p.nchunk, ck = vcol - tap * p.nchunk;
+    if (tap >= p.kh * p.kw) {
+      valid = false;
+      return 0;
+    }
+    const Chunk c = chunk_at_b(p, ck);
+    valid = lane < c.valid;
+    return tap * p.C + c.cbase + lane;
+  }
+  valid = m < p.KK;
+  return m;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ void unpack_bf16x8(const uint4& u, float* f) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ float bf2f(bf16 v) { return __bfloat162float(v); }
+
+// 32 consecutive outputs of one row (fp32 v[]) -> bf16 at dst (n valid,
+// accumulate adds the stored values first). 16-B stores when all 32 are valid
+// and dst is 16-B aligned.
+__device__ __forceinline__ void store_row32(bf16* dst, float (&v)[32], int n, bool accumulate) {
+  if (n >= 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    if (accumulate) {
+      uint4 a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = d4[i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float f[8];
+        unpack_bf16x8(a[i], f);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[8 * i + t] += f[t];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      d4[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                         pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < n) dst[i] = __float2bfloat16_rn((accumulate ? bf2f(dst[i]) : 0.f) + v[i]);
+}
+
+template <int BN, int STAGES>
+struct TcbSmem {
+  static constexpr int kABytes = kBM * 128;
+  static constexpr int kBBytes = BN * 128;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kTotal = STAGES * kStage + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(160, (TcbSmem<BN, STAGES>::kTotal <= 116 * 1024 ? 2 : 1))
+    tcb_conv_kernel(const __grid_constant__ ConvParamsB p) {
+  extern __shared__ uint8_t smem_raw[];
+  using L = TcbSmem<BN, STAGES>;
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bar_base = base + STAGES * L::kStage;
+  auto full_bar = [&](int s) { return bar_base + 8u * s; };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
+  const uint32_t accum_bar = bar_base + 8u * (2 * STAGES);
+  const uint32_t tmem_slot = bar_base + 8u * (2 * STAGES + 1);
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (tmem_slot - raw));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int ntn = (p.Ncols + BN - 1) / BN;
+  const int m0 = static_cast<int>(blockIdx.x / ntn) * kBM;
+  const int n0 = static_cast<int>(blockIdx.x % ntn) * BN;
+  const int kb_begin = blockIdx.z * p.kb_per_split;
+  int kb_end = kb_begin + p.kb_per_split;
+  if (kb_end > p.kblocks) kb_end = p.kblocks;
+  const int nkb = kb_end - kb_begin;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 128);  // one arrival per producer thread
+      mbar_init(empty_bar(s), 1);
+    }
+    mbar_init(accum_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot_ptr);
+
+  if (warp < 4) {
+    // ---------------- producers ----------------
+    const int tid = threadIdx.x;
+    const bool scalar = scalar_gathers(p);
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      if (it >= STAGES) mbar_wait(empty_bar(s), ph ^ 1);
+      const uint32_t sa = base + s * L::kStage;
+      const uint32_t sb = sa + L::kABytes;
+      const int kb = kb_begin + it;
+      if (p.kind == kFprop)
+        GatherB<BN>::fprop(p, m0, n0, kb, sa, sb, tid);
+      else if (p.kind == kDgrad)
+        GatherB<BN>::dgrad(p, m0, n0, kb, sa, sb, tid);
+      else
+        GatherB<BN>::wgrad(p, m0, n0, kb, sa, sb, tid);
+      if (scalar) {
+        // element-wise st.shared in this stage: land this thread's copies,
+        // make every write visible to the tensor core's (async) proxy, arrive
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        fence_proxy_async();
+        mbar_arrive(full_bar(s));
+      } else {
+        cp_async_arrive_noinc(full_bar(s));
+      }
+    }
+    // ---------------- epilogue ----------------
+    mbar_wait_sleep(accum_bar, 0);
+    tc_fence_after();
+    __syncwarp();
+    const int row = warp * 32 + lane;
+    const int m = m0 + row;
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+    for (int cg = 0; cg < BN / 32; ++cg) {
+      float v[32];
+      tmem_ld32(taddr + cg * 32, v);
+      if (nkb <= 0) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      if (m >= p.M) continue;
+      const int nb = n0 + cg * 32;
+      if (p.epi == kEpiPartial && p.kind != kWgrad) {
+        // split-K fprop / dgrad: fp32 partial slab z of [splits][M][Ncols]
+        if (nb >= p.Ncols) continue;
+        float* dst = p.out + (static_cast<int64_t>(blockIdx.z) * p.M + m) * p.Ncols + nb;
+        if (nb + 32 <= p.Ncols && (p.Ncols & 3) == 0) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (nb + i < p.Ncols) dst[i] = v[i];
+        }
+        continue;
+      }
+      if (p.kind == kFprop) {
+        if (nb >= p.Cout) continue;
+        if (p.bias) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (nb + i < p.Cout) v[i] += bf2f(p.bias[nb + i]);
+        }
+        if (p.relu) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        store_row32(p.y + static_cast<int64_t>(m) * p.Cout + nb, v, p.Cout - nb, p.epi == kEpiAccum);
+      } else if (p.kind == kDgrad) {
+        if (p.vec_in) {
+          const int vc = nb >> 6, off = nb & 63;
+          if (vc >= p.nchunk) continue;
+          const Chunk c = chunk_at_b(p, vc);
+          const BSeg sg = p.seg[c.seg];
+          const int valid = c.valid - off;
+          if (!sg.dx || valid <= 0) continue;
+          const int64_t at = static_cast<int64_t>(m) * sg.C + c.coff + off;
+          if (sg.mask) {
+            const bf16* xr = sg.x + at;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < valid && !(bf2f(xr[i]) > 0.f)) v[i] = 0.f;
+          }
+          store_row32(sg.dx + at, v, valid, p.epi == kEpiAccum);
+        } else {
+#pragma unroll 4
+          for (int i = 0; i < 32; ++i) {
+            const int ci = nb + i;
+            if (ci >= p.C) break;
+            const BSeg sg = p.seg[seg_of_b(p, ci)];
+            if (!sg.dx) continue;
+            const int64_t at = static_cast<int64_t>(m) * sg.C + (ci - sg.cbase);
+            float val = v[i];
+            if (sg.mask && !(bf2f(sg.x[at]) > 0.f)) val = 0.f;
+            sg.dx[at] = __float2bfloat16_rn((p.epi == kEpiAccum ? bf2f(sg.dx[at]) : 0.f) + val);
+          }
+        }
+      } else {
+        // WGRAD: row m = weight column (virtual), columns = co
+        if (p.epi == kEpiPartial) {
+          float* dst = p.out + static_cast<int64_t>(blockIdx.z) * p.Ncols * p.M;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (nb + i < p.Cout) dst[static_cast<int64_t>(nb + i) * p.M + m] = v[i];
+          continue;
+        }
+        bool valid;
+        const int widx = wgrad_widx_b(p, m, valid);
+        if (!valid) continue;
+        if (p.epi == kEpiSgd) {
+          bf16* wcol = p.w_mut + static_cast<int64_t>(nb) * p.KK + widx;
+          float wv[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) wv[i] = (nb + i < p.Cout) ? bf2f(wcol[static_cast<int64_t>(i) * p.KK]) : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (nb + i < p.Cout) wcol[static_cast<int64_t>(i) * p.KK] = __float2bfloat16_rn(wv[i] - p.lr * v[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (nb + i < p.Cout) p.out[static_cast<int64_t>(nb + i) * p.KK + widx] = v[i];
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------- MMA issuer ----------------
+    const bool a_mn = (p.kind == kWgrad);
+    const bool b_mn = (p.kind != kFprop);
+    const uint32_t idesc = make_idesc_bf16(BN, a_mn, b_mn);
+    const bool leader = elect_one();
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      mbar_wait(full_bar(s), ph);
+      fence_proxy_async();
+      tc_fence_after();
+      const uint32_t sa = base + s * L::kStage;
+      const uint32_t sb = sa + L::kABytes;
+      if (leader) {
+#pragma unroll
+        for (int kk = 0; kk < kBKb / 16; ++kk) {
+          // K-major: next 32 B inside the swizzled row; MN-major: next 16 K
+          // rows (two 8-row swizzle atoms, 2 KB), MN chunks 8 KB apart.
+          const uint64_t ad = a_mn ? make_sdesc(sa + kk * 2048, 8192, 1024, kSw128)
+                                   : make_sdesc(sa + kk * 32, 16, 1024, kSw128);
+          const uint64_t bd = b_mn ? make_sdesc(sb + kk * 2048, 8192, 1024, kSw128)
+                                   : make_sdesc(sb + kk * 32, 16, 1024, kSw128);
+          tc_mma_bf16(tmem, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(empty_bar(s));
+      }
+      __syncwarp();
+    }
+    if (leader) tc_commit(accum_bar);
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN) : "memory");
+  }
+}
+
+}  // namespace vdnnk

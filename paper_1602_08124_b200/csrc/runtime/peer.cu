@@ -41,6 +41,7 @@ Session::PeerHandle Session::peer_export() {
 void Session::peer_attach(int rank, int world, const PeerHandle* all) {
   if (world < 1 || world > vdnnk::kPeerMaxRanks || rank < 0 || rank >= world)
     throw PlanError(Err::Generic, "peer_attach: rank/world out of range (1..8 ranks)");
+  if (bf_) throw PlanError(Err::Config, "peer_attach: the fused peer exchange updates fp32 weights (elem_size 4)");
   if (!signal_) peer_export();  // allocates the signal words
   peer_detach();
   synchronize();

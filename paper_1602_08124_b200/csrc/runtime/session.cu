@@ -42,10 +42,39 @@ void Session::check(cudaError_t e, const char* what) const {
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// fp32 -> bf16 bit pattern, round to nearest even (NaN stays NaN)
+uint16_t to_bf16_bits(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return static_cast<uint16_t>((u >> 16) | 0x40u);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+// count elements of pool storage at dev -> fp32 host values
+void Session::read_device(float* host, const void* dev, size_t count) const {
+  if (!bf_) {
+    check(cudaMemcpy(host, dev, count * 4, cudaMemcpyDeviceToHost), "D2H");
+    return;
+  }
+  std::vector<uint16_t> b(count);
+  check(cudaMemcpy(b.data(), dev, count * 2, cudaMemcpyDeviceToHost), "D2H");
+  for (size_t i = 0; i < count; ++i) {
+    const uint32_t u = static_cast<uint32_t>(b[i]) << 16;
+    std::memcpy(host + i, &u, 4);
+  }
+}
+
 Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, const Options& o)
     : g_(g), d_(d), c_(c), cap_(capacity), o_(o) {
   // everything that can be rejected is rejected before the first allocation
-  if (c_.elem != 4) throw PlanError(Err::Config, "the CUDA executor stores fp32 (elem_size 4)");
+  if (c_.elem != 4 && c_.elem != 2)
+    throw PlanError(Err::Config, "the CUDA executor stores fp32 (elem_size 4) or bf16 (elem_size 2)");
+  bf_ = c_.elem == 2;
+  es_ = c_.elem;
+  if (bf_ && o_.precise) throw PlanError(Err::Config, "precise (3xTF32) contractions apply to fp32 storage");
+  if (bf_ && o_.compress_offload)
+    throw PlanError(Err::Config, "compressed offload applies to fp32 storage (bf16 maps travel as stored)");
   if (o_.offload_target != 0 && o_.compress_offload)
     throw PlanError(Err::Config, "compressed offload targets the pinned host arena only");
   plan_ = vdnnp::plan(g_, d_, c_, cap_, {}, &prog_);
@@ -130,13 +159,13 @@ void Session::acquire() {
 
   // non-pool scratch: softmax gradient + per-row loss + loss, two label slots
   const u64 n = g_.batch();
-  check(cudaMalloc(&loss_grad_, loss_grad_count_ * 4), "cudaMalloc(loss grad)");
+  check(cudaMalloc(&loss_grad_, loss_grad_count_ * es_), "cudaMalloc(loss grad)");
   check(cudaMalloc(&row_loss_, n * 4), "cudaMalloc(row loss)");
   check(cudaMalloc(&loss_, 4), "cudaMalloc(loss)");
   check(cudaMalloc(&labels_, 2 * n * 4), "cudaMalloc(labels)");
   labels_next_ = labels_ + n;
   check(cudaHostAlloc(&pinned_loss_, 4, cudaHostAllocDefault), "cudaHostAlloc(loss)");
-  scratch_bytes_ += loss_grad_count_ * 4 + n * 12 + 4;
+  scratch_bytes_ += loss_grad_count_ * es_ + n * 12 + 4;
   check(cudaMemsetAsync(labels_, 0, 2 * n * 4, cs_), "memset labels");
 
   build_program();
@@ -159,7 +188,7 @@ void Session::acquire() {
       const u64 wb = df_.at[static_cast<size_t>(i)].w_bytes;
       if (wb == 0) continue;
       grad_off_[static_cast<size_t>(i)] = grads_count_;
-      grads_count_ += wb / 4;
+      grads_count_ += wb / es_;  // fp32 gradients
     }
     check(cudaMalloc(&grads_, std::max<size_t>(grads_count_, 1) * 4), "cudaMalloc(grad arena)");
     scratch_bytes_ += grads_count_ * 4;
@@ -277,8 +306,11 @@ void Session::build_program() {
       s.gap_off = p.gap_off;
       s.gap_len = p.gap_len;
       const float* probe_x = summed(s.layer) ? F(s.in_off[0]) : nullptr;  // shapes only
-      if (summed(s.layer)) s.sum_bytes = round_up(g_.dims(l.in[0]).count() * 4, 1024);
-      if (contraction) s.part_bytes = vdnnk::conv_fprop_ws_bytes(conv_args(s.layer, s.in_off, nullptr, probe_x));
+      if (summed(s.layer)) s.sum_bytes = round_up(g_.dims(l.in[0]).count() * es_, 1024);
+      if (contraction) {
+        const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, probe_x);
+        s.part_bytes = bf_ ? vdnnk::conv_fprop_ws_bytes_bf16(a) : vdnnk::conv_fprop_ws_bytes(a);
+      }
       s.part_off = s.sum_bytes;
       s.scratch = s.part_bytes ? s.part_off + s.part_bytes : s.sum_bytes;
       fwd_.push_back(std::move(s));
@@ -303,10 +335,10 @@ void Session::build_program() {
       const bool sum = summed(s.layer) && l.kind != Kind::Actv;
       const float* probe_x = sum ? F(s.in_off[0]) : nullptr;
       size_t at = 0;
-      if (sum) s.sum_bytes = round_up(g_.dims(l.in[0]).count() * 4, 1024), at = s.sum_bytes;
+      if (sum) s.sum_bytes = round_up(g_.dims(l.in[0]).count() * es_, 1024), at = s.sum_bytes;
       if (s.stage_dy && l.kind != Kind::Actv) {
         s.stage_off = at;
-        s.stage_bytes = round_up(g_.dims(s.layer).count() * 4, 1024);
+        s.stage_bytes = round_up(g_.dims(s.layer).count() * es_, 1024);
         at += s.stage_bytes;
       }
       bool any_plane = false;
@@ -314,15 +346,16 @@ void Session::build_program() {
       if (l.kind == Kind::Conv && l.s > 1 && any_plane) {  // dgrad through a zero-inserted dY
         const Dims& y = g_.dims(s.layer);
         s.dil_off = at;
-        s.dil_bytes = round_up(y.n * ((y.h - 1) * l.s + 1) * ((y.w - 1) * l.s + 1) * y.c * 4, 1024);
+        s.dil_bytes = round_up(y.n * ((y.h - 1) * l.s + 1) * ((y.w - 1) * l.s + 1) * y.c * es_, 1024);
         at += s.dil_bytes;
       }
       if (contraction) {
-        s.part_bytes = vdnnk::conv_wgrad_ws_bytes(conv_args(s.layer, s.in_off, nullptr, probe_x));
+        const vdnnk::ConvArgs w = conv_args(s.layer, s.in_off, nullptr, probe_x);
+        s.part_bytes = bf_ ? vdnnk::conv_wgrad_ws_bytes_bf16(w) : vdnnk::conv_wgrad_ws_bytes(w);
         if (any_plane) {
           vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off, probe_x);
           a.stride = 1;
-          s.part_bytes = std::max(s.part_bytes, vdnnk::conv_dgrad_ws_bytes(a));
+          s.part_bytes = std::max(s.part_bytes, bf_ ? vdnnk::conv_dgrad_ws_bytes_bf16(a) : vdnnk::conv_dgrad_ws_bytes(a));
         }
       }
       s.part_off = at;
@@ -426,8 +459,37 @@ void Session::sum_inputs(int layer, const std::vector<u64>& in_off, float* dst) 
   const Node& l = g_.at(layer);
   std::vector<const float*> src;
   for (size_t i = 0; i < l.in.size(); ++i) src.push_back(F(in_off[i]));
-  check(vdnnk::combine(dst, src.data(), static_cast<int>(src.size()), nullptr, g_.dims(l.in[0]).count(), cs_),
-        "join sum");
+  k_combine(dst, src, nullptr, g_.dims(l.in[0]).count(), "join sum");
+}
+
+// ---------------------------------------------- storage-type dispatch ----
+void Session::k_combine(void* dst, const std::vector<const float*>& src, const void* y, size_t n, const char* what) {
+  if (bf_) {
+    std::vector<const void*> v(src.begin(), src.end());
+    check(vdnnk::combine_bf16(dst, v.data(), static_cast<int>(v.size()), y, n, cs_), what);
+  } else {
+    check(vdnnk::combine(static_cast<float*>(dst), src.data(), static_cast<int>(src.size()),
+                         static_cast<const float*>(y), n, cs_),
+          what);
+  }
+}
+
+void Session::k_add_into(float* dst, const std::vector<const float*>& src, size_t n, const char* what) {
+  if (bf_) {
+    std::vector<const void*> v(src.begin(), src.end());
+    check(vdnnk::add_into_bf16(dst, v.data(), static_cast<int>(v.size()), n, cs_), what);
+  } else {
+    check(vdnnk::add_into(dst, src.data(), static_cast<int>(src.size()), n, cs_), what);
+  }
+}
+
+void Session::k_relu_bwd(float* g0, const std::vector<const float*>& extra, const float* y, size_t n) {
+  if (bf_) {
+    std::vector<const void*> v(extra.begin(), extra.end());
+    check(vdnnk::relu_bwd_bf16(g0, v.data(), static_cast<int>(v.size()), y, n, cs_), "relu_bwd");
+  } else {
+    check(vdnnk::relu_bwd(g0, extra.data(), static_cast<int>(extra.size()), y, n, cs_), "relu_bwd");
+  }
 }
 
 vdnnk::PoolArgs Session::pool_args(int layer, const std::vector<u64>& in_off, const std::vector<u64>* planes,
@@ -508,15 +570,19 @@ void Session::init_weights() {
   for (const Node& l : g_.nodes()) {
     const size_t i = static_cast<size_t>(l.id);
     if (df_.at[i].w_bytes == 0) continue;
-    float* w = F(w_off_[i]);
     const u64 seed = o_.weight_seed + static_cast<u64>(l.id);
+    auto normal = [&](u64 off, u64 n, float sd) {
+      check(bf_ ? vdnnk::fill_normal_bf16(F(off), n, sd, seed, cs_) : vdnnk::fill_normal(F(off), n, sd, seed, cs_),
+            "init");
+    };
     if (l.kind == Kind::Conv) {
       const u64 fan = l.k * l.k * g_.in_dims(l.id).c;
-      check(vdnnk::fill_normal(w, df_.at[i].w_bytes / 4, std::sqrt(2.0f / static_cast<float>(fan)), seed, cs_), "init");
+      normal(w_off_[i], df_.at[i].w_bytes / es_, std::sqrt(2.0f / static_cast<float>(fan)));
     } else {
       const u64 in = g_.fc_inputs(l.id);
-      check(vdnnk::fill_normal(w, in * l.out, std::sqrt(2.0f / static_cast<float>(in)), seed, cs_), "init");
-      check(vdnnk::fill_const(w + in * l.out, l.out, 0.0f, cs_), "init");
+      normal(w_off_[i], in * l.out, std::sqrt(2.0f / static_cast<float>(in)));
+      const u64 b = w_off_[i] + in * l.out * es_;
+      check(bf_ ? vdnnk::fill_const_bf16(F(b), l.out, 0.0f, cs_) : vdnnk::fill_const(F(b), l.out, 0.0f, cs_), "init");
     }
   }
 }
@@ -559,20 +625,30 @@ void Session::run_fwd(const FwdStep& s, float lr) {
     case Kind::Fc: {
       vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, sum_x);
       a.relu_out = s.relu ? 1 : 0;
-      const float* bias = l.kind == Kind::Fc ? F(s.w_off) + g_.fc_inputs(s.layer) * l.out : nullptr;
-      check(vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_, part, s.part_bytes), "conv_fprop");
+      const float* bias = l.kind == Kind::Fc ? F(s.w_off + g_.fc_inputs(s.layer) * l.out * es_) : nullptr;
+      check(bf_ ? vdnnk::conv_fprop_bf16(a, F(s.w_off), bias, F(s.out_off), false, cs_, part, s.part_bytes)
+                : vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_, part, s.part_bytes),
+            "conv_fprop");
       break;
     }
     case Kind::Actv:
-      if (!s.skip) check(vdnnk::relu_fwd(F(s.out_off), g_.dims(s.layer).count(), cs_), "relu_fwd");
+      if (!s.skip)
+        check(bf_ ? vdnnk::relu_fwd_bf16(F(s.out_off), g_.dims(s.layer).count(), cs_)
+                  : vdnnk::relu_fwd(F(s.out_off), g_.dims(s.layer).count(), cs_),
+              "relu_fwd");
       break;
     case Kind::Pool:
-      check(vdnnk::maxpool_fwd(pool_args(s.layer, s.in_off, nullptr, sum_x), F(s.out_off), cs_), "maxpool_fwd");
+      check(bf_ ? vdnnk::maxpool_fwd_bf16(pool_args(s.layer, s.in_off, nullptr, sum_x), F(s.out_off), cs_)
+                : vdnnk::maxpool_fwd(pool_args(s.layer, s.in_off, nullptr, sum_x), F(s.out_off), cs_),
+            "maxpool_fwd");
       break;
     case Kind::Loss: {
       const size_t li = static_cast<size_t>(s.layer);
-      check(vdnnk::softmax_xent_fwd(F(s.in_off[0]), labels_, static_cast<int>(g_.batch()), loss_classes_[li],
-                                    loss_grad_ + loss_grad_at_[li], row_loss_, loss_, cs_, s.layer != loss_id_),
+      const int n = static_cast<int>(g_.batch());
+      check(bf_ ? vdnnk::softmax_xent_fwd_bf16(F(s.in_off[0]), labels_, n, loss_classes_[li], LG(loss_grad_at_[li]),
+                                               row_loss_, loss_, cs_, s.layer != loss_id_)
+                : vdnnk::softmax_xent_fwd(F(s.in_off[0]), labels_, n, loss_classes_[li],
+                                          loss_grad_ + loss_grad_at_[li], row_loss_, loss_, cs_, s.layer != loss_id_),
             "softmax_xent");
       break;
     }
@@ -621,9 +697,9 @@ void Session::run_bwd(const BwdStep& s, float lr) {
     std::vector<const float*> all{dy};
     all.insert(all.end(), extra.begin(), extra.end());
     dy = reinterpret_cast<float*>(scr + s.stage_off);
-    check(vdnnk::combine(dy, all.data(), static_cast<int>(all.size()), nullptr, ycount, cs_), "fold (staged)");
+    k_combine(dy, all, nullptr, ycount, "fold (staged)");
   } else if (l.kind != Kind::Actv && !extra.empty()) {
-    check(vdnnk::add_into(dy, extra.data(), static_cast<int>(extra.size()), ycount, cs_), "fold");
+    k_add_into(dy, extra, ycount, "fold");
   }
   const float* sum_x = nullptr;
   if (s.sum_bytes) {
@@ -645,13 +721,17 @@ void Session::run_bwd(const BwdStep& s, float lr) {
         if (s.dil_bytes) {  // strided conv: stride-1 dgrad over the zero-inserted dY
           const Dims& y = g_.dims(s.layer);
           float* d = reinterpret_cast<float*>(scr + s.dil_off);
-          check(vdnnk::dilate(d, dy, static_cast<int>(y.n), static_cast<int>(y.h), static_cast<int>(y.w),
-                              static_cast<int>(y.c), a.stride, cs_),
+          const int yn = static_cast<int>(y.n), yh = static_cast<int>(y.h), yw = static_cast<int>(y.w),
+                    yc = static_cast<int>(y.c);
+          check(bf_ ? vdnnk::dilate_bf16(d, dy, yn, yh, yw, yc, a.stride, cs_)
+                    : vdnnk::dilate(d, dy, yn, yh, yw, yc, a.stride, cs_),
                 "dilate dY");
           a.stride = 1;
           dyd = d;
         }
-        check(vdnnk::conv_dgrad(a, F(s.w_off), dyd, s.accumulate, cs_, part, s.part_bytes), "conv_dgrad");
+        check(bf_ ? vdnnk::conv_dgrad_bf16(a, F(s.w_off), dyd, s.accumulate, cs_, part, s.part_bytes)
+                  : vdnnk::conv_dgrad(a, F(s.w_off), dyd, s.accumulate, cs_, part, s.part_bytes),
+              "conv_dgrad");
       }
       const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, sum_x);
       // split-K partials: the split count depends only on the layer shape
@@ -659,12 +739,15 @@ void Session::run_bwd(const BwdStep& s, float lr) {
       // order -- and every bit of the update -- is independent of the offload
       // policy and of where the partials live
       float* dw = grads_ ? grads_ + grad_off_[mi] : nullptr;
-      check(vdnnk::conv_wgrad(a, dy, F(s.w_off), lr, dw, part, s.part_bytes, cs_), "conv_wgrad");
+      check(bf_ ? vdnnk::conv_wgrad_bf16(a, dy, F(s.w_off), lr, dw, part, s.part_bytes, cs_)
+                : vdnnk::conv_wgrad(a, dy, F(s.w_off), lr, dw, part, s.part_bytes, cs_),
+            "conv_wgrad");
       if (fc) {
         const u64 in = g_.fc_inputs(s.layer);
-        float* bias = F(s.w_off) + in * l.out;
+        float* bias = F(s.w_off + in * l.out * es_);
         float* db = grads_ ? grads_ + grad_off_[mi] + in * l.out : nullptr;
-        check(vdnnk::bias_grad(dy, static_cast<int>(g_.batch()), static_cast<int>(l.out), bias, lr, db, cs_),
+        const int n = static_cast<int>(g_.batch()), o = static_cast<int>(l.out);
+        check(bf_ ? vdnnk::bias_grad_bf16(dy, n, o, bias, lr, db, cs_) : vdnnk::bias_grad(dy, n, o, bias, lr, db, cs_),
               "bias_grad");
       }
       break;
@@ -676,25 +759,24 @@ void Session::run_bwd(const BwdStep& s, float lr) {
         p.mask_in[i] = (sum_x || s.mask_plane.empty()) ? 0 : s.mask_plane[static_cast<size_t>(i)];
         any_plane = any_plane || p.dx[i] != nullptr;
       }
-      if (any_plane) check(vdnnk::maxpool_bwd(p, F(s.out_off), dy, cs_), "maxpool_bwd");
+      if (any_plane)
+        check(bf_ ? vdnnk::maxpool_bwd_bf16(p, dy, cs_) : vdnnk::maxpool_bwd(p, F(s.out_off), dy, cs_), "maxpool_bwd");
       break;
     }
     case Kind::Actv:
       if (dy && s.priv_out != kNoOff) {  // shared incoming planes: masked sum into the private plane
         std::vector<const float*> all{dy};
         all.insert(all.end(), extra.begin(), extra.end());
-        check(vdnnk::combine(F(s.priv_out), all.data(), static_cast<int>(all.size()), F(s.out_off), ycount, cs_),
-              "relu_bwd (private plane)");
+        k_combine(F(s.priv_out), all, F(s.out_off), ycount, "relu_bwd (private plane)");
       } else if (dy && !s.skip) {
-        check(vdnnk::relu_bwd(dy, extra.data(), static_cast<int>(extra.size()), F(s.out_off), ycount, cs_),
-              "relu_bwd");
+        k_relu_bwd(dy, extra, F(s.out_off), ycount);
       }
       break;
     case Kind::Loss: {
       const size_t li = static_cast<size_t>(s.layer);
       if (!s.plane_off.empty() && s.plane_off[0] != kNoOff)
-        check(cudaMemcpyAsync(F(s.plane_off[0]), loss_grad_ + loss_grad_at_[li],
-                              g_.batch() * static_cast<u64>(loss_classes_[li]) * 4, cudaMemcpyDeviceToDevice, cs_),
+        check(cudaMemcpyAsync(F(s.plane_off[0]), LG(loss_grad_at_[li]),
+                              g_.batch() * static_cast<u64>(loss_classes_[li]) * es_, cudaMemcpyDeviceToDevice, cs_),
               "loss grad copy");
       break;
     }
@@ -877,8 +959,11 @@ float Session::read_loss() {
 
 void Session::synthetic_batch(u64 seed) {
   for (size_t i = 0; i < inputs_.size(); ++i) {
-    const u64 count = df_.at[static_cast<size_t>(inputs_[i])].bytes / 4;
-    check(vdnnk::fill_uniform(F(input_off_[i]), count, -1.0f, 1.0f, seed + 7919 * i, cs_), "images");
+    const u64 count = df_.at[static_cast<size_t>(inputs_[i])].bytes / es_;
+    const u64 sd = seed + 7919 * i;
+    check(bf_ ? vdnnk::fill_uniform_bf16(F(input_off_[i]), count, -1.0f, 1.0f, sd, cs_)
+              : vdnnk::fill_uniform(F(input_off_[i]), count, -1.0f, 1.0f, sd, cs_),
+          "images");
   }
   check(vdnnk::fill_labels(labels_, g_.batch(), classes_, seed + 1, cs_), "labels");
 }
@@ -898,17 +983,23 @@ void Session::set_input(int layer, const float* images, bool device) {
 void Session::get_weights(int layer, float* host, size_t count) {
   if (layer < 0 || layer >= L_ || w_off_[static_cast<size_t>(layer)] == kNoOff)
     throw PlanError(Err::Generic, "layer has no weights");
-  if (count * 4 != df_.at[static_cast<size_t>(layer)].w_bytes) throw PlanError(Err::Generic, "weight count mismatch");
+  if (count * es_ != df_.at[static_cast<size_t>(layer)].w_bytes) throw PlanError(Err::Generic, "weight count mismatch");
   synchronize();
-  check(cudaMemcpy(host, F(w_off_[static_cast<size_t>(layer)]), count * 4, cudaMemcpyDeviceToHost), "D2H");
+  read_device(host, F(w_off_[static_cast<size_t>(layer)]), count);
 }
 
 void Session::set_weights(int layer, const float* host, size_t count) {
   if (layer < 0 || layer >= L_ || w_off_[static_cast<size_t>(layer)] == kNoOff)
     throw PlanError(Err::Generic, "layer has no weights");
-  if (count * 4 != df_.at[static_cast<size_t>(layer)].w_bytes) throw PlanError(Err::Generic, "weight count mismatch");
+  if (count * es_ != df_.at[static_cast<size_t>(layer)].w_bytes) throw PlanError(Err::Generic, "weight count mismatch");
   synchronize();
-  check(cudaMemcpy(F(w_off_[static_cast<size_t>(layer)]), host, count * 4, cudaMemcpyHostToDevice), "H2D");
+  if (!bf_) {
+    check(cudaMemcpy(F(w_off_[static_cast<size_t>(layer)]), host, count * 4, cudaMemcpyHostToDevice), "H2D");
+    return;
+  }
+  std::vector<uint16_t> b(count);
+  for (size_t i = 0; i < count; ++i) b[i] = to_bf16_bits(host[i]);
+  check(cudaMemcpy(F(w_off_[static_cast<size_t>(layer)]), b.data(), count * 2, cudaMemcpyHostToDevice), "H2D");
 }
 
 void Session::read_feature(int owner, float* host, size_t count) {
@@ -919,8 +1010,8 @@ void Session::read_feature(int owner, float* host, size_t count) {
   for (const Event& e : plan_.events)
     if (e.kind == Ev::Alloc && e.buffer == owner && (e.tag == "X" || e.tag == "Y")) off = e.off;
   if (off == kNoOff) throw PlanError(Err::Generic, "owner has no feature buffer");
-  if (count * 4 > df_.at[static_cast<size_t>(owner)].bytes) throw PlanError(Err::Generic, "count too large");
-  check(cudaMemcpy(host, F(off), count * 4, cudaMemcpyDeviceToHost), "D2H");
+  if (count * es_ > df_.at[static_cast<size_t>(owner)].bytes) throw PlanError(Err::Generic, "count too large");
+  read_device(host, F(off), count);
 }
 
 Session::ProbeLayout Session::probe_layout(int layer, bool bwd) const {
@@ -935,8 +1026,8 @@ Session::ProbeLayout Session::probe_layout(int layer, bool bwd) const {
     p.segs.push_back(s);
     p.total += round_up(bytes, 256);
   };
-  auto in_bytes = [&](size_t i) { return g_.dims(l.in[i]).count() * 4; };
-  const u64 y_bytes = g_.dims(layer).count() * 4;
+  auto in_bytes = [&](size_t i) { return g_.dims(l.in[i]).count() * es_; };
+  const u64 y_bytes = g_.dims(layer).count() * es_;
   const bool contraction = l.kind == Kind::Conv || l.kind == Kind::Fc;
   if (!bwd) {
     const FwdStep* s = nullptr;
@@ -950,7 +1041,7 @@ Session::ProbeLayout Session::probe_layout(int layer, bool bwd) const {
     if (contraction) add(kPW, 0, df_.at[li].w_bytes, 0, s->w_off, false);
     if (l.kind == Kind::Actv) add(kPX, 0, y_bytes, 0, s->out_off, false);
     if (l.kind == Kind::Loss) {
-      add(kPLossGrad, 0, g_.batch() * static_cast<u64>(loss_classes_[li]) * 4, 2, loss_grad_at_[li], true);
+      add(kPLossGrad, 0, g_.batch() * static_cast<u64>(loss_classes_[li]) * es_, 2, loss_grad_at_[li], true);
       add(kPLoss, 0, 4, 3, 0, true);
     } else {
       add(kPY, 0, y_bytes, 0, s->out_off, true);
@@ -981,11 +1072,11 @@ Session::ProbeLayout Session::probe_layout(int layer, bool bwd) const {
   }
   for (size_t i = 0; i < s->plane_off.size(); ++i) {
     if (s->plane_off[i] == kNoOff) continue;
-    const u64 b = l.kind == Kind::Loss ? g_.dims(l.in[0]).count() * 4 : in_bytes(i);
+    const u64 b = l.kind == Kind::Loss ? g_.dims(l.in[0]).count() * es_ : in_bytes(i);
     if (s->accumulate) add(kPDXBefore, static_cast<int>(i), b, 0, s->plane_off[i], false);
     add(kPDX, static_cast<int>(i), b, 0, s->plane_off[i], true);
   }
-  if (contraction && grads_) add(kPDW, 0, df_.at[li].w_bytes, 1, grad_off_[li], true);
+  if (contraction && grads_) add(kPDW, 0, df_.at[li].w_bytes / es_ * 4, 1, grad_off_[li], true);  // fp32
   if (contraction && !grads_) add(kPW, 1, df_.at[li].w_bytes, 0, s->w_off, true);  // updated weights
   return p;
 }
@@ -1015,7 +1106,7 @@ void Session::probe_copy(int ev, bool after) {
       switch (s.src) {
         case 0: src = base_ + s.src_off; break;
         case 1: src = reinterpret_cast<const char*>(grads_ + s.src_off); break;
-        case 2: src = reinterpret_cast<const char*>(loss_grad_ + s.src_off); break;
+        case 2: src = static_cast<const char*>(LG(s.src_off)); break;
         default: src = reinterpret_cast<const char*>(loss_); break;
       }
       check(cudaMemcpyAsync(a.dst + s.dst, src, s.bytes, cudaMemcpyDefault, cs_), "probe copy");
@@ -1030,7 +1121,7 @@ void Session::grad_buffer(int layer, void** ptr, size_t* count) {
     return;
   }
   *ptr = grads_ + grad_off_[static_cast<size_t>(layer)];
-  *count = df_.at[static_cast<size_t>(layer)].w_bytes / 4;
+  *count = df_.at[static_cast<size_t>(layer)].w_bytes / es_;
 }
 
 void Session::grad_arena(void** ptr, size_t* count) {
@@ -1053,7 +1144,10 @@ void Session::apply_grads(float lr, float scale) {
   for (int i = 0; i < L_; ++i) {
     const size_t k = static_cast<size_t>(i);
     if (grad_off_[k] == kNoOff) continue;
-    check(vdnnk::sgd_update(F(w_off_[k]), grads_ + grad_off_[k], lr * scale, df_.at[k].w_bytes / 4, cs_), "sgd");
+    const size_t n = df_.at[k].w_bytes / es_;
+    check(bf_ ? vdnnk::sgd_update_bf16(F(w_off_[k]), grads_ + grad_off_[k], lr * scale, n, cs_)
+              : vdnnk::sgd_update(F(w_off_[k]), grads_ + grad_off_[k], lr * scale, n, cs_),
+          "sgd");
   }
 }
 

@@ -16,6 +16,7 @@ using vdnnp::i64;
 using vdnnp::u64;
 
 constexpr u64 kNoOff = ~u64{0};  // "no buffer" offset
+uint16_t to_bf16_bits(float f);  // round to nearest even
 
 struct Options {
   int device = 0;
@@ -165,6 +166,15 @@ class Session {
 
  private:
   float* F(u64 off) const { return reinterpret_cast<float*>(base_ + off); }
+  // Storage format of every pool tensor: fp32 (elem_size 4) or bf16
+  // (elem_size 2, cost_model.hpp:69); the kernel calls below dispatch on it.
+  bool bf_ = false;
+  u64 es_ = 4;
+  void* LG(u64 elem) const { return reinterpret_cast<char*>(loss_grad_) + elem * es_; }  // softmax gradient
+  void k_combine(void* dst, const std::vector<const float*>& src, const void* y, size_t n, const char* what);
+  void k_add_into(float* dst, const std::vector<const float*>& src, size_t n, const char* what);
+  void k_relu_bwd(float* g0, const std::vector<const float*>& extra, const float* y, size_t n);
+  void read_device(float* host, const void* dev, size_t count) const;  // storage -> fp32 host
   void acquire();
   void release() noexcept;
   void build_program();

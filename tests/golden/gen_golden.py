@@ -59,6 +59,16 @@ def main():
                       "result": refsim.run(spec, dec, cap, cost_spec=cost)})
     with open(os.path.join(out_dir, "small_graphs.json"), "w") as f:
         json.dump(small, f, separators=(",", ":"))
+    # BF16 storage: elem_size = 2 (cost_model.hpp:69, config.hpp:112), every BASELINE config
+    es2 = []
+    for name, batch, extra in NETS + [("vgg16", 32, 400)]:
+        spec = refsim.preset_spec(name, batch, extra)
+        decs = ["dyn", "static:all:m", "static:conv:m", "static:conv:p", "static:baseline:p"]
+        for dec in decs:
+            r = refsim.run(spec, dec, GIB12, cost_spec="es=2", events=extra == 0)
+            es2.append({"spec": spec, "cost": "es=2", "decision_spec": dec, "capacity": GIB12, "result": r})
+    with open(os.path.join(out_dir, "es2.json"), "w") as f:
+        json.dump(es2, f, separators=(",", ":"))
     print("wrote fixtures to", out_dir)
 
 

@@ -74,7 +74,10 @@ def check_session(s: V.Session, g, labels: np.ndarray, layers: List[int] = None,
     the capture budget needs; returns one record per compared tensor:
     {layer, kind, op, tensor, K, err_emu, err_plain}. err_emu compares with the
     oracle that reads contraction operands the way kind::tf32 does (TF32
-    mode; equal to err_plain in fp32 mode), err_plain with plain float64."""
+    mode; equal to err_plain in fp32 mode), err_plain with plain float64.
+    bf16 sessions (elem_size 2): the probed operands are exact bf16 values
+    and kind::f16 reads them unrounded, so plain float64 is the emulating
+    oracle too."""
     L = numeric.layers_of(g)
     todo = [l.id for l in L if l.kind in (numeric.CONV, numeric.FC, numeric.POOL, numeric.LOSS, numeric.ACTV)]
     if layers is not None:
@@ -97,7 +100,7 @@ def check_session(s: V.Session, g, labels: np.ndarray, layers: List[int] = None,
             lay = d["_layout"]
             fused = [f for f, on in (("relu", lay["relu_fused"]), ("accumulate", lay["accumulate"]),
                                      ("mask", lay["mask_planes"] != 0)) if on]
-            for r in _compare(g, L, i, bwd, d, labels, precise):
+            for r in _compare(g, L, i, bwd, d, labels, precise or s.bf16, s.bf16):
                 r["fused"] = fused
                 recs.append(r)
         del cap
@@ -112,7 +115,21 @@ def _rec(l, op, tensor, K, e_emu, e_plain):
             "err_plain": float(e_plain)}
 
 
-def _compare(g, L, i, bwd, d, labels, precise) -> List[Dict]:
+def _bf16(t: torch.Tensor) -> torch.Tensor:
+    return t.to(torch.float32).to(torch.bfloat16).to(torch.float64)
+
+
+def _summed_inputs(l, xs, bf16):
+    """bf16 sessions store an elementwise join's summed input (rounded once)
+    before the kernels read it: hand the oracle that stored sum (the join of
+    [sum, 0, ...] is the sum itself)."""
+    if not (bf16 and l.join == 1 and len(xs) > 1):
+        return xs
+    tot = _bf16(sum(x.to(torch.float64) for x in xs))
+    return [tot] + [torch.zeros_like(tot) for _ in xs[1:]]
+
+
+def _compare(g, L, i, bwd, d, labels, precise, bf16=False) -> List[Dict]:
     l = L[i]
     lay = d["_layout"]
     out: List[Dict] = []
@@ -127,7 +144,7 @@ def _compare(g, L, i, bwd, d, labels, precise) -> List[Dict]:
             ref = torch.relu(x.to(torch.float64))
             e = numeric.max_rel(y, ref)
             return [_rec(l, "fwd", "Y", 1, e, e)]
-        xs = [d[("X", j)].reshape(numeric._nhwc(sh)) for j, sh in enumerate(shapes)]
+        xs = _summed_inputs(l, [d[("X", j)].reshape(numeric._nhwc(sh)) for j, sh in enumerate(shapes)], bf16)
         w = d.get(("W", 0))
         if l.kind == numeric.LOSS:
             r = numeric.layer_forward(g, i, xs, labels=labels)
@@ -157,9 +174,11 @@ def _compare(g, L, i, bwd, d, labels, precise) -> List[Dict]:
         return [_rec(l, "relu_bwd", "DX", len(dys), e, e)]
     if l.kind == numeric.LOSS:
         return out  # copies the FWD's gradient (checked there)
-    xs = [d[("X", j)].reshape(numeric._nhwc(sh)) for j, sh in enumerate(shapes)]
+    xs = _summed_inputs(l, [d[("X", j)].reshape(numeric._nhwc(sh)) for j, sh in enumerate(shapes)], bf16)
     ndy = sum(1 for sg in lay["segs"] if sg[0] == "DY")  # > 1: shared planes the kernels read the sum of
     dy = sum(d[("DY", k)].to(torch.float64) for k in range(ndy)).reshape(numeric._nhwc(l.shape))
+    if bf16 and ndy > 1:  # the staged sum is stored (rounded once) before the kernels read it
+        dy = _bf16(dy)
     w = d.get(("W", 0))
     planes = sorted(k[1] for k in d if isinstance(k, tuple) and k[0] == "DX")
     if l.join == 1 and len(l.inputs) > 1:  # one shared map: every probed DX segment is the same extent
@@ -216,6 +235,15 @@ def _compare(g, L, i, bwd, d, labels, precise) -> List[Dict]:
 # fprop/dgrad <= 1.5e-5, wgrad <= 2.3e-4 (K = N*Ho*Wo up to 12.8 M, split-K
 # partials) against the emulating oracle; <= 1.3e-3 against float64.
 TF32_EMU_TOL = {"fprop": 1e-4, "dgrad": 1e-4, "wgrad": 5e-4}
+# BF16 storage (elem_size 2): exact products, fp32 accumulation, one
+# round-to-nearest-even per stored bf16 value (unit roundoff 2^-8 of the
+# element, so at most 2^-8 of max |ref|) -- Y, dX (including overlapping-window
+# pool sums), the softmax gradient and summed ReLU-backward planes:
+# BF16_STORE_TOL; the fp32 gradient arena (dW, db) is not rounded: BF16_DW_TOL
+# (fp32 accumulation over K up to 12.8 M); max-pool forward, a single-plane
+# ReLU and the fp32 loss value are exact.
+BF16_STORE_TOL = 2.0 ** -8 + 1e-4
+BF16_DW_TOL = 5e-4
 TF32_PLAIN_TOL = 4e-3
 EXACT_TOL = 1e-6
 
@@ -224,8 +252,22 @@ def fp32_tol(K: int) -> float:
     return 4e-6 + 1.2e-8 * K
 
 
-def violations(recs: List[Dict], precise: bool) -> List[str]:
+def violations(recs: List[Dict], precise: bool, bf16: bool = False) -> List[str]:
     bad = []
+    if bf16:
+        for r in recs:
+            if r["tensor"] in ("DW", "DB"):
+                tol = BF16_DW_TOL
+            elif (r["op"] in ("fprop", "dgrad", "pool_bwd") or r["tensor"] == "LOSS_GRAD"
+                  or (r["op"] == "relu_bwd" and r["K"] > 1)):
+                tol = BF16_STORE_TOL
+            elif r["tensor"] == "LOSS":
+                tol = 1e-5
+            else:
+                tol = EXACT_TOL
+            if r["err_plain"] > tol:
+                bad.append(f"L{r['layer']} {r['op']} {r['tensor']} K={r['K']}: {r['err_plain']:.3e} > {tol:.2e}")
+        return bad
     for r in recs:
         contraction = r["op"] in ("fprop", "dgrad", "wgrad")
         if not contraction:

@@ -48,10 +48,11 @@ def _decision(g, cm, policy):
     return V.static_decision(kind, V.AlgoMode.MemoryOptimal, g, cm)
 
 
-def _run(name, net, batch, policy, precise, layers=None, extra=0, expect_label=None):
+def _run(name, net, batch, policy, precise, layers=None, extra=0, expect_label=None, es=4):
     _need_gpu()
     g = V.build_preset(net, batch) if not extra else V.extend_vgg(extra, batch)
     cm = V.CostModel()
+    cm.elem_size = es
     d = _decision(g, cm, policy)
     if expect_label:
         assert d.label == expect_label
@@ -60,13 +61,14 @@ def _run(name, net, batch, policy, precise, layers=None, extra=0, expect_label=N
     s.set_batch(images, labels)
     s.step(0.01)  # warm step: identical inputs and weights every step (external_grads: no update)
     recs = LP.check_session(s, g, labels, layers=layers, precise=precise)
-    tag = f"{name} {'fp32' if precise else 'tf32'} {d.label}"
+    mode = "bf16" if es == 2 else ("fp32" if precise else "tf32")
+    tag = f"{name} {mode} {d.label}"
     print(tag, json.dumps(LP.summarize(recs)))
     if OUT:
-        with open(os.path.join(OUT, f"parity_{name}_{'fp32' if precise else 'tf32'}.json"), "w") as f:
+        with open(os.path.join(OUT, f"parity_{name}_{mode}.json"), "w") as f:
             json.dump({"config": tag, "plan_signature": s.plan.signature(), "records": recs}, f, indent=0)
     assert s.plan.offload_traffic_bytes > 0 or policy in ("dyn", "none")
-    bad = LP.violations(recs, precise)
+    bad = LP.violations(recs, precise, bf16=es == 2)
     assert not bad, f"{tag}: {len(bad)} violations: " + "; ".join(bad[:8])
     ops = {r["op"] for r in recs}
     return recs, ops

@@ -84,7 +84,7 @@ def run_and_compare(g, d, cm, ims, labels, precise, tag, cap=1 << 30):
     assert V.replay_check(s.measured_report(), g, d, cap) == []
     if not precise:  # layer-local (same inputs and weights every step: external_grads)
         recs = LP.check_session(s, g, labels, precise=False)
-        bad = LP.violations(recs, False)
+        bad = LP.violations(recs, False, bf16=s.bf16)
         assert not bad, f"{tag}: " + "; ".join(bad[:6])
         return loss
     grads = {k: s.get_grads(k) for k in w}
@@ -164,6 +164,15 @@ def test_graph_json_network_runs_and_matches():
     """report.hpp:44-111 graph JSON: a GoogLeNet-like module (concat of 1x1,
     3x3, 5x5 and pool branches), a residual elementwise join and two heads."""
     _need_gpu()
+    g = json_graph()
+    cm = V.CostModel()
+    ims, labels = _inputs_and_labels(g, 6)
+    for d in _decisions(g, cm):
+        for precise in (True, False):
+            run_and_compare(g, d, cm, ims, labels, precise, f"json {d.label} precise={precise}")
+
+
+def json_graph():
     from paper_1602_08124_b200 import formats
     L = []
 
@@ -194,9 +203,4 @@ def test_graph_json_network_runs_and_matches():
     lay("loss", [aux])
     f = lay("fc", [res], out_features=10)
     lay("loss", [f])
-    g = formats.graph_from_json({"batch": 4, "layers": L})
-    cm = V.CostModel()
-    ims, labels = _inputs_and_labels(g, 6)
-    for d in _decisions(g, cm):
-        for precise in (True, False):
-            run_and_compare(g, d, cm, ims, labels, precise, f"json {d.label} precise={precise}")
+    return formats.graph_from_json({"batch": 4, "layers": L})
