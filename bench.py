@@ -191,13 +191,20 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     g = V.build_preset(args.net, args.batch) if args.extra == 0 else V.extend_vgg(args.extra, args.batch)
     cm = V.CostModel()
     cap = args.capacity
+    # "<policy>b": BF16 storage -- the reference's elem_size = 2
+    # (cost_model.hpp:69): the planner sizes every tensor at 2 bytes (its own
+    # decisions and schedule), the executor stores bf16 and runs kind::f16
+    name = policy
+    bf16 = policy.endswith("b")
+    if bf16:
+        policy = policy[:-1]
+        cm.elem_size = 2
     # "<policy>z": the same plan with zero-value-compressed offload/prefetch;
     # "<policy>p": the same plan offloading into the ring neighbour's spare
     # HBM over NVLink (data parallel only: a peer GPU is the offload target)
     # "<policy>t": compressed, and maps read in backward only by TF32
     # contractions / ReLU masks travel TF32-exact (bit-identical step)
     # "<policy>f": fp32-accurate contractions (3xTF32) instead of TF32
-    name = policy
     precise = args.precise or policy.endswith("f")
     if policy.endswith("f"):
         policy = policy[:-1]
@@ -289,7 +296,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
                  + (" ->peer HBM" if peer_target else ""),
         "verdict": "PASS", "capacity_bytes": cap,
         "images_per_s": round(imgs, 2), "ms_per_step": round(ms, 3), "ms_per_step_median": round(ms_median, 3),
-        "loss": loss, "precise_fp32": bool(precise),
+        "loss": loss, "precise_fp32": bool(precise), "storage": "bf16" if bf16 else "fp32",
         "peak_pool_bytes": plan.max_mem_bytes, "arena_bytes": s.arena_info()["arena_bytes"],
         "device_used_bytes": total - free,
         "offload_bytes_per_iter": plan.offload_traffic_bytes, "prefetch_bytes_per_iter": plan.prefetch_traffic_bytes,
@@ -322,7 +329,10 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         # step, loss read back every step
         sh = g.shape(0)
         rng = np.random.default_rng(99 + device)
-        imgs_h = torch.from_numpy(rng.uniform(-1, 1, size=(sh.n, sh.h, sh.w, sh.c)).astype(np.float32)).pin_memory()
+        host_imgs = rng.uniform(-1, 1, size=(sh.n, sh.h, sh.w, sh.c)).astype(np.float32)
+        if bf16:  # the loader hands the session its storage format
+            host_imgs = V.to_bf16_bits(host_imgs).view(np.int16)
+        imgs_h = torch.from_numpy(host_imgs).pin_memory()
         ls = g.shape(g.layer(g.size() - 1).inputs[0])
         labs_h = torch.from_numpy(rng.integers(0, ls.c, size=sh.n).astype(np.int32)).pin_memory()
         # input pipeline: each step's batch is staged (pinned host -> device)
@@ -359,7 +369,8 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         ems = max(e0.elapsed_time(e1) / args.steps, wall * 1e3)
         ems = max_over_ranks(ems, world, device=f"cuda:{device}")
         res["e2e"] = {"value": round(args.batch * world / (ems * 1e-3), 2), "unit": "images/s",
-                      "h2d_bytes_per_step": imgs_h.numel() * 4 + labs_h.numel() * 4, "d2h_bytes_per_step": 4,
+                      "h2d_bytes_per_step": imgs_h.numel() * imgs_h.element_size() + labs_h.numel() * 4,
+                      "d2h_bytes_per_step": 4,
                       "ms_per_step": round(ems, 3)}
     res["_flops"] = flops
     res["_conv_ms"] = conv_ms
@@ -446,8 +457,8 @@ def main():
                     help="dyn/all/conv/none; a trailing z = same plan with compressed offload, t = compressed with "
                          "TF32-exact values where only TF32 contractions read the map, a trailing p = "
                          "offload into a peer GPU's HBM (N > 1), a trailing f = fp32-accurate 3xTF32 "
-                         "contractions. Default: dyn,dynz,dynt,all,conv,none,dynf,nonef (N > 1: dyn,dynp,dynz,dynt,"
-                         "all,conv,none)")
+                         "contractions, a trailing b = BF16 storage (elem_size 2: its own plan). Default: "
+                         "dyn,dynz,dynt,all,conv,none,dynf,nonef,dynb,noneb (N > 1: dyn,dynp,dynz,dynt,all,conv,none)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--precise", action="store_true", help="3xTF32 fp32-accurate contractions")
     ap.add_argument("--cpu-sample-batch", type=int, default=96,
@@ -484,11 +495,12 @@ def main():
     tf32_peak, peak_note = measured_tf32_peak(peaks, peaks_src)
 
     if args.policies is None:
-        args.policies = ("dyn,dynz,dynt,all,conv,none,dynf,nonef" if world == 1
+        args.policies = ("dyn,dynz,dynt,all,conv,none,dynf,nonef,dynb,noneb" if world == 1
                          else "dyn,dynp,dynz,dynt,all,conv,none")
     results = {}
     for p in [x for x in args.policies.split(",") if x]:
-        results[p] = run_policy(p, args, device, world, peaks, want_e2e=(p == "dyn"), sampler_cls=ClockSampler)
+        results[p] = run_policy(p, args, device, world, peaks, want_e2e=(p in ("dyn", "dynb")),
+                                sampler_cls=ClockSampler)
 
     head = results.get("dyn") or next(iter(results.values()))
     line = {
@@ -550,6 +562,23 @@ def main():
             "policy": "3xTF32 contractions (fp32-accurate), same plans",
             **{k: {"images_per_s": results[k].get("images_per_s"), "ms_per_step": results[k].get("ms_per_step")}
                for k in ("dynf", "nonef") if k in results}}
+    if "dynb" in results and results["dynb"].get("images_per_s"):
+        z = results["dynb"]
+        bf = peaks.get("bf16_tflops")  # burst: the conv/FC launches are timed one by one
+        line["bf16_storage"] = {
+            "policy": "BF16 storage (the reference's elem_size = 2, cost_model.hpp:69): its own vDNN_dyn plan "
+                      f"({z.get('label')}), kind::f16 tensor cores, fp32 accumulation",
+            "images_per_s": z["images_per_s"], "ms_per_step": z["ms_per_step"],
+            "e2e_images_per_s": (z.get("e2e") or {}).get("value"),
+            "offload_bytes_per_iter": z.get("offload_bytes_per_iter"), "peak_pool_bytes": z.get("peak_pool_bytes"),
+            "exposed_transfer_ms": z.get("exposed_transfer_ms"), "conv_fc_tflops": z.get("conv_fc_tflops"),
+            "conv_fc_frac_of_bf16_peak": (round(z["conv_fc_tflops"] / bf, 4) if bf and z.get("conv_fc_tflops")
+                                          else None),
+            "no_offload_images_per_s": results.get("noneb", {}).get("images_per_s"),
+            "slowdown_vs_bf16_no_offload": (round(z["ms_per_step"] / results["noneb"]["ms_per_step"], 4)
+                                            if results.get("noneb", {}).get("ms_per_step") else None),
+            "speedup_vs_fp32_dyn": (round(z["images_per_s"] / head["images_per_s"], 3)
+                                    if head.get("images_per_s") else None)}
     if "dynp" in results and results["dynp"].get("images_per_s"):
         z = results["dynp"]
         line["peer_hbm_offload"] = {

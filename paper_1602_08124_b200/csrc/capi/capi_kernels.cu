@@ -37,7 +37,10 @@ extern "C" {
 
 uint64_t vdnn_kernel_launch_count(void) { return vdnnk::launch_count(); }
 void vdnn_kernel_set_precise(int32_t on) { vdnnk::set_precise(on != 0); }
-void vdnn_kernel_set_tma(int32_t on) { vdnnk::set_tma(on != 0); }
+void vdnn_kernel_set_tma(int32_t on) {
+  vdnnk::set_tma(on != 0);
+  vdnnk::set_tma_bf16(on != 0);
+}
 uint64_t vdnn_kernel_zvc_slot_bytes(uint64_t bytes) { return vdnnk::zvc_slot_bytes(bytes); }
 vdnn_status vdnn_kernel_zvc_compress(const float* src, uint64_t count, void* host_dst, uint64_t* wire, void* stream) {
   if (!src || !host_dst || !wire) return fail(VDNN_INVALID_ARGUMENT, "null argument");

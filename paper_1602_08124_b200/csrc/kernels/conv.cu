@@ -124,29 +124,32 @@ void* driver_fn(const char* name) {
 }
 
 bool encode_tiled(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-                  const cuuint32_t* box, CUtensorMapSwizzle sw) {
+                  const cuuint32_t* box, CUtensorMapSwizzle sw, CUtensorMapDataType dt) {
   static PfnTiled fn = reinterpret_cast<PfnTiled>(driver_fn("cuTensorMapEncodeTiled"));
   if (!fn) return false;
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<cuuint32_t>(rank), const_cast<void*>(base), dims,
+  return fn(m, dt, static_cast<cuuint32_t>(rank), const_cast<void*>(base), dims,
             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // NHWC [n][h][w][c] as an im2col source: windows of k x k with padding `pad`
-// and stride `stride`; `pixels` rows of 32 channels per load.
+// and stride `stride`; `pixels` rows of one 128-byte channel chunk per load
+// (32 fp32 or, esz = 2, 64 bf16 channels).
 bool encode_im2col(CUtensorMap* m, const void* base, int n, int h, int w, int c, int k, int stride, int pad,
-                   int pixels, CUtensorMapSwizzle sw) {
+                   int pixels, CUtensorMapSwizzle sw, int esz) {
   static PfnIm2col fn = reinterpret_cast<PfnIm2col>(driver_fn("cuTensorMapEncodeIm2col"));
   if (!fn) return false;
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
                               static_cast<cuuint64_t>(n)};
-  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 4, static_cast<cuuint64_t>(w) * c * 4,
-                                 static_cast<cuuint64_t>(h) * w * c * 4};
+  const cuuint64_t e = static_cast<cuuint64_t>(esz);
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * e, static_cast<cuuint64_t>(w) * c * e,
+                                 static_cast<cuuint64_t>(h) * w * c * e};
   const int lower[2] = {-pad, -pad};
   const int upper[2] = {pad - (k - 1), pad - (k - 1)};
   const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, lower, upper, 32,
+  return fn(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+            const_cast<void*>(base), dims, strides, lower, upper, static_cast<cuuint32_t>(128 / esz),
             static_cast<cuuint32_t>(pixels), es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

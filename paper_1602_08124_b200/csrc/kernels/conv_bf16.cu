@@ -7,6 +7,7 @@
 
 #include "kernels.h"
 #include "tcb_conv.cuh"
+#include "tma_maps.h"
 
 namespace vdnnk {
 
@@ -65,29 +66,68 @@ bool build_common_b(const ConvArgs& a, ConvParamsB& p) {
   return true;
 }
 
-template <int BN, int STAGES>
-cudaError_t launch_b(const ConvParamsB& p, int splits, cudaStream_t st) {
+template <int BN, int STAGES, bool TMA>
+cudaError_t launch_b(const ConvParamsB& p, int splits, const CUtensorMap& ta, const CUtensorMap& tb,
+                     cudaStream_t st) {
   using L = TcbSmem<BN, STAGES>;
   static bool attr = false;
   if (!attr) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(tcb_conv_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    const cudaError_t e = cudaFuncSetAttribute(tcb_conv_kernel<BN, STAGES, TMA>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ncols + BN - 1) / BN);
   const dim3 grid(static_cast<unsigned>(tiles), 1, static_cast<unsigned>(splits));
-  tcb_conv_kernel<BN, STAGES><<<grid, 160, L::kTotal, st>>>(p);
+  tcb_conv_kernel<BN, STAGES, TMA><<<grid, 160, L::kTotal, st>>>(p, ta, tb);
   count_launch();
   return cudaGetLastError();
 }
 
 int tile_n(int ncols) { return ncols <= 64 ? 64 : 128; }
 
+thread_local bool g_no_tma_b = false;
+
+// Tensor maps of the TMA producer (tcb_conv.cuh TmaProducerB); false = the
+// cp.async gathers (concatenated inputs, channel counts not 8-multiples,
+// non-square windows).
+bool make_maps_b(const ConvParamsB& p, int bn, CUtensorMap* ta, CUtensorMap* tb) {
+  if (g_no_tma_b || p.nseg != 1 || !p.vec_in || !p.vec_out || p.kh != p.kw) return false;
+  const cuuint64_t taps = static_cast<cuuint64_t>(p.kh) * p.kw;
+  const cuuint64_t C = static_cast<cuuint64_t>(p.C), Co = static_cast<cuuint64_t>(p.Cout);
+  constexpr CUtensorMapDataType kBf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  if (p.kind == kFprop || p.kind == kDgrad) {
+    const bool f = p.kind == kFprop;
+    if (f ? !encode_im2col(ta, p.seg[0].x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, kBM,
+                           CU_TENSOR_MAP_SWIZZLE_128B, 2)
+          : (p.stride != 1 || !encode_im2col(ta, p.dy, p.N, p.Ho, p.Wo, p.Cout, p.kh, 1, p.kh - 1 - p.pad, kBM,
+                                             CU_TENSOR_MAP_SWIZZLE_128B, 2)))
+      return false;
+    // W as (C, tap, Cout): fprop boxes of 64 ci x BN co (K-major rows = co);
+    // dgrad boxes of 64 ci x 64 co (MN-major chunk: K rows = co)
+    const cuuint64_t dims[3] = {C, taps, Co};
+    const cuuint64_t strides[2] = {C * 2, taps * C * 2};
+    const cuuint32_t box[3] = {64, 1, static_cast<cuuint32_t>(f ? bn : 64)};
+    return encode_tiled(tb, p.w, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, kBf);
+  }
+  if (!encode_im2col(ta, p.seg[0].x, p.N, p.H, p.W, p.C, p.kh, p.stride, p.pad, kBKb, CU_TENSOR_MAP_SWIZZLE_128B, 2))
+    return false;
+  const cuuint64_t P = static_cast<cuuint64_t>(p.N) * p.Ho * p.Wo;
+  const cuuint64_t dims[2] = {Co, P};
+  const cuuint64_t strides[1] = {Co * 2};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(kBKb)};
+  return encode_tiled(tb, p.dy, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, kBf);
+}
+
 cudaError_t launch_any(const ConvParamsB& p, int splits, cudaStream_t st) {
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
-  if (tile_n(p.Ncols) == 64) return launch_b<64, 4>(p, splits, st);
-  return launch_b<128, kStagesB>(p, splits, st);
+  const int bn = tile_n(p.Ncols);
+  alignas(64) CUtensorMap ta, tb;
+  std::memset(&ta, 0, sizeof(ta));
+  std::memset(&tb, 0, sizeof(tb));
+  if (make_maps_b(p, bn, &ta, &tb))
+    return bn == 64 ? launch_b<64, 4, true>(p, splits, ta, tb, st) : launch_b<128, kStagesB, true>(p, splits, ta, tb, st);
+  return bn == 64 ? launch_b<64, 4, false>(p, splits, ta, tb, st) : launch_b<128, kStagesB, false>(p, splits, ta, tb, st);
 }
 
 // Split-K factor (same time model as conv.cu's pick_splits): waves of
@@ -221,6 +261,8 @@ __global__ void wgrad_reduce_b_kernel(const __grid_constant__ ConvParamsB p, int
 
 int reduce_blocks(int64_t total) { return static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kNumSmsB)); }
 }  // namespace
+
+void set_tma_bf16(bool on) { g_no_tma_b = !on; }
 
 size_t conv_fprop_ws_bytes_bf16(const ConvArgs& a) {
   ConvParamsB p;

@@ -158,6 +158,8 @@ size_t conv_dgrad_ws_bytes_bf16(const ConvArgs& a);
 cudaError_t conv_wgrad_bf16(const ConvArgs& a, const void* dy, void* w_mut, float lr, float* dw_out, float* ws,
                             size_t ws_bytes, cudaStream_t st);
 size_t conv_wgrad_ws_bytes_bf16(const ConvArgs& a);
+// TMA producers where eligible (default) or cp.async gathers everywhere (per thread)
+void set_tma_bf16(bool on);
 cudaError_t relu_fwd_bf16(void* y, size_t n, cudaStream_t st);
 cudaError_t relu_bwd_bf16(void* g0, const void* const* extra, int nextra, const void* y, size_t n, cudaStream_t st);
 cudaError_t add_into_bf16(void* dst, const void* const* src, int nsrc, size_t n, cudaStream_t st);

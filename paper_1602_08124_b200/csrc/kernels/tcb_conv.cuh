@@ -118,6 +118,51 @@ __device__ __forceinline__ bool scalar_gathers(const ConvParamsB& p) {
   return !p.vec_in || !p.vec_out;
 }
 
+// 64 consecutive flat K elements (r, s, c) of one im2col row (output pixel
+// q), single segment: one pixel decode, the (tap, channel) walk advanced
+// incrementally, 2-byte loads packed into eight 16-B shared stores at
+// dst(j) (j = 16-B granule). First layers (C = 3) and other channel counts
+// that are not multiples of 8.
+template <class Dst>
+__device__ __forceinline__ void gather_row64(const ConvParamsB& p, const bf16* x, bool row_ok, int oh0, int ow0,
+                                             int n, int k0, Dst dst) {
+  int tap = k0 / p.C, c = k0 - tap * p.C;
+  int r = tap / p.kw, s = tap - r * p.kw;
+  const bf16* rowp = nullptr;
+  auto locate = [&]() {
+    const int ih = oh0 + r, iw = ow0 + s;
+    rowp = (row_ok && r < p.kh && ih >= 0 && ih < p.H && iw >= 0 && iw < p.W)
+               ? x + ((static_cast<int64_t>(n) * p.H + ih) * p.W + iw) * p.C
+               : nullptr;
+  };
+  locate();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      uint32_t pair = 0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const uint16_t v = rowp ? ld_bits(rowp + c) : static_cast<uint16_t>(0);
+        pair |= static_cast<uint32_t>(v) << (16 * t);
+        if (++c == p.C) {
+          c = 0;
+          if (++s == p.kw) {
+            s = 0;
+            ++r;
+          }
+          locate();
+        }
+      }
+      w[h] = pair;
+    }
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst(j)), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                 "r"(w[3])
+                 : "memory");
+  }
+}
+
 template <int BN>
 struct GatherB {
   // ---- FPROP: A = im2col rows (pixel) x 64 channels, B = W rows (co) x 64 channels (both K-major)
@@ -156,6 +201,33 @@ struct GatherB {
           bytes = 16;
         }
         cp_async16(kmaj_addr(sb, row, j), src, bytes);
+      }
+    } else if (p.nseg == 1) {
+      // flat K = (r, s, c), one im2col row per thread (kBM = 128 threads)
+      const int m = m0 + tid;
+      const bool ok = m < p.M;
+      const Pix q = decode_pix(ok ? m : 0, p.Ho, p.Wo);
+      gather_row64(p, p.seg[0].x, ok, q.h * p.stride - p.pad, q.w * p.stride - p.pad, q.n, kb * kBKb,
+                   [&](int j) { return kmaj_addr(sa, tid, j); });
+      // B: weight row co, 64 contiguous K elements (tpr threads per row)
+      constexpr int kTpr = 128 / BN, kPer = 64 / kTpr;
+      const int row = tid / kTpr, part = tid % kTpr;
+      const int co = n0 + row;
+      const int k0 = kb * kBKb + part * kPer;
+#pragma unroll
+      for (int j = 0; j < kPer / 8; ++j) {
+        uint32_t w[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int k = k0 + 8 * j + 2 * h;
+          const uint16_t lo = (co < p.Cout && k < p.KK) ? ld_bits(p.w + static_cast<int64_t>(co) * p.KK + k) : 0;
+          const uint16_t hi =
+              (co < p.Cout && k + 1 < p.KK) ? ld_bits(p.w + static_cast<int64_t>(co) * p.KK + k + 1) : 0;
+          w[h] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+        }
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(kmaj_addr(sb, row, part * (kPer / 8) + j)),
+                     "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                     : "memory");
       }
     } else {
       // flat K = (r, s, c) over the concatenated channels; one bf16 per lane
@@ -338,6 +410,14 @@ struct GatherB {
         }
         cp_async16(mnb_addr(sa, k, mc, j), src, bytes);
       }
+    } else if (p.nseg == 1) {
+      // one pixel (K row) x 64 consecutive flat weight columns per thread
+      const int k = tid & 63, mc = tid >> 6;
+      const int pix = kb * kBKb + k;
+      const bool ok = pix < P;
+      const Pix x = decode_pix(ok ? pix : 0, p.Ho, p.Wo);
+      gather_row64(p, p.seg[0].x, ok, x.h * p.stride - p.pad, x.w * p.stride - p.pad, x.n, m0 + mc * 64,
+                   [&](int j) { return mnb_addr(sa, k, mc, j); });
     } else {
       const int e = tid & 63;
       const uint32_t eoff = (e & 7) * 2;
@@ -454,6 +534,110 @@ __device__ __forceinline__ void store_row32(bf16* dst, float (&v)[32], int n, bo
     if (i < n) dst[i] = __float2bfloat16_rn((accumulate ? bf2f(dst[i]) : 0.f) + v[i]);
 }
 
+// TMA producer (one thread; single-segment layers with 8-multiple channel
+// counts). A: im2col boxes of 128 B channel chunks (fprop: X, dgrad: dY, 128
+// pixels = the K-major A tile; wgrad: X, 64 pixels = one MN-major chunk of 64
+// weight columns). B: tiled boxes (fprop: W as (C, tap, Cout) -> BN K-major
+// rows; dgrad: the same map, 64 ci x 64 co per MN chunk; wgrad: dY [P][Cout],
+// 64 co x 64 pixels per MN chunk). Channels past C and pixels past P read as
+// zeros (TMA out-of-bounds fill). Coordinates advance incrementally: the
+// issuing thread is serial.
+template <int BN>
+struct TmaProducerB {
+  int kind;
+  int qw, qh, qn;       // fprop / dgrad: im2col window origin of the tile's first row
+  int ck, nck, r, s;    // fprop / dgrad: current (tap, 64-channel chunk)
+  int wch[2], wr[2], ws[2];  // wgrad: channel offset and tap of each MN chunk of A
+  int p0, pw, ph, pn;   // wgrad: first pixel of the stage
+
+  __device__ __forceinline__ void init(const ConvParamsB& p, int m0, int kb) {
+    kind = p.kind;
+    if (kind != kWgrad) {
+      nck = kind == kFprop ? p.nchunk : (p.Cout + 63) >> 6;
+      const int tap = kb / nck;
+      ck = kb - tap * nck;
+      r = tap / p.kw;
+      s = tap - r * p.kw;
+      if (kind == kFprop) {
+        const Pix q = decode_pix(m0, p.Ho, p.Wo);
+        qw = q.w * p.stride - p.pad;
+        qh = q.h * p.stride - p.pad;
+        qn = q.n;
+      } else {
+        const Pix q = decode_pix(m0, p.H, p.W);
+        qw = q.w - (p.kw - 1 - p.pad);
+        qh = q.h - (p.kh - 1 - p.pad);
+        qn = q.n;
+      }
+    } else {
+#pragma unroll
+      for (int mc = 0; mc < 2; ++mc) {
+        const int vc = (m0 >> 6) + mc;
+        const int tap = vc / p.nchunk, c = vc - tap * p.nchunk;
+        wr[mc] = tap / p.kw;
+        ws[mc] = tap - wr[mc] * p.kw;
+        wch[mc] = c * 64;
+        if (tap >= p.kh * p.kw) wch[mc] = -1;  // past the last tap: left zero
+      }
+      p0 = kb * kBKb;
+      const Pix q = decode_pix(p0, p.Ho, p.Wo);
+      pw = q.w;
+      ph = q.h;
+      pn = q.n;
+    }
+  }
+
+  __device__ __forceinline__ void issue(const ConvParamsB& p, const CUtensorMap* ta, const CUtensorMap* tb, int n0,
+                                        uint32_t sa, uint32_t sb, uint32_t bar) const {
+    if (kind == kFprop) {
+      tma_load_im2col(sa, ta, bar, ck * 64, qw, qh, qn, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+      tma_load_3d(sb, tb, bar, ck * 64, r * p.kw + s, n0);
+    } else if (kind == kDgrad) {
+      tma_load_im2col(sa, ta, bar, ck * 64, qw, qh, qn, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+      const int ftap = (p.kh - 1 - r) * p.kw + (p.kw - 1 - s);
+#pragma unroll
+      for (int mc = 0; mc < BN / 64; ++mc) tma_load_3d(sb + mc * 8192, tb, bar, n0 + mc * 64, ftap, ck * 64);
+    } else {
+      const int iw = pw * p.stride - p.pad, ih = ph * p.stride - p.pad;
+#pragma unroll
+      for (int mc = 0; mc < 2; ++mc)
+        if (wch[mc] >= 0)
+          tma_load_im2col(sa + mc * 8192, ta, bar, wch[mc], iw, ih, pn, static_cast<uint16_t>(ws[mc]),
+                          static_cast<uint16_t>(wr[mc]));
+#pragma unroll
+      for (int mc = 0; mc < BN / 64; ++mc) tma_load_2d(sb + mc * 8192, tb, bar, n0 + mc * 64, p0);
+    }
+  }
+
+  // bytes one stage's loads deliver (the expect_tx count)
+  __device__ __forceinline__ uint32_t bytes() const {
+    if (kind == kWgrad) return (wch[0] >= 0 ? 8192u : 0u) + (wch[1] >= 0 ? 8192u : 0u) + BN * 128u;
+    return kBM * 128u + BN * 128u;
+  }
+
+  __device__ __forceinline__ void next(const ConvParamsB& p) {
+    if (kind != kWgrad) {
+      if (++ck == nck) {
+        ck = 0;
+        if (++s == p.kw) {
+          s = 0;
+          ++r;
+        }
+      }
+    } else {
+      p0 += kBKb;
+      pw += kBKb;
+      while (pw >= p.Wo) {
+        pw -= p.Wo;
+        if (++ph == p.Ho) {
+          ph = 0;
+          ++pn;
+        }
+      }
+    }
+  }
+};
+
 template <int BN, int STAGES>
 struct TcbSmem {
   static constexpr int kABytes = kBM * 128;
@@ -462,9 +646,10 @@ struct TcbSmem {
   static constexpr int kTotal = STAGES * kStage + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool TMA>
 __global__ void __launch_bounds__(160, (TcbSmem<BN, STAGES>::kTotal <= 116 * 1024 ? 2 : 1))
-    tcb_conv_kernel(const __grid_constant__ ConvParamsB p) {
+    tcb_conv_kernel(const __grid_constant__ ConvParamsB p, const __grid_constant__ CUtensorMap tma_a,
+                    const __grid_constant__ CUtensorMap tma_b) {
   extern __shared__ uint8_t smem_raw[];
   using L = TcbSmem<BN, STAGES>;
   const uint32_t raw = smem_u32(smem_raw);
@@ -488,7 +673,7 @@ __global__ void __launch_bounds__(160, (TcbSmem<BN, STAGES>::kTotal <= 116 * 102
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), 128);  // one arrival per producer thread
+      mbar_init(full_bar(s), TMA ? 1 : 128);  // TMA: one expect_tx arrival; else one per producer thread
       mbar_init(empty_bar(s), 1);
     }
     mbar_init(accum_bar, 1);
@@ -507,7 +692,27 @@ __global__ void __launch_bounds__(160, (TcbSmem<BN, STAGES>::kTotal <= 116 * 102
   if (warp < 4) {
     // ---------------- producers ----------------
     const int tid = threadIdx.x;
+    if constexpr (TMA) {
+      if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+        TmaProducerB<BN> tp;
+        tp.init(p, m0, kb_begin);
+        const uint32_t nbytes = tp.bytes();
+        for (int it = 0; it < nkb; ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          if (it >= STAGES) mbar_wait(empty_bar(s), ph ^ 1);
+          const uint32_t sa = base + s * L::kStage;
+          mbar_expect_tx(full_bar(s), nbytes);
+          tp.issue(p, &tma_a, &tma_b, n0, sa, sa + L::kABytes, full_bar(s));
+          tp.next(p);
+        }
+      }
+      __syncwarp();
+    }
     const bool scalar = scalar_gathers(p);
+    if constexpr (!TMA)
     for (int it = 0; it < nkb; ++it) {
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;

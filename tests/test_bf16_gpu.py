@@ -185,3 +185,17 @@ def test_bf16_rejects_fp32_only_modes():
         V.Session(g, d, cm, 64 << 20, precise_fp32=True)
     with pytest.raises(V.VdnnError, match="compressed offload"):
         V.Session(g, d, cm, 64 << 20, compress_offload=True)
+
+
+def test_cpasync_gathers_bf16():
+    """The cp.async gather producers (taken for concatenated inputs and
+    channel counts that are not 8-multiples) on layers that otherwise take
+    the TMA producers: VGG-16 b16 and inception_toy b32, layer-local."""
+    _need_gpu()
+    from paper_1602_08124_b200 import _lib as L
+    L.lib().vdnn_kernel_set_tma(0)
+    try:
+        TL._run("vgg16_b16_cpasync", "vgg16", 16, "all", False, es=2)
+        TL._run("inception_toy_b32_cpasync", "inception_toy", 32, "all", False, es=2)
+    finally:
+        L.lib().vdnn_kernel_set_tma(1)

@@ -1,6 +1,6 @@
 """Per-layer timing of one VGG-16 (or other preset) training step on the GPU.
 
-    python tools/prof_layers.py [net] [batch] [policy] [--no-tma]
+    python tools/prof_layers.py [net] [batch] [policy] [--no-tma] [--bf16]
 """
 import sys
 
@@ -15,6 +15,8 @@ if "--no-tma" in sys.argv:
     L.lib().vdnn_kernel_set_tma(0)
 g = V.build_preset(net, batch)
 cm = V.CostModel()
+if "--bf16" in sys.argv:
+    cm.elem_size = 2
 if policy == "none":
     d = V.static_decision(V.PolicyKind.Baseline, V.AlgoMode.PerfOptimal, g, cm)
     cap = 150 << 30
