@@ -214,6 +214,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         policy = policy[:-1]
     if peer_target and world < 2:
         return {"policy": policy + "p", "verdict": "skipped: a peer-HBM offload target needs >= 2 GPUs"}
+    sel = None
     if policy == "dyn":
         sel = V.dynamic_select(g, cap, cm)
         if sel.decision is None:
@@ -290,6 +291,8 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     off_ms = sum((e.end - e.start) for e in m.events if e.kind == V.EventKind.Offload) * 1e-6
     pre_ms = sum((e.end - e.start) for e in m.events if e.kind == V.EventKind.Prefetch) * 1e-6
     free, total = torch.cuda.mem_get_info(device)
+    if getattr(args, "artifacts", None) and name in ("dyn", "dynb") and device == 0:
+        write_step_artifacts(args, name, g, d, cm, cap, s, m, sel)
     res = {
         "policy": name,
         "label": d.label + ({"tf32": " +zvc/tf32-exact", True: " +zvc"}.get(compress, ""))
@@ -379,6 +382,35 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
     return res
 
 
+def write_step_artifacts(args, name, g, d, cm, cap, s, m, sel):
+    """--artifacts DIR: the reference's artefact files (report.hpp:44-236) for
+    the measured step, plus the calibrated re-plan: every
+    layer's latency pinned to its measured time, the link to its measured
+    bandwidth; the schedule must not move, the planned time should track the
+    measured one."""
+    import paper_1602_08124_b200 as V
+    from paper_1602_08124_b200 import formats as F
+    out = os.path.join(args.artifacts, f"{args.net}{'' if args.extra == 0 else '+' + str(args.extra)}_b{args.batch}_{name}")
+    F.write_artifacts(out, g, d, m, sel.passes if sel else None)
+    xfer = [e for e in m.events if e.kind in (V.EventKind.Offload, V.EventKind.Prefetch)]
+    ns = sum(e.end - e.start for e in xfer)
+    gbs = sum(e.bytes for e in xfer) / ns if ns else None
+    cal = F.calibrated_cost_model(s, link_gbs=gbs)
+    r = V.simulate(g, d, cal, cap)
+    summary = {
+        "decision": d.label, "elem_size": cm.elem_size, "capacity": cap,
+        "measured_step_ns": m.total_ns, "measured_stall_ns": m.stall_ns(),
+        "default_model_plan_ns": s.plan.total_ns,
+        "calibrated_plan_ns": r.total_ns, "calibrated_stall_ns": r.stall_ns(),
+        "calibrated_rel_err": (r.total_ns - m.total_ns) / m.total_ns,
+        "link_gbs_measured": gbs,
+        "signature_planned": s.plan.signature(), "signature_calibrated": r.signature(),
+        "replay_violations": [v.kind for v in V.replay_check(m, g, d, cap)],
+    }
+    with open(os.path.join(out, "calibration.json"), "w") as f:
+        json.dump(summary, f, indent=1)
+
+
 _CPU_WARM = False
 
 
@@ -464,6 +496,9 @@ def main():
     ap.add_argument("--cpu-sample-batch", type=int, default=96,
                     help="images in the CPU reference sample (~7 s of CPU work for VGG-16 b96 on 16 cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--artifacts", default=None,
+                    help="write report.json / timeline.csv / pool_trace.csv / decision.json / graph.json / "
+                         "profile_passes.csv / calibration.json of the measured dyn (and dynb) step into DIR")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

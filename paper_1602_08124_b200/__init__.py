@@ -9,7 +9,7 @@ from .api import (
     GradientScheme, InvalidDecision, InvalidDepth, JoinRule, LayerKind, NetworkGraph, OomInfo, Phase,
     PolicyDecision, PolicyKind, PoolUseError, ProfilePassResult, RunReport, ShapeMismatch, SimOptions, Stream,
     StreamEvent, TensorShape, UnknownPreset, Violation, WrongLayerKind, baseline_footprint, build_preset,
-    dynamic_select, extend_vgg, gradient_map_bytes, greedy_downgrade, per_layer_event_peaks, program_check, replay_check,
+    dynamic_select, extend_vgg, gradient_map_bytes, greedy_downgrade, per_layer_event_peaks, placements, program_check, replay_check,
     Session, from_bf16_bits, kernel_launch_count, to_bf16_bits, report_from_events, simulate, simulate_oracle, simulate_with_trace, static_decision,
 )
 

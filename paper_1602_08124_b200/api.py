@@ -1019,6 +1019,15 @@ class Session:
         return p.value or 0
 
 
+def placements(r: "RunReport"):
+    """(kind, layer, buffer, tag, bytes, offset) of every non-SYNC event in log
+    order: what a schedule places where. SYNC rows (stalls) depend on timing
+    -- a measured log and a re-planned one stall at other steps -- everything
+    else is timing-independent (the schedule signature covers the same rows)."""
+    return [(int(e.kind), e.layer, e.buffer, e.tag, e.bytes, e.offset) for e in r.events
+            if e.kind != EventKind.Sync]
+
+
 def to_bf16_bits(a):
     """float32 array -> uint16 bf16 bit patterns, round to nearest even (NaN kept NaN)."""
     import numpy as np

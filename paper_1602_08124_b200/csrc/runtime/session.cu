@@ -1186,7 +1186,7 @@ vdnnp::Report Session::measured_report() const {
   size_t xi = 0;
   int cur = -1;          // step index of the current FWD/BWD group
   bool bwd = false;
-  i64 last_x_end = 0, horizon = 0;
+  i64 horizon = 0;
   std::map<int, i64> off_end;
   // the step an event belongs to is the next FWD/BWD row at or after it for
   // ALLOC/PREFETCH (they precede their kernel), the last one for the rest
@@ -1195,20 +1195,62 @@ vdnnp::Report Session::measured_report() const {
     if (bi < bwd_.size()) return bwd_[bi].ev;
     return cur;
   };
+  // SYNC rows are measured, not copied from the plan (the planner's model
+  // stalls at other steps than the B200 does): the compute stream's waits
+  // under the reference's sync rules (simulator.hpp:315-322 forward: FWD(n+1)
+  // after n's offloads; :400-441 backward: BWD(m) after the prefetches it
+  // reads, and after the prefetches launched during BWD(m)), i.e. the gaps
+  // kernel end -> next step start and step start -> kernel start.
+  auto sync_row = [&](int layer, i64 a, i64 b, bool backward) {
+    if (b <= a) return;
+    Event e;
+    e.kind = Ev::Sync;
+    e.lane = Lane::Compute;
+    e.layer = layer;
+    e.t0 = a;
+    e.t1 = b;
+    (backward ? r.stall_bwd : r.stall_fwd) += b - a;
+    horizon = std::max(horizon, b);
+    r.events.push_back(e);
+  };
+  const int nsteps = static_cast<int>(nst);
+  auto next_t0 = [&](int st) { return st + 1 < nsteps ? t0[static_cast<size_t>(st + 1)] : ke[static_cast<size_t>(st)]; };
+  int fwd_sync_step = -1;   // forward step with offloads whose post-kernel wait is not emitted yet
+  int bwd_tail_step = -1;   // backward step with prefetches: same, after its BWD row
+  int bwd_pre_done = -1;    // backward step whose pre-kernel wait was emitted
   for (size_t k = 0; k < plan_.events.size(); ++k) {
     const Event& pe = plan_.events[k];
     Event e = pe;
     if (!bwd && pe.kind == Ev::Prefetch) bwd = true;
     if (!bwd && pe.kind == Ev::Bwd) bwd = true;
     if (!bwd && pe.kind == Ev::Alloc && pe.lane == Lane::Memory) bwd = true;
+    if (pe.kind == Ev::Sync) continue;
+    if (fwd_sync_step >= 0 && pe.kind != Ev::Offload) {
+      const size_t st = static_cast<size_t>(fwd_sync_step);
+      sync_row(prog_.steps[st].layer, ke[st], next_t0(fwd_sync_step), false);
+      fwd_sync_step = -1;
+    }
+    if (bwd_tail_step >= 0 && pe.kind != Ev::Bwd) {
+      const size_t st = static_cast<size_t>(bwd_tail_step);
+      sync_row(prog_.steps[st].layer, ke[st], next_t0(bwd_tail_step), true);
+      bwd_tail_step = -1;
+    }
+    if (bwd && bi < bwd_.size() && (pe.kind == Ev::Bwd || (pe.kind == Ev::Alloc && pe.lane == Lane::Compute)) &&
+        bwd_pre_done != bwd_[bi].ev) {
+      const BwdStep& b = bwd_[bi];
+      bwd_pre_done = b.ev;
+      if (!b.wait_prefetch.empty())
+        sync_row(b.layer, t0[static_cast<size_t>(b.ev)], ks[static_cast<size_t>(b.ev)], true);
+    }
     switch (pe.kind) {
       case Ev::Fwd:
+        if (!fwd_[fi].offloads.empty()) fwd_sync_step = fwd_[fi].ev;
         cur = fwd_[fi++].ev;
         e.t0 = ks[static_cast<size_t>(cur)];
         e.t1 = ke[static_cast<size_t>(cur)];
-        last_x_end = 0;
         break;
       case Ev::Bwd:
+        if (!bwd_[bi].prefetches.empty()) bwd_tail_step = bwd_[bi].ev;
         cur = bwd_[bi++].ev;
         e.t0 = ks[static_cast<size_t>(cur)];
         e.t1 = ke[static_cast<size_t>(cur)];
@@ -1218,7 +1260,6 @@ vdnnp::Report Session::measured_report() const {
         e.t0 = xs[xi];
         e.t1 = xe[xi];
         ++xi;
-        last_x_end = e.t1;
         if (pe.kind == Ev::Offload) off_end[pe.buffer] = e.t1;
         break;
       case Ev::Alloc: {
@@ -1243,22 +1284,8 @@ vdnnp::Report Session::measured_report() const {
         }
         break;
       }
-      case Ev::Sync: {
-        const bool pre_kernel = k + 1 < plan_.events.size() &&
-                                (plan_.events[k + 1].kind == Ev::Alloc || plan_.events[k + 1].kind == Ev::Bwd) &&
-                                bwd && (bi < bwd_.size() && pe.layer == bwd_[bi].layer);
-        if (pre_kernel) {
-          const int st = bwd_[bi].ev;
-          e.t0 = t0[static_cast<size_t>(st)];
-          e.t1 = ks[static_cast<size_t>(st)];
-          r.stall_bwd += e.t1 - e.t0;
-        } else {
-          e.t0 = ke[static_cast<size_t>(cur)];
-          e.t1 = std::max(e.t0, last_x_end);
-          (bwd ? r.stall_bwd : r.stall_fwd) += e.t1 - e.t0;
-        }
+      case Ev::Sync:
         break;
-      }
     }
     if (pe.kind != Ev::Release || pe.layer >= 0) horizon = std::max(horizon, e.t1);
     r.events.push_back(e);

@@ -9,6 +9,7 @@ reference's own tooling (and its replay_check) can consume B200 logs:
 * events_csv (six-column timeline) ........ report.hpp:196-204
 * pool_trace_csv .......................... report.hpp:206-214
 * profile_passes_csv ...................... report.hpp:228-236
+* pool_trace_from_report / write_artifacts: the same files for a measured step
 """
 from __future__ import annotations
 
@@ -162,6 +163,52 @@ def calibrated_cost_model(session: "V.Session", link_gbs: float = None) -> V.Cos
     if link_gbs:
         cm.link_effective_bw = link_gbs * 1e9
     return cm
+
+
+def pool_trace_from_report(r: V.RunReport, alignment: int = 512) -> List:
+    """Pool trace (report.hpp:206-214 rows: time, op, tag, offset, bytes,
+    current, high_water) of a *measured* log: the ALLOC / RELEASE events in log
+    order, which is the order the planner's pool saw them
+    (memory_pool.hpp:84,96), with lengths rounded to the pool alignment
+    (memory_pool.hpp:43,59), a free carrying its extent's allocation tag
+    (memory_pool.hpp:96; a RELEASE event may name another tag,
+    simulator.hpp:456,519), and the measured timestamps. Equal to the planned
+    trace (simulate_with_trace) in every column except time."""
+    rows, cur, hw, live = [], 0, 0, {}
+    for e in r.events:
+        if e.kind == V.EventKind.Alloc:
+            need = (e.bytes + alignment - 1) // alignment * alignment
+            cur += need
+            hw = max(hw, cur)
+            live[e.offset] = (need, e.tag)
+            rows.append((e.start, "a", e.tag, e.offset, need, cur, hw))
+        elif e.kind == V.EventKind.Release:
+            need, tag = live.pop(e.offset)
+            cur -= need
+            rows.append((e.start, "f", tag, e.offset, need, cur, hw))
+    return rows
+
+
+def write_artifacts(out_dir: str, g: V.NetworkGraph, d: V.PolicyDecision, measured: V.RunReport,
+                    passes: List = None) -> Dict[str, str]:
+    """The reference's artefacts (report.hpp:44-236) for a measured B200 step:
+    graph.json, decision.json, report.json (events with tag / buffer / offset),
+    timeline.csv, pool_trace.csv and, for vDNN_dyn, profile_passes.csv."""
+    import os
+    os.makedirs(out_dir, exist_ok=True)
+    files = {
+        "graph.json": dumps(graph_to_json(g)),
+        "decision.json": dumps(decision_to_json(d)),
+        "report.json": dumps(report_to_json(measured)),
+        "timeline.csv": events_csv(measured),
+        "pool_trace.csv": pool_trace_csv(pool_trace_from_report(measured)),
+    }
+    if passes:
+        files["profile_passes.csv"] = profile_passes_csv(passes)
+    for name, text in files.items():
+        with open(os.path.join(out_dir, name), "w") as f:
+            f.write(text)
+    return {k: os.path.join(out_dir, k) for k in files}
 
 
 def dumps(obj) -> str:
