@@ -39,15 +39,20 @@ METRIC = "VGG-16 b256 train images/sec & peak GPU mem (vDNN_all/conv/dyn vs no-o
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+TRAFFIC_FILES = ("r02_conv_traffic.json", "r01_conv_traffic.json")  # newest capture first
+
+
 def conv_traffic():
-    """Mean DRAM bytes per conv-engine launch from the committed ncu capture
-    (profiles/r01_conv_traffic.json), or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_conv_traffic.json")
-    try:
-        with open(path) as f:
-            return int(json.load(f)["conv_dram_bytes_per_launch"])
-    except (OSError, KeyError, ValueError):
-        return None
+    """(mean DRAM bytes per conv-engine launch, source file) from the newest
+    committed ncu capture (profiles/r0N_conv_traffic.json), or (None, None)."""
+    for name in TRAFFIC_FILES:
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name)
+        try:
+            with open(path) as f:
+                return int(json.load(f)["conv_dram_bytes_per_launch"]), "profiles/" + name
+        except (OSError, KeyError, ValueError):
+            continue
+    return None, None
 
 
 def measured_tf32_peak(peaks, peaks_src):
@@ -233,6 +238,7 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
                              device="cpu" if torch.distributed.get_backend() == "gloo" else f"cuda:{device}")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
             cap = int(t.item())
+    free0, total0 = torch.cuda.mem_get_info(device)  # before the session: context + this process's torch state
     plan = V.simulate(g, d, cm, cap)
     if not plan.pass_:
         return {"policy": policy, "label": d.label, "verdict": plan.verdict(), "capacity": cap}
@@ -302,6 +308,12 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
         "loss": loss, "precise_fp32": bool(precise), "storage": "bf16" if bf16 else "fp32",
         "peak_pool_bytes": plan.max_mem_bytes, "arena_bytes": s.arena_info()["arena_bytes"],
         "device_used_bytes": total - free,
+        # process HBM = pool arena (<= the budget) + non-pool scratch + what was
+        # in use before the session (CUDA context, torch)
+        "hbm": {"arena_bytes": s.arena_info()["arena_bytes"], "non_pool_scratch_bytes": s.arena_info()["scratch_bytes"],
+                "context_and_other_bytes": total0 - free0,
+                "unaccounted_bytes": (total - free) - (total0 - free0) - s.arena_info()["arena_bytes"]
+                                     - s.arena_info()["scratch_bytes"]},
         "offload_bytes_per_iter": plan.offload_traffic_bytes, "prefetch_bytes_per_iter": plan.prefetch_traffic_bytes,
         "d2h_gbs": round(plan.offload_traffic_bytes / (off_ms * 1e-3) / 1e9, 2) if off_ms > 0 else None,
         "h2d_gbs": round(plan.prefetch_traffic_bytes / (pre_ms * 1e-3) / 1e9, 2) if pre_ms > 0 else None,
@@ -518,9 +530,12 @@ def main():
             torch.distributed.init_process_group("gloo")
         else:
             torch.cuda.set_device(local)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # the NCCL rank census (NVLS / P2P paths) in stderr
             torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     device = local
     torch.cuda.set_device(device)
+    from paper_1602_08124_b200.dist import bind_numa, rank_census
+    numa = bind_numa(device)  # before any pinned host arena is allocated
     peaks, peaks_src = load_peaks()
     link = link_bandwidth(device)
     # the TF32 ceiling is probed first, on a cool GPU at full clocks: the dyn
@@ -538,6 +553,7 @@ def main():
                                 sampler_cls=ClockSampler)
 
     head = results.get("dyn") or next(iter(results.values()))
+    census = rank_census(world, device, head.get("dp_exchange"), numa) if world > 1 else None
     line = {
         "metric": METRIC, "value": head.get("images_per_s"), "unit": "images/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head.get("ms_per_step"),
@@ -555,15 +571,18 @@ def main():
         "clocks": head.get("clocks"),
         "peak_gpu_mem_bytes": head.get("peak_pool_bytes"),
         "device_used_bytes": head.get("device_used_bytes"),
+        "hbm": head.get("hbm"),
     }
+    if census:
+        line["rank_census"] = census
     if head.get("_conv_ms"):
         ach = head["_flops"] / (head["_conv_ms"] * 1e-3) / 1e12
         line["roofline"] = {"bound": "tensor", "kernel": "tcgen05 conv engine (tc_conv_pair / tc_wgrad_pair / tc_conv_halo_pair / tc_wgrad_halo_pair / tc_conv / tc_conv_persist / c3tc kernels: every conv+FC fprop, dgrad, wgrad launch)",
                             "achieved": round(ach, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
-                            "frac": round(ach / tf32_peak, 4), "traffic": conv_traffic(),
+                            "frac": round(ach / tf32_peak, 4), "traffic": conv_traffic()[0],
                             "peak_note": peak_note,
                             "traffic_note": "DRAM read+write bytes per conv-engine launch (mean over one dyn step), "
-                                            "ncu capture profiles/r01_conv_traffic.json"}
+                                            f"ncu capture {conv_traffic()[1]}"}
     line["host_link"] = dict(link, **{
         "offload_bytes_per_iter": head.get("offload_bytes_per_iter"),
         "d2h_gbs_in_run": head.get("d2h_gbs"), "h2d_gbs_in_run": head.get("h2d_gbs"),

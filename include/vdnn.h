@@ -341,6 +341,12 @@ typedef struct vdnn_peer_handle {
 vdnn_status vdnn_session_peer_export(vdnn_session* s, vdnn_peer_handle* out);
 vdnn_status vdnn_session_peer_attach(vdnn_session* s, int32_t rank, int32_t world, const vdnn_peer_handle* all);
 vdnn_status vdnn_session_peer_exchange(vdnn_session* s, float lr, float grad_scale);
+/* on = 1: instead of vdnn_session_peer_exchange after the step, every layer's
+ * exchange runs inside vdnn_session_step on a side stream right after that
+ * layer's weight gradient (overlapping the rest of the backward pass), with
+ * grad_scale applied; the step ends with one barrier. Same chunks and
+ * summation order: bit-identical weights. Not with cuda_graph sessions. */
+vdnn_status vdnn_session_peer_overlap(vdnn_session* s, int32_t on, float grad_scale);
 vdnn_status vdnn_session_peer_detach(vdnn_session* s);
 /* Device offload target (offload_target = 1): the bytes the offload slots need; use a caller-provided
  * device buffer, or host a spill buffer for a peer (export its CUDA IPC handle) and offload into a

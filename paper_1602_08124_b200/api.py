@@ -969,6 +969,12 @@ class Session:
         """Fused all-reduce + SGD + weight broadcast on the compute stream."""
         _call("vdnn_session_peer_exchange", self.handle, C.c_float(lr), C.c_float(scale))
 
+    def peer_overlap(self, on: bool = True, scale: float = 1.0) -> None:
+        """Exchange each layer inside step(), on a side stream right after that
+        layer's wgrad (overlapping the rest of backward); bit-identical to
+        peer_exchange after the step."""
+        _call("vdnn_session_peer_overlap", self.handle, C.c_int32(int(on)), C.c_float(scale))
+
     def peer_detach(self) -> None:
         _call("vdnn_session_peer_detach", self.handle)
 

@@ -244,6 +244,12 @@ vdnn_status vdnn_session_peer_exchange(vdnn_session* s, float lr, float scale) {
     return VDNN_OK;
   });
 }
+vdnn_status vdnn_session_peer_overlap(vdnn_session* s, int32_t on, float scale) {
+  return guard([&] {
+    S(s).peer_overlap(on != 0, scale);
+    return VDNN_OK;
+  });
+}
 vdnn_status vdnn_session_peer_detach(vdnn_session* s) {
   return guard([&] {
     S(s).peer_detach();

@@ -79,11 +79,14 @@ void Session::peer_attach(int rank, int world, const PeerHandle* all) {
     throw;
   }
 
-  // this rank's share of the chunks
+  // this rank's share of the chunks (contiguous per layer)
   std::vector<vdnnk::PeerChunk> mine;
+  peer_first_.assign(static_cast<size_t>(L_), 0);
+  peer_count_.assign(static_cast<size_t>(L_), 0);
   uint64_t j = 0;
   for (int i = 0; i < L_; ++i) {
     const size_t k = static_cast<size_t>(i);
+    peer_first_[k] = static_cast<int>(mine.size());
     if (grad_off_[k] == kNoOff) continue;
     const uint64_t n = df_.at[k].w_bytes / 4;
     for (uint64_t s = 0; s < n; s += kChunk, ++j) {
@@ -94,6 +97,7 @@ void Session::peer_attach(int rank, int world, const PeerHandle* all) {
       c.count = static_cast<uint32_t>(std::min<uint64_t>(kChunk, n - s));
       mine.push_back(c);
     }
+    peer_count_[k] = static_cast<int>(mine.size()) - peer_first_[k];
   }
   if (!mine.empty()) {
     check(cudaMalloc(&peer_chunks_, mine.size() * sizeof(vdnnk::PeerChunk)), "cudaMalloc(peer chunks)");
@@ -115,9 +119,52 @@ void Session::peer_exchange(float lr, float scale) {
   check(vdnnk::peer_barrier(peer_, peer_epoch_, 1, cs_), "peer barrier (post)");
 }
 
+void Session::peer_overlap(bool on, float scale) {
+  if (on && peer_world_ == 0) throw PlanError(Err::Generic, "peer_overlap: call peer_attach first");
+  if (on && o_.cuda_graph)
+    throw PlanError(Err::Config, "peer_overlap: the in-step exchange's barrier epochs are per step (no CUDA graph)");
+  synchronize();
+  if (on && !xs_) {
+    check(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking), "stream");
+    check(cudaEventCreateWithFlags(&xs_done_, cudaEventDisableTiming), "event");
+    wg_ev_.assign(static_cast<size_t>(L_), nullptr);
+    for (int i = 0; i < L_; ++i)
+      if (grad_off_[static_cast<size_t>(i)] != kNoOff)
+        check(cudaEventCreateWithFlags(&wg_ev_[static_cast<size_t>(i)], cudaEventDisableTiming), "event");
+  }
+  peer_inline_ = on;
+  peer_scale_ = scale;
+}
+
+// One layer's share: every rank's dW(layer) is complete (pre barrier), then
+// reduce + SGD + broadcast of this rank's chunks of that layer. Every rank
+// enqueues the same layers in the same (backward) order, so the barrier
+// epochs match.
+void Session::peer_layer(int layer, float lr) {
+  const size_t k = static_cast<size_t>(layer);
+  check(cudaEventRecord(wg_ev_[k], cs_), "record");
+  check(cudaStreamWaitEvent(xs_, wg_ev_[k], 0), "wait");
+  vdnnk::PeerArgs a = peer_;
+  a.step = lr * peer_scale_;
+  a.chunks = peer_chunks_ ? peer_chunks_ + peer_first_[k] : nullptr;
+  a.nchunks = peer_count_[k];
+  check(vdnnk::peer_barrier(a, ++peer_epoch_, 0, xs_), "peer barrier (layer)");
+  check(vdnnk::peer_reduce_sgd(a, xs_), "peer reduce+sgd (layer)");
+}
+
+// Every rank finished every layer (its weights are written everywhere, its
+// gradients read by everyone) before any rank's next step; the compute stream
+// joins the exchange stream.
+void Session::peer_finish() {
+  check(vdnnk::peer_barrier(peer_, ++peer_epoch_, 1, xs_), "peer barrier (post)");
+  check(cudaEventRecord(xs_done_, xs_), "record");
+  check(cudaStreamWaitEvent(cs_, xs_done_, 0), "wait");
+}
+
 void Session::peer_detach() {
   if (peer_world_ == 0 && peer_maps_.empty() && !peer_chunks_) return;
   if (cs_) cudaStreamSynchronize(cs_);
+  if (xs_) cudaStreamSynchronize(xs_);  // in-step exchanges still reading the mappings
   drop_graph();
   for (void* m : peer_maps_) cudaIpcCloseMemHandle(m);
   peer_maps_.clear();
@@ -125,6 +172,7 @@ void Session::peer_detach() {
   peer_chunks_ = nullptr;
   peer_ = vdnnk::PeerArgs{};
   peer_world_ = 0;
+  peer_inline_ = false;
 }
 
 // ------------------------------------------------ device offload target ----

@@ -240,6 +240,12 @@ void Session::release() noexcept {
   if (loss_ring_) cudaFreeHost(loss_ring_), loss_ring_ = nullptr;
   if (in_stream_) cudaStreamDestroy(in_stream_), in_stream_ = nullptr;
   peer_detach();
+  if (xs_) cudaStreamSynchronize(xs_);
+  for (auto e : wg_ev_)
+    if (e) cudaEventDestroy(e);
+  wg_ev_.clear();
+  if (xs_done_) cudaEventDestroy(xs_done_), xs_done_ = nullptr;
+  if (xs_) cudaStreamDestroy(xs_), xs_ = nullptr;
   if (signal_) cudaFree(signal_), signal_ = nullptr;
   if (arena_) cudaFree(arena_), arena_ = nullptr;
   if (host_ && host_owned_) cudaFreeHost(host_);
@@ -750,6 +756,7 @@ void Session::run_bwd(const BwdStep& s, float lr) {
         check(bf_ ? vdnnk::bias_grad_bf16(dy, n, o, bias, lr, db, cs_) : vdnnk::bias_grad(dy, n, o, bias, lr, db, cs_),
               "bias_grad");
       }
+      if (peer_inline_ && grads_) peer_layer(s.layer, lr);
       break;
     }
     case Kind::Pool: {
@@ -948,6 +955,7 @@ void Session::enqueue_step(float lr) {
   check(cudaStreamWaitEvent(ms_, ev_sync_, 0), "wait");
   for (const FwdStep& s : fwd_) run_fwd(s, lr);
   for (const BwdStep& s : bwd_) run_bwd(s, lr);
+  if (peer_inline_) peer_finish();
   if (input_idle_after_ < 0) check(cudaEventRecord(input_idle_ev_, cs_), "record");
 }
 

@@ -145,6 +145,12 @@ class Session {
   PeerHandle peer_export();
   void peer_attach(int rank, int world, const PeerHandle* all);
   void peer_exchange(float lr, float scale);
+  // In-step exchange (SURVEY §8(e) placement): each layer's share is reduced,
+  // updated and broadcast on a side stream right after that layer's wgrad in
+  // BWD, overlapping the rest of the backward pass; the step ends with one
+  // barrier and the compute stream joins the side stream. Same chunks, same
+  // summation order: bit-identical to peer_exchange after the step.
+  void peer_overlap(bool on, float scale);
   void peer_detach();
   int peer_world() const { return peer_world_; }
   // Device offload target (Options::offload_target = 1): bytes the slots need,
@@ -270,6 +276,14 @@ class Session {
   void* spill_map_ = nullptr;             // IPC mapping of the peer's spill buffer (our target)
   int peer_world_ = 0;
   unsigned long long peer_epoch_ = 0;
+  bool peer_inline_ = false;              // peer_overlap: exchange inside the step
+  float peer_scale_ = 1.f;
+  cudaStream_t xs_ = nullptr;             // exchange stream
+  cudaEvent_t xs_done_ = nullptr;
+  std::vector<cudaEvent_t> wg_ev_;        // per layer: its wgrad finished (compute stream)
+  std::vector<int> peer_first_, peer_count_;  // per layer: this rank's chunk range
+  void peer_layer(int layer, float lr);   // enqueue one layer's exchange (after its wgrad)
+  void peer_finish();                     // end of step: barrier, join
 
   u64 x_off_ = 0;                // INPUT feature extent (setup allocation)
   int input_idle_after_ = -1;    // step after which the INPUT extent may take the next batch

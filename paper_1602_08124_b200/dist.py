@@ -6,8 +6,10 @@ plan (identical per-rank schedule, weak scaling). Two exchange paths:
   rank through CUDA IPC; one kernel per rank reduces its 1/N share of the
   gradients from all ranks over NVLink, applies SGD and stores the new weights
   into every rank's arena (reduce-scatter + update + all-gather in one pass,
-  bracketed by two flag barriers). torch.distributed only carries the
-  handles.
+  bracketed by flag barriers). By default (overlap=True) each
+  layer's share runs inside the step on a side stream right after that
+  layer's wgrad, overlapping the rest of the backward pass; the step ends
+  with one barrier. torch.distributed only carries the handles.
 * ``DataParallel``: one bucketed NCCL all-reduce over the session's gradient
   arena followed by the SGD kernels (the library baseline).
 
@@ -66,6 +68,38 @@ def make_data_parallel(session, world: int, device: int, mode: Optional[str] = N
     raise ValueError(f"unknown data-parallel mode {mode!r}")
 
 
+def bind_numa(device: int) -> Optional[str]:
+    """Bind this process to the CPUs next to ``device`` (NVML's ideal affinity)
+    before the session allocates its pinned host arena, so the arena's pages
+    are first touched on the GPU's NUMA node (up to 64 GB per rank for
+    VGG-416 b32 dyn). Returns the CPU list, or None if NVML is unavailable."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        pynvml.nvmlDeviceSetCpuAffinity(h)
+        cpus = sorted(os.sched_getaffinity(0))
+        return f"{cpus[0]}-{cpus[-1]} ({len(cpus)} cpus)" if cpus else None
+    except Exception:
+        return None
+
+
+def rank_census(world: int, device: int, exchange: Optional[str], numa: Optional[str], group=None):
+    """Every rank's (rank, device, GPU UUID, PCI bus id, exchange path, NUMA
+    binding), gathered on all ranks: proof the N ranks ran on N devices."""
+    import torch
+    import torch.distributed as dist
+    props = torch.cuda.get_device_properties(device)
+    me = {"rank": dist.get_rank(group) if world > 1 else 0, "device": device,
+          "uuid": str(getattr(props, "uuid", "")), "pci_bus_id": getattr(props, "pci_bus_id", None),
+          "name": props.name, "exchange": exchange, "numa_cpus": numa}
+    if world <= 1:
+        return [me]
+    out = [None] * world
+    dist.all_gather_object(out, me, group=group)
+    return out
+
+
 def ring_spill(session, world: int, group=None) -> int:
     """Peer-HBM offload target for data-parallel runs: every rank hosts a
     spill buffer (its own plan's offload bytes; the plans are identical) and
@@ -96,7 +130,7 @@ class PeerDataParallel:
 
     mode = "peer"
 
-    def __init__(self, session, world: int, group=None):
+    def __init__(self, session, world: int, group=None, overlap: Optional[bool] = None):
         import torch.distributed as dist
         self.s = session
         self.world = world
@@ -120,12 +154,19 @@ class PeerDataParallel:
         if bad:
             session.peer_detach()
             raise PeerUnavailable("; ".join(bad))
+        if overlap is None:
+            overlap = os.environ.get("VDNN_DP_OVERLAP", "1") != "0"
+        self.overlap = bool(overlap)
+        if self.overlap:
+            session.peer_overlap(True, 1.0 / world)
+            self.mode = "peer-overlap"
 
     def step(self, lr: float, want_loss: bool = False) -> Optional[float]:
-        # the exchange is enqueued after the step's kernels; the loss read
-        # (want_loss) happens inside step(), before the exchange completes
         loss = self.s.step(lr, want_loss=want_loss)
-        self.s.peer_exchange(lr, 1.0 / self.world)
+        if not self.overlap:
+            # after the step's kernels (the loss read inside step() happens
+            # before the exchange completes)
+            self.s.peer_exchange(lr, 1.0 / self.world)
         return loss
 
     def close(self) -> None:

@@ -76,6 +76,9 @@ class _FakeSession:
     def peer_detach(self):
         self.detached = True
 
+    def peer_overlap(self, on, scale):
+        self.overlap = (on, scale)
+
 
 def _peer_worker(rank, world, port, fail_rank, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))

@@ -86,7 +86,7 @@ def _worker(rank, world, port, q):
         g = V.build_preset("inception_toy", 8)
         cm = V.CostModel()
         s, w = _session(V, numeric, g, cm)
-        dp = PeerDataParallel(s, world)
+        dp = PeerDataParallel(s, world, overlap=False)  # the exchange after the step, checked in between
         report = []
         for it in range(2):
             images, labels = _batch(g, 100 + 10 * it + rank)
@@ -123,6 +123,70 @@ def _worker(rank, world, port, q):
         q.put((rank, None, repr(e)))
 
 
+def _overlap_worker(rank, world, port, q):
+    """Two sessions per rank over the same batches: the in-step exchange
+    (each layer right after its wgrad, on a side stream) and the exchange after
+    the step. Weights must be bit-identical between the two modes and across
+    ranks after every step."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import hashlib
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_1602_08124_b200 as V
+        from oracle import numeric
+        from paper_1602_08124_b200.dist import PeerDataParallel
+        g = V.build_preset("inception_toy", 8)
+        cm = V.CostModel()
+        runs = {}
+        for overlap in (True, False):
+            s, w = _session(V, numeric, g, cm)
+            dp = PeerDataParallel(s, world, overlap=overlap)
+            digests, losses = [], []
+            for it in range(3):
+                images, labels = _batch(g, 300 + 10 * it + rank)
+                s.set_batch(images, labels)
+                losses.append(dp.step(LR, want_loss=True))
+                s.synchronize()
+                h = hashlib.sha256()
+                for k in sorted(w):
+                    h.update(s.get_weights(k).tobytes())
+                digests.append(h.hexdigest())
+            runs[overlap] = (digests, losses, dp.mode)
+            dp.close()
+            del s
+        all_d = [None] * world
+        dist.all_gather_object(all_d, runs[True][0])
+        q.put((rank, {"same_modes": runs[True][0] == runs[False][0], "same_ranks": all(d == all_d[0] for d in all_d),
+                      "losses_equal": runs[True][1] == runs[False][1], "mode": runs[True][2]}, None))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, None, repr(e)))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_peer_exchange_inside_the_step_is_bit_identical(world):
+    """SURVEY §8(e) placement at world 2, 4 and 8 (N processes sharing the
+    box's one device through CUDA IPC)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_overlap_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, rep, exc in res:
+        assert exc is None, (rank, exc)
+        assert rep["mode"] == "peer-overlap", rep
+        assert rep["same_modes"] and rep["same_ranks"] and rep["losses_equal"], (rank, rep)
+
+
 def _spill_worker(rank, world, port, q):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -143,7 +207,7 @@ def _spill_worker(rank, world, port, q):
         for k, v in w.items():
             s.set_weights(k, v)
         peer = ring_spill(s, world)
-        dp = PeerDataParallel(s, world)
+        dp = PeerDataParallel(s, world, overlap=False)
         s.set_batch(images, labels)
         s.step(LR, want_loss=False)
         s.synchronize()
@@ -196,7 +260,7 @@ def test_ring_spill_offload_multiprocess_same_device():
         assert peer == (rank + 1) % world and clean and same_grads and same_w, (rank, rep)
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_peer_exchange_multiprocess_same_device(world):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -237,8 +301,10 @@ def test_bench_two_ranks_same_device_peer_exchange():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0
-    assert line["config"]["gradient_exchange"] == "peer"
-    assert line["policies"]["dyn"]["dp_exchange"] == "peer"
+    assert line["config"]["gradient_exchange"] == "peer-overlap"
+    assert line["policies"]["dyn"]["dp_exchange"] == "peer-overlap"
+    census = line["rank_census"]
+    assert [c["rank"] for c in census] == [0, 1] and all(c["exchange"] == "peer-overlap" for c in census)
     # the same plan offloading into the ring neighbour's HBM
     assert line["policies"]["dynp"]["signature"] == line["policies"]["dyn"]["signature"]
     assert line["peer_hbm_offload"]["images_per_s"] > 0
