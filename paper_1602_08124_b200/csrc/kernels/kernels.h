@@ -135,6 +135,7 @@ struct PeerArgs {
   const PeerChunk* chunks = nullptr;               // this rank's share (device memory)
   int nchunks = 0;
   float step = 0.f;                                // lr * grad_scale
+  int bf16 = 0;                                    // weights stored as bf16 (elem_size 2); gradients fp32
 };
 cudaError_t peer_barrier(const PeerArgs& a, unsigned long long epoch, int phase, cudaStream_t st);
 cudaError_t peer_reduce_sgd(const PeerArgs& a, cudaStream_t st);

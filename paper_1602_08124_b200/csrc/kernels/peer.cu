@@ -20,6 +20,7 @@
 // rank's signal array with a system-scope release store and waits until all
 // N slots of its own array reach `epoch` (acquire loads). A wait that exceeds
 // 120 s traps instead of hanging the device.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -61,10 +62,52 @@ __global__ void peer_barrier_kernel(PeerArgs a, unsigned long long epoch, int ph
   }
 }
 
+// BF16 weights (elem_size 2): the same fp32 reduction in rank order, the
+// update computed in fp32 and rounded once (nearest even), 4 weights (8 B)
+// per access.
+template <int W>
+__device__ __forceinline__ void reduce_sgd_bf16(const PeerArgs& a, const PeerChunk& ch) {
+  const bool vec = (ch.g_off & 3) == 0 && (ch.w_off & 7) == 0;
+  const uint32_t nv = vec ? ch.count / 4 : 0;
+  for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
+    float4 s = reinterpret_cast<const float4*>(a.grads[0] + ch.g_off)[i];
+#pragma unroll
+    for (int p = 1; p < W; ++p) {
+      const float4 g = reinterpret_cast<const float4*>(a.grads[p] + ch.g_off)[i];
+      s.x += g.x;
+      s.y += g.y;
+      s.z += g.z;
+      s.w += g.w;
+    }
+    const uint2 wb = reinterpret_cast<const uint2*>(a.arena[a.rank] + ch.w_off)[i];
+    const float w0 = __uint_as_float(wb.x << 16), w1 = __uint_as_float(wb.x & 0xFFFF0000u);
+    const float w2 = __uint_as_float(wb.y << 16), w3 = __uint_as_float(wb.y & 0xFFFF0000u);
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(w0 - a.step * s.x, w1 - a.step * s.y);
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(w2 - a.step * s.z, w3 - a.step * s.w);
+    const uint2 out = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+#pragma unroll
+    for (int p = 0; p < W; ++p) reinterpret_cast<uint2*>(a.arena[p] + ch.w_off)[i] = out;
+  }
+  for (uint32_t i = nv * 4 + threadIdx.x; i < ch.count; i += blockDim.x) {
+    float s = a.grads[0][ch.g_off + i];
+#pragma unroll
+    for (int p = 1; p < W; ++p) s += a.grads[p][ch.g_off + i];
+    const __nv_bfloat16 w =
+        __float2bfloat16_rn(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.arena[a.rank] + ch.w_off)[i]) -
+                            a.step * s);
+#pragma unroll
+    for (int p = 0; p < W; ++p) reinterpret_cast<__nv_bfloat16*>(a.arena[p] + ch.w_off)[i] = w;
+  }
+}
+
 template <int W>
 __global__ void __launch_bounds__(256) peer_reduce_sgd_kernel(PeerArgs a) {
   for (int c = blockIdx.x; c < a.nchunks; c += gridDim.x) {
     const PeerChunk ch = a.chunks[c];
+    if (a.bf16) {
+      reduce_sgd_bf16<W>(a, ch);
+      continue;
+    }
     const bool vec = (ch.g_off & 3) == 0 && (ch.w_off & 15) == 0;  // both 16-B aligned
     const uint32_t nv = vec ? ch.count / 4 : 0;
     for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {

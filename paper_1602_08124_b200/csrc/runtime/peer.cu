@@ -41,7 +41,6 @@ Session::PeerHandle Session::peer_export() {
 void Session::peer_attach(int rank, int world, const PeerHandle* all) {
   if (world < 1 || world > vdnnk::kPeerMaxRanks || rank < 0 || rank >= world)
     throw PlanError(Err::Generic, "peer_attach: rank/world out of range (1..8 ranks)");
-  if (bf_) throw PlanError(Err::Config, "peer_attach: the fused peer exchange updates fp32 weights (elem_size 4)");
   if (!signal_) peer_export();  // allocates the signal words
   peer_detach();
   synchronize();
@@ -54,6 +53,7 @@ void Session::peer_attach(int rank, int world, const PeerHandle* all) {
   vdnnk::PeerArgs a{};
   a.world = world;
   a.rank = rank;
+  a.bf16 = bf_ ? 1 : 0;
   try {
     for (int p = 0; p < world; ++p) {
       if (p == rank) {
@@ -88,11 +88,11 @@ void Session::peer_attach(int rank, int world, const PeerHandle* all) {
     const size_t k = static_cast<size_t>(i);
     peer_first_[k] = static_cast<int>(mine.size());
     if (grad_off_[k] == kNoOff) continue;
-    const uint64_t n = df_.at[k].w_bytes / 4;
+    const uint64_t n = df_.at[k].w_bytes / es_;
     for (uint64_t s = 0; s < n; s += kChunk, ++j) {
       if (static_cast<int>(j % static_cast<uint64_t>(world)) != rank) continue;
       vdnnk::PeerChunk c{};
-      c.w_off = w_off_[k] + 4 * s;
+      c.w_off = w_off_[k] + es_ * s;
       c.g_off = grad_off_[k] + s;
       c.count = static_cast<uint32_t>(std::min<uint64_t>(kChunk, n - s));
       mine.push_back(c);

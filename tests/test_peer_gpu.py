@@ -46,13 +46,15 @@ def _batch(g, seed):
     return images, labels
 
 
-def test_peer_exchange_world1_equals_apply_grads():
+@pytest.mark.parametrize("es", [4, 2], ids=["fp32", "bf16"])
+def test_peer_exchange_world1_equals_apply_grads(es):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_1602_08124_b200 as V
     from oracle import numeric
     g = V.build_preset("inception_toy", 8)
     cm = V.CostModel()
+    cm.elem_size = es
     images, labels = _batch(g, 41)
     outs = []
     for peer in (False, True):
@@ -123,7 +125,7 @@ def _worker(rank, world, port, q):
         q.put((rank, None, repr(e)))
 
 
-def _overlap_worker(rank, world, port, q):
+def _overlap_worker(rank, world, port, q, es=4):
     """Two sessions per rank over the same batches: the in-step exchange
     (each layer right after its wgrad, on a side stream) and the exchange after
     the step. Weights must be bit-identical between the two modes and across
@@ -139,6 +141,7 @@ def _overlap_worker(rank, world, port, q):
         from paper_1602_08124_b200.dist import PeerDataParallel
         g = V.build_preset("inception_toy", 8)
         cm = V.CostModel()
+        cm.elem_size = es
         runs = {}
         for overlap in (True, False):
             s, w = _session(V, numeric, g, cm)
@@ -165,17 +168,17 @@ def _overlap_worker(rank, world, port, q):
         q.put((rank, None, repr(e)))
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_peer_exchange_inside_the_step_is_bit_identical(world):
+@pytest.mark.parametrize("world,es", [(2, 4), (4, 4), (8, 4), (2, 2)], ids=["w2", "w4", "w8", "w2-bf16"])
+def test_peer_exchange_inside_the_step_is_bit_identical(world, es):
     """SURVEY §8(e) placement at world 2, 4 and 8 (N processes sharing the
-    box's one device through CUDA IPC)."""
+    box's one device through CUDA IPC); bf16 weights (elem_size 2) too."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_overlap_worker, args=(r, world, port, q)) for r in range(world)]
+    ps = [ctx.Process(target=_overlap_worker, args=(r, world, port, q, es)) for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=600) for _ in range(world)]
