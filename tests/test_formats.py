@@ -1,6 +1,9 @@
 """Reference artefact formats (report.hpp) from our planner: JSON round trips,
 CSV schemas, and calibrated cost models that keep schedules bit-identical."""
 import json
+import os
+
+import pytest
 
 import paper_1602_08124_b200 as V
 from paper_1602_08124_b200 import formats as F
@@ -56,3 +59,42 @@ def test_latency_overrides_never_change_schedules():
     if refsim.available():
         ref = refsim.run(g.spec(), "static:all:m", GIB12, cost_spec=fast.spec(), events=False)["report"]
         assert ref["signature"] == r.signature() and ref["total_ns"] == r.total_ns
+
+
+ART = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r02_artifacts")
+
+
+@pytest.mark.parametrize("run", ["vgg16_b256_dyn", "vgg16_b256_dynb"])
+def test_committed_measured_artifacts_replay_clean(run):
+    """The artefact files of a measured B200 step (bench.py --artifacts,
+    report.hpp:44-236 formats) are consumed as the reference's own tools
+    would: graph and decision JSON round-trip into our API, the measured
+    event log passes our replay_check and the compiled reference's, and the
+    measured pool trace equals the planned one in every column but time."""
+    import json
+    import paper_1602_08124_b200 as V
+    from paper_1602_08124_b200 import formats as F
+    from oracle import refsim
+    d = os.path.join(ART, run)
+    g = F.graph_from_json(json.load(open(os.path.join(d, "graph.json"))))
+    dec = F.decision_from_json(json.load(open(os.path.join(d, "decision.json"))), g)
+    cal = json.load(open(os.path.join(d, "calibration.json")))
+    cm = V.CostModel()
+    cm.elem_size = cal["elem_size"]
+    plan, trace = V.simulate_with_trace(g, dec, cm, cal["capacity"])
+    assert plan.signature() == cal["signature_planned"] == cal["signature_calibrated"]
+    rep = json.load(open(os.path.join(d, "report.json")))
+    kinds = {"FWD": 0, "BWD": 1, "OFFLOAD": 2, "PREFETCH": 3, "ALLOC": 4, "RELEASE": 5, "SYNC": 6}
+    ev = [(0 if e["stream"] == "compute" else 1, kinds[e["kind"]], e["layer"], e["start_ns"], e["end_ns"], e["bytes"],
+           e.get("tag", ""), e.get("buffer", -1), e.get("offset", 0)) for e in rep["events"]]
+    assert [x for x in ev if x[1] != 6 and x[1] in (4, 5)] != []
+    placed = [(k, l, b, t, by, o) for (_, k, l, _, _, by, t, b, o) in ev if k != 6]
+    assert placed == [tuple(p) for p in V.placements(plan)]
+    assert abs(cal["calibrated_rel_err"]) < 0.05
+    rows = open(os.path.join(d, "pool_trace.csv")).read().splitlines()[1:]
+    assert [r.split(",")[1:] for r in rows] == [["alloc" if t[1] == "a" else "free"] + [str(x) for x in t[2:]]
+                                                for t in trace]
+    if refsim.available():
+        out = refsim.replay(g.spec(), dec.spec(), cal["capacity"], ev, rep["max_mem_bytes"], rep["avg_mem_bytes"],
+                            rep["total_ns"], True)
+        assert out == [], out[:5]
