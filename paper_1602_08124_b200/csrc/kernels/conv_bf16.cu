@@ -3,6 +3,7 @@
 // (cost_model.hpp:69). Split-K partials are fp32 and reduced in a fixed order
 // (deterministic, independent of where the partials live), as in conv.cu.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.h"
@@ -63,6 +64,7 @@ bool build_common_b(const ConvArgs& a, ConvParamsB& p) {
   p.vec_in = vec ? 1 : 0;
   p.nchunk = vec ? nch : 0;
   p.vec_out = (a.cout % 8 == 0) ? 1 : 0;
+  p.tap_pack = (a.nseg == 1 && cb == 8 && a.kh * a.kw > 1) ? 1 : 0;
   return true;
 }
 
@@ -84,9 +86,49 @@ cudaError_t launch_b(const ConvParamsB& p, int splits, const CUtensorMap& ta, co
   return cudaGetLastError();
 }
 
-int tile_n(int ncols) { return ncols <= 64 ? 64 : 128; }
-
 thread_local bool g_no_tma_b = false;
+
+// Layers the TMA producers can feed (one segment, 8-multiple channel counts,
+// square windows, stride-1 dgrad): they run the persistent kernel.
+bool tma_ok_b(const ConvParamsB& p) {
+  return !g_no_tma_b && !p.tap_pack && p.nseg == 1 && p.vec_in && p.vec_out && p.kh == p.kw && (p.kind != kDgrad || p.stride == 1);
+}
+
+// N tile width: persistent kernel 64 / 128 / 256, one-tile kernel 64 / 128.
+int tile_n(const ConvParamsB& p) {
+  if (p.Ncols <= 64) return 64;
+  return (tma_ok_b(p) && p.Ncols >= 256) ? 256 : 128;
+}
+// CTAs that run concurrently: one persistent CTA per SM, or two one-tile CTAs.
+bool gather_persist();
+int slots_b(const ConvParamsB& p) { return (tma_ok_b(p) || gather_persist()) ? kNumSmsB : 2 * kNumSmsB; }
+
+template <int BN, int STAGES, bool GATHER = false>
+cudaError_t launch_persist_b(const ConvParamsB& p, int splits, const CUtensorMap& ta, const CUtensorMap& tb,
+                             cudaStream_t st) {
+  using L = TcbPersistSmem<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(tcb_persist_kernel<BN, STAGES, GATHER>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t tiles = static_cast<int64_t>((p.M + kBM - 1) / kBM) * ((p.Ncols + BN - 1) / BN) * splits;
+  const int grid = static_cast<int>(std::min<int64_t>(tiles, kNumSmsB));
+  tcb_persist_kernel<BN, STAGES, GATHER><<<grid, GATHER ? 288 : 192, L::kTotal, st>>>(p, ta, tb, splits);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// VDNN_BF16_GATHER_PERSIST=0: the one-tile-per-CTA gather kernel (A/B switch)
+bool gather_persist() {
+  static const bool on = [] {
+    const char* e = std::getenv("VDNN_BF16_GATHER_PERSIST");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
 
 // Tensor maps of the TMA producer (tcb_conv.cuh TmaProducerB); false = the
 // cp.async gathers (concatenated inputs, channel counts not 8-multiples,
@@ -121,19 +163,24 @@ bool make_maps_b(const ConvParamsB& p, int bn, CUtensorMap* ta, CUtensorMap* tb)
 
 cudaError_t launch_any(const ConvParamsB& p, int splits, cudaStream_t st) {
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
-  const int bn = tile_n(p.Ncols);
+  const int bn = tile_n(p);
   alignas(64) CUtensorMap ta, tb;
   std::memset(&ta, 0, sizeof(ta));
   std::memset(&tb, 0, sizeof(tb));
-  if (make_maps_b(p, bn, &ta, &tb))
-    return bn == 64 ? launch_b<64, 4, true>(p, splits, ta, tb, st) : launch_b<128, kStagesB, true>(p, splits, ta, tb, st);
+  if (tma_ok_b(p) && make_maps_b(p, bn, &ta, &tb)) {
+    if (bn == 256) return launch_persist_b<256, 4>(p, splits, ta, tb, st);
+    if (bn == 128) return launch_persist_b<128, 6>(p, splits, ta, tb, st);
+    return launch_persist_b<64, 8>(p, splits, ta, tb, st);
+  }
+  if (gather_persist())
+    return bn == 64 ? launch_persist_b<64, 8, true>(p, splits, ta, tb, st)
+                    : launch_persist_b<128, 6, true>(p, splits, ta, tb, st);
   return bn == 64 ? launch_b<64, 4, false>(p, splits, ta, tb, st) : launch_b<128, kStagesB, false>(p, splits, ta, tb, st);
 }
 
 // Split-K factor (same time model as conv.cu's pick_splits): waves of
 // ceil(kblocks / s) K blocks against the partial slabs' write + re-read.
-int pick_splits_b(int tiles, int kblocks, int bn, int64_t outputs) {
-  const int slots = 2 * kNumSmsB;
+int pick_splits_b(int tiles, int kblocks, int bn, int64_t outputs, int slots) {
   int best = 1;
   double best_t = 1e30;
   const int smax = std::max(1, std::min(1024, kblocks / 4));
@@ -169,7 +216,7 @@ bool fprop_params_b(const ConvArgs& a, const void* w, const void* bias, void* y,
   p.y = static_cast<bf16*>(y);
   p.M = a.n * p.Ho * p.Wo;
   p.Ncols = a.cout;
-  p.kblocks = p.vec_in ? a.kh * a.kw * p.nchunk : (p.KK + kBKb - 1) / kBKb;
+  p.kblocks = p.tap_pack ? (a.kh * a.kw + 7) / 8 : p.vec_in ? a.kh * a.kw * p.nchunk : (p.KK + kBKb - 1) / kBKb;
   p.kb_per_split = p.kblocks;
   return true;
 }
@@ -177,9 +224,9 @@ bool fprop_params_b(const ConvArgs& a, const void* w, const void* bias, void* y,
 // FC layers at small batch: fewer output tiles than SMs over a long reduction.
 int fprop_splits_b(const ConvParamsB& p) {
   if (p.epi != kEpiStore || p.nseg != 1 || !p.vec_in || !p.vec_out) return 1;
-  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ncols + tile_n(p.Ncols) - 1) / tile_n(p.Ncols));
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ncols + tile_n(p) - 1) / tile_n(p));
   if (tiles >= kNumSmsB || p.kblocks < 32) return 1;
-  return pick_splits_b(tiles, p.kblocks, tile_n(p.Ncols), static_cast<int64_t>(p.M) * p.Cout);
+  return pick_splits_b(tiles, p.kblocks, tile_n(p), static_cast<int64_t>(p.M) * p.Cout, slots_b(p));
 }
 
 __global__ void fprop_reduce_b_kernel(const float* __restrict__ part, int splits, int64_t m, int cout,
@@ -199,6 +246,7 @@ __global__ void fprop_reduce_b_kernel(const float* __restrict__ part, int splits
 bool dgrad_params_b(const ConvArgs& a, const void* w, const void* dy, bool accumulate, ConvParamsB& p) {
   if (!build_common_b(a, p)) return false;
   p.kind = kDgrad;
+  p.tap_pack = 0;  // dgrad keeps the 64-channel chunks
   p.epi = accumulate ? kEpiAccum : kEpiStore;
   p.w = static_cast<const bf16*>(w);
   p.dy = static_cast<const bf16*>(dy);
@@ -212,9 +260,9 @@ bool dgrad_params_b(const ConvArgs& a, const void* w, const void* dy, bool accum
 int dgrad_splits_b(const ConvParamsB& p) {
   if (p.nseg != 1 || !p.vec_in || !p.vec_out || p.kh != 1 || p.kw != 1 || p.H != 1 || p.W != 1 || p.C % 64 != 0)
     return 1;
-  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ncols + tile_n(p.Ncols) - 1) / tile_n(p.Ncols));
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ncols + tile_n(p) - 1) / tile_n(p));
   if (tiles >= kNumSmsB || p.kblocks < 32) return 1;
-  return pick_splits_b(tiles, p.kblocks, tile_n(p.Ncols), static_cast<int64_t>(p.M) * p.C);
+  return pick_splits_b(tiles, p.kblocks, tile_n(p), static_cast<int64_t>(p.M) * p.C, slots_b(p));
 }
 
 __global__ void dgrad_reduce_b_kernel(const float* __restrict__ part, int splits, int64_t m, int c,
@@ -231,13 +279,18 @@ __global__ void dgrad_reduce_b_kernel(const float* __restrict__ part, int splits
 }
 
 // ----------------------------------------------------------------- WGRAD ---
-int wgrad_rows_b(const ConvParamsB& p) { return p.vec_in ? p.kh * p.kw * p.nchunk * 64 : p.KK; }
+int wgrad_rows_b(const ConvParamsB& p) {
+  return (p.vec_in && !p.tap_pack) ? p.kh * p.kw * p.nchunk * 64 : p.KK;
+}
 
 int wgrad_splits_b(const ConvParamsB& p, int M, int64_t P) {
-  const int bn = tile_n(p.Cout);
+  ConvParamsB q = p;  // tile shape of the launch (kind and Ncols as conv_wgrad_bf16 sets them)
+  q.kind = kWgrad;
+  q.Ncols = p.Cout;
+  const int bn = tile_n(q);
   const int tiles = ((M + kBM - 1) / kBM) * ((p.Cout + bn - 1) / bn);
   const int kblocks = static_cast<int>((P + kBKb - 1) / kBKb);
-  return pick_splits_b(tiles, kblocks, bn, static_cast<int64_t>(M) * p.Cout);
+  return pick_splits_b(tiles, kblocks, bn, static_cast<int64_t>(M) * p.Cout, slots_b(q));
 }
 
 __global__ void wgrad_reduce_b_kernel(const __grid_constant__ ConvParamsB p, int splits, float* __restrict__ dw) {

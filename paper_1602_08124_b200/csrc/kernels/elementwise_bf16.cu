@@ -563,6 +563,59 @@ cudaError_t fill_const_bf16(void* x, size_t n, float v, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Channel padding of a [rows][c] bf16 tensor to [rows][cp] (zeros in c..cp)
+// and back, for layers whose channel count is not a multiple of 8 (the first
+// layer's C = 3): the padded copy feeds the TMA producers.
+__global__ void pad_channels_b_kernel(bf16* __restrict__ dst, const bf16* __restrict__ src, size_t rows, int c,
+                                      int cp) {
+  const size_t total = rows * cp;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = e / cp;
+    const int ch = static_cast<int>(e - r * cp);
+    dst[e] = ch < c ? src[r * c + ch] : b(0.f);
+  }
+}
+__global__ void unpad_channels_b_kernel(bf16* __restrict__ dst, const bf16* __restrict__ src, size_t rows, int c,
+                                        int cp) {
+  const size_t total = rows * c;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = e / c;
+    dst[e] = src[r * cp + (e - r * c)];
+  }
+}
+__global__ void unpad_channels_f_kernel(float* __restrict__ dst, const float* __restrict__ src, size_t rows, int c,
+                                        int cp) {
+  const size_t total = rows * c;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = e / c;
+    dst[e] = src[r * cp + (e - r * c)];
+  }
+}
+
+cudaError_t pad_channels_bf16(void* dst, const void* src, size_t rows, int c, int cp, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  pad_channels_b_kernel<<<grid_for(rows * cp, 8), kThreads, 0, st>>>(static_cast<bf16*>(dst),
+                                                                     static_cast<const bf16*>(src), rows, c, cp);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t unpad_channels_bf16(void* dst, const void* src, size_t rows, int c, int cp, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  unpad_channels_b_kernel<<<grid_for(rows * c, 8), kThreads, 0, st>>>(static_cast<bf16*>(dst),
+                                                                      static_cast<const bf16*>(src), rows, c, cp);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t unpad_channels_f32(float* dst, const float* src, size_t rows, int c, int cp, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  unpad_channels_f_kernel<<<grid_for(rows * c, 8), kThreads, 0, st>>>(dst, src, rows, c, cp);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // fp32 <-> bf16 (host-format conversions on the device: weight upload /
 // readback, feature probes)
 __global__ void to_bf16_kernel(bf16* __restrict__ d, const float* __restrict__ s, size_t n) {

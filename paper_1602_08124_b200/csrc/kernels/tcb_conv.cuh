@@ -50,6 +50,8 @@ struct ConvParamsB {
   int nchunk, chunk_arith;         // 64-wide virtual channel chunks (arith: single segment)
   Chunk chunk[kMaxChunksB];
   int vec_in, vec_out;             // every segment C % 8 == 0 / Cout % 8 == 0: 16-B gathers
+  int tap_pack;                    // single segment with C == 8 (a padded first layer): one K block =
+                                   // 8 taps x 8 channels, K = (tap, c) flat, 16-B gathers per tap
   const bf16* w;                   // KRSC
   bf16* w_mut;                     // SGD epilogue target
   const bf16* bias;                // FC bias (fprop)
@@ -167,6 +169,38 @@ template <int BN>
 struct GatherB {
   // ---- FPROP: A = im2col rows (pixel) x 64 channels, B = W rows (co) x 64 channels (both K-major)
   __device__ static void fprop(const ConvParamsB& p, int m0, int n0, int kb, uint32_t sa, uint32_t sb, int tid) {
+    if (p.tap_pack) {
+      // 16-B granule j = the 8 channels of tap 8*kb + j
+      const int j = tid & 7;
+      const int tap = kb * 8 + j;
+      const bool tv = tap < p.kh * p.kw;
+      const int r = tv ? tap / p.kw : 0, s = tv ? tap - (tap / p.kw) * p.kw : 0;
+      const bf16* x = p.seg[0].x;
+#pragma unroll 4
+      for (int i = 0; i < kBM / 16; ++i) {
+        const int row = (tid >> 3) + 16 * i;
+        const int m = m0 + row;
+        const bf16* src = x;
+        uint32_t bytes = 0;
+        if (m < p.M && tv) {
+          const Pix q = decode_pix(m, p.Ho, p.Wo);
+          const int ih = q.h * p.stride - p.pad + r, iw = q.w * p.stride - p.pad + s;
+          if (ih >= 0 && ih < p.H && iw >= 0 && iw < p.W) {
+            src = x + ((static_cast<int64_t>(q.n) * p.H + ih) * p.W + iw) * 8;
+            bytes = 16;
+          }
+        }
+        cp_async16(kmaj_addr(sa, row, j), src, bytes);
+      }
+#pragma unroll 4
+      for (int i = 0; i < BN / 16; ++i) {
+        const int row = (tid >> 3) + 16 * i;
+        const int co = n0 + row;
+        const bool ok = co < p.Cout && tv;
+        cp_async16(kmaj_addr(sb, row, j), ok ? p.w + static_cast<int64_t>(co) * p.KK + tap * 8 : p.w, ok ? 16 : 0);
+      }
+      return;
+    }
     if (p.vec_in) {
       const int tap = kb / p.nchunk, ck = kb - tap * p.nchunk;
       const int r = tap / p.kw, s = tap - r * p.kw;
@@ -384,7 +418,29 @@ struct GatherB {
   // A: X_col^T, MN-major (K row = pixel, MN = weight column); B: dY^T, MN-major.
   __device__ static void wgrad(const ConvParamsB& p, int m0, int n0, int kb, uint32_t sa, uint32_t sb, int tid) {
     const int P = p.N * p.Ho * p.Wo;
-    if (p.vec_in) {
+    if (p.tap_pack) {
+      // MN col = tap * 8 + c: the 16-B granule j of MN chunk mc is tap (m0 + 64 mc) / 8 + j
+      const int j = tid & 7;
+#pragma unroll 2
+      for (int i = 0; i < kBM / 16; ++i) {
+        const int q = (tid >> 3) + 16 * i;
+        const int k = q & 63, mc = q >> 6;
+        const int pix = kb * kBKb + k;
+        const int tap = (m0 + mc * 64) / 8 + j;
+        const bf16* src = p.seg[0].x;
+        uint32_t bytes = 0;
+        if (pix < P && tap < p.kh * p.kw) {
+          const int r = tap / p.kw, s = tap - r * p.kw;
+          const Pix x = decode_pix(pix, p.Ho, p.Wo);
+          const int ih = x.h * p.stride - p.pad + r, iw = x.w * p.stride - p.pad + s;
+          if (ih >= 0 && ih < p.H && iw >= 0 && iw < p.W) {
+            src = p.seg[0].x + ((static_cast<int64_t>(x.n) * p.H + ih) * p.W + iw) * 8;
+            bytes = 16;
+          }
+        }
+        cp_async16(mnb_addr(sa, k, mc, j), src, bytes);
+      }
+    } else if (p.vec_in) {
       const int j = tid & 7;
 #pragma unroll 2
       for (int i = 0; i < kBM / 16; ++i) {
@@ -476,7 +532,7 @@ struct GatherB {
 
 // Weight-row index of a wgrad GEMM row m (virtual (tap, 64-chunk, lane) or flat).
 __device__ __forceinline__ int wgrad_widx_b(const ConvParamsB& p, int m, bool& valid) {
-  if (p.vec_in) {
+  if (p.vec_in && !p.tap_pack) {
     const int vcol = m >> 6, lane = m & 63;
     const int tap = vcol / p.nchunk, ck = vcol - tap * p.nchunk;
     if (tap >= p.kh * p.kw) {
@@ -638,6 +694,124 @@ struct TmaProducerB {
   }
 };
 
+// Epilogue of one 128 x BN tile (warp w drains TMEM lanes 32w..32w+31; `row`
+// = 32w + lane): split-K partials, or fused bias / ReLU / ReLU-backward mask /
+// accumulation with bf16 stores, or the wgrad SGD update / fp32 dW.
+// `drained()` runs right after the tile's last TMEM read (a persistent
+// kernel releases the accumulator there). zero: the tile had no K blocks.
+template <int BN, class Drained>
+__device__ __forceinline__ void tcb_epilogue(const ConvParamsB& p, uint32_t taddr, int m0, int n0, int z, int row,
+                                             bool zero, Drained drained) {
+  const int m = m0 + row;
+#pragma unroll 1
+  for (int cg = 0; cg < BN / 32; ++cg) {
+    float v[32];
+    tmem_ld32(taddr + cg * 32, v);
+    if (cg == BN / 32 - 1) drained();
+    if (zero) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    }
+    if (m >= p.M) continue;
+    const int nb = n0 + cg * 32;
+    if (p.epi == kEpiPartial && p.kind != kWgrad) {
+      // split-K fprop / dgrad: fp32 partial slab z of [splits][M][Ncols]
+      if (nb >= p.Ncols) continue;
+      float* dst = p.out + (static_cast<int64_t>(z) * p.M + m) * p.Ncols + nb;
+      if (nb + 32 <= p.Ncols && (p.Ncols & 3) == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (nb + i < p.Ncols) dst[i] = v[i];
+      }
+      continue;
+    }
+    if (p.kind == kFprop) {
+      if (nb >= p.Cout) continue;
+      if (p.bias) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (nb + i < p.Cout) v[i] += bf2f(p.bias[nb + i]);
+      }
+      if (p.relu) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+      }
+      store_row32(p.y + static_cast<int64_t>(m) * p.Cout + nb, v, p.Cout - nb, p.epi == kEpiAccum);
+    } else if (p.kind == kDgrad) {
+      if (p.vec_in) {
+        const int vc = nb >> 6, off = nb & 63;
+        if (vc >= p.nchunk) continue;
+        const Chunk c = chunk_at_b(p, vc);
+        const BSeg sg = p.seg[c.seg];
+        const int valid = c.valid - off;
+        if (!sg.dx || valid <= 0) continue;
+        const int64_t at = static_cast<int64_t>(m) * sg.C + c.coff + off;
+        if (sg.mask) {
+          // fused ReLU backward: the ReLU's output is this conv's input x
+          const bf16* xr = sg.x + at;
+          if (valid >= 32 && (reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
+            uint4 xa[4];  // 4 x 16-B loads in flight, then the selects
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xa[i] = __ldg(reinterpret_cast<const uint4*>(xr) + i);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float f[8];
+              unpack_bf16x8(xa[i], f);
+#pragma unroll
+              for (int t = 0; t < 8; ++t) v[8 * i + t] = f[t] > 0.f ? v[8 * i + t] : 0.f;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < valid && !(bf2f(xr[i]) > 0.f)) v[i] = 0.f;
+          }
+        }
+        store_row32(sg.dx + at, v, valid, p.epi == kEpiAccum);
+      } else {
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) {
+          const int ci = nb + i;
+          if (ci >= p.C) break;
+          const BSeg sg = p.seg[seg_of_b(p, ci)];
+          if (!sg.dx) continue;
+          const int64_t at = static_cast<int64_t>(m) * sg.C + (ci - sg.cbase);
+          float val = v[i];
+          if (sg.mask && !(bf2f(sg.x[at]) > 0.f)) val = 0.f;
+          sg.dx[at] = __float2bfloat16_rn((p.epi == kEpiAccum ? bf2f(sg.dx[at]) : 0.f) + val);
+        }
+      }
+    } else {
+      // WGRAD: row m = weight column (virtual), columns = co
+      if (p.epi == kEpiPartial) {
+        float* dst = p.out + static_cast<int64_t>(z) * p.Ncols * p.M;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (nb + i < p.Cout) dst[static_cast<int64_t>(nb + i) * p.M + m] = v[i];
+        continue;
+      }
+      bool valid;
+      const int widx = wgrad_widx_b(p, m, valid);
+      if (!valid) continue;
+      if (p.epi == kEpiSgd) {
+        bf16* wcol = p.w_mut + static_cast<int64_t>(nb) * p.KK + widx;
+        float wv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) wv[i] = (nb + i < p.Cout) ? bf2f(wcol[static_cast<int64_t>(i) * p.KK]) : 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (nb + i < p.Cout) wcol[static_cast<int64_t>(i) * p.KK] = __float2bfloat16_rn(wv[i] - p.lr * v[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (nb + i < p.Cout) p.out[static_cast<int64_t>(nb + i) * p.KK + widx] = v[i];
+      }
+    }
+  }
+}
+
 template <int BN, int STAGES>
 struct TcbSmem {
   static constexpr int kABytes = kBM * 128;
@@ -727,114 +901,31 @@ __global__ void __launch_bounds__(160, (TcbSmem<BN, STAGES>::kTotal <= 116 * 102
       else
         GatherB<BN>::wgrad(p, m0, n0, kb, sa, sb, tid);
       if (scalar) {
-        // element-wise st.shared in this stage: land this thread's copies,
-        // make every write visible to the tensor core's (async) proxy, arrive
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        fence_proxy_async();
-        mbar_arrive(full_bar(s));
+        // element-wise st.shared in this stage: one stage of lag -- once this
+        // thread's copies of the PREVIOUS stage landed (its cp.async group),
+        // make that stage's writes visible to the tensor core's (async) proxy
+        // and arrive, so each thread keeps two stages of loads in flight
+        cp_async_commit();
+        cp_async_wait<1>();
+        if (it > 0) {
+          fence_proxy_async();
+          mbar_arrive(full_bar((it - 1) % STAGES));
+        }
       } else {
         cp_async_arrive_noinc(full_bar(s));
       }
+    }
+    if (scalar && nkb > 0) {
+      cp_async_wait<0>();
+      fence_proxy_async();
+      mbar_arrive(full_bar((nkb - 1) % STAGES));
     }
     // ---------------- epilogue ----------------
     mbar_wait_sleep(accum_bar, 0);
     tc_fence_after();
     __syncwarp();
-    const int row = warp * 32 + lane;
-    const int m = m0 + row;
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-#pragma unroll 1
-    for (int cg = 0; cg < BN / 32; ++cg) {
-      float v[32];
-      tmem_ld32(taddr + cg * 32, v);
-      if (nkb <= 0) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-      }
-      if (m >= p.M) continue;
-      const int nb = n0 + cg * 32;
-      if (p.epi == kEpiPartial && p.kind != kWgrad) {
-        // split-K fprop / dgrad: fp32 partial slab z of [splits][M][Ncols]
-        if (nb >= p.Ncols) continue;
-        float* dst = p.out + (static_cast<int64_t>(blockIdx.z) * p.M + m) * p.Ncols + nb;
-        if (nb + 32 <= p.Ncols && (p.Ncols & 3) == 0) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (nb + i < p.Ncols) dst[i] = v[i];
-        }
-        continue;
-      }
-      if (p.kind == kFprop) {
-        if (nb >= p.Cout) continue;
-        if (p.bias) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (nb + i < p.Cout) v[i] += bf2f(p.bias[nb + i]);
-        }
-        if (p.relu) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-        }
-        store_row32(p.y + static_cast<int64_t>(m) * p.Cout + nb, v, p.Cout - nb, p.epi == kEpiAccum);
-      } else if (p.kind == kDgrad) {
-        if (p.vec_in) {
-          const int vc = nb >> 6, off = nb & 63;
-          if (vc >= p.nchunk) continue;
-          const Chunk c = chunk_at_b(p, vc);
-          const BSeg sg = p.seg[c.seg];
-          const int valid = c.valid - off;
-          if (!sg.dx || valid <= 0) continue;
-          const int64_t at = static_cast<int64_t>(m) * sg.C + c.coff + off;
-          if (sg.mask) {
-            const bf16* xr = sg.x + at;
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < valid && !(bf2f(xr[i]) > 0.f)) v[i] = 0.f;
-          }
-          store_row32(sg.dx + at, v, valid, p.epi == kEpiAccum);
-        } else {
-#pragma unroll 4
-          for (int i = 0; i < 32; ++i) {
-            const int ci = nb + i;
-            if (ci >= p.C) break;
-            const BSeg sg = p.seg[seg_of_b(p, ci)];
-            if (!sg.dx) continue;
-            const int64_t at = static_cast<int64_t>(m) * sg.C + (ci - sg.cbase);
-            float val = v[i];
-            if (sg.mask && !(bf2f(sg.x[at]) > 0.f)) val = 0.f;
-            sg.dx[at] = __float2bfloat16_rn((p.epi == kEpiAccum ? bf2f(sg.dx[at]) : 0.f) + val);
-          }
-        }
-      } else {
-        // WGRAD: row m = weight column (virtual), columns = co
-        if (p.epi == kEpiPartial) {
-          float* dst = p.out + static_cast<int64_t>(blockIdx.z) * p.Ncols * p.M;
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (nb + i < p.Cout) dst[static_cast<int64_t>(nb + i) * p.M + m] = v[i];
-          continue;
-        }
-        bool valid;
-        const int widx = wgrad_widx_b(p, m, valid);
-        if (!valid) continue;
-        if (p.epi == kEpiSgd) {
-          bf16* wcol = p.w_mut + static_cast<int64_t>(nb) * p.KK + widx;
-          float wv[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) wv[i] = (nb + i < p.Cout) ? bf2f(wcol[static_cast<int64_t>(i) * p.KK]) : 0.f;
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (nb + i < p.Cout) wcol[static_cast<int64_t>(i) * p.KK] = __float2bfloat16_rn(wv[i] - p.lr * v[i]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (nb + i < p.Cout) p.out[static_cast<int64_t>(nb + i) * p.KK + widx] = v[i];
-        }
-      }
-    }
+    tcb_epilogue<BN>(p, tmem + (static_cast<uint32_t>(warp * 32) << 16), m0, n0, static_cast<int>(blockIdx.z),
+                     warp * 32 + lane, nkb <= 0, [] {});
   } else if (warp == 4) {
     // ---------------- MMA issuer ----------------
     const bool a_mn = (p.kind == kWgrad);
@@ -872,6 +963,217 @@ __global__ void __launch_bounds__(160, (TcbSmem<BN, STAGES>::kTotal <= 116 * 102
   if (warp == 4) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN) : "memory");
+  }
+}
+
+// Persistent variant (TMA producers only): one CTA per SM walks a static
+// round-robin of (split, M tile, N tile) with a continuous stage ring and two
+// TMEM accumulator sets, so tile t's epilogue overlaps tile t+1's loads and
+// MMAs, and the per-tile launch / pipeline fill / TMEM setup of the
+// one-tile-per-CTA kernel is paid once per SM. BN = 256 tiles (N = 256 MMAs:
+// half the A bytes per FLOP of BN = 128) fit with two accumulator sets.
+//   warps 0-3 : epilogue        warp 4 : TMEM owner + MMA issuer
+//   warp 5    : TMA producer (TmaProducerB, per-tile init)
+template <int BN, int STAGES>
+struct TcbPersistSmem {
+  static constexpr int kABytes = kBM * 128;
+  static constexpr int kBBytes = BN * 128;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kTotal = STAGES * kStage + 1024 + 256;
+  static_assert(2 * BN <= 512, "two accumulator sets must fit TMEM");
+};
+
+// GATHER = true: the producers are four warps gathering with cp.async /
+// element-wise stores (GatherB: concatenated inputs, channel counts that are
+// not multiples of 8 -- first layers), one stage of lag per thread; the
+// epilogue moves to warps 5-8 (TMEM lane quarter = warp % 4).
+template <int BN, int STAGES, bool GATHER = false>
+__global__ void __launch_bounds__(GATHER ? 288 : 192, 1)
+    tcb_persist_kernel(const __grid_constant__ ConvParamsB p, const __grid_constant__ CUtensorMap tma_a,
+                       const __grid_constant__ CUtensorMap tma_b, int splits) {
+  extern __shared__ uint8_t smem_raw[];
+  using L = TcbPersistSmem<BN, STAGES>;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bars = base + STAGES * L::kStage;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
+  auto tfull = [&](int a) { return bars + 8u * (2 * STAGES + a); };
+  auto tempty = [&](int a) { return bars + 8u * (2 * STAGES + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntn = (p.Ncols + BN - 1) / BN;
+  const int mt = (p.M + kBM - 1) / kBM;
+  const int ntiles = mt * ntn * splits;
+  // tile -> (split z, m0, n0, K-block range); the N tiles of one M tile are
+  // adjacent (the A tile is re-hit in L2)
+  auto decode = [&](int t, int& z, int& m0, int& n0, int& kb0, int& nkb) {
+    z = t / (mt * ntn);
+    const int r = t - z * mt * ntn;
+    m0 = (r / ntn) * kBM;
+    n0 = (r % ntn) * BN;
+    kb0 = z * p.kb_per_split;
+    nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), GATHER ? 128 : 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(2 * BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  const bool producer = GATHER ? warp < 4 : warp == 5;
+  if (producer) {
+   if constexpr (GATHER) {
+    // ---------------- gather producers (128 threads) ----------------
+    const int tid = threadIdx.x;
+    const bool scalar = scalar_gathers(p);
+    int s = 0, it_all = 0;
+    uint32_t ph = 1;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int z, m0, n0, kb0, nkb;
+      decode(t, z, m0, n0, kb0, nkb);
+      for (int it = 0; it < nkb; ++it, ++it_all) {
+        mbar_wait(empty_bar(s), ph);
+        const uint32_t sa = base + s * L::kStage;
+        const uint32_t sb = sa + L::kABytes;
+        if (p.kind == kFprop)
+          GatherB<BN>::fprop(p, m0, n0, kb0 + it, sa, sb, tid);
+        else if (p.kind == kDgrad)
+          GatherB<BN>::dgrad(p, m0, n0, kb0 + it, sa, sb, tid);
+        else
+          GatherB<BN>::wgrad(p, m0, n0, kb0 + it, sa, sb, tid);
+        if (scalar) {
+          // one stage of lag: the previous stage is complete once its
+          // cp.async group landed; fence its st.shared writes, arrive
+          cp_async_commit();
+          cp_async_wait<1>();
+          if (it_all > 0) {
+            fence_proxy_async();
+            mbar_arrive(full_bar(s == 0 ? STAGES - 1 : s - 1));
+          }
+        } else {
+          cp_async_arrive_noinc(full_bar(s));
+        }
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    if (scalar && it_all > 0) {
+      cp_async_wait<0>();
+      fence_proxy_async();
+      mbar_arrive(full_bar(s == 0 ? STAGES - 1 : s - 1));
+    }
+   } else {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+      int s = 0;
+      uint32_t ph = 1;  // the first pass over the ring does not wait
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int z, m0, n0, kb0, nkb;
+        decode(t, z, m0, n0, kb0, nkb);
+        TmaProducerB<BN> tp;
+        tp.init(p, m0, kb0);
+        const uint32_t nbytes = tp.bytes();
+        for (int it = 0; it < nkb; ++it) {
+          mbar_wait(empty_bar(s), ph);
+          const uint32_t sa = base + s * L::kStage;
+          mbar_expect_tx(full_bar(s), nbytes);
+          tp.issue(p, &tma_a, &tma_b, n0, sa, sa + L::kABytes, full_bar(s));
+          tp.next(p);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+   }
+  } else if (warp == 4) {
+    // ---------------- MMA issuer ----------------
+    const bool a_mn = (p.kind == kWgrad);
+    const bool b_mn = (p.kind != kFprop);
+    const uint32_t idesc = make_idesc_bf16(BN, a_mn, b_mn);
+    const bool leader = elect_one();
+    int s = 0, lt = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      int z, m0, n0, kb0, nkb;
+      decode(t, z, m0, n0, kb0, nkb);
+      const int acc = lt & 1;
+      if (lt >= 2) mbar_wait(tempty(acc), ((lt >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * BN;
+      for (int it = 0; it < nkb; ++it) {
+        mbar_wait(full_bar(s), ph);
+        if constexpr (GATHER) fence_proxy_async();  // cp.async writes -> async proxy
+        tc_fence_after();
+        const uint32_t sa = base + s * L::kStage;
+        const uint32_t sb = sa + L::kABytes;
+        if (leader) {
+#pragma unroll
+          for (int kk = 0; kk < kBKb / 16; ++kk) {
+            const uint64_t ad = a_mn ? make_sdesc(sa + kk * 2048, 8192, 1024, kSw128)
+                                     : make_sdesc(sa + kk * 32, 16, 1024, kSw128);
+            const uint64_t bd = b_mn ? make_sdesc(sb + kk * 2048, 8192, 1024, kSw128)
+                                     : make_sdesc(sb + kk * 32, 16, 1024, kSw128);
+            tc_mma_bf16(d, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(empty_bar(s));
+        }
+        __syncwarp();
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      if (leader) tc_commit(tfull(acc));
+      __syncwarp();
+    }
+  } else if (GATHER ? warp >= 5 : warp < 4) {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int lt = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      int z, m0, n0, kb0, nkb;
+      decode(t, z, m0, n0, kb0, nkb);
+      const int acc = lt & 1;
+      mbar_wait_sleep(tfull(acc), (lt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t ta = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      const uint32_t release = tempty(acc);
+      tcb_epilogue<BN>(p, ta, m0, n0, z, q * 32 + lane, nkb <= 0, [&] {
+        tc_fence_before();
+        mbar_arrive(release);
+      });
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN) : "memory");
   }
 }
 

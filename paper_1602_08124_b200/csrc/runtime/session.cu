@@ -313,12 +313,21 @@ void Session::build_program() {
       s.gap_len = p.gap_len;
       const float* probe_x = summed(s.layer) ? F(s.in_off[0]) : nullptr;  // shapes only
       if (summed(s.layer)) s.sum_bytes = round_up(g_.dims(l.in[0]).count() * es_, 1024);
+      size_t at = s.sum_bytes;
+      s.pad_c = padded_channels(s.layer);
+      if (s.pad_c) {  // [X padded | W padded]
+        const Dims& x = g_.dims(l.in[0]);
+        s.x8_off = at;
+        s.w8_off = at + round_up(x.n * x.h * x.w * static_cast<u64>(s.pad_c) * 2, 1024);
+        at = s.w8_off + round_up(l.out * l.k * l.k * static_cast<u64>(s.pad_c) * 2, 1024);
+      }
       if (contraction) {
-        const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, probe_x);
+        vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, probe_x);
+        if (s.pad_c) a.c[0] = s.pad_c;
         s.part_bytes = bf_ ? vdnnk::conv_fprop_ws_bytes_bf16(a) : vdnnk::conv_fprop_ws_bytes(a);
       }
-      s.part_off = s.sum_bytes;
-      s.scratch = s.part_bytes ? s.part_off + s.part_bytes : s.sum_bytes;
+      s.part_off = at;
+      s.scratch = s.part_bytes ? s.part_off + s.part_bytes : at;
       fwd_.push_back(std::move(s));
     } else {
       BwdStep s;
@@ -355,8 +364,18 @@ void Session::build_program() {
         s.dil_bytes = round_up(y.n * ((y.h - 1) * l.s + 1) * ((y.w - 1) * l.s + 1) * y.c * es_, 1024);
         at += s.dil_bytes;
       }
+      s.pad_c = any_plane ? 0 : padded_channels(s.layer);
+      if (s.pad_c) {  // [X padded | W padded | fp32 dW of the padded weights]
+        const Dims& x = g_.dims(l.in[0]);
+        const u64 wn = l.out * l.k * l.k * static_cast<u64>(s.pad_c);
+        s.x8_off = at;
+        s.w8_off = at + round_up(x.n * x.h * x.w * static_cast<u64>(s.pad_c) * 2, 1024);
+        s.dw8_off = s.w8_off + round_up(wn * 2, 1024);
+        at = s.dw8_off + (o_.external_grads ? round_up(wn * 4, 1024) : 0);
+      }
       if (contraction) {
-        const vdnnk::ConvArgs w = conv_args(s.layer, s.in_off, nullptr, probe_x);
+        vdnnk::ConvArgs w = conv_args(s.layer, s.in_off, nullptr, probe_x);
+        if (s.pad_c) w.c[0] = s.pad_c;
         s.part_bytes = bf_ ? vdnnk::conv_wgrad_ws_bytes_bf16(w) : vdnnk::conv_wgrad_ws_bytes(w);
         if (any_plane) {
           vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off, probe_x);
@@ -457,6 +476,31 @@ void Session::fuse_relus() {
 bool Session::summed(int layer) const {
   const Node& l = g_.at(layer);
   return l.join == Join::Elementwise && l.in.size() > 1;
+}
+
+// BF16 conv over the raw input with a channel count that is not a multiple
+// of 8 (C = 3 images): its rows (6 B per pixel) cannot feed TMA, so the step
+// pads X and W to 8 channels (zeros) in its scratch and runs the padded
+// contraction; zero channels add nothing to Y, and their weight gradients are
+// zero, so the update of the real weights is unchanged.
+int Session::padded_channels(int layer) const {
+  const Node& l = g_.at(layer);
+  static const bool on = [] {  // VDNN_BF16_PAD=0: the unpadded gather path (A/B switch)
+    const char* e = std::getenv("VDNN_BF16_PAD");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || !bf_ || l.kind != Kind::Conv || l.in.size() != 1 || g_.at(l.in[0]).kind != Kind::Input) return 0;
+  const int c = static_cast<int>(g_.dims(l.in[0]).c);
+  return c % 8 == 0 ? 0 : (c + 7) / 8 * 8;
+}
+
+// X and W of a padded step into the scratch; `a` then describes the padded X.
+void Session::pad_operands(vdnnk::ConvArgs& a, int cp, char* x8, const float* w, char* w8) {
+  const int c = a.c[0];
+  check(vdnnk::pad_channels_bf16(x8, a.x[0], static_cast<size_t>(a.n) * a.h * a.w, c, cp, cs_), "pad X");
+  check(vdnnk::pad_channels_bf16(w8, w, static_cast<size_t>(a.cout) * a.kh * a.kw, c, cp, cs_), "pad W");
+  a.x[0] = reinterpret_cast<const float*>(x8);
+  a.c[0] = cp;
 }
 
 // X of an elementwise join (net_graph.hpp:290-296: identical shapes) = the
@@ -632,8 +676,13 @@ void Session::run_fwd(const FwdStep& s, float lr) {
       vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, sum_x);
       a.relu_out = s.relu ? 1 : 0;
       const float* bias = l.kind == Kind::Fc ? F(s.w_off + g_.fc_inputs(s.layer) * l.out * es_) : nullptr;
-      check(bf_ ? vdnnk::conv_fprop_bf16(a, F(s.w_off), bias, F(s.out_off), false, cs_, part, s.part_bytes)
-                : vdnnk::conv_fprop(a, F(s.w_off), bias, F(s.out_off), false, cs_, part, s.part_bytes),
+      const float* w = F(s.w_off);
+      if (s.pad_c) {
+        w = reinterpret_cast<float*>(scr + s.w8_off);
+        pad_operands(a, s.pad_c, scr + s.x8_off, F(s.w_off), scr + s.w8_off);
+      }
+      check(bf_ ? vdnnk::conv_fprop_bf16(a, w, bias, F(s.out_off), false, cs_, part, s.part_bytes)
+                : vdnnk::conv_fprop(a, w, bias, F(s.out_off), false, cs_, part, s.part_bytes),
             "conv_fprop");
       break;
     }
@@ -739,15 +788,29 @@ void Session::run_bwd(const BwdStep& s, float lr) {
                   : vdnnk::conv_dgrad(a, F(s.w_off), dyd, s.accumulate, cs_, part, s.part_bytes),
               "conv_dgrad");
       }
-      const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, sum_x);
+      vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, sum_x);
       // split-K partials: the split count depends only on the layer shape
       // (the launch always gets the bytes it asks for), so the reduction
       // order -- and every bit of the update -- is independent of the offload
       // policy and of where the partials live
       float* dw = grads_ ? grads_ + grad_off_[mi] : nullptr;
-      check(bf_ ? vdnnk::conv_wgrad_bf16(a, dy, F(s.w_off), lr, dw, part, s.part_bytes, cs_)
-                : vdnnk::conv_wgrad(a, dy, F(s.w_off), lr, dw, part, s.part_bytes, cs_),
-            "conv_wgrad");
+      if (s.pad_c) {
+        // padded weights: the update (or fp32 dW) lands in the padded copy,
+        // then the real channels are copied back
+        const size_t rows = l.out * l.k * l.k;
+        const int c = a.c[0];
+        char* w8 = scr + s.w8_off;
+        float* dw8 = dw ? reinterpret_cast<float*>(scr + s.dw8_off) : nullptr;
+        pad_operands(a, s.pad_c, scr + s.x8_off, F(s.w_off), w8);
+        check(vdnnk::conv_wgrad_bf16(a, dy, w8, lr, dw8, part, s.part_bytes, cs_), "conv_wgrad (padded)");
+        check(dw ? vdnnk::unpad_channels_f32(dw, dw8, rows, c, s.pad_c, cs_)
+                 : vdnnk::unpad_channels_bf16(F(s.w_off), w8, rows, c, s.pad_c, cs_),
+              "unpad weights");
+      } else {
+        check(bf_ ? vdnnk::conv_wgrad_bf16(a, dy, F(s.w_off), lr, dw, part, s.part_bytes, cs_)
+                  : vdnnk::conv_wgrad(a, dy, F(s.w_off), lr, dw, part, s.part_bytes, cs_),
+              "conv_wgrad");
+      }
       if (fc) {
         const u64 in = g_.fc_inputs(s.layer);
         float* bias = F(s.w_off + in * l.out * es_);

@@ -71,6 +71,10 @@ struct FwdStep {
   size_t scratch = 0;
   size_t sum_bytes = 0;          // elementwise join: the summed input X
   size_t part_off = 0, part_bytes = 0;
+  // BF16 first layer (raw input, C % 8 != 0): channel-padded copies of X and
+  // W in the step's scratch feed the TMA producers
+  int pad_c = 0;                 // padded channel count (0 = not padded)
+  size_t x8_off = 0, w8_off = 0;
 };
 
 struct BwdStep {
@@ -97,6 +101,8 @@ struct BwdStep {
   // conv dgrad) | split-K partials]
   size_t scratch = 0;
   size_t sum_bytes = 0, stage_off = 0, stage_bytes = 0, dil_off = 0, dil_bytes = 0, part_off = 0, part_bytes = 0;
+  int pad_c = 0;                 // as FwdStep; plus the fp32 dW of the padded weights (external grads)
+  size_t x8_off = 0, w8_off = 0, dw8_off = 0;
 };
 
 class Session {
@@ -198,6 +204,8 @@ class Session {
   vdnnk::PoolArgs pool_args(int layer, const std::vector<u64>& in_off, const std::vector<u64>* planes,
                             const float* sum_x) const;
   bool summed(int layer) const;  // elementwise join over >= 2 inputs
+  int padded_channels(int layer) const;  // BF16 first layer: padded C (0 = none)
+  void pad_operands(vdnnk::ConvArgs& a, int cp, char* x8, const float* w, char* w8);
   void sum_inputs(int layer, const std::vector<u64>& in_off, float* dst);
   void check(cudaError_t e, const char* what) const;
 

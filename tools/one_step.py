@@ -1,4 +1,4 @@
-"""One training step of a preset (for ncu launch lists): python tools/one_step.py [net] [batch] [policy]"""
+"""One training step of a preset (for ncu launch lists): python tools/one_step.py [net] [batch] [policy] [--bf16]"""
 import sys
 
 sys.path.insert(0, ".")
@@ -9,6 +9,8 @@ batch = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 policy = sys.argv[3] if len(sys.argv) > 3 else "none"
 g = V.build_preset(net, batch)
 cm = V.CostModel()
+if "--bf16" in sys.argv:
+    cm.elem_size = 2
 if policy == "none":
     d, cap = V.static_decision(V.PolicyKind.Baseline, V.AlgoMode.PerfOptimal, g, cm), 150 << 30
 else:

@@ -3,7 +3,7 @@ bench.py / one_step.py: per kernel family, the launch count, summed time,
 share of the step and DRAM bytes per launch, over the LAST training step
 (the launches after the last tf32 probe / before the end).
 
-    python tools/summarize_launches.py gpurun_out/r01_launches_dyn.csv [--per-step N]
+    python tools/summarize_launches.py gpurun_out/r01_launches_dyn.csv [--per-step N] [--steps N]
 """
 import csv
 import re
@@ -43,11 +43,17 @@ def main():
     # everything before it)
     probe = [i for i, k in enumerate(ks) if "tf32_peak" in k["name"]]
     ks = ks[probe[-1] + 1:] if probe else ks
-    first = sys.argv[sys.argv.index("--first") + 1] if "--first" in sys.argv else "c3tc_fprop"
-    starts = [i for i, k in enumerate(ks) if first in k["name"]]
-    step = ks[starts[-2]:starts[-1]] if len(starts) >= 2 else ks[starts[-1]:]
-    if per:
-        step = ks[starts[-1]:starts[-1] + per]
+    if "--steps" in sys.argv:
+        # N identical steps after the synthetic-data fills: the last N-th
+        n = int(sys.argv[sys.argv.index("--steps") + 1])
+        ks = [k for k in ks if "fill_" not in k["name"]]
+        step = ks[len(ks) - len(ks) // n:]
+    else:
+        first = sys.argv[sys.argv.index("--first") + 1] if "--first" in sys.argv else "c3tc_fprop"
+        starts = [i for i, k in enumerate(ks) if first in k["name"]]
+        step = ks[starts[-2]:starts[-1]] if len(starts) >= 2 else ks[starts[-1]:]
+        if per:
+            step = ks[starts[-1]:starts[-1] + per]
     tot = sum(k.get("gpu__time_duration.sum", 0) for k in step)
     agg = defaultdict(lambda: [0, 0.0, 0.0, 0.0])
     for k in step:
@@ -63,7 +69,8 @@ def main():
     if "--traffic-json" in sys.argv:
         # DRAM bytes per conv-engine launch (bench.py's roofline "traffic")
         import json
-        conv = [k for k in step if k["name"].startswith("void tc_") or "c3tc" in k["name"]]
+        conv = [k for k in step if "tc_conv" in k["name"] or "tc_wgrad" in k["name"] or "tcb_conv" in k["name"]
+                or "c3tc" in k["name"]]
         byt = sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0) for k in conv)
         out = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                          "--clock-control none, python bench.py --policies dyn --steps 1 --warmup 3 (last step): "
