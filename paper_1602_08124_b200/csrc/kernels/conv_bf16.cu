@@ -8,9 +8,18 @@
 
 #include "kernels.h"
 #include "tcb_conv.cuh"
+#include "tcb_halo.cuh"
 #include "tma_maps.h"
 
 namespace vdnnk {
+
+// first-layer kernels (conv_c3tcb.cu)
+bool c3b_fprop_eligible(const ConvArgs& a);
+bool c3b_wgrad_eligible(const ConvArgs& a);
+size_t c3b_wgrad_ws_bytes(const ConvArgs& a);
+cudaError_t c3b_fprop(const ConvArgs& a, const void* w, void* y, cudaStream_t st);
+cudaError_t c3b_wgrad(const ConvArgs& a, const void* dy, void* w, float lr, float* dw_out, float* ws, size_t ws_bytes,
+                      cudaStream_t st);
 
 namespace {
 constexpr int kNumSmsB = 148;
@@ -87,6 +96,11 @@ cudaError_t launch_b(const ConvParamsB& p, int splits, const CUtensorMap& ta, co
 }
 
 thread_local bool g_no_tma_b = false;
+// VDNN_BF16_C3=0: first layers on the generic engine (A/B switch)
+const bool g_no_c3b = [] {
+  const char* e = std::getenv("VDNN_BF16_C3");
+  return e && std::atoi(e) == 0;
+}();
 
 // Layers the TMA producers can feed (one segment, 8-multiple channel counts,
 // square windows, stride-1 dgrad): they run the persistent kernel.
@@ -161,7 +175,103 @@ bool make_maps_b(const ConvParamsB& p, int bn, CUtensorMap* ta, CUtensorMap* tb)
   return encode_tiled(tb, p.dy, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, kBf);
 }
 
+// Halo-reuse kernel (tcb_halo.cuh) for stride-1 k x k FPROP / DGRAD over one
+// NHWC tensor: 64-multiple channel counts, <= 128 output columns, a padded
+// input row that fits one TMA box (<= 256 pixels) and >= 75% of a tile's 256
+// virtual rows real outputs (VGG: 224x224x64, 112x112x{64,128}).
+// VDNN_BF16_HALO=0 disables (A/B switch).
+bool halo_params_b(const ConvParamsB& p, HaloParamsB& h) {
+  static const bool on = [] {
+    const char* e = std::getenv("VDNN_BF16_HALO");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || g_no_tma_b || (p.kind != kFprop && p.kind != kDgrad)) return false;
+  if (p.nseg != 1 || !p.vec_in || p.tap_pack || p.stride != 1 || p.kh != p.kw || p.kh != 3) return false;
+  if (p.C % 64 != 0 || p.Cout % 64 != 0 || p.bias) return false;
+  std::memset(&h, 0, sizeof(h));
+  h.kind = p.kind;
+  h.N = p.N;
+  h.kh = p.kh;
+  h.kw = p.kw;
+  if (p.kind == kFprop) {
+    h.Hin = p.H, h.Win = p.W, h.Cin = p.C, h.pad = p.pad;
+    h.Hout = p.Ho, h.Wout = p.Wo, h.Cout = p.Cout;
+    h.out = p.y;
+    h.relu = p.relu;
+  } else {
+    if (p.seg[0].dx == nullptr || p.pad > p.kh - 1) return false;
+    h.Hin = p.Ho, h.Win = p.Wo, h.Cin = p.Cout, h.pad = p.kh - 1 - p.pad;
+    h.Hout = p.H, h.Wout = p.W, h.Cout = p.C;
+    h.out = p.seg[0].dx;
+    h.mask_x = p.seg[0].mask ? p.seg[0].x : nullptr;
+  }
+  if (h.Cout > 128) return false;
+  h.accum = p.epi == kEpiAccum;
+  h.P = h.Win + 2 * h.pad;
+  if (h.P > 256 || h.Wout + h.kw - 1 != h.P) return false;
+  h.TH = 256 / h.P;
+  if (4 * h.TH * h.Wout < 3 * 256) return false;
+  h.nck = h.Cin / 64;
+  h.tiles_h = (h.Hout + h.TH - 1) / h.TH;
+  return true;
+}
+
+template <int BN, int AS, int BS>
+cudaError_t launch_halo_b(HaloParamsB& h, const ConvParamsB& p, cudaStream_t st) {
+  using L = HaloSmemB<BN, AS, BS>;
+  alignas(64) CUtensorMap ta, tb;
+  std::memset(&ta, 0, sizeof(ta));
+  std::memset(&tb, 0, sizeof(tb));
+  const bf16* src = p.kind == kFprop ? p.seg[0].x : p.dy;
+  {
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(h.Cin), static_cast<cuuint64_t>(h.Win),
+                                static_cast<cuuint64_t>(h.Hin), static_cast<cuuint64_t>(h.N)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(h.Cin) * 2, static_cast<cuuint64_t>(h.Win) * h.Cin * 2,
+                                   static_cast<cuuint64_t>(h.Hin) * h.Win * h.Cin * 2};
+    const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(h.P), static_cast<cuuint32_t>(h.TH), 1};
+    if (!encode_tiled(&ta, src, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
+      return cudaErrorNotSupported;
+  }
+  const int taps = p.kh * p.kw;
+  if (p.kind == kFprop) {
+    // W [Cout][KK] (KRSC): 64-channel x BN-row K-major boxes
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.KK), static_cast<cuuint64_t>(p.Cout)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.KK) * 2};
+    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(BN)};
+    if (!encode_tiled(&tb, p.w, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
+      return cudaErrorNotSupported;
+  } else {
+    // W [co][tap][ci] as (ci, tap, co): a 64 ci x 64 co box of one tap is an
+    // MN-major SWIZZLE_128B chunk (K = co rows of 64 ci)
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.C), static_cast<cuuint64_t>(taps),
+                                static_cast<cuuint64_t>(p.Cout)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.C) * 2, static_cast<cuuint64_t>(taps) * p.C * 2};
+    const cuuint32_t box[3] = {64, 1, 64};
+    if (!encode_tiled(&tb, p.w, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
+      return cudaErrorNotSupported;
+  }
+  h.ntn = (h.Cout + BN - 1) / BN;
+  h.ntiles = h.N * h.tiles_h * h.ntn;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(tcb_halo_kernel<BN, AS, BS, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  tcb_halo_kernel<BN, AS, BS, 3><<<std::min(h.ntiles, kNumSmsB), 192, L::kTotal, st>>>(h, ta, tb);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_any(const ConvParamsB& p, int splits, cudaStream_t st) {
+  if (splits == 1) {
+    HaloParamsB h;
+    if (halo_params_b(p, h)) {
+      const cudaError_t e = h.Cout <= 64 ? launch_halo_b<64, 4, 8>(h, p, st) : launch_halo_b<128, 4, 4>(h, p, st);
+      if (e != cudaErrorNotSupported) return e;
+    }
+  }
   if (p.M <= 0 || p.Ncols <= 0) return cudaSuccess;
   const int bn = tile_n(p);
   alignas(64) CUtensorMap ta, tb;
@@ -315,9 +425,12 @@ __global__ void wgrad_reduce_b_kernel(const __grid_constant__ ConvParamsB p, int
 int reduce_blocks(int64_t total) { return static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kNumSmsB)); }
 }  // namespace
 
+bool conv_bf16_c3_native(const ConvArgs& a) { return !g_no_c3b && c3b_fprop_eligible(a) && c3b_wgrad_eligible(a); }
+
 void set_tma_bf16(bool on) { g_no_tma_b = !on; }
 
 size_t conv_fprop_ws_bytes_bf16(const ConvArgs& a) {
+  if (c3b_fprop_eligible(a)) return 0;
   ConvParamsB p;
   if (!fprop_params_b(a, nullptr, nullptr, nullptr, false, p)) return 0;
   const int s = fprop_splits_b(p);
@@ -326,6 +439,7 @@ size_t conv_fprop_ws_bytes_bf16(const ConvArgs& a) {
 
 cudaError_t conv_fprop_bf16(const ConvArgs& a, const void* w, const void* bias, void* y, bool accumulate,
                             cudaStream_t st, float* ws, size_t ws_bytes) {
+  if (!accumulate && bias == nullptr && !g_no_c3b && c3b_fprop_eligible(a)) return c3b_fprop(a, w, y, st);
   ConvParamsB p;
   if (!fprop_params_b(a, w, bias, y, accumulate, p)) return cudaErrorInvalidValue;
   const size_t per = static_cast<size_t>(p.M) * p.Cout * sizeof(float);
@@ -381,11 +495,14 @@ size_t conv_wgrad_ws_bytes_bf16(const ConvArgs& a) {
   const int M = wgrad_rows_b(p);
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
   const int s = wgrad_splits_b(p, M, P);
-  return s > 1 ? static_cast<size_t>(s) * M * a.cout * sizeof(float) : 0;
+  const size_t b = s > 1 ? static_cast<size_t>(s) * M * a.cout * sizeof(float) : 0;
+  return c3b_wgrad_eligible(a) ? std::max(b, c3b_wgrad_ws_bytes(a)) : b;
 }
 
 cudaError_t conv_wgrad_bf16(const ConvArgs& a, const void* dy, void* w_mut, float lr, float* dw_out, float* ws,
                             size_t ws_bytes, cudaStream_t st) {
+  if (!g_no_c3b && c3b_wgrad_eligible(a) && ws != nullptr && ws_bytes >= c3b_wgrad_ws_bytes(a))
+    return c3b_wgrad(a, dy, w_mut, lr, dw_out, ws, ws_bytes, st);
   ConvParamsB p;
   if (!build_common_b(a, p)) return cudaErrorInvalidValue;
   p.kind = kWgrad;

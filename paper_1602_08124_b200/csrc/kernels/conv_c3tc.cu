@@ -87,6 +87,46 @@ __device__ __forceinline__ void c3_row(const float* __restrict__ x, const C3Geom
   }
 }
 
+// Compile-time window (KT x KT taps of CT channels, e.g. VGG's 3 x 3 x 3):
+// the 27 loads sit at constant offsets from KT row pointers and clipping is
+// two KT-bit masks -- no table reads and no per-element address arithmetic
+// (the table-driven row issues ~10 instructions per element; the builders
+// are then issue-bound, not HBM-bound). KT = 0: the table-driven row.
+template <int KT, int CT>
+__device__ __forceinline__ void c3_row_t(const float* __restrict__ x, const C3Geom& g, const int* off, const int* rs,
+                                         int m, float (&v)[32]) {
+  if constexpr (KT == 0) {
+    c3_row(x, g, off, rs, m, v);
+  } else {
+    static_assert(KT * KT * CT <= 32, "window must fit one K block");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    if (m >= g.P) return;
+    const int n = m / g.HoWo;
+    const int rem = m - n * g.HoWo;
+    const int oh = rem / g.Wo, ow = rem - oh * g.Wo;
+    const int ih0 = oh * g.stride - g.pad, iw0 = ow * g.stride - g.pad;
+    uint32_t rmask = 0, cmask = 0;
+#pragma unroll
+    for (int r = 0; r < KT; ++r) rmask |= (ih0 + r >= 0 && ih0 + r < g.H) ? (1u << r) : 0u;
+#pragma unroll
+    for (int s = 0; s < KT; ++s) cmask |= (iw0 + s >= 0 && iw0 + s < g.W) ? (1u << s) : 0u;
+    const float* x0 = x + ((static_cast<int64_t>(n) * g.H + ih0) * g.W + iw0) * CT;
+    const int64_t rstride = static_cast<int64_t>(g.W) * CT;
+    const bool full = rmask == (1u << KT) - 1 && cmask == (1u << KT) - 1;
+#pragma unroll
+    for (int r = 0; r < KT; ++r) {
+      const float* xr = x0 + r * rstride;
+#pragma unroll
+      for (int s = 0; s < KT; ++s) {
+#pragma unroll
+        for (int c = 0; c < CT; ++c)
+          if (full || (((rmask >> r) & (cmask >> s)) & 1u)) v[(r * KT + s) * CT + c] = __ldg(xr + s * CT + c);
+      }
+    }
+  }
+}
+
 // Multi-K-block variant (kh*kw*C > 32, e.g. AlexNet / OverFeat 11x11x3 =
 // 363 = 12 K blocks): table entries for all KB*32 im2col columns.
 constexpr int kMkMaxKB = 12;
@@ -151,6 +191,7 @@ __device__ __forceinline__ void c3_row_kb(const float* __restrict__ x, const C3G
 // warps 0-3 epilogue, 4-11 builders (two groups of 4 warps taking alternate
 // tiles, one pixel row per thread), 12 MMA (+ TMEM owner). TMEM: 2 x NBP columns.
 constexpr int kFpThreads = 416;
+template <int KT, int CT>
 __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_kernel(const float* __restrict__ x,
                                                                    const float* __restrict__ w,
                                                                    const __grid_constant__ CUtensorMap tma_y,
@@ -216,10 +257,15 @@ __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_kernel(const float* 
     const int grp = (warp - 4) >> 2;
     const int row = (threadIdx.x - 128) & 127;
     int it = grp;
-    for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += 2 * gridDim.x, it += 2) {
+    // software-pipelined: the next tile's loads are in flight while this
+    // tile's row waits for its stage and is stored
+    float v[32], nv[32];
+    const int tile0 = blockIdx.x + grp * gridDim.x;
+    if (tile0 < ntiles) c3_row_t<KT, CT>(x, g, tab, tab + 32, tile0 * kBM + row, v);
+    for (int tile = tile0; tile < ntiles; tile += 2 * gridDim.x, it += 2) {
       const int s = it % kFpStages;
-      float v[32];
-      c3_row(x, g, tab, tab + 32, tile * kBM + row, v);  // loads in flight while the stage drains
+      const int nt = tile + 2 * gridDim.x;
+      if (nt < ntiles) c3_row_t<KT, CT>(x, g, tab, tab + 32, nt * kBM + row, nv);
       if (it >= kFpStages) mbar_wait(empty_bar(s), ((it / kFpStages) & 1) ^ 1);
       const uint32_t sa = sa0 + s * 16384;
 #pragma unroll
@@ -229,6 +275,8 @@ __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_kernel(const float* 
                      : "memory");
       fence_proxy_async();
       mbar_arrive(full_bar(s));
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = nv[i];
     }
   } else if (warp == 12) {
     // ---------------- MMA issuer ----------------
@@ -305,6 +353,7 @@ __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_kernel(const float* 
 // drain TMEM), warp 8 lane 0 TMA, warp 9 MMA + TMEM.
 constexpr int kWgThreads = 320;
 constexpr uint32_t kWgStage = 16384 + 4096;
+template <int KT, int CT>
 __global__ void __launch_bounds__(kWgThreads, 1) c3tc_wgrad_kernel(const float* __restrict__ x,
                                                                    const __grid_constant__ CUtensorMap tma_dy,
                                                                    C3Geom g, int ppb, float* __restrict__ part) {
@@ -354,11 +403,17 @@ __global__ void __launch_bounds__(kWgThreads, 1) c3tc_wgrad_kernel(const float* 
 
   if (warp < 8) {
     // ---------------- builders ----------------
+    // software-pipelined: stage it + 8's loads are in flight while stage it
+    // waits for its slot and is stored
+    auto pix = [&](int i) {
+      const int m = p_begin + i * kBK + lane;
+      return m < p_end ? m : g.P;
+    };
+    float v[32], nv[32];
+    if (warp < nkb) c3_row_t<KT, CT>(x, g, tab, tab + 32, pix(warp), v);
     for (int it = warp; it < nkb; it += 8) {
       const int s = it % kWgStages;
-      const int m = p_begin + it * kBK + lane;
-      float v[32];
-      c3_row(x, g, tab, tab + 32, m < p_end ? m : g.P, v);  // loads in flight while the stage drains
+      if (it + 8 < nkb) c3_row_t<KT, CT>(x, g, tab, tab + 32, pix(it + 8), nv);
       if (it >= kWgStages) mbar_wait(empty_bar(s), ((it / kWgStages) & 1) ^ 1);
       const uint32_t sbb = base + s * kWgStage + 16384;
 #pragma unroll
@@ -368,6 +423,8 @@ __global__ void __launch_bounds__(kWgThreads, 1) c3tc_wgrad_kernel(const float* 
                      : "memory");
       fence_proxy_async();
       mbar_arrive(full_bar(s));
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = nv[i];
     }
     // ---------------- epilogue: warp w owns TMEM lanes 32w.. = co ----------------
     if (warp < nchunk) {
@@ -844,16 +901,17 @@ cudaError_t c3tc_fprop(const ConvArgs& a, const float* w, float* y, cudaStream_t
     return cudaGetLastError();
   }
   const size_t smem = fprop_smem(NB);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(c3tc_fprop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  const bool k3c3 = g.k == 3 && g.C == 3;
+  auto kern = k3c3 ? c3tc_fprop_kernel<3, 3> : c3tc_fprop_kernel<0, 0>;
+  static size_t attr[2] = {0, 0};
+  if (smem > attr[k3c3]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[k3c3] = smem;
   }
   const int ntiles = (g.P + kBM - 1) / kBM;
   const int grid = std::min(kSms, ntiles);
-  c3tc_fprop_kernel<<<grid, kFpThreads, smem, st>>>(a.x[0], w, ty, g, NB, NBP, a.relu_out);
+  kern<<<grid, kFpThreads, smem, st>>>(a.x[0], w, ty, g, NB, NBP, a.relu_out);
   count_launch();
   return cudaGetLastError();
 }
@@ -875,12 +933,13 @@ cudaError_t c3tc_wgrad(const ConvArgs& a, const float* dy, float* w, float lr, f
   const cuuint32_t b3[3] = {32, 32, static_cast<cuuint32_t>(g.Cout / 32)};
   if (!encode_tiled(&tdy, dy, 3, d3, s3, b3, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
   const size_t smem = wgrad_smem();
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(c3tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  const bool k3c3 = g.k == 3 && g.C == 3;
+  auto kern = k3c3 ? c3tc_wgrad_kernel<3, 3> : c3tc_wgrad_kernel<0, 0>;
+  static size_t attr[2] = {0, 0};
+  if (smem > attr[k3c3]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[k3c3] = smem;
   }
   const int KB = kblocks_of(a);
   if (KB > 1) {
@@ -894,7 +953,7 @@ cudaError_t c3tc_wgrad(const ConvArgs& a, const float* dy, float* w, float lr, f
     }
     c3tc_wgrad_mk_kernel<<<nb, kWgThreads, smk, st>>>(a.x[0], tdy, g, ppb, KB, pow2_at_least(KB * 32), ws);
   } else {
-    c3tc_wgrad_kernel<<<nb, kWgThreads, smem, st>>>(a.x[0], tdy, g, ppb, ws);
+    kern<<<nb, kWgThreads, smem, st>>>(a.x[0], tdy, g, ppb, ws);
   }
   count_launch();
   cudaError_t e = cudaGetLastError();

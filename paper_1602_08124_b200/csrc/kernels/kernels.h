@@ -175,6 +175,9 @@ cudaError_t sgd_update_bf16(void* w, const float* g, float lr, size_t n, cudaStr
 cudaError_t fill_normal_bf16(void* w, size_t n, float stddev, uint64_t seed, cudaStream_t st);
 cudaError_t fill_uniform_bf16(void* x, size_t n, float lo, float hi, uint64_t seed, cudaStream_t st);
 cudaError_t fill_const_bf16(void* x, size_t n, float v, cudaStream_t st);
+// First layers (C <= 8, kh*kw*C <= 64) that the dedicated BF16 kernels of
+// conv_c3tcb.cu run in fprop and wgrad (no channel padding needed)
+bool conv_bf16_c3_native(const ConvArgs& a);
 // [rows][c] <-> [rows][cp] channel padding (zeros in c..cp)
 cudaError_t pad_channels_bf16(void* dst, const void* src, size_t rows, int c, int cp, cudaStream_t st);
 cudaError_t unpad_channels_bf16(void* dst, const void* src, size_t rows, int c, int cp, cudaStream_t st);

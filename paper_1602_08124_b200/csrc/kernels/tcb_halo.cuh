@@ -1,0 +1,261 @@
+// Halo-reuse FPROP / DGRAD for the BF16 engine (included by conv_bf16.cu
+// after tcb_conv.cuh): stride-1 k x k convolutions with 64-multiple channel
+// counts and narrow outputs (<= 128 columns), i.e. VGG's 224x224x64 and
+// 112x112x128 layers.
+//
+// Why: the im2col TMA producer (tcb_conv.cuh) stages every input pixel once
+// per filter tap -- 9 x 16 KB boxes per 128 output pixels for a 3x3 conv over
+// 64 channels -- and at N = 64 / 128 columns that fill, not the tensor pipe,
+// bounds the layer (ncu, 224x224x64 fprop: L1/TMA throughput 87% of peak,
+// 22 GB through the xbar for 3.3 GB of X and Y, tensor pipe 21% active).
+// Here, as in the TF32 halo kernel (tc_conv_halo.cuh), output pixels live on
+// a virtual grid whose row pitch is the padded input width P = Win + 2*pad:
+// the input pixel of output v = y*P + x under tap (r, s) is padded input pixel
+// v + r*P + s, so one TMA box of TH padded input rows x P pixels x 64 channels
+// (zero fill = padding) serves the kw taps of filter row r through A
+// descriptors advanced by s rows of 128 B (SWIZZLE_128B is a function of the
+// absolute shared-memory address: tools/halo_probe.cu). A fill per 256
+// virtual rows: kh boxes of <= 33 KB per 64 channels instead of kh*kw boxes.
+//
+//   FPROP  A = X box (K-major), B = W[co][r][s][c0:c0+64] (K-major, one 2D box)
+//   DGRAD  A = dY box (K-major, pad' = k-1-pad), B[k = co][n = ci] =
+//          W[co][flipped tap][ci] (MN-major: 64 ci x 64 co boxes), fused
+//          ReLU backward (dX *= x > 0) and accumulation in the epilogue.
+// Tile = 256 virtual rows (two M = 128 MMAs per tap, h = 0, 1) x BN columns;
+// persistent CTAs (one per SM), two TMEM accumulator sets (4 x BN columns)
+// so tile t's epilogue overlaps tile t+1's main loop.
+//   warps 0-3 : epilogue (TMEM lanes 32w..): bf16 RNE stores
+//   warp 4    : TMEM owner + MMA issuer (one elected lane)
+//   warp 5    : TMA producer (one lane), in consumption order
+#pragma once
+
+namespace vdnnk {
+
+struct HaloParamsB {
+  int kind;               // kFprop or kDgrad
+  int N, Hin, Win, Cin;   // A source: fprop X, dgrad dY (NHWC bf16)
+  int pad;                // fprop: pad; dgrad: kh - 1 - pad
+  int kh, kw;
+  int Hout, Wout, Cout;   // output: fprop Y, dgrad dX (NHWC bf16)
+  int P, TH, nck, tiles_h, ntn, ntiles;
+  int relu, accum;
+  bf16* out;
+  const bf16* mask_x;     // dgrad: dX *= (x > 0), x laid out like out; null = none
+};
+
+template <int BN, int AS, int BS>
+struct HaloSmemB {
+  static constexpr int kASlot = 33 * 1024;  // >= 258 rows x 128 B (256 virtual rows + 2 tap shifts)
+  static constexpr int kBSlot = BN * 128;
+  static constexpr int kTotal = AS * kASlot + BS * kBSlot + 1024 + 256;
+  static constexpr int kAccCols = 2 * BN;   // two M = 128 halves
+  static_assert(2 * kAccCols <= 512, "two accumulator sets must fit TMEM");
+};
+
+template <int BN, int AS, int BS, int KW>
+__global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant__ HaloParamsB p,
+                                                          const __grid_constant__ CUtensorMap tma_a,
+                                                          const __grid_constant__ CUtensorMap tma_b) {
+  using L = HaloSmemB<BN, AS, BS>;
+  constexpr int kTmemCols = 2 * L::kAccCols;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bslots = base + AS * L::kASlot;
+  const uint32_t bars = bslots + BS * L::kBSlot;
+  auto full_a = [&](int s) { return bars + 8u * s; };
+  auto empty_a = [&](int s) { return bars + 8u * (AS + s); };
+  auto full_b = [&](int s) { return bars + 8u * (2 * AS + s); };
+  auto empty_b = [&](int s) { return bars + 8u * (2 * AS + BS + s); };
+  auto tfull = [&](int a) { return bars + 8u * (2 * AS + 2 * BS + a); };
+  auto tempty = [&](int a) { return bars + 8u * (2 * AS + 2 * BS + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * AS + 2 * BS + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(full_a(s), 1);
+      mbar_init(empty_a(s), 1);
+    }
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(full_b(s), 1);
+      mbar_init(empty_b(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  const uint32_t abytes = static_cast<uint32_t>(p.TH * p.P * 128);
+  if (warp == 5) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+      int sa = 0, sb = 0;
+      uint32_t pha = 1, phb = 1;  // the first pass over each ring does not wait
+      for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        const int tn = tile % p.ntn, t2 = tile / p.ntn;
+        const int th = t2 % p.tiles_h, n = t2 / p.tiles_h;
+        const int y0 = th * p.TH, n0 = tn * BN;
+        for (int c = 0; c < p.nck; ++c) {
+          for (int r = 0; r < p.kh; ++r) {
+            mbar_wait(empty_a(sa), pha);
+            mbar_expect_tx(full_a(sa), abytes);
+            tma_load_4d(base + sa * L::kASlot, &tma_a, full_a(sa), c * 64, -p.pad, y0 + r - p.pad, n);
+            if (++sa == AS) {
+              sa = 0;
+              pha ^= 1;
+            }
+#pragma unroll
+            for (int s = 0; s < KW; ++s) {
+              mbar_wait(empty_b(sb), phb);
+              mbar_expect_tx(full_b(sb), L::kBSlot);
+              const uint32_t bdst = bslots + sb * L::kBSlot;
+              if (p.kind == kFprop) {
+                tma_load_2d(bdst, &tma_b, full_b(sb), (r * KW + s) * p.Cin + c * 64, n0);
+              } else {
+                const int ftap = (p.kh - 1 - r) * KW + (KW - 1 - s);
+#pragma unroll
+                for (int mc = 0; mc < BN / 64; ++mc)
+                  tma_load_3d(bdst + mc * 8192, &tma_b, full_b(sb), n0 + mc * 64, ftap, c * 64);
+              }
+              if (++sb == BS) {
+                sb = 0;
+                phb ^= 1;
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    // ---------------- MMA issuer ----------------
+    // Descriptors precomputed (the 14-bit start-address field advances by
+    // offset >> 4), taps unrolled, ring indices wrapped: a B sub-stage is
+    // only 8 MMAs. The whole warp runs the loop; one elected lane issues.
+    const bool leader = elect_one();
+    const bool b_mn = p.kind != kFprop;
+    const uint32_t idesc = make_idesc_bf16(BN, false, b_mn);
+    const uint64_t adesc0 = make_sdesc(base, 16, 1024, kSw128);
+    const uint64_t bdesc0 = b_mn ? make_sdesc(bslots, 8192, 1024, kSw128) : make_sdesc(bslots, 16, 1024, kSw128);
+    const uint32_t kstep_b = b_mn ? (2048 >> 4) : (32 >> 4);  // next K = 16 slice of B
+    int sa = 0, sb = 0, lt = 0;
+    uint32_t pha = 0, phb = 0;
+    const int nstage = p.nck * p.kh;
+    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      if (lt >= 2) mbar_wait(tempty(acc), ((lt >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d0 = tmem + acc * L::kAccCols;
+      uint32_t first = 1;
+      for (int st = 0; st < nstage; ++st) {
+        mbar_wait(full_a(sa), pha);
+        tc_fence_after();
+        const uint64_t ad = adesc0 + static_cast<uint64_t>((sa * L::kASlot) >> 4);
+#pragma unroll
+        for (int s = 0; s < KW; ++s) {
+          mbar_wait(full_b(sb), phb);
+          tc_fence_after();
+          const uint64_t bd = bdesc0 + static_cast<uint64_t>((sb * L::kBSlot) >> 4);
+          if (leader) {
+#pragma unroll
+            for (int kk = 0; kk < kBKb / 16; ++kk) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                tc_mma_bf16(d0 + h * BN, ad + static_cast<uint64_t>(((h * kBM + s) * 128 + kk * 32) >> 4),
+                            bd + static_cast<uint64_t>(kk * kstep_b), idesc, (first && kk == 0) ? 0u : 1u);
+            }
+            tc_commit(empty_b(sb));
+          }
+          __syncwarp();
+          first = 0;
+          if (++sb == BS) {
+            sb = 0;
+            phb ^= 1;
+          }
+        }
+        if (leader) tc_commit(empty_a(sa));
+        __syncwarp();
+        if (++sa == AS) {
+          sa = 0;
+          pha ^= 1;
+        }
+      }
+      if (leader) tc_commit(tfull(acc));
+      __syncwarp();
+    }
+  } else if (warp < 4) {
+    // ---------------- epilogue ----------------
+    const int row = warp * 32 + lane;
+    int lt = 0;
+    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      const int tn = tile % p.ntn, t2 = tile / p.ntn;
+      const int th = t2 % p.tiles_h, n = t2 / p.tiles_h;
+      const int y0 = th * p.TH, n0 = tn * BN;
+      mbar_wait_sleep(tfull(acc), (lt >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int v = h * kBM + row;
+        const int yl = v / p.P, x = v - yl * p.P, y = y0 + yl;
+        const bool valid = yl < p.TH && x < p.Wout && y < p.Hout;
+        const int64_t pix = (static_cast<int64_t>(n) * p.Hout + y) * p.Wout + x;
+        const uint32_t taddr = tmem + acc * L::kAccCols + h * BN + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+        for (int cg = 0; cg < BN / 32; ++cg) {
+          float vals[32];
+          tmem_ld32(taddr + cg * 32, vals);
+          if (h == 1 && cg == BN / 32 - 1) {
+            // last TMEM read of this accumulator set: hand it back to the MMA warp
+            tc_fence_before();
+            mbar_arrive(tempty(acc));
+          }
+          const int nb = n0 + cg * 32;
+          if (!valid || nb >= p.Cout) continue;
+          if (p.relu) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) vals[i] = fmaxf(vals[i], 0.f);
+          }
+          if (p.mask_x) {
+            const uint4* xr = reinterpret_cast<const uint4*>(p.mask_x + pix * p.Cout + nb);
+            uint4 xa[4];  // loads in flight together, then the selects
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xa[i] = __ldg(xr + i);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float f[8];
+              unpack_bf16x8(xa[i], f);
+#pragma unroll
+              for (int t = 0; t < 8; ++t) vals[8 * i + t] = f[t] > 0.f ? vals[8 * i + t] : 0.f;
+            }
+          }
+          store_row32(p.out + pix * p.Cout + nb, vals, 32, p.accum != 0);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+}  // namespace vdnnk

@@ -491,7 +491,10 @@ int Session::padded_channels(int layer) const {
   }();
   if (!on || !bf_ || l.kind != Kind::Conv || l.in.size() != 1 || g_.at(l.in[0]).kind != Kind::Input) return 0;
   const int c = static_cast<int>(g_.dims(l.in[0]).c);
-  return c % 8 == 0 ? 0 : (c + 7) / 8 * 8;
+  if (c % 8 == 0) return 0;
+  const std::vector<u64> shape_only(l.in.size(), 0);  // shapes only, no pointer is dereferenced
+  if (vdnnk::conv_bf16_c3_native(conv_args(layer, shape_only, nullptr, nullptr))) return 0;
+  return (c + 7) / 8 * 8;
 }
 
 // X and W of a padded step into the scratch; `a` then describes the padded X.
