@@ -9,6 +9,8 @@
 #include "kernels.h"
 #include "tcb_conv.cuh"
 #include "tcb_halo.cuh"
+#include "tc_conv_pair.cuh"
+#include "tcb_pair.cuh"
 #include "tma_maps.h"
 
 namespace vdnnk {
@@ -264,6 +266,39 @@ cudaError_t launch_halo_b(HaloParamsB& h, const ConvParamsB& p, cudaStream_t st)
   return cudaGetLastError();
 }
 
+// CTA-pair kernel (tcb_pair.cuh) for TMA-fed layers with 256-column tiles:
+// at least one (split, M256, N256) item per SM pair; wgrad only when every
+// 128-row half holds real weight rows (M % 256 == 0: constant stage bytes).
+// VDNN_BF16_PAIR=0 disables (A/B switch).
+bool pair_ok_b(const ConvParamsB& p, int splits) {
+  static const bool on = [] {
+    const char* e = std::getenv("VDNN_BF16_PAIR");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || !tma_ok_b(p) || tile_n(p) != 256) return false;
+  if (p.kind == kWgrad && p.M % 256 != 0) return false;
+  const int64_t items = static_cast<int64_t>((p.M + 255) / 256) * ((p.Ncols + 255) / 256) * splits;
+  return items >= kNumSmsB / 2;
+}
+
+template <int STAGES>
+cudaError_t launch_pair_b(const ConvParamsB& p, int splits, const CUtensorMap& ta, const CUtensorMap& tb,
+                          cudaStream_t st) {
+  using L = TcbPairSmem<STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(tcb_pair_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t items = static_cast<int64_t>((p.M + 255) / 256) * ((p.Ncols + 255) / 256) * splits;
+  const int grid = 2 * static_cast<int>(std::min<int64_t>(items, kNumSmsB / 2));
+  tcb_pair_kernel<STAGES><<<grid, 192, L::kTotal, st>>>(p, ta, tb, splits);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_any(const ConvParamsB& p, int splits, cudaStream_t st) {
   if (splits == 1) {
     HaloParamsB h;
@@ -277,6 +312,7 @@ cudaError_t launch_any(const ConvParamsB& p, int splits, cudaStream_t st) {
   alignas(64) CUtensorMap ta, tb;
   std::memset(&ta, 0, sizeof(ta));
   std::memset(&tb, 0, sizeof(tb));
+  if (pair_ok_b(p, splits) && make_maps_b(p, 128, &ta, &tb)) return launch_pair_b<6>(p, splits, ta, tb, st);
   if (tma_ok_b(p) && make_maps_b(p, bn, &ta, &tb)) {
     if (bn == 256) return launch_persist_b<256, 4>(p, splits, ta, tb, st);
     if (bn == 128) return launch_persist_b<128, 6>(p, splits, ta, tb, st);
@@ -489,13 +525,95 @@ cudaError_t conv_dgrad_bf16(const ConvArgs& a, const void* w, const void* dy, bo
   return cudaGetLastError();
 }
 
+// Halo WGRAD (tcb_halo.cuh) for stride-1 3x3 layers with 64-multiple input
+// channels and 64 / 128 output channels whose padded input row fits a box.
+// VDNN_BF16_HALO_WGRAD=0 disables (A/B switch).
+constexpr size_t kSmemLimitB = 227 * 1024;
+bool halo_wgb_params(const ConvParamsB& p, HaloWgParamsB& h) {
+  static const bool on = [] {
+    const char* e = std::getenv("VDNN_BF16_HALO_WGRAD");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || g_no_tma_b) return false;
+  if (p.nseg != 1 || !p.vec_in || p.tap_pack || p.stride != 1 || p.kh != p.kw || p.kh != 3) return false;
+  if (p.C % 64 != 0 || (p.Cout != 64 && p.Cout != 128) || p.pad > p.kh - 1) return false;
+  std::memset(&h, 0, sizeof(h));
+  h.N = p.N, h.H = p.H, h.W = p.W, h.C = p.C, h.Cout = p.Cout, h.kh = p.kh, h.kw = p.kw, h.pad = p.pad;
+  h.P = p.W + 2 * p.pad;
+  h.Hout = p.Ho, h.Wout = p.Wo;
+  if (h.Wout + h.kw - 1 != h.P || h.P > 240) return false;
+  h.Kp = (h.P + 15) / 16 * 16;
+  h.nck = p.C / 64;
+  const int nblk = h.kh * h.nck, gmax = 512 / (2 * p.Cout);
+  h.ngroups = (nblk + gmax - 1) / gmax;
+  h.G = (nblk + h.ngroups - 1) / h.ngroups;
+  h.nrows = h.N * h.Hout;
+  const int splits = std::max(1, kNumSmsB / h.ngroups);
+  h.rows_per = (h.nrows + splits - 1) / splits;
+  h.M = p.kh * p.kw * h.nck * 64;
+  h.a_slot = halo_wgb_a_slot(h.Kp);
+  h.b_slot = halo_wgb_b_slot(h.Kp, p.Cout);
+  h.BS = 2;
+  const size_t fixed = 1024 + 256 + static_cast<size_t>(h.BS) * h.b_slot;
+  if (fixed + 2 * static_cast<size_t>(h.a_slot) > kSmemLimitB) return false;
+  h.AS = static_cast<int>(std::min<size_t>(kHwbMaxAS, (kSmemLimitB - fixed) / h.a_slot));
+  return true;
+}
+int halo_wgb_splits(const HaloWgParamsB& h) { return (h.nrows + h.rows_per - 1) / h.rows_per; }
+size_t halo_wgb_smem(const HaloWgParamsB& h) {
+  return 1024 + 256 + static_cast<size_t>(h.BS) * h.b_slot + static_cast<size_t>(h.AS) * h.a_slot;
+}
+
+template <int BN>
+cudaError_t launch_halo_wgrad_b(HaloWgParamsB& h, const ConvParamsB& p, cudaStream_t st) {
+  alignas(64) CUtensorMap tx, tdy;
+  std::memset(&tx, 0, sizeof(tx));
+  std::memset(&tdy, 0, sizeof(tdy));
+  {
+    // X as (c, w, h, n): one padded input row of 64 channels per box (zero fill = padding)
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(h.C), static_cast<cuuint64_t>(h.W),
+                                static_cast<cuuint64_t>(h.H), static_cast<cuuint64_t>(h.N)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(h.C) * 2, static_cast<cuuint64_t>(h.W) * h.C * 2,
+                                   static_cast<cuuint64_t>(h.H) * h.W * h.C * 2};
+    const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(h.P), 1, 1};
+    if (!encode_tiled(&tx, p.seg[0].x, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
+      return cudaErrorNotSupported;
+  }
+  {
+    // dY as (co, x, y, n): one output row of 64 channels, P pixels (x >= Wout zero-filled)
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(h.Cout), static_cast<cuuint64_t>(h.Wout),
+                                static_cast<cuuint64_t>(h.Hout), static_cast<cuuint64_t>(h.N)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(h.Cout) * 2, static_cast<cuuint64_t>(h.Wout) * h.Cout * 2,
+                                   static_cast<cuuint64_t>(h.Hout) * h.Wout * h.Cout * 2};
+    const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(h.P), 1, 1};
+    if (!encode_tiled(&tdy, p.dy, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
+      return cudaErrorNotSupported;
+  }
+  const size_t smem = halo_wgb_smem(h);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(tcb_wgrad_halo_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  tcb_wgrad_halo_kernel<BN><<<halo_wgb_splits(h) * h.ngroups, 192, smem, st>>>(h, tx, tdy);
+  count_launch();
+  return cudaGetLastError();
+}
+
 size_t conv_wgrad_ws_bytes_bf16(const ConvArgs& a) {
   ConvParamsB p;
   if (!build_common_b(a, p)) return 0;
   const int M = wgrad_rows_b(p);
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
   const int s = wgrad_splits_b(p, M, P);
-  const size_t b = s > 1 ? static_cast<size_t>(s) * M * a.cout * sizeof(float) : 0;
+  size_t b = s > 1 ? static_cast<size_t>(s) * M * a.cout * sizeof(float) : 0;
+  ConvParamsB q = p;
+  q.kind = kWgrad;
+  HaloWgParamsB h;
+  if (halo_wgb_params(q, h)) b = std::max(b, static_cast<size_t>(halo_wgb_splits(h)) * h.M * a.cout * sizeof(float));
   return c3b_wgrad_eligible(a) ? std::max(b, c3b_wgrad_ws_bytes(a)) : b;
 }
 
@@ -514,6 +632,22 @@ cudaError_t conv_wgrad_bf16(const ConvArgs& a, const void* dy, void* w_mut, floa
   p.Ncols = a.cout;
   const int64_t P = static_cast<int64_t>(a.n) * p.Ho * p.Wo;
   p.kblocks = static_cast<int>((P + kBKb - 1) / kBKb);
+  {
+    HaloWgParamsB h;
+    if (ws != nullptr && halo_wgb_params(p, h) &&
+        ws_bytes >= static_cast<size_t>(halo_wgb_splits(h)) * h.M * a.cout * sizeof(float)) {
+      h.part = ws;
+      cudaError_t e = p.Cout == 64 ? launch_halo_wgrad_b<64>(h, p, st) : launch_halo_wgrad_b<128>(h, p, st);
+      if (e == cudaSuccess) {
+        p.out = ws;
+        wgrad_reduce_b_kernel<<<reduce_blocks(static_cast<int64_t>(p.Cout) * p.M), 256, 0, st>>>(
+            p, halo_wgb_splits(h), dw_out);
+        count_launch();
+        return cudaGetLastError();
+      }
+      if (e != cudaErrorNotSupported) return e;
+    }
+  }
   const size_t per = static_cast<size_t>(p.M) * a.cout * sizeof(float);
   const int splits = clamp_splits(p, ws ? wgrad_splits_b(p, p.M, P) : 1, per, ws_bytes);
   if (splits <= 1) {

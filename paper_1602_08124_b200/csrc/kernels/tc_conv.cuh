@@ -130,6 +130,15 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sr
                "r"(x), "r"(y), "r"(z)
                : "memory");
 }
+// L2 prefetch of [src, src + bytes) in 16 KB bulk requests (bytes % 16 == 0):
+// epilogue operands (the dgrad ReLU mask) warmed while the main loop runs.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint64_t bytes) {
+  const char* s = static_cast<const char*>(src);
+  for (uint64_t o = 0; o < bytes; o += 16384) {
+    const uint32_t n = static_cast<uint32_t>(bytes - o < 16384 ? bytes - o : 16384);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s + o), "r"(n) : "memory");
+  }
+}
 __device__ __forceinline__ void bulk_commit_and_drain() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

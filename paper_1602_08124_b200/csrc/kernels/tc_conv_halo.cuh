@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(192, 1) tc_conv_halo_kernel(const __grid_const
         const int tn = tile % p.ntn, t2 = tile / p.ntn;
         const int th = t2 % p.tiles_h, n = t2 / p.tiles_h;
         const int y0 = th * p.TH, n0 = tn * BN;
+        if (p.mask_x && tn == 0 && y0 < p.Hout)  // the dgrad ReLU mask into L2 (tc_conv_halo_pair.cuh)
+          prefetch_l2_bulk(p.mask_x + (static_cast<int64_t>(n) * p.Hout + y0) * p.Wout * p.Cout,
+                           static_cast<uint64_t>(min(p.TH, p.Hout - y0)) * p.Wout * p.Cout * sizeof(float));
         for (int c = 0; c < p.nck; ++c) {
           for (int r = 0; r < p.kh; ++r) {
             mbar_wait(empty_a(sa), pha);

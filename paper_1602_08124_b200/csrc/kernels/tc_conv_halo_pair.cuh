@@ -119,6 +119,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         const int thp = t2 % tiles_hp, n = t2 / tiles_hp;
         const int y0 = (2 * thp + static_cast<int>(rank)) * p.TH;
         const int nb = tn * BN + static_cast<int>(rank) * (BN / 2);
+        if (p.mask_x && tn == 0 && y0 < p.Hout) {
+          // the dgrad epilogue's ReLU mask (x rows of this CTA's output rows,
+          // every channel) into L2 while the main loop runs: its loads then
+          // hit L2 instead of serialising DRAM round trips per column group
+          const int rows = min(p.TH, p.Hout - y0);
+          prefetch_l2_bulk(p.mask_x + (static_cast<int64_t>(n) * p.Hout + y0) * p.Wout * p.Cout,
+                           static_cast<uint64_t>(rows) * p.Wout * p.Cout * sizeof(float));
+        }
         for (int c = 0; c < p.nck; ++c) {
           for (int r = 0; r < p.kh; ++r) {
             mbar_wait(empty_a(sa), pha);

@@ -111,6 +111,9 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
         const int tn = tile % p.ntn, t2 = tile / p.ntn;
         const int th = t2 % p.tiles_h, n = t2 / p.tiles_h;
         const int y0 = th * p.TH, n0 = tn * BN;
+        if (p.mask_x && tn == 0 && y0 < p.Hout)  // the dgrad ReLU mask into L2 while the main loop runs
+          prefetch_l2_bulk(p.mask_x + (static_cast<int64_t>(n) * p.Hout + y0) * p.Wout * p.Cout,
+                           static_cast<uint64_t>(min(p.TH, p.Hout - y0)) * p.Wout * p.Cout * sizeof(bf16));
         for (int c = 0; c < p.nck; ++c) {
           for (int r = 0; r < p.kh; ++r) {
             mbar_wait(empty_a(sa), pha);
@@ -255,6 +258,214 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
   if (warp == 4) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+}  // namespace vdnnk
+
+namespace vdnnk {
+
+// ------------------------------------------------------- halo WGRAD -------
+// dW[co][r][s][ci] = sum_p dY[p][co] * X[p + r*P + s][ci] on the virtual pixel
+// grid (pitch P = W + 2*pad; dY is 0 on the garbage columns x >= Wout, which
+// the TMA box's out-of-bounds fill provides). One pipeline unit is one output
+// row: B = that dY row (Cout/64 MN-major chunks of Kp pixel rows), and per
+// block (tap row r, 64-channel chunk c) of this CTA's group one TMA box of the
+// padded input row y + r - pad. A K = 16 MMA reads M = 128 rows = two
+// shifted views of that ONE staged box: MN-major chunks LBO = 128 B apart, so
+// A[(v, ci)][k] = X[k + s0 + v][ci] (SWIZZLE_128B is address-based, as for
+// the fprop halo kernel); two MMAs per K step cover the views s = 0..3 (s = 3
+// unused for 3x3: 75% of the rows useful), and every input row is staged
+// once per (r, c) instead of once per tap (the im2col wgrad stages it 9
+// times). A CTA owns G blocks (G x 2 x Cout TMEM columns) and a range of
+// rows; its fp32 partial [Cout][M] (M rows = (tap, 64-chunk, ci), the layout
+// wgrad_reduce_b_kernel sums) goes to slab z.
+struct HaloWgParamsB {
+  int N, H, W, C, Cout, kh, kw, pad, P, Kp, Hout, Wout, nck;
+  int G, ngroups, rows_per, nrows, M;
+  int AS, BS;               // ring depths (A: one padded input row per (r, c); B: one dY row)
+  uint32_t a_slot, b_slot;  // bytes per slot (1024-aligned)
+  float* part;              // [splits][Cout][M]
+};
+constexpr int kHwbMaxAS = 4;
+inline uint32_t halo_wgb_a_slot(int Kp) { return ((static_cast<uint32_t>(Kp) + 8) * 128 + 1023u) & ~1023u; }
+inline uint32_t halo_wgb_b_slot(int Kp, int bn) {
+  return ((static_cast<uint32_t>(bn / 64) * Kp * 128) + 1023u) & ~1023u;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1) tcb_wgrad_halo_kernel(const __grid_constant__ HaloWgParamsB p,
+                                                                const __grid_constant__ CUtensorMap tma_x,
+                                                                const __grid_constant__ CUtensorMap tma_dy) {
+  const int AS = p.AS, BS = p.BS;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bslots = base + AS * p.a_slot;
+  const uint32_t bars = bslots + BS * p.b_slot;
+  auto full_a = [&](int s) { return bars + 8u * s; };
+  auto empty_a = [&](int s) { return bars + 8u * (AS + s); };
+  auto full_b = [&](int s) { return bars + 8u * (2 * AS + s); };
+  auto empty_b = [&](int s) { return bars + 8u * (2 * AS + BS + s); };
+  const uint32_t done_bar = bars + 8u * (2 * AS + 2 * BS);
+  const uint32_t tmem_slot = bars + 8u * (2 * AS + 2 * BS + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int z = blockIdx.x / p.ngroups, grp = blockIdx.x - z * p.ngroups;
+  const int g0 = grp * p.G;
+  const int G = min(p.G, p.kh * p.nck - g0);  // (r, c) blocks of this CTA: index j -> block g0 + j
+  const int row0 = z * p.rows_per;
+  const int row1 = min(row0 + p.rows_per, p.nrows);
+  const int nrows = max(0, row1 - row0);
+  const int ncol = G * 2 * BN;
+  int tcols = 32;
+  while (tcols < ncol) tcols <<= 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(full_a(s), 1);
+      mbar_init(empty_a(s), 1);
+    }
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(full_b(s), 1);
+      mbar_init(empty_b(s), 1);
+    }
+    mbar_init(done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // rows the boxes never write: B rows [P, Kp) must be 0 (they meet A rows of
+  // garbage pixels), A rows [P, a_slot / 128) must be finite
+  for (int s = 0; s < AS; ++s)
+    for (uint32_t o = p.P * 128 + threadIdx.x * 16; o < p.a_slot; o += blockDim.x * 16)
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + s * p.a_slot + o), "r"(0) : "memory");
+  for (int s = 0; s < BS; ++s)
+    for (int ch = 0; ch < BN / 64; ++ch)
+      for (int o = p.P * 128 + threadIdx.x * 16; o < p.Kp * 128; o += blockDim.x * 16)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(bslots + s * p.b_slot + ch * p.Kp * 128 + o),
+                     "r"(0)
+                     : "memory");
+  fence_proxy_async();
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  if (warp == 5) {
+    // ---------------- TMA producer (one thread, in consumption order) ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_x) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_dy) : "memory");
+      int sa = 0, sb = 0;
+      uint32_t pha = 1, phb = 1;
+      const uint32_t abytes = static_cast<uint32_t>(p.P) * 128, bbytes = (BN / 64) * abytes;
+      for (int row = row0; row < row1; ++row) {
+        const int n = row / p.Hout, y = row - n * p.Hout;
+        mbar_wait(empty_b(sb), phb);
+        mbar_expect_tx(full_b(sb), bbytes);
+        for (int ch = 0; ch < BN / 64; ++ch)
+          tma_load_4d(bslots + sb * p.b_slot + ch * p.Kp * 128, &tma_dy, full_b(sb), ch * 64, 0, y, n);
+        if (++sb == BS) {
+          sb = 0;
+          phb ^= 1;
+        }
+        for (int j = 0; j < G; ++j) {
+          const int blk = g0 + j, r = blk / p.nck, c = blk - r * p.nck;
+          mbar_wait(empty_a(sa), pha);
+          mbar_expect_tx(full_a(sa), abytes);
+          tma_load_4d(base + sa * p.a_slot, &tma_x, full_a(sa), c * 64, -p.pad, y + r - p.pad, n);
+          if (++sa == AS) {
+            sa = 0;
+            pha ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = make_idesc_bf16(BN, true, true);
+    const bool leader = elect_one();
+    const int ksteps = p.Kp / 16;
+    const uint32_t lbo_b = static_cast<uint32_t>(p.Kp) * 128;
+    int sa = 0, sb = 0;
+    uint32_t pha = 0, phb = 0;
+    for (int i = 0; i < nrows; ++i) {
+      mbar_wait(full_b(sb), phb);
+      tc_fence_after();
+      const uint32_t b0 = bslots + sb * p.b_slot;
+      for (int j = 0; j < G; ++j) {
+        mbar_wait(full_a(sa), pha);
+        tc_fence_after();
+        const uint32_t a0 = base + sa * p.a_slot;
+        if (leader) {
+          for (int kk = 0; kk < ksteps; ++kk) {
+            const uint64_t bd = make_sdesc(b0 + kk * 2048, lbo_b, 1024, kSw128);
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              tc_mma_bf16(tmem + (j * 2 + q) * BN, make_sdesc(a0 + q * 256 + kk * 2048, 128, 1024, kSw128), bd, idesc,
+                          (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(empty_a(sa));
+        }
+        __syncwarp();
+        if (++sa == AS) {
+          sa = 0;
+          pha ^= 1;
+        }
+      }
+      if (leader) tc_commit(empty_b(sb));
+      __syncwarp();
+      if (++sb == BS) {
+        sb = 0;
+        phb ^= 1;
+      }
+    }
+    if (leader) {
+      if (nrows > 0)
+        tc_commit(done_bar);
+      else
+        mbar_arrive(done_bar);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: TMEM lane l = (view l / 64, ci = l % 64) ----------------
+    mbar_wait_sleep(done_bar, 0);
+    tc_fence_after();
+    const int l = warp * 32 + lane;
+    const int ci = l & 63;
+    float* dst = p.part + static_cast<int64_t>(z) * p.Cout * p.M;
+    for (int j = 0; j < G; ++j) {
+      const int blk = g0 + j, r = blk / p.nck, c = blk - r * p.nck;
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        const int s = 2 * q + (l >> 6);
+        const int m = ((r * p.kw + s) * p.nck + c) * 64 + ci;
+#pragma unroll 1
+        for (int cg = 0; cg < BN / 32; ++cg) {
+          float v[32];
+          tmem_ld32(tmem + (j * 2 + q) * BN + cg * 32 + (static_cast<uint32_t>(warp * 32) << 16), v);
+          if (s >= p.kw) continue;  // the fourth shifted view (taps past the kernel)
+          if (nrows <= 0) {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) v[t] = 0.f;
+          }
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (cg * 32 + t < p.Cout) dst[static_cast<int64_t>(cg * 32 + t) * p.M + m] = v[t];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
   }
 }
 
