@@ -285,10 +285,88 @@ __global__ void maxpool_fwd_b_kernel(const __grid_constant__ PoolDevB d, bf16* _
   }
 }
 
+// 2x2 / stride-2 pooling over one segment with no edge gaps (VGG): 32-bit
+// index math, the four 16-B window loads issued together, max / scatter from
+// registers (the generic kernels decode 64-bit indices and, backward, read
+// the window twice).
+namespace {
+bool pool2x2_fast(const PoolDevB& d) {
+  const int64_t outs8 = static_cast<int64_t>(d.n) * d.ho * d.wo * (d.ctot / 8);
+  return d.nseg == 1 && d.window == 2 && d.stride == 2 && d.h == 2 * d.ho && d.w == 2 * d.wo && d.c[0] % 8 == 0 &&
+         outs8 < (int64_t{1} << 31) && static_cast<int64_t>(d.n) * d.h * d.w * d.c[0] < (int64_t{1} << 40);
+}
+}  // namespace
+
+__global__ void maxpool2x2_fwd_b_kernel(const bf16* __restrict__ x, bf16* __restrict__ y, uint32_t total,
+                                        uint32_t cv, uint32_t wo, int w, int C) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t c8 = i % cv, t = i / cv;
+    const uint32_t ow = t % wo, nh = t / wo;  // nh = n * ho + oh: input rows 2nh, 2nh + 1
+    const size_t pitch = static_cast<size_t>(w) * C;
+    const bf16* p = x + (static_cast<size_t>(2 * nh) * w + 2 * ow) * C + c8 * 8;
+    const V8 a = ld8(p), b2 = ld8(p + C), c = ld8(p + pitch), e = ld8(p + pitch + C);
+    V8 m;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float v = a.v[k];
+      if (b2.v[k] > v) v = b2.v[k];
+      if (c.v[k] > v) v = c.v[k];
+      if (e.v[k] > v) v = e.v[k];
+      m.v[k] = v;
+    }
+    st8(y + static_cast<size_t>(i) * 8, m);
+  }
+}
+
+// first maximum in scan order gets dY (masked by x > 0 for a fused ReLU
+// backward), the other three positions 0 -- maxpool_bwd_scatter_b_kernel's rule
+__global__ void maxpool2x2_bwd_b_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dy,
+                                        bf16* __restrict__ dx, uint32_t total, uint32_t cv, uint32_t wo, int w, int C,
+                                        int msk) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t c8 = i % cv, t = i / cv;
+    const uint32_t ow = t % wo, nh = t / wo;
+    const size_t pitch = static_cast<size_t>(w) * C;
+    const size_t o = (static_cast<size_t>(2 * nh) * w + 2 * ow) * C + c8 * 8;
+    V8 v[4];
+    v[0] = ld8(x + o);
+    v[1] = ld8(x + o + C);
+    v[2] = ld8(x + o + pitch);
+    v[3] = ld8(x + o + pitch + C);
+    const V8 g = ld8(dy + static_cast<size_t>(i) * 8);
+    V8 out[4];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float m = v[0].v[k];
+#pragma unroll
+      for (int j = 1; j < 4; ++j)
+        if (v[j].v[k] > m) m = v[j].v[k];
+      bool done = false;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool hit = !done && v[j].v[k] == m;
+        out[j].v[k] = (hit && (!msk || v[j].v[k] > 0.f)) ? g.v[k] : 0.f;
+        done = done || hit;
+      }
+    }
+    st8(dx + o, out[0]);
+    st8(dx + o + C, out[1]);
+    st8(dx + o + pitch, out[2]);
+    st8(dx + o + pitch + C, out[3]);
+  }
+}
+
 cudaError_t maxpool_fwd_bf16(const PoolArgs& a, void* y, cudaStream_t st) {
   const PoolDevB d = to_dev_b(a);
   const size_t outs = static_cast<size_t>(d.n) * d.ho * d.wo * d.ctot;
   if (outs == 0) return cudaSuccess;
+  if (pool2x2_fast(d)) {
+    const uint32_t cv = static_cast<uint32_t>(d.ctot / 8), total = static_cast<uint32_t>(outs / 8);
+    maxpool2x2_fwd_b_kernel<<<grid_for(total, 2), kThreads, 0, st>>>(d.x[0], static_cast<bf16*>(y), total, cv,
+                                                                     static_cast<uint32_t>(d.wo), d.w, d.c[0]);
+    count_launch();
+    return cudaGetLastError();
+  }
   if (vec8(d))
     maxpool_fwd_b_kernel<8><<<grid_for(outs / 8, 2), kThreads, 0, st>>>(d, static_cast<bf16*>(y));
   else
@@ -420,6 +498,13 @@ cudaError_t maxpool_bwd_bf16(const PoolArgs& a, const void* dy, cudaStream_t st)
           if (e != cudaSuccess) return e;
         }
     const size_t outs = static_cast<size_t>(d.n) * d.ho * d.wo * d.ctot;
+    if (pool2x2_fast(d) && d.dx[0]) {
+      const uint32_t cv = static_cast<uint32_t>(d.ctot / 8), total = static_cast<uint32_t>(outs / 8);
+      maxpool2x2_bwd_b_kernel<<<grid_for(total, 2), kThreads, 0, st>>>(
+          d.x[0], g, d.dx[0], total, cv, static_cast<uint32_t>(d.wo), d.w, d.c[0], d.mask[0]);
+      count_launch();
+      return cudaGetLastError();
+    }
     if (v8)
       maxpool_bwd_scatter_b_kernel<8><<<grid_for(outs / 8, 2), kThreads, 0, st>>>(d, g);
     else
