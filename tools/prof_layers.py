@@ -1,6 +1,6 @@
 """Per-layer timing of one VGG-16 (or other preset) training step on the GPU.
 
-    python tools/prof_layers.py [net] [batch] [policy] [--no-tma] [--bf16]
+    python tools/prof_layers.py [net] [batch] [policy] [--no-tma] [--bf16] [--precise]
 """
 import sys
 
@@ -23,7 +23,7 @@ if policy == "none":
 else:
     d = V.dynamic_select(g, 12884901888, cm).decision
     cap = 12884901888
-s = V.Session(g, d, cm, cap, record_timeline=True)
+s = V.Session(g, d, cm, cap, record_timeline=True, precise_fp32="--precise" in sys.argv)
 s.synthetic_batch(1)
 for _ in range(3):
     s.step(0.01, want_loss=False)
