@@ -621,6 +621,18 @@ cudaError_t launch(ConvParams& p, int splits, cudaStream_t st) {
   std::memset(&tb, 0, sizeof(tb));
   std::memset(&tc, 0, sizeof(tc));
   if (g_precise) {
+    // TMA producer + split warps (the lo tiles computed from the landed hi
+    // tiles); the cp.async gathers when the maps do not apply
+    static const bool tma_precise = [] {
+      const char* e = std::getenv("VDNN_PRECISE_TMA");
+      return !e || std::atoi(e) != 0;
+    }();
+    if (tma_precise && !g_no_tma && (p.kind != kWgrad || p.wkw == kBK)) {
+      if (p.Ncols <= 64 && make_maps<64>(p, &ta, &tb, &tc))
+        return launch_bn<64, kStagesPrecise, true, true>(p, ta, tb, tc, splits, st);
+      if (p.Ncols > 64 && make_maps<128>(p, &ta, &tb, &tc))
+        return launch_bn<128, kStagesPrecise, true, true>(p, ta, tb, tc, splits, st);
+    }
     if (p.Ncols <= 64) return launch_bn<64, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
     return launch_bn<128, kStagesPrecise, true, false>(p, ta, tb, tc, splits, st);
   }

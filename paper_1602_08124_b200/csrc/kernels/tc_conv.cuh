@@ -649,6 +649,7 @@ struct TcSmem {
   static constexpr int kHalf = kABytes + kBBytes;
   static constexpr int kStage = PRECISE ? 2 * kHalf : kHalf;
   static constexpr int kTotal = STAGES * kStage + 1024 /*align slack*/ + 256 /*barriers*/;
+  static_assert(8 * (3 * STAGES + 2) <= 256, "barriers must fit their slot");
 };
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -665,10 +666,10 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 
 // lo = x - tf32_trunc(x) for every fp32 of a stage's A|B tiles (layout-agnostic
 // elementwise pass: the lo tiles mirror the hi tiles byte for byte).
-template <int BYTES>
+template <int BYTES, int NT = 128>
 __device__ __forceinline__ void split_lo(uint32_t hi, uint32_t lo, int tid) {
 #pragma unroll 4
-  for (int off = tid * 16; off < BYTES; off += 128 * 16) {
+  for (int off = tid * 16; off < BYTES; off += NT * 16) {
     uint32_t a, b, c, d;
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(hi + off));
     const float fa = __uint_as_float(a) - __uint_as_float(a & 0xFFFFE000u);
@@ -817,6 +818,10 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTo
   auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
   const uint32_t accum_bar = bar_base + 8u * (2 * STAGES);
   const uint32_t tmem_slot = bar_base + 8u * (2 * STAGES + 1);
+  // PRECISE with TMA: warps 1-3 write each landed stage's lo tiles, then
+  // arrive here; the MMA waits on split_bar instead of full_bar
+  auto split_bar = [&](int s) { return bar_base + 8u * (2 * STAGES + 2 + s); };
+  constexpr bool kSplitWarps = PRECISE && TMA;
   uint32_t* tmem_slot_ptr =
       reinterpret_cast<uint32_t*>(smem_raw + (tmem_slot - raw));
 
@@ -838,6 +843,8 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTo
       mbar_init(empty_bar(s), 1);
     }
     mbar_init(accum_bar, 1);
+    if constexpr (kSplitWarps)
+      for (int s = 0; s < STAGES; ++s) mbar_init(split_bar(s), 96);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 4) {
@@ -869,6 +876,19 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTo
           mbar_expect_tx(full_bar(s), kBytes);
           tp.issue(p, &tma_a, &tma_b, n0, sa, sa + L::kABytes, full_bar(s));
           tp.next(p);
+        }
+      }
+      if constexpr (kSplitWarps) {
+        if (warp > 0) {
+          // lo = x - tf32(x) of every landed stage (96 threads), then release it to the MMA
+          for (int it = 0; it < nkb; ++it) {
+            const int s = it % STAGES;
+            mbar_wait(full_bar(s), (it / STAGES) & 1);
+            const uint32_t sa = base + s * L::kStage;
+            split_lo<L::kHalf, 96>(sa, sa + L::kHalf, tid - 32);
+            fence_proxy_async();
+            mbar_arrive(split_bar(s));
+          }
         }
       }
       __syncwarp();
@@ -1115,7 +1135,7 @@ __global__ void __launch_bounds__(160, (TcSmem<BN, STAGES, PRECISE, BM, KW>::kTo
     for (int it = 0; it < nkb; ++it) {
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;
-      mbar_wait(full_bar(s), ph);
+      mbar_wait(kSplitWarps ? split_bar(s) : full_bar(s), ph);
       if constexpr (!TMA) fence_proxy_async();  // cp.async/st.shared writes -> async proxy
       tc_fence_after();
       const uint32_t sa = base + s * L::kStage;

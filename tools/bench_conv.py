@@ -6,8 +6,10 @@ from paper_1602_08124_b200 import _lib as L
 dev = torch.device("cuda")
 shapes = [(256, 224, 224, 64, 64), (256, 112, 112, 128, 128), (256, 56, 56, 256, 256), (256, 28, 28, 512, 512),
           (256, 14, 14, 512, 512), (256, 112, 112, 64, 128)]
-if len(sys.argv) > 1 and sys.argv[1] == "notma":
+if "notma" in sys.argv[1:]:
     L.lib().vdnn_kernel_set_tma(0)
+if "precise" in sys.argv[1:]:
+    L.lib().vdnn_kernel_set_precise(1)
 def t(fn, n=int(__import__("os").environ.get("REPS", "5"))):
     fn(); torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
