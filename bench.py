@@ -502,7 +502,7 @@ def main():
                          "TF32-exact values where only TF32 contractions read the map, a trailing p = "
                          "offload into a peer GPU's HBM (N > 1), a trailing f = fp32-accurate 3xTF32 "
                          "contractions, a trailing b = BF16 storage (elem_size 2: its own plan). Default: "
-                         "dyn,dynz,dynt,all,conv,none,dynf,nonef,dynb,noneb (N > 1: dyn,dynp,dynz,dynt,all,conv,none)")
+                         "dyn,dynz,dynt,all,conv,none,dynf,nonef,dynb,dynzb,noneb (N > 1: dyn,dynp,dynz,dynt,all,conv,none)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--precise", action="store_true", help="3xTF32 fp32-accurate contractions")
     ap.add_argument("--cpu-sample-batch", type=int, default=96,
@@ -545,7 +545,7 @@ def main():
     tf32_peak, peak_note = measured_tf32_peak(peaks, peaks_src)
 
     if args.policies is None:
-        args.policies = ("dyn,dynz,dynt,all,conv,none,dynf,nonef,dynb,noneb" if world == 1
+        args.policies = ("dyn,dynz,dynt,all,conv,none,dynf,nonef,dynb,dynzb,noneb" if world == 1
                          else "dyn,dynp,dynz,dynt,all,conv,none")
     results = {}
     for p in [x for x in args.policies.split(",") if x]:
@@ -633,6 +633,14 @@ def main():
                                             if results.get("noneb", {}).get("ms_per_step") else None),
             "speedup_vs_fp32_dyn": (round(z["images_per_s"] / head["images_per_s"], 3)
                                     if head.get("images_per_s") else None)}
+        zb = results.get("dynzb", {})
+        if zb.get("images_per_s"):
+            # the same BF16 plan with lossless zero-value-compressed transfers (bit-identical step)
+            line["bf16_storage"]["compressed_offload"] = {
+                "images_per_s": zb["images_per_s"], "ms_per_step": zb["ms_per_step"],
+                "wire_ratio": zb.get("wire_ratio"), "exposed_transfer_ms": zb.get("exposed_transfer_ms"),
+                "slowdown_vs_bf16_no_offload": (round(zb["ms_per_step"] / results["noneb"]["ms_per_step"], 4)
+                                                if results.get("noneb", {}).get("ms_per_step") else None)}
     if "dynp" in results and results["dynp"].get("images_per_s"):
         z = results["dynp"]
         line["peer_hbm_offload"] = {

@@ -431,6 +431,14 @@ vdnn_status vdnn_kernel_zvc_compress_tf32(const float* src, uint64_t count, void
                                           void* stream);
 vdnn_status vdnn_kernel_zvc_decompress(const void* host_src, uint64_t count, float* dst, uint64_t* wire,
                                        void* stream);
+/* BF16 maps (elem_size = 2): lossless zero-value-compressed copy of `count` bf16 (count % 8 == 0, 16-B
+   aligned) into a mapped pinned slot of >= vdnn_kernel_zvc_slot_bytes_bf16(2*count) bytes and back.
+   Replaces nothing in the reference (a transfer format under its schedule). */
+uint64_t vdnn_kernel_zvc_slot_bytes_bf16(uint64_t bytes);
+vdnn_status vdnn_kernel_zvc_compress_bf16(const void* src, uint64_t count, void* host_dst, uint64_t* wire,
+                                          void* stream);
+vdnn_status vdnn_kernel_zvc_decompress_bf16(const void* host_src, uint64_t count, void* dst, uint64_t* wire,
+                                            void* stream);
 /* Measured tcgen05 kind::tf32 ceiling of the current device in TFLOP/s (roofline denominator). */
 vdnn_status vdnn_kernel_tf32_peak(double* tflops);
 vdnn_status vdnn_kernel_maxpool_fwd(const vdnn_conv_desc* d, int32_t window, int32_t stride, float* y, void* stream);

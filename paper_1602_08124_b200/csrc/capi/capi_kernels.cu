@@ -68,6 +68,25 @@ vdnn_status vdnn_kernel_zvc_decompress(const void* host_src, uint64_t count, flo
                                            static_cast<cudaStream_t>(stream)),
                      "zvc_decompress");
 }
+uint64_t vdnn_kernel_zvc_slot_bytes_bf16(uint64_t bytes) { return vdnnk::zvc_slot_bytes_bf16(bytes); }
+vdnn_status vdnn_kernel_zvc_compress_bf16(const void* src, uint64_t count, void* host_dst, uint64_t* wire,
+                                          void* stream) {
+  if (!src || !host_dst || !wire) return fail(VDNN_INVALID_ARGUMENT, "null argument");
+  if (count % 8 != 0 || !vdnnk::zvc_eligible(src, count * 2) || !vdnnk::zvc_eligible(host_dst, 16))
+    return fail(VDNN_INVALID_ARGUMENT, "bf16 zvc needs count % 8 == 0 and 16-B aligned buffers");
+  return cuda_status(vdnnk::zvc_compress_bf16(src, count, host_dst, reinterpret_cast<unsigned long long*>(wire),
+                                              static_cast<cudaStream_t>(stream)),
+                     "zvc_compress_bf16");
+}
+vdnn_status vdnn_kernel_zvc_decompress_bf16(const void* host_src, uint64_t count, void* dst, uint64_t* wire,
+                                            void* stream) {
+  if (!host_src || !dst) return fail(VDNN_INVALID_ARGUMENT, "null argument");
+  if (count % 8 != 0 || !vdnnk::zvc_eligible(dst, count * 2) || !vdnnk::zvc_eligible(host_src, 16))
+    return fail(VDNN_INVALID_ARGUMENT, "bf16 zvc needs count % 8 == 0 and 16-B aligned buffers");
+  return cuda_status(vdnnk::zvc_decompress_bf16(host_src, count, dst, reinterpret_cast<unsigned long long*>(wire),
+                                                static_cast<cudaStream_t>(stream)),
+                     "zvc_decompress_bf16");
+}
 vdnn_status vdnn_kernel_tf32_peak(double* tflops) {
   if (!tflops) return fail(VDNN_INVALID_ARGUMENT, "null output");
   return cuda_status(vdnnk::tf32_peak_probe(tflops), "tf32 peak probe");

@@ -118,6 +118,16 @@ cudaError_t zvc_compress(const float* src, uint64_t count, void* host_dst, unsig
                          bool tf32 = false);
 cudaError_t zvc_decompress(const void* host_src, uint64_t count, float* dst, unsigned long long* wire,
                            cudaStream_t st);
+// BF16 maps (elem_size = 2): chunks of 2048 bf16, a 64-bit zero mask per lane,
+// nonzeros as u16 or (narrow top bytes) 1.5 B each; `count` = bf16 elements
+// (multiple of 8). Lossless: every restored bit pattern equals the original.
+constexpr int kZvcbChunk = 2048;
+constexpr int kZvcbSlot = 256 + 16 + 2 * kZvcbChunk;  // mask + header + dense values (worst case)
+uint64_t zvc_slot_bytes_bf16(uint64_t bytes);
+cudaError_t zvc_compress_bf16(const void* src, uint64_t count, void* host_dst, unsigned long long* wire,
+                              cudaStream_t st);
+cudaError_t zvc_decompress_bf16(const void* host_src, uint64_t count, void* dst, unsigned long long* wire,
+                                cudaStream_t st);
 // Data-parallel exchange over peer memory (peer.cu): barrier flags and the
 // fused reduce + SGD + broadcast of the weight gradients.
 constexpr int kPeerMaxRanks = 8;

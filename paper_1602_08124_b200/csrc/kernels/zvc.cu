@@ -260,6 +260,170 @@ __global__ void __launch_bounds__(kWarps * 32) zvc_decompress_kernel(const uint8
   if (lane == 0 && bytes && wire) atomicAdd(wire, bytes);
 }
 
+// ---------------------------------------------------------------- BF16 ----
+// Per 2048-bf16 chunk c, at byte c * kZvcbSlot of the host slot:
+//   u32 mask[64]   lane l's words 2l (bits of its uint4 groups j = 0..3) and
+//                  2l + 1 (j = 4..7): bit 8(j & 3) + e <-> bf16 8*(32j + l) + e
+//   u32 hdr[4]     hdr[0] = mode, hdr[1] = top byte base, hdr[2] = nonzeros
+//   mode 0: u16 vals[nnz] lane-major (lane 0's nonzeros in (j, e) order, ...)
+//   mode 1: u8 lo[nnz] (the low byte: exponent LSB + 7 mantissa bits), padded
+//           to 16 B, then u8 nib[(nnz+1)/2]: the top byte (sign + 7 exponent
+//           bits) as a 4-bit offset from hdr[1], two per byte -- when a
+//           chunk's top bytes span <= 15 (ReLU maps: positive, a few octaves).
+// A value is "zero" only as the bit pattern 0x0000 (-0.0, NaN, denormals kept).
+__global__ void __launch_bounds__(kWarps * 32) zvcb_compress_kernel(const uint4* __restrict__ src, int64_t n8,
+                                                                    uint8_t* __restrict__ dst,
+                                                                    unsigned long long* __restrict__ wire) {
+  __shared__ __align__(16) uint16_t stage[kWarps][kZvcbChunk + 16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nchunks = (n8 + kZvcbChunk / 8 - 1) / (kZvcbChunk / 8);
+  unsigned long long bytes = 0;
+  uint16_t* st = stage[warp];
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(kWarps) + warp; c < nchunks;
+       c += static_cast<int64_t>(gridDim.x) * kWarps) {
+    const int64_t b8 = c * (kZvcbChunk / 8);
+    uint4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t i = b8 + j * 32 + lane;
+      v[j] = i < n8 ? __ldcs(src + i) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    uint32_t m[2] = {0u, 0u}, tmin = 255, tmax = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t h = (w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+        if (h != 0u) {
+          m[j >> 2] |= 1u << (8 * (j & 3) + e);
+          tmin = min(tmin, h >> 8);
+          tmax = max(tmax, h >> 8);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+      tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    }
+    uint32_t total;
+    uint32_t k = warp_excl_scan(__popc(m[0]) + __popc(m[1]), total);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t h = (w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+        if (h != 0u) st[k++] = static_cast<uint16_t>(h);
+      }
+    }
+    __syncwarp();
+    uint8_t* out = dst + c * kZvcbSlot;
+    reinterpret_cast<uint2*>(out)[lane] = make_uint2(m[0], m[1]);
+    const uint32_t mode = (total > 0 && tmax - tmin <= 15u) ? 1u : 0u;
+    if (lane == 0) *reinterpret_cast<uint4*>(out + 256) = make_uint4(mode, tmin, total, 0u);
+    uint32_t payload;
+    if (mode == 0) {
+      payload = pad16(2 * total);
+    } else {
+      // pack in place: every lane reads its values (pairs p = lane + 32i)
+      // into registers first, then writes the low bytes and nibble bytes
+      const uint32_t npairs = (total + 1) / 2;
+      uint32_t w[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t pr = lane + 32u * i;
+        w[i] = pr < npairs ? (static_cast<uint32_t>(st[2 * pr]) |
+                              (2 * pr + 1 < total ? static_cast<uint32_t>(st[2 * pr + 1]) << 16 : 0u))
+                           : 0u;
+      }
+      __syncwarp();
+      uint8_t* pk = reinterpret_cast<uint8_t*>(st);
+      const uint32_t off1 = pad16(total);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t pr = lane + 32u * i;
+        if (pr >= npairs) continue;
+        const uint32_t a = w[i] & 0xFFFFu, b = w[i] >> 16;
+        pk[2 * pr] = static_cast<uint8_t>(a & 0xFFu);
+        if (2 * pr + 1 < total) pk[2 * pr + 1] = static_cast<uint8_t>(b & 0xFFu);
+        const uint32_t hi = (2 * pr + 1 < total) ? ((b >> 8) - tmin) : 0u;
+        pk[off1 + pr] = static_cast<uint8_t>(((a >> 8) - tmin) | (hi << 4));
+      }
+      __syncwarp();
+      payload = off1 + pad16(npairs);
+    }
+    warp_copy_out(reinterpret_cast<const float*>(st), out + 256 + kHdr, payload, lane);
+    __syncwarp();
+    bytes += 256 + kHdr + payload;
+  }
+  if (lane == 0 && bytes) atomicAdd(wire, bytes);
+}
+
+__global__ void __launch_bounds__(kWarps * 32) zvcb_decompress_kernel(const uint8_t* __restrict__ srcb, int64_t n8,
+                                                                      uint4* __restrict__ dst,
+                                                                      unsigned long long* __restrict__ wire) {
+  __shared__ __align__(16) uint16_t stage[kWarps][kZvcbChunk + 16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nchunks = (n8 + kZvcbChunk / 8 - 1) / (kZvcbChunk / 8);
+  unsigned long long bytes = 0;
+  uint16_t* st = stage[warp];
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(kWarps) + warp; c < nchunks;
+       c += static_cast<int64_t>(gridDim.x) * kWarps) {
+    const uint8_t* in = srcb + c * kZvcbSlot;
+    const uint2 mm = __ldcs(reinterpret_cast<const uint2*>(in) + lane);
+    const uint4 hdr = __ldcs(reinterpret_cast<const uint4*>(in + 256));
+    const uint32_t m[2] = {mm.x, mm.y};
+    uint32_t total;
+    uint32_t k = warp_excl_scan(__popc(m[0]) + __popc(m[1]), total);
+    const uint32_t payload = hdr.x == 0 ? pad16(2 * total) : pad16(total) + pad16((total + 1) / 2);
+    {
+      const uint4* i4 = reinterpret_cast<const uint4*>(in + 256 + kHdr);
+      uint4* st4 = reinterpret_cast<uint4*>(st);
+      for (uint32_t i = lane; i < payload / 16; i += 32) st4[i] = __ldcs(i4 + i);
+    }
+    __syncwarp();
+    if (hdr.x == 1) {  // unpack to u16 in place (read every pair into registers first)
+      const uint8_t* pk = reinterpret_cast<const uint8_t*>(st);
+      const uint32_t off1 = pad16(total), npairs = (total + 1) / 2;
+      uint32_t w[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t pr = lane + 32u * i;
+        if (pr >= npairs) continue;
+        const uint32_t nb = pk[off1 + pr];
+        const uint32_t a = static_cast<uint32_t>(pk[2 * pr]) | (((nb & 15u) + hdr.y) << 8);
+        const uint32_t b = (2 * pr + 1 < total) ? (static_cast<uint32_t>(pk[2 * pr + 1]) | (((nb >> 4) + hdr.y) << 8))
+                                                : 0u;
+        w[i] = a | (b << 16);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t pr = lane + 32u * i;
+        if (pr >= npairs) continue;
+        st[2 * pr] = static_cast<uint16_t>(w[i] & 0xFFFFu);
+        if (2 * pr + 1 < total) st[2 * pr + 1] = static_cast<uint16_t>(w[i] >> 16);
+      }
+      __syncwarp();
+    }
+    const int64_t b8 = c * (kZvcbChunk / 8);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if ((m[j >> 2] >> (8 * (j & 3) + e)) & 1u) w[e >> 1] |= static_cast<uint32_t>(st[k++]) << (16 * (e & 1));
+      const int64_t i = b8 + j * 32 + lane;
+      if (i < n8) dst[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    __syncwarp();
+    bytes += 256 + kHdr + payload;
+  }
+  if (lane == 0 && bytes && wire) atomicAdd(wire, bytes);
+}
+
 // Enough resident warps to keep ~50 GB/s of PCIe requests in flight, few
 // enough (and light enough: 33 KB smem, 256 threads) to co-reside with the
 // conv kernels on the compute stream.
@@ -277,6 +441,35 @@ int zvc_grid(int64_t nchunks) {
 }
 
 }  // namespace
+
+uint64_t zvc_slot_bytes_bf16(uint64_t bytes) {
+  const uint64_t n = bytes / 2;
+  return ((n + kZvcbChunk - 1) / kZvcbChunk) * kZvcbSlot;
+}
+
+cudaError_t zvc_compress_bf16(const void* src, uint64_t count, void* dst, unsigned long long* wire,
+                              cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  if (count % 8 != 0) return cudaErrorInvalidValue;
+  const int64_t n8 = static_cast<int64_t>(count / 8);
+  const int64_t nchunks = (n8 + kZvcbChunk / 8 - 1) / (kZvcbChunk / 8);
+  zvcb_compress_kernel<<<zvc_grid(nchunks), kWarps * 32, 0, st>>>(static_cast<const uint4*>(src), n8,
+                                                                   static_cast<uint8_t*>(dst), wire);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t zvc_decompress_bf16(const void* src, uint64_t count, void* dst, unsigned long long* wire,
+                                cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  if (count % 8 != 0) return cudaErrorInvalidValue;
+  const int64_t n8 = static_cast<int64_t>(count / 8);
+  const int64_t nchunks = (n8 + kZvcbChunk / 8 - 1) / (kZvcbChunk / 8);
+  zvcb_decompress_kernel<<<zvc_grid(nchunks), kWarps * 32, 0, st>>>(static_cast<const uint8_t*>(src), n8,
+                                                                     static_cast<uint4*>(dst), wire);
+  count_launch();
+  return cudaGetLastError();
+}
 
 uint64_t zvc_slot_bytes(uint64_t bytes) {
   const uint64_t n = bytes / 4;

@@ -73,8 +73,8 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
   bf_ = c_.elem == 2;
   es_ = c_.elem;
   if (bf_ && o_.precise) throw PlanError(Err::Config, "precise (3xTF32) contractions apply to fp32 storage");
-  if (bf_ && o_.compress_offload)
-    throw PlanError(Err::Config, "compressed offload applies to fp32 storage (bf16 maps travel as stored)");
+  if (bf_ && o_.compress_offload == 2)
+    throw PlanError(Err::Config, "TF32-exact transfers apply to fp32 storage (bf16 maps use the lossless format)");
   if (o_.offload_target != 0 && o_.compress_offload)
     throw PlanError(Err::Config, "compressed offload targets the pinned host arena only");
   plan_ = vdnnp::plan(g_, d_, c_, cap_, {}, &prog_);
@@ -110,8 +110,8 @@ Session::Session(const Net& g, const Decision& d, const Cost& c, u64 capacity, c
     if (x.to_host && host_slot_[static_cast<size_t>(x.owner)] == kNoOff) {
       host_slot_[static_cast<size_t>(x.owner)] = host_bytes_;
       // compressed mode: a slot holds the worst case (every chunk dense + its mask)
-      host_bytes_ += round_up(o_.compress_offload ? std::max<u64>(x.bytes, vdnnk::zvc_slot_bytes(x.bytes)) : x.bytes,
-                              4096);
+      const u64 slot = bf_ ? vdnnk::zvc_slot_bytes_bf16(x.bytes) : vdnnk::zvc_slot_bytes(x.bytes);
+      host_bytes_ += round_up(o_.compress_offload ? std::max<u64>(x.bytes, slot) : x.bytes, 4096);
     }
   if (host_bytes_ > 0 && o_.offload_target == 0 && !o_.host_arena)
     throw PlanError(Err::Config, "plan offloads but the host arena is disabled");
@@ -653,7 +653,8 @@ void Session::run_fwd(const FwdStep& s, float lr) {
     for (const Transfer& t : s.offloads) {
       if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev)], ms_), "record");
       if (t.zvc)
-        check(vdnnk::zvc_compress(F(t.dev_off), t.bytes / 4, host_dev_ + t.host_off, wire_, ms_, t.tf32),
+        check(bf_ ? vdnnk::zvc_compress_bf16(F(t.dev_off), t.bytes / 2, host_dev_ + t.host_off, wire_, ms_)
+                  : vdnnk::zvc_compress(F(t.dev_off), t.bytes / 4, host_dev_ + t.host_off, wire_, ms_, t.tf32),
               "zvc offload");
       else {
         check(cudaMemcpyAsync(host_ + t.host_off, base_ + t.dev_off, t.bytes, cudaMemcpyDefault, ms_), "offload copy");
@@ -731,7 +732,8 @@ void Session::run_bwd(const BwdStep& s, float lr) {
     for (const Transfer& t : s.prefetches) {
       if (timed_) check(cudaEventRecord(ev_[2 * (fwd_.size() + bwd_.size() + t.ev)], ms_), "record");
       if (t.zvc)
-        check(vdnnk::zvc_decompress(host_dev_ + t.host_off, t.bytes / 4, F(t.dev_off), wire_ + 1, ms_),
+        check(bf_ ? vdnnk::zvc_decompress_bf16(host_dev_ + t.host_off, t.bytes / 2, F(t.dev_off), wire_ + 1, ms_)
+                  : vdnnk::zvc_decompress(host_dev_ + t.host_off, t.bytes / 4, F(t.dev_off), wire_ + 1, ms_),
               "zvc prefetch");
       else {
         check(cudaMemcpyAsync(base_ + t.dev_off, host_ + t.host_off, t.bytes, cudaMemcpyDefault, ms_), "prefetch copy");

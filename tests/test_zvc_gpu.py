@@ -229,3 +229,110 @@ def test_tf32_exact_session_bit_identical(net, batch):
         assert np.array_equal(a.view(np.int32), b.view(np.int32))
     assert t2["offload_wire"] == t2["prefetch_wire"]
     assert t2["offload_wire"] < t1["offload_wire"]
+
+
+# ------------------------------------------------------------------ BF16 ----
+# BF16 maps (elem_size = 2, kernels/zvc.cu zvcb_*): per 2048-bf16 chunk a
+# 256-B mask + 16-B header, then the nonzeros as u16 or -- when their top
+# bytes span <= 15 -- one low byte each plus a 4-bit top-byte offset.
+
+def _expected_wire_bf16(bits):
+    u = bits.cpu().numpy().view(np.uint16)
+    n = u.size
+    u = np.concatenate([u, np.zeros((-n) % 2048, dtype=np.uint16)]).reshape(-1, 2048)
+    total = 0
+    for row in u:
+        nzv = row[row != 0]
+        nnz = nzv.size
+        top = nzv >> 8
+        if nnz and int(top.max()) - int(top.min()) <= 15:
+            total += 272 + _pad16(nnz) + _pad16((nnz + 1) // 2)
+        else:
+            total += 272 + _pad16(2 * nnz)
+    return total
+
+
+def _roundtrip_bf16(bits):
+    """bits: int16 CUDA tensor of bf16 bit patterns (numel % 8 == 0)."""
+    n = bits.numel()
+    lib = L.lib()
+    slot = lib.vdnn_kernel_zvc_slot_bytes_bf16(C.c_uint64(2 * n))
+    host = torch.empty(slot // 4 + 4, dtype=torch.float32).pin_memory()
+    host.fill_(float("nan"))
+    wire = torch.zeros(2, dtype=torch.int64, device="cuda")
+    y = torch.full_like(bits, 0x3F80)
+    assert lib.vdnn_kernel_zvc_compress_bf16(C.c_void_p(bits.data_ptr()), C.c_uint64(n), C.c_void_p(host.data_ptr()),
+                                             C.c_void_p(wire.data_ptr()), None) == 0, lib.vdnn_last_error()
+    assert lib.vdnn_kernel_zvc_decompress_bf16(C.c_void_p(host.data_ptr()), C.c_uint64(n), C.c_void_p(y.data_ptr()),
+                                               C.c_void_p(wire.data_ptr() + 8), None) == 0, lib.vdnn_last_error()
+    torch.cuda.synchronize()
+    assert torch.equal(bits, y), "bf16 round trip not bit-exact"
+    w = wire.cpu().tolist()
+    assert w[0] == w[1] == _expected_wire_bf16(bits)
+    return w[0]
+
+
+def _relu_bits(n, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.relu(torch.randn(n, device="cuda", generator=g)).to(torch.bfloat16)
+    return x.view(torch.int16).contiguous()
+
+
+@pytest.mark.parametrize("n", [8, 2048, 2056, 2048 * 5 + 16, 1 << 20])
+def test_zvc_bf16_roundtrip_relu_like(n):
+    w = _roundtrip_bf16(_relu_bits(n, n))
+    if n >= 2048:
+        assert w < 2 * n * 0.6  # about half zeros: mask + 1.5 B per nonzero
+
+
+def test_zvc_bf16_special_values_and_modes():
+    # -0.0, NaN, Inf, denormals are values (only 0x0000 is a zero); a chunk with
+    # a wide exponent span takes the u16 mode, a narrow one the packed mode
+    specials = torch.tensor([0x8000, 0x7FC0, 0x7F80, 0xFF80, 0x0001, 0x807F, 0x3F80, 0x0000], dtype=torch.int32)
+    specials = (specials - (specials > 32767).to(torch.int32) * 65536).to(torch.int16)
+    wide = specials.repeat(2048 // 8 * 3).cuda()
+    _roundtrip_bf16(wide)
+    narrow = torch.full((4096,), 0x3F81, dtype=torch.int16, device="cuda")
+    narrow[::3] = 0
+    narrow[1::7] = 0x4000
+    _roundtrip_bf16(narrow)
+    _roundtrip_bf16(torch.zeros(2048 * 2, dtype=torch.int16, device="cuda"))       # all zero: 272 B a chunk
+    _roundtrip_bf16(torch.full((2048 * 2,), 0x4049, dtype=torch.int16, device="cuda"))  # dense, one top byte
+    odd = _relu_bits(2048 + 8, 3)
+    odd[-1] = 0x3F80  # a chunk whose nonzero count is odd at the end
+    _roundtrip_bf16(odd)
+
+
+def test_zvc_bf16_rejects_bad_arguments():
+    lib = L.lib()
+    x = torch.zeros(16, dtype=torch.int16, device="cuda")
+    assert lib.vdnn_kernel_zvc_compress_bf16(C.c_void_p(x.data_ptr()), C.c_uint64(12), None, None, None) == \
+        L.INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("net,batch", [("alexnet", 16), ("inception_toy", 16)])
+def test_compressed_session_bit_identical_bf16(net, batch):
+    """BF16 storage (elem_size = 2) with lossless compressed transfers: losses
+    and weights after two steps equal the copy-engine BF16 run bit for bit."""
+    g = V.build_preset(net, batch)
+    cm = V.CostModel()
+    cm.elem_size = 2
+    d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
+    cap = 8 << 30
+
+    def run(compress):
+        s = V.Session(g, d, cm, cap, compress_offload=compress)
+        s.synthetic_batch(7)
+        losses = [s.step(0.01) for _ in range(2)]
+        ws = [s.get_weights(l.id) for l in g.layers() if l.kind in (V.LayerKind.Conv, V.LayerKind.Fc)]
+        return losses, ws, s.transfer_stats()
+
+    l0, w0, t0 = run(False)
+    l1, w1, t1 = run(True)
+    assert l0 == l1
+    for a, b in zip(w0, w1):
+        assert np.array_equal(a.view(np.int32), b.view(np.int32))
+    assert t1["offload_wire"] == t1["prefetch_wire"]
+    assert t1["offload_wire"] < t1["offload_planned"]
+    with pytest.raises(V.VdnnError):
+        V.Session(g, d, cm, cap, compress_offload="tf32")
