@@ -703,42 +703,6 @@ template <int BN, class Drained>
 __device__ __forceinline__ void tcb_epilogue(const ConvParamsB& p, uint32_t taddr, int m0, int n0, int z, int row,
                                              bool zero, Drained drained) {
   const int m = m0 + row;
-  if (p.kind == kWgrad && p.epi == kEpiSgd) {
-    // fused SGD: the W values of the next column group are loaded while this
-    // group is updated (each thread owns one weight column widx and its BN
-    // rows co; a W element is read and written by that thread only), so the
-    // tile pays one W round trip instead of BN / 32 (FC layers: K = batch is
-    // a few K blocks and the epilogue is most of the tile)
-    bool valid = false;
-    const int widx = m < p.M ? wgrad_widx_b(p, m, valid) : 0;
-    uint16_t wc[32], wn[32];
-    auto load = [&](int cg, uint16_t(&w)[32]) {
-      const int nb = n0 + cg * 32;
-      const uint16_t* col = reinterpret_cast<const uint16_t*>(p.w_mut) + static_cast<int64_t>(nb) * p.KK + widx;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) w[i] = (valid && nb + i < p.Cout) ? col[static_cast<int64_t>(i) * p.KK] : 0;
-    };
-    load(0, wc);
-#pragma unroll 1
-    for (int cg = 0; cg < BN / 32; ++cg) {
-      float v[32];
-      tmem_ld32(taddr + cg * 32, v);
-      if (cg == BN / 32 - 1) drained();
-      if (cg + 1 < BN / 32) load(cg + 1, wn);
-      const int nb = n0 + cg * 32;
-      if (valid) {
-        bf16* col = p.w_mut + static_cast<int64_t>(nb) * p.KK + widx;
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (nb + i < p.Cout)
-            col[static_cast<int64_t>(i) * p.KK] =
-                __float2bfloat16_rn(__uint_as_float(static_cast<uint32_t>(wc[i]) << 16) - p.lr * (zero ? 0.f : v[i]));
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) wc[i] = wn[i];
-    }
-    return;
-  }
 #pragma unroll 1
   for (int cg = 0; cg < BN / 32; ++cg) {
     float v[32];

@@ -211,51 +211,16 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
       const int tn = tile % p.ntn, t2 = tile / p.ntn;
       const int th = t2 % p.tiles_h, n = t2 / p.tiles_h;
       const int y0 = th * p.TH, n0 = tn * BN;
-      // dgrad ReLU mask signs, one bit per output column, loaded BEFORE the
-      // accumulator wait: the loads overlap this tile's MMAs instead of
-      // exposing one round trip per column group
-      uint32_t mbits[2][BN / 32];
-      if (p.mask_x) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int v = h * kBM + row;
-          const int yl = v / p.P, x = v - yl * p.P, y = y0 + yl;
-          const bool valid = yl < p.TH && x < p.Wout && y < p.Hout;
-          const int64_t pix = (static_cast<int64_t>(n) * p.Hout + y) * p.Wout + x;
-#pragma unroll
-          for (int cg = 0; cg < BN / 32; ++cg) {
-            const int nb = n0 + cg * 32;
-            uint32_t bits = 0;
-            if (valid && nb < p.Cout) {
-              const uint4* xr = reinterpret_cast<const uint4*>(p.mask_x + pix * p.Cout + nb);
-              uint4 xa[4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) xa[i] = __ldg(xr + i);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const uint32_t w[4] = {xa[i].x, xa[i].y, xa[i].z, xa[i].w};
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                  const uint32_t hb = (w[t >> 1] >> (16 * (t & 1))) & 0xFFFFu;
-                  // bf16 x > 0: sign clear and not +0 (NaN compares false: its bits are > 0x7F80)
-                  bits |= ((hb != 0u && hb <= 0x7F80u) ? 1u : 0u) << (8 * i + t);
-                }
-              }
-            }
-            mbits[h][cg] = bits;
-          }
-        }
-      }
       mbar_wait_sleep(tfull(acc), (lt >> 1) & 1);
       tc_fence_after();
-#pragma unroll
+#pragma unroll 1
       for (int h = 0; h < 2; ++h) {
         const int v = h * kBM + row;
         const int yl = v / p.P, x = v - yl * p.P, y = y0 + yl;
         const bool valid = yl < p.TH && x < p.Wout && y < p.Hout;
         const int64_t pix = (static_cast<int64_t>(n) * p.Hout + y) * p.Wout + x;
         const uint32_t taddr = tmem + acc * L::kAccCols + h * BN + (static_cast<uint32_t>(warp * 32) << 16);
-#pragma unroll
+#pragma unroll 1
         for (int cg = 0; cg < BN / 32; ++cg) {
           float vals[32];
           tmem_ld32(taddr + cg * 32, vals);
@@ -271,9 +236,17 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
             for (int i = 0; i < 32; ++i) vals[i] = fmaxf(vals[i], 0.f);
           }
           if (p.mask_x) {
-            const uint32_t bits = mbits[h][cg];
+            const uint4* xr = reinterpret_cast<const uint4*>(p.mask_x + pix * p.Cout + nb);
+            uint4 xa[4];  // loads in flight together, then the selects
 #pragma unroll
-            for (int i = 0; i < 32; ++i) vals[i] = ((bits >> i) & 1u) ? vals[i] : 0.f;
+            for (int i = 0; i < 4; ++i) xa[i] = __ldg(xr + i);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float f[8];
+              unpack_bf16x8(xa[i], f);
+#pragma unroll
+              for (int t = 0; t < 8; ++t) vals[8 * i + t] = f[t] > 0.f ? vals[8 * i + t] : 0.f;
+            }
           }
           store_row32(p.out + pix * p.Cout + nb, vals, 32, p.accum != 0);
         }

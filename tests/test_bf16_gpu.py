@@ -183,8 +183,10 @@ def test_bf16_rejects_fp32_only_modes():
     d = V.static_decision(V.PolicyKind.VdnnAll, V.AlgoMode.MemoryOptimal, g, cm)
     with pytest.raises(V.VdnnError, match="3xTF32"):
         V.Session(g, d, cm, 64 << 20, precise_fp32=True)
-    with pytest.raises(V.VdnnError, match="compressed offload"):
-        V.Session(g, d, cm, 64 << 20, compress_offload=True)
+    # lossless compression applies to bf16 maps too (tests/test_zvc_gpu.py);
+    # the TF32-exact format is fp32-only
+    with pytest.raises(V.VdnnError, match="TF32-exact"):
+        V.Session(g, d, cm, 64 << 20, compress_offload="tf32")
 
 
 def test_cpasync_gathers_bf16():

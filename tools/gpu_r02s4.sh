@@ -1,5 +1,1 @@
-mkdir -p gpurun_out/r02s4_sanitizer
-for t in memcheck racecheck synccheck; do
-  timeout 1500 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize_step.py > gpurun_out/r02s4_sanitizer/$t.log 2>&1
-  echo "$t rc=$?"; tail -n 3 gpurun_out/r02s4_sanitizer/$t.log
-done
+timeout 900 python -m pytest tests/test_bf16_gpu.py -x -q 2>&1 | tail -n 2
