@@ -218,7 +218,7 @@ bool halo_params_b(const ConvParamsB& p, HaloParamsB& h) {
   return true;
 }
 
-template <int BN, int AS, int BS>
+template <int BN, int AS, int BS, bool RESB = false>
 cudaError_t launch_halo_b(HaloParamsB& h, const ConvParamsB& p, cudaStream_t st) {
   using L = HaloSmemB<BN, AS, BS>;
   alignas(64) CUtensorMap ta, tb;
@@ -254,14 +254,15 @@ cudaError_t launch_halo_b(HaloParamsB& h, const ConvParamsB& p, cudaStream_t st)
   }
   h.ntn = (h.Cout + BN - 1) / BN;
   h.ntiles = h.N * h.tiles_h * h.ntn;
+  if (RESB && (h.ntn != 1 || h.nck * h.kh * 3 != BS)) return cudaErrorNotSupported;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(tcb_halo_kernel<BN, AS, BS, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    cudaError_t e = cudaFuncSetAttribute(tcb_halo_kernel<BN, AS, BS, 3, RESB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  tcb_halo_kernel<BN, AS, BS, 3><<<std::min(h.ntiles, kNumSmsB), 192, L::kTotal, st>>>(h, ta, tb);
+  tcb_halo_kernel<BN, AS, BS, 3, RESB><<<std::min(h.ntiles, kNumSmsB), 192, L::kTotal, st>>>(h, ta, tb);
   count_launch();
   return cudaGetLastError();
 }
@@ -303,7 +304,14 @@ cudaError_t launch_any(const ConvParamsB& p, int splits, cudaStream_t st) {
   if (splits == 1) {
     HaloParamsB h;
     if (halo_params_b(p, h)) {
-      const cudaError_t e = h.Cout <= 64 ? launch_halo_b<64, 4, 8>(h, p, st) : launch_halo_b<128, 4, 4>(h, p, st);
+      static const bool resb = [] {  // VDNN_BF16_HALO_RESB=0: stream the filter per tile (A/B switch)
+        const char* e = std::getenv("VDNN_BF16_HALO_RESB");
+        return !e || std::atoi(e) != 0;
+      }();
+      cudaError_t e = cudaErrorNotSupported;
+      if (resb && h.Cout == 64 && h.nck == 1) e = launch_halo_b<64, 4, 9, true>(h, p, st);  // 64 -> 64: 72 KB filter
+      if (e == cudaErrorNotSupported)
+        e = h.Cout <= 64 ? launch_halo_b<64, 4, 8>(h, p, st) : launch_halo_b<128, 4, 4>(h, p, st);
       if (e != cudaErrorNotSupported) return e;
     }
   }

@@ -52,7 +52,11 @@ struct HaloSmemB {
   static_assert(2 * kAccCols <= 512, "two accumulator sets must fit TMEM");
 };
 
-template <int BN, int AS, int BS, int KW>
+// RESB: the whole filter (nck x kh x KW slots of BN x 64) is loaded once per
+// CTA and stays resident (BS = that slot count): the per-tile B stream --
+// 72 KB per 256 virtual rows at 64 -> 64 channels, 45% of the L2 -> SM fill
+// -- disappears (224x224x64 fprop / dgrad).
+template <int BN, int AS, int BS, int KW, bool RESB = false>
 __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant__ HaloParamsB p,
                                                           const __grid_constant__ CUtensorMap tma_a,
                                                           const __grid_constant__ CUtensorMap tma_b) {
@@ -107,6 +111,21 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
       int sa = 0, sb = 0;
       uint32_t pha = 1, phb = 1;  // the first pass over each ring does not wait
+      if constexpr (RESB) {  // the whole filter, once, on full_b(0) (host: ntn == 1)
+        mbar_expect_tx(full_b(0), static_cast<uint32_t>(BS) * L::kBSlot);
+        for (int c = 0; c < p.nck; ++c)
+          for (int r = 0; r < p.kh; ++r)
+            for (int s = 0; s < KW; ++s) {
+              const uint32_t bdst = bslots + ((c * p.kh + r) * KW + s) * L::kBSlot;
+              if (p.kind == kFprop) {
+                tma_load_2d(bdst, &tma_b, full_b(0), (r * KW + s) * p.Cin + c * 64, 0);
+              } else {
+                const int ftap = (p.kh - 1 - r) * KW + (KW - 1 - s);
+                for (int mc = 0; mc < BN / 64; ++mc)
+                  tma_load_3d(bdst + mc * 8192, &tma_b, full_b(0), mc * 64, ftap, c * 64);
+              }
+            }
+      }
       for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
         const int tn = tile % p.ntn, t2 = tile / p.ntn;
         const int th = t2 % p.tiles_h, n = t2 / p.tiles_h;
@@ -125,6 +144,7 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
             }
 #pragma unroll
             for (int s = 0; s < KW; ++s) {
+              if constexpr (RESB) continue;
               mbar_wait(empty_b(sb), phb);
               mbar_expect_tx(full_b(sb), L::kBSlot);
               const uint32_t bdst = bslots + sb * L::kBSlot;
@@ -160,6 +180,7 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
     int sa = 0, sb = 0, lt = 0;
     uint32_t pha = 0, phb = 0;
     const int nstage = p.nck * p.kh;
+    if constexpr (RESB) mbar_wait(full_b(0), 0);
     for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++lt) {
       const int acc = lt & 1;
       if (lt >= 2) mbar_wait(tempty(acc), ((lt >> 1) & 1) ^ 1);
@@ -172,8 +193,12 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
         const uint64_t ad = adesc0 + static_cast<uint64_t>((sa * L::kASlot) >> 4);
 #pragma unroll
         for (int s = 0; s < KW; ++s) {
-          mbar_wait(full_b(sb), phb);
-          tc_fence_after();
+          if constexpr (RESB) {
+            sb = st * KW + s;
+          } else {
+            mbar_wait(full_b(sb), phb);
+            tc_fence_after();
+          }
           const uint64_t bd = bdesc0 + static_cast<uint64_t>((sb * L::kBSlot) >> 4);
           if (leader) {
 #pragma unroll
@@ -183,10 +208,11 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
                 tc_mma_bf16(d0 + h * BN, ad + static_cast<uint64_t>(((h * kBM + s) * 128 + kk * 32) >> 4),
                             bd + static_cast<uint64_t>(kk * kstep_b), idesc, (first && kk == 0) ? 0u : 1u);
             }
-            tc_commit(empty_b(sb));
+            if constexpr (!RESB) tc_commit(empty_b(sb));
           }
           __syncwarp();
           first = 0;
+          if (RESB) continue;
           if (++sb == BS) {
             sb = 0;
             phb ^= 1;
