@@ -450,6 +450,377 @@ __global__ void __launch_bounds__(kWbThreads, 1) c3b_wgrad_kernel(const uint16_t
   }
 }
 
+// ------------------------------------------------------ multi-K fprop ------
+// Windows past one K block (AlexNet / OverFeat 11x11x3 = 363 = 6 K blocks of
+// 64): same warp roles as c3b_fprop_kernel, a tile is KB stages (one per K
+// block), W stays resident (KB x NB rows x 128 B: 72 KB at 96 channels).
+// Builder groups take stages round-robin (stage it -> group it % 2) so a
+// group's consecutive stages are 2 <= ring depth apart (parity waits stay
+// unambiguous; alternating whole tiles would put them KB stages apart).
+constexpr int kMkMaxKB = 6;
+constexpr int kFbmStages = 4;
+__device__ __forceinline__ void c3b_table_mk(const C3B& g, int kbn, int* off, int* rs) {
+  for (int i = threadIdx.x; i < kbn * kKb; i += blockDim.x) {
+    if (i < g.KK) {
+      const int tap = i / g.C, c = i - tap * g.C;
+      const int r = tap / g.k, s = tap - r * g.k;
+      off[i] = (r * g.W + s) * g.C + c;
+      rs[i] = r | (s << 8);
+    } else {
+      off[i] = 0;
+      rs[i] = 0;
+    }
+  }
+}
+struct C3BPix {
+  int64_t base;
+  int ih0, iw0;
+  bool valid, interior;
+};
+__device__ __forceinline__ C3BPix c3b_pix(const C3B& g, int m) {
+  C3BPix q;
+  q.valid = m < g.P;
+  const int mm = q.valid ? m : 0;
+  const int n = mm / g.HoWo;
+  const int rem = mm - n * g.HoWo;
+  const int oh = rem / g.Wo, ow = rem - oh * g.Wo;
+  q.ih0 = oh * g.stride - g.pad;
+  q.iw0 = ow * g.stride - g.pad;
+  q.base = ((static_cast<int64_t>(n) * g.H + q.ih0) * g.W + q.iw0) * g.C;
+  q.interior = q.ih0 >= 0 && q.ih0 + g.k <= g.H && q.iw0 >= 0 && q.iw0 + g.k <= g.W;
+  return q;
+}
+// the 64 im2col values of K block kb for pixel q, packed in bf16 pairs
+__device__ __forceinline__ void c3b_row_kb(const uint16_t* __restrict__ x, const C3B& g, const int* off, const int* rs,
+                                           const C3BPix& q, int kb, uint32_t (&u)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) u[i] = 0u;
+  if (!q.valid) return;
+  const int k0 = kb * kKb;
+  const uint16_t* xb = x + q.base;
+  if (q.interior) {
+#pragma unroll
+    for (int i = 0; i < kKb; ++i)
+      if (k0 + i < g.KK) u[i >> 1] |= static_cast<uint32_t>(__ldg(xb + off[k0 + i])) << ((i & 1) * 16);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kKb; ++i) {
+      if (k0 + i < g.KK) {
+        const int t = rs[k0 + i];
+        const int ih = q.ih0 + (t & 0xff), iw = q.iw0 + (t >> 8);
+        if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
+          u[i >> 1] |= static_cast<uint32_t>(__ldg(xb + off[k0 + i])) << ((i & 1) * 16);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kFbThreads, 1) c3b_fprop_mk_kernel(const uint16_t* __restrict__ x,
+                                                                     const uint16_t* __restrict__ w,
+                                                                     const __grid_constant__ CUtensorMap tma_y, C3B g,
+                                                                     int NB, int NBP, int KB, int relu) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bblk = (static_cast<uint32_t>(NB) * 128 + 1023u) & ~1023u;  // one K block of W
+  const uint32_t sb = base;
+  const uint32_t sa0 = sb + KB * bblk;
+  const uint32_t so = sa0 + kFbmStages * 16384;
+  const int NG = (NB + 63) / 64;
+  const uint32_t obytes = NG * 16384;
+  const uint32_t bars = so + 2 * obytes;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (kFbmStages + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * kFbmStages + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * kFbmStages + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * kFbmStages + 4);
+  int* tab = reinterpret_cast<int*>(smem_raw + (bars + 8u * (2 * kFbmStages + 6) - raw));
+  const int* off = tab;
+  const int* rs = tab + kMkMaxKB * kKb;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (g.P + kBM - 1) / kBM;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kFbmStages; ++s) {
+      mbar_init(full_bar(s), 128);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  c3b_table_mk(g, KB, tab, tab + kMkMaxKB * kKb);
+  // W -> KB resident K-major blocks (rows >= Cout and k >= KK are 0)
+  for (int i = threadIdx.x; i < KB * NB * 8; i += blockDim.x) {
+    const int kb = i / (NB * 8), r = i - kb * NB * 8;
+    const int co = r >> 3, j = r & 7;
+    uint32_t q[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k0 = kb * kKb + j * 8 + 2 * e;
+      const uint32_t lo = (co < g.Cout && k0 < g.KK) ? w[static_cast<int64_t>(co) * g.KK + k0] : 0u;
+      const uint32_t hi = (co < g.Cout && k0 + 1 < g.KK) ? w[static_cast<int64_t>(co) * g.KK + k0 + 1] : 0u;
+      q[e] = lo | (hi << 16);
+    }
+    st_shared_v4(kmaj_addr(sb + kb * bblk, co, j), q[0], q[1], q[2], q[3]);
+  }
+  fence_proxy_async();
+  if (warp == 12) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(2 * NBP)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  if (warp >= 4 && warp < 12) {
+    // ---------------- builders: 2 groups take stages round-robin ----------------
+    const int grp = (warp - 4) >> 2;
+    const int t = (threadIdx.x - 128) & 127;
+    int cur_tl = -1;
+    C3BPix q{};
+    const int total = ((ntiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                       static_cast<int>(gridDim.x)) * KB;
+    for (int it = grp; it < total; it += 2) {
+      const int tl = it / KB, kb = it - tl * KB;
+      if (tl != cur_tl) {
+        cur_tl = tl;
+        q = c3b_pix(g, (static_cast<int>(blockIdx.x) + tl * static_cast<int>(gridDim.x)) * kBM + t);
+      }
+      const int s = it % kFbmStages;
+      uint32_t u[32];
+      c3b_row_kb(x, g, off, rs, q, kb, u);  // loads in flight while the stage drains
+      if (it >= kFbmStages) mbar_wait(empty_bar(s), ((it / kFbmStages) & 1) ^ 1);
+      const uint32_t sa = sa0 + s * 16384;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) st_shared_v4(kmaj_addr(sa, t, j), u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
+      fence_proxy_async();
+      mbar_arrive(full_bar(s));
+    }
+  } else if (warp == 12) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = make_idesc_bf16(NB, false, false);
+    const bool leader = elect_one();
+    int it = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      if (lt >= 2) mbar_wait(tempty_bar(acc), ((lt >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < KB; ++kb, ++it) {
+        const int s = it % kFbmStages;
+        mbar_wait(full_bar(s), (it / kFbmStages) & 1);
+        tc_fence_after();
+        const uint32_t sa = sa0 + s * 16384;
+        if (leader) {
+#pragma unroll
+          for (int kk = 0; kk < kKb / 16; ++kk)
+            tc_mma_bf16(tmem + acc * NBP, make_sdesc(sa + kk * 32, 16, 1024, kSw128),
+                        make_sdesc(sb + kb * bblk + kk * 32, 16, 1024, kSw128), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(empty_bar(s));
+        }
+        __syncwarp();
+      }
+      if (leader) tc_commit(tfull_bar(acc));
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue (as c3b_fprop_kernel) ----------------
+    const int row = warp * 32 + lane;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      const uint32_t ob = so + (it & 1) * obytes;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait_sleep(tfull_bar(acc), (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + acc * NBP + (static_cast<uint32_t>(warp * 32) << 16);
+      for (int cg = 0; cg < NB / 32; ++cg) {
+        float v[32];
+        tmem_ld32(taddr + cg * 32, v);
+        if (relu) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        const uint32_t rowaddr = ob + (cg >> 1) * 16384 + row * 128;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = (cg & 1) * 4 + jj;
+          st_shared_v4(rowaddr + (((j ^ (row & 7)) & 7) << 4), pack_bf16x2(v[8 * jj], v[8 * jj + 1]),
+                       pack_bf16x2(v[8 * jj + 2], v[8 * jj + 3]), pack_bf16x2(v[8 * jj + 4], v[8 * jj + 5]),
+                       pack_bf16x2(v[8 * jj + 6], v[8 * jj + 7]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty_bar(acc));
+      fence_proxy_async();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 0) {
+        for (int gi = 0; gi < NG; ++gi) tma_store_2d(&tma_y, ob + gi * 16384, gi * 64, tile * kBM, false);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * NBP) : "memory");
+  }
+}
+
+// ------------------------------------------------------ multi-K wgrad ------
+// D[co][k] over all KB*64 im2col columns at once (N = KB*64 <= 384: MMAs of
+// N <= 256 and the rest), 64 pixels per stage: A = dY^T (two 64-co MN-major
+// chunks by two 2D TMA boxes; channels past Cout are zero fill), B = KB
+// MN-major chunks of im2col^T built by a warp pair per stage (warp h of the
+// pair: pixel rows 32h + lane). kMkWbStages pairs and a ring of the same
+// depth: a builder's consecutive stages are exactly one ring apart.
+constexpr int kMkWbStages = 3;
+__global__ void __launch_bounds__(kWbThreads, 1) c3b_wgrad_mk_kernel(const uint16_t* __restrict__ x,
+                                                                     const __grid_constant__ CUtensorMap tma_dy, C3B g,
+                                                                     int ppb, int KB, int ncols,
+                                                                     float* __restrict__ part) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t stage = 16384 + static_cast<uint32_t>(KB) * 8192;
+  const uint32_t bars = base + kMkWbStages * stage;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (kMkWbStages + s); };
+  const uint32_t done_bar = bars + 8u * (2 * kMkWbStages);
+  const uint32_t tmem_slot = bars + 8u * (2 * kMkWbStages + 1);
+  int* tab = reinterpret_cast<int*>(smem_raw + (bars + 8u * (2 * kMkWbStages + 2) - raw));
+  const int* off = tab;
+  const int* rs = tab + kMkMaxKB * kKb;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p_begin = blockIdx.x * ppb;
+  const int p_end = min(p_begin + ppb, g.P);
+  const int nkb = p_end > p_begin ? (p_end - p_begin + kKb - 1) / kKb : 0;
+  const int nt = KB * kKb;
+  const int n1 = nt <= 256 ? nt : 256, n2 = nt - n1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMkWbStages; ++s) {
+      mbar_init(full_bar(s), 65);  // the building pair's 64 lanes + the TMA thread's expect_tx arrival
+      mbar_init(empty_bar(s), 1);
+    }
+    mbar_init(done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  c3b_table_mk(g, KB, tab, tab + kMkMaxKB * kKb);
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
+
+  if (warp < 8) {
+    // ---------------- builders ----------------
+    const int pr = warp >> 1, half = warp & 1;
+    for (int it = pr; warp < 2 * kMkWbStages && it < nkb; it += kMkWbStages) {
+      const int s = it % kMkWbStages;
+      const int row = half * 32 + lane;
+      const int m = p_begin + it * kKb + row;
+      const C3BPix q = c3b_pix(g, m < p_end ? m : g.P);
+      if (it >= kMkWbStages) mbar_wait(empty_bar(s), ((it / kMkWbStages) & 1) ^ 1);
+      const uint32_t sbb = base + s * stage + 16384;
+      for (int kb = 0; kb < KB; ++kb) {
+        uint32_t u[32];
+        c3b_row_kb(x, g, off, rs, q, kb, u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) st_shared_v4(mnb_addr(sbb, row, kb, j), u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
+      }
+      fence_proxy_async();
+      mbar_arrive(full_bar(s));
+    }
+    // ---------------- epilogue: warp w owns TMEM lanes 32w.. = co ----------------
+    if (warp < 4 && warp * 32 < g.Cout) {
+      mbar_wait_sleep(done_bar, 0);
+      tc_fence_after();
+      const int co = warp * 32 + lane;
+      float* dst = part + (static_cast<int64_t>(blockIdx.x) * g.Cout + co) * g.KK;
+      for (int cg = 0; cg < nt / 32; ++cg) {
+        float v[32];
+        tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cg * 32, v);
+        if (nkb <= 0) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        if (co < g.Cout) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (cg * 32 + i < g.KK) dst[cg * 32 + i] = v[i];
+        }
+      }
+    }
+  } else if (warp == 8) {
+    // ---------------- TMA producer (dY tiles: two 64-co boxes per stage) ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_dy) : "memory");
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % kMkWbStages;
+        if (it >= kMkWbStages) mbar_wait(empty_bar(s), ((it / kMkWbStages) & 1) ^ 1);
+        mbar_expect_tx(full_bar(s), 16384u);
+        tma_load_2d(base + s * stage, &tma_dy, full_bar(s), 0, p_begin + it * kKb);
+        tma_load_2d(base + s * stage + 8192, &tma_dy, full_bar(s), 64, p_begin + it * kKb);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc1 = make_idesc_bf16(n1, true, true);
+    const uint32_t idesc2 = make_idesc_bf16(n2 > 0 ? n2 : 16, true, true);
+    const bool leader = elect_one();
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % kMkWbStages;
+      mbar_wait(full_bar(s), (it / kMkWbStages) & 1);
+      tc_fence_after();
+      const uint32_t sa = base + s * stage;
+      const uint32_t sbb = sa + 16384;
+      if (leader) {
+#pragma unroll
+        for (int kk = 0; kk < kKb / 16; ++kk) {
+          const uint64_t ad = make_sdesc(sa + kk * 2048, 8192, 1024, kSw128);
+          tc_mma_bf16(tmem, ad, make_sdesc(sbb + kk * 2048, 8192, 1024, kSw128), idesc1, (it > 0 || kk > 0) ? 1u : 0u);
+          if (n2 > 0)
+            tc_mma_bf16(tmem + n1, ad, make_sdesc(sbb + (n1 / 64) * 8192 + kk * 2048, 8192, 1024, kSw128), idesc2,
+                        (it > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(empty_bar(s));
+      }
+      __syncwarp();
+    }
+    if (leader) {
+      if (nkb > 0)
+        tc_commit(done_bar);
+      else
+        mbar_arrive(done_bar);
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+  }
+}
+
 // Partials [nparts][count] summed in part order; bf16 SGD update (one
 // rounding) or the fp32 dW.
 __global__ void c3b_reduce_kernel(const float* __restrict__ part, int nparts, int64_t count, bf16* __restrict__ w,
@@ -502,14 +873,29 @@ int wgrad_blocks(const C3B& g) { return std::max(1, std::min(kSmsC3, (g.P + 255)
 bool c3b_common(const ConvArgs& a) {
   const int64_t P = static_cast<int64_t>(a.n) * a.ho() * a.wo();
   const int64_t X = static_cast<int64_t>(a.n) * a.h * a.w * a.c[0];
-  return a.nseg == 1 && a.c[0] <= 8 && a.kh == a.kw && a.kh * a.kw * a.c[0] <= kKb && a.kh < 256 && P > 0 &&
-         P < (int64_t{1} << 31) - kBM && X < (int64_t{1} << 40);
+  return a.nseg == 1 && a.c[0] <= 8 && a.kh == a.kw && a.kh * a.kw * a.c[0] <= kMkMaxKB * kKb && a.kh < 256 &&
+         P > 0 && P < (int64_t{1} << 31) - kBM && X < (int64_t{1} << 40);
+}
+int kblocks_of(const ConvArgs& a) { return (a.kh * a.kw * a.c[0] + kKb - 1) / kKb; }
+size_t fprop_mk_smem(int NB, int KB) {
+  const size_t bblk = (static_cast<size_t>(NB) * 128 + 1023) & ~size_t{1023};
+  return 1024 + KB * bblk + kFbmStages * 16384 + 2 * static_cast<size_t>((NB + 63) / 64) * 16384 +
+         8 * (2 * kFbmStages + 6) + 2 * kMkMaxKB * kKb * sizeof(int) + 64;
+}
+size_t wgrad_mk_smem(int KB) {
+  return 1024 + kMkWbStages * (16384 + static_cast<size_t>(KB) * 8192) + 8 * (2 * kMkWbStages + 2) +
+         2 * kMkMaxKB * kKb * sizeof(int) + 64;
 }
 
 }  // namespace
 
-bool c3b_fprop_eligible(const ConvArgs& a) { return c3b_common(a) && a.cout % 8 == 0 && a.cout <= 128; }
-bool c3b_wgrad_eligible(const ConvArgs& a) { return c3b_common(a) && (a.cout == 64 || a.cout == 128); }
+bool c3b_fprop_eligible(const ConvArgs& a) {
+  return c3b_common(a) && a.cout % 8 == 0 && a.cout <= 128 &&
+         (kblocks_of(a) == 1 || fprop_mk_smem((a.cout + 31) / 32 * 32, kblocks_of(a)) <= 227 * 1024);
+}
+bool c3b_wgrad_eligible(const ConvArgs& a) {
+  return c3b_common(a) && (kblocks_of(a) == 1 ? (a.cout == 64 || a.cout == 128) : (a.cout % 8 == 0 && a.cout <= 128));
+}
 size_t c3b_wgrad_ws_bytes(const ConvArgs& a) {
   const C3B g = geom_of(a);
   return static_cast<size_t>(wgrad_blocks(g)) * g.Cout * g.KK * sizeof(float);
@@ -526,6 +912,23 @@ cudaError_t c3b_fprop(const ConvArgs& a, const void* w, void* y, cudaStream_t st
   const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(kBM)};
   if (!encode_tiled(&ty, y, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
     return cudaErrorInvalidValue;
+  const int KB = kblocks_of(a);
+  if (KB > 1) {
+    const size_t smk = fprop_mk_smem(NB, KB);
+    static size_t attr_mk = 0;
+    if (smk > attr_mk) {
+      cudaError_t e = cudaFuncSetAttribute(c3b_fprop_mk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smk));
+      if (e != cudaSuccess) return e;
+      attr_mk = smk;
+    }
+    const int ntiles = (g.P + kBM - 1) / kBM;
+    c3b_fprop_mk_kernel<<<std::min(kSmsC3, ntiles), kFbThreads, smk, st>>>(
+        static_cast<const uint16_t*>(static_cast<const void*>(a.x[0])), static_cast<const uint16_t*>(w), ty, g, NB,
+        NBP, KB, a.relu_out);
+    count_launch();
+    return cudaGetLastError();
+  }
   const size_t smem = fprop_smem(NB);
   const bool k3c3 = g.k == 3 && g.C == 3;
   auto kern = k3c3 ? c3b_fprop_kernel<3, 3> : c3b_fprop_kernel<0, 0>;
@@ -553,6 +956,26 @@ cudaError_t c3b_wgrad(const ConvArgs& a, const void* dy, void* w, float lr, floa
   int ppb = (g.P + nb - 1) / nb;
   ppb = (ppb + kKb - 1) / kKb * kKb;
   nb = static_cast<int>((g.P + ppb - 1) / ppb);
+  const int KB = kblocks_of(a);
+  if (KB > 1) {
+    // dY [P][Cout]: 64 co x 64 pixel boxes (MN-major chunks), co past Cout zero-filled
+    alignas(64) CUtensorMap t2;
+    const cuuint64_t d2[2] = {static_cast<cuuint64_t>(g.Cout), static_cast<cuuint64_t>(g.P)};
+    const cuuint64_t s2[1] = {static_cast<cuuint64_t>(g.Cout) * 2};
+    const cuuint32_t b2[2] = {64, 64};
+    if (!encode_tiled(&t2, dy, 2, d2, s2, b2, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
+      return cudaErrorInvalidValue;
+    const size_t smk = wgrad_mk_smem(KB);
+    static size_t attr_mk = 0;
+    if (smk > attr_mk) {
+      cudaError_t e = cudaFuncSetAttribute(c3b_wgrad_mk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smk));
+      if (e != cudaSuccess) return e;
+      attr_mk = smk;
+    }
+    c3b_wgrad_mk_kernel<<<nb, kWbThreads, smk, st>>>(static_cast<const uint16_t*>(static_cast<const void*>(a.x[0])),
+                                                     t2, g, ppb, KB, pow2_at_least(KB * kKb), ws);
+  } else {
   // dY [P][Cout] as (64 co, pixel, co-chunk): one 64-pixel box per stage, MN-major 8 KB chunks
   alignas(64) CUtensorMap tdy;
   const cuuint64_t d3[3] = {64, static_cast<cuuint64_t>(g.P), static_cast<cuuint64_t>(g.Cout / 64)};
@@ -571,6 +994,7 @@ cudaError_t c3b_wgrad(const ConvArgs& a, const void* dy, void* w, float lr, floa
   }
   kern<<<nb, kWbThreads, smem, st>>>(static_cast<const uint16_t*>(static_cast<const void*>(a.x[0])), tdy,
                                                  g, ppb, ws);
+  }
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
