@@ -201,3 +201,52 @@ def test_cpasync_gathers_bf16():
         TL._run("inception_toy_b32_cpasync", "inception_toy", 32, "all", False, es=2)
     finally:
         L.lib().vdnn_kernel_set_tma(1)
+
+
+@pytest.mark.parametrize("net,batch", [("alexnet", 16), ("vgg16", 4)])
+def test_bf16_fused_sgd_matches_external_gradients(net, batch):
+    """The fused wgrad + SGD epilogues (pair / persistent / first-layer
+    reduce kernels) apply w <- bf16(w - lr * dW) with the dW the same kernels
+    write in external-gradient mode: one step with SGD equals the rounded
+    update computed on the host (fused multiply-add, as the device rounds it)
+    from an external-gradient step, to within one bf16 ulp and exactly for
+    almost every weight."""
+    _need_gpu()
+    g = V.build_preset(net, batch)
+    cm = _cm()
+    d = V.static_decision(V.PolicyKind.Baseline, V.AlgoMode.PerfOptimal, g, cm)
+    w = numeric.he_weights(g, cm, seed=21)
+    rng = np.random.default_rng(22)
+    sh = g.shape(0)
+    images = rng.uniform(-1, 1, size=(batch, sh.h, sh.w, sh.c)).astype(np.float32)
+    labels = rng.integers(0, 10, size=batch).astype(np.int32)
+    lr = 0.05
+
+    def session(ext):
+        s = V.Session(g, d, cm, 8 << 30, external_grads=ext)
+        for k, v in w.items():
+            s.set_weights(k, v)
+        s.set_batch(images, labels)
+        s.step(lr)
+        return s
+
+    a = session(True)
+    grads = {k: a.get_grads(k) for k in w}
+    before = {k: a.get_weights(k) for k in w}  # bf16-rounded initial weights (external grads: no update)
+    del a
+    gc.collect()
+    b = session(False)
+    exact = total = 0
+    for k in w:
+        got = b.get_weights(k)
+        # the device fuses the multiply-add (one fp32 rounding, then RNE to
+        # bf16): at w ~ lr * dW a separately rounded product would differ by
+        # many bf16 ulps of the tiny result
+        fused = (before[k].astype(np.float64) - np.float64(np.float32(lr)) * grads[k].astype(np.float64))
+        want = V.from_bf16_bits(V.to_bf16_bits(fused.astype(np.float32)))
+        # got and want are bf16 values: compare their 16-bit patterns
+        ulp = np.abs(V.to_bf16_bits(want).astype(np.int64) - V.to_bf16_bits(got).astype(np.int64))
+        assert int(ulp.max()) <= 1, (k, int(ulp.max()))
+        exact += int((ulp == 0).sum())
+        total += ulp.size
+    assert exact >= 0.99 * total, (exact, total)

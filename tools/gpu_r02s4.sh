@@ -1,3 +1,1 @@
-mkdir -p gpurun_out
-timeout 600 python tools/algo_probe.py 32 > gpurun_out/r02s4_algo_probe.txt 2>&1
-cat gpurun_out/r02s4_algo_probe.txt
+timeout 900 python -m pytest tests/test_bf16_gpu.py -x -q -k "fused_sgd" 2>&1 | tail -n 3
