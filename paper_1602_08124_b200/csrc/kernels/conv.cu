@@ -493,7 +493,7 @@ cudaError_t launch_halo_pair(HaloParams& h, const ConvParams& p, cudaStream_t st
     attr_smem = smem;
   }
   const int grid = 2 * std::min(ntiles, persist_sms() / 2);
-  tc_conv_halo_pair_kernel<BN, AS, BS, KW, RESB><<<grid, 192, smem, st>>>(h, ta, tb);
+  tc_conv_halo_pair_kernel<BN, AS, BS, KW, RESB><<<grid, kHaloPairThreads, smem, st>>>(h, ta, tb);
   count_launch();
   return cudaGetLastError();
 }

@@ -262,7 +262,7 @@ cudaError_t launch_halo_b(HaloParamsB& h, const ConvParamsB& p, cudaStream_t st)
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  tcb_halo_kernel<BN, AS, BS, 3, RESB><<<std::min(h.ntiles, kNumSmsB), 192, L::kTotal, st>>>(h, ta, tb);
+  tcb_halo_kernel<BN, AS, BS, 3, RESB><<<std::min(h.ntiles, kNumSmsB), kHaloBThreads, L::kTotal, st>>>(h, ta, tb);
   count_launch();
   return cudaGetLastError();
 }

@@ -18,7 +18,8 @@
 //   warp 5    : TMA producer; both CTAs' loads complete on the LEADER's full
 //               barriers (.cta_group::2 TMA), the leader's single arrive
 //               expects both CTAs' bytes; empty / tfull barriers are
-//               multicast commits; tempty counts 256 arrivals in the leader.
+//               multicast commits; tempty counts 256 arrivals per epilogue
+//               warpgroup in the leader (kHaloEpiGroups, both CTAs).
 // RESB: when one CTA's half of the whole filter fits next to the A ring
 // (64 -> 64 channels: 9 taps x 2 chunks x 4 KB = 72 KB), B is loaded once per
 // CTA and stays resident: the per-tile B stream (as many L2 -> SM bytes as
@@ -37,8 +38,17 @@ struct HaloPairSmem {
   static_assert(2 * kAccCols <= 512, "two accumulator sets must fit TMEM");
 };
 
+// Epilogue warpgroups: group 0 = warps 0-3, group g >= 1 = warps 6 + 4(g-1)
+// .. (TMEM lane quarter = warp % 4); group g drains M half g % 2 and column
+// half g / 2 of the tile, so the dgrad's ReLU-mask loads and the stores of
+// the whole tile are in flight together (with one warpgroup the epilogue --
+// four serial DRAM round trips per tile -- bounded the 224x224x64 dgrad:
+// tensor pipe 36% active, long-scoreboard stalls; 2.73 -> 2.43 ms with two;
+// four measured slower, 2.86).
+constexpr int kHaloEpiGroups = 2;
+constexpr int kHaloPairThreads = 32 * (6 + 4 * (kHaloEpiGroups - 1));
 template <int BN, int AS, int BS, int KW, bool RESB = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kHaloPairThreads, 1)
     tc_conv_halo_pair_kernel(const __grid_constant__ HaloParams p, const __grid_constant__ CUtensorMap tma_a,
                              const __grid_constant__ CUtensorMap tma_b) {
   using L = HaloPairSmem<BN, AS, BS>;
@@ -73,7 +83,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 256);
+      mbar_init(tempty(a), 256 * kHaloEpiGroups);  // both CTAs' epilogue warpgroups
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -224,9 +234,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         __syncwarp();
       }
     }
-  } else {
+  } else if (warp < 4 || warp >= 6) {
     // ---------------- epilogue (this CTA's 256 virtual rows) ----------------
-    const int row = warp * 32 + lane;
+    const int gi = warp < 4 ? 0 : 1 + (warp - 6) / 4;
+    const int hsel = gi & 1;
+    const int cgs = (BN / 32) / (kHaloEpiGroups / 2);  // column groups per warpgroup
+    const int cg0 = (gi >> 1) * cgs;
+    const int qw = warp & 3;
+    const int row = qw * 32 + lane;
     const uint32_t ltempty0 = map_to_rank(tempty(0), 0), ltempty1 = map_to_rank(tempty(1), 0);
     int lt = 0;
     for (int tile = pair; tile < ntiles; tile += npairs, ++lt) {
@@ -236,18 +251,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const int y0 = (2 * thp + static_cast<int>(rank)) * p.TH, n0 = tn * BN;
       mbar_wait_sleep(tfull(acc), (lt >> 1) & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
+      {
+        const int h = hsel;
         const int v = h * kBM + row;
         const int yl = v / p.P, x = v - yl * p.P, y = y0 + yl;
         const bool valid = yl < p.TH && x < p.Wout && y < p.Hout;
         const int64_t pix = (static_cast<int64_t>(n) * p.Hout + y) * p.Wout + x;
-        const uint32_t taddr = tmem + acc * L::kAccCols + h * BN + (static_cast<uint32_t>(warp * 32) << 16);
+        const uint32_t taddr = tmem + acc * L::kAccCols + h * BN + (static_cast<uint32_t>(qw * 32) << 16);
 #pragma unroll 1
-        for (int cg = 0; cg < BN / 32; ++cg) {
+        for (int cg = cg0; cg < cg0 + cgs; ++cg) {
           float vals[32];
           tmem_ld32(taddr + cg * 32, vals);
-          if (h == 1 && cg == BN / 32 - 1) {
+          if (cg == cg0 + cgs - 1) {
             // last TMEM read of this accumulator set: release it to the leader's MMA warp
             tc_fence_before();
             mbar_arrive_cluster(acc ? ltempty1 : ltempty0);

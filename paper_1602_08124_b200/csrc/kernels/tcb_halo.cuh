@@ -56,8 +56,12 @@ struct HaloSmemB {
 // CTA and stays resident (BS = that slot count): the per-tile B stream --
 // 72 KB per 256 virtual rows at 64 -> 64 channels, 45% of the L2 -> SM fill
 // -- disappears (224x224x64 fprop / dgrad).
+// Two epilogue warpgroups (warps 0-3: M half 0, warps 6-9: M half 1; TMEM
+// lane quarter = warp % 4) keep the dgrad's ReLU-mask loads and the stores of
+// both halves in flight together (as tc_conv_halo_pair.cuh).
+constexpr int kHaloBThreads = 320;
 template <int BN, int AS, int BS, int KW, bool RESB = false>
-__global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant__ HaloParamsB p,
+__global__ void __launch_bounds__(kHaloBThreads, 1) tcb_halo_kernel(const __grid_constant__ HaloParamsB p,
                                                           const __grid_constant__ CUtensorMap tma_a,
                                                           const __grid_constant__ CUtensorMap tma_b) {
   using L = HaloSmemB<BN, AS, BS>;
@@ -87,7 +91,7 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 128);
+      mbar_init(tempty(a), 256);  // both epilogue warpgroups
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -228,9 +232,11 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
       if (leader) tc_commit(tfull(acc));
       __syncwarp();
     }
-  } else if (warp < 4) {
+  } else if (warp < 4 || warp >= 6) {
     // ---------------- epilogue ----------------
-    const int row = warp * 32 + lane;
+    const int hsel = warp < 4 ? 0 : 1;
+    const int qw = warp & 3;
+    const int row = qw * 32 + lane;
     int lt = 0;
     for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++lt) {
       const int acc = lt & 1;
@@ -239,18 +245,18 @@ __global__ void __launch_bounds__(192, 1) tcb_halo_kernel(const __grid_constant_
       const int y0 = th * p.TH, n0 = tn * BN;
       mbar_wait_sleep(tfull(acc), (lt >> 1) & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
+      {
+        const int h = hsel;
         const int v = h * kBM + row;
         const int yl = v / p.P, x = v - yl * p.P, y = y0 + yl;
         const bool valid = yl < p.TH && x < p.Wout && y < p.Hout;
         const int64_t pix = (static_cast<int64_t>(n) * p.Hout + y) * p.Wout + x;
-        const uint32_t taddr = tmem + acc * L::kAccCols + h * BN + (static_cast<uint32_t>(warp * 32) << 16);
+        const uint32_t taddr = tmem + acc * L::kAccCols + h * BN + (static_cast<uint32_t>(qw * 32) << 16);
 #pragma unroll 1
         for (int cg = 0; cg < BN / 32; ++cg) {
           float vals[32];
           tmem_ld32(taddr + cg * 32, vals);
-          if (h == 1 && cg == BN / 32 - 1) {
+          if (cg == BN / 32 - 1) {
             // last TMEM read of this accumulator set: hand it back to the MMA warp
             tc_fence_before();
             mbar_arrive(tempty(acc));
