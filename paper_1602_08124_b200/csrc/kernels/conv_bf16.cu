@@ -295,7 +295,7 @@ cudaError_t launch_pair_b(const ConvParamsB& p, int splits, const CUtensorMap& t
   }
   const int64_t items = static_cast<int64_t>((p.M + 255) / 256) * ((p.Ncols + 255) / 256) * splits;
   const int grid = 2 * static_cast<int>(std::min<int64_t>(items, kNumSmsB / 2));
-  tcb_pair_kernel<STAGES><<<grid, 192, L::kTotal, st>>>(p, ta, tb, splits);
+  tcb_pair_kernel<STAGES><<<grid, kTcbPairThreads, L::kTotal, st>>>(p, ta, tb, splits);
   count_launch();
   return cudaGetLastError();
 }

@@ -701,13 +701,13 @@ struct TmaProducerB {
 // kernel releases the accumulator there). zero: the tile had no K blocks.
 template <int BN, class Drained>
 __device__ __forceinline__ void tcb_epilogue(const ConvParamsB& p, uint32_t taddr, int m0, int n0, int z, int row,
-                                             bool zero, Drained drained) {
+                                             bool zero, Drained drained, int cg_lo = 0, int cg_hi = BN / 32) {
   const int m = m0 + row;
 #pragma unroll 1
-  for (int cg = 0; cg < BN / 32; ++cg) {
+  for (int cg = cg_lo; cg < cg_hi; ++cg) {
     float v[32];
     tmem_ld32(taddr + cg * 32, v);
-    if (cg == BN / 32 - 1) drained();
+    if (cg == cg_hi - 1) drained();
     if (zero) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.f;

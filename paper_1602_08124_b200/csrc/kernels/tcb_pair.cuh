@@ -22,7 +22,8 @@
 //   warp 5    : TMA producer of this CTA's halves; both CTAs' loads complete
 //               on the LEADER's full barrier, whose single expect_tx arrive
 //               covers both CTAs' bytes; empty / tfull: multicast commits;
-//               tempty: 256 arrivals in the leader (both CTAs' epilogues).
+//               tempty: 512 arrivals in the leader (both CTAs' two epilogue
+//               warpgroups, warps 0-3 and 6-9).
 // Two TMEM accumulator sets (2 x 256 columns per SM): tile t's epilogue
 // overlaps tile t+1's main loop.
 #pragma once
@@ -46,8 +47,13 @@ struct TcbPairSmem {
   static constexpr int kTotal = STAGES * kStage + 1024 + 256;
 };
 
+// Two epilogue warpgroups (warps 0-3: columns [0, 128), warps 6-9: columns
+// [128, 256) of the tile; TMEM lane quarter = warp % 4): the stores -- and
+// the W round trips of a fused-SGD wgrad -- of both column halves are in
+// flight together.
+constexpr int kTcbPairThreads = 320;
 template <int STAGES>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcbPairThreads, 1)
     tcb_pair_kernel(const __grid_constant__ ConvParamsB p, const __grid_constant__ CUtensorMap tma_a,
                     const __grid_constant__ CUtensorMap tma_b, int splits) {
   using L = TcbPairSmem<STAGES>;
@@ -86,7 +92,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 256);
+      mbar_init(tempty(a), 512);  // both CTAs' two epilogue warpgroups
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -192,8 +198,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         __syncwarp();
       }
     }
-  } else if (warp < 4) {
-    // ---------------- epilogue (this CTA's 128 rows) ----------------
+  } else if (warp < 4 || warp >= 6) {
+    // ---------------- epilogue (this CTA's 128 rows, one column half per warpgroup) ----------------
+    const int qw = warp & 3, chalf = warp < 4 ? 0 : 1;
     const uint32_t lt0 = map_to_rank(tempty(0), 0), lt1 = map_to_rank(tempty(1), 0);
     int lt = 0;
     for (int t = pair; t < ntiles; t += npairs, ++lt) {
@@ -202,12 +209,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const int acc = lt & 1;
       mbar_wait_sleep(tfull(acc), (lt >> 1) & 1);
       tc_fence_after();
-      const uint32_t ta = tmem + acc * BN + (static_cast<uint32_t>(warp * 32) << 16);
-      tcb_epilogue<BN>(p, ta, m0, n0, z, warp * 32 + lane, nkb <= 0, [&] {
+      const uint32_t ta = tmem + acc * BN + (static_cast<uint32_t>(qw * 32) << 16);
+      tcb_epilogue<BN>(p, ta, m0, n0, z, qw * 32 + lane, nkb <= 0, [&] {
         // last TMEM read of this accumulator set: release it to the leader's MMA warp
         tc_fence_before();
         mbar_arrive_cluster(acc ? lt1 : lt0);
-      });
+      }, chalf * (BN / 64), (chalf + 1) * (BN / 64));
     }
   }
   tc_fence_before();

@@ -1,3 +1,6 @@
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --kernel-name-base demangled -k regex:"halo" --csv --log-file gpurun_out/r02s4_launches_haloB.csv python tools/one_step.py vgg16 256 none --bf16 > /dev/null 2>&1
-timeout 900 python -m pytest tests/test_kernels_gpu.py tests/test_layer_parity_gpu.py tests/test_bf16_gpu.py -x -q 2>&1 | tail -n 2
+timeout 300 python tools/prof_layers.py vgg16 256 none --bf16 > gpurun_out/r02s4_layers_bf16_v6.txt 2>&1
+awk '$2=="conv"||$2=="fc"' gpurun_out/r02s4_layers_bf16_v6.txt | tail -13; tail -1 gpurun_out/r02s4_layers_bf16_v6.txt
+timeout 300 python tools/prof_layers.py alexnet 128 none --bf16 > gpurun_out/r02s4_layers_alexnet_bf16.txt 2>&1
+awk '$2=="fc"||$2=="total"' gpurun_out/r02s4_layers_alexnet_bf16.txt
+timeout 900 python -m pytest tests/test_bf16_gpu.py -x -q 2>&1 | tail -n 2
