@@ -36,7 +36,7 @@ namespace vdnnk {
 namespace {
 
 constexpr int kSmsC3 = 148;
-constexpr int kFbStages = 4;
+constexpr int kFbStages = 8;
 constexpr int kWbStages = 8;
 constexpr int kWbPrefetch = 16;  // wgrad: dY stages prefetched into L2 ahead of the ring
 constexpr int kKb = 64;          // bf16 per K block (one 128-B operand row)
@@ -141,7 +141,14 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 // smem: [B: NB rows x 128 B][A: kFbStages x 16 KB][OUT: 2 x NG x 16 KB][barriers][table]
 // (NG = 64-channel output groups). warps 0-3 epilogue, 4-11 builders, 12 MMA
 // (+ TMEM owner). TMEM: 2 x NBP columns.
-constexpr int kFbThreads = 416;
+// kFbGroups builder groups of 4 warps take alternate tiles (stage spacing
+// kFbGroups <= ring depth): the builders are latency-bound (27 loads per row,
+// then one stage), so more groups keep more tiles' loads in flight.
+constexpr int kFbGroups = 4;
+constexpr int kFbMmaWarp = 4 + 4 * kFbGroups;
+constexpr int kFbThreads = 32 * (kFbMmaWarp + 1);
+constexpr int kFbmThreads = 416;  // the multi-K kernel: 2 groups, MMA warp 12
+static_assert(kFbGroups <= kFbStages, "builder spacing must fit the ring");
 template <int KT, int CT>
 __global__ void __launch_bounds__(kFbThreads, 1) c3b_fprop_kernel(const uint16_t* __restrict__ x,
                                                                   const uint16_t* __restrict__ w,
@@ -192,7 +199,7 @@ __global__ void __launch_bounds__(kFbThreads, 1) c3b_fprop_kernel(const uint16_t
     st_shared_v4(kmaj_addr(sb, co, j), q[0], q[1], q[2], q[3]);
   }
   fence_proxy_async();
-  if (warp == 12) {
+  if (warp == kFbMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
                  "r"(2 * NBP)
                  : "memory");
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(kFbThreads, 1) c3b_fprop_kernel(const uint16_t
   uint32_t tmem;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot) : "memory");
 
-  if (warp >= 4 && warp < 12) {
+  if (warp >= 4 && warp < kFbMmaWarp) {
     // ---------------- builders ----------------
     const int grp = (warp - 4) >> 2;
     const int row = (threadIdx.x - 128) & 127;
@@ -214,9 +221,9 @@ __global__ void __launch_bounds__(kFbThreads, 1) c3b_fprop_kernel(const uint16_t
     uint32_t u[32], nu[32];
     const int tile0 = blockIdx.x + grp * gridDim.x;
     if (tile0 < ntiles) c3b_row_t<KT, CT>(x, g, tab, tab + kKb, tile0 * kBM + row, u);
-    for (int tile = tile0; tile < ntiles; tile += 2 * gridDim.x, it += 2) {
+    for (int tile = tile0; tile < ntiles; tile += kFbGroups * gridDim.x, it += kFbGroups) {
       const int s = it % kFbStages;
-      const int nt = tile + 2 * gridDim.x;
+      const int nt = tile + kFbGroups * gridDim.x;
       if (nt < ntiles) c3b_row_t<KT, CT>(x, g, tab, tab + kKb, nt * kBM + row, nu);
       if (it >= kFbStages) mbar_wait(empty_bar(s), ((it / kFbStages) & 1) ^ 1);
       const uint32_t sa = sa0 + s * 16384;
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(kFbThreads, 1) c3b_fprop_kernel(const uint16_t
 #pragma unroll
       for (int i = 0; i < 32; ++i) u[i] = nu[i];
     }
-  } else if (warp == 12) {
+  } else if (warp == kFbMmaWarp) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       const uint32_t idesc = make_idesc_bf16(NB, false, false);
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(kFbThreads, 1) c3b_fprop_kernel(const uint16_t
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 12) {
+  if (warp == kFbMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * NBP) : "memory");
   }
@@ -515,7 +522,7 @@ __device__ __forceinline__ void c3b_row_kb(const uint16_t* __restrict__ x, const
   }
 }
 
-__global__ void __launch_bounds__(kFbThreads, 1) c3b_fprop_mk_kernel(const uint16_t* __restrict__ x,
+__global__ void __launch_bounds__(kFbmThreads, 1) c3b_fprop_mk_kernel(const uint16_t* __restrict__ x,
                                                                      const uint16_t* __restrict__ w,
                                                                      const __grid_constant__ CUtensorMap tma_y, C3B g,
                                                                      int NB, int NBP, int KB, int relu) {
@@ -923,7 +930,7 @@ cudaError_t c3b_fprop(const ConvArgs& a, const void* w, void* y, cudaStream_t st
       attr_mk = smk;
     }
     const int ntiles = (g.P + kBM - 1) / kBM;
-    c3b_fprop_mk_kernel<<<std::min(kSmsC3, ntiles), kFbThreads, smk, st>>>(
+    c3b_fprop_mk_kernel<<<std::min(kSmsC3, ntiles), kFbmThreads, smk, st>>>(
         static_cast<const uint16_t*>(static_cast<const void*>(a.x[0])), static_cast<const uint16_t*>(w), ty, g, NB,
         NBP, KB, a.relu_out);
     count_launch();
