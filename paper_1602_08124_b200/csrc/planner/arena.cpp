@@ -11,7 +11,7 @@
 namespace vdnnp {
 
 Arena::Arena(u64 capacity, bool trace) : cap_(capacity), trace_(trace) {
-  if (capacity > 0) segs_.push_back(Seg{0, capacity, false, 0, {}});
+  if (capacity > 0) segs_.push_back(Seg{0, capacity, false, 0, -1});
 }
 
 // The byte*ns usage integral needs a clock that never runs backwards
@@ -46,7 +46,12 @@ std::optional<u64> Arena::place(u64 bytes, const std::string& tag, i64 t, bool p
   Seg gap = segs_[pick];
   const u64 spare = gap.len - len;
   const u64 off = from_top ? gap.off + spare : gap.off;
-  Seg blk{off, len, true, bytes, tag};
+  int32_t tag_id = -1;
+  if (trace_) {
+    tag_id = static_cast<int32_t>(tags_.size());
+    tags_.push_back(tag);
+  }
+  Seg blk{off, len, true, bytes, tag_id};
   if (spare == 0) {
     segs_[pick] = blk;
   } else if (from_top) {
@@ -54,7 +59,7 @@ std::optional<u64> Arena::place(u64 bytes, const std::string& tag, i64 t, bool p
     segs_.insert(segs_.begin() + static_cast<std::ptrdiff_t>(pick) + 1, blk);
   } else {
     segs_[pick] = blk;
-    segs_.insert(segs_.begin() + static_cast<std::ptrdiff_t>(pick) + 1, Seg{off + len, spare, false, 0, {}});
+    segs_.insert(segs_.begin() + static_cast<std::ptrdiff_t>(pick) + 1, Seg{off + len, spare, false, 0, -1});
   }
   live_ += len;
   hw_ = std::max(hw_, live_);
@@ -67,7 +72,7 @@ void Arena::free_at(u64 off, i64 t) {
   size_t i = seg_at(off);
   const Seg gone = segs_[i];
   live_ -= gone.len;
-  segs_[i] = Seg{gone.off, gone.len, false, 0, {}};
+  segs_[i] = Seg{gone.off, gone.len, false, 0, -1};
   // merge with a free right neighbour, then with a free left neighbour
   if (i + 1 < segs_.size() && !segs_[i + 1].used) {
     segs_[i].len += segs_[i + 1].len;
@@ -77,7 +82,7 @@ void Arena::free_at(u64 off, i64 t) {
     segs_[i - 1].len += segs_[i].len;
     segs_.erase(segs_.begin() + static_cast<std::ptrdiff_t>(i));
   }
-  if (trace_) rows_.push_back(TraceRow{t, 'f', gone.tag, gone.off, gone.len, live_, hw_});
+  if (trace_) rows_.push_back(TraceRow{t, 'f', tags_[static_cast<size_t>(gone.tag)], gone.off, gone.len, live_, hw_});
 }
 
 u64 Arena::requested_at(u64 off) const { return segs_[seg_at(off)].req; }

@@ -181,12 +181,16 @@ class Arena {
   u64 capacity() const { return cap_; }
 
  private:
+  // trivially copyable (the segment vector is spliced on every place / free;
+  // a std::string member made that a string move per shifted segment):
+  // the tag is an index into tags_, recorded only when tracing
   struct Seg {
     u64 off = 0, len = 0;
     bool used = false;
     u64 req = 0;
-    std::string tag;
+    int32_t tag = -1;
   };
+  std::vector<std::string> tags_;
   void clock_to(i64 t);
   size_t seg_at(u64 off) const;  // index of the segment starting at off
   u64 cap_;
