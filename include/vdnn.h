@@ -269,6 +269,10 @@ typedef struct vdnn_session_options {
                                 vdnn_session_set_offload_buffer / _spill_attach (e.g. a peer GPU's HBM) */
   int32_t cuda_graph;        /* 1: replay each step as one CUDA graph (captured on the 2nd step, re-captured
                                 when lr changes) */
+  int32_t algo_kernels;      /* 0: the implicit-GEMM kernels for every planned conv algorithm (fastest on the
+                                B200; the planned workspace is reserved); 1: GEMM_WS layers run the
+                                reference's algorithm -- im2col into the planned workspace + a 1x1 GEMM
+                                (cost_model.hpp:163-168); FFT layers stay implicit (no FFT kernel) */
 } vdnn_session_options;
 void vdnn_session_options_default(vdnn_session_options* o);
 

@@ -112,6 +112,7 @@ class SessionOptions(C.Structure):
         ("device", C.c_int32), ("weight_seed", C.c_uint64), ("external_grads", C.c_int32),
         ("record_timeline", C.c_int32), ("host_arena", C.c_int32), ("precise_fp32", C.c_int32),
         ("compress_offload", C.c_int32), ("offload_target", C.c_int32), ("cuda_graph", C.c_int32),
+        ("algo_kernels", C.c_int32),
     ]
 
 

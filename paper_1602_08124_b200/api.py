@@ -749,7 +749,8 @@ class Session:
     def __init__(self, g: NetworkGraph, decision: PolicyDecision, cost: Optional[CostModel] = None,
                  capacity: int = 12884901888, device: int = 0, weight_seed: int = 5000,
                  external_grads: bool = False, record_timeline: bool = False, precise_fp32: bool = False,
-                 compress_offload=False, offload_target: str = "host", cuda_graph: bool = False):
+                 compress_offload=False, offload_target: str = "host", cuda_graph: bool = False,
+                 algo_kernels: str = "fastest"):
         """compress_offload: move offloads/prefetches through the SMs in a
         lossless zero-value-compressed form (same schedule, bit-identical
         restored buffers, fewer bytes on the host link). "tf32": the same,
@@ -760,7 +761,15 @@ class Session:
         model) or "device" (a device buffer given to set_offload_buffer, or a
         peer GPU's spill buffer via spill_export / spill_attach: NVLink).
         cuda_graph: replay each step as one CUDA graph (captured on the second
-        step; re-captured when lr changes)."""
+        step; re-captured when lr changes).
+        algo_kernels: "fastest" runs the implicit-GEMM kernels for every planned
+        conv algorithm (the planned workspace is still reserved); "planned" runs
+        GEMM_WS layers as the reference's algorithm -- im2col into the planned
+        workspace + a 1x1 GEMM (cost_model.hpp:163-168); FFT layers stay
+        implicit (no FFT kernel: slower than implicit GEMM on this part,
+        profiles/r02s4_algo_probe.txt)."""
+        if algo_kernels not in ("fastest", "planned"):
+            raise ValueError(f"algo_kernels must be 'fastest' or 'planned', not {algo_kernels!r}")
         if offload_target not in ("host", "device"):
             raise ValueError(f"offload_target must be 'host' or 'device', not {offload_target!r}")
         self.graph = g
@@ -779,6 +788,7 @@ class Session:
         opt.compress_offload = 2 if compress_offload == "tf32" else int(bool(compress_offload))
         opt.offload_target = 0 if offload_target == "host" else 1
         opt.cuda_graph = int(cuda_graph)
+        opt.algo_kernels = 1 if algo_kernels == "planned" else 0
         d = decision._handle(g)
         c = self.cost._c()
         h = C.c_void_p()

@@ -51,6 +51,7 @@ void vdnn_session_options_default(vdnn_session_options* o) {
   o->compress_offload = 0;
   o->offload_target = 0;
   o->cuda_graph = 0;
+  o->algo_kernels = 0;
 }
 
 vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, const vdnn_cost_model* cm,
@@ -70,6 +71,7 @@ vdnn_status vdnn_session_create(const vdnn_graph* g, const vdnn_decision* d, con
       o.compress_offload = opt->compress_offload;
       o.offload_target = opt->offload_target;
       o.cuda_graph = opt->cuda_graph != 0;
+      o.algo_kernels = opt->algo_kernels;
     }
     if (!g->net.finalized()) throw vdnnp::PlanError(vdnnp::Err::Generic, "graph is not finalized");
     auto* s = new vdnnrt::Session(g->net, d->d, vdnncapi::cost_from(cm), capacity, o);

@@ -185,6 +185,14 @@ cudaError_t sgd_update_bf16(void* w, const float* g, float lr, size_t n, cudaStr
 cudaError_t fill_normal_bf16(void* w, size_t n, float stddev, uint64_t seed, cudaStream_t st);
 cudaError_t fill_uniform_bf16(void* x, size_t n, float lo, float hi, uint64_t seed, cudaStream_t st);
 cudaError_t fill_const_bf16(void* x, size_t n, float v, cudaStream_t st);
+// The reference's GEMM_WS algorithm as kernels (conv_gemmws.cu): im2col of a
+// single-segment conv input into the planned workspace (gemmws_col_bytes),
+// the contraction as a 1x1 conv over it (gemmws_args), and col2im of the
+// column gradient into dX (fused ReLU-backward mask / accumulation).
+uint64_t gemmws_col_bytes(const ConvArgs& a, int es);
+cudaError_t im2col(const ConvArgs& a, int es, void* col, cudaStream_t st);
+cudaError_t col2im(const ConvArgs& a, int es, const void* dcol, bool accumulate, cudaStream_t st);
+ConvArgs gemmws_args(const ConvArgs& a, const void* col, void* dcol);
 // First layers (C <= 8, kh*kw*C <= 64) that the dedicated BF16 kernels of
 // conv_c3tcb.cu run in fprop and wgrad (no channel padding needed)
 bool conv_bf16_c3_native(const ConvArgs& a);

@@ -497,6 +497,19 @@ int Session::padded_channels(int layer) const {
   return (c + 7) / 8 * 8;
 }
 
+// GEMM_WS as the reference's algorithm (algo_kernels = 1): a single-input
+// conv whose planned algorithm is GEMM_WS and whose planned workspace holds
+// the im2col matrix (cost_model.hpp:163-168 sizes it exactly so).
+bool Session::gemmws(int layer, u64 ws_off, u64 ws_bytes) const {
+  if (o_.algo_kernels != 1 || ws_off == kNoOff || ws_bytes == 0) return false;
+  const Node& l = g_.at(layer);
+  if (l.kind != Kind::Conv || l.in.size() != 1 || summed(layer) || padded_channels(layer)) return false;
+  const auto it = d_.algos.find(layer);
+  if (it == d_.algos.end() || it->second != Algo::GemmWs) return false;
+  const std::vector<u64> shape_only(1, 0);
+  return vdnnk::gemmws_col_bytes(conv_args(layer, shape_only, nullptr, nullptr), static_cast<int>(es_)) <= ws_bytes;
+}
+
 // X and W of a padded step into the scratch; `a` then describes the padded X.
 void Session::pad_operands(vdnnk::ConvArgs& a, int cp, char* x8, const float* w, char* w8) {
   const int c = a.c[0];
@@ -681,6 +694,16 @@ void Session::run_fwd(const FwdStep& s, float lr) {
       a.relu_out = s.relu ? 1 : 0;
       const float* bias = l.kind == Kind::Fc ? F(s.w_off + g_.fc_inputs(s.layer) * l.out * es_) : nullptr;
       const float* w = F(s.w_off);
+      if (gemmws(s.layer, s.ws_off, s.ws_bytes)) {
+        // GEMM_WS: im2col into the planned workspace, then Y = col x W^T
+        float* col = F(s.ws_off);
+        check(vdnnk::im2col(a, static_cast<int>(es_), col, cs_), "im2col");
+        const vdnnk::ConvArgs g1 = vdnnk::gemmws_args(a, col, nullptr);
+        check(bf_ ? vdnnk::conv_fprop_bf16(g1, w, nullptr, F(s.out_off), false, cs_, nullptr, 0)
+                  : vdnnk::conv_fprop(g1, w, nullptr, F(s.out_off), false, cs_, nullptr, 0),
+              "conv_fprop (GEMM_WS)");
+        break;
+      }
       if (s.pad_c) {
         w = reinterpret_cast<float*>(scr + s.w8_off);
         pad_operands(a, s.pad_c, scr + s.x8_off, F(s.w_off), scr + s.w8_off);
@@ -774,6 +797,30 @@ void Session::run_bwd(const BwdStep& s, float lr) {
       const bool fc = l.kind == Kind::Fc;
       bool any_plane = false;
       for (u64 o : s.plane_off) any_plane = any_plane || o != kNoOff;
+      if (gemmws(s.layer, s.ws_off, s.ws_bytes)) {
+        // GEMM_WS: dcol = dY x W into the planned workspace, col2im into dX
+        // (fused ReLU-backward mask / accumulation); then col = im2col(X) in
+        // the same workspace and dW = dY^T x col (fused SGD / fp32 dW)
+        float* col = F(s.ws_off);
+        float* dw = grads_ ? grads_ + grad_off_[mi] : nullptr;
+        if (any_plane) {
+          vdnnk::ConvArgs ad = conv_args(s.layer, s.in_off, &s.plane_off, nullptr);
+          ad.mask_in[0] = s.mask_plane.empty() ? 0 : s.mask_plane[0];
+          vdnnk::ConvArgs g1 = vdnnk::gemmws_args(ad, col, col);
+          check(bf_ ? vdnnk::conv_dgrad_bf16(g1, F(s.w_off), dy, false, cs_, nullptr, 0)
+                    : vdnnk::conv_dgrad(g1, F(s.w_off), dy, false, cs_, nullptr, 0),
+                "conv_dgrad (GEMM_WS)");
+          check(vdnnk::col2im(ad, static_cast<int>(es_), col, s.accumulate, cs_), "col2im");
+        }
+        const vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, nullptr, nullptr);
+        check(vdnnk::im2col(a, static_cast<int>(es_), col, cs_), "im2col");
+        const vdnnk::ConvArgs g2 = vdnnk::gemmws_args(a, col, nullptr);
+        check(bf_ ? vdnnk::conv_wgrad_bf16(g2, dy, F(s.w_off), lr, dw, part, s.part_bytes, cs_)
+                  : vdnnk::conv_wgrad(g2, dy, F(s.w_off), lr, dw, part, s.part_bytes, cs_),
+              "conv_wgrad (GEMM_WS)");
+        if (peer_inline_ && grads_) peer_layer(s.layer, lr);
+        break;
+      }
       if (any_plane) {
         vdnnk::ConvArgs a = conv_args(s.layer, s.in_off, &s.plane_off, sum_x);
         for (int i = 0; i < a.nseg; ++i) a.mask_in[i] = sum_x ? 0 : s.mask_plane[static_cast<size_t>(i)];

@@ -41,6 +41,10 @@ struct Options {
   // step, re-captured when lr changes): both streams' work, the transfers and
   // their event gating become graph nodes; one launch per step.
   bool cuda_graph = false;
+  // 0: implicit GEMM for every planned conv algorithm (workspace reserved);
+  // 1: GEMM_WS layers run im2col into the planned workspace + a 1x1 GEMM
+  // (kernels/conv_gemmws.cu); FFT layers stay implicit
+  int algo_kernels = 0;
 };
 
 struct Transfer {
@@ -205,6 +209,8 @@ class Session {
                             const float* sum_x) const;
   bool summed(int layer) const;  // elementwise join over >= 2 inputs
   int padded_channels(int layer) const;  // BF16 first layer: padded C (0 = none)
+  // algo_kernels = 1 and the layer's planned algorithm is GEMM_WS with its workspace extent at ws_off
+  bool gemmws(int layer, u64 ws_off, u64 ws_bytes) const;
   void pad_operands(vdnnk::ConvArgs& a, int cp, char* x8, const float* w, char* w8);
   void sum_inputs(int layer, const std::vector<u64>& in_off, float* dst);
   void check(cudaError_t e, const char* what) const;
