@@ -21,6 +21,7 @@
 // conv_smallc.cu. FLOPs as the reference counts them:
 // 2*k^2*C*Cout*Ho*Wo*N per pass (cost_model.hpp:100-106).
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "tc_conv.cuh"
@@ -356,7 +357,7 @@ constexpr uint32_t kWgStage = 16384 + 4096;
 template <int KT, int CT>
 __global__ void __launch_bounds__(kWgThreads, 1) c3tc_wgrad_kernel(const float* __restrict__ x,
                                                                    const __grid_constant__ CUtensorMap tma_dy,
-                                                                   C3Geom g, int ppb, float* __restrict__ part) {
+                                                                   C3Geom g, int ppb, int pf, float* __restrict__ part) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -447,10 +448,10 @@ __global__ void __launch_bounds__(kWgThreads, 1) c3tc_wgrad_kernel(const float* 
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_dy) : "memory");
       for (int it = 0; it < nkb; ++it) {
         const int s = it % kWgStages;
-        // warm L2 with the tile kPrefetch stages ahead: the ring's loads then hit L2
-        if (it + kPrefetch < nkb)
+        // warm L2 with the tile `pf` stages ahead: the ring's loads then hit L2
+        if (pf > 0 && it + pf < nkb)
           asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(&tma_dy), "r"(0),
-                       "r"(p_begin + (it + kPrefetch) * kBK), "r"(0)
+                       "r"(p_begin + (it + pf) * kBK), "r"(0)
                        : "memory");
         if (it >= kWgStages) mbar_wait(empty_bar(s), ((it / kWgStages) & 1) ^ 1);
         mbar_expect_tx(full_bar(s), static_cast<uint32_t>(nchunk * 4096));
@@ -953,7 +954,11 @@ cudaError_t c3tc_wgrad(const ConvArgs& a, const float* dy, float* w, float lr, f
     }
     c3tc_wgrad_mk_kernel<<<nb, kWgThreads, smk, st>>>(a.x[0], tdy, g, ppb, KB, pow2_at_least(KB * 32), ws);
   } else {
-    kern<<<nb, kWgThreads, smem, st>>>(a.x[0], tdy, g, ppb, ws);
+    static const int pf = [] {  // VDNN_C3_PREFETCH: dY stages prefetched into L2 ahead of the ring (A/B)
+      const char* e = std::getenv("VDNN_C3_PREFETCH");
+      return e ? std::atoi(e) : kPrefetch;
+    }();
+    kern<<<nb, kWgThreads, smem, st>>>(a.x[0], tdy, g, ppb, pf, ws);
   }
   count_launch();
   cudaError_t e = cudaGetLastError();

@@ -26,6 +26,7 @@
 // Numerics are the BF16 engine's (tcb_conv.cuh): exact bf16 products, fp32
 // accumulation, one rounding per stored value.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "tcb_conv.cuh"
@@ -314,7 +315,7 @@ constexpr uint32_t kWbStage = 16384 + 8192;
 template <int KT, int CT>
 __global__ void __launch_bounds__(kWbThreads, 1) c3b_wgrad_kernel(const uint16_t* __restrict__ x,
                                                                   const __grid_constant__ CUtensorMap tma_dy, C3B g,
-                                                                  int ppb, float* __restrict__ part) {
+                                                                  int ppb, int pf, float* __restrict__ part) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -415,10 +416,10 @@ __global__ void __launch_bounds__(kWbThreads, 1) c3b_wgrad_kernel(const uint16_t
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_dy) : "memory");
       for (int it = 0; it < nkb; ++it) {
         const int s = it % kWbStages;
-        // warm L2 with the tile kWbPrefetch stages ahead: the ring's loads then hit L2
-        if (it + kWbPrefetch < nkb)
+        // warm L2 with the tile `pf` stages ahead: the ring's loads then hit L2
+        if (pf > 0 && it + pf < nkb)
           asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(&tma_dy), "r"(0),
-                       "r"(p_begin + (it + kWbPrefetch) * kKb), "r"(0)
+                       "r"(p_begin + (it + pf) * kKb), "r"(0)
                        : "memory");
         if (it >= kWbStages) mbar_wait(empty_bar(s), ((it / kWbStages) & 1) ^ 1);
         mbar_expect_tx(full_bar(s), static_cast<uint32_t>(nchunk * 8192));
@@ -999,8 +1000,12 @@ cudaError_t c3b_wgrad(const ConvArgs& a, const void* dy, void* w, float lr, floa
     if (e != cudaSuccess) return e;
     attr[k3c3] = smem;
   }
+  static const int pf = [] {  // VDNN_C3_PREFETCH: dY stages prefetched into L2 ahead of the ring (A/B)
+    const char* e = std::getenv("VDNN_C3_PREFETCH");
+    return e ? std::atoi(e) : kWbPrefetch;
+  }();
   kern<<<nb, kWbThreads, smem, st>>>(static_cast<const uint16_t*>(static_cast<const void*>(a.x[0])), tdy,
-                                                 g, ppb, ws);
+                                                 g, ppb, pf, ws);
   }
   count_launch();
   cudaError_t e = cudaGetLastError();
