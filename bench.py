@@ -42,17 +42,37 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 TRAFFIC_FILES = ("r02_conv_traffic.json", "r01_conv_traffic.json")  # newest capture first
 
 
-def conv_traffic():
-    """(mean DRAM bytes per conv-engine launch, source file) from the newest
-    committed ncu capture (profiles/r0N_conv_traffic.json), or (None, None)."""
+def conv_traffic(key="conv_dram_bytes_per_launch"):
+    """(mean DRAM bytes per launch, source file) from the newest committed ncu
+    capture (profiles/r0N_conv_traffic.json; `key`: the whole conv engine or
+    the dominant kernel), or (None, None)."""
     for name in TRAFFIC_FILES:
         path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name)
         try:
             with open(path) as f:
-                return int(json.load(f)["conv_dram_bytes_per_launch"]), "profiles/" + name
+                return int(json.load(f)[key]), "profiles/" + name
         except (OSError, KeyError, ValueError):
             continue
     return None, None
+
+
+def pair_fprop_layers(g, es):
+    """Conv layers whose FPROP runs the dominant kernel of the step -- the
+    CTA-pair kernel (fp32 storage: tc_conv_pair_kernel, conv.cu launch():
+    >= 256 output columns in 128-multiples and >= 148 pair tiles of 256 x 256;
+    BF16: tcb_pair_kernel, >= 256 columns)."""
+    import paper_1602_08124_b200 as V
+    out = []
+    for l in g.layers():
+        if l.kind != V.LayerKind.Conv:
+            continue
+        sh = g.shape(l.id)
+        co, m = sh.c, sh.n * sh.h * sh.w
+        if es == 4 and co >= 256 and co % 128 == 0 and ((m + 255) // 256) * (co // 256) >= 148:
+            out.append(l.id)
+        elif es == 2 and co >= 256:
+            out.append(l.id)
+    return out
 
 
 def measured_tf32_peak(peaks, peaks_src):
@@ -389,6 +409,12 @@ def run_policy(policy, args, device, world, peaks, want_e2e, sampler_cls):
                       "ms_per_step": round(ems, 3)}
     res["_flops"] = flops
     res["_conv_ms"] = conv_ms
+    # the dominant kernel's FPROP launches of the measured step (per-op CUDA
+    # events on the compute stream): algorithmic FLOPs per launch and time
+    dom = pair_fprop_layers(g, cm.elem_size)
+    res["_dom_n"] = len(dom)
+    res["_dom_flops"] = sum(cm.flops(g, i, False) for i in dom)
+    res["_dom_ms"] = sum(fwd_ms[i] for i in dom)
     del s
     torch.cuda.synchronize(device)
     return res
@@ -577,12 +603,35 @@ def main():
         line["rank_census"] = census
     if head.get("_conv_ms"):
         ach = head["_flops"] / (head["_conv_ms"] * 1e-3) / 1e12
-        line["roofline"] = {"bound": "tensor", "kernel": "tcgen05 conv engine (tc_conv_pair / tc_wgrad_pair / tc_conv_halo_pair / tc_wgrad_halo_pair / tc_conv / tc_conv_persist / c3tc kernels: every conv+FC fprop, dgrad, wgrad launch)",
-                            "achieved": round(ach, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
-                            "frac": round(ach / tf32_peak, 4), "traffic": conv_traffic()[0],
-                            "peak_note": peak_note,
-                            "traffic_note": "DRAM read+write bytes per conv-engine launch (mean over one dyn step), "
-                                            f"ncu capture {conv_traffic()[1]}"}
+        engine = {"kernels": "every conv+FC fprop, dgrad, wgrad launch of the step (tc_conv_pair / tc_wgrad_pair / "
+                             "tc_conv_halo_pair / tc_wgrad_halo_pair / tc_conv / tc_conv_persist / c3tc)",
+                  "achieved": round(ach, 1), "frac": round(ach / tf32_peak, 4),
+                  "traffic": conv_traffic()[0],
+                  "traffic_note": f"mean DRAM read+write bytes per conv-engine launch, ncu {conv_traffic()[1]}"}
+        bf = (peaks or {}).get("bf16_tflops")
+        if head.get("_dom_ms"):
+            # the dominant kernel (39% of the dyn step's serialized kernel time,
+            # profiles/r02s4_launches_vgg16_b256_dyn_summary.txt): its FPROP
+            # launches, algorithmic FLOPs (2 k^2 Cin Cout Ho Wo N each) over
+            # their CUDA-event durations in the measured step
+            dach = head["_dom_flops"] / (head["_dom_ms"] * 1e-3) / 1e12
+            line["roofline"] = {
+                "bound": "tensor",
+                "kernel": f"tc_conv_pair_kernel<5,1,4> (TF32 CTA pair, M256xN256xK8): the FPROP launches of the "
+                          f"{head['_dom_n']} conv layers with >= 256 output channels",
+                "achieved": round(dach, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
+                "frac": round(dach / tf32_peak, 4),
+                "frac_of_half_bf16_burst": (round(dach / (bf / 2), 4) if bf else None),
+                "traffic": conv_traffic("pair_dram_bytes_per_launch")[0],
+                "peak_note": peak_note + ("; kind::tf32 runs at half the f16 rate, so MEASURED_PEAKS' bf16 burst "
+                                          f"{bf} TFLOP/s / 2 is the other denominator" if bf else ""),
+                "traffic_note": "mean DRAM read+write bytes per tc_conv_pair_kernel launch of one dyn step, ncu "
+                                f"{conv_traffic('pair_dram_bytes_per_launch')[1]}",
+                "engine": engine}
+        else:
+            line["roofline"] = dict({"bound": "tensor", "kernel": "tcgen05 conv engine", "achieved": engine["achieved"],
+                                     "peak": round(tf32_peak, 1), "unit": "TFLOP/s", "frac": engine["frac"],
+                                     "traffic": engine["traffic"], "peak_note": peak_note}, engine=engine)
     line["host_link"] = dict(link, **{
         "offload_bytes_per_iter": head.get("offload_bytes_per_iter"),
         "d2h_gbs_in_run": head.get("d2h_gbs"), "h2d_gbs_in_run": head.get("h2d_gbs"),
