@@ -553,8 +553,16 @@ bool halo_wgb_params(const ConvParamsB& p, HaloWgParamsB& h) {
   h.Kp = (h.P + 15) / 16 * 16;
   h.nck = p.C / 64;
   const int nblk = h.kh * h.nck, gmax = 512 / (2 * p.Cout);
-  h.ngroups = (nblk + gmax - 1) / gmax;
-  h.G = (nblk + h.ngroups - 1) / h.ngroups;
+  // G = the largest divisor of the block count that fits TMEM: every group
+  // of CTAs carries the same number of blocks (64 -> 128 channels: 3 blocks,
+  // G = 2 left half the CTAs idle for a third of the time)
+  h.G = 1;
+  for (int gd = std::min(gmax, nblk); gd >= 1; --gd)
+    if (nblk % gd == 0) {
+      h.G = gd;
+      break;
+    }
+  h.ngroups = nblk / h.G;
   h.nrows = h.N * h.Hout;
   const int splits = std::max(1, kNumSmsB / h.ngroups);
   h.rows_per = (h.nrows + splits - 1) / splits;
