@@ -13,7 +13,8 @@
 //   of the virtual pitch-P grid, two M=256 pair MMAs per tap: h = 0, 1) and
 //   stages its own padded input box plus B rows n0 + r*BN/2. A rank-1 tile past
 //   the last row tile computes on TMA zero fill and stores nothing.
-//   warps 0-3 : epilogue of this CTA's 256 virtual rows (as tc_conv_halo)
+//   warps 0-3, 6-9 : epilogue of this CTA's 256 virtual rows, one M half per
+//               warpgroup (kHaloEpiGroups; TMEM lane quarter = warp % 4)
 //   warp 4    : TMEM alloc (cta_group::2); in the leader the MMA issuer
 //   warp 5    : TMA producer; both CTAs' loads complete on the LEADER's full
 //               barriers (.cta_group::2 TMA), the leader's single arrive

@@ -24,7 +24,8 @@
 // Tile = 256 virtual rows (two M = 128 MMAs per tap, h = 0, 1) x BN columns;
 // persistent CTAs (one per SM), two TMEM accumulator sets (4 x BN columns)
 // so tile t's epilogue overlaps tile t+1's main loop.
-//   warps 0-3 : epilogue (TMEM lanes 32w..): bf16 RNE stores
+//   warps 0-3, 6-9 : epilogue, one M half per warpgroup (TMEM lane quarter
+//               = warp % 4): bf16 RNE stores, fused ReLU / mask / accumulate
 //   warp 4    : TMEM owner + MMA issuer (one elected lane)
 //   warp 5    : TMA producer (one lane), in consumption order
 #pragma once

@@ -15,8 +15,9 @@
 //   256-column N tile) items; CTA rank r stages A rows m0 + 128r and B
 //   columns n0 + 128r (fprop: 128 K-major W rows; dgrad: two 64-ci MN-major
 //   W^T chunks; wgrad: two 64-co MN-major dY chunks).
-//   warps 0-3 : epilogue of this CTA's 128 rows (tcb_epilogue: fused bias /
-//               ReLU / ReLU-backward mask / accumulate, SGD / dW, partials)
+//   warps 0-3, 6-9 : epilogue of this CTA's 128 rows, one column half per
+//               warpgroup (tcb_epilogue: fused bias / ReLU / ReLU-backward
+//               mask / accumulate, SGD / dW, partials)
 //   warp 4    : TMEM alloc (cta_group::2, both CTAs); in the leader the MMA
 //               issuer (tcgen05.mma.cta_group::2.kind::f16, M256 N256 K16)
 //   warp 5    : TMA producer of this CTA's halves; both CTAs' loads complete
