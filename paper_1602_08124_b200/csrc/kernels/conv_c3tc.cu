@@ -281,24 +281,32 @@ __global__ void __launch_bounds__(kFpThreads, 1) c3tc_fprop_kernel(const float* 
     }
   } else if (warp == 12) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_tf32(NB, false, false);
-      int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int s = it % kFpStages, acc = it & 1;
-        mbar_wait(full_bar(s), (it / kFpStages) & 1);
-        if (it >= 2) mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t sa = sa0 + s * 16384;
+    // whole warp in the loop, one elected lane issues; descriptors advanced
+    // by constants, running stage / phase counters (see c3tc_wgrad_kernel)
+    const uint32_t idesc = make_idesc_tf32(NB, false, false);
+    const bool leader = elect_one();
+    const uint64_t ad0 = make_sdesc(sa0, 16, 1024, kSw128), bd = make_sdesc(sb, 16, 1024, kSw128);
+    int it = 0, s = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      mbar_wait(full_bar(s), ph);
+      if (it >= 2) mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t ad = ad0 + static_cast<uint64_t>(s) * (16384 >> 4);
 #pragma unroll
         for (int kk = 0; kk < kBK / 8; ++kk)
-          tc_mma_tf32(tmem + acc * NBP, make_sdesc(sa + kk * 32, 16, 1024, kSw128),
-                      make_sdesc(sb + kk * 32, 16, 1024, kSw128), idesc, kk > 0 ? 1u : 0u);
+          tc_mma_tf32(tmem + acc * NBP, ad + kk * 2, bd + kk * 2, idesc, kk > 0 ? 1u : 0u);
         tc_commit(empty_bar(s));
         tc_commit(tfull_bar(acc));
       }
+      __syncwarp();
+      if (++s == kFpStages) {
+        s = 0;
+        ph ^= 1;
+      }
     }
-    __syncwarp();
   } else {
     // ---------------- epilogue ----------------
     const int row = warp * 32 + lane;
@@ -461,20 +469,37 @@ __global__ void __launch_bounds__(kWgThreads, 1) c3tc_wgrad_kernel(const float* 
     __syncwarp();
   } else {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_tf32(32, true, true);
-      for (int it = 0; it < nkb; ++it) {
-        const int s = it % kWgStages;
-        mbar_wait(full_bar(s), (it / kWgStages) & 1);
-        tc_fence_after();
-        const uint32_t sa = base + s * kWgStage;
-        const uint32_t sbb = sa + 16384;
+    // N = 32 MMAs are short (one per 8 pixels), so the issue loop itself is
+    // the limiter (ncu: the MMA warp never waited for a full stage and spent
+    // ~575 cycles per stage on dependent uniform-datapath instructions): the
+    // descriptors are built once and advanced by constants, the stage and
+    // phase are running counters (no division), and the whole warp runs the
+    // loop with one elected lane issuing
+    const uint32_t idesc = make_idesc_tf32(32, true, true);
+    const bool leader = elect_one();
+    const uint64_t ad0 = make_sdesc(base, 4096, 512, kSw128Base32);
+    const uint64_t bd0 = make_sdesc(base + 16384, 4096, 512, kSw128Base32);
+    constexpr uint64_t kStageLo = kWgStage >> 4, kKkLo = 1024 >> 4;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int it = 0; it < nkb; ++it) {
+      mbar_wait(full_bar(s), ph);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t so = static_cast<uint64_t>(s) * kStageLo;
+        const uint64_t ad = ad0 + so, bd = bd0 + so;
+        tc_mma_tf32(tmem, ad, bd, idesc, it > 0 ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < kBK / 8; ++kk)
-          tc_mma_tf32(tmem, make_sdesc(sa + kk * 1024, 4096, 512, kSw128Base32),
-                      make_sdesc(sbb + kk * 1024, 4096, 512, kSw128Base32), idesc, (it > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 1; kk < kBK / 8; ++kk) tc_mma_tf32(tmem, ad + kk * kKkLo, bd + kk * kKkLo, idesc, 1u);
         tc_commit(empty_bar(s));
       }
+      __syncwarp();
+      if (++s == kWgStages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    if (leader) {
       if (nkb > 0)
         tc_commit(done_bar);
       else

@@ -237,24 +237,32 @@ __global__ void __launch_bounds__(kFbThreads, 1) c3b_fprop_kernel(const uint16_t
     }
   } else if (warp == kFbMmaWarp) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(NB, false, false);
-      const int nk = (g.KK + 15) / 16;  // K = 16 steps that hold live columns
-      int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int s = it % kFbStages, acc = it & 1;
-        mbar_wait(full_bar(s), (it / kFbStages) & 1);
-        if (it >= 2) mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t sa = sa0 + s * 16384;
+    // whole warp in the loop, one elected lane issues; descriptors advanced
+    // by constants, running stage / phase counters (see c3b_wgrad_kernel)
+    const uint32_t idesc = make_idesc_bf16(NB, false, false);
+    const int nk = (g.KK + 15) / 16;  // K = 16 steps that hold live columns
+    const bool leader = elect_one();
+    const uint64_t ad0 = make_sdesc(sa0, 16, 1024, kSw128), bd = make_sdesc(sb, 16, 1024, kSw128);
+    int it = 0, s = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      mbar_wait(full_bar(s), ph);
+      if (it >= 2) mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t ad = ad0 + static_cast<uint64_t>(s) * (16384 >> 4);
         for (int kk = 0; kk < nk; ++kk)
-          tc_mma_bf16(tmem + acc * NBP, make_sdesc(sa + kk * 32, 16, 1024, kSw128),
-                      make_sdesc(sb + kk * 32, 16, 1024, kSw128), idesc, kk > 0 ? 1u : 0u);
+          tc_mma_bf16(tmem + acc * NBP, ad + kk * 2, bd + kk * 2, idesc, kk > 0 ? 1u : 0u);
         tc_commit(empty_bar(s));
         tc_commit(tfull_bar(acc));
       }
+      __syncwarp();
+      if (++s == kFbStages) {
+        s = 0;
+        ph ^= 1;
+      }
     }
-    __syncwarp();
   } else {
     // ---------------- epilogue ----------------
     const int row = warp * 32 + lane;
@@ -429,20 +437,34 @@ __global__ void __launch_bounds__(kWbThreads, 1) c3b_wgrad_kernel(const uint16_t
     __syncwarp();
   } else {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(64, true, true);
-      for (int it = 0; it < nkb; ++it) {
-        const int s = it % kWbStages;
-        mbar_wait(full_bar(s), (it / kWbStages) & 1);
-        tc_fence_after();
-        const uint32_t sa = base + s * kWbStage;
-        const uint32_t sbb = sa + 16384;
+    // (as c3tc_wgrad_kernel: descriptors built once and advanced by
+    // constants, running stage / phase counters, whole warp + elected lane --
+    // the short N = 64 MMAs leave the issue loop as the limiter otherwise)
+    const uint32_t idesc = make_idesc_bf16(64, true, true);
+    const bool leader = elect_one();
+    const uint64_t ad0 = make_sdesc(base, 8192, 1024, kSw128);
+    const uint64_t bd0 = make_sdesc(base + 16384, 8192, 1024, kSw128);
+    constexpr uint64_t kStageLo = kWbStage >> 4, kKkLo = 2048 >> 4;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int it = 0; it < nkb; ++it) {
+      mbar_wait(full_bar(s), ph);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t so = static_cast<uint64_t>(s) * kStageLo;
+        const uint64_t ad = ad0 + so, bd = bd0 + so;
+        tc_mma_bf16(tmem, ad, bd, idesc, it > 0 ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < kKb / 16; ++kk)
-          tc_mma_bf16(tmem, make_sdesc(sa + kk * 2048, 8192, 1024, kSw128),
-                      make_sdesc(sbb + kk * 2048, 8192, 1024, kSw128), idesc, (it > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 1; kk < kKb / 16; ++kk) tc_mma_bf16(tmem, ad + kk * kKkLo, bd + kk * kKkLo, idesc, 1u);
         tc_commit(empty_bar(s));
       }
+      __syncwarp();
+      if (++s == kWbStages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    if (leader) {
       if (nkb > 0)
         tc_commit(done_bar);
       else
