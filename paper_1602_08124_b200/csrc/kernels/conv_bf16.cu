@@ -209,6 +209,11 @@ bool halo_params_b(const ConvParamsB& p, HaloParamsB& h) {
   }
   if (h.Cout > 128) return false;
   h.accum = p.epi == kEpiAccum;
+  static const int epi_t = [] {  // VDNN_BF16_EPI_T=0: lanes store their rows directly (A/B switch)
+    const char* e = std::getenv("VDNN_BF16_EPI_T");
+    return !e || std::atoi(e) != 0 ? 1 : 0;
+  }();
+  h.epi_t = epi_t;
   h.P = h.Win + 2 * h.pad;
   if (h.P > 256 || h.Wout + h.kw - 1 != h.P) return false;
   h.TH = 256 / h.P;
@@ -295,7 +300,11 @@ cudaError_t launch_pair_b(const ConvParamsB& p, int splits, const CUtensorMap& t
   }
   const int64_t items = static_cast<int64_t>((p.M + 255) / 256) * ((p.Ncols + 255) / 256) * splits;
   const int grid = 2 * static_cast<int>(std::min<int64_t>(items, kNumSmsB / 2));
-  tcb_pair_kernel<STAGES><<<grid, kTcbPairThreads, L::kTotal, st>>>(p, ta, tb, splits);
+  static const int epi_t = [] {  // VDNN_BF16_EPI_T=0: lanes store their rows directly (A/B switch)
+    const char* e = std::getenv("VDNN_BF16_EPI_T");
+    return !e || std::atoi(e) != 0 ? 1 : 0;
+  }();
+  tcb_pair_kernel<STAGES><<<grid, kTcbPairThreads, L::kTotal, st>>>(p, ta, tb, splits, epi_t);
   count_launch();
   return cudaGetLastError();
 }

@@ -590,6 +590,59 @@ __device__ __forceinline__ void store_row32(bf16* dst, float (&v)[32], int n, bo
     if (i < n) dst[i] = __float2bfloat16_rn((accumulate ? bf2f(dst[i]) : 0.f) + v[i]);
 }
 
+// Warp-cooperative store of a 32-row x 32-column bf16 block whose row r sits
+// in lane r (the TMEM lane layout) through a 2 KB per-warp shared-memory
+// transpose. Stored straight from the lanes, every 16-B st.global of the warp
+// touches 32 rows (32 half-sectors on as many lines); transposed, it covers 8
+// rows x 64 B (16 full sectors), a quarter of the L1 / L2 store requests.
+// Each lane passes its own row's destination (null: row not stored) and,
+// for the fused ReLU-backward select, its row of x (null: no mask); the
+// reader of a chunk fetches both from the row's lane. The 16-B chunk index is
+// XOR-swizzled with (row >> 1) & 3, so the row writes and the chunk reads are
+// bank-conflict free. The mask is applied per element after the transpose:
+// rounding then zeroing equals zeroing then rounding, so the stored values
+// are bit-identical to store_row32's.
+__device__ __forceinline__ void store_tile32_t(uint32_t scratch, const float (&v)[32], bf16* dst, const bf16* mask) {
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;
+  // the rows this lane stores (8i + lane / 4, chunk q) and their ReLU-mask
+  // chunks: the mask loads are issued first so they fly during the transpose
+  bf16* d[4];
+  uint4 x[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = 8 * i + (lane >> 2);
+    d[i] = reinterpret_cast<bf16*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), r));
+    const bf16* mk = reinterpret_cast<const bf16*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mask), r));
+    x[i] = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);  // 1.0: keep
+    if (mk && d[i]) x[i] = __ldg(reinterpret_cast<const uint4*>(mk) + q);
+  }
+  __syncwarp();  // the previous block's chunk reads are done
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(scratch + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)),
+                 "r"(pack_bf16x2(v[8 * c], v[8 * c + 1])), "r"(pack_bf16x2(v[8 * c + 2], v[8 * c + 3])),
+                 "r"(pack_bf16x2(v[8 * c + 4], v[8 * c + 5])), "r"(pack_bf16x2(v[8 * c + 6], v[8 * c + 7]))
+                 : "memory");
+  __syncwarp();
+  // bf16 bits b: x > 0 <=> 0 < b <= 0x7f80 (+inf) -- sign clear, nonzero, not NaN
+  auto keep = [](uint32_t b) {
+    return (((b & 0xffffu) - 1u) < 0x7f80u ? 0xffffu : 0u) | (((b >> 16) - 1u) < 0x7f80u ? 0xffff0000u : 0u);
+  };
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = 8 * i + (lane >> 2);
+    uint4 w;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                 : "r"(scratch + r * 64 + ((q ^ ((r >> 1) & 3)) << 4))
+                 : "memory");
+    if (d[i])
+      reinterpret_cast<uint4*>(d[i])[q] =
+          make_uint4(w.x & keep(x[i].x), w.y & keep(x[i].y), w.z & keep(x[i].z), w.w & keep(x[i].w));
+  }
+}
+
 // TMA producer (one thread; single-segment layers with 8-multiple channel
 // counts). A: im2col boxes of 128 B channel chunks (fprop: X, dgrad: dY, 128
 // pixels = the K-major A tile; wgrad: X, 64 pixels = one MN-major chunk of 64
@@ -701,7 +754,8 @@ struct TmaProducerB {
 // kernel releases the accumulator there). zero: the tile had no K blocks.
 template <int BN, class Drained>
 __device__ __forceinline__ void tcb_epilogue(const ConvParamsB& p, uint32_t taddr, int m0, int n0, int z, int row,
-                                             bool zero, Drained drained, int cg_lo = 0, int cg_hi = BN / 32) {
+                                             bool zero, Drained drained, int cg_lo = 0, int cg_hi = BN / 32,
+                                             uint32_t scratch = 0) {
   const int m = m0 + row;
 #pragma unroll 1
   for (int cg = cg_lo; cg < cg_hi; ++cg) {
@@ -712,8 +766,34 @@ __device__ __forceinline__ void tcb_epilogue(const ConvParamsB& p, uint32_t tadd
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.f;
     }
-    if (m >= p.M) continue;
     const int nb = n0 + cg * 32;
+    if (scratch && p.epi == kEpiStore) {
+      // full 32-column blocks of a plain bf16 store: transposed through the
+      // warp's scratch (every condition here is warp-uniform)
+      if (p.kind == kFprop && (p.Cout & 7) == 0 && nb + 32 <= p.Cout) {
+        if (p.bias) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += bf2f(p.bias[nb + i]);
+        }
+        if (p.relu) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        store_tile32_t(scratch, v, m < p.M ? p.y + static_cast<int64_t>(m) * p.Cout + nb : nullptr, nullptr);
+        continue;
+      }
+      if (p.kind == kDgrad && p.vec_in && (nb >> 6) < p.nchunk) {
+        const Chunk c = chunk_at_b(p, nb >> 6);
+        const BSeg sg = p.seg[c.seg];
+        const int co = c.coff + (nb & 63);
+        if (sg.dx && c.valid - (nb & 63) >= 32 && (sg.C & 7) == 0 && (co & 7) == 0) {
+          const int64_t at = static_cast<int64_t>(m) * sg.C + co;
+          store_tile32_t(scratch, v, m < p.M ? sg.dx + at : nullptr, sg.mask ? sg.x + at : nullptr);
+          continue;
+        }
+      }
+    }
+    if (m >= p.M) continue;
     if (p.epi == kEpiPartial && p.kind != kWgrad) {
       // split-K fprop / dgrad: fp32 partial slab z of [splits][M][Ncols]
       if (nb >= p.Ncols) continue;

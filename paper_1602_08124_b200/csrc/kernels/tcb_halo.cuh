@@ -40,6 +40,7 @@ struct HaloParamsB {
   int Hout, Wout, Cout;   // output: fprop Y, dgrad dX (NHWC bf16)
   int P, TH, nck, tiles_h, ntn, ntiles;
   int relu, accum;
+  int epi_t;              // 1: stores transposed through shared memory (store_tile32_t)
   bf16* out;
   const bf16* mask_x;     // dgrad: dX *= (x > 0), x laid out like out; null = none
 };
@@ -48,7 +49,8 @@ template <int BN, int AS, int BS>
 struct HaloSmemB {
   static constexpr int kASlot = 33 * 1024;  // >= 258 rows x 128 B (256 virtual rows + 2 tap shifts)
   static constexpr int kBSlot = BN * 128;
-  static constexpr int kTotal = AS * kASlot + BS * kBSlot + 1024 + 256;
+  static constexpr int kEpiScratch = 8 * 2048;  // store_tile32_t transpose, one 2 KB block per epilogue warp
+  static constexpr int kTotal = AS * kASlot + BS * kBSlot + 1024 + 256 + kEpiScratch;
   static constexpr int kAccCols = 2 * BN;   // two M = 128 halves
   static_assert(2 * kAccCols <= 512, "two accumulator sets must fit TMEM");
 };
@@ -263,11 +265,17 @@ __global__ void __launch_bounds__(kHaloBThreads, 1) tcb_halo_kernel(const __grid
             mbar_arrive(tempty(acc));
           }
           const int nb = n0 + cg * 32;
-          if (!valid || nb >= p.Cout) continue;
           if (p.relu) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) vals[i] = fmaxf(vals[i], 0.f);
           }
+          if (p.epi_t && !p.accum && nb < p.Cout) {  // warp-uniform; rows of invalid pixels store nothing
+            const int64_t at = pix * p.Cout + nb;
+            store_tile32_t(bars + 256 + (hsel * 4 + qw) * 2048, vals, valid ? p.out + at : nullptr,
+                           p.mask_x ? p.mask_x + at : nullptr);
+            continue;
+          }
+          if (!valid || nb >= p.Cout) continue;
           if (p.mask_x) {
             const uint4* xr = reinterpret_cast<const uint4*>(p.mask_x + pix * p.Cout + nb);
             uint4 xa[4];  // loads in flight together, then the selects

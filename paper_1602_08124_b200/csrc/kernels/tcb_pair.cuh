@@ -45,7 +45,8 @@ struct TcbPairSmem {
   static constexpr int kABytes = kBM * 128;  // this CTA's 128 A rows (or 2 MN chunks) x 64 bf16
   static constexpr int kBBytes = 128 * 128;  // this CTA's half of B: 128 rows (or 2 MN chunks) x 64 bf16
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kTotal = STAGES * kStage + 1024 + 256;
+  static constexpr int kEpiScratch = 8 * 2048;  // store_tile32_t transpose, one 2 KB block per epilogue warp
+  static constexpr int kTotal = STAGES * kStage + 1024 + 256 + kEpiScratch;
 };
 
 // Two epilogue warpgroups (warps 0-3: columns [0, 128), warps 6-9: columns
@@ -56,7 +57,7 @@ constexpr int kTcbPairThreads = 320;
 template <int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcbPairThreads, 1)
     tcb_pair_kernel(const __grid_constant__ ConvParamsB p, const __grid_constant__ CUtensorMap tma_a,
-                    const __grid_constant__ CUtensorMap tma_b, int splits) {
+                    const __grid_constant__ CUtensorMap tma_b, int splits, int epi_t) {
   using L = TcbPairSmem<STAGES>;
   constexpr int BN = 256;
   constexpr int kTmemCols = 2 * BN;
@@ -215,7 +216,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcbPairThreads, 1)
         // last TMEM read of this accumulator set: release it to the leader's MMA warp
         tc_fence_before();
         mbar_arrive_cluster(acc ? lt1 : lt0);
-      }, chalf * (BN / 64), (chalf + 1) * (BN / 64));
+      }, chalf * (BN / 64), (chalf + 1) * (BN / 64),
+                     epi_t ? bars + 256 + (chalf * 4 + qw) * 2048 : 0u);
     }
   }
   tc_fence_before();
