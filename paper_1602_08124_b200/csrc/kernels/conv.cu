@@ -390,6 +390,11 @@ bool halo_params(const ConvParams& p, HaloParams& h) {
   // once per 256 columns.
   if (h.Cout > 128 || (h.Cout > 64 && h.Cin < 128)) return false;
   h.accum = p.epi == kEpiAccum;
+  static const int epi_t = [] {  // VDNN_HALO_EPI_T=0: lanes store their rows directly (A/B switch)
+    const char* e = std::getenv("VDNN_HALO_EPI_T");
+    return !e || std::atoi(e) != 0 ? 1 : 0;
+  }();
+  h.epi_t = epi_t;
   h.P = h.Win + 2 * h.pad;
   if (h.P > 256 || h.Wout + h.kw - 1 != h.P) return false;
   h.TH = 256 / h.P;

@@ -41,6 +41,7 @@ struct HaloParams {
   int Hout, Wout, Cout;   // output: fprop Y, dgrad dX (NHWC)
   int P, TH, nck, tiles_h, ntn, ntiles;
   int relu, accum;
+  int epi_t;              // halo pair: stores transposed through shared memory (store_half32_f32)
   float* out;
   const float* mask_x;    // dgrad: dX *= (x > 0), x laid out like out; null = none
 };

@@ -29,12 +29,55 @@
 
 namespace vdnnk {
 
+// Warp-cooperative store of 16 fp32 columns of 32 rows (row r in lane r, the
+// TMEM lane layout) through a 2 KB per-warp shared-memory transpose: a warp's
+// 16-B st.global then covers 8 rows x 64 B (full sectors) instead of 32 rows
+// x 16 B. dst / mask: this lane's row at the first column (null: row not
+// stored / no ReLU mask); the mask chunks are loaded before the transpose and
+// selected per element after it (the same x > 0 select as the per-lane path,
+// so the stored values are bit-identical). Chunk index XOR (row >> 1) & 3:
+// conflict-free row writes and chunk reads.
+__device__ __forceinline__ void store_half32_f32(uint32_t scratch, const float* v, float* dst, const float* mask) {
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;
+  float* d[4];
+  float4 x[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = 8 * i + (lane >> 2);
+    d[i] = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), r));
+    const float* mk = reinterpret_cast<const float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mask), r));
+    x[i] = make_float4(1.f, 1.f, 1.f, 1.f);
+    if (mk && d[i]) x[i] = __ldg(reinterpret_cast<const float4*>(mk) + q);
+  }
+  __syncwarp();  // the previous block's chunk reads are done
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(scratch + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)),
+                 "f"(v[4 * c]), "f"(v[4 * c + 1]), "f"(v[4 * c + 2]), "f"(v[4 * c + 3])
+                 : "memory");
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = 8 * i + (lane >> 2);
+    float4 w;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(w.x), "=f"(w.y), "=f"(w.z), "=f"(w.w)
+                 : "r"(scratch + r * 64 + ((q ^ ((r >> 1) & 3)) << 4))
+                 : "memory");
+    if (d[i])
+      reinterpret_cast<float4*>(d[i])[q] = make_float4(x[i].x > 0.f ? w.x : 0.f, x[i].y > 0.f ? w.y : 0.f,
+                                                       x[i].z > 0.f ? w.z : 0.f, x[i].w > 0.f ? w.w : 0.f);
+  }
+}
+
 template <int BN, int AS, int BS>
 struct HaloPairSmem {
   static constexpr int kASlot = 33 * 1024;       // >= 258 rows x 128 B
   static constexpr int kBSlot = (BN / 2) * 128;  // this CTA's half of B
-  static constexpr int kTotal = AS * kASlot + BS * kBSlot + 1024 + 256;
-  static int total(int nbslots) { return AS * kASlot + nbslots * kBSlot + 1024 + 256; }
+  static constexpr int kEpiScratch = 8 * 2048;  // store_half32_f32 transpose, one 2 KB block per epilogue warp
+  static constexpr int kTotal = AS * kASlot + BS * kBSlot + 1024 + 256 + kEpiScratch;
+  static int total(int nbslots) { return AS * kASlot + nbslots * kBSlot + 1024 + 256 + kEpiScratch; }
   static constexpr int kAccCols = 2 * BN;  // h = 0, 1
   static_assert(2 * kAccCols <= 512, "two accumulator sets must fit TMEM");
 };
@@ -269,11 +312,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kHaloPairThreads, 1)
             mbar_arrive_cluster(acc ? ltempty1 : ltempty0);
           }
           const int nb = n0 + cg * 32;
-          if (!valid || nb >= p.Cout) continue;
           if (p.relu) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) vals[i] = fmaxf(vals[i], 0.f);
           }
+          // 64-column tiles only: at BN = 128 the A/B of tools/ab_halo_epi_t.sh measured no gain
+          // (112^2 layers 0.89-0.92 -> 0.94 ms), at BN = 64 224^2x64 fprop 2.05-2.11 -> 1.90-1.93 ms
+          if (BN == 64 && p.epi_t && !p.accum && nb < p.Cout) {  // warp-uniform; invalid pixels store nothing
+            const int64_t at = pix * p.Cout + nb;
+            const uint32_t scr = bars + 256 + ((warp < 4 ? warp : warp - 2) * 2048);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+              store_half32_f32(scr, vals + 16 * hh, valid ? p.out + at + 16 * hh : nullptr,
+                               p.mask_x ? p.mask_x + at + 16 * hh : nullptr);
+            continue;
+          }
+          if (!valid || nb >= p.Cout) continue;
           if (p.mask_x) {
             const float4* xr = reinterpret_cast<const float4*>(p.mask_x + pix * p.Cout + nb);
             float4 xv[8];
